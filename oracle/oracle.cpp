@@ -1,0 +1,816 @@
+// oracle.cpp -- the CPU ORACLE for TokenSim's batched design-space sweep.
+//
+// TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference legs may load this library.  It shares no code,
+// header, table or constant generator with the CUDA path (paper_2503_08415_b200/),
+// and it imports nothing from it.
+//
+// What it is: a plain, slow, single-threaded simulation of ONE sweep point,
+// written as the algorithm of SURVEY.md §8(c) step by step (c.1 derived
+// constants, c.2 workload, c.4 iteration loop, c.5 cost table, c.6 metrics and
+// digests), using std::set / std::vector and explicit per-request block lists.
+// No blocking, fusion, incremental aggregates or reordering: every quantity is
+// recomputed from its definition when it is needed.
+//
+// Paper anchors (PAPER.md line numbers): iteration-level scheduling with the
+// default end-of-iteration breakpoint P:243; continuous vs static batching
+// P:166-169; PagedAttention blocks P:172-173; preemption by moving
+// KV to host P:456-457; max-memory-ratio admission P:460; compute
+// simulator returning iteration time P:216 with prefill compute-bound / decode
+// memory-bound P:160-161; latency percentiles P:321; TTFT and mTPOT SLOs
+// P:458-465; memory footprint over time P:552-565.  Every reading of an
+// ambiguous passage is listed in DESIGN.md ("Readings").
+//
+// Build: g++ -std=c++17 -O2 -ffp-contract=off -fPIC -shared (no -ffast-math).
+// Every fp64 expression is evaluated in the order written in SURVEY §8(c).
+
+#include "oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+typedef uint64_t u64;
+typedef int64_t i64;
+typedef uint32_t u32;
+
+bool fail(const std::string &m) {
+  g_err = m;
+  return false;
+}
+
+// ----------------------------------------------------------------- c.2 Philox4x32-10
+// Random123 / cuRAND definition: 10 rounds, multipliers 0xD2511F53, 0xCD9E8D57,
+// Weyl key increments 0x9E3779B9, 0xBB67AE85; round output
+// {hi1^c1^k0, lo1, hi0^c3^k1, lo0}.
+void philox(const u32 ctr_in[4], const u32 key_in[2], u32 out[4]) {
+  u32 c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+  u32 k0 = key_in[0], k1 = key_in[1];
+  for (int round = 0; round < 10; ++round) {
+    u64 p0 = (u64)0xD2511F53u * (u64)c[0];
+    u64 p1 = (u64)0xCD9E8D57u * (u64)c[2];
+    u32 hi0 = (u32)(p0 >> 32), lo0 = (u32)p0;
+    u32 hi1 = (u32)(p1 >> 32), lo1 = (u32)p1;
+    u32 n[4] = {hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0};
+    c[0] = n[0]; c[1] = n[1]; c[2] = n[2]; c[3] = n[3];
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+// ----------------------------------------------------------------- c.2 det_log
+// ln(u) = e*ln2 + ln(m), ln(m) = 2*atanh(s), s = (m-1)/(m+1), atanh by its
+// series in z = s^2 (13 terms, c_k = 1/(2k+1)) -- only + - * / and frexp.
+double det_log(double u) {
+  int e = 0;
+  double m = std::frexp(u, &e);
+  if (m < 0x1.6a09e667f3bcdp-1) {
+    m = m * 2.0;
+    e = e - 1;
+  }
+  double s = (m - 1.0) / (m + 1.0);
+  double z = s * s;
+  double p = 1.0 / 25.0;  // c_12
+  for (int k = 11; k >= 0; --k) {
+    double pz = p * z;
+    p = pz + 1.0 / (double)(2 * k + 1);
+  }
+  const double LN2 = 0x1.62e42fefa39efp-1;
+  double a = (double)e * LN2;
+  double b = (2.0 * s) * p;
+  return a + b;
+}
+
+// ----------------------------------------------------------------- c.6 digests
+u64 mix(u64 x) {
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+u64 fold(std::initializer_list<u64> f) {
+  u64 h = 0x9E3779B97F4A7C15ull;
+  for (u64 v : f) h = mix(h ^ v);
+  return h;
+}
+
+u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
+
+// ----------------------------------------------------------------- per-worker profile
+struct Profile {
+  double peak_flops, mem_bw, eff_flops, eff_bw;
+  u64 mem_capacity;
+  double reserve_frac, iter_overhead_s, host_link_bw;
+  u32 tp_degree;
+  double tp_link_bw;
+  u64 kv_blocks_override;
+};
+
+Profile profile_of(const oracle_cfg &c, int decode_worker) {
+  Profile p;
+  if (!decode_worker) {
+    p = {c.peak_flops, c.mem_bw, c.eff_flops, c.eff_bw, c.mem_capacity, c.reserve_frac,
+         c.iter_overhead_s, c.host_link_bw, c.tp_degree, c.tp_link_bw, c.kv_blocks_override};
+  } else {
+    p = {c.d_peak_flops, c.d_mem_bw, c.d_eff_flops, c.d_eff_bw, c.d_mem_capacity,
+         c.d_reserve_frac, c.d_iter_overhead_s, c.d_host_link_bw, c.d_tp_degree,
+         c.d_tp_link_bw, c.d_kv_blocks_override};
+  }
+  return p;
+}
+
+// ----------------------------------------------------------------- c.1 derived constants
+bool derive(const oracle_cfg &c, int decode_worker, oracle_derived &d) {
+  const Profile pr = profile_of(c, decode_worker);
+  const u64 s = c.dtype_bytes, L = c.L, h = c.h, V = c.vocab, f = c.ffn;
+  const u64 q = (u64)c.n_heads * c.head_dim;
+  const u64 g = (u64)c.n_kv * c.head_dim;
+  // W = s*[ L*(h*(q+2g) + q*h + (gated?3:2)*h*f) + (tied?1:2)*V*h + (2L+1)*h ]
+  const u64 per_layer = h * (q + 2 * g) + q * h + (c.gated ? 3 : 2) * h * f;
+  d.W = s * (L * per_layer + (c.tied ? 1 : 2) * V * h + (2 * L + 1) * h);
+  d.kvb = 2 * L * g * s;
+  d.block_bytes = (u64)c.block_size * d.kvb;
+  d.reserve = (u64)std::floor((double)pr.mem_capacity * pr.reserve_frac);
+  if (pr.kv_blocks_override) {
+    d.total_blocks = pr.kv_blocks_override;
+  } else {
+    if (pr.mem_capacity < d.W + d.reserve)
+      return fail("mem_capacity " + std::to_string(pr.mem_capacity) + " < weights " +
+                  std::to_string(d.W) + " + reserve " + std::to_string(d.reserve));
+    d.total_blocks = (pr.mem_capacity - d.W - d.reserve) / d.block_bytes;
+  }
+  d.ratio_limit = (u64)std::floor(c.max_mem_ratio * (double)d.total_blocks);
+  d.invF = 1.0 / (pr.peak_flops * pr.eff_flops);
+  d.invB = 1.0 / (pr.mem_bw * pr.eff_bw);
+  d.invH = 1.0 / pr.host_link_bw;
+  d.invT = 1.0 / ((double)pr.tp_degree * pr.tp_link_bw);
+  d.scale_ns = 1e9 / c.rate;
+  d.slo_ttft_ns = (i64)std::floor(c.slo_ttft_s * 1e9 + 0.5);
+  d.slo_mtpot_ns = (i64)std::floor(c.slo_mtpot_s * 1e9 + 0.5);
+  return true;
+}
+
+// ----------------------------------------------------------------- c.2 workload
+u32 table_draw(u32 n, const u32 *lo, const u32 *hi, const u32 *thr, u32 x, u32 y) {
+  u32 b = n - 1;  // last bucket takes the rest
+  for (u32 i = 0; i + 1 < n; ++i) {
+    if (x < thr[i]) {
+      b = i;
+      break;
+    }
+  }
+  return lo[b] + (u32)(((u64)y * (u64)(hi[b] - lo[b])) >> 32);
+}
+
+bool workload(const oracle_cfg &c, std::vector<i64> &a, std::vector<u32> &p, std::vector<u32> &o) {
+  const u32 n = c.num_requests;
+  a.assign(n, 0);
+  p.assign(n, 0);
+  o.assign(n, 0);
+  if (c.len_dist == OR_LEN_TRACE) {
+    for (u32 i = 0; i < n; ++i) {
+      a[i] = c.trace_arrival_ns[i];
+      p[i] = c.trace_prompt[i];
+      o[i] = c.trace_output[i];
+    }
+    return true;
+  }
+  const u32 key[2] = {(u32)(c.seed & 0xffffffffu), (u32)(c.seed >> 32)};
+  const double scale_ns = 1e9 / c.rate;
+  i64 acc = 0;
+  for (u32 i = 0; i < n; ++i) {
+    const u32 cx[4] = {i, 0, 0, 0}, cy[4] = {i, 1, 0, 0};
+    u32 X[4], Y[4];
+    philox(cx, key, X);
+    philox(cy, key, Y);
+    const u64 v = ((u64)X[0] << 21) | (u64)(X[1] >> 11);
+    const double u = (double)(v + 1) * 0x1p-53;
+    const double E = -det_log(u);
+    const double es = E * scale_ns;
+    const i64 gap = (i64)std::floor(es + 0.5);
+    acc += gap;
+    a[i] = acc;
+    u32 pl = 0, ol = 0;
+    if (c.len_dist == OR_LEN_FIXED) {
+      pl = c.prompt_a;
+      ol = c.output_a;
+    } else if (c.len_dist == OR_LEN_UNIFORM) {
+      pl = c.prompt_a + (u32)(((u64)X[2] * (u64)(c.prompt_b - c.prompt_a + 1)) >> 32);
+      ol = c.output_a + (u32)(((u64)Y[0] * (u64)(c.output_b - c.output_a + 1)) >> 32);
+    } else if (c.len_dist == OR_LEN_TABLE) {
+      pl = table_draw(c.pt_n, c.pt_lo, c.pt_hi, c.pt_thr, X[2], X[3]);
+      ol = table_draw(c.ot_n, c.ot_lo, c.ot_hi, c.ot_thr, Y[0], Y[1]);
+    } else {
+      return fail("unknown len_dist");
+    }
+    if (ol > c.max_model_len - pl) ol = c.max_model_len - pl;  // o = min(o, mml - p)
+    p[i] = pl;
+    o[i] = ol;
+  }
+  return true;
+}
+
+// ----------------------------------------------------------------- c.5 cost model
+struct Prefill {
+  u64 P, c0;
+};
+
+struct CostCtx {
+  u64 L, h, q, g, f, fu, V, s;
+  double invF, invB, invH, invT, overhead;
+  u32 tp;
+};
+
+CostCtx cost_ctx(const oracle_cfg &c, const oracle_derived &d, int decode_worker) {
+  const Profile pr = profile_of(c, decode_worker);
+  CostCtx k;
+  k.L = c.L;
+  k.h = c.h;
+  k.q = (u64)c.n_heads * c.head_dim;
+  k.g = (u64)c.n_kv * c.head_dim;
+  k.f = c.ffn;
+  k.fu = c.gated ? 2 * (u64)c.ffn : (u64)c.ffn;
+  k.V = c.vocab;
+  k.s = c.dtype_bytes;
+  k.invF = d.invF;
+  k.invB = d.invB;
+  k.invH = d.invH;
+  k.invT = d.invT;
+  k.overhead = pr.iter_overhead_s;
+  k.tp = pr.tp_degree;
+  return k;
+}
+
+i64 iter_time(const CostCtx &K, const std::vector<Prefill> &pf, const std::vector<u64> &dec,
+              u64 swap_bytes) {
+  u64 Np = 0, Ap = 0, Kp = 0, Cd = 0;
+  const u64 Sp = pf.size(), D = dec.size();
+  for (const Prefill &e : pf) {
+    Np += e.P;
+    Ap += e.P * e.c0 + e.P * (e.P + 1) / 2;
+    Kp += e.c0 + e.P;
+  }
+  for (u64 c : dec) Cd += c;
+  const u64 N = Np + D, S = Sp + D;
+  const u64 h = K.h, q = K.q, g = K.g, f = K.f, fu = K.fu, V = K.V, s = K.s;
+  auto roof = [&](u64 F, u64 B) { return std::fmax((double)F * K.invF, (double)B * K.invB); };
+  double tQKV = 0.0, tATTP = 0.0, tATTD = 0.0, tO = 0.0, tUP = 0.0, tDOWN = 0.0, tLM = 0.0;
+  if (N > 0) {
+    tQKV = roof(2 * N * h * (q + 2 * g), s * (h * (q + 2 * g) + N * h + N * (q + 2 * g)));
+    tO = roof(2 * N * q * h, s * (q * h + N * q + N * h));
+    tUP = roof(2 * N * h * fu, s * (h * fu + N * h + N * fu));
+    tDOWN = roof(2 * N * f * h, s * (f * h + N * f + N * h));
+  }
+  if (Np > 0) tATTP = roof(4 * q * Ap, s * (Np * (2 * q + 2 * g) + 2 * g * Kp));
+  if (D > 0) tATTD = roof(4 * q * Cd, s * (D * (2 * q + 2 * g) + 2 * g * Cd));
+  if (S > 0) tLM = roof(2 * S * h * V, s * (V * h + S * h + S * V));
+  const double t_layer = ((((tQKV + tATTP) + tATTD) + tO) + tUP) + tDOWN;
+  double T = t_layer * (double)K.L;
+  T = T + tLM;
+  if (K.tp > 1) {
+    const u64 b_ar = 2 * (u64)(K.tp - 1) * N * h * s;
+    const double ar = (double)b_ar * K.invT;
+    T = T + ar * (double)(2 * K.L);
+  }
+  if (swap_bytes > 0) {
+    const double sw = (double)swap_bytes * K.invH;
+    T = T + sw;
+  }
+  T = T + K.overhead;
+  const double Tn = T * 1e9;
+  return (i64)std::floor(Tn + 0.5);
+}
+
+// ----------------------------------------------------------------- state
+enum Kind { K_DEC = 0, K_PRE_FRESH = 1, K_PRE_RECOMP = 2 };
+
+struct Req {
+  i64 a = 0;
+  u32 p = 0, o = 0;
+  u32 status = 0;  // 0 unfinished, 1 finished, 2 rejected
+  u64 ctx = 0, gen = 0;
+  i64 first_tok = 0, last_tok = 0, max_gap = 0;
+  u32 n_preempt = 0;
+  std::vector<u32> blocks;  // logical order
+  i64 finish = 0;
+  u64 finish_k = 0;
+};
+
+}  // namespace
+
+struct oracle_run {
+  oracle_summary summary;
+  std::vector<oracle_record> records;
+  std::vector<oracle_iter> iters;
+  std::vector<oracle_sample> trace[2];
+  std::vector<oracle_event> events;
+};
+
+namespace {
+
+// ----------------------------------------------------------------- c.6 metrics
+void metrics(const oracle_cfg &c, const oracle_derived &d, const std::vector<Req> &req,
+             oracle_summary &S) {
+  const u64 n = req.size();
+  std::vector<double> vals[5];
+  double tp_sum = 0.0, norm_sum = 0.0;
+  i64 ttft_sum = 0, e2e_sum = 0, mt_sum = 0;
+  u64 n_fin = 0, good_mt = 0, good_both = 0;
+  i64 last_finish = 0;
+  for (u64 i = 0; i < n; ++i) {
+    const Req &r = req[i];
+    if (r.status != 1) continue;
+    const i64 ttft = r.first_tok - r.a, e2e = r.finish - r.a, mt = r.max_gap;
+    ++n_fin;
+    last_finish = std::max(last_finish, r.finish);
+    vals[0].push_back((double)ttft / 1e9);
+    vals[2].push_back((double)e2e / 1e9);
+    vals[4].push_back((double)mt / 1e9);
+    ttft_sum += ttft;
+    e2e_sum += e2e;
+    mt_sum += mt;
+    if (r.o >= 2) {
+      const double v = (double)(e2e - ttft) / (double)(r.o - 1);
+      vals[1].push_back(v / 1e9);
+      tp_sum += v;
+    }
+    const double nv = (double)e2e / (double)r.o;
+    vals[3].push_back(nv / 1e9);
+    norm_sum += nv;
+    if (mt <= d.slo_mtpot_ns) {
+      ++good_mt;
+      if (ttft <= d.slo_ttft_ns) ++good_both;
+    }
+  }
+  const u32 qbp[4] = {5000, 9000, 9900, 10000};
+  for (int m = 0; m < 5; ++m) {
+    std::vector<double> v = vals[m];
+    std::sort(v.begin(), v.end());
+    const u64 cnt = v.size();
+    for (int qi = 0; qi < 4; ++qi) {
+      if (cnt == 0) {
+        S.stat[m][qi] = 0.0;
+        continue;
+      }
+      u64 rank = ((u64)qbp[qi] * cnt + 9999) / 10000;
+      if (rank < 1) rank = 1;
+      S.stat[m][qi] = v[rank - 1];
+    }
+    double mean = 0.0;
+    if (cnt > 0) {
+      if (m == 0) mean = ((double)ttft_sum / (double)cnt) / 1e9;
+      if (m == 2) mean = ((double)e2e_sum / (double)cnt) / 1e9;
+      if (m == 4) mean = ((double)mt_sum / (double)cnt) / 1e9;
+      if (m == 1) mean = (tp_sum / (double)cnt) / 1e9;
+      if (m == 3) mean = (norm_sum / (double)cnt) / 1e9;
+    }
+    S.stat[m][4] = mean;
+  }
+  S.last_finish_ns = last_finish;
+  S.first_arrival_ns = n ? req[0].a : 0;
+  const i64 span = last_finish - S.first_arrival_ns;
+  if (n_fin > 0 && span > 0) {
+    const double sec = (double)span / 1e9;
+    S.throughput_rps = (double)n_fin / sec;
+    S.goodput_mtpot_rps = (double)good_mt / sec;
+    S.goodput_both_rps = (double)good_both / sec;
+  }
+  (void)c;
+}
+
+// memory trace from the iteration list (c.6 "Memory trace")
+void build_trace(const oracle_cfg &c, const std::vector<oracle_iter> &it, u32 worker, i64 t_final,
+                 std::vector<oracle_sample> &out, bool &overflow) {
+  out.clear();
+  if (c.trace_mode == OR_TRACE_FULL) {
+    for (const oracle_iter &x : it) {
+      if (x.worker != worker) continue;
+      if (out.size() >= c.trace_cap_samples) {
+        overflow = true;
+        break;
+      }
+      out.push_back({x.t_start, x.T_ns, (u64)x.blocks * (u64)x.T_ns, (u32)x.blocks, 1u});
+    }
+  } else if (c.trace_mode == OR_TRACE_BINNED) {
+    const i64 W = (i64)c.trace_bin_ns;
+    const i64 nbins = (t_final + W - 1) / W;
+    for (i64 b = 0; b < nbins; ++b) {
+      if ((u64)out.size() >= c.trace_cap_samples) {
+        overflow = true;
+        break;
+      }
+      oracle_sample s = {b * W, W, 0, 0, 0};
+      const i64 lo = b * W, hi = (b + 1) * W;
+      for (const oracle_iter &x : it) {
+        if (x.worker != worker) continue;
+        const i64 ts = x.t_start, te = x.t_start + x.T_ns;
+        if (ts >= lo && ts < hi) s.n_iter += 1;
+        const i64 ov = std::min(te, hi) - std::max(ts, lo);
+        if (ov > 0) {
+          s.block_ns += x.blocks * (u64)ov;
+          s.blocks_max = std::max<u32>(s.blocks_max, (u32)x.blocks);
+        }
+      }
+      out.push_back(s);
+    }
+  }
+}
+
+bool check_invariants(const std::vector<Req> &req, const std::set<u32> &R, const std::set<u32> &Q,
+                      const std::set<u32> &freeset, u64 total, u64 bs) {
+  std::set<u32> seen(freeset.begin(), freeset.end());
+  u64 alloc = 0;
+  for (u32 id : R) {
+    const Req &r = req[id];
+    if (r.blocks.size() != ceil_div(r.ctx, bs)) return fail("held != ceil(ctx/bs) for request " + std::to_string(id));
+    for (u32 b : r.blocks) {
+      if (b >= total) return fail("block id out of range");
+      if (!seen.insert(b).second) return fail("block " + std::to_string(b) + " in two lists");
+      ++alloc;
+    }
+  }
+  for (u32 id : Q) {
+    if (!req[id].blocks.empty()) return fail("queued request holds blocks");
+    if (R.count(id)) return fail("request in both R and Q");
+  }
+  if (freeset.size() + alloc != total) return fail("free + allocated != total");
+  return true;
+}
+
+// ----------------------------------------------------------------- c.4 unified worker loop
+oracle_run *simulate_unified(const oracle_cfg &c) {
+  oracle_derived d;
+  if (!derive(c, 0, d)) return nullptr;
+  const CostCtx K = cost_ctx(c, d, 0);
+  std::vector<i64> A;
+  std::vector<u32> Pl, Ol;
+  if (!workload(c, A, Pl, Ol)) return nullptr;
+  const u32 n = c.num_requests;
+  const u64 bs = c.block_size, total = d.total_blocks;
+  const bool SWAPM = c.preempt == OR_SWAP;
+  const bool RATIO = c.kind == OR_CONT_RATIO;
+
+  std::vector<Req> req(n);
+  for (u32 i = 0; i < n; ++i) {
+    req[i].a = A[i];
+    req[i].p = Pl[i];
+    req[i].o = Ol[i];
+  }
+  oracle_run *run = new oracle_run();
+  std::memset(&run->summary, 0, sizeof(run->summary));
+  oracle_summary &S = run->summary;
+
+  std::set<u32> freeset;
+  for (u64 b = 0; b < total; ++b) freeset.insert((u32)b);
+  std::set<u32> R, Q;
+  i64 t = 0;
+  u64 k = 0;
+  u32 arr = 0, adm = 0;
+  u64 sched_d = 0, block_d = 0, req_d = 0;
+  u64 req_iters = 0, n_preempt_total = 0, swap_out_total = 0, swap_in_total = 0;
+  u64 peak = 0, block_ns_sum = 0, n_rej_total = 0;
+
+  auto alloc_lowest = [&](u32 id, u64 cnt) {
+    for (u64 j = 0; j < cnt; ++j) {
+      const u32 b = *freeset.begin();
+      freeset.erase(freeset.begin());
+      req[id].blocks.push_back(b);
+      block_d += fold({k, 1, id, b});
+      if (c.keep_events) run->events.push_back({k, 1, id, b, 0});
+    }
+  };
+  auto free_all = [&](u32 id) {
+    for (u32 b : req[id].blocks) {  // logical order
+      freeset.insert(b);
+      block_d += fold({k, 2, id, b});
+      if (c.keep_events) run->events.push_back({k, 2, id, b, 0});
+    }
+    req[id].blocks.clear();
+  };
+
+  while (true) {
+    // 0. termination
+    if (adm == n && R.empty() && Q.empty()) break;
+    if (c.horizon_ns >= 0 && t >= c.horizon_ns) {
+      S.status_flags |= 4;
+      break;
+    }
+    // 1. ingest: requests with a_i <= t are visible at this boundary (reading A2)
+    while (arr < n && req[arr].a <= t) ++arr;
+    // 2. idle skip
+    if (R.empty() && Q.empty() && adm == arr) {
+      t = req[arr].a;
+      continue;
+    }
+    std::map<u32, Kind> kind;
+    // 3. decode reservation + preemption (reading A7)
+    const u64 F = freeset.size();
+    std::vector<u32> Rv(R.begin(), R.end());
+    auto need_of = [&](u32 id) -> u64 { return (req[id].ctx % bs == 0) ? 1 : 0; };
+    u64 sum_need = 0;
+    for (u32 id : Rv) sum_need += need_of(id);
+    u64 m = 0, swap_out = 0;
+    if (sum_need > F) {
+      const u64 nr = Rv.size();
+      for (m = 1; m <= nr; ++m) {
+        u64 lhs = 0, rhs = F;
+        for (u64 j = 0; j < nr - m; ++j) lhs += need_of(Rv[j]);
+        for (u64 j = nr - m; j < nr; ++j) rhs += req[Rv[j]].blocks.size();
+        if (lhs <= rhs) break;
+      }
+      if (m >= nr) {
+        g_err = "preemption would evict r_1 (validation should make this impossible)";
+        delete run;
+        return nullptr;
+      }
+      for (u64 i = 0; i < m; ++i) {  // r_n, r_{n-1}, ..., r_{n-m+1}
+        const u32 id = Rv[nr - 1 - i];
+        Req &x = req[id];
+        const u64 held = x.blocks.size();
+        free_all(id);
+        x.n_preempt += 1;
+        if (SWAPM) {
+          swap_out += held * d.block_bytes;
+        } else {
+          x.ctx = 0;
+        }
+        R.erase(id);
+        Q.insert(id);
+      }
+      n_preempt_total += m;
+    }
+    for (u32 id : R) {  // surviving requests, ascending id
+      kind[id] = K_DEC;
+      if (need_of(id)) alloc_lowest(id, 1);
+    }
+    const u64 D3 = R.size();
+    u64 n_res = 0, n_adm = 0, n_rej = 0, swap_in = 0;
+    u64 tokens = D3;
+    if (m == 0) {
+      // 4. resume, head first, stop at the first misfit (reading A6)
+      std::vector<u32> Qv(Q.begin(), Q.end());
+      for (u32 id : Qv) {
+        Req &x = req[id];
+        u64 need, tok;
+        if (SWAPM) {
+          need = ceil_div(x.ctx, bs) + ((x.ctx % bs == 0) ? 1 : 0);
+          tok = 1;
+        } else {
+          need = ceil_div(x.p + x.gen, bs);
+          tok = x.p + x.gen;
+        }
+        const bool ok = (R.size() + 1 <= c.max_num_seqs) && (tokens + tok <= c.max_batched_tokens) &&
+                        ((i64)freeset.size() - (i64)need >= (i64)c.watermark_blocks);
+        if (!ok) break;
+        alloc_lowest(id, need);
+        Q.erase(id);
+        R.insert(id);
+        ++n_res;
+        tokens += tok;
+        if (SWAPM) {
+          swap_in += ceil_div(x.ctx, bs) * d.block_bytes;
+          kind[id] = K_DEC;
+        } else {
+          kind[id] = K_PRE_RECOMP;
+        }
+      }
+      // 5. fresh FCFS admission (STATIC P:167/A16; ratio P:460/A15)
+      if (Q.empty() && (c.kind != OR_STATIC || R.empty())) {
+        while (adm < arr) {
+          Req &x = req[adm];
+          const u64 need = ceil_div(x.p, bs);
+          const u64 cap = RATIO ? d.ratio_limit : total - c.watermark_blocks;
+          if (need > cap) {
+            x.status = 2;
+            ++n_rej;
+            ++adm;
+            continue;
+          }
+          const u64 fr = freeset.size();
+          if (R.size() + 1 > c.max_num_seqs) break;
+          if (tokens + x.p > c.max_batched_tokens) break;
+          if ((i64)fr - (i64)need < (i64)c.watermark_blocks) break;
+          if (RATIO && (total - fr) + need > d.ratio_limit) break;
+          alloc_lowest(adm, need);
+          R.insert(adm);
+          kind[adm] = K_PRE_FRESH;
+          tokens += x.p;
+          ++n_adm;
+          ++adm;
+        }
+      }
+    }
+    n_rej_total += n_rej;
+    // 6. empty batch
+    if (R.empty()) continue;
+    // 7. cost (c.5)
+    std::vector<Prefill> pf;
+    std::vector<u64> dec;
+    u64 Np = 0, Cd = 0;
+    for (u32 id : R) {
+      const Req &x = req[id];
+      if (kind[id] == K_DEC) {
+        dec.push_back(x.ctx + 1);
+        Cd += x.ctx + 1;
+      } else if (kind[id] == K_PRE_FRESH) {
+        pf.push_back({x.p, 0});
+        Np += x.p;
+      } else {
+        pf.push_back({x.p + x.gen, 0});
+        Np += x.p + x.gen;
+      }
+    }
+    const i64 T = iter_time(K, pf, dec, swap_out + swap_in);
+    // 8. commit
+    const i64 ts = t, te = t + T;
+    const u64 blocks = total - freeset.size();
+    const u64 entries = R.size();
+    u64 n_fin = 0;
+    std::vector<u32> Rc(R.begin(), R.end());
+    for (u32 id : Rc) {
+      Req &x = req[id];
+      const Kind kd = kind[id];
+      if (kd == K_PRE_FRESH) {
+        x.ctx = x.p;
+        x.gen = 1;
+        x.first_tok = te;
+        x.last_tok = te;
+      } else {
+        if (kd == K_PRE_RECOMP) {
+          x.ctx = x.p + x.gen;
+          x.gen += 1;
+        } else {
+          x.ctx += 1;
+          x.gen += 1;
+        }
+        const i64 gap = te - x.last_tok;
+        x.max_gap = std::max(x.max_gap, gap);
+        x.last_tok = te;
+      }
+      if (x.gen == x.o) {
+        x.status = 1;
+        x.finish = te;
+        x.finish_k = k;
+        req_d += fold({id, (u64)(x.first_tok - x.a), (u64)(x.finish - x.a), (u64)x.max_gap,
+                       x.n_preempt, k});
+        free_all(id);
+        R.erase(id);
+        ++n_fin;
+      }
+    }
+    sched_d += fold({k, (u64)ts, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej,
+                     n_fin, blocks});
+    run->iters.push_back({k, ts, T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej, n_fin,
+                          blocks, 0, 0});
+    req_iters += entries;
+    peak = std::max(peak, blocks);
+    block_ns_sum += blocks * (u64)T;
+    swap_out_total += swap_out;
+    swap_in_total += swap_in;
+    if (te < t) {
+      g_err = "clock went backwards";
+      delete run;
+      return nullptr;
+    }
+    t = te;
+    ++k;
+    if (c.check_invariants && !check_invariants(req, R, Q, freeset, total, bs)) {
+      delete run;
+      return nullptr;
+    }
+  }
+
+  // records + summary
+  run->records.resize(n);
+  u64 n_fin = 0;
+  for (u32 i = 0; i < n; ++i) {
+    const Req &x = req[i];
+    oracle_record &rec = run->records[i];
+    rec.ttft_ns = (x.gen >= 1 || x.status == 1) ? x.first_tok - x.a : 0;
+    rec.e2e_ns = x.status == 1 ? x.finish - x.a : 0;
+    rec.mtpot_ns = x.status == 1 ? x.max_gap : 0;
+    rec.n_preempt = x.n_preempt;
+    rec.status = x.status;
+    rec.finish_k = x.status == 1 ? x.finish_k : 0;
+    if (x.status == 1) ++n_fin;
+  }
+  S.n_requests = n;
+  S.n_finished = n_fin;
+  S.n_rejected = n_rej_total;
+  S.n_unfinished = n - n_fin - n_rej_total;
+  if (n_rej_total == n) S.status_flags |= 2;
+  S.n_iterations = k;
+  S.n_request_iterations = req_iters;
+  S.n_preemptions = n_preempt_total;
+  S.swap_out_bytes = swap_out_total;
+  S.swap_in_bytes = swap_in_total;
+  S.t_final = t;
+  S.sched_digest = sched_d;
+  S.block_digest = block_d;
+  S.request_digest = req_d;
+  S.total_blocks = total;
+  S.peak_blocks = peak;
+  S.block_ns_sum = block_ns_sum;
+  S.mean_util = (t > 0 && total > 0) ? (double)block_ns_sum / ((double)total * (double)t) : 0.0;
+  metrics(c, d, req, S);
+  bool ovf = false;
+  build_trace(c, run->iters, 0, t, run->trace[0], ovf);
+  if (ovf) S.status_flags |= 1;
+  return run;
+}
+
+// ----------------------------------------------------------------- a.9 P/D pair
+oracle_run *simulate_pd(const oracle_cfg &c) {
+  (void)c;
+  g_err = "PD_PAIR not implemented";
+  return nullptr;
+}
+
+}  // namespace
+
+// ======================================================================== C ABI
+extern "C" {
+
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  philox(ctr, key, out);
+}
+
+double oracle_det_log(double u) { return det_log(u); }
+
+int oracle_derive(const oracle_cfg *cfg, int decode_worker, oracle_derived *out) {
+  return derive(*cfg, decode_worker, *out) ? 0 : -1;
+}
+
+int oracle_workload(const oracle_cfg *cfg, int64_t *arrival, uint32_t *prompt, uint32_t *output) {
+  std::vector<i64> a;
+  std::vector<u32> p, o;
+  if (!workload(*cfg, a, p, o)) return -1;
+  for (u32 i = 0; i < cfg->num_requests; ++i) {
+    arrival[i] = a[i];
+    prompt[i] = p[i];
+    output[i] = o[i];
+  }
+  return 0;
+}
+
+int64_t oracle_iter_time_ns(const oracle_cfg *cfg, int decode_worker, uint32_t n_prefill,
+                            const uint32_t *P, const uint32_t *c0, uint32_t n_decode,
+                            const uint32_t *c, uint64_t swap_bytes) {
+  oracle_derived d;
+  if (!derive(*cfg, decode_worker, d)) return -1;
+  const CostCtx K = cost_ctx(*cfg, d, decode_worker);
+  std::vector<Prefill> pf;
+  std::vector<u64> dec;
+  for (u32 i = 0; i < n_prefill; ++i) pf.push_back({P[i], c0[i]});
+  for (u32 i = 0; i < n_decode; ++i) dec.push_back(c[i]);
+  return iter_time(K, pf, dec, swap_bytes);
+}
+
+uint64_t oracle_fold(const uint64_t *fields, uint32_t n) {
+  u64 h = 0x9E3779B97F4A7C15ull;
+  for (u32 i = 0; i < n; ++i) h = mix(h ^ fields[i]);
+  return h;
+}
+
+oracle_run *oracle_simulate(const oracle_cfg *cfg) {
+  g_err.clear();
+  if (cfg->topology == OR_PD_PAIR) return simulate_pd(*cfg);
+  return simulate_unified(*cfg);
+}
+
+const char *oracle_error(void) { return g_err.c_str(); }
+
+void oracle_summary_get(const oracle_run *r, oracle_summary *out) { *out = r->summary; }
+
+uint64_t oracle_records(const oracle_run *r, oracle_record *out) {
+  if (out) std::copy(r->records.begin(), r->records.end(), out);
+  return r->records.size();
+}
+uint64_t oracle_iters(const oracle_run *r, oracle_iter *out) {
+  if (out) std::copy(r->iters.begin(), r->iters.end(), out);
+  return r->iters.size();
+}
+uint64_t oracle_trace(const oracle_run *r, int worker, oracle_sample *out) {
+  const std::vector<oracle_sample> &v = r->trace[worker ? 1 : 0];
+  if (out) std::copy(v.begin(), v.end(), out);
+  return v.size();
+}
+uint64_t oracle_events(const oracle_run *r, oracle_event *out) {
+  if (out) std::copy(r->events.begin(), r->events.end(), out);
+  return r->events.size();
+}
+void oracle_free(oracle_run *r) { delete r; }
+
+}  // extern "C"

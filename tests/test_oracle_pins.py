@@ -1,0 +1,497 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+Each test ties the oracle to something other than itself: known-answer vectors
+(Random123), published model facts (parameter counts), closed forms
+(roofline limits, Lindley recursion, isolated requests), hand-worked traces
+(SURVEY §8(c.8)), statistics the paper/spec fixes (Poisson arrivals S:111/S:125)
+and invariants.  Golden values live in
+tests/golden/*.json with their citations.
+"""
+import json
+import math
+import os
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import sweep_inputs as si
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+LN2 = float.fromhex("0x1.62e42fefa39efp-1")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def trace_cfg(reqs, hw=si.A100_IDEAL, pol=si.Policy(), model=si.LLAMA2_7B, **opt):
+    w = si.Workload(len(reqs), [1.0], [0], len_dist=si.TRACE,
+                    trace_arrival_ns=[r[0] for r in reqs], trace_prompt=[r[1] for r in reqs],
+                    trace_output=[r[2] for r in reqs], prompt_table=None, output_table=None)
+    return si.SweepConfig("trace", model, [hw], [pol], w, si.Options(**opt))
+
+
+# ------------------------------------------------------------------ a.1 generator
+def test_philox_known_answers(oracle_lib):
+    for v in gold("philox_kat.json")["vectors"]:
+        ctr = [int(x, 16) for x in v["ctr"]]
+        key = [int(x, 16) for x in v["key"]]
+        assert list(oracle_lib.philox(ctr, key)) == [int(x, 16) for x in v["out"]]
+
+
+def test_det_log_exact_cases(oracle_lib):
+    assert oracle_lib.det_log(1.0) == 0.0
+    for k in range(1, 64):
+        assert oracle_lib.det_log(2.0 ** -k) == (-k) * LN2
+
+
+def test_det_log_matches_libm(oracle_lib):
+    rng = np.random.default_rng(1)
+    us = np.concatenate([rng.random(20000), 1.0 - rng.random(2000) * 1e-12,
+                         np.exp(-rng.random(2000) * 700)])
+    worst_ulp = 0.0
+    for u in us:
+        if u <= 0.0:
+            continue
+        ref = math.log(u)
+        got = oracle_lib.det_log(float(u))
+        if ref != 0.0:
+            worst_ulp = max(worst_ulp, abs(got - ref) / math.ulp(ref))
+    # within 2 ulp of libm log (SURVEY c.8 quotes <= 3.6e-16 relative on its sample)
+    assert worst_ulp <= 2.0, worst_ulp
+
+
+def _gen(cfg):
+    from oracle import oracle as O
+    return O.workload(cfg, 0)
+
+
+def test_arrivals_are_poisson(oracle_lib):
+    from scipy import stats
+    lam = 2.0
+    cfg = si.SweepConfig("w", si.LLAMA2_7B, [si.A100], [si.Policy()], si.Workload(50000, [lam], [7]))
+    a, p, o = _gen(cfg)
+    gaps = np.diff(np.concatenate([[0], a])) / 1e9
+    assert gaps.min() >= 0
+    # mean inter-arrival within [0.45, 0.55] s at qps = 2 (we use a 3% band)
+    assert abs(gaps.mean() - 1 / lam) < 0.03 / lam
+    # exponential shape (no dropped minus sign, no wrong scale)
+    assert stats.kstest(gaps, "expon", args=(0, 1 / lam)).pvalue > 1e-3
+    # counts in disjoint equal windows have dispersion index in [0.8, 1.2]
+    a1 = a[:10000] / 1e9
+    counts = np.bincount(np.floor(a1).astype(int))[:-1]
+    assert 0.8 <= counts.var() / counts.mean() <= 1.2
+
+
+def test_workload_determinism_and_seeds(oracle_lib):
+    cfg = si.SweepConfig("w", si.LLAMA2_7B, [si.A100], [si.Policy()], si.Workload(1000, [2.0], [7, 8]))
+    from oracle import oracle as O
+    a0, p0, o0 = O.workload(cfg, 0)
+    a1, p1, o1 = O.workload(cfg, 0)
+    b, q, r = O.workload(cfg, 1)
+    assert (a0 == a1).all() and (p0 == p1).all() and (o0 == o1).all()
+    assert not (a0 == b).all() and not (p0 == q).all()
+    # rate only rescales the exponentials: a(lambda=4) ~= a(lambda=2)/2
+    cfg4 = replace(cfg, workload=replace(cfg.workload, rates=[4.0]))
+    a4, p4, o4 = O.workload(cfg4, 0)
+    assert (p4 == p0).all() and (o4 == o0).all()
+    assert np.abs(a4 - a0 / 2).max() <= 1000  # one rounding per gap, <= n * 1 ns
+
+
+def test_length_table_statistics(oracle_lib):
+    n = 200000
+    cfg = si.SweepConfig("w", si.LLAMA2_7B, [si.A100], [si.Policy()], si.Workload(n, [1.0], [7]))
+    a, p, o = _gen(cfg)
+    for vals, t in ((p, si.SHAREGPT_PROMPT), (None, si.SHAREGPT_OUTPUT)):
+        edges = list(t.thr) + [2 ** 32]
+        probs = np.diff([0] + edges) / 2 ** 32
+        if vals is None:
+            # unclamped output draws: only requests whose clamp is inactive
+            mask = o < 2048 - p
+            vals = o[mask]
+            probs_eff = None
+        else:
+            probs_eff = probs
+        bucket = np.searchsorted(np.asarray(t.hi), vals, side="right")
+        assert (vals >= t.lo[0]).all() and (vals < t.hi[-1]).all()
+        if probs_eff is not None:
+            freq = np.bincount(bucket, minlength=len(t.lo)) / len(vals)
+            sig = np.sqrt(probs_eff * (1 - probs_eff) / len(vals))
+            assert (np.abs(freq - probs_eff) < 5 * sig + 1e-12).all(), (freq, probs_eff)
+            # analytic mean of lo + floor(y*(hi-lo)/2^32) with y uniform
+            mean = sum(pr * (lo + (hi - lo - 1) / 2) for pr, lo, hi in zip(probs, t.lo, t.hi))
+            assert abs(vals.mean() - mean) / mean < 0.01
+            # within-bucket uniformity of the multiply-shift draw (bucket [64,128))
+            sel = vals[bucket == 3]
+            assert abs(sel.mean() - (64 + 127) / 2) < 1.0
+    assert (p + o <= 2048).all() and (o >= 1).all()
+    assert abs(p.mean() - 161.31) < 2.0  # vLLM's published ShareGPT prompt mean (A25, ext)
+
+
+def test_fixed_and_uniform_lengths(oracle_lib):
+    w = si.Workload(5000, [1.0], [3], len_dist=si.FIXED, prompt_a=128, output_a=1024)
+    a, p, o = _gen(si.SweepConfig("w", si.LLAMA2_7B, [si.A100], [si.Policy()], w))
+    assert (p == 128).all() and (o == 1024).all()
+    w = si.Workload(20000, [1.0], [3], len_dist=si.UNIFORM, prompt_a=10, prompt_b=20, output_a=1, output_b=4)
+    a, p, o = _gen(si.SweepConfig("w", si.LLAMA2_7B, [si.A100], [si.Policy()], w))
+    assert p.min() == 10 and p.max() == 20 and o.min() == 1 and o.max() == 4
+    cnt = np.bincount(o)[1:]
+    assert (np.abs(cnt / cnt.sum() - 0.25) < 0.02).all()
+
+
+# ------------------------------------------------------------------ c.1 constants
+BIG = si.Hw(mem_capacity=10 ** 12)
+
+
+def _one(model, hw=None, pol=si.Policy()):
+    if hw is None:
+        hw = BIG if model is si.LLAMA2_70B else si.A100
+    return si.SweepConfig("m", model, [hw], [pol], si.Workload(1, [1.0], [0]))
+
+
+def test_weight_bytes_match_published_params(oracle_lib):
+    pub = gold("llama2_published.json")["models"]
+    for m in (si.LLAMA2_7B, si.LLAMA2_13B, si.LLAMA2_70B):
+        d = oracle_lib.derive(_one(m))
+        ref = pub[m.name]
+        assert (m.num_layers, m.hidden, m.num_heads, m.num_kv_heads) == (ref["L"], ref["h"], ref["n_heads"], ref["n_kv"])
+        assert d["W"] == 2 * ref["params"]
+        assert d["kvb"] == ref["kvb"]
+        assert d["block_bytes"] == 16 * ref["kvb"]
+
+
+def test_block_capacity_ladder(oracle_lib):
+    got = [oracle_lib.derive(_one(si.LLAMA2_7B, si.Hw(mem_capacity=c * 10 ** 9)))["total_blocks"]
+           for c in (20, 40, 80, 160, 320, 640)]
+    assert got == [658, 2923, 7453, 16513, 34633, 70872]
+    assert oracle_lib.derive(_one(si.LLAMA2_13B))["total_blocks"] == 3812
+    assert [oracle_lib.derive(_one(si.LLAMA2_70B, h))["total_blocks"] for h in si.c4_hws()] == [2679, 31670, 89654]
+    # capacity below the weights is rejected ("lower than the model parameter size")
+    with pytest.raises(Exception):
+        oracle_lib.derive(_one(si.LLAMA2_7B, si.Hw(mem_capacity=10 * 10 ** 9)))
+
+
+def test_ratio_limit(oracle_lib):
+    d = oracle_lib.derive(_one(si.LLAMA2_7B, pol=si.Policy(kind=si.CONT_RATIO, max_mem_ratio=0.9)))
+    assert d["ratio_limit"] == math.floor(0.9 * 7453)
+
+
+# ------------------------------------------------------------------ a.6 cost model
+def _t(cfg, prefills=(), decodes=(), swap=0):
+    from oracle import oracle as O
+    return O.iter_time_ns(cfg, [(P, 0) for P in prefills], decodes, swap)
+
+
+def test_cost_closed_form_rows(oracle_lib):
+    for row in gold("cost_closed_form.json")["rows"]:
+        hw = si.A100 if row.get("defaults") else si.A100_IDEAL
+        cfg = _one(si.LLAMA2_7B, hw)
+        dec = [c for c, b in row["decodes"] for _ in range(b)]
+        assert _t(cfg, row["prefills"], dec) == row["T_ns"], row["desc"]
+
+
+@pytest.mark.parametrize("model", [si.LLAMA2_7B, si.LLAMA2_13B, si.LLAMA2_70B])
+def test_cost_memory_bound_limit(oracle_lib, model):
+    """Infinite FLOP/s: a decode step reads every linear weight once plus the KV
+    of its context; per extra context token exactly kvb bytes."""
+    pub = gold("llama2_published.json")["models"][model.name]
+    B = 2.039e12
+    cfg = _one(model, si.Hw(peak_flops=1e30, mem_bw=B, eff_flops=1, eff_bw=1, iter_overhead_s=0,
+                                    mem_capacity=10 ** 12))
+    L, h, V = model.num_layers, model.hidden, model.vocab
+    # weights the decode step touches = all params except the input embedding and the norms (A19)
+    wbytes = 2 * (pub["params"] - V * h - (2 * L + 1) * h)
+    # generous bound on activation + logit bytes per token (far below any weight matrix)
+    act = L * 2 * 8 * (h + model.ffn_dim) + 4 * V
+    t1 = _t(cfg, decodes=[1])
+    assert 0 <= t1 * 1e-9 * B - wbytes < act
+    t2 = _t(cfg, decodes=[1001])
+    assert abs((t2 - t1) - 1000 * pub["kvb"] / B * 1e9) <= 2
+    # batch: b decodes share one weight read
+    tb = _t(cfg, decodes=[1] * 64)
+    assert 0 <= tb * 1e-9 * B - wbytes < 64 * act
+
+
+@pytest.mark.parametrize("model", [si.LLAMA2_7B, si.LLAMA2_70B])
+def test_cost_compute_bound_limit(oracle_lib, model):
+    """Infinite bandwidth: a prefill of P tokens costs 2 FLOPs per linear weight per token
+    plus causal attention 4*q*L*P(P+1)/2 plus one LM-head row."""
+    pub = gold("llama2_published.json")["models"][model.name]
+    F = 312e12
+    cfg = _one(model, si.Hw(peak_flops=F, mem_bw=1e30, eff_flops=1, eff_bw=1, iter_overhead_s=0,
+                                    mem_capacity=10 ** 12))
+    L, h, V = model.num_layers, model.hidden, model.vocab
+    q = model.num_heads * model.head_dim
+    linear = pub["params"] - 2 * V * h - (2 * L + 1) * h
+    for P in (1, 128, 2048):
+        flops = 2 * P * linear + 4 * q * L * P * (P + 1) // 2 + 2 * h * V
+        assert abs(_t(cfg, prefills=[P]) - flops / F * 1e9) <= 2
+
+
+def test_cost_tp_allreduce_and_swap_terms(oracle_lib):
+    m = si.LLAMA2_70B
+    base = si.Hw(peak_flops=2 * 312e12, mem_bw=2 * 2.039e12, mem_capacity=160 * 10 ** 9,
+                 eff_flops=1, eff_bw=1, iter_overhead_s=0, host_link_bw=32e9)
+    tp = replace(base, tp_degree=2, tp_link_bw=300e9)
+    for N in (1, 37):
+        t0 = _t(_one(m, base), decodes=[100] * N)
+        t1 = _t(_one(m, tp), decodes=[100] * N)
+        # ring all-reduce: 2(t-1)/t * N*h*s bytes per all-reduce, 2 per layer
+        expect = 2 * m.num_layers * (2 * 1 / 2) * N * m.hidden * 2 / 300e9 * 1e9
+        assert abs((t1 - t0) - expect) <= 2
+    x = 7 * 16 * 327680
+    assert abs(_t(_one(m, base), decodes=[5], swap=x) - _t(_one(m, base), decodes=[5]) - x / 32e9 * 1e9) <= 1
+
+
+def test_cost_monotone_random_plans(oracle_lib):
+    rng = np.random.default_rng(5)
+    cfg = _one(si.LLAMA2_13B, si.A100)
+    for _ in range(100):
+        pf = list(rng.integers(1, 2048, rng.integers(0, 4)))
+        dec = list(rng.integers(1, 2048, rng.integers(0, 40)))
+        if not pf and not dec:
+            dec = [1]
+        t = _t(cfg, pf, dec)
+        assert _t(cfg, pf, dec + [int(rng.integers(1, 2048))]) >= t
+        assert _t(cfg, pf + [int(rng.integers(1, 2048))], dec) >= t
+        if dec:
+            assert _t(cfg, pf, [c + 1 for c in dec]) >= t
+    # phase classes: prefill 2048 compute-bound, decode b=1 memory-bound
+    fast_bw = si.Hw(mem_bw=2.039e14)
+    fast_f = si.Hw(peak_flops=312e14)
+    assert _t(_one(si.LLAMA2_7B, fast_f), prefills=[2048]) < 0.2 * _t(_one(si.LLAMA2_7B), prefills=[2048])
+    assert _t(_one(si.LLAMA2_7B, fast_bw), decodes=[1]) < 0.2 * _t(_one(si.LLAMA2_7B), decodes=[1])
+    assert abs(_t(_one(si.LLAMA2_7B, si.Hw(peak_flops=624e12)), decodes=[1])
+               / _t(_one(si.LLAMA2_7B), decodes=[1]) - 1) < 0.01
+
+
+# ------------------------------------------------------------------ a.2-a.7 hand-worked traces
+def _sim(cfg, **kw):
+    from oracle import oracle as O
+    return O.simulate(cfg, 0, check_invariants=True, **kw)
+
+
+def test_single_request_trace(oracle_lib):
+    g = gold("hand_traces.json")["single"]
+    cfg = trace_cfg(g["requests"])
+    assert _t(cfg, prefills=[20]) == g["T_pre_20"]
+    assert _t(cfg, decodes=[21]) == g["T_dec_21"] and _t(cfg, decodes=[22]) == g["T_dec_22"]
+    r = _sim(cfg, keep_events=True, want=("summary", "records", "iters", "events"))
+    rec = r["records"][0]
+    assert (rec["ttft_ns"], rec["e2e_ns"], rec["mtpot_ns"]) == (g["ttft"], g["e2e"], g["mtpot"])
+    allocs = [int(e["block"]) for e in r["events"] if e["kind"] == 1]
+    assert allocs == g["blocks"]
+    s = r["summary"]
+    assert s["n_iterations"] == 3 and s["n_request_iterations"] == 3
+    assert abs(s["stat"][1][0] - (g["e2e"] - g["ttft"]) / 2 / 1e9) < 1e-18  # TPOT 6,488,846.5 ns
+
+
+def test_two_request_trace(oracle_lib):
+    g = gold("hand_traces.json")["two"]
+    r = _sim(trace_cfg(g["requests"]), keep_events=True, want=("summary", "records", "iters", "events"))
+    assert list(r["iters"]["T_ns"]) == g["iter_T"]
+    assert list(r["iters"]["S_p"]) == [1, 1, 0] and list(r["iters"]["D"]) == [0, 1, 2]
+    for i, key in ((0, "r0"), (1, "r1")):
+        assert r["records"][i]["ttft_ns"] == g[key]["ttft"]
+        assert r["records"][i]["e2e_ns"] == g[key]["e2e"]
+    for rid, blocks in g["blocks"].items():
+        got = [int(e["block"]) for e in r["events"] if e["kind"] == 1 and e["req"] == int(rid)]
+        assert got == blocks
+
+
+def test_isolated_requests_closed_form(oracle_lib):
+    g = gold("hand_traces.json")["isolated"]
+    cfg = trace_cfg([(0, g["p"], g["o"]), (10 ** 12, g["p"], g["o"])])
+    r = _sim(cfg)
+    expect_e2e = _t(cfg, prefills=[g["p"]]) + sum(_t(cfg, decodes=[g["p"] + j]) for j in range(1, g["o"]))
+    for rec in r["records"]:
+        assert rec["ttft_ns"] == g["ttft"] and rec["e2e_ns"] == g["e2e"] == expect_e2e
+
+
+@pytest.mark.parametrize("mode", [si.SWAP, si.RECOMPUTE])
+def test_preemption_hand_trace(oracle_lib, mode):
+    g = gold("hand_traces.json")["preemption"]
+    model = replace(si.LLAMA2_7B, max_model_len=g["max_model_len"])
+    hw = replace(si.A100_IDEAL, kv_blocks_override=g["total_blocks"])
+    pol = si.Policy(preempt=mode, block_size=g["block_size"])
+    cfg = trace_cfg(g["requests"], hw=hw, pol=pol, model=model)
+    r = _sim(cfg, keep_events=True, want=("summary", "records", "iters", "events"))
+    s, it = r["summary"], r["iters"]
+    assert s["n_iterations"] == g["iterations"] and s["n_request_iterations"] == g["request_iterations"]
+    ev = [[int(e["k"]), int(e["kind"]), int(e["req"]), int(e["block"])] for e in r["events"]]
+    assert ev == g["events"]
+    assert list(it["m"]) == [0, 0, 0, 0, 0, 1, 0] and list(it["n_resumed"]) == [0] * 6 + [1]
+    bb = g["block_size"] * 524288
+    if mode == si.SWAP:
+        assert s["swap_out_bytes"] == g["swap_blocks_out"] * bb and s["swap_in_bytes"] == g["swap_blocks_in"] * bb
+        assert list(it["S_p"]) == [2, 0, 0, 0, 0, 0, 0]
+        assert it["C_d"][6] == 9
+    else:
+        assert s["swap_out_bytes"] == 0 and s["swap_in_bytes"] == 0
+        assert list(it["S_p"]) == [2, 0, 0, 0, 0, 0, 1] and it["N_p"][6] == 9
+    r1 = r["records"][1]
+    assert r1["n_preempt"] == 1 and r["records"][0]["n_preempt"] == 0
+    assert r1["mtpot_ns"] == it["T_ns"][5] + it["T_ns"][6]           # gap spans It6 + It7
+    assert r1["mtpot_ns"] > max(it["T_ns"][1:5])
+
+
+def test_single_server_lindley(oracle_lib):
+    """max_num_seqs = 1 is the FCFS single-server queue: start_i = max(a_i, fin_{i-1})."""
+    rng = np.random.default_rng(11)
+    n = 25
+    a = np.cumsum(rng.integers(0, 400_000_000, n))
+    p = rng.integers(1, 300, n)
+    o = rng.integers(1, 40, n)
+    cfg = trace_cfg(list(zip(a.tolist(), p.tolist(), o.tolist())), pol=si.Policy(max_num_seqs=1))
+    r = _sim(cfg)
+    fin = 0
+    for i in range(n):
+        start = max(int(a[i]), fin)
+        tp = _t(cfg, prefills=[int(p[i])])
+        td = [_t(cfg, decodes=[int(p[i]) + j]) for j in range(1, int(o[i]))]
+        fin = start + tp + sum(td)
+        rec = r["records"][i]
+        assert rec["ttft_ns"] == start + tp - a[i]
+        assert rec["e2e_ns"] == fin - a[i]
+        assert rec["mtpot_ns"] == (max(td) if td else 0)
+
+
+def test_static_batching_bubbles(oracle_lib):
+    """outputs {2,3,5,8}, batch 4 -> the next batch starts only after the 8-token
+    request finishes (P:426 'shorter requests have to wait'); continuous batching admits
+    the fifth request as soon as a slot frees."""
+    reqs = [(0, 10, 2), (0, 10, 3), (0, 10, 5), (0, 10, 8), (0, 10, 3)]
+    st = _sim(trace_cfg(reqs, pol=si.Policy(kind=si.STATIC, max_num_seqs=4)))["records"]
+    co = _sim(trace_cfg(reqs, pol=si.Policy(kind=si.CONT, max_num_seqs=4)))["records"]
+    assert st[4]["ttft_ns"] > st[3]["e2e_ns"]
+    assert co[4]["ttft_ns"] < co[3]["e2e_ns"]
+    assert co["e2e_ns"].max() <= st["e2e_ns"].max()                        # S:361 makespan
+    # batch of one degenerates to sequential FCFS
+    b1s = _sim(trace_cfg(reqs, pol=si.Policy(kind=si.STATIC, max_num_seqs=1)))["records"]
+    b1c = _sim(trace_cfg(reqs, pol=si.Policy(kind=si.CONT, max_num_seqs=1)))["records"]
+    assert (b1s == b1c).all()
+
+
+def test_mixed_arrival_joins_next_boundary(oracle_lib):
+    """a request arriving mid-iteration joins at the next boundary."""
+    cfg = trace_cfg([(0, 100, 50), (1, 100, 5)])
+    r = _sim(cfg, want=("summary", "records", "iters"))
+    it = r["iters"]
+    assert it["S_p"][0] == 1 and it["S_p"][1] == 1 and it["D"][1] == 1
+    assert r["records"][1]["ttft_ns"] == it["T_ns"][0] + it["T_ns"][1] - 1
+
+
+# ------------------------------------------------------------------ invariants / properties
+def _random_micro(rng):
+    n = int(rng.integers(1, 60))
+    a = np.sort(rng.integers(0, 3_000_000_000, n))
+    p = rng.integers(1, 64, n)
+    o = rng.integers(1, 64, n)
+    mml = 128
+    model = replace(si.LLAMA2_7B, max_model_len=mml)
+    bs = int(rng.choice([1, 4, 16]))
+    total = int(rng.integers(-(-mml // bs), -(-mml // bs) + 40))
+    hw = replace(si.A100, kv_blocks_override=total)
+    kind = rng.choice([si.STATIC, si.CONT, si.CONT_RATIO])
+    pol = si.Policy(kind=str(kind), preempt=str(rng.choice([si.SWAP, si.RECOMPUTE])),
+                    max_mem_ratio=float(rng.choice([0.3, 0.7, 1.0])),
+                    max_num_seqs=int(rng.choice([1, 3, 8, 256])), block_size=bs,
+                    max_batched_tokens=int(rng.choice([mml, 300, si.UINT32_MAX])),
+                    watermark_blocks=int(rng.integers(0, total - (-(-mml // bs)) + 1)))
+    return trace_cfg(list(zip(a.tolist(), p.tolist(), o.tolist())), hw=hw, pol=pol, model=model,
+                     trace_mode=si.FULL), o
+
+
+def test_invariants_random_micro_configs(oracle_lib):
+    rng = np.random.default_rng(2024)
+    for _ in range(150):
+        cfg, o = _random_micro(rng)
+        r = _sim(cfg, want=("summary", "records", "iters", "trace"))
+        s, rec = r["summary"], r["records"]
+        fin = rec["status"] == 1
+        assert s["n_finished"] + s["n_rejected"] == len(rec)
+        assert s["n_request_iterations"] == int(o[fin].sum())
+        assert (rec["e2e_ns"][fin] >= rec["ttft_ns"][fin]).all()
+        first = rec["ttft_ns"][fin] + np.asarray(cfg.workload.trace_arrival_ns)[fin]
+        assert (np.diff(first) >= 0).all()                                   # S:392 FCFS
+        tr = r["trace"][0]
+        assert (tr["blocks_max"] <= s["total_blocks"]).all()
+        assert int(tr["block_ns"].sum()) == s["block_ns_sum"]
+        if cfg.policies[0].kind != si.CONT_RATIO:
+            assert s["n_rejected"] == 0
+
+
+def test_binned_trace_integral_equals_full(oracle_lib):
+    cfg = replace(si.c1(), options=si.Options(trace_mode=si.BINNED, trace_bin_ns=250_000_000))
+    from oracle import oracle as O
+    rb = O.simulate(cfg, 0, want=("summary", "trace"))
+    rf = O.simulate(replace(cfg, options=si.Options(trace_mode=si.FULL, trace_cap_bytes=1 << 24)), 0,
+                    want=("summary", "trace", "iters"))
+    assert int(rb["trace"][0]["block_ns"].sum()) == int(rf["trace"][0]["block_ns"].sum()) == rb["summary"]["block_ns_sum"]
+    assert len(rb["trace"][0]) == -(-rb["summary"]["t_final"] // 250_000_000)
+    assert int(rb["trace"][0]["n_iter"].sum()) == rb["summary"]["n_iterations"]
+    assert rb["trace"][0]["blocks_max"].max() == rb["summary"]["peak_blocks"]
+
+
+def test_nearest_rank_quantiles(oracle_lib):
+    """nearest rank = ceil(q*n)-th smallest.  Isolated o=1 requests have
+    e2e = T_pre(p) exactly, so the latency multiset is known in closed form."""
+    ps = [int(x) for x in np.random.default_rng(3).permutation(np.arange(5, 105))]
+    cfg = trace_cfg([(i * 10 ** 11, p, 1) for i, p in enumerate(ps)])
+    r = _sim(cfg)
+    lat = sorted(_t(cfg, prefills=[p]) / 1e9 for p in ps)
+    st = r["summary"]["stat"]
+    for j, q in enumerate((0.50, 0.90, 0.99, 1.00)):
+        assert st[2][j] == lat[math.ceil(q * len(lat)) - 1]
+    assert st[2][3] == max(lat) and st[1].tolist() == [0.0] * 5     # o = 1: TPOT excluded
+    assert abs(st[2][4] - sum(lat) / len(lat)) < 1e-12
+
+
+def test_goodput_definition(oracle_lib):
+    cfg = replace(si.c1(), workload=replace(si.c1().workload, rates=[40.0]),
+                  options=si.Options(slo_ttft_s=0.06, slo_mtpot_s=0.08))
+    from oracle import oracle as O
+    r = O.simulate(cfg, 0)
+    rec, s = r["records"], r["summary"]
+    a, p, o = O.workload(cfg, 0)
+    fin = rec["status"] == 1
+    span = (int((rec["e2e_ns"] + a)[fin].max()) - int(a[0])) / 1e9
+    ok_mt = fin & (rec["mtpot_ns"] <= 80_000_000)
+    ok_both = ok_mt & (rec["ttft_ns"] <= 60_000_000)
+    assert 0 < ok_both.sum() < ok_mt.sum() < fin.sum()
+    assert s["goodput_mtpot_rps"] == pytest.approx(ok_mt.sum() / span, rel=1e-12)
+    assert s["goodput_both_rps"] == pytest.approx(ok_both.sum() / span, rel=1e-12)
+    assert s["throughput_rps"] == pytest.approx(fin.sum() / span, rel=1e-12)
+
+
+def test_finding1_continuous_beats_static(oracle_lib):
+    """Finding 1 as a trend check: NORM latency P50/P99 of continuous
+    batching <= static batching at every rate, and the gap grows with load."""
+    from oracle import oracle as O
+    gaps = []
+    for lam in (1.0, 2.0, 4.0):
+        w = si.Workload(2000, [lam], [0])
+        out = {}
+        for k in (si.STATIC, si.CONT):
+            cfg = si.SweepConfig("f1", si.LLAMA2_7B, [si.A100], [si.Policy(kind=k, max_num_seqs=16)], w)
+            out[k] = O.simulate(cfg, 0)["summary"]["stat"][3]
+        assert out[si.CONT][0] <= out[si.STATIC][0] and out[si.CONT][2] <= out[si.STATIC][2]
+        gaps.append(out[si.STATIC][0] - out[si.CONT][0])
+    assert gaps[0] < gaps[-1]
+
+
+def test_finding2_ratio_reduces_preemption(oracle_lib):
+    """Finding 2: limiting new-request admission to a memory ratio reduces
+    preemptions on a preemption-heavy scenario."""
+    from oracle import oracle as O
+    w = si.Workload(1500, [12.0], [0])
+    res = {}
+    for r in (1.0, 0.7):
+        k = si.CONT_RATIO if r < 1 else si.CONT
+        cfg = si.SweepConfig("f2", si.LLAMA2_13B, [si.A100], [si.Policy(kind=k, max_mem_ratio=r)], w)
+        res[r] = O.simulate(cfg, 0)["summary"]
+    assert res[1.0]["n_preemptions"] > 0
+    assert res[0.7]["n_preemptions"] < res[1.0]["n_preemptions"]
+    assert res[0.7]["stat"][4][3] < res[1.0]["stat"][4][3]         # max mTPOT shrinks
