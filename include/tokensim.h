@@ -1,0 +1,275 @@
+/* tokensim.h -- C ABI of the B200-native batched design-space sweep.
+ *
+ * What this library computes (PAPER.md = arXiv 2503.08415, TokenSim; P:NNN =
+ * PAPER.md line): thousands of independent LLM-serving simulations ("points"),
+ * one per (hardware profile x scheduling/memory policy x arrival rate x seed).
+ * Each point replays TokenSim's worker loop: a workload of requests
+ * "generated from datasets and parameters" with Poisson arrivals
+ * (reading A24); an iteration-level scheduler invoked at the default
+ * end-of-iteration breakpoint doing continuous or static batching
+ * with FCFS admission, max-memory-ratio admission (P:460,
+ * P:477) and preemption by moving KV to host or recomputing it;
+ * a block-granular PagedAttention allocator; a per-operator
+ * roofline compute simulator that advances an
+ * integer-nanosecond clock; and emits per-request TTFT / TPOT / E2E /
+ * normalized / mTPOT latencies and KV memory over
+ * time.  The exact semantics are SURVEY.md §8(c) under the
+ * readings listed in DESIGN.md; results are bit-identical to oracle/.
+ *
+ * Execution: every step runs in sm_100a CUDA kernels (workload generation,
+ * one persistent warp per point, quantile/summary kernels).  The host side of
+ * this library only validates inputs, derives per-profile constants, lays out
+ * the workspace and launches.  There is no CPU fallback: without a CUDA device
+ * tokensim_sweep_run returns TOKENSIM_E_CUDA.
+ *
+ * Conventions
+ *  - Every call returns a tokensim_status; nothing throws across the ABI.
+ *    On failure the message is available from tokensim_last_error().
+ *  - Every input struct starts with struct_size = sizeof(struct); a mismatch
+ *    is TOKENSIM_E_INVALID (ABI versioning; "unknown keys are errors").
+ *  - Pointers are HOST pointers unless the name starts with d_ (DEVICE).
+ *  - Ownership: create deep-copies every input (arrays included); the caller
+ *    may free its inputs when create returns.  The handle owns its device
+ *    tables.  The run workspace is caller-owned device memory (or, if NULL is
+ *    passed, handle-owned); it holds the per-point results and must stay alive
+ *    until the next run or destroy.  Getters copy into caller buffers; the
+ *    two-call pattern applies (out = NULL or capacity = 0 returns *n_out);
+ *    a too-small buffer returns TOKENSIM_E_TRUNCATED with *n_out = required.
+ *  - A handle is used by one host thread at a time; handles are independent.
+ *  - Results do not depend on device, begin/end/stride or the number of GPUs.
+ */
+#ifndef TOKENSIM_H
+#define TOKENSIM_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status ------------------------------------------------------------ */
+typedef enum {
+  TOKENSIM_OK = 0,
+  TOKENSIM_E_INVALID = -1,   /* validation failed; message names the field path     */
+  TOKENSIM_E_NOMEM = -2,     /* host/device allocation failed or workspace too small */
+  TOKENSIM_E_CUDA = -3,      /* CUDA error (message carries cudaGetErrorString)      */
+  TOKENSIM_E_STATE = -4,     /* call out of order (getter before run, point not run) */
+  TOKENSIM_E_RANGE = -5,     /* point / metric / quantile / worker out of range      */
+  TOKENSIM_E_TRUNCATED = -6, /* caller buffer too small; *n_out = required count     */
+  TOKENSIM_E_OVERFLOW = -7   /* the point's memory trace overflowed its cap          */
+} tokensim_status;
+
+/* ---- enums --------------------------------------------------------------- */
+enum { TOKENSIM_STATIC = 0, TOKENSIM_CONT = 1, TOKENSIM_CONT_RATIO = 2 };   /* policy.kind   */
+enum { TOKENSIM_SWAP = 0, TOKENSIM_RECOMPUTE = 1 };                         /* policy.preempt*/
+enum { TOKENSIM_LEN_SHAREGPT_SYNTH_V1 = 0, TOKENSIM_LEN_FIXED = 1, TOKENSIM_LEN_UNIFORM = 2,
+       TOKENSIM_LEN_TABLE = 3, TOKENSIM_LEN_TRACE = 4 };                      /* len_dist      */
+enum { TOKENSIM_TRACE_NONE = 0, TOKENSIM_TRACE_BINNED = 1, TOKENSIM_TRACE_FULL = 2 };
+enum { TOKENSIM_UNIFIED = 0, TOKENSIM_PD_PAIR = 1 };                        /* topology      */
+enum { TOKENSIM_TTFT = 0, TOKENSIM_TPOT = 1, TOKENSIM_E2E = 2, TOKENSIM_NORM = 3,
+       TOKENSIM_MTPOT = 4 };                                                /* metric        */
+enum { TOKENSIM_REQ_UNFINISHED = 0, TOKENSIM_REQ_FINISHED = 1, TOKENSIM_REQ_REJECTED = 2 };
+enum { TOKENSIM_PT_TRACE_OVERFLOW = 1, TOKENSIM_PT_ALL_REJECTED = 2, TOKENSIM_PT_HORIZON_HIT = 4,
+       TOKENSIM_PT_INTERNAL_ERROR = 16 };                                   /* status_flags  */
+
+/* ---- inputs -------------------------------------------------------------- */
+/* Transformer shape.  q = num_heads*head_dim, g = num_kv_heads*head_dim.
+ * Weight bytes W and KV bytes per token kvb = 2*L*g*dtype_bytes are derived (SURVEY c.1). */
+typedef struct {
+  uint32_t struct_size;
+  uint32_t num_layers, hidden, num_heads, num_kv_heads, head_dim, ffn_dim, vocab;
+  uint32_t dtype_bytes;      /* 2 (fp16)                  */
+  uint32_t gated_mlp;        /* 1: up+gate (LLaMA)               */
+  uint32_t tied_embeddings;  /* 0                                */
+  uint32_t max_model_len;    /* 2048; <= 1<<20                   */
+} tokensim_model;
+
+/* Roofline hardware profile.  For tensor parallelism give
+ * the AGGREGATE profile (t*F, t*B, t*C) plus tp_degree/tp_link_bw (reading A22). */
+typedef struct {
+  uint32_t struct_size;
+  double peak_flops;          /* FLOP/s, > 0                            */
+  double mem_bw;              /* B/s, > 0                               */
+  double eff_flops, eff_bw;   /* derating in (0,1] (0.6 / 0.8)   */
+  uint64_t mem_capacity;      /* bytes (decimal)                        */
+  double reserve_frac;        /* 0.05                           */
+  double iter_overhead_s;     /* 200e-6                         */
+  double host_link_bw;        /* B/s, swap link (32e9)           */
+  uint32_t tp_degree;         /* 1                                      */
+  double tp_link_bw;          /* B/s per direction, > 0 if tp_degree>1  */
+  uint64_t kv_blocks_override;/* 0 = derive from capacity (tests only)  */
+} tokensim_hw;
+
+/* Local scheduler + memory policy. */
+typedef struct {
+  uint32_t struct_size;
+  uint32_t kind;              /* TOKENSIM_STATIC | CONT | CONT_RATIO          */
+  uint32_t preempt;           /* TOKENSIM_SWAP | RECOMPUTE                    */
+  double max_mem_ratio;       /* CONT_RATIO: (0,1]                    */
+  uint32_t max_num_seqs;      /* 256, in [1, 1024]                            */
+  uint32_t max_batched_tokens;/* UINT32_MAX = off; else >= max_model_len      */
+  uint32_t block_size;        /* 16 tokens                            */
+  uint32_t watermark_blocks;  /* 0                                            */
+} tokensim_policy;
+
+/* Bucketed length table: bucket b covers [lo[b], hi[b]); cdf32 holds n_buckets-1 u32
+ * thresholds (draw x < cdf32[b]); the last bucket takes the rest. */
+typedef struct {
+  uint32_t n_buckets;
+  const uint32_t *lo, *hi, *cdf32;
+} tokensim_len_table;
+
+/* Workload.  rates x seeds are grid axes. */
+typedef struct {
+  uint32_t struct_size;
+  uint32_t num_requests;                /* >= 1 per point                         */
+  uint32_t num_rates;
+  const double *rates;                  /* req/s, > 0                             */
+  uint32_t num_seeds;
+  const uint64_t *seeds;
+  uint32_t len_dist;                    /* TOKENSIM_LEN_*                         */
+  uint32_t prompt_a, prompt_b, output_a, output_b;   /* FIXED: a; UNIFORM: [a,b]  */
+  const tokensim_len_table *prompt_table, *output_table;  /* TABLE                */
+  const int64_t *trace_arrival_ns;      /* TRACE: non-decreasing, >= 0            */
+  const uint32_t *trace_prompt, *trace_output;
+} tokensim_workload;
+
+typedef struct {
+  uint32_t struct_size;
+  uint32_t topology;          /* TOKENSIM_UNIFIED | PD_PAIR                          */
+  double pd_link_bw;          /* B/s, P->D KV link (200e9)                    */
+  uint32_t trace_mode;        /* TOKENSIM_TRACE_NONE | BINNED | FULL                 */
+  uint64_t trace_bin_ns;      /* BINNED bin width (1e9)                              */
+  uint64_t trace_cap_bytes;   /* per point per worker; samples are 32 B              */
+  uint32_t iteration_trace_cap;  /* per point; 0 = off (debug / parity)              */
+  double slo_ttft_s;          /* 15                                          */
+  double slo_mtpot_s;         /* 0.3                                         */
+  int64_t horizon_ns;         /* -1 = run to completion                              */
+} tokensim_options;
+
+/* ---- results ------------------------------------------------------------- */
+typedef struct {               /* 32 B; index = request id                         */
+  int64_t ttft_ns;             /* first token - arrival (0 if no token yet)        */
+  int64_t e2e_ns;              /* finish - arrival (FINISHED only)                 */
+  int64_t mtpot_ns;            /* max inter-token gap excluding TTFT (A26)         */
+  uint16_t n_preempt;
+  uint8_t status;              /* TOKENSIM_REQ_*                                   */
+  uint8_t pad;
+  uint32_t finish_iter;        /* iteration index k of the finishing iteration     */
+} tokensim_request_record;
+
+typedef struct {               /* 32 B                                             */
+  int64_t t_ns;                /* FULL: iteration start; BINNED: bin start         */
+  int64_t dur_ns;              /* FULL: iteration time T_ns; BINNED: bin width      */
+  uint64_t block_ns;           /* integral of blocks-in-use over the sample        */
+  uint32_t blocks_max;         /* max blocks in use over the sample                */
+  uint32_t n_iter;             /* iterations starting inside the sample            */
+} tokensim_mem_sample;
+
+typedef struct {               /* 80 B, debug / parity                             */
+  uint64_t k;
+  int64_t t_start_ns, T_ns;
+  uint32_t n_prefill, n_decode;
+  uint64_t N_p, C_d;
+  uint32_t n_preempted, n_resumed, n_admitted, n_rejected, n_finished, blocks_in_use;
+  uint32_t worker, pad;
+} tokensim_iter_record;
+
+typedef struct {               /* 384 B, little-endian; the all-gather payload */
+  uint32_t version, status_flags;                                   /*   0 */
+  uint64_t point;                                                   /*   8 */
+  uint64_t n_requests, n_finished, n_rejected, n_unfinished;        /*  16 */
+  uint64_t n_iterations, n_request_iterations, n_preemptions;       /*  48 */
+  uint64_t swap_out_bytes, swap_in_bytes;                           /*  72 */
+  int64_t first_arrival_ns, last_finish_ns;                         /*  88 */
+  uint64_t sched_digest, block_digest, request_digest;              /* 104 */
+  uint32_t total_blocks, peak_blocks;                               /* 128 */
+  double mean_util;                                                 /* 136 */
+  double stat[5][5];  /* [TTFT,TPOT,E2E,NORM,MTPOT][P50,P90,P99,max,mean] s;  144 */
+  double throughput_rps, goodput_mtpot_rps, goodput_both_rps;       /* 344 */
+  int64_t t_final_ns;                                               /* 368 */
+  uint64_t block_ns_sum;                                            /* 376 */
+} tokensim_summary;
+
+typedef struct tokensim_sweep tokensim_sweep;   /* opaque handle */
+
+/* ---- lifecycle ----------------------------------------------------------- */
+/* Validate, derive per-profile constants (SURVEY c.1) and upload the tables.
+ * n_hw profiles x n_pol policies x rates x seeds points (PD_PAIR: n_hw^2 pairs).
+ * Errors: E_INVALID (message names the field, e.g.
+ * "hw[3].mem_capacity: 20000000000 < weights 13476831232 + reserve ..."), E_NOMEM, E_CUDA.
+ * On failure *out = NULL and nothing is leaked. */
+tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensim_hw *hw, uint32_t n_hw,
+                                      const tokensim_policy *pol, uint32_t n_pol,
+                                      const tokensim_workload *workload, const tokensim_options *options,
+                                      tokensim_sweep **out);
+/* point = ((hw*n_pol + pol)*n_rates + rate)*n_seeds + seed (row-major grid). */
+uint64_t tokensim_sweep_num_points(const tokensim_sweep *h);
+/* Device bytes needed to run points begin, begin+stride, ... < end. */
+tokensim_status tokensim_sweep_workspace_size(const tokensim_sweep *h, uint64_t begin, uint64_t end,
+                                              uint64_t stride, size_t *bytes);
+/* Enqueue the whole sweep on cuda_stream (a cudaStream_t; NULL = legacy default stream) on
+ * `device`: workload generation -> persistent simulation kernel -> quantile/summary kernel.
+ * d_workspace: >= workspace_size bytes of device memory, 256-B aligned, or NULL for a
+ * handle-owned allocation.  Asynchronous: results are valid after the stream completes
+ * (getters synchronize).  Errors: E_RANGE (bad range), E_NOMEM (workspace too small), E_CUDA. */
+tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin, uint64_t end,
+                                   uint64_t stride, void *d_workspace, size_t ws_bytes,
+                                   void *cuda_stream);
+/* Number of points run by the last tokensim_sweep_run. */
+uint64_t tokensim_sweep_num_run(const tokensim_sweep *h);
+
+/* ---- results ------------------------------------------------------------- */
+/* Exact nearest-rank quantiles (rank = max(1, ceil(q_bp*n/10^4))) of
+ * `metric` over the point's finished requests, in seconds (0 if no sample).  q_bp in
+ * [0, 10000].  Computed by a GPU select kernel over the point's records.  For points this
+ * process did not run, only q_bp in {5000, 9000, 9900, 10000} are served, from summaries
+ * imported with tokensim_import_summaries; anything else is E_STATE. */
+tokensim_status tokensim_get_latency_quantiles(const tokensim_sweep *h, uint64_t point, uint32_t metric,
+                                               const uint32_t *q_bp, uint32_t n_q, double *out_seconds);
+/* KV memory over time of one worker (0 = unified / prefill, 1 = decode in
+ * PD_PAIR).  Returns E_OVERFLOW (with the samples that fit) if the trace hit its cap. */
+tokensim_status tokensim_get_mem_trace(const tokensim_sweep *h, uint64_t point, uint32_t worker,
+                                       tokensim_mem_sample *out, uint64_t capacity, uint64_t *n_out);
+tokensim_status tokensim_get_summary(const tokensim_sweep *h, uint64_t point, tokensim_summary *out);
+/* All summaries of the last run, in run order (point begin, begin+stride, ...). */
+tokensim_status tokensim_get_summaries(const tokensim_sweep *h, tokensim_summary *out, uint64_t capacity,
+                                       uint64_t *n_out);
+/* Device pointer to the last run's summaries (n_run x 384 B) for an all-gather. */
+tokensim_status tokensim_get_summaries_device(const tokensim_sweep *h, const void **d_ptr, size_t *bytes);
+/* Install summaries of points run elsewhere (after the all-gather); each record carries
+ * its point index.  bytes must be a multiple of 384. */
+tokensim_status tokensim_import_summaries(tokensim_sweep *h, const void *host_ptr, size_t bytes);
+tokensim_status tokensim_get_request_records(const tokensim_sweep *h, uint64_t point,
+                                             tokensim_request_record *out, uint64_t capacity, uint64_t *n_out);
+/* Per-iteration schedule trace (debug/parity; needs options.iteration_trace_cap > 0). */
+tokensim_status tokensim_get_iteration_trace(const tokensim_sweep *h, uint64_t point,
+                                             tokensim_iter_record *out, uint64_t capacity, uint64_t *n_out);
+/* Per-point workload the kernels generated (group of the point's rate and seed). */
+tokensim_status tokensim_get_workload(const tokensim_sweep *h, uint64_t point, int64_t *arrival_ns,
+                                      uint32_t *prompt, uint32_t *output, uint64_t capacity);
+
+/* Launch facts of the last run: per-kernel device times from CUDA events recorded on the
+ * run's stream (valid once the stream has completed; this call synchronizes), the launch
+ * geometry of the simulation kernel, and the host->device bytes the run copied. */
+typedef struct {
+  double ms_workload, ms_sim, ms_summary;   /* kernel durations, milliseconds          */
+  uint32_t n_launches;                      /* kernels this library launched in the run */
+  uint32_t sim_blocks, sim_warps_per_block; /* persistent grid                          */
+  uint32_t smem_per_warp;                   /* bytes of shared memory per point/warp    */
+  uint64_t n_run;                           /* points run                               */
+  uint64_t h2d_bytes;                       /* tables (first run on a device) + order   */
+  uint64_t workspace_bytes;
+} tokensim_run_info;
+tokensim_status tokensim_get_run_info(const tokensim_sweep *h, tokensim_run_info *out);
+
+/* Message of the last failing call on h (NULL: the calling thread's last create error). */
+const char *tokensim_last_error(const tokensim_sweep *h);
+void tokensim_sweep_destroy(tokensim_sweep *h);
+
+/* Library/kernel version string, e.g. "tokensim-b200 1 sm_100a". */
+const char *tokensim_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOKENSIM_H */

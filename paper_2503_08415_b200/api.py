@@ -1,0 +1,282 @@
+"""Python API of the B200 sweep -- thin marshalling over the C ABI (include/tokensim.h).
+
+    from paper_2503_08415_b200 import Sweep
+    import sweep_inputs as si
+    sw = Sweep(si.c2())
+    sw.run()                         # all points on the current CUDA device / stream
+    s = sw.summaries()               # numpy structured array, one 384-B record per point
+
+PyTorch provides device memory (the run workspace is a torch uint8 tensor), the
+stream (torch.cuda.current_stream()) and, in ``run_distributed``, the process
+group.  Every step of the sweep runs in the library's CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+import sweep_inputs as si
+
+from . import _lib as T
+
+
+class TokensimError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{T.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_KIND = {si.STATIC: T.STATIC, si.CONT: T.CONT, si.CONT_RATIO: T.CONT_RATIO}
+_PRE = {si.SWAP: T.SWAP, si.RECOMPUTE: T.RECOMPUTE}
+_LEN = {si.FIXED: T.LEN_FIXED, si.UNIFORM: T.LEN_UNIFORM, si.TABLE: T.LEN_TABLE, si.TRACE: T.LEN_TRACE,
+        "sharegpt_synth_v1": T.LEN_SHAREGPT_SYNTH_V1}
+_TRC = {si.NONE_TRACE: T.TRACE_NONE, si.BINNED: T.TRACE_BINNED, si.FULL: T.TRACE_FULL}
+_TOP = {si.UNIFIED: T.UNIFIED, si.PD_PAIR: T.PD_PAIR}
+METRICS = {"ttft": T.TTFT, "tpot": T.TPOT, "e2e": T.E2E, "norm": T.NORM, "mtpot": T.MTPOT}
+
+
+def _arr(values, dtype, ctype):
+    a = np.ascontiguousarray(np.asarray(values, dtype=dtype))
+    return a, a.ctypes.data_as(C.POINTER(ctype))
+
+
+def marshal(cfg: si.SweepConfig):
+    """SweepConfig -> ctypes structs (+ keepalive list)."""
+    keep = []
+    m = cfg.model
+    cm = T.Model(C.sizeof(T.Model), m.num_layers, m.hidden, m.num_heads, m.num_kv_heads, m.head_dim,
+                 m.ffn_dim, m.vocab, m.dtype_bytes, m.gated_mlp, m.tied_embeddings, m.max_model_len)
+    hws = (T.Hw * len(cfg.hws))()
+    for i, h in enumerate(cfg.hws):
+        hws[i] = T.Hw(C.sizeof(T.Hw), h.peak_flops, h.mem_bw, h.eff_flops, h.eff_bw, h.mem_capacity,
+                      h.reserve_frac, h.iter_overhead_s, h.host_link_bw, h.tp_degree, h.tp_link_bw,
+                      h.kv_blocks_override)
+    pols = (T.Policy * len(cfg.policies))()
+    for i, p in enumerate(cfg.policies):
+        pols[i] = T.Policy(C.sizeof(T.Policy), _KIND[p.kind], _PRE[p.preempt], p.max_mem_ratio,
+                           p.max_num_seqs, p.max_batched_tokens, p.block_size, p.watermark_blocks)
+    w = cfg.workload
+    rates, prates = _arr(w.rates, np.float64, C.c_double)
+    seeds, pseeds = _arr(w.seeds, np.uint64, C.c_uint64)
+    keep += [rates, seeds, hws, pols]
+    cw = T.Workload()
+    cw.struct_size = C.sizeof(T.Workload)
+    cw.num_requests = w.num_requests
+    cw.num_rates, cw.rates = len(w.rates), prates
+    cw.num_seeds, cw.seeds = len(w.seeds), pseeds
+    cw.len_dist = _LEN[w.len_dist]
+    cw.prompt_a, cw.prompt_b, cw.output_a, cw.output_b = w.prompt_a, w.prompt_b, w.output_a, w.output_b
+    if w.len_dist == si.TABLE:
+        tabs = []
+        for t in (w.prompt_table, w.output_table):
+            lo, plo = _arr(t.lo, np.uint32, C.c_uint32)
+            hi, phi = _arr(t.hi, np.uint32, C.c_uint32)
+            th, pth = _arr(list(t.thr) + [0], np.uint32, C.c_uint32)
+            lt = T.LenTable(len(t.lo), plo, phi, pth)
+            keep += [lo, hi, th, lt]
+            tabs.append(lt)
+        cw.prompt_table = C.pointer(tabs[0])
+        cw.output_table = C.pointer(tabs[1])
+    if w.len_dist == si.TRACE:
+        ta, pta = _arr(w.trace_arrival_ns, np.int64, C.c_int64)
+        tp, ptp = _arr(w.trace_prompt, np.uint32, C.c_uint32)
+        to, pto = _arr(w.trace_output, np.uint32, C.c_uint32)
+        keep += [ta, tp, to]
+        cw.trace_arrival_ns, cw.trace_prompt, cw.trace_output = pta, ptp, pto
+    o = cfg.options
+    co = T.Options(C.sizeof(T.Options), _TOP[o.topology], o.pd_link_bw, _TRC[o.trace_mode], o.trace_bin_ns,
+                   o.trace_cap_bytes, o.iteration_trace_cap, o.slo_ttft_s, o.slo_mtpot_s, o.horizon_ns)
+    return cm, hws, pols, cw, co, keep
+
+
+class Sweep:
+    """One sweep handle (tokensim_sweep)."""
+
+    def __init__(self, cfg: si.SweepConfig):
+        self.cfg = cfg
+        self._L = T.lib()
+        cm, hws, pols, cw, co, keep = marshal(cfg)
+        h = C.c_void_p()
+        st = self._L.tokensim_sweep_create(C.byref(cm), hws, len(cfg.hws), pols, len(cfg.policies),
+                                           C.byref(cw), C.byref(co), C.byref(h))
+        if st != T.OK:
+            raise TokensimError(st, self._L.tokensim_last_error(None).decode())
+        self._h = h
+        self._ws = None
+        self._n_req = cfg.workload.num_requests
+
+    # ------------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.tokensim_sweep_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int, what: str):
+        if st != T.OK:
+            raise TokensimError(st, f"{what}: {self._L.tokensim_last_error(self._h).decode()}")
+
+    @property
+    def num_points(self) -> int:
+        return int(self._L.tokensim_sweep_num_points(self._h))
+
+    def workspace_size(self, begin: int = 0, end: Optional[int] = None, stride: int = 1) -> int:
+        end = self.num_points if end is None else end
+        b = C.c_size_t()
+        self._check(self._L.tokensim_sweep_workspace_size(self._h, begin, end, stride, C.byref(b)), "workspace_size")
+        return b.value
+
+    def run(self, begin: int = 0, end: Optional[int] = None, stride: int = 1, device=None, stream=None,
+            workspace=None):
+        """Enqueue the sweep of points begin, begin+stride, ... < end on a CUDA stream.
+
+        The workspace is a torch uint8 CUDA tensor (allocated here if not given) and
+        stays referenced by this object until the next run."""
+        import torch
+        end = self.num_points if end is None else end
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        need = self.workspace_size(begin, end, stride)
+        if workspace is None:
+            if self._ws is None or self._ws.numel() < need or self._ws.device != dev:
+                self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+            workspace = self._ws
+        else:
+            self._ws = workspace
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        st = self._L.tokensim_sweep_run(self._h, dev.index, begin, end, stride, C.c_void_p(workspace.data_ptr()),
+                                        workspace.numel(), C.c_void_p(sptr))
+        self._check(st, "run")
+        return self
+
+    # ------------------------------------------------------------------ results
+    @property
+    def num_run(self) -> int:
+        return int(self._L.tokensim_sweep_num_run(self._h))
+
+    def summaries(self) -> np.ndarray:
+        n = C.c_uint64()
+        self._check(self._L.tokensim_get_summaries(self._h, None, 0, C.byref(n)), "get_summaries")
+        out = np.zeros(n.value, T.SUMMARY_DTYPE)
+        if n.value:
+            self._check(self._L.tokensim_get_summaries(self._h, out.ctypes.data, n.value, C.byref(n)),
+                        "get_summaries")
+        return out
+
+    def summary(self, point: int) -> np.void:
+        out = np.zeros(1, T.SUMMARY_DTYPE)
+        self._check(self._L.tokensim_get_summary(self._h, point, out.ctypes.data), "get_summary")
+        return out[0]
+
+    def summaries_device(self):
+        """torch uint8 view of the last run's summaries in device memory (for all-gather)."""
+        p = C.c_void_p()
+        b = C.c_size_t()
+        self._check(self._L.tokensim_get_summaries_device(self._h, C.byref(p), C.byref(b)), "get_summaries_device")
+        off = p.value - self._ws.data_ptr()
+        return self._ws[off:off + b.value]
+
+    def import_summaries(self, arr: np.ndarray):
+        arr = np.ascontiguousarray(arr, dtype=T.SUMMARY_DTYPE)
+        self._check(self._L.tokensim_import_summaries(self._h, arr.ctypes.data, arr.nbytes), "import_summaries")
+
+    def records(self, point: int) -> np.ndarray:
+        out = np.zeros(self._n_req, T.RECORD_DTYPE)
+        n = C.c_uint64()
+        self._check(self._L.tokensim_get_request_records(self._h, point, out.ctypes.data, len(out), C.byref(n)),
+                    "get_request_records")
+        return out
+
+    def mem_trace(self, point: int, worker: int = 0, allow_overflow: bool = True) -> np.ndarray:
+        n = C.c_uint64()
+        self._check(self._L.tokensim_get_mem_trace(self._h, point, worker, None, 0, C.byref(n)), "get_mem_trace")
+        out = np.zeros(n.value, T.SAMPLE_DTYPE)
+        if n.value:
+            st = self._L.tokensim_get_mem_trace(self._h, point, worker, out.ctypes.data, n.value, C.byref(n))
+            if not (st == T.OK or (allow_overflow and st == T.E_OVERFLOW)):
+                self._check(st, "get_mem_trace")
+        return out
+
+    def iteration_trace(self, point: int) -> np.ndarray:
+        n = C.c_uint64()
+        self._check(self._L.tokensim_get_iteration_trace(self._h, point, None, 0, C.byref(n)), "get_iteration_trace")
+        out = np.zeros(n.value, T.ITER_DTYPE)
+        if n.value:
+            self._check(self._L.tokensim_get_iteration_trace(self._h, point, out.ctypes.data, n.value, C.byref(n)),
+                        "get_iteration_trace")
+        return out
+
+    def latency_quantiles(self, point: int, metric, q_bp: Sequence[int]) -> np.ndarray:
+        metric = METRICS[metric] if isinstance(metric, str) else int(metric)
+        q, pq = _arr(q_bp, np.uint32, C.c_uint32)
+        out = np.zeros(len(q), np.float64)
+        self._check(self._L.tokensim_get_latency_quantiles(self._h, point, metric, pq, len(q),
+                                                           out.ctypes.data_as(C.POINTER(C.c_double))),
+                    "get_latency_quantiles")
+        return out
+
+    def run_info(self) -> dict:
+        ri = T.RunInfo()
+        self._check(self._L.tokensim_get_run_info(self._h, C.byref(ri)), "get_run_info")
+        return {n: getattr(ri, n) for n, _ in T.RunInfo._fields_}
+
+    def workload(self, point: int):
+        n = self._n_req
+        a = np.zeros(n, np.int64)
+        p = np.zeros(n, np.uint32)
+        o = np.zeros(n, np.uint32)
+        self._check(self._L.tokensim_get_workload(self._h, point, a.ctypes.data_as(C.POINTER(C.c_int64)),
+                                                  p.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                  o.ctypes.data_as(C.POINTER(C.c_uint32)), n), "get_workload")
+        return a, p, o
+
+
+def version() -> str:
+    return T.lib().tokensim_version().decode()
+
+
+def sweep(cfg: si.SweepConfig, device=None) -> np.ndarray:
+    """End-to-end convenience: create, run every point on one GPU, return host summaries."""
+    sw = Sweep(cfg)
+    try:
+        sw.run(device=device)
+        return sw.summaries()
+    finally:
+        sw.close()
+
+
+def shard_range(num_points: int, rank: int, world: int):
+    """Points owned by `rank`: p = rank (mod world)."""
+    return rank, num_points, world
+
+
+def run_distributed(cfg: si.SweepConfig, group=None):
+    """One process per GPU: rank r runs points r, r+W, ...; the 384-B summaries of all
+    points are then all-gathered (the only collective; NCCL over NVLink on GPUs) and
+    imported so every rank can answer summary queries for every point.
+
+    Returns (sweep handle, all summaries sorted by point)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    sw = Sweep(cfg)
+    b, e, s = shard_range(sw.num_points, rank, world)
+    sw.run(b, e, s)
+    per = -(-sw.num_points // world)  # max points per rank
+    local = sw.summaries_device()
+    buf = torch.zeros(per * T.SUMMARY_DTYPE.itemsize, dtype=torch.uint8, device=local.device)
+    buf[:local.numel()] = local
+    out = torch.empty(world * buf.numel(), dtype=torch.uint8, device=local.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    allv = out.cpu().numpy().view(T.SUMMARY_DTYPE)
+    allv = allv[allv["version"] != 0]
+    sw.import_summaries(allv)
+    return sw, np.sort(allv, order="point")

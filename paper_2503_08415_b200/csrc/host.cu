@@ -1,0 +1,833 @@
+// host.cu -- the C ABI (include/tokensim.h): validation, derived constants (SURVEY c.1),
+// device tables, workspace layout, launch sequence and result getters.
+//
+// The host only marshals: every step of the sweep (a.1-a.8) runs in the kernels of
+// sweep.cu.  Derived per-profile constants are computed here once per create (they are
+// inputs of the simulation, like the profile itself), in the fp64 order of SURVEY c.1.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ts_internal.cuh"
+
+using namespace ts;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+// SHAREGPT_SYNTH_V1 (reading A25): bucket bounds and u32 thresholds.
+const uint32_t kPromptLo[7] = {4, 16, 32, 64, 128, 256, 512};
+const uint32_t kPromptHi[7] = {16, 32, 64, 128, 256, 512, 1024};
+const uint32_t kPromptThr[6] = {644245094u, 1309965025u, 2040109466u, 2770253906u, 3457448673u, 3994319585u};
+const uint32_t kOutputLo[8] = {4, 16, 32, 64, 128, 256, 512, 1024};
+const uint32_t kOutputHi[8] = {16, 32, 64, 128, 256, 512, 1024, 2048};
+const uint32_t kOutputThr[7] = {429496730u, 773094113u, 1159641170u, 1717986918u, 2448131359u, 3307124818u,
+                                4101693768u};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, total;
+  u64 n_run;
+  u32 warps_total, wpb, blocks;
+  size_t smem;
+};
+
+}  // namespace
+
+struct tokensim_sweep {
+  tokensim_model model{};
+  std::vector<tokensim_hw> hw;
+  std::vector<tokensim_policy> pol;
+  std::vector<double> rates;
+  std::vector<uint64_t> seeds;
+  tokensim_workload wl{};
+  tokensim_options opt{};
+  std::vector<uint32_t> ptab, otab;  // n | lo | hi | thr
+  std::vector<int64_t> tr_a;
+  std::vector<uint32_t> tr_p, tr_o;
+  // derived
+  DevModel M{};
+  std::vector<DevHw> dhw;
+  std::vector<DevHP> dhp;
+  std::vector<DevPol> dpol;
+  std::vector<double> est_T1;  // per (hw,pol): rough per-iteration time for LPT ordering
+  u32 cap = 256, nwords_max = 1, bt_len = 1, n_hw_axis = 0;
+  u64 n_points = 0;
+  // device tables
+  int dev = -1;
+  char *d_tab = nullptr;
+  size_t off_hw = 0, off_hp = 0, off_pol = 0, off_rates = 0, off_seeds = 0, off_pt = 0, off_ot = 0,
+         off_tra = 0, off_trp = 0, off_tro = 0;
+  // last run
+  bool ran = false;
+  u64 begin = 0, end = 0, stride = 1, n_run = 0;
+  char *ws = nullptr;
+  size_t ws_bytes = 0;
+  char *owned_ws = nullptr;
+  size_t owned_bytes = 0;
+  cudaStream_t stream = nullptr;
+  SweepParams P{};
+  Layout lay{};
+  std::vector<tokensim_summary> imported;  // indexed by point; version 0 = absent
+  std::string err;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  u32 n_launches = 0;
+  u64 h2d_bytes = 0, table_bytes_pending = 0;
+};
+
+namespace {
+
+tokensim_status fail(tokensim_sweep *h, tokensim_status s, const std::string &m) {
+  if (h) h->err = m;
+  else g_create_err = m;
+  return s;
+}
+tokensim_status cuda_fail(tokensim_sweep *h, cudaError_t e, const char *what) {
+  return fail(h, TOKENSIM_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
+
+// ---- c.1 derived constants (host side of the product; independent of oracle/)
+u64 weight_bytes(const tokensim_model &m) {
+  const u64 L = m.num_layers, h = m.hidden, V = m.vocab, f = m.ffn_dim, s = m.dtype_bytes;
+  const u64 q = (u64)m.num_heads * m.head_dim, g = (u64)m.num_kv_heads * m.head_dim;
+  const u64 layer = h * (q + 2 * g) + q * h + (m.gated_mlp ? 3 : 2) * h * f;
+  return s * (L * layer + (m.tied_embeddings ? 1 : 2) * V * h + (2 * L + 1) * h);
+}
+
+std::string hwpath(u32 i, const char *f) { return "hw[" + std::to_string(i) + "]." + f; }
+
+}  // namespace
+
+extern "C" {
+
+const char *tokensim_version(void) { return "tokensim-b200 1 sm_100a"; }
+
+const char *tokensim_last_error(const tokensim_sweep *h) {
+  return h ? h->err.c_str() : g_create_err.c_str();
+}
+
+tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensim_hw *hw, uint32_t n_hw,
+                                      const tokensim_policy *pol, uint32_t n_pol,
+                                      const tokensim_workload *wl, const tokensim_options *opt,
+                                      tokensim_sweep **out) {
+  g_create_err.clear();
+  if (!out) return fail(nullptr, TOKENSIM_E_INVALID, "out: NULL");
+  *out = nullptr;
+  if (!model || !hw || !pol || !wl || !opt) return fail(nullptr, TOKENSIM_E_INVALID, "NULL input struct");
+  if (model->struct_size != sizeof(tokensim_model)) return fail(nullptr, TOKENSIM_E_INVALID, "model.struct_size mismatch");
+  if (wl->struct_size != sizeof(tokensim_workload)) return fail(nullptr, TOKENSIM_E_INVALID, "workload.struct_size mismatch");
+  if (opt->struct_size != sizeof(tokensim_options)) return fail(nullptr, TOKENSIM_E_INVALID, "options.struct_size mismatch");
+  if (n_hw == 0) return fail(nullptr, TOKENSIM_E_INVALID, "n_hw: must be >= 1");
+  if (n_pol == 0) return fail(nullptr, TOKENSIM_E_INVALID, "n_pol: must be >= 1");
+  for (u32 i = 0; i < n_hw; ++i)
+    if (hw[i].struct_size != sizeof(tokensim_hw)) return fail(nullptr, TOKENSIM_E_INVALID, hwpath(i, "struct_size") + " mismatch");
+  for (u32 i = 0; i < n_pol; ++i)
+    if (pol[i].struct_size != sizeof(tokensim_policy))
+      return fail(nullptr, TOKENSIM_E_INVALID, "policies[" + std::to_string(i) + "].struct_size mismatch");
+
+  const tokensim_model &m = *model;
+  if (!m.num_layers || !m.hidden || !m.num_heads || !m.num_kv_heads || !m.head_dim || !m.ffn_dim || !m.vocab ||
+      !m.dtype_bytes)
+    return fail(nullptr, TOKENSIM_E_INVALID, "model: every dimension must be >= 1");
+  if (m.max_model_len < 2 || m.max_model_len > (1u << 20))
+    return fail(nullptr, TOKENSIM_E_INVALID, "model.max_model_len: must be in [2, 2^20]");
+  if (opt->topology != TOKENSIM_UNIFIED)
+    return fail(nullptr, TOKENSIM_E_INVALID, "options.topology: PD_PAIR is not available in this build yet");
+  if (opt->trace_mode > TOKENSIM_TRACE_FULL) return fail(nullptr, TOKENSIM_E_INVALID, "options.trace_mode: unknown");
+  if (opt->trace_mode == TOKENSIM_TRACE_BINNED && opt->trace_bin_ns == 0)
+    return fail(nullptr, TOKENSIM_E_INVALID, "options.trace_bin_ns: must be > 0");
+  if (!(opt->slo_ttft_s >= 0) || !(opt->slo_mtpot_s >= 0))
+    return fail(nullptr, TOKENSIM_E_INVALID, "options.slo_*: must be >= 0");
+
+  const tokensim_workload &w = *wl;
+  if (w.num_requests == 0) return fail(nullptr, TOKENSIM_E_INVALID, "workload.num_requests: must be >= 1");
+  if (w.num_requests > (1u << 30)) return fail(nullptr, TOKENSIM_E_INVALID, "workload.num_requests: too large");
+  if (w.num_rates == 0 || !w.rates) return fail(nullptr, TOKENSIM_E_INVALID, "workload.rates: empty");
+  if (w.num_seeds == 0 || !w.seeds) return fail(nullptr, TOKENSIM_E_INVALID, "workload.seeds: empty");
+  for (u32 i = 0; i < w.num_rates; ++i)
+    if (!(w.rates[i] > 0) || !std::isfinite(w.rates[i]))
+      return fail(nullptr, TOKENSIM_E_INVALID, "workload.rates[" + std::to_string(i) + "]: must be > 0");
+
+  tokensim_sweep *h = new tokensim_sweep();
+  h->model = m;
+  h->hw.assign(hw, hw + n_hw);
+  h->pol.assign(pol, pol + n_pol);
+  h->rates.assign(w.rates, w.rates + w.num_rates);
+  h->seeds.assign(w.seeds, w.seeds + w.num_seeds);
+  h->wl = w;
+  h->opt = *opt;
+  const u32 mml = m.max_model_len;
+  auto bad = [&](const std::string &msg) {
+    delete h;
+    return fail(nullptr, TOKENSIM_E_INVALID, msg);
+  };
+
+  // ---- workload lengths
+  auto load_table = [&](const tokensim_len_table *t, const char *name, std::vector<u32> &dst, u32 max_hi,
+                        std::string &e) -> bool {
+    if (!t || t->n_buckets == 0 || !t->lo || !t->hi || (t->n_buckets > 1 && !t->cdf32)) {
+      e = std::string("workload.") + name + ": missing table";
+      return false;
+    }
+    dst.clear();
+    dst.push_back(t->n_buckets);
+    for (u32 b = 0; b < t->n_buckets; ++b) {
+      if (t->lo[b] < 1 || t->hi[b] <= t->lo[b] || t->hi[b] > max_hi + 1) {
+        e = std::string("workload.") + name + ".bucket[" + std::to_string(b) + "]: need 1 <= lo < hi <= " +
+            std::to_string(max_hi + 1);
+        return false;
+      }
+    }
+    for (u32 b = 0; b < t->n_buckets; ++b) dst.push_back(t->lo[b]);
+    for (u32 b = 0; b < t->n_buckets; ++b) dst.push_back(t->hi[b]);
+    for (u32 b = 0; b + 1 < t->n_buckets; ++b) {
+      if (b && t->cdf32[b] < t->cdf32[b - 1]) {
+        e = std::string("workload.") + name + ".cdf32: must be non-decreasing";
+        return false;
+      }
+      dst.push_back(t->cdf32[b]);
+    }
+    dst.push_back(0);
+    return true;
+  };
+  std::string e;
+  switch (w.len_dist) {
+    case TOKENSIM_LEN_SHAREGPT_SYNTH_V1: {
+      if (mml < 2048) return bad("workload.len_dist: SHAREGPT_SYNTH_V1 needs max_model_len >= 2048");
+      tokensim_len_table pt = {7, kPromptLo, kPromptHi, kPromptThr}, ot = {8, kOutputLo, kOutputHi, kOutputThr};
+      load_table(&pt, "prompt_table", h->ptab, mml - 1, e);
+      load_table(&ot, "output_table", h->otab, 1u << 30, e);
+      break;
+    }
+    case TOKENSIM_LEN_TABLE:
+      if (!load_table(w.prompt_table, "prompt_table", h->ptab, mml - 1, e)) return bad(e);
+      if (!load_table(w.output_table, "output_table", h->otab, 1u << 30, e)) return bad(e);
+      break;
+    case TOKENSIM_LEN_FIXED:
+      if (w.prompt_a < 1 || w.output_a < 1 || (u64)w.prompt_a + w.output_a > mml)
+        return bad("workload.prompt_a/output_a: need >= 1 and prompt + output <= max_model_len");
+      break;
+    case TOKENSIM_LEN_UNIFORM:
+      if (w.prompt_a < 1 || w.prompt_b < w.prompt_a || w.prompt_b > mml - 1 || w.output_a < 1 ||
+          w.output_b < w.output_a)
+        return bad("workload.prompt_[ab]/output_[ab]: need 1 <= a <= b, prompt_b < max_model_len");
+      break;
+    case TOKENSIM_LEN_TRACE: {
+      if (w.num_rates != 1 || w.num_seeds != 1)
+        return bad("workload: TRACE mode takes exactly one rate and one seed (they are unused)");
+      if (!w.trace_arrival_ns || !w.trace_prompt || !w.trace_output) return bad("workload.trace_*: NULL");
+      h->tr_a.assign(w.trace_arrival_ns, w.trace_arrival_ns + w.num_requests);
+      h->tr_p.assign(w.trace_prompt, w.trace_prompt + w.num_requests);
+      h->tr_o.assign(w.trace_output, w.trace_output + w.num_requests);
+      for (u32 i = 0; i < w.num_requests; ++i) {
+        if (h->tr_a[i] < 0 || (i && h->tr_a[i] < h->tr_a[i - 1]))
+          return bad("workload.trace_arrival_ns[" + std::to_string(i) + "]: must be >= 0 and non-decreasing");
+        if (h->tr_p[i] < 1 || h->tr_o[i] < 1 || (u64)h->tr_p[i] + h->tr_o[i] > mml)
+          return bad("workload.trace[" + std::to_string(i) + "]: need prompt, output >= 1 and sum <= max_model_len");
+      }
+      break;
+    }
+    default:
+      return bad("workload.len_dist: unknown");
+  }
+
+  // ---- model constants
+  DevModel &M = h->M;
+  M.L = m.num_layers;
+  M.h = m.hidden;
+  M.q = (u64)m.num_heads * m.head_dim;
+  M.g = (u64)m.num_kv_heads * m.head_dim;
+  M.f = m.ffn_dim;
+  M.fu = m.gated_mlp ? 2 * (u64)m.ffn_dim : (u64)m.ffn_dim;
+  M.V = m.vocab;
+  M.s = m.dtype_bytes;
+  M.q2g = M.q + 2 * M.g;
+  M.hq2g = M.h * M.q2g;
+  M.qh = M.q * M.h;
+  M.hfu = M.h * M.fu;
+  M.fh = M.f * M.h;
+  M.Vh = M.V * M.h;
+  M.att_tok = 2 * M.q + 2 * M.g;
+  M.g2 = 2 * M.g;
+  M.kvb = 2 * M.L * M.g * M.s;
+  M.mml = mml;
+  const u64 W = weight_bytes(m);
+
+  // ---- policies
+  u32 max_mns = 1, min_bs = 0xffffffffu;
+  bool any_swap = false;
+  for (u32 i = 0; i < n_pol; ++i) {
+    const tokensim_policy &p = pol[i];
+    const std::string pp = "policies[" + std::to_string(i) + "].";
+    if (p.kind > TOKENSIM_CONT_RATIO) return bad(pp + "kind: unknown");
+    if (p.preempt > TOKENSIM_RECOMPUTE) return bad(pp + "preempt: unknown");
+    if (p.kind == TOKENSIM_CONT_RATIO && !(p.max_mem_ratio > 0 && p.max_mem_ratio <= 1))
+      return bad(pp + "max_mem_ratio: must be in (0, 1]");
+    if (p.max_num_seqs < 1 || p.max_num_seqs > 1024) return bad(pp + "max_num_seqs: must be in [1, 1024]");
+    if (p.max_batched_tokens < mml) return bad(pp + "max_batched_tokens: must be >= max_model_len");
+    if (p.block_size < 1) return bad(pp + "block_size: must be >= 1");
+    max_mns = std::max(max_mns, p.max_num_seqs);
+    min_bs = std::min(min_bs, p.block_size);
+    any_swap |= p.preempt == TOKENSIM_SWAP;
+    DevPol d;
+    d.kind = p.kind;
+    d.preempt = p.preempt;
+    d.mns = p.max_num_seqs;
+    d.mbt = p.max_batched_tokens;
+    d.bs = p.block_size;
+    d.wm = p.watermark_blocks;
+    h->dpol.push_back(d);
+  }
+  h->cap = max_mns <= 32 ? 32 : (max_mns <= 256 ? 256 : 1024);
+  h->bt_len = (u32)ceil_div(mml, min_bs);
+
+  // ---- hardware profiles and (hw, pol) block accounting
+  u64 max_words = 1;
+  for (u32 i = 0; i < n_hw; ++i) {
+    const tokensim_hw &x = hw[i];
+    if (!(x.peak_flops > 0) || !(x.mem_bw > 0) || !std::isfinite(x.peak_flops) || !std::isfinite(x.mem_bw))
+      return bad(hwpath(i, "peak_flops/mem_bw") + ": must be finite and > 0");
+    if (!(x.eff_flops > 0 && x.eff_flops <= 1) || !(x.eff_bw > 0 && x.eff_bw <= 1))
+      return bad(hwpath(i, "eff_flops/eff_bw") + ": must be in (0, 1]");
+    if (!(x.reserve_frac >= 0 && x.reserve_frac < 1)) return bad(hwpath(i, "reserve_frac") + ": must be in [0, 1)");
+    if (!(x.iter_overhead_s >= 0)) return bad(hwpath(i, "iter_overhead_s") + ": must be >= 0");
+    if (x.tp_degree < 1) return bad(hwpath(i, "tp_degree") + ": must be >= 1");
+    if (x.tp_degree > 1 && !(x.tp_link_bw > 0)) return bad(hwpath(i, "tp_link_bw") + ": must be > 0 when tp_degree > 1");
+    if (any_swap && !(x.host_link_bw > 0)) return bad(hwpath(i, "host_link_bw") + ": must be > 0 with SWAP");
+    DevHw d;
+    d.invF = 1.0 / (x.peak_flops * x.eff_flops);
+    d.invB = 1.0 / (x.mem_bw * x.eff_bw);
+    d.invH = x.host_link_bw > 0 ? 1.0 / x.host_link_bw : 0.0;
+    d.invT = x.tp_degree > 1 ? 1.0 / ((double)x.tp_degree * x.tp_link_bw) : 0.0;
+    d.overhead = x.iter_overhead_s;
+    d.tp = x.tp_degree;
+    d.pad = 0;
+    h->dhw.push_back(d);
+    const u64 reserve = (u64)std::floor((double)x.mem_capacity * x.reserve_frac);
+    for (u32 j = 0; j < n_pol; ++j) {
+      const tokensim_policy &p = pol[j];
+      DevHP hp;
+      hp.block_bytes = (u64)p.block_size * M.kvb;
+      if (x.kv_blocks_override) {
+        hp.total_blocks = x.kv_blocks_override;
+      } else {
+        if (x.mem_capacity < W + reserve)
+          return bad(hwpath(i, "mem_capacity") + ": " + std::to_string(x.mem_capacity) + " < weights " +
+                     std::to_string(W) + " + reserve " + std::to_string(reserve));
+        hp.total_blocks = (x.mem_capacity - W - reserve) / hp.block_bytes;
+      }
+      const u64 min_blocks = ceil_div(mml, p.block_size);
+      if (hp.total_blocks < min_blocks)
+        return bad(hwpath(i, "mem_capacity") + ": " + std::to_string(hp.total_blocks) + " KV blocks of " +
+                   std::to_string(p.block_size) + " tokens cannot hold one max_model_len request (policies[" +
+                   std::to_string(j) + "])");
+      if (hp.total_blocks > (1ull << 21))
+        return bad(hwpath(i, "mem_capacity") + ": more than 2^21 KV blocks per worker is not supported");
+      if ((u64)p.watermark_blocks > hp.total_blocks - min_blocks)
+        return bad("policies[" + std::to_string(j) + "].watermark_blocks: must be <= total_blocks - ceil(max_model_len/block_size) = " +
+                   std::to_string(hp.total_blocks - min_blocks) + " on hw[" + std::to_string(i) + "]");
+      hp.ratio_limit = (u64)std::floor(p.max_mem_ratio * (double)hp.total_blocks);
+      hp.cap_fresh = p.kind == TOKENSIM_CONT_RATIO ? hp.ratio_limit : hp.total_blocks - p.watermark_blocks;
+      hp.nwords = (u32)ceil_div(hp.total_blocks, 32);
+      hp.pad = 0;
+      max_words = std::max<u64>(max_words, hp.nwords);
+      h->dhp.push_back(hp);
+      // LPT estimate: weights over bandwidth + overhead is the decode step floor
+      h->est_T1.push_back((double)W / (x.mem_bw * x.eff_bw) + x.iter_overhead_s);
+    }
+  }
+  h->nwords_max = (u32)((max_words + 31) & ~31ull);
+  h->n_hw_axis = n_hw;
+  h->n_points = (u64)n_hw * n_pol * w.num_rates * w.num_seeds;
+  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max);
+  if (per_warp > 227 * 1024) {
+    delete h;
+    return fail(nullptr, TOKENSIM_E_INVALID, "max_num_seqs x total_blocks needs more than 227 KB of shared memory per point");
+  }
+  *out = h;
+  return TOKENSIM_OK;
+}
+
+uint64_t tokensim_sweep_num_points(const tokensim_sweep *h) { return h ? h->n_points : 0; }
+uint64_t tokensim_sweep_num_run(const tokensim_sweep *h) { return h && h->ran ? h->n_run : 0; }
+
+static bool range_ok(const tokensim_sweep *h, u64 begin, u64 end, u64 stride) {
+  return stride >= 1 && begin <= end && end <= h->n_points;
+}
+static u64 count_run(u64 begin, u64 end, u64 stride) { return end > begin ? (end - begin + stride - 1) / stride : 0; }
+
+static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int blocks_per_sm_limit) {
+  Layout L{};
+  const u64 n = h->wl.num_requests;
+  const bool trace_mode = h->wl.len_dist == TOKENSIM_LEN_TRACE;
+  const u64 groups = trace_mode ? 1 : (u64)h->rates.size() * h->seeds.size();
+  L.n_run = n_run;
+  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max);
+  u32 wpb = (u32)std::max<size_t>(1, std::min<size_t>(4, (227 * 1024) / per_warp));
+  u32 bps = (u32)std::max<size_t>(1, (227 * 1024) / (per_warp * wpb));
+  bps = std::min<u32>(bps, 16);
+  if (blocks_per_sm_limit > 0) bps = std::min<u32>(bps, (u32)blocks_per_sm_limit);
+  const u64 need_warps = std::max<u64>(1, n_run);
+  u64 blocks = std::min<u64>((u64)sm_count * bps, ceil_div(need_warps, wpb));
+  L.wpb = wpb;
+  L.blocks = (u32)std::max<u64>(1, blocks);
+  L.warps_total = L.blocks * wpb;
+  L.smem = per_warp * wpb;
+  const u64 trace_cap = h->opt.trace_mode == TOKENSIM_TRACE_NONE ? 0 : h->opt.trace_cap_bytes / sizeof(tokensim_mem_sample);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align256(o + bytes);
+    return at;
+  };
+  L.arrival = take(trace_mode ? 0 : groups * n * 8);
+  L.prompt = take(trace_mode ? 0 : groups * n * 4);
+  L.output = take(trace_mode ? 0 : groups * n * 4);
+  L.rec = take(n_run * n * sizeof(tokensim_request_record));
+  L.stats = take(n_run * sizeof(SimStats));
+  L.trace = take(n_run * 2 * trace_cap * sizeof(tokensim_mem_sample));
+  L.itrec = take(n_run * (u64)h->opt.iteration_trace_cap * sizeof(tokensim_iter_record));
+  L.summ = take(n_run * sizeof(tokensim_summary));
+  L.bt = take((size_t)L.warps_total * 2 * h->cap * h->bt_len * 4);
+  L.order = take(n_run * 4 + 4);
+  L.queue = take(256);
+  L.scratch = take(n > kSummarySmemKeys ? n_run * n * 8 : 0);
+  L.total = o;
+  return L;
+}
+
+static int device_sms(int dev) {
+  int sms = 148;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) == cudaSuccess && count > 0) {
+    int d = dev >= 0 ? dev : 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) sms = 148;
+  } else {
+    cudaGetLastError();
+  }
+  return sms;
+}
+
+tokensim_status tokensim_sweep_workspace_size(const tokensim_sweep *h, uint64_t begin, uint64_t end,
+                                              uint64_t stride, size_t *bytes) {
+  if (!h || !bytes) return TOKENSIM_E_INVALID;
+  if (!range_ok(h, begin, end, stride)) return TOKENSIM_E_RANGE;
+  const Layout L = make_layout(h, count_run(begin, end, stride), device_sms(-1), 0);
+  *bytes = L.total;
+  return TOKENSIM_OK;
+}
+
+static tokensim_status upload_tables(tokensim_sweep *h, int dev) {
+  if (h->d_tab && h->dev == dev) return TOKENSIM_OK;
+  if (h->d_tab) {
+    cudaSetDevice(h->dev);
+    cudaFree(h->d_tab);
+    h->d_tab = nullptr;
+  }
+  cudaSetDevice(dev);
+  std::vector<char> blob;
+  auto put = [&](const void *p, size_t bytes) {
+    const size_t at = blob.size();
+    blob.resize(align256(at + bytes));
+    if (bytes) std::memcpy(blob.data() + at, p, bytes);
+    return at;
+  };
+  h->off_hw = put(h->dhw.data(), h->dhw.size() * sizeof(DevHw));
+  h->off_hp = put(h->dhp.data(), h->dhp.size() * sizeof(DevHP));
+  h->off_pol = put(h->dpol.data(), h->dpol.size() * sizeof(DevPol));
+  h->off_rates = put(h->rates.data(), h->rates.size() * sizeof(double));
+  h->off_seeds = put(h->seeds.data(), h->seeds.size() * sizeof(uint64_t));
+  h->off_pt = put(h->ptab.data(), h->ptab.size() * 4);
+  h->off_ot = put(h->otab.data(), h->otab.size() * 4);
+  h->off_tra = put(h->tr_a.data(), h->tr_a.size() * 8);
+  h->off_trp = put(h->tr_p.data(), h->tr_p.size() * 4);
+  h->off_tro = put(h->tr_o.data(), h->tr_o.size() * 4);
+  cudaError_t e = cudaMalloc(&h->d_tab, blob.size());
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMalloc(tables)");
+  e = cudaMemcpy(h->d_tab, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMemcpy(tables)");
+  h->table_bytes_pending = blob.size();
+  for (int i = 0; i < 4; ++i) {
+    if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+    h->ev[i] = nullptr;
+    e = cudaEventCreate(&h->ev[i]);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaEventCreate");
+  }
+  h->dev = dev;
+  return TOKENSIM_OK;
+}
+
+tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin, uint64_t end, uint64_t stride,
+                                   void *d_workspace, size_t ws_bytes, void *cuda_stream) {
+  if (!h) return TOKENSIM_E_INVALID;
+  if (!range_ok(h, begin, end, stride)) return fail(h, TOKENSIM_E_RANGE, "run: bad point range");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(h, TOKENSIM_E_CUDA, "run: no CUDA device (there is no CPU fallback)");
+  }
+  if (device < 0 || device >= count) return fail(h, TOKENSIM_E_RANGE, "run: bad device index");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaSetDevice");
+  tokensim_status s = upload_tables(h, device);
+  if (s != TOKENSIM_OK) return s;
+  const u64 n_run = count_run(begin, end, stride);
+  int sms = device_sms(device);
+  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max);
+  Layout L0 = make_layout(h, n_run, sms, 0);
+  int occ = 0;
+  e = sim_occupancy((int)h->cap, (int)L0.wpb, per_warp * L0.wpb, &occ);
+  if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
+  if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
+  const Layout L = make_layout(h, n_run, sms, occ);
+  char *ws = static_cast<char *>(d_workspace);
+  if (!ws) {
+    if (h->owned_bytes < L.total) {
+      if (h->owned_ws) cudaFree(h->owned_ws);
+      h->owned_ws = nullptr;
+      h->owned_bytes = 0;
+      e = cudaMalloc(&h->owned_ws, L.total);
+      if (e != cudaSuccess) return fail(h, TOKENSIM_E_NOMEM, std::string("cudaMalloc(workspace): ") + cudaGetErrorString(e));
+      h->owned_bytes = L.total;
+    }
+    ws = h->owned_ws;
+    ws_bytes = h->owned_bytes;
+  }
+  if (ws_bytes < L.total)
+    return fail(h, TOKENSIM_E_NOMEM, "run: workspace too small: " + std::to_string(ws_bytes) + " < " + std::to_string(L.total));
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+
+  SweepParams P{};
+  P.M = h->M;
+  P.hw = reinterpret_cast<const DevHw *>(h->d_tab + h->off_hw);
+  P.hp = reinterpret_cast<const DevHP *>(h->d_tab + h->off_hp);
+  P.pol = reinterpret_cast<const DevPol *>(h->d_tab + h->off_pol);
+  P.rates = reinterpret_cast<const double *>(h->d_tab + h->off_rates);
+  P.seeds = reinterpret_cast<const u64 *>(h->d_tab + h->off_seeds);
+  P.n_hw = h->n_hw_axis;
+  P.n_pol = (u32)h->pol.size();
+  P.n_rates = (u32)h->rates.size();
+  P.n_seeds = (u32)h->seeds.size();
+  P.topology = h->opt.topology;
+  P.n_req = h->wl.num_requests;
+  const bool trace_mode = h->wl.len_dist == TOKENSIM_LEN_TRACE;
+  P.len_dist = h->wl.len_dist == TOKENSIM_LEN_SHAREGPT_SYNTH_V1 ? (u32)TOKENSIM_LEN_TABLE : h->wl.len_dist;
+  P.n_groups = trace_mode ? 0 : P.n_rates * P.n_seeds;
+  P.prompt_a = h->wl.prompt_a;
+  P.prompt_b = h->wl.prompt_b;
+  P.output_a = h->wl.output_a;
+  P.output_b = h->wl.output_b;
+  P.pt = reinterpret_cast<const u32 *>(h->d_tab + h->off_pt);
+  P.ot = reinterpret_cast<const u32 *>(h->d_tab + h->off_ot);
+  if (trace_mode) {
+    P.arrival = reinterpret_cast<i64 *>(h->d_tab + h->off_tra);
+    P.prompt = reinterpret_cast<u32 *>(h->d_tab + h->off_trp);
+    P.output = reinterpret_cast<u32 *>(h->d_tab + h->off_tro);
+    P.group_of_point_mode = 1;
+  } else {
+    P.arrival = reinterpret_cast<i64 *>(ws + L.arrival);
+    P.prompt = reinterpret_cast<u32 *>(ws + L.prompt);
+    P.output = reinterpret_cast<u32 *>(ws + L.output);
+    P.group_of_point_mode = 0;
+  }
+  P.begin = begin;
+  P.stride = stride;
+  P.n_run = n_run;
+  P.order = reinterpret_cast<const u32 *>(ws + L.order);
+  P.queue = reinterpret_cast<u32 *>(ws + L.queue);
+  P.rec = reinterpret_cast<tokensim_request_record *>(ws + L.rec);
+  P.stats = reinterpret_cast<SimStats *>(ws + L.stats);
+  P.trace = reinterpret_cast<tokensim_mem_sample *>(ws + L.trace);
+  P.trace_cap = h->opt.trace_mode == TOKENSIM_TRACE_NONE ? 0 : h->opt.trace_cap_bytes / sizeof(tokensim_mem_sample);
+  P.itrec = reinterpret_cast<tokensim_iter_record *>(ws + L.itrec);
+  P.it_cap = h->opt.iteration_trace_cap;
+  P.summ = reinterpret_cast<tokensim_summary *>(ws + L.summ);
+  P.bt = reinterpret_cast<u32 *>(ws + L.bt);
+  P.bt_len = h->bt_len;
+  P.cap_slots = h->cap;
+  P.nwords_max = h->nwords_max;
+  P.n_warps_total = L.warps_total;
+  P.trace_mode = h->opt.trace_mode;
+  P.bin_ns = h->opt.trace_bin_ns ? h->opt.trace_bin_ns : 1;
+  P.horizon = h->opt.horizon_ns;
+  P.slo_ttft_ns = (i64)std::floor(h->opt.slo_ttft_s * 1e9 + 0.5);
+  P.slo_mtpot_ns = (i64)std::floor(h->opt.slo_mtpot_s * 1e9 + 0.5);
+  P.pd_link_inv = h->opt.pd_link_bw > 0 ? 1.0 / h->opt.pd_link_bw : 0.0;
+  P.scratch = reinterpret_cast<u64 *>(ws + L.scratch);
+
+  // longest-estimated-first order (LPT): simulated span / per-iteration floor
+  std::vector<u32> order(n_run + 1, 0);
+  {
+    std::vector<std::pair<double, u32>> est(n_run);
+    for (u64 j = 0; j < n_run; ++j) {
+      const Coords c = decode_point(begin + j * stride, P.n_pol, P.n_rates, P.n_seeds);
+      const double span = (double)P.n_req / h->rates[c.rate];
+      est[j] = {span / h->est_T1[(size_t)c.hw * P.n_pol + c.pol], (u32)j};
+    }
+    std::stable_sort(est.begin(), est.end(), [](const std::pair<double, u32> &a, const std::pair<double, u32> &b) {
+      return a.first > b.first;
+    });
+    for (u64 j = 0; j < n_run; ++j) order[j] = est[j].second;
+  }
+  e = cudaMemcpyAsync(ws + L.order, order.data(), (n_run + 1) * 4, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMemcpyAsync(order)");
+  e = cudaMemsetAsync(ws + L.queue, 0, 256, st);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMemsetAsync(queue)");
+  h->n_launches = 0;
+  cudaEventRecord(h->ev[0], st);
+  if (n_run > 0 && !trace_mode) {
+    e = launch_workload(P, st);
+    if (e != cudaSuccess) return cuda_fail(h, e, "workload_kernel");
+    ++h->n_launches;
+  }
+  cudaEventRecord(h->ev[1], st);
+  if (n_run > 0) {
+    e = launch_sim(P, (int)h->cap, (int)L.wpb, (int)L.blocks, L.smem, st);
+    if (e != cudaSuccess) return cuda_fail(h, e, "sim_kernel");
+    ++h->n_launches;
+  }
+  cudaEventRecord(h->ev[2], st);
+  if (n_run > 0) {
+    e = launch_summary(P, st);
+    if (e != cudaSuccess) return cuda_fail(h, e, "summary_kernel");
+    ++h->n_launches;
+  }
+  cudaEventRecord(h->ev[3], st);
+  h->h2d_bytes = h->table_bytes_pending + (n_run + 1) * 4;
+  h->table_bytes_pending = 0;
+  // the host order buffer is pageable: the copy above is staged before return
+  h->ran = true;
+  h->begin = begin;
+  h->end = end;
+  h->stride = stride;
+  h->n_run = n_run;
+  h->ws = ws;
+  h->ws_bytes = ws_bytes;
+  h->stream = st;
+  h->P = P;
+  h->lay = L;
+  return TOKENSIM_OK;
+}
+
+static tokensim_status local_index(const tokensim_sweep *h, u64 point, u64 *j) {
+  if (point >= h->n_points) return TOKENSIM_E_RANGE;
+  if (!h->ran || point < h->begin || point >= h->end || (point - h->begin) % h->stride) return TOKENSIM_E_STATE;
+  *j = (point - h->begin) / h->stride;
+  return TOKENSIM_OK;
+}
+
+static tokensim_status sync_run(tokensim_sweep *h) {
+  cudaSetDevice(h->dev);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "stream");
+  return TOKENSIM_OK;
+}
+
+static tokensim_status copy_d2h(tokensim_sweep *h, void *dst, const void *src, size_t bytes) {
+  if (!bytes) return TOKENSIM_OK;
+  cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMemcpy D2H");
+  return TOKENSIM_OK;
+}
+
+tokensim_status tokensim_get_summary(const tokensim_sweep *hc, uint64_t point, tokensim_summary *out) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h || !out) return TOKENSIM_E_INVALID;
+  u64 j;
+  tokensim_status s = local_index(h, point, &j);
+  if (s == TOKENSIM_E_STATE && point < h->imported.size() && h->imported[point].version) {
+    *out = h->imported[point];
+    return TOKENSIM_OK;
+  }
+  if (s != TOKENSIM_OK) return fail(h, s, "get_summary: point not run by this handle");
+  if ((s = sync_run(h)) != TOKENSIM_OK) return s;
+  return copy_d2h(h, out, h->P.summ + j, sizeof(tokensim_summary));
+}
+
+tokensim_status tokensim_get_summaries(const tokensim_sweep *hc, tokensim_summary *out, uint64_t capacity,
+                                       uint64_t *n_out) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h || !n_out) return TOKENSIM_E_INVALID;
+  if (!h->ran) return fail(h, TOKENSIM_E_STATE, "get_summaries: no run");
+  *n_out = h->n_run;
+  if (!out || capacity == 0) return TOKENSIM_OK;
+  if (capacity < h->n_run) return TOKENSIM_E_TRUNCATED;
+  tokensim_status s = sync_run(h);
+  if (s != TOKENSIM_OK) return s;
+  return copy_d2h(h, out, h->P.summ, h->n_run * sizeof(tokensim_summary));
+}
+
+tokensim_status tokensim_get_summaries_device(const tokensim_sweep *h, const void **d_ptr, size_t *bytes) {
+  if (!h || !d_ptr || !bytes) return TOKENSIM_E_INVALID;
+  if (!h->ran) return TOKENSIM_E_STATE;
+  *d_ptr = h->P.summ;
+  *bytes = h->n_run * sizeof(tokensim_summary);
+  return TOKENSIM_OK;
+}
+
+tokensim_status tokensim_import_summaries(tokensim_sweep *h, const void *host_ptr, size_t bytes) {
+  if (!h || (!host_ptr && bytes)) return TOKENSIM_E_INVALID;
+  if (bytes % sizeof(tokensim_summary)) return fail(h, TOKENSIM_E_INVALID, "import_summaries: bytes % 384 != 0");
+  const tokensim_summary *s = static_cast<const tokensim_summary *>(host_ptr);
+  if (h->imported.size() < h->n_points) h->imported.resize(h->n_points);
+  for (size_t i = 0; i < bytes / sizeof(tokensim_summary); ++i) {
+    if (!s[i].version) continue;
+    if (s[i].point >= h->n_points) return fail(h, TOKENSIM_E_RANGE, "import_summaries: point out of range");
+    h->imported[s[i].point] = s[i];
+  }
+  return TOKENSIM_OK;
+}
+
+tokensim_status tokensim_get_request_records(const tokensim_sweep *hc, uint64_t point, tokensim_request_record *out,
+                                             uint64_t capacity, uint64_t *n_out) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h || !n_out) return TOKENSIM_E_INVALID;
+  u64 j;
+  tokensim_status s = local_index(h, point, &j);
+  if (s != TOKENSIM_OK) return fail(h, s, "get_request_records: point not run by this handle");
+  const u64 n = h->wl.num_requests;
+  *n_out = n;
+  if (!out || capacity == 0) return TOKENSIM_OK;
+  if (capacity < n) return TOKENSIM_E_TRUNCATED;
+  if ((s = sync_run(h)) != TOKENSIM_OK) return s;
+  return copy_d2h(h, out, h->P.rec + j * n, n * sizeof(tokensim_request_record));
+}
+
+tokensim_status tokensim_get_iteration_trace(const tokensim_sweep *hc, uint64_t point, tokensim_iter_record *out,
+                                             uint64_t capacity, uint64_t *n_out) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h || !n_out) return TOKENSIM_E_INVALID;
+  u64 j;
+  tokensim_status s = local_index(h, point, &j);
+  if (s != TOKENSIM_OK) return fail(h, s, "get_iteration_trace: point not run by this handle");
+  if (h->opt.iteration_trace_cap == 0) return fail(h, TOKENSIM_E_STATE, "iteration trace disabled (iteration_trace_cap = 0)");
+  if ((s = sync_run(h)) != TOKENSIM_OK) return s;
+  SimStats st;
+  if ((s = copy_d2h(h, &st, h->P.stats + j, sizeof st)) != TOKENSIM_OK) return s;
+  *n_out = st.iter_n;
+  if (!out || capacity == 0) return TOKENSIM_OK;
+  if (capacity < st.iter_n) return TOKENSIM_E_TRUNCATED;
+  return copy_d2h(h, out, h->P.itrec + j * h->P.it_cap, st.iter_n * sizeof(tokensim_iter_record));
+}
+
+tokensim_status tokensim_get_mem_trace(const tokensim_sweep *hc, uint64_t point, uint32_t worker,
+                                       tokensim_mem_sample *out, uint64_t capacity, uint64_t *n_out) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h || !n_out) return TOKENSIM_E_INVALID;
+  if (worker > (h->opt.topology == TOKENSIM_PD_PAIR ? 1u : 0u)) return TOKENSIM_E_RANGE;
+  u64 j;
+  tokensim_status s = local_index(h, point, &j);
+  if (s != TOKENSIM_OK) return fail(h, s, "get_mem_trace: point not run by this handle");
+  if (h->opt.trace_mode == TOKENSIM_TRACE_NONE) return fail(h, TOKENSIM_E_STATE, "memory trace disabled");
+  if ((s = sync_run(h)) != TOKENSIM_OK) return s;
+  SimStats st;
+  if ((s = copy_d2h(h, &st, h->P.stats + j, sizeof st)) != TOKENSIM_OK) return s;
+  const u64 cnt = st.trace_n[worker];
+  *n_out = cnt;
+  if (!out || capacity == 0) return TOKENSIM_OK;
+  if (capacity < cnt) return TOKENSIM_E_TRUNCATED;
+  s = copy_d2h(h, out, h->P.trace + (j * 2 + worker) * h->P.trace_cap, cnt * sizeof(tokensim_mem_sample));
+  if (s != TOKENSIM_OK) return s;
+  return (st.flags & TOKENSIM_PT_TRACE_OVERFLOW) ? TOKENSIM_E_OVERFLOW : TOKENSIM_OK;
+}
+
+tokensim_status tokensim_get_latency_quantiles(const tokensim_sweep *hc, uint64_t point, uint32_t metric,
+                                               const uint32_t *q_bp, uint32_t n_q, double *out_seconds) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h || (!q_bp && n_q) || (!out_seconds && n_q)) return TOKENSIM_E_INVALID;
+  if (metric > TOKENSIM_MTPOT) return fail(h, TOKENSIM_E_RANGE, "get_latency_quantiles: metric out of range");
+  for (u32 i = 0; i < n_q; ++i)
+    if (q_bp[i] > 10000) return fail(h, TOKENSIM_E_RANGE, "get_latency_quantiles: q_bp must be in [0, 10000]");
+  if (n_q == 0) return TOKENSIM_OK;
+  u64 j;
+  tokensim_status s = local_index(h, point, &j);
+  if (s == TOKENSIM_E_STATE && point < h->imported.size() && h->imported[point].version) {
+    for (u32 i = 0; i < n_q; ++i) {
+      const int col = q_bp[i] == 5000 ? 0 : q_bp[i] == 9000 ? 1 : q_bp[i] == 9900 ? 2 : q_bp[i] == 10000 ? 3 : -1;
+      if (col < 0) return fail(h, TOKENSIM_E_STATE, "get_latency_quantiles: only P50/P90/P99/max are available for points run elsewhere");
+      out_seconds[i] = h->imported[point].stat[metric][col];
+    }
+    return TOKENSIM_OK;
+  }
+  if (s != TOKENSIM_OK) return fail(h, s, "get_latency_quantiles: point not run by this handle");
+  if ((s = sync_run(h)) != TOKENSIM_OK) return s;
+  const u64 n = h->wl.num_requests;
+  char *buf = nullptr;
+  const size_t bytes = align256(n_q * 4) + align256(n_q * 8) + n * 8;
+  cudaError_t e = cudaMalloc(&buf, bytes);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMalloc(quantiles)");
+  u32 *d_q = reinterpret_cast<u32 *>(buf);
+  double *d_out = reinterpret_cast<double *>(buf + align256(n_q * 4));
+  u64 *d_keys = reinterpret_cast<u64 *>(buf + align256(n_q * 4) + align256(n_q * 8));
+  e = cudaMemcpy(d_q, q_bp, n_q * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_quantiles(h->P, j, metric, d_q, n_q, d_out, d_keys, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e == cudaSuccess) e = cudaMemcpy(out_seconds, d_out, n_q * 8, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  if (e != cudaSuccess) return cuda_fail(h, e, "quantile_kernel");
+  return TOKENSIM_OK;
+}
+
+tokensim_status tokensim_get_workload(const tokensim_sweep *hc, uint64_t point, int64_t *arrival_ns,
+                                      uint32_t *prompt, uint32_t *output, uint64_t capacity) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h) return TOKENSIM_E_INVALID;
+  u64 j;
+  tokensim_status s = local_index(h, point, &j);
+  if (s != TOKENSIM_OK) return fail(h, s, "get_workload: point not run by this handle");
+  const u64 n = h->wl.num_requests;
+  if (capacity < n) return TOKENSIM_E_TRUNCATED;
+  if ((s = sync_run(h)) != TOKENSIM_OK) return s;
+  const Coords c = decode_point(point, h->P.n_pol, h->P.n_rates, h->P.n_seeds);
+  const u64 g = h->P.group_of_point_mode ? 0 : (u64)c.rate * h->P.n_seeds + c.seed;
+  if (arrival_ns && (s = copy_d2h(h, arrival_ns, h->P.arrival + g * n, n * 8)) != TOKENSIM_OK) return s;
+  if (prompt && (s = copy_d2h(h, prompt, h->P.prompt + g * n, n * 4)) != TOKENSIM_OK) return s;
+  if (output && (s = copy_d2h(h, output, h->P.output + g * n, n * 4)) != TOKENSIM_OK) return s;
+  return TOKENSIM_OK;
+}
+
+tokensim_status tokensim_get_run_info(const tokensim_sweep *hc, tokensim_run_info *out) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h || !out) return TOKENSIM_E_INVALID;
+  if (!h->ran) return fail(h, TOKENSIM_E_STATE, "get_run_info: no run");
+  tokensim_status s = sync_run(h);
+  if (s != TOKENSIM_OK) return s;
+  float ms[3] = {0, 0, 0};
+  for (int i = 0; i < 3; ++i) {
+    cudaError_t e = cudaEventElapsedTime(&ms[i], h->ev[i], h->ev[i + 1]);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaEventElapsedTime");
+  }
+  out->ms_workload = ms[0];
+  out->ms_sim = ms[1];
+  out->ms_summary = ms[2];
+  out->n_launches = h->n_launches;
+  out->sim_blocks = h->lay.blocks;
+  out->sim_warps_per_block = h->lay.wpb;
+  out->smem_per_warp = (u32)sim_smem_per_warp((int)h->cap, h->nwords_max);
+  out->n_run = h->n_run;
+  out->h2d_bytes = h->h2d_bytes;
+  out->workspace_bytes = h->lay.total;
+  return TOKENSIM_OK;
+}
+
+void tokensim_sweep_destroy(tokensim_sweep *h) {
+  if (!h) return;
+  if (h->dev >= 0) cudaSetDevice(h->dev);
+  for (int i = 0; i < 4; ++i)
+    if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+  if (h->d_tab) cudaFree(h->d_tab);
+  if (h->owned_ws) cudaFree(h->owned_ws);
+  delete h;
+}
+
+}  // extern "C"

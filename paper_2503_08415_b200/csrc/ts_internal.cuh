@@ -1,0 +1,127 @@
+// ts_internal.cuh -- device-side data layout shared by the kernels and the host runtime.
+// Nothing here is shared with oracle/ (the oracle has its own structs and code).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/tokensim.h"
+
+namespace ts {
+
+typedef uint64_t u64;
+typedef int64_t i64;
+typedef uint32_t u32;
+
+// Model constants (SURVEY c.5 notation), all exact integers.
+struct DevModel {
+  u64 L, h, q, g, f, fu, V, s;
+  u64 q2g;     // q + 2g
+  u64 hq2g;    // h*(q+2g)
+  u64 qh;      // q*h
+  u64 hfu;     // h*f_u
+  u64 fh;      // f*h
+  u64 Vh;      // V*h
+  u64 att_tok; // 2q + 2g
+  u64 g2;      // 2g
+  u64 kvb;     // 2*L*g*s
+  u32 mml, pad;
+};
+
+// Per hardware profile: fp64 reciprocals (c.1) and the cost-model knobs.
+struct DevHw {
+  double invF, invB, invH, invT, overhead;
+  u32 tp, pad;
+};
+
+// Per (hardware profile, policy) pair: block accounting (c.1).
+struct DevHP {
+  u64 total_blocks, block_bytes, ratio_limit, cap_fresh;
+  u32 nwords, pad;
+};
+
+struct DevPol {
+  u32 kind, preempt, mns, mbt, bs, wm;
+};
+
+// Per point, written once by the simulation kernel.
+struct SimStats {
+  u32 flags, pad;
+  u64 n_finished, n_rejected, n_iterations, n_req_iters, n_preempt, swap_out, swap_in;
+  i64 last_finish, t_final;
+  u64 sched_d, block_d, req_d;
+  u64 total_blocks, peak_blocks, block_ns_sum;
+  u64 trace_n[2];
+  u64 iter_n;
+  u64 n_transfers, transfer_bytes;
+  u64 reserved[3];
+};
+
+struct SweepParams {
+  DevModel M;
+  const DevHw *hw;      // [n_hw]
+  const DevHP *hp;      // [n_hw * n_pol]
+  const DevPol *pol;    // [n_pol]
+  const double *rates;  // [n_rates]
+  const u64 *seeds;     // [n_seeds]
+  u32 n_hw, n_pol, n_rates, n_seeds;
+  u32 topology, n_req;
+  // workload: generated per (rate, seed) group; TRACE mode has one group
+  u32 len_dist, n_groups;
+  u32 prompt_a, prompt_b, output_a, output_b;
+  const u32 *pt;  // prompt table: n | lo[n] | hi[n] | thr[n-1]   (device)
+  const u32 *ot;  // output table
+  const i64 *trace_a;
+  const u32 *trace_p, *trace_o;
+  i64 *arrival;   // [group][n]
+  u32 *prompt;    // [group][n]
+  u32 *output;    // [group][n]
+  u32 group_of_point_mode;  // 0: (rate,seed) grid; 1: single TRACE group
+  // run range (local index j -> point begin + j*stride)
+  u64 begin, stride, n_run;
+  const u32 *order;  // [n_run] local indices, longest-estimated first
+  u32 *queue;        // [1] atomic work counter
+  // outputs, indexed by local j
+  tokensim_request_record *rec;  // [j][n]
+  SimStats *stats;               // [j]
+  tokensim_mem_sample *trace;    // [j][2][trace_cap]
+  u64 trace_cap;
+  tokensim_iter_record *itrec;   // [j][it_cap]
+  u64 it_cap;
+  tokensim_summary *summ;        // [j]
+  // per-warp scratch: block tables [warp][2][cap_slots][bt_len]
+  u32 *bt;
+  u32 bt_len, cap_slots, nwords_max, n_warps_total;
+  u32 trace_mode, pad0;
+  u64 bin_ns;
+  i64 horizon, slo_ttft_ns, slo_mtpot_ns;
+  double pd_link_inv;  // 1 / pd_link_bw
+  u64 *scratch;        // summary keys when n_req exceeds the shared-memory key buffer
+};
+
+// point -> grid coordinates (row-major)
+struct Coords {
+  u32 hw, pol, rate, seed;
+};
+__host__ __device__ inline Coords decode_point(u64 point, u32 n_pol, u32 n_rates, u32 n_seeds) {
+  Coords c;
+  c.seed = (u32)(point % n_seeds);
+  point /= n_seeds;
+  c.rate = (u32)(point % n_rates);
+  point /= n_rates;
+  c.pol = (u32)(point % n_pol);
+  c.hw = (u32)(point / n_pol);
+  return c;
+}
+
+// launchers (sweep.cu)
+cudaError_t launch_workload(const SweepParams &p, cudaStream_t st);
+cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
+                       cudaStream_t st);
+cudaError_t launch_summary(const SweepParams &p, cudaStream_t st);
+cudaError_t launch_quantiles(const SweepParams &p, u64 j, u32 metric, const u32 *d_ranks, u32 n_q,
+                             double *d_out, u64 *d_keys, cudaStream_t st);
+constexpr u32 kSummarySmemKeys = 12288;  // keys held in shared memory by summary_kernel
+size_t sim_smem_per_warp(int cap, u32 nwords_max);
+cudaError_t sim_occupancy(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
+
+}  // namespace ts

@@ -1,0 +1,185 @@
+"""CUDA path vs oracle, element by element, through the C ABI (-m gpu).
+
+Bar (BASELINE.json north_star): schedules, batch compositions, preemptions, block ids and
+per-request token counts bit-exact (digests + records + iteration traces); fp64
+latencies/quantiles within 1e-9 relative (expected equal: both sides evaluate the same
+fp64 expressions in the same order without FMA)."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import sweep_inputs as si
+
+from parity import (compare_iters, compare_records, compare_summary, compare_trace, oracle_points,
+                    sample_points)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2503_08415_b200 import build
+    build.build()
+    import paper_2503_08415_b200 as P
+    return P
+
+
+def run_gpu(api, cfg, begin=0, end=None, stride=1):
+    sw = api.Sweep(cfg)
+    sw.run(begin, end, stride)
+    return sw
+
+
+def check_points(sw, cfg, points, records=True, trace=False, iters=False):
+    want = ["summary"] + (["records"] if records else []) + (["trace"] if trace else []) + \
+           (["iters"] if iters else [])
+    ora = oracle_points(cfg, points, want=tuple(want))
+    bad = []
+    for p in points:
+        o = ora[p]
+        bad += compare_summary(sw.summary(p), o["summary"], p)
+        if records:
+            bad += compare_records(sw.records(p), o["records"], p)
+        if trace:
+            bad += compare_trace(sw.mem_trace(p), o["trace"][0], p)
+        if iters:
+            bad += compare_iters(sw.iteration_trace(p), o["iters"], p)
+    assert not bad, "\n".join(bad[:20])
+
+
+def test_c1_bit_exact(api):
+    cfg = replace(si.c1(), options=si.Options(iteration_trace_cap=1 << 20))
+    sw = run_gpu(api, cfg)
+    check_points(sw, cfg, [0], records=True, trace=True, iters=True)
+
+
+def test_workload_generator(api):
+    from oracle import oracle as O
+    cfg = si.c2()
+    sw = run_gpu(api, cfg)
+    for p in (0, 7, 63, 64, 127):
+        ga, gp, go = sw.workload(p)
+        oa, op, oo = O.workload(cfg, p)
+        assert (ga == oa).all() and (gp == op).all() and (go == oo).all(), p
+
+
+def test_c2_every_point(api):
+    cfg = si.c2()
+    sw = run_gpu(api, cfg)
+    check_points(sw, cfg, list(range(cfg.num_points)), records=True)
+
+
+def test_c2_sharding_invariance(api):
+    cfg = si.c2()
+    full = run_gpu(api, cfg).summaries()
+    for b, s in ((1, 3), (2, 5), (0, 8)):
+        part = run_gpu(api, cfg, b, None, s).summaries()
+        ref = full[b::s]
+        assert (part.view(np.uint8).reshape(len(part), -1) == ref.view(np.uint8).reshape(len(ref), -1)).all()
+
+
+def _micro(rng):
+    n = int(rng.integers(1, 80))
+    a = np.sort(rng.integers(0, 3_000_000_000, n))
+    if rng.random() < 0.3:
+        a[:] = a[0]  # identical arrival times
+    p = rng.integers(1, 64, n)
+    if rng.random() < 0.3:
+        p = (p // 16 + 1) * 16 % 64 + 16  # p % 16 == 0
+    o = rng.integers(1, 64, n)
+    if rng.random() < 0.2:
+        o[:] = 1
+    mml = 128
+    model = replace(si.LLAMA2_7B, max_model_len=mml)
+    bs = int(rng.choice([1, 4, 16]))
+    mb = -(-mml // bs)
+    total = int(rng.integers(mb, mb + 40))
+    hw = replace(si.A100, kv_blocks_override=total, tp_degree=int(rng.choice([1, 2])), tp_link_bw=300e9)
+    pol = si.Policy(kind=str(rng.choice([si.STATIC, si.CONT, si.CONT_RATIO])),
+                    preempt=str(rng.choice([si.SWAP, si.RECOMPUTE])),
+                    max_mem_ratio=float(rng.choice([0.3, 0.7, 1.0])),
+                    max_num_seqs=int(rng.choice([1, 3, 8, 33, 256])), block_size=bs,
+                    max_batched_tokens=int(rng.choice([mml, 300, si.UINT32_MAX])),
+                    watermark_blocks=int(rng.integers(0, total - mb + 1)))
+    w = si.Workload(n, [1.0], [0], len_dist=si.TRACE, trace_arrival_ns=a.tolist(), trace_prompt=p.tolist(),
+                    trace_output=o.tolist(), prompt_table=None, output_table=None)
+    mode = si.FULL if rng.random() < 0.5 else si.BINNED
+    opts = si.Options(trace_mode=mode, trace_bin_ns=int(rng.choice([10_000_000, 1_000_000_000])),
+                      iteration_trace_cap=1 << 16, horizon_ns=int(rng.choice([-1, -1, -1, 500_000_000])))
+    return si.SweepConfig("micro", model, [hw], [pol], w, opts)
+
+
+def test_adversarial_micro_configs(api):
+    """Capacity of a few blocks (preemption storms), max_num_seqs = 1, o = 1, p % 16 == 0,
+    identical arrivals, tiny ratios (rejections), STATIC, RECOMPUTE, TP, horizon, FULL trace."""
+    rng = np.random.default_rng(7)
+    for it in range(60):
+        cfg = _micro(rng)
+        sw = run_gpu(api, cfg)
+        check_points(sw, cfg, [0], records=True, trace=True, iters=True)
+
+
+def test_preemption_heavy_grid(api):
+    """C2-shaped grid squeezed onto a small KV pool: every policy x preemption mode."""
+    pols = [si.Policy(kind=k, preempt=pm, max_mem_ratio=r) for k, r in
+            ((si.CONT, 1.0), (si.CONT_RATIO, 0.8), (si.STATIC, 1.0)) for pm in (si.SWAP, si.RECOMPUTE)]
+    cfg = si.SweepConfig("pressure", si.LLAMA2_13B, [si.Hw(mem_capacity=30 * 10 ** 9), si.A100], pols,
+                         si.Workload(300, [4.0, 16.0], [0, 1]))
+    sw = run_gpu(api, cfg)
+    check_points(sw, cfg, list(range(cfg.num_points)), records=True, trace=True)
+    assert sw.summaries()["n_preemptions"].sum() > 0
+
+
+def test_quantile_getter_arbitrary_q(api):
+    from oracle import oracle as O
+    cfg = si.c2()
+    sw = run_gpu(api, cfg)
+    qs = [0, 1, 100, 2500, 5000, 7500, 9000, 9500, 9900, 9990, 10000]
+    for p in (3, 77):
+        o = O.simulate(cfg, p)
+        rec = o["records"]
+        a, pr, out = O.workload(cfg, p)
+        fin = rec["status"] == 1
+        vals = {
+            "ttft": rec["ttft_ns"][fin] / 1e9, "e2e": rec["e2e_ns"][fin] / 1e9, "mtpot": rec["mtpot_ns"][fin] / 1e9,
+            "norm": (rec["e2e_ns"][fin] / out[fin].astype(np.float64)) / 1e9,
+        }
+        m2 = fin & (out >= 2)
+        vals["tpot"] = ((rec["e2e_ns"][m2] - rec["ttft_ns"][m2]) / (out[m2] - 1).astype(np.float64)) / 1e9
+        for name, v in vals.items():
+            v = np.sort(v)
+            got = sw.latency_quantiles(p, name, qs)
+            ref = [v[max(1, -(-q * len(v) // 10000)) - 1] for q in qs]
+            assert np.array_equal(got, np.asarray(ref)), (p, name)
+
+
+def test_c3_sampled(api):
+    """Full C3 sweep (4,608 points, 10k requests each) on the GPU; the oracle on a
+    deterministic sample incl. grid corners."""
+    cfg = si.c3()
+    sw = run_gpu(api, cfg)
+    s = sw.summaries()
+    assert (s["n_finished"] == 10_000).all() and (s["status_flags"] & 16 == 0).all()
+    corners = [0, 1, 2, 3, 4, 5, 4607, 4606, 4605, 1536 * 1 + 17, 3 * 1535, 3 * 1535 + 2]
+    pts = sample_points(cfg.num_points, target=16, corners=corners)
+    check_points(sw, cfg, pts, records=True)
+
+
+def test_c4_sampled(api):
+    cfg = si.c4()
+    sw = run_gpu(api, cfg)
+    s = sw.summaries()
+    assert (s["status_flags"] & 16 == 0).all()
+    pts = sample_points(cfg.num_points, target=12, corners=[0, 191, 192, 2303, 768 + 5, 1536 + 100])
+    check_points(sw, cfg, pts, records=True)
+
+
+def test_sharegpt_builtin_equals_table(api):
+    cfg = si.c1()
+    a = run_gpu(api, cfg).summaries()
+    b = run_gpu(api, replace(cfg, workload=replace(cfg.workload, len_dist="sharegpt_synth_v1"))).summaries()
+    assert a.tobytes() == b.tobytes()
