@@ -144,7 +144,11 @@ typedef struct {
   double slo_ttft_s;          /* 15                                          */
   double slo_mtpot_s;         /* 0.3                                         */
   int64_t horizon_ns;         /* -1 = run to completion                              */
+  uint32_t flags;             /* TOKENSIM_OPT_*; 0 = defaults                        */
 } tokensim_options;
+/* options.flags: evaluate quiescent decode stretches one iteration at a time instead of
+ * 32 at once (results are identical either way; this exists to prove it). */
+enum { TOKENSIM_OPT_NO_FAST_FORWARD = 1 };
 
 /* ---- results ------------------------------------------------------------- */
 typedef struct {               /* 32 B; index = request id                         */

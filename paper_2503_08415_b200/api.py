@@ -87,7 +87,8 @@ def marshal(cfg: si.SweepConfig):
         cw.trace_arrival_ns, cw.trace_prompt, cw.trace_output = pta, ptp, pto
     o = cfg.options
     co = T.Options(C.sizeof(T.Options), _TOP[o.topology], o.pd_link_bw, _TRC[o.trace_mode], o.trace_bin_ns,
-                   o.trace_cap_bytes, o.iteration_trace_cap, o.slo_ttft_s, o.slo_mtpot_s, o.horizon_ns)
+                   o.trace_cap_bytes, o.iteration_trace_cap, o.slo_ttft_s, o.slo_mtpot_s, o.horizon_ns,
+                   0 if o.fast_forward else T.OPT_NO_FAST_FORWARD)
     return cm, hws, pols, cw, co, keep
 
 

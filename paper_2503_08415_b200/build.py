@@ -15,8 +15,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("sweep.cu", "host.cu")]
-HEADERS = [os.path.join(CSRC, "ts_internal.cuh"), os.path.join(ROOT, "include", "tokensim.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("workload.cu", "sim.cu", "metrics.cu", "host.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in ("ts_internal.cuh", "dev_common.cuh")] + \
+    [os.path.join(ROOT, "include", "tokensim.h")]
 LIB = os.path.join(PKG, "libtokensim.so")
 
 NVCC_FLAGS = [

@@ -1,0 +1,85 @@
+// dev_common.cuh -- warp-level primitives and the c.6 digest mixer shared by the kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ts_internal.cuh"
+
+namespace ts {
+
+#define FULLMASK 0xffffffffu
+
+__device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ u32 lanemask_lt() {
+  u32 m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ u32 scan_incl(u32 x) {
+  const u32 l = lane_id();
+#pragma unroll
+  for (u32 o = 1; o < 32; o <<= 1) {
+    u32 y = __shfl_up_sync(FULLMASK, x, o);
+    if (l >= o) x += y;
+  }
+  return x;
+}
+__device__ __forceinline__ u64 warp_sum64(u64 x) {
+#pragma unroll
+  for (u32 o = 16; o; o >>= 1) x += __shfl_xor_sync(FULLMASK, x, o);
+  return x;
+}
+__device__ __forceinline__ u64 shfl64(u64 x, u32 src) { return __shfl_sync(FULLMASK, x, src); }
+__device__ __forceinline__ i64 shfl64i(i64 x, u32 src) { return __shfl_sync(FULLMASK, x, src); }
+
+// r-th (0-based) set bit of w (r < popc(w))
+__device__ __forceinline__ u32 select_bit(u32 w, u32 r) {
+  u32 pos = 0;
+#pragma unroll
+  for (u32 s = 16; s; s >>= 1) {
+    const u32 c = __popc(w & ((1u << s) - 1u));
+    if (r >= c) {
+      r -= c;
+      pos += s;
+      w >>= s;
+    }
+  }
+  return pos;
+}
+// keep w without its `tk` lowest set bits (tk <= popc(w))
+__device__ __forceinline__ u32 clear_lowest(u32 w, u32 tk, u32 c) {
+  if (tk == 0) return w;
+  if (tk >= c) return 0u;
+  return w & ~((1u << select_bit(w, tk)) - 1u);
+}
+
+// ------------------------------------------------------------------ c.6 digests
+__device__ __forceinline__ u64 mix64(u64 x) {
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+#define FOLD_INIT 0x9E3779B97F4A7C15ull
+__device__ __forceinline__ u64 fold4(u64 a, u64 b, u64 c, u64 d) {
+  u64 h = FOLD_INIT;
+  h = mix64(h ^ a);
+  h = mix64(h ^ b);
+  h = mix64(h ^ c);
+  h = mix64(h ^ d);
+  return h;
+}
+
+// block size arithmetic: shifts/masks when block_size is a power of two (the common case)
+struct BSz {
+  u32 bs, sh, mask;
+  bool p2;
+  __device__ __forceinline__ u32 div(u32 x) const { return p2 ? (x >> sh) : x / bs; }
+  __device__ __forceinline__ u32 mod(u32 x) const { return p2 ? (x & mask) : x % bs; }
+  __device__ __forceinline__ u32 cdiv(u32 x) const { return p2 ? ((x + mask) >> sh) : (x + bs - 1) / bs; }
+};
+
+}  // namespace ts

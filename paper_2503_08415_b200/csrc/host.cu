@@ -285,10 +285,31 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
     d.mbt = p.max_batched_tokens;
     d.bs = p.block_size;
     d.wm = p.watermark_blocks;
+    d.bs_sh = (p.block_size & (p.block_size - 1)) ? 0xffffffffu : (u32)__builtin_ctz(p.block_size);
+    d.pad = 0;
     h->dpol.push_back(d);
   }
   h->cap = max_mns <= 32 ? 32 : (max_mns <= 256 ? 256 : 1024);
   h->bt_len = (u32)ceil_div(mml, min_bs);
+  if (h->bt_len > (1u << 17)) return bad("model.max_model_len / policies[].block_size: more than 2^17 blocks per request");
+  // every F_o / B_o of the c.5 cost table must stay an exact fp64 integer (< 2^53)
+  {
+    typedef unsigned __int128 u128;
+    const u128 lim = (u128)1 << 53;
+    u128 worst = 0;
+    for (u32 i = 0; i < n_pol; ++i) {
+      const u128 mns = pol[i].max_num_seqs;
+      const u128 Np = std::min<u128>(pol[i].max_batched_tokens, mns * mml);
+      const u128 N = Np + mns, S = mns;
+      const u128 Ap = mns * (u128)mml * (mml + 1) / 2, Cd = mns * (u128)(mml + 1);
+      const u128 cand[] = {2 * N * M.hq2g, M.s * (M.hq2g + N * M.h + N * M.q2g), 2 * N * M.hfu,
+                           M.s * (M.hfu + N * M.h + N * M.fu), 4 * (u128)M.q * Ap, 4 * (u128)M.q * Cd,
+                           M.s * (N * M.att_tok + M.g2 * (Np > Cd ? Np : Cd)), 2 * S * M.Vh,
+                           M.s * (M.Vh + S * M.h + S * M.V)};
+      for (u128 c : cand) worst = std::max(worst, c);
+    }
+    if (worst >= lim) return bad("model x policies: cost-table integers exceed 2^53 (not exact in fp64)");
+  }
 
   // ---- hardware profiles and (hw, pol) block accounting
   u64 max_words = 1;
@@ -564,6 +585,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.slo_mtpot_ns = (i64)std::floor(h->opt.slo_mtpot_s * 1e9 + 0.5);
   P.pd_link_inv = h->opt.pd_link_bw > 0 ? 1.0 / h->opt.pd_link_bw : 0.0;
   P.scratch = reinterpret_cast<u64 *>(ws + L.scratch);
+  P.ff_enable = (h->opt.flags & TOKENSIM_OPT_NO_FAST_FORWARD) ? 0u : 1u;
 
   // longest-estimated-first order (LPT): simulated span / per-iteration floor
   std::vector<u32> order(n_run + 1, 0);

@@ -1,0 +1,1037 @@
+// sim.cu -- a.2-a.7: the persistent per-point simulation kernel.
+//
+// ONE WARP PER POINT, pulled from an atomic longest-first queue.  The running set R and
+// the resume queue Q are one array of request slots in ascending id (R is a prefix, Q
+// the suffix: preemption moves the R/Q boundary left, resume moves it right), held
+// structure-of-arrays in shared memory together with the free-block bitmap and the
+// block-table slot pool.  Per-slot work is lane-parallel (32 slots per warp step);
+// FCFS admission is a prefix scan + ballot; the victim count is the closed form of c.4
+// step 3; block allocation extracts the K lowest free bits of the bitmap in one pass
+// and hands them out in phase/id order (reading A14).
+//
+// Quiescent decode stretches are evaluated time-parallel: when no
+// admission, resume, preemption or finish can happen for a while, lane j computes
+// iteration k+j (its cost, start time by a 64-bit prefix scan, its block allocations,
+// its schedule digest and trace sample) and the warp commits up to 32 iterations at
+// once -- bit-identical to stepping them one by one.
+//
+// PAPER.md anchors: worker loop / default end-of-iteration breakpoint P:243; continuous
+// vs static batching P:166-169; PagedAttention P:172-173; preemption
+// P:456-457; max-memory-ratio admission P:460; compute simulator P:216.
+#include "dev_common.cuh"
+
+namespace ts {
+
+// ------------------------------------------------------------------ a.6 cost model
+// All F_o/B_o of the c.5 table are integers < 2^53 (validated at create), so forming them
+// with fp64 products/sums is exact and equals (double)(u64 value) -- the oracle's form.
+struct CostK {
+  double h, q2g, hq2g, qh, q, q4, hfu, fu, fh, f, Vh, V, s, att_tok, g2, L, twoL, bar_coef;
+  double invF, invB, invH, invT, overhead;
+  u32 tp;
+};
+
+__device__ __forceinline__ CostK make_costk(const DevModel &M, const DevHw &H) {
+  CostK K;
+  K.h = __ull2double_rn(M.h);
+  K.q2g = __ull2double_rn(M.q2g);
+  K.hq2g = __ull2double_rn(M.hq2g);
+  K.qh = __ull2double_rn(M.qh);
+  K.q = __ull2double_rn(M.q);
+  K.q4 = __ull2double_rn(4 * M.q);
+  K.hfu = __ull2double_rn(M.hfu);
+  K.fu = __ull2double_rn(M.fu);
+  K.fh = __ull2double_rn(M.fh);
+  K.f = __ull2double_rn(M.f);
+  K.Vh = __ull2double_rn(M.Vh);
+  K.V = __ull2double_rn(M.V);
+  K.s = __ull2double_rn(M.s);
+  K.att_tok = __ull2double_rn(M.att_tok);
+  K.g2 = __ull2double_rn(M.g2);
+  K.L = __ull2double_rn(M.L);
+  K.twoL = __ull2double_rn(2 * M.L);
+  K.bar_coef = H.tp > 1 ? __ull2double_rn(2 * (u64)(H.tp - 1) * M.h * M.s) : 0.0;
+  K.invF = H.invF;
+  K.invB = H.invB;
+  K.invH = H.invH;
+  K.invT = H.invT;
+  K.overhead = H.overhead;
+  K.tp = H.tp;
+  return K;
+}
+
+__device__ __forceinline__ double roof(double F, double B, const CostK &K) {
+  return fmax(__dmul_rn(F, K.invF), __dmul_rn(B, K.invB));
+}
+
+// T_ns of a batch from its exact aggregates (c0 = 0, so K_p = N_p); SURVEY c.5 order.
+__device__ __forceinline__ i64 iter_time_ns(const CostK &K, u64 Np, u64 Ap, u64 Sp, u64 D, u64 Cd,
+                                            u64 swap_bytes) {
+  const double N = __ull2double_rn(Np + D), S = __ull2double_rn(Sp + D);
+  double tQKV = 0.0, tATTP = 0.0, tATTD = 0.0, tO = 0.0, tUP = 0.0, tDOWN = 0.0, tLM = 0.0;
+  const double N2 = __dmul_rn(2.0, N);
+  if (Np + D > 0) {
+    const double Nh = __dmul_rn(N, K.h);
+    tQKV = roof(__dmul_rn(N2, K.hq2g), __dmul_rn(K.s, __dadd_rn(__dadd_rn(K.hq2g, Nh), __dmul_rn(N, K.q2g))), K);
+    tO = roof(__dmul_rn(N2, K.qh), __dmul_rn(K.s, __dadd_rn(__dadd_rn(K.qh, __dmul_rn(N, K.q)), Nh)), K);
+    tUP = roof(__dmul_rn(N2, K.hfu), __dmul_rn(K.s, __dadd_rn(__dadd_rn(K.hfu, Nh), __dmul_rn(N, K.fu))), K);
+    tDOWN = roof(__dmul_rn(N2, K.fh), __dmul_rn(K.s, __dadd_rn(__dadd_rn(K.fh, __dmul_rn(N, K.f)), Nh)), K);
+  }
+  if (Np > 0) {
+    const double Npd = __ull2double_rn(Np);
+    tATTP = roof(__dmul_rn(K.q4, __ull2double_rn(Ap)),
+                 __dmul_rn(K.s, __dadd_rn(__dmul_rn(Npd, K.att_tok), __dmul_rn(K.g2, Npd))), K);
+  }
+  if (D > 0) {
+    const double Dd = __ull2double_rn(D), Cdd = __ull2double_rn(Cd);
+    tATTD = roof(__dmul_rn(K.q4, Cdd), __dmul_rn(K.s, __dadd_rn(__dmul_rn(Dd, K.att_tok), __dmul_rn(K.g2, Cdd))), K);
+  }
+  if (Sp + D > 0)
+    tLM = roof(__dmul_rn(__dmul_rn(2.0, S), K.Vh),
+               __dmul_rn(K.s, __dadd_rn(__dadd_rn(K.Vh, __dmul_rn(S, K.h)), __dmul_rn(S, K.V))), K);
+  const double tl =
+      __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(tQKV, tATTP), tATTD), tO), tUP), tDOWN);
+  double T = __dmul_rn(tl, K.L);
+  T = __dadd_rn(T, tLM);
+  if (K.tp > 1) T = __dadd_rn(T, __dmul_rn(__dmul_rn(__dmul_rn(K.bar_coef, N), K.invT), K.twoL));
+  if (swap_bytes > 0) T = __dadd_rn(T, __dmul_rn(__ull2double_rn(swap_bytes), K.invH));
+  T = __dadd_rn(T, K.overhead);
+  return (i64)floor(__dadd_rn(__dmul_rn(T, 1e9), 0.5));
+}
+
+// ------------------------------------------------------------------ per-warp shared memory
+struct WarpSmem {
+  u32 *id, *ctx, *rem, *info;       // info: bt slot (bits 0-15) | n_preempt (bits 16-31)
+  i64 *last, *maxgap, *arr, *ttft;  // last token time, max gap, arrival, ttft
+  u32 *req_cum, *req_pt;            // block requesters: cumulative count; pos|j<<10|tpos<<15
+  u32 *scratch;                     // 32 words (fast-forward histogram / bucket cursors)
+  u32 *btfree;                      // cap/32 words, bit = free block-table slot
+  u32 *bitmap;                      // free-block bitmap, bit = free block
+};
+
+__host__ __device__ inline size_t smem_per_warp_bytes(u32 cap, u32 nwords_max) {
+  size_t b = (size_t)cap * (4 * 4 + 8 * 4 + 4 * 2) + 32 * 4 + (size_t)(cap / 32) * 4 + (size_t)nwords_max * 4;
+  return (b + 15) & ~(size_t)15;
+}
+size_t sim_smem_per_warp(int cap, u32 nwords_max) { return smem_per_warp_bytes((u32)cap, nwords_max); }
+
+__device__ __forceinline__ WarpSmem carve(unsigned char *base, u32 cap) {
+  WarpSmem S;
+  i64 *p64 = reinterpret_cast<i64 *>(base);
+  S.last = p64;
+  S.maxgap = p64 + cap;
+  S.arr = p64 + 2 * cap;
+  S.ttft = p64 + 3 * cap;
+  u32 *p32 = reinterpret_cast<u32 *>(p64 + 4 * cap);
+  S.id = p32;
+  S.ctx = p32 + cap;
+  S.rem = p32 + 2 * cap;
+  S.info = p32 + 3 * cap;
+  S.req_cum = p32 + 4 * cap;
+  S.req_pt = p32 + 5 * cap;
+  S.scratch = p32 + 6 * cap;
+  S.btfree = p32 + 6 * cap + 32;
+  S.bitmap = p32 + 6 * cap + 32 + cap / 32;
+  return S;
+}
+
+#define PT_POS(pt) ((pt)&1023u)
+#define PT_J(pt) (((pt) >> 10) & 31u)
+#define PT_TPOS(pt) ((pt) >> 15)
+
+// ------------------------------------------------------------------ a.5 allocator
+// Return `held` blocks of table `tbl` to the bitmap (order-free: the block digest is a
+// wrapping sum) and lower the lowest-free-word hint.
+__device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 held, u32 id, u64 k,
+                                            u64 &dig_b, u32 &hint) {
+  u32 mn = 0xffffffffu;
+  for (u32 x = lane_id(); x < held; x += 32) {
+    const u32 b = tbl[x];
+    atomicOr(&bitmap[b >> 5], 1u << (b & 31u));
+    dig_b += fold4(k, 2, id, b);
+    mn = min(mn, b >> 5);
+  }
+  mn = __reduce_min_sync(FULLMASK, mn);
+  hint = min(hint, mn);
+}
+
+// Hand out the K lowest free blocks, in order, to the E requesters in S.req_* (entry e
+// owns order indices [req_cum[e-1], req_cum[e]) and writes its table from tpos).  This is
+// "serve the requesters one after another with take-the-lowest-free-block" (c.4 steps
+// 3-5, reading A14) done in one bitmap pass.  Entry iteration offsets (fast-forward)
+// shift the digest's iteration index.
+__device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl, u64 k, u64 &dig_b,
+                              u32 &hint, u32 nwords) {
+  const u32 lane = lane_id();
+  u32 o_base = 0, w = hint;
+  while (o_base < K) {
+    if (w >= nwords) return false;
+    const u32 wi = w + lane;
+    u32 word = wi < nwords ? S.bitmap[wi] : 0u;
+    const u32 c = __popc(word);
+    const u32 cum = scan_incl(c);
+    const u32 tot = __shfl_sync(FULLMASK, cum, 31);
+    if (tot == 0) {
+      w += 32;
+      continue;
+    }
+    const u32 take = min(tot, K - o_base);
+    const u32 before = cum - c;
+    for (u32 r0 = 0; r0 < take; r0 += 32) {
+      const u32 idx = r0 + lane;
+      const bool act = idx < take;
+      const u32 tgt = act ? idx : 0u;
+      u32 lo = 0;
+#pragma unroll
+      for (u32 s = 16; s; s >>= 1) {
+        const u32 v = __shfl_sync(FULLMASK, cum, lo + s - 1);
+        if (v <= tgt) lo += s;
+      }
+      const u32 wv = __shfl_sync(FULLMASK, word, lo);
+      const u32 bv = __shfl_sync(FULLMASK, before, lo);
+      if (act) {
+        const u32 blk = (w + lo) * 32 + select_bit(wv, tgt - bv);
+        const u32 o = o_base + idx;
+        u32 a = 0, bnd = E;
+        while (a < bnd) {
+          const u32 mid = (a + bnd) >> 1;
+          if (S.req_cum[mid] <= o) a = mid + 1;
+          else bnd = mid;
+        }
+        const u32 start = a ? S.req_cum[a - 1] : 0u;
+        const u32 pt = S.req_pt[a];
+        const u32 pos = PT_POS(pt);
+        const u32 tpos = PT_TPOS(pt) + (o - start);
+        const u32 slot = S.info[pos] & 0xffffu;
+        bt[(size_t)slot * btl + tpos] = blk;
+        dig_b += fold4(k + PT_J(pt), 1, S.id[pos], blk);
+      }
+    }
+    const u32 tk = take > before ? min(c, take - before) : 0u;
+    if (tk && wi < nwords) {
+      word = clear_lowest(word, tk, c);
+      S.bitmap[wi] = word;
+    }
+    o_base += take;
+    if (o_base < K) {
+      w += 32;
+    } else {
+      const u32 nz = __ballot_sync(FULLMASK, word != 0u);
+      w = nz ? w + (u32)(__ffs(nz) - 1) : w + 32;
+    }
+  }
+  hint = w;
+  __syncwarp();
+  return true;
+}
+
+// Give `cnt` lanes (take=1, rank 0..cnt-1) the lowest free block-table slots.
+__device__ __forceinline__ u32 alloc_btslots(u32 *btfree, u32 nw, bool take, u32 rank, u32 cnt) {
+  const u32 lane = lane_id();
+  u32 word = lane < nw ? btfree[lane] : 0u;
+  const u32 c = __popc(word);
+  const u32 cum = scan_incl(c);
+  const u32 before = cum - c;
+  const u32 tgt = take ? rank : 0u;
+  u32 lo = 0;
+#pragma unroll
+  for (u32 s = 16; s; s >>= 1) {
+    const u32 v = __shfl_sync(FULLMASK, cum, lo + s - 1);
+    if (v <= tgt) lo += s;
+  }
+  const u32 wv = __shfl_sync(FULLMASK, word, lo);
+  const u32 bv = __shfl_sync(FULLMASK, before, lo);
+  const u32 slot = lo * 32 + select_bit(wv, tgt - bv);
+  const u32 tk = cnt > before ? min(c, cnt - before) : 0u;
+  if (tk && lane < nw) btfree[lane] = clear_lowest(word, tk, c);
+  __syncwarp();
+  return slot;
+}
+
+__device__ __forceinline__ void write_record(tokensim_request_record *r, i64 ttft, i64 e2e, i64 mt,
+                                             u32 npre, u32 status, u32 fin_k) {
+  ulonglong2 *q = reinterpret_cast<ulonglong2 *>(r);
+  q[0] = make_ulonglong2((unsigned long long)ttft, (unsigned long long)e2e);
+  const u64 w3 = (u64)(npre & 0xffffu) | ((u64)(status & 0xffu) << 16) | ((u64)fin_k << 32);
+  q[1] = make_ulonglong2((unsigned long long)mt, (unsigned long long)w3);
+}
+
+__device__ __forceinline__ u64 sched_fold(u64 k, i64 ts, i64 T, u64 Sp, u64 D, u64 Np, u64 Cd, u64 m, u64 nres,
+                                          u64 nadm, u64 nrej, u64 nfin, u64 blocks) {
+  u64 h = FOLD_INIT;
+  h = mix64(h ^ k);
+  h = mix64(h ^ (u64)ts);
+  h = mix64(h ^ (u64)T);
+  h = mix64(h ^ Sp);
+  h = mix64(h ^ D);
+  h = mix64(h ^ Np);
+  h = mix64(h ^ Cd);
+  h = mix64(h ^ m);
+  h = mix64(h ^ nres);
+  h = mix64(h ^ nadm);
+  h = mix64(h ^ nrej);
+  h = mix64(h ^ nfin);
+  h = mix64(h ^ blocks);
+  return h;
+}
+
+__device__ __forceinline__ i64 scan_incl_i64(i64 x) {
+  const u32 l = lane_id();
+#pragma unroll
+  for (u32 o = 1; o < 32; o <<= 1) {
+    const i64 y = __shfl_up_sync(FULLMASK, x, o);
+    if (l >= o) x += y;
+  }
+  return x;
+}
+
+// ------------------------------------------------------------------ a.2-a.7 one point
+// Everything is executed by all 32 lanes; scalar state is lane-uniform in registers.
+template <int CAP>
+__device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S, u32 *bt) {
+  static_assert(CAP % 32 == 0 && CAP <= 1024, "CAP");
+  const u32 lane = lane_id();
+  const u32 ltm = lanemask_lt();
+  const u64 point = P.begin + j * P.stride;
+  const Coords cd = decode_point(point, P.n_pol, P.n_rates, P.n_seeds);
+  const DevHw H = P.hw[cd.hw];
+  const DevHP HP = P.hp[(size_t)cd.hw * P.n_pol + cd.pol];
+  const DevPol PL = P.pol[cd.pol];
+  const CostK K = make_costk(P.M, H);
+  const u32 g = P.group_of_point_mode ? 0u : cd.rate * P.n_seeds + cd.seed;
+  const u32 n = P.n_req;
+  const i64 *A = P.arrival + (size_t)g * n;
+  const u32 *PR = P.prompt + (size_t)g * n;
+  const u32 *OU = P.output + (size_t)g * n;
+  tokensim_request_record *rec = P.rec + (size_t)j * n;
+  tokensim_mem_sample *trc = P.trace + (size_t)j * 2 * P.trace_cap;
+  tokensim_iter_record *itr = P.itrec + (size_t)j * P.it_cap;
+  const BSz B = {PL.bs, PL.bs_sh, PL.bs - 1u, PL.bs_sh != 0xffffffffu};
+  const bool SWAPM = PL.preempt == TOKENSIM_SWAP;
+  const bool RATIO = PL.kind == TOKENSIM_CONT_RATIO;
+  const bool STATICP = PL.kind == TOKENSIM_STATIC;
+  const u64 total = HP.total_blocks;
+  const u32 nwords = HP.nwords;
+  const u32 btl = P.bt_len;
+  const u32 mns = PL.mns, mbt = PL.mbt;
+  const i64 wm = (i64)PL.wm;
+  const bool ff_on = P.ff_enable != 0;
+
+  // ---- init: records, bitmap, slot pool
+  {
+    ulonglong2 *r2 = reinterpret_cast<ulonglong2 *>(rec);
+    const ulonglong2 z = make_ulonglong2(0ull, 0ull);
+    for (u32 x = lane; x < 2 * n; x += 32) r2[x] = z;
+    const u32 full_words = (u32)(total >> 5), tail = (u32)(total & 31u);
+    for (u32 w = lane; w < nwords; w += 32)
+      S.bitmap[w] = w < full_words ? 0xffffffffu : (w == full_words && tail ? ((1u << tail) - 1u) : 0u);
+    for (u32 w = lane; w < CAP / 32; w += 32) S.btfree[w] = 0xffffffffu;
+    __syncwarp();
+  }
+
+  i64 t = 0;
+  u64 k = 0;
+  u32 arr = 0, adm = 0, nR = 0, nQ = 0;
+  u64 nfree = total;
+  u32 hint = 0;
+  u32 rmin = 0;  // min rem over R after the last commit (0 when unknown / R empty)
+  u64 dig_s = 0, dig_b = 0, dig_r = 0;  // per-lane partial digests
+  u64 req_iters = 0, npre = 0, swo_tot = 0, swi_tot = 0, nrej_tot = 0, nfin_tot = 0, peak = 0, bns = 0;
+  u64 ff_iters = 0, ff_runs = 0;
+  i64 last_fin = 0;
+  u32 flags = 0;
+  u32 hd_idx = 0xffffffffu, hd_p = 0;  // cached prompt length of the fresh-queue head
+  // sched-field buffer: lane (k mod 32) holds normal iteration k's fields until the flush
+  i64 b_t = 0, b_T = 0;
+  u64 b_np = 0, b_cd = 0;
+  u32 b_k = 0, b_blk = 0, b_spd = 0, b_mres = 0, b_adfin = 0, b_rej = 0;
+  bool b_valid = false;
+  auto put_iter = [&](u64 kk, i64 ts_, i64 T_, u32 Sp_, u32 D_, u64 Np_, u64 Cd_, u32 m_, u32 nres_, u32 nadm_,
+                      u32 nrej_, u32 nfin_, u32 blk_) {
+    if (kk < P.it_cap) {
+      tokensim_iter_record ir;
+      ir.k = kk;
+      ir.t_start_ns = ts_;
+      ir.T_ns = T_;
+      ir.n_prefill = Sp_;
+      ir.n_decode = D_;
+      ir.N_p = Np_;
+      ir.C_d = Cd_;
+      ir.n_preempted = m_;
+      ir.n_resumed = nres_;
+      ir.n_admitted = nadm_;
+      ir.n_rejected = nrej_;
+      ir.n_finished = nfin_;
+      ir.blocks_in_use = blk_;
+      ir.worker = 0;
+      ir.pad = 0;
+      itr[kk] = ir;
+    }
+  };
+  auto flush_sched = [&]() {
+    if (b_valid) {
+      dig_s += sched_fold(b_k, b_t, b_T, b_spd & 0xffffu, b_spd >> 16, b_np, b_cd, b_mres & 0xffffu, b_mres >> 16,
+                          b_adfin & 0xffffu, b_rej, b_adfin >> 16, b_blk);
+      put_iter(b_k, b_t, b_T, b_spd & 0xffffu, b_spd >> 16, b_np, b_cd, b_mres & 0xffffu, b_mres >> 16,
+               b_adfin & 0xffffu, b_rej, b_adfin >> 16, b_blk);
+    }
+    b_valid = false;
+  };
+  // memory trace state (lane-uniform)
+  const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
+  const bool FULLT = P.trace_mode == TOKENSIM_TRACE_FULL;
+  const i64 W = (i64)P.bin_ns;
+  u64 tn = 0, bin = 0, acc_bns = 0;
+  i64 bin_end = W;
+  u32 acc_max = 0, acc_nit = 0;
+  auto flush_bin = [&]() {
+    if (tn < P.trace_cap) {
+      if (lane == 0) {
+        tokensim_mem_sample s;
+        s.t_ns = (i64)bin * W;
+        s.dur_ns = W;
+        s.block_ns = acc_bns;
+        s.blocks_max = acc_max;
+        s.n_iter = acc_nit;
+        trc[tn] = s;
+      }
+    } else {
+      flags |= TOKENSIM_PT_TRACE_OVERFLOW;
+    }
+    ++tn;
+    ++bin;
+    bin_end += W;
+    acc_bns = 0;
+    acc_max = 0;
+    acc_nit = 0;
+  };
+
+  // arrival window: lane l holds A[win + l]
+  u32 win = 0;
+  i64 wa = lane < n ? A[lane] : INT64_MAX;
+
+  while (true) {
+    // 0. termination
+    if (adm == n && nR == 0 && nQ == 0) break;
+    if (P.horizon >= 0 && t >= P.horizon) {
+      flags |= TOKENSIM_PT_HORIZON_HIT;
+      break;
+    }
+    // 1. ingest: a_i <= t become visible at this boundary
+    while (arr < n) {
+      if (arr >= win + 32) {
+        win = arr;
+        wa = win + lane < n ? A[win + lane] : INT64_MAX;
+      }
+      const u32 m = __ballot_sync(FULLMASK, (win + lane >= arr) && (wa <= t));
+      arr += __popc(m);
+      if (arr < win + 32) break;
+    }
+    // 2. idle skip
+    if (nR == 0 && nQ == 0 && adm == arr) {
+      t = __shfl_sync(FULLMASK, wa, arr - win);
+      continue;
+    }
+
+    // ---------------------------------------------------------------- fast-forward (H3)
+    if (ff_on && nQ == 0 && nR > 0 && rmin >= 3) {
+      // Fresh admission must be impossible for the whole stretch: STATIC with R != {} never
+      // admits; an empty fresh queue is cut at the next arrival; a blocked head stays blocked
+      // while R is frozen and the free count only falls (c.4 step 5 is monotone).
+      bool quiet = true, head_mem = false;
+      u32 need_h = 0;
+      if (!STATICP && adm < arr) {
+        if (hd_idx != adm) {
+          hd_idx = adm;
+          hd_p = PR[adm];
+        }
+        need_h = B.cdiv(hd_p);
+        if ((u64)need_h > HP.cap_fresh) quiet = false;  // would be rejected at this boundary
+        else if (!((u64)nR + 1 > mns || (u64)nR + hd_p > mbt)) head_mem = true;
+      }
+      if (quiet) {
+        // pass over R: C_d(0), needs histogram by iteration offset (lane j <-> iteration k+j)
+        S.scratch[lane] = 0;
+        __syncwarp();
+        u64 cdp = 0;
+        for (u32 b0 = 0; b0 < nR; b0 += 32) {
+          const u32 jj = b0 + lane;
+          if (jj < nR) {
+            const u32 c = S.ctx[jj];
+            cdp += c + 1;
+            const u32 r = B.mod(c);
+            for (u32 jx = r ? B.bs - r : 0u; jx < 32; jx += B.bs) atomicAdd(&S.scratch[jx], 1u);
+          }
+        }
+        __syncwarp();
+        const u64 Cd0 = warp_sum64(cdp);
+        const u32 nj = S.scratch[lane];
+        const u32 Aj = scan_incl(nj);  // cumulative blocks allocated through iteration k+lane
+        // lane-parallel cost of iteration k+lane: D = nR decodes, C_d grows by nR per iteration
+        const u64 Cdj = Cd0 + (u64)lane * nR;
+        const i64 Tj = iter_time_ns(K, 0, 0, 0, nR, Cdj, 0);
+        const i64 tej = t + scan_incl_i64(Tj);
+        const i64 tsj = tej - Tj;
+        // cut: stop before the first iteration that is not quiescent
+        const i64 a_next = arr < n ? __shfl_sync(FULLMASK, wa, arr - win) : INT64_MAX;
+        bool ok = ((u64)Aj <= nfree) && (Aj <= (u32)CAP) && (lane + 1 < rmin);
+        if (lane > 0) {
+          if (P.horizon >= 0 && tsj >= P.horizon) ok = false;
+          if (adm == arr && tsj >= a_next) ok = false;
+        }
+        if (head_mem) {  // blocked by memory at this boundary? (monotone afterwards)
+          const u64 n0 = __shfl_sync(FULLMASK, Aj, 0);
+          const u64 fr = nfree - n0;
+          const bool blocked = ((i64)fr - (i64)need_h < wm) || (RATIO && (total - fr) + need_h > HP.ratio_limit);
+          if (!blocked) ok = false;
+        }
+        const u32 okm = __ballot_sync(FULLMASK, ok);
+        const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+        if (J >= 2) {
+          flush_sched();  // keep the normal-iteration buffer consistent with k jumping ahead
+          const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
+          // requester list ordered by (iteration, slot): bucket cursors = exclusive scan
+          S.scratch[lane] = Aj - nj;
+          __syncwarp();
+          if (Ktot > 0) {
+            const u32 nrep = (32 + B.bs - 1) / B.bs;
+            for (u32 b0 = 0; b0 < nR; b0 += 32) {
+              const u32 jj = b0 + lane;
+              const u32 c = jj < nR ? S.ctx[jj] : 0u;
+              const u32 r = B.mod(c);
+              u32 jx = r ? B.bs - r : 0u;
+              for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
+                const bool v = jj < nR && jx < J;
+                const u32 key = v ? jx : 64u + lane;
+                const u32 peers = __match_any_sync(FULLMASK, key);
+                u32 base = 0;
+                if (v) base = S.scratch[jx];
+                __syncwarp();
+                if (v) {
+                  const u32 e = base + __popc(peers & ltm);
+                  S.req_cum[e] = e + 1;
+                  S.req_pt[e] = jj | (jx << 10) | (B.div(c + jx) << 15);
+                  if ((peers & ltm) == 0u) S.scratch[jx] = base + __popc(peers);
+                }
+                __syncwarp();
+              }
+            }
+            if (!alloc_ordered(S, Ktot, Ktot, bt, btl, k, dig_b, hint, nwords)) {
+              flags |= TOKENSIM_PT_INTERNAL_ERROR;
+              break;
+            }
+          }
+          const u64 blk0 = total - nfree;
+          nfree -= Ktot;
+          // iteration records, digests, counters (lanes j < J)
+          const bool lj = lane < J;
+          const u64 blkj = blk0 + Aj;
+          if (lj) {
+            dig_s += sched_fold(k + lane, tsj, Tj, 0, nR, 0, Cdj, 0, 0, 0, 0, 0, blkj);
+            put_iter(k + lane, tsj, Tj, 0, nR, 0, Cdj, 0, 0, 0, 0, 0, (u32)blkj);
+          }
+          const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
+          const i64 tsl = __shfl_sync(FULLMASK, tsj, J - 1);
+          u64 bt_part = lj ? blkj * (u64)Tj : 0ull;
+          const u64 bns_add = warp_sum64(bt_part);
+          i64 tmax = lj ? Tj : 0;
+#pragma unroll
+          for (u32 o = 16; o; o >>= 1) {
+            const i64 y = __shfl_xor_sync(FULLMASK, tmax, o);
+            tmax = y > tmax ? y : tmax;
+          }
+          // slot updates for J decode iterations
+          for (u32 b0 = 0; b0 < nR; b0 += 32) {
+            const u32 jj = b0 + lane;
+            if (jj < nR) {
+              S.ctx[jj] += J;
+              S.rem[jj] -= J;
+              if (tmax > S.maxgap[jj]) S.maxgap[jj] = tmax;
+              S.last[jj] = tend;
+            }
+          }
+          __syncwarp();
+          // memory trace
+          if (BINNED) {
+            while (true) {
+              const i64 bstart = bin_end - W;
+              i64 ov = 0;
+              bool cnt_here = false;
+              if (lj) {
+                const i64 lo = tsj > bstart ? tsj : bstart;
+                const i64 hi = tej < bin_end ? tej : bin_end;
+                ov = hi - lo;
+                cnt_here = tsj >= bstart && tsj < bin_end;
+              }
+              const u64 add = warp_sum64(ov > 0 ? blkj * (u64)ov : 0ull);
+              const u32 mx = __reduce_max_sync(FULLMASK, ov > 0 ? (u32)blkj : 0u);
+              acc_bns += add;
+              acc_max = max(acc_max, mx);
+              acc_nit += __popc(__ballot_sync(FULLMASK, cnt_here));
+              if (tend > bin_end || tsl >= bin_end) flush_bin();
+              else break;
+            }
+          } else if (FULLT) {
+            if (lj && tn + lane < P.trace_cap) {
+              tokensim_mem_sample s;
+              s.t_ns = tsj;
+              s.dur_ns = Tj;
+              s.block_ns = blkj * (u64)Tj;
+              s.blocks_max = (u32)blkj;
+              s.n_iter = 1;
+              trc[tn + lane] = s;
+            }
+            if (tn + J > P.trace_cap) flags |= TOKENSIM_PT_TRACE_OVERFLOW;
+            tn += J;
+          }
+          const u64 blk_last = blk0 + Ktot;
+          peak = blk_last > peak ? blk_last : peak;
+          bns += bns_add;
+          req_iters += (u64)nR * J;
+          rmin -= J;
+          ff_iters += J;
+          ++ff_runs;
+          t = tend;
+          k += J;
+          continue;
+        }
+        rmin = 0;  // retry only after the next normal commit recomputes it
+      }
+    }
+
+    // ---------------------------------------------------------------- 3. decode reservation
+    // one pass: needing survivors -> requester list (ascending id), sum of c = ctx+1
+    u32 E = 0;
+    u64 cdp = 0, npp = 0, app = 0;
+    for (u32 b0 = 0; b0 < nR; b0 += 32) {
+      const u32 jj = b0 + lane;
+      const u32 c = jj < nR ? S.ctx[jj] : 1u;
+      const bool need = jj < nR && B.mod(c) == 0;
+      if (jj < nR) cdp += c + 1;
+      const u32 bal = __ballot_sync(FULLMASK, need);
+      if (need) {
+        const u32 e = E + __popc(bal & ltm);
+        S.req_cum[e] = e + 1;
+        S.req_pt[e] = jj | (B.div(c) << 15);
+      }
+      E += __popc(bal);
+    }
+    u32 m = 0;
+    u64 swap_out = 0;
+    if ((u64)E > nfree) {
+      // minimal m with sum_{j<=n-m} need_j <= F + sum_{j>n-m} held_j (SURVEY c.4 step 3)
+      u64 Sn = E, Hh = 0;
+      do {
+        ++m;
+        const u32 c = S.ctx[nR - m];
+        Sn -= (B.mod(c) == 0) ? 1 : 0;
+        Hh += B.cdiv(c);
+      } while (Sn > nfree + Hh);
+      u64 csub = 0;
+      for (u32 v = nR - m; v < nR; ++v) {  // victims: latest arrivals (reading A7)
+        const u32 c = S.ctx[v];
+        const u32 held = B.cdiv(c);
+        const u32 slot = S.info[v] & 0xffffu;
+        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, dig_b, hint);
+        nfree += held;
+        csub += c + 1;
+        if (SWAPM) swap_out += (u64)held * HP.block_bytes;
+        __syncwarp();
+        if (lane == 0) {
+          S.info[v] += 1u << 16;
+          if (!SWAPM) S.ctx[v] = 0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) cdp -= csub;
+      E = (u32)Sn;  // the requester list is in position order: victims are its tail
+      nR -= m;
+      nQ += m;
+      npre += m;
+    }
+    const u32 nR3 = nR;
+    u32 Kb = E;
+    nfree -= E;
+    u32 nres = 0, nadm = 0, nrej = 0;
+    u64 swap_in = 0, tokens = nR;
+    if (m == 0) {
+      // 4. resume, head first, stop at the first misfit
+      if (nQ > 0) {
+        u64 cum_need = 0, cum_tok = 0;
+        for (u32 b0 = 0; b0 < nQ; b0 += 32) {
+          const u32 jj = nR3 + b0 + lane;
+          const bool valid = b0 + lane < nQ;
+          u32 need = 0, tok = 0, held0 = 0, c = 0;
+          if (valid) {
+            if (SWAPM) {
+              c = S.ctx[jj];
+              need = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
+              tok = 1;
+              held0 = B.cdiv(c);
+            } else {
+              const u32 id = S.id[jj];
+              const u32 Pq = PR[id] + (OU[id] - S.rem[jj]);  // p + gen
+              need = B.cdiv(Pq);
+              tok = Pq;
+            }
+          }
+          const u32 cn = scan_incl(need), ct = scan_incl(tok);
+          const bool ok = valid && ((u64)nR3 + b0 + lane + 1 <= (u64)mns) &&
+                          (tokens + cum_tok + ct <= (u64)mbt) && ((i64)nfree - (i64)(cum_need + cn) >= wm);
+          const u32 okm = __ballot_sync(FULLMASK, ok);
+          const u32 cnt = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+          if (lane < cnt) {
+            S.req_cum[E + lane] = Kb + cn;
+            S.req_pt[E + lane] = jj;
+            if (SWAPM) {
+              cdp += c + 1;
+            } else {
+              S.ctx[jj] = tok;  // recompute prefill of P = p + gen; ctx after commit
+              npp += tok;
+              app += (u64)tok * (tok + 1) / 2;
+            }
+          }
+          const u64 sw = warp_sum64(lane < cnt ? (u64)held0 : 0ull);
+          if (cnt) {
+            const u32 sn = __shfl_sync(FULLMASK, cn, cnt - 1), stk = __shfl_sync(FULLMASK, ct, cnt - 1);
+            cum_need += sn;
+            cum_tok += stk;
+            Kb += sn;
+            E += cnt;
+            nres += cnt;
+            if (SWAPM) swap_in += sw * HP.block_bytes;
+          }
+          if (cnt < 32) break;
+        }
+        nfree -= cum_need;
+        tokens += cum_tok;
+        nR += nres;
+        nQ -= nres;
+        __syncwarp();
+      }
+      // 5. fresh FCFS admission
+      if (nQ == 0 && (!STATICP || nR == 0)) {
+        while (adm < arr) {
+          const u32 i = adm + lane;
+          const bool valid = i < arr;
+          const u32 p = valid ? PR[i] : 0u;
+          const u32 o = valid ? OU[i] : 0u;
+          const i64 a = valid ? A[i] : 0;
+          const u32 need = B.cdiv(p);
+          const bool rej = valid && (u64)need > HP.cap_fresh;
+          const bool el = valid && !rej;
+          const u32 ce = scan_incl(el ? 1u : 0u);
+          const u32 cneed = scan_incl(el ? need : 0u);
+          const u32 cp = scan_incl(el ? p : 0u);
+          const bool ok = el && ((u64)nR + ce <= (u64)mns) && (tokens + cp <= (u64)mbt) &&
+                          ((i64)nfree - (i64)cneed >= wm) && (!RATIO || (total - nfree) + cneed <= HP.ratio_limit);
+          const u32 failm = __ballot_sync(FULLMASK, el && !ok);
+          const u32 nvalid = min(32u, arr - adm);
+          const u32 stop = failm ? (u32)(__ffs(failm) - 1) : nvalid;
+          const bool take = el && lane < stop;
+          const bool rj = rej && lane < stop;
+          const u32 takem = __ballot_sync(FULLMASK, take);
+          const u32 cnt = __popc(takem);
+          if (cnt) {
+            const u32 rank = __popc(takem & ltm);
+            const u32 slot = alloc_btslots(S.btfree, CAP / 32, take, rank, cnt);
+            if (take) {
+              const u32 pos = nR + rank;
+              S.id[pos] = i;
+              S.ctx[pos] = p;  // fresh prefill of P = p; ctx after commit
+              S.rem[pos] = o;
+              S.info[pos] = slot;
+              S.last[pos] = 0;
+              S.maxgap[pos] = 0;
+              S.arr[pos] = a;
+              S.ttft[pos] = 0;
+              S.req_cum[E + rank] = Kb + cneed;
+              S.req_pt[E + rank] = pos;
+              npp += p;
+              app += (u64)p * (p + 1) / 2;
+            }
+          }
+          if (rj) reinterpret_cast<uint8_t *>(rec + i)[26] = (uint8_t)TOKENSIM_REQ_REJECTED;
+          const u32 nrj = __popc(__ballot_sync(FULLMASK, rj));
+          if (stop) {
+            const u32 sneed = __shfl_sync(FULLMASK, cneed, stop - 1);
+            const u32 sp = __shfl_sync(FULLMASK, cp, stop - 1);
+            nfree -= sneed;
+            Kb += sneed;
+            tokens += sp;
+          }
+          E += cnt;
+          nR += cnt;
+          nadm += cnt;
+          nrej += nrj;
+          adm += stop;
+          __syncwarp();
+          if (stop < nvalid) break;
+        }
+      }
+    }
+    nrej_tot += nrej;
+    // 6. empty batch (every candidate rejected): back to 0 without advancing t
+    if (nR == 0) continue;
+    // block extraction for all requesters of this iteration, in phase order
+    if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, dig_b, hint, nwords)) {
+      flags |= TOKENSIM_PT_INTERNAL_ERROR;
+      break;
+    }
+    // 7. cost: decodes are positions [0, D), prefills [D, nR)
+    const u32 D = nR3 + (SWAPM ? nres : 0u);
+    const u32 Sp = nR - D;
+    const u64 Cd = warp_sum64(cdp);
+    u64 Np = 0, Ap = 0;
+    if (Sp) {
+      Np = warp_sum64(npp);
+      Ap = warp_sum64(app);
+    }
+    const i64 T = iter_time_ns(K, Np, Ap, Sp, D, Cd, swap_out + swap_in);
+    // 8. commit
+    const i64 ts = t, te = t + T;
+    const u64 blocks = total - nfree;
+    u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
+    const u32 fresh0 = nR3 + nres;
+    for (u32 b0 = 0; b0 < nR; b0 += 32) {
+      const u32 jj = b0 + lane;
+      bool fin = false;
+      if (jj < nR) {
+        const u32 r = S.rem[jj] - 1;
+        S.rem[jj] = r;
+        if (jj >= fresh0) {
+          S.ttft[jj] = te - S.arr[jj];
+          S.last[jj] = te;
+        } else {
+          if (jj < D) S.ctx[jj] += 1;
+          const i64 gap = te - S.last[jj];
+          if (gap > S.maxgap[jj]) S.maxgap[jj] = gap;
+          S.last[jj] = te;
+        }
+        fin = r == 0;
+        if (fin) {
+          const u32 id = S.id[jj];
+          const i64 ttft = S.ttft[jj], e2e = te - S.arr[jj], mt = S.maxgap[jj];
+          const u32 np_ = S.info[jj] >> 16;
+          write_record(rec + id, ttft, e2e, mt, np_, TOKENSIM_REQ_FINISHED, (u32)k);
+          u64 h = FOLD_INIT;
+          h = mix64(h ^ (u64)id);
+          h = mix64(h ^ (u64)ttft);
+          h = mix64(h ^ (u64)e2e);
+          h = mix64(h ^ (u64)mt);
+          h = mix64(h ^ (u64)np_);
+          h = mix64(h ^ k);
+          dig_r += h;
+        } else {
+          rmin_l = min(rmin_l, r);
+        }
+      }
+      u32 fm = __ballot_sync(FULLMASK, fin);
+      __syncwarp();
+      if (fm && first_fin == 0xffffffffu) first_fin = b0 + (u32)(__ffs(fm) - 1);
+      nfin += __popc(fm);
+      while (fm) {
+        const u32 l = (u32)(__ffs(fm) - 1);
+        fm &= fm - 1;
+        const u32 pos = b0 + l;
+        const u32 c = S.ctx[pos];
+        const u32 held = B.cdiv(c);
+        const u32 slot = S.info[pos] & 0xffffu;
+        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, dig_b, hint);
+        nfree += held;
+        if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
+      }
+    }
+    rmin = __reduce_min_sync(FULLMASK, rmin_l);
+    __syncwarp();
+    req_iters += nR;
+    if (nfin) {
+      // stable compaction of R u Q, dropping finished entries (rem == 0 within R)
+      const u32 len = nR + nQ;
+      u32 out = first_fin;
+      for (u32 b0 = first_fin; b0 < len; b0 += 32) {
+        const u32 jj = b0 + lane;
+        const bool valid = jj < len;
+        u32 vid = 0, vctx = 0, vrem = 0, vinfo = 0;
+        i64 vl = 0, vm = 0, va = 0, vt = 0;
+        if (valid) {
+          vid = S.id[jj];
+          vctx = S.ctx[jj];
+          vrem = S.rem[jj];
+          vinfo = S.info[jj];
+          vl = S.last[jj];
+          vm = S.maxgap[jj];
+          va = S.arr[jj];
+          vt = S.ttft[jj];
+        }
+        const bool keep = valid && vrem != 0;
+        const u32 km = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) {
+          const u32 d = out + __popc(km & ltm);
+          S.id[d] = vid;
+          S.ctx[d] = vctx;
+          S.rem[d] = vrem;
+          S.info[d] = vinfo;
+          S.last[d] = vl;
+          S.maxgap[d] = vm;
+          S.arr[d] = va;
+          S.ttft[d] = vt;
+        }
+        __syncwarp();
+        out += __popc(km);
+      }
+      nR -= nfin;
+      nfin_tot += nfin;
+      last_fin = te;
+    }
+    if (nR == 0) rmin = 0;
+    // schedule digest fields (buffered; folded 32 iterations at a time)
+    if (lane == (u32)(k & 31)) {
+      b_k = (u32)k;
+      b_t = ts;
+      b_T = T;
+      b_spd = Sp | (D << 16);
+      b_np = Np;
+      b_cd = Cd;
+      b_mres = m | (nres << 16);
+      b_adfin = nadm | (nfin << 16);
+      b_rej = nrej;
+      b_blk = (u32)blocks;
+      b_valid = true;
+    }
+    if ((k & 31) == 31) flush_sched();
+    peak = blocks > peak ? blocks : peak;
+    bns += blocks * (u64)T;
+    swo_tot += swap_out;
+    swi_tot += swap_in;
+    if (BINNED) {
+      while (bin_end <= ts) flush_bin();
+      ++acc_nit;
+      i64 s = ts;
+      while (te > bin_end) {
+        if (bin_end > s) {
+          acc_bns += blocks * (u64)(bin_end - s);
+          acc_max = max(acc_max, (u32)blocks);
+        }
+        s = bin_end;
+        flush_bin();
+      }
+      if (te > s) {
+        acc_bns += blocks * (u64)(te - s);
+        acc_max = max(acc_max, (u32)blocks);
+      }
+    } else if (FULLT) {
+      if (tn < P.trace_cap) {
+        if (lane == 0) {
+          tokensim_mem_sample s;
+          s.t_ns = ts;
+          s.dur_ns = T;
+          s.block_ns = blocks * (u64)T;
+          s.blocks_max = (u32)blocks;
+          s.n_iter = 1;
+          trc[tn] = s;
+        }
+      } else {
+        flags |= TOKENSIM_PT_TRACE_OVERFLOW;
+      }
+      ++tn;
+    }
+    t = te;
+    ++k;
+  }
+  flush_sched();
+  if (BINNED) {
+    while ((i64)bin * W < t) flush_bin();
+  }
+  // unfinished requests still in R u Q: first-token latency and preemption count
+  for (u32 x = lane; x < nR + nQ; x += 32) {
+    const u32 id = S.id[x];
+    write_record(rec + id, S.ttft[x], 0, 0, S.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);
+  }
+  dig_s = warp_sum64(dig_s);
+  dig_b = warp_sum64(dig_b);
+  dig_r = warp_sum64(dig_r);
+  if (lane == 0) {
+    SimStats st;
+    st.flags = flags | ((nrej_tot == n) ? (u32)TOKENSIM_PT_ALL_REJECTED : 0u);
+    st.pad = 0;
+    st.n_finished = nfin_tot;
+    st.n_rejected = nrej_tot;
+    st.n_iterations = k;
+    st.n_req_iters = req_iters;
+    st.n_preempt = npre;
+    st.swap_out = swo_tot;
+    st.swap_in = swi_tot;
+    st.last_finish = last_fin;
+    st.t_final = t;
+    st.sched_d = dig_s;
+    st.block_d = dig_b;
+    st.req_d = dig_r;
+    st.total_blocks = total;
+    st.peak_blocks = peak;
+    st.block_ns_sum = bns;
+    st.trace_n[0] = min(tn, P.trace_cap);
+    st.trace_n[1] = 0;
+    st.iter_n = min(k, P.it_cap);
+    st.n_transfers = 0;
+    st.transfer_bytes = 0;
+    st.ff_iters = ff_iters;
+    st.ff_runs = ff_runs;
+    st.reserved = 0;
+    P.stats[j] = st;
+  }
+  __syncwarp();
+}
+
+template <int CAP>
+__global__ void __launch_bounds__(128) sim_kernel(SweepParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const u32 lane = lane_id(), wib = threadIdx.x >> 5;
+  const size_t per_warp = smem_per_warp_bytes(CAP, P.nwords_max);
+  const WarpSmem S = carve(smem_raw + wib * per_warp, CAP);
+  const u32 gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
+  u32 *bt = P.bt + (size_t)gwarp * 2 * CAP * P.bt_len;
+  while (true) {
+    u32 qi = 0;
+    if (lane == 0) qi = atomicAdd(P.queue, 1u);
+    qi = __shfl_sync(FULLMASK, qi, 0);
+    if ((u64)qi >= P.n_run) break;
+    const u64 j = P.order[qi];
+    simulate_unified<CAP>(P, j, S, bt);
+  }
+}
+
+template <int CAP>
+static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  sim_kernel<CAP><<<blocks, wpb * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sim(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
+  switch (cap) {
+    case 32: return launch_sim_t<32>(p, wpb, blocks, smem, st);
+    case 256: return launch_sim_t<256>(p, wpb, blocks, smem, st);
+    case 1024: return launch_sim_t<1024>(p, wpb, blocks, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int CAP>
+static cudaError_t occ_t(int wpb, size_t smem, int *b) {
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP>, wpb * 32, smem);
+}
+cudaError_t sim_occupancy(int cap, int wpb, size_t smem, int *b) {
+  switch (cap) {
+    case 32: return occ_t<32>(wpb, smem, b);
+    case 256: return occ_t<256>(wpb, smem, b);
+    case 1024: return occ_t<1024>(wpb, smem, b);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ts

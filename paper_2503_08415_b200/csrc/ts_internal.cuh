@@ -41,6 +41,8 @@ struct DevHP {
 
 struct DevPol {
   u32 kind, preempt, mns, mbt, bs, wm;
+  u32 bs_sh;  // log2(bs) if bs is a power of two, else 0xffffffff
+  u32 pad;
 };
 
 // Per point, written once by the simulation kernel.
@@ -53,7 +55,8 @@ struct SimStats {
   u64 trace_n[2];
   u64 iter_n;
   u64 n_transfers, transfer_bytes;
-  u64 reserved[3];
+  u64 ff_iters, ff_runs;  // iterations committed by fast-forward stretches, stretch count
+  u64 reserved;
 };
 
 struct SweepParams {
@@ -96,6 +99,7 @@ struct SweepParams {
   i64 horizon, slo_ttft_ns, slo_mtpot_ns;
   double pd_link_inv;  // 1 / pd_link_bw
   u64 *scratch;        // summary keys when n_req exceeds the shared-memory key buffer
+  u32 ff_enable, pad1; // time-parallel evaluation of quiescent decode stretches (H3)
 };
 
 // point -> grid coordinates (row-major)

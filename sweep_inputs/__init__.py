@@ -139,6 +139,7 @@ class Options:
     slo_ttft_s: float = 15.0
     slo_mtpot_s: float = 0.3
     horizon_ns: int = -1
+    fast_forward: bool = True          # CUDA path only: time-parallel quiescent stretches
 
 
 @dataclass(frozen=True)

@@ -109,7 +109,8 @@ def _micro(rng):
                     trace_output=o.tolist(), prompt_table=None, output_table=None)
     mode = si.FULL if rng.random() < 0.5 else si.BINNED
     opts = si.Options(trace_mode=mode, trace_bin_ns=int(rng.choice([10_000_000, 1_000_000_000])),
-                      iteration_trace_cap=1 << 16, horizon_ns=int(rng.choice([-1, -1, -1, 500_000_000])))
+                      iteration_trace_cap=1 << 16, horizon_ns=int(rng.choice([-1, -1, -1, 500_000_000])),
+                      fast_forward=bool(rng.random() < 0.8))
     return si.SweepConfig("micro", model, [hw], [pol], w, opts)
 
 
@@ -183,3 +184,18 @@ def test_sharegpt_builtin_equals_table(api):
     a = run_gpu(api, cfg).summaries()
     b = run_gpu(api, replace(cfg, workload=replace(cfg.workload, len_dist="sharegpt_synth_v1"))).summaries()
     assert a.tobytes() == b.tobytes()
+
+
+def test_fast_forward_is_bit_identical(api):
+    """Time-parallel evaluation of quiescent stretches must not change a single
+    bit of any result: compare full summaries, records and traces with it switched off."""
+    for cfg in (si.c2(), replace(si.c1(), options=si.Options(trace_mode=si.FULL, iteration_trace_cap=1 << 16)),
+                replace(si.c1(), options=si.Options(trace_bin_ns=7_000_000))):
+        on = run_gpu(api, cfg)
+        off = run_gpu(api, replace(cfg, options=replace(cfg.options, fast_forward=False)))
+        assert on.summaries().tobytes() == off.summaries().tobytes()
+        for p in range(0, cfg.num_points, 13):
+            assert on.records(p).tobytes() == off.records(p).tobytes()
+            assert on.mem_trace(p).tobytes() == off.mem_trace(p).tobytes()
+        if cfg.options.iteration_trace_cap:
+            assert on.iteration_trace(0).tobytes() == off.iteration_trace(0).tobytes()
