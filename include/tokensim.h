@@ -266,6 +266,13 @@ typedef struct {
 } tokensim_run_info;
 tokensim_status tokensim_get_run_info(const tokensim_sweep *h, tokensim_run_info *out);
 
+/* Per-point execution profile of the last run (observability): iterations simulated, how
+ * many of them were committed by time-parallel fast-forward stretches, and SM cycles. */
+typedef struct {
+  uint64_t n_iterations, ff_iterations, ff_stretches, sm_cycles;
+} tokensim_point_profile;
+tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t point, tokensim_point_profile *out);
+
 /* Message of the last failing call on h (NULL: the calling thread's last create error). */
 const char *tokensim_last_error(const tokensim_sweep *h);
 void tokensim_sweep_destroy(tokensim_sweep *h);

@@ -67,6 +67,10 @@ class Options(C.Structure):
                 ("slo_ttft_s", f64), ("slo_mtpot_s", f64), ("horizon_ns", i64), ("flags", u32)]
 
 
+class PointProfile(C.Structure):
+    _fields_ = [("n_iterations", u64), ("ff_iterations", u64), ("ff_stretches", u64), ("sm_cycles", u64)]
+
+
 class RunInfo(C.Structure):
     _fields_ = [("ms_workload", f64), ("ms_sim", f64), ("ms_summary", f64), ("n_launches", u32),
                 ("sim_blocks", u32), ("sim_warps_per_block", u32), ("smem_per_warp", u32), ("n_run", u64),
@@ -102,6 +106,7 @@ EXPORTS = [
     "tokensim_get_summaries", "tokensim_get_summaries_device", "tokensim_import_summaries",
     "tokensim_get_request_records", "tokensim_get_iteration_trace", "tokensim_get_workload",
     "tokensim_last_error", "tokensim_sweep_destroy", "tokensim_version", "tokensim_get_run_info",
+    "tokensim_get_point_profile",
 ]
 
 _lib = None
@@ -152,5 +157,7 @@ def lib():
     L.tokensim_version.restype = C.c_char_p
     L.tokensim_get_run_info.argtypes = [vp, C.POINTER(RunInfo)]
     L.tokensim_get_run_info.restype = C.c_int
+    L.tokensim_get_point_profile.argtypes = [vp, u64, C.POINTER(PointProfile)]
+    L.tokensim_get_point_profile.restype = C.c_int
     _lib = L
     return L

@@ -229,6 +229,11 @@ class Sweep:
         self._check(self._L.tokensim_get_run_info(self._h, C.byref(ri)), "get_run_info")
         return {n: getattr(ri, n) for n, _ in T.RunInfo._fields_}
 
+    def point_profile(self, point: int) -> dict:
+        pp = T.PointProfile()
+        self._check(self._L.tokensim_get_point_profile(self._h, point, C.byref(pp)), "get_point_profile")
+        return {n: getattr(pp, n) for n, _ in T.PointProfile._fields_}
+
     def workload(self, point: int):
         n = self._n_req
         a = np.zeros(n, np.int64)

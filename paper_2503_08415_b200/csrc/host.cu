@@ -818,6 +818,22 @@ tokensim_status tokensim_get_workload(const tokensim_sweep *hc, uint64_t point, 
   return TOKENSIM_OK;
 }
 
+tokensim_status tokensim_get_point_profile(const tokensim_sweep *hc, uint64_t point, tokensim_point_profile *out) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h || !out) return TOKENSIM_E_INVALID;
+  u64 j;
+  tokensim_status s = local_index(h, point, &j);
+  if (s != TOKENSIM_OK) return fail(h, s, "get_point_profile: point not run by this handle");
+  if ((s = sync_run(h)) != TOKENSIM_OK) return s;
+  SimStats st;
+  if ((s = copy_d2h(h, &st, h->P.stats + j, sizeof st)) != TOKENSIM_OK) return s;
+  out->n_iterations = st.n_iterations;
+  out->ff_iterations = st.ff_iters;
+  out->ff_stretches = st.ff_runs;
+  out->sm_cycles = st.cycles;
+  return TOKENSIM_OK;
+}
+
 tokensim_status tokensim_get_run_info(const tokensim_sweep *hc, tokensim_run_info *out) {
   tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
   if (!h || !out) return TOKENSIM_E_INVALID;

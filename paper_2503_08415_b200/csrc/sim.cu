@@ -316,6 +316,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const u32 mns = PL.mns, mbt = PL.mbt;
   const i64 wm = (i64)PL.wm;
   const bool ff_on = P.ff_enable != 0;
+  const long long clk0 = clock64();
 
   // ---- init: records, bitmap, slot pool
   {
@@ -341,11 +342,12 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   i64 last_fin = 0;
   u32 flags = 0;
   u32 hd_idx = 0xffffffffu, hd_p = 0;  // cached prompt length of the fresh-queue head
-  // sched-field buffer: lane (k mod 32) holds normal iteration k's fields until the flush
+  // sched-field buffer: lane nbuf holds a normal iteration's fields until 32 are buffered
   i64 b_t = 0, b_T = 0;
-  u64 b_np = 0, b_cd = 0;
-  u32 b_k = 0, b_blk = 0, b_spd = 0, b_mres = 0, b_adfin = 0, b_rej = 0;
+  u64 b_np = 0, b_cd = 0, b_k = 0;
+  u32 b_blk = 0, b_spd = 0, b_mres = 0, b_adfin = 0, b_rej = 0;
   bool b_valid = false;
+  u32 nbuf = 0;
   auto put_iter = [&](u64 kk, i64 ts_, i64 T_, u32 Sp_, u32 D_, u64 Np_, u64 Cd_, u32 m_, u32 nres_, u32 nadm_,
                       u32 nrej_, u32 nfin_, u32 blk_) {
     if (kk < P.it_cap) {
@@ -406,9 +408,18 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     acc_nit = 0;
   };
 
-  // arrival window: lane l holds A[win + l]
+  // request window: lane l holds arrival/prompt/output of request win + l
   u32 win = 0;
-  i64 wa = lane < n ? A[lane] : INT64_MAX;
+  i64 wa = INT64_MAX;
+  u32 wp = 0, wo = 0;
+  auto load_win = [&](u32 base) {
+    win = base;
+    const u32 i = base + lane;
+    wa = i < n ? A[i] : INT64_MAX;
+    wp = i < n ? PR[i] : 0u;
+    wo = i < n ? OU[i] : 0u;
+  };
+  load_win(0);
 
   while (true) {
     // 0. termination
@@ -419,10 +430,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     }
     // 1. ingest: a_i <= t become visible at this boundary
     while (arr < n) {
-      if (arr >= win + 32) {
-        win = arr;
-        wa = win + lane < n ? A[win + lane] : INT64_MAX;
-      }
+      if (arr >= win + 32) load_win(arr);
       const u32 m = __ballot_sync(FULLMASK, (win + lane >= arr) && (wa <= t));
       arr += __popc(m);
       if (arr < win + 32) break;
@@ -434,37 +442,62 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     }
 
     // ---------------------------------------------------------------- fast-forward (H3)
-    if (ff_on && nQ == 0 && nR > 0 && rmin >= 3) {
-      // Fresh admission must be impossible for the whole stretch: STATIC with R != {} never
-      // admits; an empty fresh queue is cut at the next arrival; a blocked head stays blocked
-      // while R is frozen and the free count only falls (c.4 step 5 is monotone).
-      bool quiet = true, head_mem = false;
+    if (ff_on && nR > 0 && rmin >= 2) {
+      // The stretch must admit nothing and resume nothing.  With Q != {} fresh admission is
+      // off (c.4 step 5) and a Q head that cannot resume now cannot resume later (R frozen,
+      // free count only falls).  With Q = {}: STATIC never admits while R != {}; an empty fresh
+      // queue is cut at the next arrival; a blocked fresh head stays blocked (step 5 is
+      // monotone in the free count and the allocated count).
+      bool quiet = true, mem_check = false;
       u32 need_h = 0;
-      if (!STATICP && adm < arr) {
+      bool ratio_h = false;
+      if (nQ > 0) {
+        const u32 x = nR;  // Q head position
+        u32 tokq;
+        if (SWAPM) {
+          const u32 c = S.ctx[x];
+          need_h = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
+          tokq = 1;
+        } else {
+          const u32 id = S.id[x];
+          tokq = PR[id] + (OU[id] - S.rem[x]);
+          need_h = B.cdiv(tokq);
+        }
+        if (!((u64)nR + 1 > mns || (u64)nR + tokq > mbt)) mem_check = true;
+      } else if (!STATICP && adm < arr) {
         if (hd_idx != adm) {
           hd_idx = adm;
-          hd_p = PR[adm];
+          const u32 off = adm - win;
+          const u32 pw = __shfl_sync(FULLMASK, wp, off & 31u);
+          hd_p = (adm >= win && off < 32) ? pw : PR[adm];
         }
         need_h = B.cdiv(hd_p);
         if ((u64)need_h > HP.cap_fresh) quiet = false;  // would be rejected at this boundary
-        else if (!((u64)nR + 1 > mns || (u64)nR + hd_p > mbt)) head_mem = true;
+        else if (!((u64)nR + 1 > mns || (u64)nR + hd_p > mbt)) {
+          mem_check = true;
+          ratio_h = RATIO;
+        }
       }
       if (quiet) {
-        // pass over R: C_d(0), needs histogram by iteration offset (lane j <-> iteration k+j)
+        // pass over R: C_d(0), min rem and its multiplicity, needs histogram by iteration
+        // offset (lane j <-> iteration k+j)
         S.scratch[lane] = 0;
         __syncwarp();
         u64 cdp = 0;
+        u32 rmn = 0xffffffffu;
         for (u32 b0 = 0; b0 < nR; b0 += 32) {
           const u32 jj = b0 + lane;
           if (jj < nR) {
             const u32 c = S.ctx[jj];
             cdp += c + 1;
+            rmn = min(rmn, S.rem[jj]);
             const u32 r = B.mod(c);
             for (u32 jx = r ? B.bs - r : 0u; jx < 32; jx += B.bs) atomicAdd(&S.scratch[jx], 1u);
           }
         }
         __syncwarp();
         const u64 Cd0 = warp_sum64(cdp);
+        const u32 rm = __reduce_min_sync(FULLMASK, rmn);
         const u32 nj = S.scratch[lane];
         const u32 Aj = scan_incl(nj);  // cumulative blocks allocated through iteration k+lane
         // lane-parallel cost of iteration k+lane: D = nR decodes, C_d grows by nR per iteration
@@ -472,23 +505,23 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const i64 Tj = iter_time_ns(K, 0, 0, 0, nR, Cdj, 0);
         const i64 tej = t + scan_incl_i64(Tj);
         const i64 tsj = tej - Tj;
-        // cut: stop before the first iteration that is not quiescent
-        const i64 a_next = arr < n ? __shfl_sync(FULLMASK, wa, arr - win) : INT64_MAX;
-        bool ok = ((u64)Aj <= nfree) && (Aj <= (u32)CAP) && (lane + 1 < rmin);
+        // cut: the stretch is the longest prefix of iterations that stay quiescent; the
+        // last one may finish requests (rem reaching 0), no earlier one may
+        // (warp collectives stay outside lane-dependent branches)
+        const i64 a_next = __shfl_sync(FULLMASK, wa, (arr - win) & 31u);
+        bool ok = ((u64)Aj <= nfree) && (Aj <= (u32)CAP) && (lane < rm);
         if (lane > 0) {
           if (P.horizon >= 0 && tsj >= P.horizon) ok = false;
-          if (adm == arr && tsj >= a_next) ok = false;
+          if (nQ == 0 && adm == arr && arr < n && tsj >= a_next) ok = false;
         }
-        if (head_mem) {  // blocked by memory at this boundary? (monotone afterwards)
-          const u64 n0 = __shfl_sync(FULLMASK, Aj, 0);
-          const u64 fr = nfree - n0;
-          const bool blocked = ((i64)fr - (i64)need_h < wm) || (RATIO && (total - fr) + need_h > HP.ratio_limit);
+        if (mem_check) {  // head blocked by memory at this boundary? (then for the whole stretch)
+          const u64 fr = nfree - (u64)__shfl_sync(FULLMASK, Aj, 0);
+          const bool blocked = ((i64)fr - (i64)need_h < wm) || (ratio_h && (total - fr) + need_h > HP.ratio_limit);
           if (!blocked) ok = false;
         }
         const u32 okm = __ballot_sync(FULLMASK, ok);
         const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
         if (J >= 2) {
-          flush_sched();  // keep the normal-iteration buffer consistent with k jumping ahead
           const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
           // requester list ordered by (iteration, slot): bucket cursors = exclusive scan
           S.scratch[lane] = Aj - nj;
@@ -523,34 +556,70 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           }
           const u64 blk0 = total - nfree;
           nfree -= Ktot;
-          // iteration records, digests, counters (lanes j < J)
-          const bool lj = lane < J;
-          const u64 blkj = blk0 + Aj;
-          if (lj) {
-            dig_s += sched_fold(k + lane, tsj, Tj, 0, nR, 0, Cdj, 0, 0, 0, 0, 0, blkj);
-            put_iter(k + lane, tsj, Tj, 0, nR, 0, Cdj, 0, 0, 0, 0, 0, (u32)blkj);
-          }
+          const u64 klast = k + J - 1;
+          // slot updates for J decode iterations; requests reaching rem == 0 finish in the last
           const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
           const i64 tsl = __shfl_sync(FULLMASK, tsj, J - 1);
-          u64 bt_part = lj ? blkj * (u64)Tj : 0ull;
-          const u64 bns_add = warp_sum64(bt_part);
+          const bool lj = lane < J;
           i64 tmax = lj ? Tj : 0;
 #pragma unroll
           for (u32 o = 16; o; o >>= 1) {
             const i64 y = __shfl_xor_sync(FULLMASK, tmax, o);
             tmax = y > tmax ? y : tmax;
           }
-          // slot updates for J decode iterations
+          u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
           for (u32 b0 = 0; b0 < nR; b0 += 32) {
             const u32 jj = b0 + lane;
+            bool fin = false;
             if (jj < nR) {
+              const u32 r = S.rem[jj] - J;
+              S.rem[jj] = r;
               S.ctx[jj] += J;
-              S.rem[jj] -= J;
-              if (tmax > S.maxgap[jj]) S.maxgap[jj] = tmax;
+              const i64 mg = tmax > S.maxgap[jj] ? tmax : S.maxgap[jj];
+              S.maxgap[jj] = mg;
               S.last[jj] = tend;
+              fin = r == 0;
+              if (fin) {
+                const u32 id = S.id[jj];
+                const i64 ttft = S.ttft[jj], e2e = tend - S.arr[jj];
+                const u32 np_ = S.info[jj] >> 16;
+                write_record(rec + id, ttft, e2e, mg, np_, TOKENSIM_REQ_FINISHED, (u32)klast);
+                u64 h = FOLD_INIT;
+                h = mix64(h ^ (u64)id);
+                h = mix64(h ^ (u64)ttft);
+                h = mix64(h ^ (u64)e2e);
+                h = mix64(h ^ (u64)mg);
+                h = mix64(h ^ (u64)np_);
+                h = mix64(h ^ klast);
+                dig_r += h;
+              } else {
+                rmin_l = min(rmin_l, r);
+              }
+            }
+            u32 fm = __ballot_sync(FULLMASK, fin);
+            __syncwarp();
+            if (fm && first_fin == 0xffffffffu) first_fin = b0 + (u32)(__ffs(fm) - 1);
+            nfin += __popc(fm);
+            while (fm) {
+              const u32 l = (u32)(__ffs(fm) - 1);
+              fm &= fm - 1;
+              const u32 pos = b0 + l;
+              const u32 held = B.cdiv(S.ctx[pos]);
+              const u32 slot = S.info[pos] & 0xffffu;
+              free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, dig_b, hint);
+              nfree += held;
+              if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
             }
           }
           __syncwarp();
+          // iteration records, digests, counters (lanes j < J)
+          const u64 blkj = blk0 + Aj;
+          if (lj) {
+            const u32 nf = lane == J - 1 ? nfin : 0u;
+            dig_s += sched_fold(k + lane, tsj, Tj, 0, nR, 0, Cdj, 0, 0, 0, 0, nf, blkj);
+            put_iter(k + lane, tsj, Tj, 0, nR, 0, Cdj, 0, 0, 0, 0, nf, (u32)blkj);
+          }
+          const u64 bns_add = warp_sum64(lj ? blkj * (u64)Tj : 0ull);
           // memory trace
           if (BINNED) {
             while (true) {
@@ -573,13 +642,13 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             }
           } else if (FULLT) {
             if (lj && tn + lane < P.trace_cap) {
-              tokensim_mem_sample s;
-              s.t_ns = tsj;
-              s.dur_ns = Tj;
-              s.block_ns = blkj * (u64)Tj;
-              s.blocks_max = (u32)blkj;
-              s.n_iter = 1;
-              trc[tn + lane] = s;
+              tokensim_mem_sample sm;
+              sm.t_ns = tsj;
+              sm.dur_ns = Tj;
+              sm.block_ns = blkj * (u64)Tj;
+              sm.blocks_max = (u32)blkj;
+              sm.n_iter = 1;
+              trc[tn + lane] = sm;
             }
             if (tn + J > P.trace_cap) flags |= TOKENSIM_PT_TRACE_OVERFLOW;
             tn += J;
@@ -588,15 +657,54 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           peak = blk_last > peak ? blk_last : peak;
           bns += bns_add;
           req_iters += (u64)nR * J;
-          rmin -= J;
+          if (nfin) {
+            const u32 len = nR + nQ;
+            u32 out = first_fin;
+            for (u32 b0 = first_fin; b0 < len; b0 += 32) {
+              const u32 jj = b0 + lane;
+              const bool valid = jj < len;
+              u32 vid = 0, vctx = 0, vrem = 0, vinfo = 0;
+              i64 vl = 0, vm = 0, va = 0, vt = 0;
+              if (valid) {
+                vid = S.id[jj];
+                vctx = S.ctx[jj];
+                vrem = S.rem[jj];
+                vinfo = S.info[jj];
+                vl = S.last[jj];
+                vm = S.maxgap[jj];
+                va = S.arr[jj];
+                vt = S.ttft[jj];
+              }
+              const bool keep = valid && vrem != 0;
+              const u32 km = __ballot_sync(FULLMASK, keep);
+              __syncwarp();
+              if (keep) {
+                const u32 d = out + __popc(km & ltm);
+                S.id[d] = vid;
+                S.ctx[d] = vctx;
+                S.rem[d] = vrem;
+                S.info[d] = vinfo;
+                S.last[d] = vl;
+                S.maxgap[d] = vm;
+                S.arr[d] = va;
+                S.ttft[d] = vt;
+              }
+              __syncwarp();
+              out += __popc(km);
+            }
+            nR -= nfin;
+            nfin_tot += nfin;
+            last_fin = tend;
+          }
+          rmin = nR ? __reduce_min_sync(FULLMASK, rmin_l) : 0u;
           ff_iters += J;
           ++ff_runs;
           t = tend;
           k += J;
           continue;
         }
-        rmin = 0;  // retry only after the next normal commit recomputes it
       }
+      rmin = 0;  // retry only after the next normal commit recomputes it
     }
 
     // ---------------------------------------------------------------- 3. decode reservation
@@ -714,9 +822,20 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         while (adm < arr) {
           const u32 i = adm + lane;
           const bool valid = i < arr;
-          const u32 p = valid ? PR[i] : 0u;
-          const u32 o = valid ? OU[i] : 0u;
-          const i64 a = valid ? A[i] : 0;
+          const u32 off = i - win;
+          const bool inw = i >= win && off < 32;
+          u32 p = __shfl_sync(FULLMASK, wp, off & 31u);
+          u32 o = __shfl_sync(FULLMASK, wo, off & 31u);
+          i64 a = __shfl_sync(FULLMASK, wa, off & 31u);
+          if (!valid) {
+            p = 0;
+            o = 0;
+            a = 0;
+          } else if (!inw) {
+            p = PR[i];
+            o = OU[i];
+            a = A[i];
+          }
           const u32 need = B.cdiv(p);
           const bool rej = valid && (u64)need > HP.cap_fresh;
           const bool el = valid && !rej;
@@ -887,8 +1006,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     }
     if (nR == 0) rmin = 0;
     // schedule digest fields (buffered; folded 32 iterations at a time)
-    if (lane == (u32)(k & 31)) {
-      b_k = (u32)k;
+    if (lane == nbuf) {
+      b_k = k;
       b_t = ts;
       b_T = T;
       b_spd = Sp | (D << 16);
@@ -900,7 +1019,10 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       b_blk = (u32)blocks;
       b_valid = true;
     }
-    if ((k & 31) == 31) flush_sched();
+    if (++nbuf == 32) {
+      flush_sched();
+      nbuf = 0;
+    }
     peak = blocks > peak ? blocks : peak;
     bns += blocks * (u64)T;
     swo_tot += swap_out;
@@ -978,7 +1100,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     st.transfer_bytes = 0;
     st.ff_iters = ff_iters;
     st.ff_runs = ff_runs;
-    st.reserved = 0;
+    st.cycles = (u64)(clock64() - clk0);
     P.stats[j] = st;
   }
   __syncwarp();

@@ -56,7 +56,7 @@ struct SimStats {
   u64 iter_n;
   u64 n_transfers, transfer_bytes;
   u64 ff_iters, ff_runs;  // iterations committed by fast-forward stretches, stretch count
-  u64 reserved;
+  u64 cycles;             // SM clock cycles the warp spent on this point
 };
 
 struct SweepParams {

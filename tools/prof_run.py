@@ -29,3 +29,22 @@ for _ in range(a.reps):
     print(a.config, "points", len(s), "req-its", int(s["n_request_iterations"].sum()),
           "iters max", int(s["n_iterations"].max()), "sim ms %.3f" % info["ms_sim"],
           "grid", info["sim_blocks"], "x", info["sim_warps_per_block"], "smem/warp", info["smem_per_warp"])
+if os.environ.get("PROFILE_POINTS"):
+    import numpy as np
+    prof = [sw.point_profile(p) for p in range(end)]
+    it = np.array([x["n_iterations"] for x in prof], dtype=np.float64)
+    ff = np.array([x["ff_iterations"] for x in prof], dtype=np.float64)
+    st = np.array([x["ff_stretches"] for x in prof], dtype=np.float64)
+    cy = np.array([x["sm_cycles"] for x in prof], dtype=np.float64)
+    ri = s["n_request_iterations"].astype(np.float64)
+    normal = it - ff
+    print("points", end, "sum cycles %.3e max %.3e" % (cy.sum(), cy.max()),
+          "ff frac %.3f" % (ff.sum() / it.sum()), "avg stretch %.1f" % (ff.sum() / max(1, st.sum())))
+    # least-squares split of cycles into per-normal-iteration, per-stretch and per-request-iteration costs
+    X = np.stack([normal, st, ri], 1)
+    coef, *_ = np.linalg.lstsq(X, cy, rcond=None)
+    print("cycles ~ %.0f/normal-iter + %.0f/stretch + %.2f/req-iter" % tuple(coef))
+    order = np.argsort(-cy)[:8]
+    for p in order:
+        print("  point", p, "cycles %.3e" % cy[p], "iters", int(it[p]), "ff", int(ff[p]), "stretches", int(st[p]),
+              "req-its", int(ri[p]), "preempt", int(s["n_preemptions"][p]), "peak", int(s["peak_blocks"][p]))
