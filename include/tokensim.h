@@ -270,6 +270,10 @@ tokensim_status tokensim_get_run_info(const tokensim_sweep *h, tokensim_run_info
  * many of them were committed by time-parallel fast-forward stretches, and SM cycles. */
 typedef struct {
   uint64_t n_iterations, ff_iterations, ff_stretches, sm_cycles;
+  uint64_t cycles_ff, cycles_ff_failed, cycles_normal;  /* split of sm_cycles by path */
+  uint64_t stretch_phase_cycles[8];  /* inside successful stretches: scan of R / cost + cut /
+                                        block allocation / slot updates + finishes / digests /
+                                        memory trace / compaction / bookkeeping             */
 } tokensim_point_profile;
 tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t point, tokensim_point_profile *out);
 

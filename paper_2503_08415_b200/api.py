@@ -232,7 +232,9 @@ class Sweep:
     def point_profile(self, point: int) -> dict:
         pp = T.PointProfile()
         self._check(self._L.tokensim_get_point_profile(self._h, point, C.byref(pp)), "get_point_profile")
-        return {n: getattr(pp, n) for n, _ in T.PointProfile._fields_}
+        d = {n: getattr(pp, n) for n, _ in T.PointProfile._fields_}
+        d["stretch_phase_cycles"] = list(d["stretch_phase_cycles"])
+        return d
 
     def workload(self, point: int):
         n = self._n_req

@@ -25,10 +25,13 @@ __device__ __forceinline__ u32 scan_incl(u32 x) {
   }
   return x;
 }
+// Exact wrapping 64-bit warp sum with three 32-bit REDUX ops: split into 21/21/22-bit
+// digits (each digit sum over 32 lanes stays below 2^27) and recombine mod 2^64.
 __device__ __forceinline__ u64 warp_sum64(u64 x) {
-#pragma unroll
-  for (u32 o = 16; o; o >>= 1) x += __shfl_xor_sync(FULLMASK, x, o);
-  return x;
+  const u32 a = __reduce_add_sync(FULLMASK, (u32)(x & 0x1FFFFFull));
+  const u32 b = __reduce_add_sync(FULLMASK, (u32)((x >> 21) & 0x1FFFFFull));
+  const u32 c = __reduce_add_sync(FULLMASK, (u32)(x >> 42));
+  return (u64)a + ((u64)b << 21) + ((u64)c << 42);
 }
 __device__ __forceinline__ u64 shfl64(u64 x, u32 src) { return __shfl_sync(FULLMASK, x, src); }
 __device__ __forceinline__ i64 shfl64i(i64 x, u32 src) { return __shfl_sync(FULLMASK, x, src); }

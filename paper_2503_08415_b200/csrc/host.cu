@@ -831,6 +831,10 @@ tokensim_status tokensim_get_point_profile(const tokensim_sweep *hc, uint64_t po
   out->ff_iterations = st.ff_iters;
   out->ff_stretches = st.ff_runs;
   out->sm_cycles = st.cycles;
+  out->cycles_ff = st.cyc_ff;
+  out->cycles_ff_failed = st.cyc_ff_fail;
+  out->cycles_normal = st.cyc_normal;
+  for (int q = 0; q < 8; ++q) out->stretch_phase_cycles[q] = st.phase[q];
   return TOKENSIM_OK;
 }
 

@@ -104,13 +104,13 @@ struct WarpSmem {
   u32 *id, *ctx, *rem, *info;       // info: bt slot (bits 0-15) | n_preempt (bits 16-31)
   i64 *last, *maxgap, *arr, *ttft;  // last token time, max gap, arrival, ttft
   u32 *req_cum, *req_pt;            // block requesters: cumulative count; pos|j<<10|tpos<<15
-  u32 *scratch;                     // 32 words (fast-forward histogram / bucket cursors)
+  u32 *scratch;                     // 64 words: fast-forward histogram / cursors, residue masks
   u32 *btfree;                      // cap/32 words, bit = free block-table slot
   u32 *bitmap;                      // free-block bitmap, bit = free block
 };
 
 __host__ __device__ inline size_t smem_per_warp_bytes(u32 cap, u32 nwords_max) {
-  size_t b = (size_t)cap * (4 * 4 + 8 * 4 + 4 * 2) + 32 * 4 + (size_t)(cap / 32) * 4 + (size_t)nwords_max * 4;
+  size_t b = (size_t)cap * (4 * 4 + 8 * 4 + 4 * 2) + 64 * 4 + (size_t)(cap / 32) * 4 + (size_t)nwords_max * 4;
   return (b + 15) & ~(size_t)15;
 }
 size_t sim_smem_per_warp(int cap, u32 nwords_max) { return smem_per_warp_bytes((u32)cap, nwords_max); }
@@ -130,8 +130,8 @@ __device__ __forceinline__ WarpSmem carve(unsigned char *base, u32 cap) {
   S.req_cum = p32 + 4 * cap;
   S.req_pt = p32 + 5 * cap;
   S.scratch = p32 + 6 * cap;
-  S.btfree = p32 + 6 * cap + 32;
-  S.bitmap = p32 + 6 * cap + 32 + cap / 32;
+  S.btfree = p32 + 6 * cap + 64;
+  S.bitmap = p32 + 6 * cap + 64 + cap / 32;
   return S;
 }
 
@@ -162,6 +162,7 @@ __device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 hel
 // shift the digest's iteration index.
 __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl, u64 k, u64 &dig_b,
                               u32 &hint, u32 nwords) {
+  const bool unit = E == K;  // every requester takes one block: owner of order index o is o
   const u32 lane = lane_id();
   u32 o_base = 0, w = hint;
   while (o_base < K) {
@@ -192,13 +193,17 @@ __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl,
       if (act) {
         const u32 blk = (w + lo) * 32 + select_bit(wv, tgt - bv);
         const u32 o = o_base + idx;
-        u32 a = 0, bnd = E;
-        while (a < bnd) {
-          const u32 mid = (a + bnd) >> 1;
-          if (S.req_cum[mid] <= o) a = mid + 1;
-          else bnd = mid;
+        u32 a = o, start = o;
+        if (!unit) {
+          a = 0;
+          u32 bnd = E;
+          while (a < bnd) {
+            const u32 mid = (a + bnd) >> 1;
+            if (S.req_cum[mid] <= o) a = mid + 1;
+            else bnd = mid;
+          }
+          start = a ? S.req_cum[a - 1] : 0u;
         }
-        const u32 start = a ? S.req_cum[a - 1] : 0u;
         const u32 pt = S.req_pt[a];
         const u32 pos = PT_POS(pt);
         const u32 tpos = PT_TPOS(pt) + (o - start);
@@ -339,6 +344,15 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   u64 dig_s = 0, dig_b = 0, dig_r = 0;  // per-lane partial digests
   u64 req_iters = 0, npre = 0, swo_tot = 0, swi_tot = 0, nrej_tot = 0, nfin_tot = 0, peak = 0, bns = 0;
   u64 ff_iters = 0, ff_runs = 0;
+  u64 cyc_ff = 0, cyc_ff_fail = 0, cyc_normal = 0;
+  long long clk_a = 0, clk_p = 0;
+  u64 ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define PH(i)                            \
+  do {                                   \
+    const long long _c = clock64();      \
+    ph[i] += (u64)(_c - clk_p);          \
+    clk_p = _c;                          \
+  } while (0)
   i64 last_fin = 0;
   u32 flags = 0;
   u32 hd_idx = 0xffffffffu, hd_p = 0;  // cached prompt length of the fresh-queue head
@@ -442,6 +456,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     }
 
     // ---------------------------------------------------------------- fast-forward (H3)
+    clk_a = clock64();
+    clk_p = clk_a;
     if (ff_on && nR > 0 && rmin >= 2) {
       // The stretch must admit nothing and resume nothing.  With Q != {} fresh admission is
       // off (c.4 step 5) and a Q head that cannot resume now cannot resume later (R frozen,
@@ -463,7 +479,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           tokq = PR[id] + (OU[id] - S.rem[x]);
           need_h = B.cdiv(tokq);
         }
-        if (!((u64)nR + 1 > mns || (u64)nR + tokq > mbt)) mem_check = true;
+        if (!((u64)nR + 1 > mns || (u64)nR + tokq > mbt)) {
+          mem_check = true;
+          // resume is certain even if every running request takes a block now: don't try
+          if ((i64)nfree - (i64)nR - (i64)need_h >= wm) quiet = false;
+        }
       } else if (!STATICP && adm < arr) {
         if (hd_idx != adm) {
           hd_idx = adm;
@@ -476,30 +496,44 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         else if (!((u64)nR + 1 > mns || (u64)nR + hd_p > mbt)) {
           mem_check = true;
           ratio_h = RATIO;
+          // admission is certain even if every running request takes a block now: don't try
+          if ((i64)nfree - (i64)nR - (i64)need_h >= wm &&
+              (!RATIO || (total - nfree + nR) + need_h <= HP.ratio_limit))
+            quiet = false;
         }
       }
       if (quiet) {
-        // pass over R: C_d(0), min rem and its multiplicity, needs histogram by iteration
-        // offset (lane j <-> iteration k+j)
+        // pass over R: C_d(0), min rem, and the needs histogram by iteration offset (lane j
+        // <-> iteration k+j).  A slot needs a block at offsets j = j0 (mod bs), j0 = -ctx mod bs,
+        // so n_j = cnt[j mod bs]: count slots per j0 with match_any (no atomics).
         S.scratch[lane] = 0;
+        S.scratch[32 + lane] = 0;
         __syncwarp();
         u64 cdp = 0;
         u32 rmn = 0xffffffffu;
         for (u32 b0 = 0; b0 < nR; b0 += 32) {
           const u32 jj = b0 + lane;
+          u32 key = 64u + lane;
           if (jj < nR) {
             const u32 c = S.ctx[jj];
             cdp += c + 1;
             rmn = min(rmn, S.rem[jj]);
             const u32 r = B.mod(c);
-            for (u32 jx = r ? B.bs - r : 0u; jx < 32; jx += B.bs) atomicAdd(&S.scratch[jx], 1u);
+            const u32 j0 = r ? B.bs - r : 0u;
+            if (j0 < 32) key = j0;
           }
+          const u32 peers = __match_any_sync(FULLMASK, key);
+          if (key < 32 && (peers & ltm) == 0u) {
+            S.scratch[key] += __popc(peers);
+            S.scratch[32 + key] = peers;  // slot positions of this residue (meaningful if nR <= 32)
+          }
+          __syncwarp();
         }
-        __syncwarp();
         const u64 Cd0 = warp_sum64(cdp);
         const u32 rm = __reduce_min_sync(FULLMASK, rmn);
-        const u32 nj = S.scratch[lane];
+        const u32 nj = S.scratch[B.bs >= 32 ? lane : B.mod(lane)];
         const u32 Aj = scan_incl(nj);  // cumulative blocks allocated through iteration k+lane
+        PH(0);
         // lane-parallel cost of iteration k+lane: D = nR decodes, C_d grows by nR per iteration
         const u64 Cdj = Cd0 + (u64)lane * nR;
         const i64 Tj = iter_time_ns(K, 0, 0, 0, nR, Cdj, 0);
@@ -523,10 +557,58 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
         if (J >= 2) {
           const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
+          PH(1);
           // requester list ordered by (iteration, slot): bucket cursors = exclusive scan
+          __syncwarp();  // every lane has read its histogram bucket
           S.scratch[lane] = Aj - nj;
           __syncwarp();
-          if (Ktot > 0) {
+          bool done_alloc = Ktot == 0;
+          if (!done_alloc && nR <= 32 && Ktot <= 32 && hint < nwords) {
+            // fused small case: lane o takes the o-th lowest free block of the 32-word window at
+            // the hint and serves order index o = (iteration jb, r-th slot of jb's residue class)
+            const u32 wi = hint + lane;
+            u32 word = wi < nwords ? S.bitmap[wi] : 0u;
+            const u32 cw = __popc(word);
+            const u32 cum = scan_incl(cw);
+            if (__shfl_sync(FULLMASK, cum, 31) >= Ktot) {
+              const bool act = lane < Ktot;
+              const u32 o = act ? lane : 0u;
+              u32 jb = 0;
+#pragma unroll
+              for (u32 st = 16; st; st >>= 1) {
+                const u32 v = __shfl_sync(FULLMASK, Aj, jb + st - 1);
+                if (v <= o) jb += st;
+              }
+              const u32 excl = __shfl_sync(FULLMASK, Aj - nj, jb);
+              u32 lo = 0;
+#pragma unroll
+              for (u32 st = 16; st; st >>= 1) {
+                const u32 v = __shfl_sync(FULLMASK, cum, lo + st - 1);
+                if (v <= o) lo += st;
+              }
+              const u32 wv = __shfl_sync(FULLMASK, word, lo);
+              const u32 bv = __shfl_sync(FULLMASK, cum - cw, lo);
+              if (act) {
+                const u32 mask = S.scratch[32 + (B.bs >= 32 ? jb : B.mod(jb))];
+                const u32 pos = select_bit(mask, o - excl);
+                const u32 blk = (hint + lo) * 32 + select_bit(wv, o - bv);
+                const u32 tpos = B.div(S.ctx[pos] + jb);
+                bt[(size_t)(S.info[pos] & 0xffffu) * btl + tpos] = blk;
+                dig_b += fold4(k + jb, 1, S.id[pos], blk);
+              }
+              const u32 before = cum - cw;
+              const u32 tk = Ktot > before ? min(cw, Ktot - before) : 0u;
+              if (tk && wi < nwords) {
+                word = clear_lowest(word, tk, cw);
+                S.bitmap[wi] = word;
+              }
+              const u32 nz = __ballot_sync(FULLMASK, word != 0u);
+              hint = nz ? hint + (u32)(__ffs(nz) - 1) : hint + 32;
+              __syncwarp();
+              done_alloc = true;
+            }
+          }
+          if (!done_alloc) {
             const u32 nrep = (32 + B.bs - 1) / B.bs;
             for (u32 b0 = 0; b0 < nR; b0 += 32) {
               const u32 jj = b0 + lane;
@@ -557,6 +639,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const u64 blk0 = total - nfree;
           nfree -= Ktot;
           const u64 klast = k + J - 1;
+          PH(2);
           // slot updates for J decode iterations; requests reaching rem == 0 finish in the last
           const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
           const i64 tsl = __shfl_sync(FULLMASK, tsj, J - 1);
@@ -612,6 +695,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             }
           }
           __syncwarp();
+          PH(3);
           // iteration records, digests, counters (lanes j < J)
           const u64 blkj = blk0 + Aj;
           if (lj) {
@@ -620,6 +704,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             put_iter(k + lane, tsj, Tj, 0, nR, 0, Cdj, 0, 0, 0, 0, nf, (u32)blkj);
           }
           const u64 bns_add = warp_sum64(lj ? blkj * (u64)Tj : 0ull);
+          PH(4);
           // memory trace
           if (BINNED) {
             while (true) {
@@ -657,6 +742,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           peak = blk_last > peak ? blk_last : peak;
           bns += bns_add;
           req_iters += (u64)nR * J;
+          PH(5);
           if (nfin) {
             const u32 len = nR + nQ;
             u32 out = first_fin;
@@ -696,15 +782,21 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             nfin_tot += nfin;
             last_fin = tend;
           }
+          PH(6);
           rmin = nR ? __reduce_min_sync(FULLMASK, rmin_l) : 0u;
+          PH(7);
           ff_iters += J;
           ++ff_runs;
           t = tend;
           k += J;
+          cyc_ff += (u64)(clock64() - clk_a);
           continue;
         }
       }
       rmin = 0;  // retry only after the next normal commit recomputes it
+      const long long c1 = clock64();
+      cyc_ff_fail += (u64)(c1 - clk_a);
+      clk_a = c1;
     }
 
     // ---------------------------------------------------------------- 3. decode reservation
@@ -1061,6 +1153,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     }
     t = te;
     ++k;
+    cyc_normal += (u64)(clock64() - clk_a);
   }
   flush_sched();
   if (BINNED) {
@@ -1101,6 +1194,10 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     st.ff_iters = ff_iters;
     st.ff_runs = ff_runs;
     st.cycles = (u64)(clock64() - clk0);
+    st.cyc_ff = cyc_ff;
+    st.cyc_ff_fail = cyc_ff_fail;
+    st.cyc_normal = cyc_normal;
+    for (int q = 0; q < 8; ++q) st.phase[q] = ph[q];
     P.stats[j] = st;
   }
   __syncwarp();

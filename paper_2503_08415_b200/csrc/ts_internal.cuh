@@ -57,6 +57,8 @@ struct SimStats {
   u64 n_transfers, transfer_bytes;
   u64 ff_iters, ff_runs;  // iterations committed by fast-forward stretches, stretch count
   u64 cycles;             // SM clock cycles the warp spent on this point
+  u64 cyc_ff, cyc_ff_fail, cyc_normal;  // cycles in stretches / failed attempts / normal iterations
+  u64 phase[8];                         // stretch phases: pass/cost/list+alloc/update/fold/trace/compact/tail
 };
 
 struct SweepParams {

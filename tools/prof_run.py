@@ -44,7 +44,13 @@ if os.environ.get("PROFILE_POINTS"):
     X = np.stack([normal, st, ri], 1)
     coef, *_ = np.linalg.lstsq(X, cy, rcond=None)
     print("cycles ~ %.0f/normal-iter + %.0f/stretch + %.2f/req-iter" % tuple(coef))
-    order = np.argsort(-cy)[:8]
+    order = np.argsort(-cy)[:6]
     for p in order:
+        x = prof[p]
+        nn = max(1, x["n_iterations"] - x["ff_iterations"])
         print("  point", p, "cycles %.3e" % cy[p], "iters", int(it[p]), "ff", int(ff[p]), "stretches", int(st[p]),
-              "req-its", int(ri[p]), "preempt", int(s["n_preemptions"][p]), "peak", int(s["peak_blocks"][p]))
+              "req-its", int(ri[p]), "preempt", int(s["n_preemptions"][p]),
+              "| cyc/stretch %.0f  cyc/normal %.0f  failed-ff %.2e" % (x["cycles_ff"] / max(1, x["ff_stretches"]),
+                                                                       x["cycles_normal"] / nn, x["cycles_ff_failed"]))
+        ns = max(1, x["ff_stretches"])
+        print("     stretch phases (cycles/stretch):", " ".join("%.0f" % (c / ns) for c in x["stretch_phase_cycles"]))
