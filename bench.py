@@ -87,6 +87,9 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:  # first sample before the timed region
+                time.sleep(0.02)
         except Exception:
             self.proc = None
 
@@ -96,21 +99,22 @@ class ClockSampler:
             if len(parts) >= 9:
                 self.rows.append(parts)
 
-    def stop(self):
+    def stop(self, first: int = 0):
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
-        if not self.rows:
+        rows = self.rows[first:] or self.rows[-1:]  # samples taken during the timed region
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def measured_peaks():
@@ -235,12 +239,13 @@ def run_ours(args):
     assert (s["status_flags"] & 16 == 0).all(), "internal error flag set"
 
     clocks = ClockSampler(local)
+    clocks.start()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     sim_ms, wl_ms, sum_ms = [], [], []
     launches = 0
     barrier()
-    clocks.start()
+    n_clk0 = len(clocks.rows)
     for i in range(args.steps):
         with torch.cuda.stream(stream):
             flush.fill_(i & 0xff)  # L2 flush between timed steps (not timed)
@@ -253,7 +258,7 @@ def run_ours(args):
         sum_ms.append(info["ms_summary"])
         launches += info["n_launches"]
     barrier()
-    clk = clocks.stop()
+    clk = clocks.stop(n_clk0)
     total_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
     t = torch.tensor([total_ms, float(ri_local), sum(sim_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -346,7 +351,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOAD_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
