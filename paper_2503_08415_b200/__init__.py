@@ -5,5 +5,5 @@ allocation, roofline cost model, metrics) runs in hand-written sm_100a CUDA kern
 behind the C ABI in include/tokensim.h; this package is the thin Python binding.
 """
 from ._lib import LIB_PATH, RECORD_DTYPE, SAMPLE_DTYPE, ITER_DTYPE, SUMMARY_DTYPE  # noqa: F401
-from .api import (Sweep, TokensimError, METRICS, sweep, run_distributed, shard_range,  # noqa: F401
-                  version, marshal)
+from .api import (Sweep, TokensimError, METRICS, sweep, run_distributed, gather_summaries,  # noqa: F401
+                  shard_range, version, marshal)

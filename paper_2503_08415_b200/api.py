@@ -266,25 +266,42 @@ def shard_range(num_points: int, rank: int, world: int):
     return rank, num_points, world
 
 
-def run_distributed(cfg: si.SweepConfig, group=None):
-    """One process per GPU: rank r runs points r, r+W, ...; the 384-B summaries of all
-    points are then all-gathered (the only collective; NCCL over NVLink on GPUs) and
-    imported so every rank can answer summary queries for every point.
+def gather_summaries(local, num_points: int, group=None):
+    """All-gather every rank's 384-B point summaries (the sweep's only collective).
 
-    Returns (sweep handle, all summaries sorted by point)."""
+    `local` is a torch uint8 tensor (device summaries from `Sweep.summaries_device()`, NCCL)
+    or a numpy SUMMARY_DTYPE array (host, e.g. gloo).  Each rank contributes a fixed-size
+    slot of ceil(P / world) records (zero padding has version 0 and is dropped).
+    Returns all summaries sorted by point."""
     import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    per = -(-num_points // world) * T.SUMMARY_DTYPE.itemsize
+    if isinstance(local, np.ndarray):
+        local = torch.from_numpy(np.ascontiguousarray(local).view(np.uint8).copy())
+    buf = torch.zeros(per, dtype=torch.uint8, device=local.device)
+    buf[:local.numel()] = local
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty(world * per, dtype=torch.uint8, device=local.device)
+        dist.all_gather_into_tensor(out, buf, group=group)
+    else:
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(parts, buf, group=group)
+        out = torch.cat(parts)
+    allv = out.cpu().numpy().view(T.SUMMARY_DTYPE)
+    allv = allv[allv["version"] != 0]
+    return np.sort(allv, order="point")
+
+
+def run_distributed(cfg: si.SweepConfig, group=None):
+    """One process per GPU: rank r runs points r, r+W, ...; the summaries of all points are
+    then all-gathered (NCCL over NVLink) and imported so every rank can answer summary and
+    P50/P90/P99/max queries for every point.  Returns (sweep handle, all summaries)."""
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     sw = Sweep(cfg)
     b, e, s = shard_range(sw.num_points, rank, world)
     sw.run(b, e, s)
-    per = -(-sw.num_points // world)  # max points per rank
-    local = sw.summaries_device()
-    buf = torch.zeros(per * T.SUMMARY_DTYPE.itemsize, dtype=torch.uint8, device=local.device)
-    buf[:local.numel()] = local
-    out = torch.empty(world * buf.numel(), dtype=torch.uint8, device=local.device)
-    dist.all_gather_into_tensor(out, buf, group=group)
-    allv = out.cpu().numpy().view(T.SUMMARY_DTYPE)
-    allv = allv[allv["version"] != 0]
+    allv = gather_summaries(sw.summaries_device(), sw.num_points, group)
     sw.import_summaries(allv)
-    return sw, np.sort(allv, order="point")
+    return sw, allv
