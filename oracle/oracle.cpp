@@ -30,6 +30,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <set>
 #include <string>
@@ -293,6 +294,10 @@ i64 iter_time(const CostCtx &K, const std::vector<Prefill> &pf, const std::vecto
   return (i64)std::floor(Tn + 0.5);
 }
 
+struct CostK_ {
+  CostCtx k;
+};
+
 // ----------------------------------------------------------------- state
 enum Kind { K_DEC = 0, K_PRE_FRESH = 1, K_PRE_RECOMP = 2 };
 
@@ -404,27 +409,30 @@ void build_trace(const oracle_cfg &c, const std::vector<oracle_iter> &it, u32 wo
       out.push_back({x.t_start, x.T_ns, (u64)x.blocks * (u64)x.T_ns, (u32)x.blocks, 1u});
     }
   } else if (c.trace_mode == OR_TRACE_BINNED) {
+    // bins [bW, (b+1)W) for b < ceil(t_final / W); each iteration adds blocks x overlap to every
+    // bin it overlaps, and counts in the bin holding its start (reading R5)
     const i64 W = (i64)c.trace_bin_ns;
     const i64 nbins = (t_final + W - 1) / W;
-    for (i64 b = 0; b < nbins; ++b) {
-      if ((u64)out.size() >= c.trace_cap_samples) {
-        overflow = true;
-        break;
-      }
-      oracle_sample s = {b * W, W, 0, 0, 0};
-      const i64 lo = b * W, hi = (b + 1) * W;
-      for (const oracle_iter &x : it) {
-        if (x.worker != worker) continue;
-        const i64 ts = x.t_start, te = x.t_start + x.T_ns;
-        if (ts >= lo && ts < hi) s.n_iter += 1;
-        const i64 ov = std::min(te, hi) - std::max(ts, lo);
-        if (ov > 0) {
-          s.block_ns += x.blocks * (u64)ov;
-          s.blocks_max = std::max<u32>(s.blocks_max, (u32)x.blocks);
+    std::vector<oracle_sample> bins((size_t)nbins);
+    for (i64 b = 0; b < nbins; ++b) bins[(size_t)b] = {b * W, W, 0, 0, 0};
+    for (const oracle_iter &x : it) {
+      if (x.worker != worker) continue;
+      const i64 ts = x.t_start, te = x.t_start + x.T_ns;
+      const i64 b0 = ts / W;
+      if (b0 < nbins) bins[(size_t)b0].n_iter += 1;
+      for (i64 b = b0; b < nbins && b * W < te; ++b) {
+        const i64 lo = std::max(ts, b * W), hi = std::min(te, (b + 1) * W);
+        if (hi - lo > 0) {
+          bins[(size_t)b].block_ns += x.blocks * (u64)(hi - lo);
+          bins[(size_t)b].blocks_max = std::max<u32>(bins[(size_t)b].blocks_max, (u32)x.blocks);
         }
       }
-      out.push_back(s);
     }
+    if ((u64)nbins > c.trace_cap_samples) {
+      overflow = true;
+      bins.resize((size_t)c.trace_cap_samples);
+    }
+    out = bins;
   }
 }
 
@@ -732,10 +740,436 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
 }
 
 // ----------------------------------------------------------------- a.9 P/D pair
+// SURVEY §8(a.9), readings A35 and R-PD1..R-PD7 in DESIGN.md.  Two workers per point: P runs
+// prefill-only iterations and emits the first token; at the end-of-prefill
+// breakpoint the request joins D's pending FIFO still holding its P blocks; D pulls pending
+// requests FCFS at its boundaries, allocates ceil(p/bs) blocks and starts a p*kvb-byte transfer on
+// the FIFO P->D link; the request becomes runnable on D at the first D boundary
+// >= transfer end; P frees its blocks at its first boundary >= transfer end.  The two workers are
+// advanced in time order of their next boundary, D first on ties (reading A2).  An idle worker
+// wakes at the earliest event that can change its decision.
 oracle_run *simulate_pd(const oracle_cfg &c) {
-  (void)c;
-  g_err = "PD_PAIR not implemented";
-  return nullptr;
+  if (c.kind == OR_CONT_RATIO) {
+    g_err = "PD_PAIR supports STATIC and CONT policies only";
+    return nullptr;
+  }
+  oracle_derived dP, dD;
+  if (!derive(c, 0, dP) || !derive(c, 1, dD)) return nullptr;
+  const CostK_ KP = {cost_ctx(c, dP, 0)}, KD = {cost_ctx(c, dD, 1)};
+  std::vector<i64> A;
+  std::vector<u32> Pl, Ol;
+  if (!workload(c, A, Pl, Ol)) return nullptr;
+  const u32 n = c.num_requests;
+  const u64 bs = c.block_size, totP = dP.total_blocks, totD = dD.total_blocks;
+  const bool SWAPM = c.preempt == OR_SWAP;
+  const i64 INF = INT64_MAX;
+  const double inv_link = 1.0 / c.pd_link_bw;
+
+  struct PReq {
+    i64 a = 0;
+    u32 p = 0, o = 0, status = 0;
+    u64 ctx = 0, gen = 0;
+    i64 first_tok = 0, last_tok = 0, max_gap = 0, finish = 0, join = 0, xend = 0;
+    u32 n_preempt = 0;
+    bool xstarted = false;
+    std::vector<u32> pblocks, dblocks;
+    u64 finish_k = 0;
+  };
+  std::vector<PReq> req(n);
+  for (u32 i = 0; i < n; ++i) {
+    req[i].a = A[i];
+    req[i].p = Pl[i];
+    req[i].o = Ol[i];
+  }
+  oracle_run *run = new oracle_run();
+  std::memset(&run->summary, 0, sizeof(run->summary));
+  oracle_summary &S = run->summary;
+  std::set<u32> freeP, freeD;
+  for (u64 b = 0; b < totP; ++b) freeP.insert((u32)b);
+  for (u64 b = 0; b < totD; ++b) freeD.insert((u32)b);
+  std::deque<u32> pending;    // finished prefill, waiting for D admission (join order = id order)
+  std::deque<u32> pholders;   // hold P blocks until their transfer ends (same FIFO order)
+  std::set<u32> xfer, R, Q;   // D: transferring, running, preempted
+  i64 tP = 0, tD = 0, link_busy = 0, lastP = 0, lastD = 0;
+  bool P_idle = false, D_idle = false;
+  u64 kP = 0, kD = 0;
+  u32 arr = 0, adm = 0, n_done = 0;
+  u64 sched_d = 0, block_d = 0, req_d = 0, req_iters = 0, npre = 0, swo = 0, swi = 0, nrej_tot = 0;
+  u64 peakD = 0, bnsD = 0, n_xfer = 0, xfer_bytes = 0;
+
+  auto ev = [&](u64 k, u32 kind, u32 worker, u32 id, u32 b) {
+    block_d += fold({k, kind + 2 * worker, id, b});
+    if (c.keep_events) run->events.push_back({k, kind, id, b, worker});
+  };
+  auto finish_req = [&](u32 id, i64 te, u64 k) {
+    PReq &x = req[id];
+    x.status = 1;
+    x.finish = te;
+    x.finish_k = k;
+    req_d += fold({id, (u64)(x.first_tok - x.a), (u64)(x.finish - x.a), (u64)x.max_gap, x.n_preempt, k});
+    ++n_done;
+  };
+
+  while (true) {
+    if (n_done == n) break;
+    const i64 tnext = std::min(tP, tD);
+    if (tnext == INF) {
+      g_err = "P/D deadlock: both workers wait";
+      delete run;
+      return nullptr;
+    }
+    if (c.horizon_ns >= 0 && tnext >= c.horizon_ns) {
+      S.status_flags |= 4;
+      break;
+    }
+    if (tD <= tP) {
+      // ================================================================ D boundary
+      const i64 t = tD;
+      // 1. finished transfers become runnable (ascending id)
+      std::vector<u32> xv(xfer.begin(), xfer.end());
+      for (u32 id : xv) {
+        if (req[id].xend <= t) {
+          xfer.erase(id);
+          R.insert(id);
+        }
+      }
+      std::map<u32, Kind> kind;
+      // 3. decode reservation + preemption over R
+      const u64 F = freeD.size();
+      std::vector<u32> Rv(R.begin(), R.end());
+      auto need_of = [&](u32 id) -> u64 { return (req[id].ctx % bs == 0) ? 1 : 0; };
+      u64 sum_need = 0;
+      for (u32 id : Rv) sum_need += need_of(id);
+      u64 m = 0, swap_out = 0;
+      if (sum_need > F) {
+        const u64 nr = Rv.size();
+        for (m = 1; m <= nr; ++m) {
+          u64 lhs = 0, rhs = F;
+          for (u64 j = 0; j < nr - m; ++j) lhs += need_of(Rv[j]);
+          for (u64 j = nr - m; j < nr; ++j) rhs += req[Rv[j]].dblocks.size();
+          if (lhs <= rhs) break;
+        }
+        // blocks held by in-flight transfers are not preemptible, so on D the minimal m may
+        // be all of R (reading R-PD4); m <= nr always holds since m = nr satisfies the condition
+        if (m > nr) {
+          g_err = "P/D: no victim count satisfies c.4 step 3";
+          delete run;
+          return nullptr;
+        }
+        for (u64 i = 0; i < m; ++i) {
+          const u32 id = Rv[nr - 1 - i];
+          PReq &x = req[id];
+          const u64 held = x.dblocks.size();
+          for (u32 b : x.dblocks) {
+            freeD.insert(b);
+            ev(kD, 2, 1, id, b);
+          }
+          x.dblocks.clear();
+          x.n_preempt += 1;
+          if (SWAPM) swap_out += held * dD.block_bytes;
+          else x.ctx = 0;
+          R.erase(id);
+          Q.insert(id);
+        }
+        npre += m;
+      }
+      for (u32 id : R) {
+        kind[id] = K_DEC;
+        if (need_of(id)) {
+          const u32 b = *freeD.begin();
+          freeD.erase(freeD.begin());
+          req[id].dblocks.push_back(b);
+          ev(kD, 1, 1, id, b);
+        }
+      }
+      const u64 D3 = R.size();
+      u64 n_res = 0, n_adm = 0, swap_in = 0, tokens = D3;
+      if (m == 0) {
+        // 4. resume (|R| counts transferring requests too)
+        std::vector<u32> Qv(Q.begin(), Q.end());
+        for (u32 id : Qv) {
+          PReq &x = req[id];
+          u64 need, tok;
+          if (SWAPM) {
+            need = ceil_div(x.ctx, bs) + ((x.ctx % bs == 0) ? 1 : 0);
+            tok = 1;
+          } else {
+            need = ceil_div(x.p + x.gen, bs);
+            tok = x.p + x.gen;
+          }
+          const bool ok = (R.size() + xfer.size() + 1 <= c.max_num_seqs) &&
+                          (tokens + tok <= c.max_batched_tokens) &&
+                          ((i64)freeD.size() - (i64)need >= (i64)c.watermark_blocks);
+          if (!ok) break;
+          for (u64 j = 0; j < need; ++j) {
+            const u32 b = *freeD.begin();
+            freeD.erase(freeD.begin());
+            x.dblocks.push_back(b);
+            ev(kD, 1, 1, id, b);
+          }
+          Q.erase(id);
+          R.insert(id);
+          ++n_res;
+          tokens += tok;
+          if (SWAPM) {
+            swap_in += ceil_div(x.ctx, bs) * dD.block_bytes;
+            kind[id] = K_DEC;
+          } else {
+            kind[id] = K_PRE_RECOMP;
+          }
+        }
+        // 5. pull pending requests (FCFS), start their KV transfers
+        if (Q.empty() && (c.kind != OR_STATIC || (R.empty() && xfer.empty()))) {
+          while (!pending.empty() && req[pending.front()].join <= t) {
+            const u32 id = pending.front();
+            PReq &x = req[id];
+            const u64 need = ceil_div(x.p, bs);
+            if (R.size() + xfer.size() + 1 > c.max_num_seqs) break;
+            if ((i64)freeD.size() - (i64)need < (i64)c.watermark_blocks) break;
+            for (u64 j = 0; j < need; ++j) {
+              const u32 b = *freeD.begin();
+              freeD.erase(freeD.begin());
+              x.dblocks.push_back(b);
+              ev(kD, 1, 1, id, b);
+            }
+            const u64 bytes = (u64)x.p * dD.kvb;
+            const double sec = (double)bytes * inv_link;
+            const i64 dur = (i64)std::floor(sec * 1e9 + 0.5);
+            const i64 start = std::max(t, link_busy);
+            x.xend = start + dur;
+            x.xstarted = true;
+            link_busy = x.xend;
+            xfer.insert(id);
+            pending.pop_front();
+            ++n_adm;
+            ++n_xfer;
+            xfer_bytes += bytes;
+            if (P_idle && x.xend < tP) tP = x.xend;  // P may be waiting for these P blocks
+          }
+        }
+      }
+      if (R.empty()) {  // 6. nothing runnable: wait for a transfer end or a pending join
+        i64 wake = INF;
+        for (u32 id : xfer) wake = std::min(wake, req[id].xend);
+        for (u32 id : pending)
+          if (req[id].join > t) wake = std::min(wake, req[id].join);
+        tD = wake;
+        D_idle = true;
+        continue;
+      }
+      // 7. cost on D's profile
+      std::vector<Prefill> pf;
+      std::vector<u64> dec;
+      u64 Np = 0, Cd = 0;
+      for (u32 id : R) {
+        const PReq &x = req[id];
+        if (kind[id] == K_DEC) {
+          dec.push_back(x.ctx + 1);
+          Cd += x.ctx + 1;
+        } else {
+          pf.push_back({x.p + x.gen, 0});
+          Np += x.p + x.gen;
+        }
+      }
+      const i64 T = iter_time(KD.k, pf, dec, swap_out + swap_in);
+      const i64 te = t + T;
+      const u64 blocks = totD - freeD.size();
+      const u64 entries = R.size();
+      u64 n_fin = 0;
+      std::vector<u32> Rc(R.begin(), R.end());
+      for (u32 id : Rc) {
+        PReq &x = req[id];
+        if (kind[id] == K_PRE_RECOMP) {
+          x.ctx = x.p + x.gen;
+          x.gen += 1;
+        } else {
+          x.ctx += 1;
+          x.gen += 1;
+        }
+        const i64 gap = te - x.last_tok;
+        x.max_gap = std::max(x.max_gap, gap);
+        x.last_tok = te;
+        if (x.gen == x.o) {
+          finish_req(id, te, kD);
+          for (u32 b : x.dblocks) {
+            freeD.insert(b);
+            ev(kD, 2, 1, id, b);
+          }
+          x.dblocks.clear();
+          R.erase(id);
+          ++n_fin;
+        }
+      }
+      sched_d += fold({kD | (1ull << 40), (u64)t, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0, n_fin,
+                       blocks});
+      run->iters.push_back({kD, t, T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0, n_fin, blocks, 1, 0});
+      req_iters += entries;
+      peakD = std::max(peakD, blocks);
+      bnsD += blocks * (u64)T;
+      swo += swap_out;
+      swi += swap_in;
+      tD = te;
+      lastD = te;
+      ++kD;
+      D_idle = false;
+    } else {
+      // ================================================================ P boundary
+      const i64 t = tP;
+      // P blocks of finished transfers are freed (transfer order)
+      while (!pholders.empty()) {
+        const u32 id = pholders.front();
+        PReq &x = req[id];
+        if (!(x.xstarted && x.xend <= t)) break;
+        for (u32 b : x.pblocks) {
+          freeP.insert(b);
+          ev(kP, 2, 0, id, b);
+        }
+        x.pblocks.clear();
+        pholders.pop_front();
+      }
+      while (arr < n && req[arr].a <= t) ++arr;
+      std::vector<u32> batch;
+      u64 tokens = 0, n_rej = 0;
+      while (adm < arr) {
+        PReq &x = req[adm];
+        const u64 need = ceil_div(x.p, bs);
+        if (need > totP - c.watermark_blocks) {
+          x.status = 2;
+          ++n_rej;
+          ++n_done;
+          ++adm;
+          continue;
+        }
+        if (batch.size() + 1 > c.max_num_seqs) break;
+        if (tokens + x.p > c.max_batched_tokens) break;
+        if ((i64)freeP.size() - (i64)need < (i64)c.watermark_blocks) break;
+        for (u64 j = 0; j < need; ++j) {
+          const u32 b = *freeP.begin();
+          freeP.erase(freeP.begin());
+          x.pblocks.push_back(b);
+          ev(kP, 1, 0, adm, b);
+        }
+        batch.push_back(adm);
+        tokens += x.p;
+        ++adm;
+      }
+      nrej_tot += n_rej;
+      if (batch.empty()) {  // idle: wait for an arrival or for P blocks to come back
+        i64 wake = arr < n ? req[arr].a : INF;
+        if (!pholders.empty() && req[pholders.front()].xstarted) wake = std::min(wake, req[pholders.front()].xend);
+        tP = wake;
+        P_idle = true;
+        continue;
+      }
+      std::vector<Prefill> pf;
+      u64 Np = 0;
+      for (u32 id : batch) {
+        pf.push_back({req[id].p, 0});
+        Np += req[id].p;
+      }
+      const i64 T = iter_time(KP.k, pf, {}, 0);
+      const i64 te = t + T;
+      const u64 blocks = totP - freeP.size();
+      u64 n_fin = 0;
+      for (u32 id : batch) {  // the first token; the end-of-prefill breakpoint
+        PReq &x = req[id];
+        x.ctx = x.p;
+        x.gen = 1;
+        x.first_tok = te;
+        x.last_tok = te;
+        if (x.gen == x.o) {
+          finish_req(id, te, kP);
+          for (u32 b : x.pblocks) {
+            freeP.insert(b);
+            ev(kP, 2, 0, id, b);
+          }
+          x.pblocks.clear();
+          ++n_fin;
+        } else {
+          x.join = te;
+          pending.push_back(id);
+          pholders.push_back(id);
+        }
+      }
+      sched_d += fold({kP, (u64)t, (u64)T, pf.size(), 0, Np, 0, 0, 0, batch.size(), n_rej, n_fin, blocks});
+      run->iters.push_back({kP, t, T, pf.size(), 0, Np, 0, 0, 0, batch.size(), n_rej, n_fin, blocks, 0, 0});
+      req_iters += batch.size();
+      tP = te;
+      lastP = te;
+      ++kP;
+      P_idle = false;
+      if (D_idle && te < tD) tD = te;  // new pending requests join at te
+    }
+    if (c.check_invariants) {
+      // conservation on both workers; held = ceil(ctx/bs) on D's running set
+      u64 hp = 0, hd = 0;
+      for (u32 i = 0; i < n; ++i) {
+        hp += req[i].pblocks.size();
+        hd += req[i].dblocks.size();
+      }
+      bool ok = hp + freeP.size() == totP && hd + freeD.size() == totD;
+      for (u32 id : R) ok &= req[id].dblocks.size() == ceil_div(req[id].ctx, bs);
+      for (u32 id : xfer) ok &= req[id].dblocks.size() == ceil_div(req[id].p, bs);
+      for (u32 id : Q) ok &= req[id].dblocks.empty();
+      if (!ok) {
+        g_err = "P/D invariant violated";
+        delete run;
+        return nullptr;
+      }
+    }
+  }
+
+  run->records.resize(n);
+  u64 n_fin = 0;
+  for (u32 i = 0; i < n; ++i) {
+    const PReq &x = req[i];
+    oracle_record &rec = run->records[i];
+    rec.ttft_ns = (x.gen >= 1 || x.status == 1) ? x.first_tok - x.a : 0;
+    rec.e2e_ns = x.status == 1 ? x.finish - x.a : 0;
+    rec.mtpot_ns = x.status == 1 ? x.max_gap : 0;
+    rec.n_preempt = x.n_preempt;
+    rec.status = x.status;
+    rec.finish_k = x.status == 1 ? x.finish_k : 0;
+    if (x.status == 1) ++n_fin;
+  }
+  const i64 t_final = std::max(lastP, lastD);
+  S.n_requests = n;
+  S.n_finished = n_fin;
+  S.n_rejected = nrej_tot;
+  S.n_unfinished = n - n_fin - nrej_tot;
+  if (nrej_tot == n) S.status_flags |= 2;
+  S.n_iterations = kP + kD;
+  S.n_request_iterations = req_iters;
+  S.n_preemptions = npre;
+  S.swap_out_bytes = swo;
+  S.swap_in_bytes = swi;
+  S.t_final = t_final;
+  S.sched_digest = sched_d;
+  S.block_digest = block_d;
+  S.request_digest = req_d;
+  S.total_blocks = totD;
+  S.peak_blocks = peakD;
+  S.block_ns_sum = bnsD;
+  S.mean_util = (t_final > 0 && totD > 0) ? (double)bnsD / ((double)totD * (double)t_final) : 0.0;
+  S.n_transfers = n_xfer;
+  S.transfer_bytes = xfer_bytes;
+  // metrics over records (same definitions as the unified worker)
+  std::vector<Req> rr(n);
+  for (u32 i = 0; i < n; ++i) {
+    rr[i].a = req[i].a;
+    rr[i].p = req[i].p;
+    rr[i].o = req[i].o;
+    rr[i].status = req[i].status;
+    rr[i].first_tok = req[i].first_tok;
+    rr[i].finish = req[i].finish;
+    rr[i].max_gap = req[i].max_gap;
+  }
+  metrics(c, dD, rr, S);
+  bool ovf = false;
+  build_trace(c, run->iters, 0, t_final, run->trace[0], ovf);
+  build_trace(c, run->iters, 1, t_final, run->trace[1], ovf);
+  if (ovf) S.status_flags |= 1;
+  return run;
 }
 
 }  // namespace

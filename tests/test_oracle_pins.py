@@ -495,3 +495,115 @@ def test_finding2_ratio_reduces_preemption(oracle_lib):
     assert res[1.0]["n_preemptions"] > 0
     assert res[0.7]["n_preemptions"] < res[1.0]["n_preemptions"]
     assert res[0.7]["stat"][4][3] < res[1.0]["stat"][4][3]         # max mTPOT shrinks
+
+
+# ------------------------------------------------------------------ a.9 P/D pair
+def _pd_cfg(reqs, hwP=si.A100_IDEAL, hwD=None, pol=si.Policy(), model=si.LLAMA2_7B, **opt):
+    hwD = hwD or replace(si.A100_IDEAL, mem_bw=4e12)
+    w = si.Workload(len(reqs), [1.0], [0], len_dist=si.TRACE, trace_arrival_ns=[r[0] for r in reqs],
+                    trace_prompt=[r[1] for r in reqs], trace_output=[r[2] for r in reqs],
+                    prompt_table=None, output_table=None)
+    return si.SweepConfig("pd", model, [hwP, hwD], [pol], w, si.Options(topology=si.PD_PAIR, **opt))
+
+
+def _pd_sim(cfg, **kw):
+    from oracle import oracle as O
+    return O.simulate(cfg, 1, check_invariants=True, **kw)  # point 1 = (P = hw0, D = hw1)
+
+
+def _xfer_ns(p, kvb=524288, bw=200e9):
+    return math.floor(p * kvb / bw * 1e9 + 0.5)
+
+
+def test_pd_isolated_requests_closed_form(oracle_lib):
+    """Isolated requests: e2e = T_pre on P + KV transfer p*kvb/link + decode
+    steps on D; mTPOT includes the transfer in the first decode gap; P frees its blocks when
+    the transfer ends (A35)."""
+    from oracle import oracle as O
+    reqs = [(0, 20, 3), (10 ** 12, 100, 9), (2 * 10 ** 12, 16, 2), (3 * 10 ** 12, 7, 1)]
+    cfg = _pd_cfg(reqs)
+    r = _pd_sim(cfg, keep_events=True, want=("summary", "records", "iters", "events"))
+    for i, (a, p, o) in enumerate(reqs):
+        tp = O.iter_time_ns(cfg, [(p, 0)], [], point=1, decode_worker=0)
+        td = [O.iter_time_ns(cfg, [], [p + j], point=1, decode_worker=1) for j in range(1, o)]
+        rec = r["records"][i]
+        assert rec["ttft_ns"] == tp
+        if o == 1:
+            assert rec["e2e_ns"] == tp and rec["mtpot_ns"] == 0
+        else:
+            x = _xfer_ns(p)
+            assert rec["e2e_ns"] == tp + x + sum(td)
+            assert rec["mtpot_ns"] == max([x + td[0]] + td[1:])
+    s = r["summary"]
+    assert s["n_transfers"] == 3 and s["transfer_bytes"] == (20 + 100 + 16) * 524288
+    assert s["n_request_iterations"] == sum(o for _, _, o in reqs)
+    ev = r["events"]
+    # request 0: two P blocks allocated by P's first iteration, freed at P's next boundary
+    p0 = ev[(ev["req"] == 0) & (ev["worker"] == 0)]
+    assert [(int(e["k"]), int(e["kind"]), int(e["block"])) for e in p0] == [(0, 1, 0), (0, 1, 1), (1, 2, 0), (1, 2, 1)]
+    d0 = ev[(ev["req"] == 0) & (ev["worker"] == 1)]
+    assert [int(e["kind"]) for e in d0] == [1, 1, 2, 2]   # ceil(20/16) blocks pulled, freed at finish
+
+
+def test_pd_link_is_fifo(oracle_lib):
+    """two transfers on one link serialize -- the second completes ~2x later."""
+    from oracle import oracle as O
+    cfg = _pd_cfg([(0, 64, 2), (0, 64, 2)], pd_link_bw=1e9)   # slow link: transfers dominate
+    r = _pd_sim(cfg, want=("summary", "records", "iters"))
+    x = _xfer_ns(64, bw=1e9)
+    tp = O.iter_time_ns(cfg, [(64, 0), (64, 0)], [], point=1, decode_worker=0)
+    rec = r["records"]
+    assert rec["ttft_ns"][0] == rec["ttft_ns"][1] == tp
+    d1 = O.iter_time_ns(cfg, [], [65], point=1, decode_worker=1)
+    assert rec["e2e_ns"][0] == tp + x + d1
+    assert rec["e2e_ns"][1] == tp + 2 * x + d1
+
+
+def _random_pd(rng):
+    n = int(rng.integers(1, 50))
+    a = np.sort(rng.integers(0, 2_000_000_000, n))
+    p = rng.integers(1, 64, n)
+    o = rng.integers(1, 64, n)
+    mml = 128
+    model = replace(si.LLAMA2_7B, max_model_len=mml)
+    bs = int(rng.choice([4, 16]))
+    mb = -(-mml // bs)
+    hwP = replace(si.A100, kv_blocks_override=int(rng.integers(mb, mb + 30)), peak_flops=float(rng.choice([78e12, 312e12])))
+    hwD = replace(si.A100, kv_blocks_override=int(rng.integers(mb, mb + 30)), mem_bw=float(rng.choice([1e12, 4e12])))
+    pol = si.Policy(kind=str(rng.choice([si.STATIC, si.CONT])), preempt=str(rng.choice([si.SWAP, si.RECOMPUTE])),
+                    max_num_seqs=int(rng.choice([2, 8, 256])), block_size=bs)
+    return _pd_cfg(list(zip(a.tolist(), p.tolist(), o.tolist())), hwP=hwP, hwD=hwD, pol=pol, model=model,
+                   pd_link_bw=float(rng.choice([1e9, 200e9])), trace_mode=si.FULL), p, o
+
+
+def test_pd_invariants_random(oracle_lib):
+    """every finished request with o >= 2 makes exactly one P->D transfer of p*kvb bytes,
+    completed before its first decode; conservation on both workers every boundary."""
+    rng = np.random.default_rng(99)
+    for _ in range(80):
+        cfg, p, o = _random_pd(rng)
+        r = _pd_sim(cfg, want=("summary", "records", "iters", "trace"))
+        s, rec = r["summary"], r["records"]
+        assert s["n_finished"] == len(rec) and s["n_request_iterations"] == int(o.sum())
+        multi = o >= 2
+        assert s["n_transfers"] == int(multi.sum()) and s["transfer_bytes"] == int(p[multi].sum()) * 524288
+        for i in np.nonzero(multi)[0]:
+            assert rec["mtpot_ns"][i] >= _xfer_ns(int(p[i]), bw=cfg.options.pd_link_bw)
+        it = r["iters"]
+        assert (it["S_p"][it["worker"] == 0] == it["n_admitted"][it["worker"] == 0]).all()   # P: prefill only
+        if cfg.policies[0].preempt == si.SWAP:
+            assert (it["S_p"][it["worker"] == 1] == 0).all()   # D: no prefill except RECOMPUTE (A35)
+
+
+def test_pd_finding5_prefill_footprint(oracle_lib):
+    """Finding 5: prefill-side KV footprint is much lower than decode-side."""
+    from oracle import oracle as O
+    w = si.Workload(1500, [6.0], [0], len_dist=si.FIXED, prompt_a=128, output_a=1024)
+    cfg = si.SweepConfig("pdfp", si.LLAMA2_7B, [si.A100, si.A100], [si.Policy()], w,
+                         si.Options(topology=si.PD_PAIR, trace_bin_ns=1_000_000_000))
+    r = O.simulate(cfg, 1, want=("summary", "trace"))
+    tp, td = r["trace"]
+    sel = slice(5, 65)   # the paper's [5, 65] s window (P:537)
+    uP = tp["block_ns"][sel].sum() / O.derive(cfg, 1, 0)["total_blocks"]
+    uD = td["block_ns"][sel].sum() / O.derive(cfg, 1, 1)["total_blocks"]
+    assert uP < 0.5 * uD
