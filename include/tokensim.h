@@ -274,6 +274,7 @@ typedef struct {
   uint64_t stretch_phase_cycles[8];  /* inside successful stretches: scan of R / cost + cut /
                                         block allocation / slot updates + finishes / digests /
                                         memory trace / compaction / bookkeeping             */
+  uint64_t n_transfers, transfer_bytes;  /* PD_PAIR: P->D KV transfers started and their bytes */
 } tokensim_point_profile;
 tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t point, tokensim_point_profile *out);
 

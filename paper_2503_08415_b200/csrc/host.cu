@@ -33,7 +33,7 @@ const uint32_t kOutputThr[7] = {429496730u, 773094113u, 1159641170u, 1717986918u
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, total;
+  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, ring, fifo, total;
   u64 n_run;
   u32 warps_total, wpb, blocks;
   size_t smem;
@@ -59,7 +59,7 @@ struct tokensim_sweep {
   std::vector<DevPol> dpol;
   std::vector<double> est_T1;  // per (hw,pol): rough per-iteration time for LPT ordering
   u32 cap = 256, nwords_max = 1, bt_len = 1, n_hw_axis = 0;
-  u64 n_points = 0;
+  u64 n_points = 0, max_total_blocks = 0;
   // device tables
   int dev = -1;
   char *d_tab = nullptr;
@@ -140,8 +140,9 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
     return fail(nullptr, TOKENSIM_E_INVALID, "model: every dimension must be >= 1");
   if (m.max_model_len < 2 || m.max_model_len > (1u << 20))
     return fail(nullptr, TOKENSIM_E_INVALID, "model.max_model_len: must be in [2, 2^20]");
-  if (opt->topology != TOKENSIM_UNIFIED)
-    return fail(nullptr, TOKENSIM_E_INVALID, "options.topology: PD_PAIR is not available in this build yet");
+  if (opt->topology > TOKENSIM_PD_PAIR) return fail(nullptr, TOKENSIM_E_INVALID, "options.topology: unknown");
+  if (opt->topology == TOKENSIM_PD_PAIR && !(opt->pd_link_bw > 0))
+    return fail(nullptr, TOKENSIM_E_INVALID, "options.pd_link_bw: must be > 0 with PD_PAIR");
   if (opt->trace_mode > TOKENSIM_TRACE_FULL) return fail(nullptr, TOKENSIM_E_INVALID, "options.trace_mode: unknown");
   if (opt->trace_mode == TOKENSIM_TRACE_BINNED && opt->trace_bin_ns == 0)
     return fail(nullptr, TOKENSIM_E_INVALID, "options.trace_bin_ns: must be > 0");
@@ -270,6 +271,8 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
     const std::string pp = "policies[" + std::to_string(i) + "].";
     if (p.kind > TOKENSIM_CONT_RATIO) return bad(pp + "kind: unknown");
     if (p.preempt > TOKENSIM_RECOMPUTE) return bad(pp + "preempt: unknown");
+    if (opt->topology == TOKENSIM_PD_PAIR && p.kind == TOKENSIM_CONT_RATIO)
+      return bad(pp + "kind: PD_PAIR supports STATIC and CONT (reading R-PD1)");
     if (p.kind == TOKENSIM_CONT_RATIO && !(p.max_mem_ratio > 0 && p.max_mem_ratio <= 1))
       return bad(pp + "max_mem_ratio: must be in (0, 1]");
     if (p.max_num_seqs < 1 || p.max_num_seqs > 1024) return bad(pp + "max_num_seqs: must be in [1, 1024]");
@@ -368,8 +371,12 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
   }
   h->nwords_max = (u32)((max_words + 31) & ~31ull);
   h->n_hw_axis = n_hw;
-  h->n_points = (u64)n_hw * n_pol * w.num_rates * w.num_seeds;
-  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max);
+  const u64 hw_axis = opt->topology == TOKENSIM_PD_PAIR ? (u64)n_hw * n_hw : (u64)n_hw;
+  h->n_points = hw_axis * n_pol * w.num_rates * w.num_seeds;
+  u64 max_total = 0;
+  for (const DevHP &x : h->dhp) max_total = std::max(max_total, x.total_blocks);
+  h->max_total_blocks = max_total;
+  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max, opt->topology == TOKENSIM_PD_PAIR);
   if (per_warp > 227 * 1024) {
     delete h;
     return fail(nullptr, TOKENSIM_E_INVALID, "max_num_seqs x total_blocks needs more than 227 KB of shared memory per point");
@@ -392,7 +399,8 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   const bool trace_mode = h->wl.len_dist == TOKENSIM_LEN_TRACE;
   const u64 groups = trace_mode ? 1 : (u64)h->rates.size() * h->seeds.size();
   L.n_run = n_run;
-  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max);
+  const bool pd = h->opt.topology == TOKENSIM_PD_PAIR;
+  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max, pd);
   u32 wpb = (u32)std::max<size_t>(1, std::min<size_t>(4, (227 * 1024) / per_warp));
   u32 bps = (u32)std::max<size_t>(1, (227 * 1024) / (per_warp * wpb));
   bps = std::min<u32>(bps, 16);
@@ -422,6 +430,8 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   L.order = take(n_run * 4 + 4);
   L.queue = take(256);
   L.scratch = take(n > kSummarySmemKeys ? n_run * n * 8 : 0);
+  L.ring = take(pd ? (size_t)L.warps_total * h->max_total_blocks * 4 : 0);
+  L.fifo = take(pd ? (size_t)L.warps_total * n * 32 : 0);
   L.total = o;
   return L;
 }
@@ -504,7 +514,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   if (s != TOKENSIM_OK) return s;
   const u64 n_run = count_run(begin, end, stride);
   int sms = device_sms(device);
-  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max);
+  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max, h->opt.topology == TOKENSIM_PD_PAIR);
   Layout L0 = make_layout(h, n_run, sms, 0);
   int occ = 0;
   e = sim_occupancy((int)h->cap, (int)L0.wpb, per_warp * L0.wpb, &occ);
@@ -586,6 +596,9 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.pd_link_inv = h->opt.pd_link_bw > 0 ? 1.0 / h->opt.pd_link_bw : 0.0;
   P.scratch = reinterpret_cast<u64 *>(ws + L.scratch);
   P.ff_enable = (h->opt.flags & TOKENSIM_OPT_NO_FAST_FORWARD) ? 0u : 1u;
+  P.pd_ring = reinterpret_cast<u32 *>(ws + L.ring);
+  P.pd_ring_len = h->max_total_blocks ? h->max_total_blocks : 1;
+  P.pd_fifo = reinterpret_cast<unsigned char *>(ws + L.fifo);
 
   // longest-estimated-first order (LPT): simulated span / per-iteration floor
   std::vector<u32> order(n_run + 1, 0);
@@ -594,7 +607,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
     for (u64 j = 0; j < n_run; ++j) {
       const Coords c = decode_point(begin + j * stride, P.n_pol, P.n_rates, P.n_seeds);
       const double span = (double)P.n_req / h->rates[c.rate];
-      est[j] = {span / h->est_T1[(size_t)c.hw * P.n_pol + c.pol], (u32)j};
+      const u32 hwe = P.topology == TOKENSIM_PD_PAIR ? c.hw % P.n_hw : c.hw;  // decode worker dominates
+      est[j] = {span / h->est_T1[(size_t)hwe * P.n_pol + c.pol], (u32)j};
     }
     std::stable_sort(est.begin(), est.end(), [](const std::pair<double, u32> &a, const std::pair<double, u32> &b) {
       return a.first > b.first;
@@ -834,6 +848,8 @@ tokensim_status tokensim_get_point_profile(const tokensim_sweep *hc, uint64_t po
   out->cycles_ff = st.cyc_ff;
   out->cycles_ff_failed = st.cyc_ff_fail;
   out->cycles_normal = st.cyc_normal;
+  out->n_transfers = st.n_transfers;
+  out->transfer_bytes = st.transfer_bytes;
   for (int q = 0; q < 8; ++q) out->stretch_phase_cycles[q] = st.phase[q];
   return TOKENSIM_OK;
 }
@@ -855,7 +871,7 @@ tokensim_status tokensim_get_run_info(const tokensim_sweep *hc, tokensim_run_inf
   out->n_launches = h->n_launches;
   out->sim_blocks = h->lay.blocks;
   out->sim_warps_per_block = h->lay.wpb;
-  out->smem_per_warp = (u32)sim_smem_per_warp((int)h->cap, h->nwords_max);
+  out->smem_per_warp = (u32)sim_smem_per_warp((int)h->cap, h->nwords_max, h->opt.topology == TOKENSIM_PD_PAIR);
   out->n_run = h->n_run;
   out->h2d_bytes = h->h2d_bytes;
   out->workspace_bytes = h->lay.total;

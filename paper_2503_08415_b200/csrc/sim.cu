@@ -113,7 +113,13 @@ __host__ __device__ inline size_t smem_per_warp_bytes(u32 cap, u32 nwords_max) {
   size_t b = (size_t)cap * (4 * 4 + 8 * 4 + 4 * 2) + 64 * 4 + (size_t)(cap / 32) * 4 + (size_t)nwords_max * 4;
   return (b + 15) & ~(size_t)15;
 }
-size_t sim_smem_per_warp(int cap, u32 nwords_max) { return smem_per_warp_bytes((u32)cap, nwords_max); }
+// P/D extra per warp: slot states, the prefill batch (id, slot, p, o) and P's bitmap
+__host__ __device__ inline size_t smem_pd_extra(u32 cap, u32 nwords_max) {
+  return ((size_t)cap * 4 * 5 + (size_t)nwords_max * 4 + 15) & ~(size_t)15;
+}
+size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd) {
+  return smem_per_warp_bytes((u32)cap, nwords_max) + (pd ? smem_pd_extra((u32)cap, nwords_max) : 0);
+}
 
 __device__ __forceinline__ WarpSmem carve(unsigned char *base, u32 cap) {
   WarpSmem S;
@@ -142,13 +148,13 @@ __device__ __forceinline__ WarpSmem carve(unsigned char *base, u32 cap) {
 // ------------------------------------------------------------------ a.5 allocator
 // Return `held` blocks of table `tbl` to the bitmap (order-free: the block digest is a
 // wrapping sum) and lower the lowest-free-word hint.
-__device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 held, u32 id, u64 k,
+__device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 held, u32 id, u64 k, u32 kind_off,
                                             u64 &dig_b, u32 &hint) {
   u32 mn = 0xffffffffu;
   for (u32 x = lane_id(); x < held; x += 32) {
     const u32 b = tbl[x];
     atomicOr(&bitmap[b >> 5], 1u << (b & 31u));
-    dig_b += fold4(k, 2, id, b);
+    dig_b += fold4(k, 2 + kind_off, id, b);
     mn = min(mn, b >> 5);
   }
   mn = __reduce_min_sync(FULLMASK, mn);
@@ -160,7 +166,7 @@ __device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 hel
 // "serve the requesters one after another with take-the-lowest-free-block" (c.4 steps
 // 3-5, reading A14) done in one bitmap pass.  Entry iteration offsets (fast-forward)
 // shift the digest's iteration index.
-__device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl, u64 k, u64 &dig_b,
+__device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl, u64 k, u32 kind_off, u64 &dig_b,
                               u32 &hint, u32 nwords) {
   const bool unit = E == K;  // every requester takes one block: owner of order index o is o
   const u32 lane = lane_id();
@@ -209,7 +215,7 @@ __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl,
         const u32 tpos = PT_TPOS(pt) + (o - start);
         const u32 slot = S.info[pos] & 0xffffu;
         bt[(size_t)slot * btl + tpos] = blk;
-        dig_b += fold4(k + PT_J(pt), 1, S.id[pos], blk);
+        dig_b += fold4(k + PT_J(pt), 1 + kind_off, S.id[pos], blk);
       }
     }
     const u32 tk = take > before ? min(c, take - before) : 0u;
@@ -289,6 +295,8 @@ __device__ __forceinline__ i64 scan_incl_i64(i64 x) {
   }
   return x;
 }
+
+#include "sim_pd.cuh"
 
 // ------------------------------------------------------------------ a.2-a.7 one point
 // Everything is executed by all 32 lanes; scalar state is lane-uniform in registers.
@@ -631,7 +639,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
                 __syncwarp();
               }
             }
-            if (!alloc_ordered(S, Ktot, Ktot, bt, btl, k, dig_b, hint, nwords)) {
+            if (!alloc_ordered(S, Ktot, Ktot, bt, btl, k, 0, dig_b, hint, nwords)) {
               flags |= TOKENSIM_PT_INTERNAL_ERROR;
               break;
             }
@@ -689,7 +697,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               const u32 pos = b0 + l;
               const u32 held = B.cdiv(S.ctx[pos]);
               const u32 slot = S.info[pos] & 0xffffu;
-              free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, dig_b, hint);
+              free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, 0, dig_b, hint);
               nfree += held;
               if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
             }
@@ -832,7 +840,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 c = S.ctx[v];
         const u32 held = B.cdiv(c);
         const u32 slot = S.info[v] & 0xffffu;
-        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, dig_b, hint);
+        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, 0, dig_b, hint);
         nfree += held;
         csub += c + 1;
         if (SWAPM) swap_out += (u64)held * HP.block_bytes;
@@ -985,7 +993,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     // 6. empty batch (every candidate rejected): back to 0 without advancing t
     if (nR == 0) continue;
     // block extraction for all requesters of this iteration, in phase order
-    if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, dig_b, hint, nwords)) {
+    if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, 0, dig_b, hint, nwords)) {
       flags |= TOKENSIM_PT_INTERNAL_ERROR;
       break;
     }
@@ -1048,7 +1056,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 c = S.ctx[pos];
         const u32 held = B.cdiv(c);
         const u32 slot = S.info[pos] & 0xffffu;
-        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, dig_b, hint);
+        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, 0, dig_b, hint);
         nfree += held;
         if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
       }
@@ -1207,7 +1215,9 @@ template <int CAP>
 __global__ void __launch_bounds__(128) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
-  const size_t per_warp = smem_per_warp_bytes(CAP, P.nwords_max);
+  const bool pd = P.topology == TOKENSIM_PD_PAIR;
+  const size_t base = smem_per_warp_bytes(CAP, P.nwords_max);
+  const size_t per_warp = base + (pd ? smem_pd_extra(CAP, P.nwords_max) : 0);
   const WarpSmem S = carve(smem_raw + wib * per_warp, CAP);
   const u32 gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
   u32 *bt = P.bt + (size_t)gwarp * 2 * CAP * P.bt_len;
@@ -1217,7 +1227,8 @@ __global__ void __launch_bounds__(128) sim_kernel(SweepParams P) {
     qi = __shfl_sync(FULLMASK, qi, 0);
     if ((u64)qi >= P.n_run) break;
     const u64 j = P.order[qi];
-    simulate_unified<CAP>(P, j, S, bt);
+    if (pd) simulate_pd<CAP>(P, j, S, smem_raw + wib * per_warp + base, bt);
+    else simulate_unified<CAP>(P, j, S, bt);
   }
 }
 

@@ -102,6 +102,9 @@ struct SweepParams {
   double pd_link_inv;  // 1 / pd_link_bw
   u64 *scratch;        // summary keys when n_req exceeds the shared-memory key buffer
   u32 ff_enable, pad1; // time-parallel evaluation of quiescent decode stretches (H3)
+  u32 *pd_ring;        // P/D: per-warp ring of P block ids [warp][pd_ring_len]
+  u64 pd_ring_len;
+  unsigned char *pd_fifo;  // P/D: per-warp pending/transfer FIFO [warp][n_req] x 32 B
 };
 
 // point -> grid coordinates (row-major)
@@ -127,7 +130,7 @@ cudaError_t launch_summary(const SweepParams &p, cudaStream_t st);
 cudaError_t launch_quantiles(const SweepParams &p, u64 j, u32 metric, const u32 *d_ranks, u32 n_q,
                              double *d_out, u64 *d_keys, cudaStream_t st);
 constexpr u32 kSummarySmemKeys = 12288;  // keys held in shared memory by summary_kernel
-size_t sim_smem_per_warp(int cap, u32 nwords_max);
+size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd);
 cudaError_t sim_occupancy(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
 
 }  // namespace ts

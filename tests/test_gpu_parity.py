@@ -199,3 +199,72 @@ def test_fast_forward_is_bit_identical(api):
             assert on.mem_trace(p).tobytes() == off.mem_trace(p).tobytes()
         if cfg.options.iteration_trace_cap:
             assert on.iteration_trace(0).tobytes() == off.iteration_trace(0).tobytes()
+
+
+# ------------------------------------------------------------------ a.9 P/D pair
+def check_pd_points(sw, cfg, points, iters=False):
+    want = ("summary", "records", "trace") + (("iters",) if iters else ())
+    ora = oracle_points(cfg, points, want=want)
+    bad = []
+    for p in points:
+        o = ora[p]
+        bad += compare_summary(sw.summary(p), o["summary"], p)
+        bad += compare_records(sw.records(p), o["records"], p)
+        for w in (0, 1):
+            bad += compare_trace(sw.mem_trace(p, w), o["trace"][w], p)
+        prof = sw.point_profile(p)
+        if (prof["n_transfers"], prof["transfer_bytes"]) != (o["summary"]["n_transfers"], o["summary"]["transfer_bytes"]):
+            bad.append(f"point {p}: transfers gpu={prof['n_transfers']},{prof['transfer_bytes']} "
+                       f"oracle={o['summary']['n_transfers']},{o['summary']['transfer_bytes']}")
+        if iters:
+            g, oi = sw.iteration_trace(p), o["iters"]
+            pairs = [("k", "k"), ("t_start_ns", "t_start"), ("T_ns", "T_ns"), ("n_prefill", "S_p"),
+                     ("n_decode", "D"), ("n_admitted", "n_admitted"), ("n_finished", "n_finished"),
+                     ("blocks_in_use", "blocks"), ("worker", "worker")]
+            for i in range(min(len(g), len(oi))):
+                diff = [f for f, of in pairs if int(g[f][i]) != int(oi[of][i])]
+                if diff:
+                    bad.append(f"point {p}: first divergent PD iteration {i}: {diff}")
+                    break
+    assert not bad, "\n".join(bad[:20])
+
+
+def _micro_pd(rng):
+    n = int(rng.integers(1, 60))
+    a = np.sort(rng.integers(0, 2_000_000_000, n))
+    p = rng.integers(1, 64, n)
+    o = rng.integers(1, 64, n)
+    mml = 128
+    model = replace(si.LLAMA2_7B, max_model_len=mml)
+    bs = int(rng.choice([4, 16]))
+    mb = -(-mml // bs)
+    hws = [replace(si.A100, kv_blocks_override=int(rng.integers(mb, mb + 30)),
+                   peak_flops=float(rng.choice([78e12, 312e12])), mem_bw=float(rng.choice([1e12, 4e12])))
+           for _ in range(2)]
+    pol = si.Policy(kind=str(rng.choice([si.STATIC, si.CONT])), preempt=str(rng.choice([si.SWAP, si.RECOMPUTE])),
+                    max_num_seqs=int(rng.choice([2, 8, 256])), block_size=bs)
+    w = si.Workload(n, [1.0], [0], len_dist=si.TRACE, trace_arrival_ns=a.tolist(), trace_prompt=p.tolist(),
+                    trace_output=o.tolist(), prompt_table=None, output_table=None)
+    opts = si.Options(topology=si.PD_PAIR, pd_link_bw=float(rng.choice([1e9, 200e9])),
+                      trace_mode=str(rng.choice([si.FULL, si.BINNED])), trace_bin_ns=50_000_000,
+                      iteration_trace_cap=1 << 16)
+    return si.SweepConfig("micro-pd", model, hws, [pol], w, opts)
+
+
+def test_pd_micro_configs(api):
+    rng = np.random.default_rng(17)
+    for _ in range(40):
+        cfg = _micro_pd(rng)
+        sw = run_gpu(api, cfg)
+        check_pd_points(sw, cfg, list(range(cfg.num_points)), iters=True)
+
+
+def test_c5_reduced_grid(api):
+    """C5's 16x16 (P, D) profile pairs x {SWAP, RECOMPUTE}, 3 of its rates, 300 requests per point."""
+    base = si.c5()
+    cfg = replace(si.subset(base, rates=[0, 8, 15], seeds=[0]), workload=replace(
+        si.subset(base, rates=[0, 8, 15], seeds=[0]).workload, num_requests=300))
+    sw = run_gpu(api, cfg)
+    s = sw.summaries()
+    assert (s["n_finished"] == 300).all() and (s["status_flags"] & 16 == 0).all()
+    check_pd_points(sw, cfg, sample_points(cfg.num_points, target=40, corners=[0, 1, 767, 768, 1535]))
