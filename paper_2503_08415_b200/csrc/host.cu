@@ -33,7 +33,8 @@ const uint32_t kOutputThr[7] = {429496730u, 773094113u, 1159641170u, 1717986918u
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, ring, fifo, total;
+  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, ring, fifo, evlog, itlog,
+      total;
   u64 n_run;
   u32 warps_total, wpb, blocks;
   size_t smem;
@@ -432,6 +433,8 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   L.scratch = take(n > kSummarySmemKeys ? n_run * n * 8 : 0);
   L.ring = take(pd ? (size_t)L.warps_total * h->max_total_blocks * 4 : 0);
   L.fifo = take(pd ? (size_t)L.warps_total * n * 32 : 0);
+  L.evlog = take((size_t)L.warps_total * 1024 * 16);
+  L.itlog = take((size_t)L.warps_total * 256 * 64);
   L.total = o;
   return L;
 }
@@ -599,6 +602,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.pd_ring = reinterpret_cast<u32 *>(ws + L.ring);
   P.pd_ring_len = h->max_total_blocks ? h->max_total_blocks : 1;
   P.pd_fifo = reinterpret_cast<unsigned char *>(ws + L.fifo);
+  P.evlog = reinterpret_cast<uint4 *>(ws + L.evlog);
+  P.itlog = reinterpret_cast<ulonglong2 *>(ws + L.itlog);
 
   // longest-estimated-first order (LPT): simulated span / per-iteration floor
   std::vector<u32> order(n_run + 1, 0);

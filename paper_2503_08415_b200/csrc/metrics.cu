@@ -162,10 +162,19 @@ __global__ void __launch_bounds__(256) summary_kernel(SweepParams P, u64 *scratc
   const i64 slo_t = P.slo_ttft_ns, slo_m = P.slo_mtpot_ns;
 
   // counts for goodput, sums for integer means
-  u64 g_mt = 0, g_both = 0, s_ttft = 0, s_e2e = 0, s_mt = 0;
+  u64 g_mt = 0, g_both = 0, s_ttft = 0, s_e2e = 0, s_mt = 0, dig_r = 0;
   for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
     const tokensim_request_record r = rec[i];
     if (r.status != TOKENSIM_REQ_FINISHED) continue;
+    // request digest (c.6): fold(id, ttft, e2e, mtpot, n_preempt, finish_k), wrapping sum
+    u64 h = FOLD_INIT;
+    h = mix64(h ^ (u64)i);
+    h = mix64(h ^ (u64)r.ttft_ns);
+    h = mix64(h ^ (u64)r.e2e_ns);
+    h = mix64(h ^ (u64)r.mtpot_ns);
+    h = mix64(h ^ (u64)r.n_preempt);
+    h = mix64(h ^ (u64)r.finish_iter);
+    dig_r += h;
     s_ttft += (u64)r.ttft_ns;
     s_e2e += (u64)r.e2e_ns;
     s_mt += (u64)r.mtpot_ns;
@@ -179,6 +188,7 @@ __global__ void __launch_bounds__(256) summary_kernel(SweepParams P, u64 *scratc
   s_ttft = block_reduce_u64(s_ttft, false, sh);
   s_e2e = block_reduce_u64(s_e2e, false, sh);
   s_mt = block_reduce_u64(s_mt, false, sh);
+  dig_r = block_reduce_u64(dig_r, false, sh);
   // sequential fp64 sums for TPOT / NORM in ascending id (SURVEY c.6)
   __shared__ double seq_tp, seq_norm;
   if (threadIdx.x == 0) {
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(256) summary_kernel(SweepParams P, u64 *scratc
     S.last_finish_ns = st.last_finish;
     S.sched_digest = st.sched_d;
     S.block_digest = st.block_d;
-    S.request_digest = st.req_d;
+    S.request_digest = dig_r;
     S.total_blocks = (u32)st.total_blocks;
     S.peak_blocks = (u32)st.peak_blocks;
     S.mean_util = (st.t_final > 0 && st.total_blocks > 0)

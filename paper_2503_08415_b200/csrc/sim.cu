@@ -145,17 +145,53 @@ __device__ __forceinline__ WarpSmem carve(unsigned char *base, u32 cap) {
 #define PT_J(pt) (((pt) >> 10) & 31u)
 #define PT_TPOS(pt) ((pt) >> 15)
 
+// ------------------------------------------------------------------ digest logs
+// Digest terms are not folded on the per-iteration dependency chain: block events and
+// per-iteration schedule fields are appended to small per-warp logs in global memory and
+// folded lane-parallel when a log fills (the digests are wrapping sums: order-free).
+constexpr u32 EVCAP = 1024;  // block events per flush
+constexpr u32 ITCAP = 256;   // iterations per flush
+struct Logs {
+  uint4 *ev;
+  ulonglong2 *it;               // 4 x 16 B per iteration entry
+  tokensim_iter_record *itr;
+  u64 it_cap, it_base;          // processing-order index of it[0]
+  u64 dig_s, dig_b;             // per-lane partial sums
+  u32 nev, nit;
+};
+
+__device__ __noinline__ void ev_flush(Logs &L) {
+  __syncwarp();
+  for (u32 x = lane_id(); x < L.nev; x += 32) {
+    const uint4 e = L.ev[x];
+    L.dig_b += fold4(e.x, e.y, e.z, e.w);
+  }
+  L.nev = 0;
+  __syncwarp();
+}
+__device__ __forceinline__ void ev_reserve(Logs &L, u32 cnt) {
+  if (L.nev + cnt > EVCAP) ev_flush(L);
+}
+__device__ __forceinline__ void ev_put(Logs &L, u32 idx, u64 k, u32 kind, u32 id, u32 blk) {
+  L.ev[L.nev + idx] = make_uint4((u32)k, kind, id, blk);
+}
+
 // ------------------------------------------------------------------ a.5 allocator
 // Return `held` blocks of table `tbl` to the bitmap (order-free: the block digest is a
 // wrapping sum) and lower the lowest-free-word hint.
 __device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 held, u32 id, u64 k, u32 kind_off,
-                                            u64 &dig_b, u32 &hint) {
+                                            Logs &L, u32 &hint) {
   u32 mn = 0xffffffffu;
-  for (u32 x = lane_id(); x < held; x += 32) {
-    const u32 b = tbl[x];
-    atomicOr(&bitmap[b >> 5], 1u << (b & 31u));
-    dig_b += fold4(k, 2 + kind_off, id, b);
-    mn = min(mn, b >> 5);
+  for (u32 x0 = 0; x0 < held; x0 += 32) {
+    ev_reserve(L, 32);
+    const u32 x = x0 + lane_id();
+    if (x < held) {
+      const u32 b = tbl[x];
+      atomicOr(&bitmap[b >> 5], 1u << (b & 31u));
+      ev_put(L, x - x0, k, 2 + kind_off, id, b);
+      mn = min(mn, b >> 5);
+    }
+    L.nev += min(32u, held - x0);
   }
   mn = __reduce_min_sync(FULLMASK, mn);
   hint = min(hint, mn);
@@ -166,7 +202,7 @@ __device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 hel
 // "serve the requesters one after another with take-the-lowest-free-block" (c.4 steps
 // 3-5, reading A14) done in one bitmap pass.  Entry iteration offsets (fast-forward)
 // shift the digest's iteration index.
-__device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl, u64 k, u32 kind_off, u64 &dig_b,
+__device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl, u64 k, u32 kind_off, Logs &L,
                               u32 &hint, u32 nwords) {
   const bool unit = E == K;  // every requester takes one block: owner of order index o is o
   const u32 lane = lane_id();
@@ -185,6 +221,7 @@ __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl,
     const u32 take = min(tot, K - o_base);
     const u32 before = cum - c;
     for (u32 r0 = 0; r0 < take; r0 += 32) {
+      ev_reserve(L, 32);
       const u32 idx = r0 + lane;
       const bool act = idx < take;
       const u32 tgt = act ? idx : 0u;
@@ -215,8 +252,9 @@ __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl,
         const u32 tpos = PT_TPOS(pt) + (o - start);
         const u32 slot = S.info[pos] & 0xffffu;
         bt[(size_t)slot * btl + tpos] = blk;
-        dig_b += fold4(k + PT_J(pt), 1 + kind_off, S.id[pos], blk);
+        ev_put(L, idx - r0, k + PT_J(pt), 1 + kind_off, S.id[pos], blk);
       }
+      L.nev += min(32u, take - r0);
     }
     const u32 tk = take > before ? min(c, take - before) : 0u;
     if (tk && wi < nwords) {
@@ -286,6 +324,54 @@ __device__ __forceinline__ u64 sched_fold(u64 k, i64 ts, i64 T, u64 Sp, u64 D, u
   return h;
 }
 
+// iteration entry: k (worker in bit 40), t_start, T, N_p, C_d, blocks,
+// S_p | D<<16 | m<<32 | n_resumed<<48, n_admitted | n_finished<<16 | n_rejected<<32
+__device__ __noinline__ void it_flush(Logs &L) {
+  __syncwarp();
+  for (u32 x = lane_id(); x < L.nit; x += 32) {
+    const ulonglong2 a = L.it[4 * x], b = L.it[4 * x + 1], c = L.it[4 * x + 2], d = L.it[4 * x + 3];
+    const u64 k = a.x, Np = b.y, Cd = c.x, blocks = c.y, w6 = d.x, w7 = d.y;
+    const i64 ts = (i64)a.y, T = (i64)b.x;
+    const u64 Sp = w6 & 0xffff, D = (w6 >> 16) & 0xffff, m = (w6 >> 32) & 0xffff, nres = w6 >> 48;
+    const u64 nadm = w7 & 0xffff, nfin = (w7 >> 16) & 0xffff, nrej = w7 >> 32;
+    L.dig_s += sched_fold(k, ts, T, Sp, D, Np, Cd, m, nres, nadm, nrej, nfin, blocks);
+    const u64 idx = L.it_base + x;
+    if (idx < L.it_cap) {
+      tokensim_iter_record ir;
+      ir.k = k & ((1ull << 40) - 1);
+      ir.t_start_ns = ts;
+      ir.T_ns = T;
+      ir.n_prefill = (u32)Sp;
+      ir.n_decode = (u32)D;
+      ir.N_p = Np;
+      ir.C_d = Cd;
+      ir.n_preempted = (u32)m;
+      ir.n_resumed = (u32)nres;
+      ir.n_admitted = (u32)nadm;
+      ir.n_rejected = (u32)nrej;
+      ir.n_finished = (u32)nfin;
+      ir.blocks_in_use = (u32)blocks;
+      ir.worker = (u32)(k >> 40);
+      ir.pad = 0;
+      L.itr[idx] = ir;
+    }
+  }
+  L.it_base += L.nit;
+  L.nit = 0;
+  __syncwarp();
+}
+__device__ __forceinline__ void it_reserve(Logs &L, u32 cnt) {
+  if (L.nit + cnt > ITCAP) it_flush(L);
+}
+__device__ __forceinline__ void it_put(Logs &L, u32 idx, u64 k, i64 ts, i64 T, u64 Np, u64 Cd, u64 blocks, u64 Sp,
+                                       u64 D, u64 m, u64 nres, u64 nadm, u64 nfin, u64 nrej) {
+  ulonglong2 *e = L.it + 4 * (size_t)(L.nit + idx);
+  e[0] = make_ulonglong2(k, (unsigned long long)ts);
+  e[1] = make_ulonglong2((unsigned long long)T, Np);
+  e[2] = make_ulonglong2(Cd, blocks);
+  e[3] = make_ulonglong2(Sp | (D << 16) | (m << 32) | (nres << 48), nadm | (nfin << 16) | (nrej << 32));
+}
+
 __device__ __forceinline__ i64 scan_incl_i64(i64 x) {
   const u32 l = lane_id();
 #pragma unroll
@@ -349,7 +435,18 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   u64 nfree = total;
   u32 hint = 0;
   u32 rmin = 0;  // min rem over R after the last commit (0 when unknown / R empty)
-  u64 dig_s = 0, dig_b = 0, dig_r = 0;  // per-lane partial digests
+  u64 ff_mem_wait = 0, ff_mem_k = 0;  // after a memory-cut failure: skip attempts while nfree <= wait, k < k
+  const u32 gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  Logs L;
+  L.ev = P.evlog + (size_t)gwarp * EVCAP;
+  L.it = P.itlog + (size_t)gwarp * ITCAP * 4;
+  L.itr = itr;
+  L.it_cap = P.it_cap;
+  L.it_base = 0;
+  L.dig_s = 0;
+  L.dig_b = 0;
+  L.nev = 0;
+  L.nit = 0;
   u64 req_iters = 0, npre = 0, swo_tot = 0, swi_tot = 0, nrej_tot = 0, nfin_tot = 0, peak = 0, bns = 0;
   u64 ff_iters = 0, ff_runs = 0;
   u64 cyc_ff = 0, cyc_ff_fail = 0, cyc_normal = 0;
@@ -364,43 +461,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   i64 last_fin = 0;
   u32 flags = 0;
   u32 hd_idx = 0xffffffffu, hd_p = 0;  // cached prompt length of the fresh-queue head
-  // sched-field buffer: lane nbuf holds a normal iteration's fields until 32 are buffered
-  i64 b_t = 0, b_T = 0;
-  u64 b_np = 0, b_cd = 0, b_k = 0;
-  u32 b_blk = 0, b_spd = 0, b_mres = 0, b_adfin = 0, b_rej = 0;
-  bool b_valid = false;
-  u32 nbuf = 0;
-  auto put_iter = [&](u64 kk, i64 ts_, i64 T_, u32 Sp_, u32 D_, u64 Np_, u64 Cd_, u32 m_, u32 nres_, u32 nadm_,
-                      u32 nrej_, u32 nfin_, u32 blk_) {
-    if (kk < P.it_cap) {
-      tokensim_iter_record ir;
-      ir.k = kk;
-      ir.t_start_ns = ts_;
-      ir.T_ns = T_;
-      ir.n_prefill = Sp_;
-      ir.n_decode = D_;
-      ir.N_p = Np_;
-      ir.C_d = Cd_;
-      ir.n_preempted = m_;
-      ir.n_resumed = nres_;
-      ir.n_admitted = nadm_;
-      ir.n_rejected = nrej_;
-      ir.n_finished = nfin_;
-      ir.blocks_in_use = blk_;
-      ir.worker = 0;
-      ir.pad = 0;
-      itr[kk] = ir;
-    }
-  };
-  auto flush_sched = [&]() {
-    if (b_valid) {
-      dig_s += sched_fold(b_k, b_t, b_T, b_spd & 0xffffu, b_spd >> 16, b_np, b_cd, b_mres & 0xffffu, b_mres >> 16,
-                          b_adfin & 0xffffu, b_rej, b_adfin >> 16, b_blk);
-      put_iter(b_k, b_t, b_T, b_spd & 0xffffu, b_spd >> 16, b_np, b_cd, b_mres & 0xffffu, b_mres >> 16,
-               b_adfin & 0xffffu, b_rej, b_adfin >> 16, b_blk);
-    }
-    b_valid = false;
-  };
   // memory trace state (lane-uniform)
   const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
   const bool FULLT = P.trace_mode == TOKENSIM_TRACE_FULL;
@@ -466,7 +526,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     // ---------------------------------------------------------------- fast-forward (H3)
     clk_a = clock64();
     clk_p = clk_a;
-    if (ff_on && nR > 0 && rmin >= 2) {
+    if (ff_on && nR > 0 && rmin >= 2 && (nfree > ff_mem_wait || k >= ff_mem_k)) {
       // The stretch must admit nothing and resume nothing.  With Q != {} fresh admission is
       // off (c.4 step 5) and a Q head that cannot resume now cannot resume later (R frozen,
       // free count only falls).  With Q = {}: STATIC never admits while R != {}; an empty fresh
@@ -563,6 +623,12 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         }
         const u32 okm = __ballot_sync(FULLMASK, ok);
         const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+        // a stretch cut short by memory will not grow until blocks come back: remember the level
+        const u32 memcut = __ballot_sync(FULLMASK, !((u64)Aj <= nfree));
+        if (J < 2 && memcut && (u32)(__ffs(memcut) - 1) < 2) {
+          ff_mem_wait = nfree;
+          ff_mem_k = k + 4;  // the needs pattern shifts with the ctx residues: retry soon anyway
+        }
         if (J >= 2) {
           const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
           PH(1);
@@ -579,6 +645,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             const u32 cw = __popc(word);
             const u32 cum = scan_incl(cw);
             if (__shfl_sync(FULLMASK, cum, 31) >= Ktot) {
+              ev_reserve(L, 32);
               const bool act = lane < Ktot;
               const u32 o = act ? lane : 0u;
               u32 jb = 0;
@@ -602,8 +669,9 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
                 const u32 blk = (hint + lo) * 32 + select_bit(wv, o - bv);
                 const u32 tpos = B.div(S.ctx[pos] + jb);
                 bt[(size_t)(S.info[pos] & 0xffffu) * btl + tpos] = blk;
-                dig_b += fold4(k + jb, 1, S.id[pos], blk);
+                ev_put(L, o, k + jb, 1, S.id[pos], blk);
               }
+              L.nev += Ktot;
               const u32 before = cum - cw;
               const u32 tk = Ktot > before ? min(cw, Ktot - before) : 0u;
               if (tk && wi < nwords) {
@@ -639,7 +707,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
                 __syncwarp();
               }
             }
-            if (!alloc_ordered(S, Ktot, Ktot, bt, btl, k, 0, dig_b, hint, nwords)) {
+            if (!alloc_ordered(S, Ktot, Ktot, bt, btl, k, 0, L, hint, nwords)) {
               flags |= TOKENSIM_PT_INTERNAL_ERROR;
               break;
             }
@@ -675,14 +743,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
                 const i64 ttft = S.ttft[jj], e2e = tend - S.arr[jj];
                 const u32 np_ = S.info[jj] >> 16;
                 write_record(rec + id, ttft, e2e, mg, np_, TOKENSIM_REQ_FINISHED, (u32)klast);
-                u64 h = FOLD_INIT;
-                h = mix64(h ^ (u64)id);
-                h = mix64(h ^ (u64)ttft);
-                h = mix64(h ^ (u64)e2e);
-                h = mix64(h ^ (u64)mg);
-                h = mix64(h ^ (u64)np_);
-                h = mix64(h ^ klast);
-                dig_r += h;
               } else {
                 rmin_l = min(rmin_l, r);
               }
@@ -697,7 +757,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               const u32 pos = b0 + l;
               const u32 held = B.cdiv(S.ctx[pos]);
               const u32 slot = S.info[pos] & 0xffffu;
-              free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, 0, dig_b, hint);
+              free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, 0, L, hint);
               nfree += held;
               if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
             }
@@ -706,11 +766,9 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           PH(3);
           // iteration records, digests, counters (lanes j < J)
           const u64 blkj = blk0 + Aj;
-          if (lj) {
-            const u32 nf = lane == J - 1 ? nfin : 0u;
-            dig_s += sched_fold(k + lane, tsj, Tj, 0, nR, 0, Cdj, 0, 0, 0, 0, nf, blkj);
-            put_iter(k + lane, tsj, Tj, 0, nR, 0, Cdj, 0, 0, 0, 0, nf, (u32)blkj);
-          }
+          it_reserve(L, 32);
+          if (lj) it_put(L, lane, k + lane, tsj, Tj, 0, Cdj, blkj, 0, nR, 0, 0, 0, lane == J - 1 ? nfin : 0u, 0);
+          L.nit += J;
           const u64 bns_add = warp_sum64(lj ? blkj * (u64)Tj : 0ull);
           PH(4);
           // memory trace
@@ -840,7 +898,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 c = S.ctx[v];
         const u32 held = B.cdiv(c);
         const u32 slot = S.info[v] & 0xffffu;
-        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, 0, dig_b, hint);
+        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, 0, L, hint);
         nfree += held;
         csub += c + 1;
         if (SWAPM) swap_out += (u64)held * HP.block_bytes;
@@ -993,7 +1051,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     // 6. empty batch (every candidate rejected): back to 0 without advancing t
     if (nR == 0) continue;
     // block extraction for all requesters of this iteration, in phase order
-    if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, 0, dig_b, hint, nwords)) {
+    if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, 0, L, hint, nwords)) {
       flags |= TOKENSIM_PT_INTERNAL_ERROR;
       break;
     }
@@ -1033,14 +1091,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const i64 ttft = S.ttft[jj], e2e = te - S.arr[jj], mt = S.maxgap[jj];
           const u32 np_ = S.info[jj] >> 16;
           write_record(rec + id, ttft, e2e, mt, np_, TOKENSIM_REQ_FINISHED, (u32)k);
-          u64 h = FOLD_INIT;
-          h = mix64(h ^ (u64)id);
-          h = mix64(h ^ (u64)ttft);
-          h = mix64(h ^ (u64)e2e);
-          h = mix64(h ^ (u64)mt);
-          h = mix64(h ^ (u64)np_);
-          h = mix64(h ^ k);
-          dig_r += h;
         } else {
           rmin_l = min(rmin_l, r);
         }
@@ -1056,7 +1106,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 c = S.ctx[pos];
         const u32 held = B.cdiv(c);
         const u32 slot = S.info[pos] & 0xffffu;
-        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, 0, dig_b, hint);
+        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, 0, L, hint);
         nfree += held;
         if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
       }
@@ -1105,24 +1155,10 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       last_fin = te;
     }
     if (nR == 0) rmin = 0;
-    // schedule digest fields (buffered; folded 32 iterations at a time)
-    if (lane == nbuf) {
-      b_k = k;
-      b_t = ts;
-      b_T = T;
-      b_spd = Sp | (D << 16);
-      b_np = Np;
-      b_cd = Cd;
-      b_mres = m | (nres << 16);
-      b_adfin = nadm | (nfin << 16);
-      b_rej = nrej;
-      b_blk = (u32)blocks;
-      b_valid = true;
-    }
-    if (++nbuf == 32) {
-      flush_sched();
-      nbuf = 0;
-    }
+    // schedule digest fields (logged; folded lane-parallel when the log fills)
+    it_reserve(L, 1);
+    if (lane == 0) it_put(L, 0, k, ts, T, Np, Cd, blocks, Sp, D, m, nres, nadm, nfin, nrej);
+    L.nit += 1;
     peak = blocks > peak ? blocks : peak;
     bns += blocks * (u64)T;
     swo_tot += swap_out;
@@ -1163,7 +1199,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     ++k;
     cyc_normal += (u64)(clock64() - clk_a);
   }
-  flush_sched();
+  ev_flush(L);
+  it_flush(L);
   if (BINNED) {
     while ((i64)bin * W < t) flush_bin();
   }
@@ -1172,9 +1209,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     const u32 id = S.id[x];
     write_record(rec + id, S.ttft[x], 0, 0, S.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);
   }
-  dig_s = warp_sum64(dig_s);
-  dig_b = warp_sum64(dig_b);
-  dig_r = warp_sum64(dig_r);
+  const u64 dig_s = warp_sum64(L.dig_s);
+  const u64 dig_b = warp_sum64(L.dig_b);
   if (lane == 0) {
     SimStats st;
     st.flags = flags | ((nrej_tot == n) ? (u32)TOKENSIM_PT_ALL_REJECTED : 0u);
@@ -1190,7 +1226,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     st.t_final = t;
     st.sched_d = dig_s;
     st.block_d = dig_b;
-    st.req_d = dig_r;
+    st.req_d = 0;  // computed from the records by summary_kernel
     st.total_blocks = total;
     st.peak_blocks = peak;
     st.block_ns_sum = bns;

@@ -161,7 +161,16 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
   u32 nD = 0, nX = 0, nQ = 0, nRun = 0;  // D slots: all / in-flight (tail) / preempted / running
   u32 ftail = 0, fpfree = 0, fdadm = 0, fvis = 0;
   u64 ring_tail = 0;
-  u64 dig_s = 0, dig_b = 0, dig_r = 0;
+  Logs L;
+  L.ev = P.evlog + (size_t)gwarp * EVCAP;
+  L.it = P.itlog + (size_t)gwarp * ITCAP * 4;
+  L.itr = itr;
+  L.it_cap = P.it_cap;
+  L.it_base = 0;
+  L.dig_s = 0;
+  L.dig_b = 0;
+  L.nev = 0;
+  L.nit = 0;
   u64 req_iters = 0, npre = 0, swo = 0, swi = 0, nrej_tot = 0, nfin_tot = 0, peakD = 0, bnsD = 0, n_xfer = 0,
       xbytes = 0;
   u32 flags = 0;
@@ -185,42 +194,10 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
   load_win(0);
   auto fold_iter = [&](u64 kk, u32 worker, i64 ts, i64 T, u64 Sp, u64 D_, u64 Np, u64 Cd, u64 m, u64 nres,
                        u64 nadm, u64 nrej, u64 nfin, u64 blocks) {
-    // every lane holds the same value; lane 0 contributes (digest partials are summed at the end)
-    const u64 h = sched_fold(kk | ((u64)worker << 40), ts, T, Sp, D_, Np, Cd, m, nres, nadm, nrej, nfin, blocks);
-    if (lane == 0) {
-      dig_s += h;
-      if (nit < P.it_cap) {
-        tokensim_iter_record ir;
-        ir.k = kk;
-        ir.t_start_ns = ts;
-        ir.T_ns = T;
-        ir.n_prefill = (u32)Sp;
-        ir.n_decode = (u32)D_;
-        ir.N_p = Np;
-        ir.C_d = Cd;
-        ir.n_preempted = (u32)m;
-        ir.n_resumed = (u32)nres;
-        ir.n_admitted = (u32)nadm;
-        ir.n_rejected = (u32)nrej;
-        ir.n_finished = (u32)nfin;
-        ir.blocks_in_use = (u32)blocks;
-        ir.worker = worker;
-        ir.pad = 0;
-        itr[nit] = ir;
-      }
-    }
+    it_reserve(L, 1);
+    if (lane == 0) it_put(L, 0, kk | ((u64)worker << 40), ts, T, Np, Cd, blocks, Sp, D_, m, nres, nadm, nfin, nrej);
+    L.nit += 1;
     ++nit;
-  };
-  auto finish_record = [&](u32 id, i64 ttft, i64 e2e, i64 mt, u32 npr, u64 kk) {
-    write_record(rec + id, ttft, e2e, mt, npr, TOKENSIM_REQ_FINISHED, (u32)kk);
-    u64 h = FOLD_INIT;
-    h = mix64(h ^ (u64)id);
-    h = mix64(h ^ (u64)ttft);
-    h = mix64(h ^ (u64)e2e);
-    h = mix64(h ^ (u64)mt);
-    h = mix64(h ^ (u64)npr);
-    h = mix64(h ^ kk);
-    return h;
   };
   auto xfer_ns = [&](u32 p) -> i64 {
     const u64 bytes = (u64)p * P.M.kvb;
@@ -292,8 +269,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
           } while (stt[vpos] != ST_RUN);
           const u32 c = S.ctx[vpos];
           const u32 held = B.cdiv(c);
-          free_blocks(S.bitmap, btD + (size_t)(S.info[vpos] & 0xffffu) * btl, held, S.id[vpos], kD, 2, dig_b,
-                      hintD);
+          free_blocks(S.bitmap, btD + (size_t)(S.info[vpos] & 0xffffu) * btl, held, S.id[vpos], kD, 2, L, hintD);
           nfreeD += held;
           csub += c + 1;
           if (SWAPM) swap_out += (u64)held * HPD.block_bytes;
@@ -444,7 +420,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
           }
         }
       }
-      if (Kb > 0 && !alloc_ordered(S, E, Kb, btD, btl, kD, 2, dig_b, hintD, nwD)) {
+      if (Kb > 0 && !alloc_ordered(S, E, Kb, btD, btl, kD, 2, L, hintD, nwD)) {
         flags |= TOKENSIM_PT_INTERNAL_ERROR;
         break;
       }
@@ -483,7 +459,9 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
             if (gap > S.maxgap[jj]) S.maxgap[jj] = gap;
             S.last[jj] = te;
             fin = r == 0;
-            if (fin) dig_r += finish_record(S.id[jj], S.ttft[jj], te - S.arr[jj], S.maxgap[jj], S.info[jj] >> 16, kD);
+            if (fin)
+              write_record(rec + S.id[jj], S.ttft[jj], te - S.arr[jj], S.maxgap[jj], S.info[jj] >> 16,
+                           TOKENSIM_REQ_FINISHED, (u32)kD);
           }
         }
         u32 fm = __ballot_sync(FULLMASK, fin);
@@ -496,7 +474,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
           const u32 pos = b0 + l;
           const u32 held = B.cdiv(S.ctx[pos]);
           const u32 slot = S.info[pos] & 0xffffu;
-          free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], kD, 2, dig_b, hintD);
+          free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], kD, 2, L, hintD);
           nfreeD += held;
           if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
         }
@@ -562,11 +540,16 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       while (fpfree < fdadm && pf_end <= t) {
         const FifoEnt e = fifo[fpfree];
         u32 mn = 0xffffffffu;
-        for (u32 x = lane; x < e.len; x += 32) {
-          const u32 b = ring[(e.seg + x) % ring_len];
-          atomicOr(&bmP[b >> 5], 1u << (b & 31u));
-          dig_b += fold4(kP, 2, e.id, b);
-          mn = min(mn, b >> 5);
+        for (u32 x0 = 0; x0 < e.len; x0 += 32) {
+          ev_reserve(L, 32);
+          const u32 x = x0 + lane;
+          if (x < e.len) {
+            const u32 b = ring[(e.seg + x) % ring_len];
+            atomicOr(&bmP[b >> 5], 1u << (b & 31u));
+            ev_put(L, x - x0, kP, 2, e.id, b);
+            mn = min(mn, b >> 5);
+          }
+          L.nev += min(32u, e.len - x0);
         }
         mn = __reduce_min_sync(FULLMASK, mn);
         hintP = min(hintP, mn);
@@ -648,7 +631,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
         P_idle = true;
         continue;
       }
-      if (!alloc_ordered(SP, E, Kb, btP, btl, kP, 0, dig_b, hintP, nwP)) {
+      if (!alloc_ordered(SP, E, Kb, btP, btl, kP, 0, L, hintP, nwP)) {
         flags |= TOKENSIM_PT_INTERNAL_ERROR;
         break;
       }
@@ -668,7 +651,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
         const u32 need = B.cdiv(p);
         if (one) {
           const i64 a = A[id];
-          dig_r += finish_record(id, te - a, te - a, 0, 0, kP);
+          write_record(rec + id, te - a, te - a, 0, 0, TOKENSIM_REQ_FINISHED, (u32)kP);
         }
         const u32 pm = __ballot_sync(FULLMASK, push);
         const u32 segx = scan_incl(push ? need : 0u) - (push ? need : 0u);
@@ -695,7 +678,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
           const u32 lseg = __shfl_sync(FULLMASK, segx, l);
           const u32 *tbl = btP + (size_t)lpos * btl;
           if (lone) {
-            free_blocks(bmP, tbl, lneed, lid, kP, 0, dig_b, hintP);
+            free_blocks(bmP, tbl, lneed, lid, kP, 0, L, hintP);
             nfreeP += lneed;
           } else {
             for (u32 x = lane; x < lneed; x += 32) ring[(ring_tail + lseg + x) % ring_len] = tbl[x];
@@ -732,9 +715,10 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     const u32 id = fifo[x].id;
     write_record(rec + id, fifo[x].join - A[id], 0, 0, 0, TOKENSIM_REQ_UNFINISHED, 0);
   }
-  dig_s = warp_sum64(dig_s);
-  dig_b = warp_sum64(dig_b);
-  dig_r = warp_sum64(dig_r);
+  ev_flush(L);
+  it_flush(L);
+  const u64 dig_s = warp_sum64(L.dig_s);
+  const u64 dig_b = warp_sum64(L.dig_b);
   if (lane == 0) {
     SimStats st;
     st.flags = flags | ((nrej_tot == n) ? (u32)TOKENSIM_PT_ALL_REJECTED : 0u);
@@ -750,7 +734,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     st.t_final = t_final;
     st.sched_d = dig_s;
     st.block_d = dig_b;
-    st.req_d = dig_r;
+    st.req_d = 0;  // computed from the records by summary_kernel
     st.total_blocks = totD;
     st.peak_blocks = peakD;
     st.block_ns_sum = bnsD;

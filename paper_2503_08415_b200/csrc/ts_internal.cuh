@@ -105,6 +105,8 @@ struct SweepParams {
   u32 *pd_ring;        // P/D: per-warp ring of P block ids [warp][pd_ring_len]
   u64 pd_ring_len;
   unsigned char *pd_fifo;  // P/D: per-warp pending/transfer FIFO [warp][n_req] x 32 B
+  uint4 *evlog;            // per-warp block-event log [warp][1024]
+  ulonglong2 *itlog;       // per-warp iteration log [warp][256][4]
 };
 
 // point -> grid coordinates (row-major)
