@@ -275,6 +275,9 @@ typedef struct {
                                         block allocation / slot updates + finishes / digests /
                                         memory trace / compaction / bookkeeping             */
   uint64_t n_transfers, transfer_bytes;  /* PD_PAIR: P->D KV transfers started and their bytes */
+  uint64_t normal_phase_cycles[8];  /* normal iterations: reservation+preemption / resume /
+                                       admission / block allocation / cost / commit pass /
+                                       compaction / digests+trace                           */
 } tokensim_point_profile;
 tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t point, tokensim_point_profile *out);
 

@@ -70,7 +70,8 @@ class Options(C.Structure):
 class PointProfile(C.Structure):
     _fields_ = [("n_iterations", u64), ("ff_iterations", u64), ("ff_stretches", u64), ("sm_cycles", u64),
                 ("cycles_ff", u64), ("cycles_ff_failed", u64), ("cycles_normal", u64),
-                ("stretch_phase_cycles", u64 * 8), ("n_transfers", u64), ("transfer_bytes", u64)]
+                ("stretch_phase_cycles", u64 * 8), ("n_transfers", u64), ("transfer_bytes", u64),
+                ("normal_phase_cycles", u64 * 8)]
 
 
 class RunInfo(C.Structure):

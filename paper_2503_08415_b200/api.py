@@ -234,6 +234,7 @@ class Sweep:
         self._check(self._L.tokensim_get_point_profile(self._h, point, C.byref(pp)), "get_point_profile")
         d = {n: getattr(pp, n) for n, _ in T.PointProfile._fields_}
         d["stretch_phase_cycles"] = list(d["stretch_phase_cycles"])
+        d["normal_phase_cycles"] = list(d["normal_phase_cycles"])
         return d
 
     def workload(self, point: int):

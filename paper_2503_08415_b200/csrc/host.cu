@@ -855,6 +855,7 @@ tokensim_status tokensim_get_point_profile(const tokensim_sweep *hc, uint64_t po
   out->cycles_normal = st.cyc_normal;
   out->n_transfers = st.n_transfers;
   out->transfer_bytes = st.transfer_bytes;
+  for (int q = 0; q < 8; ++q) out->normal_phase_cycles[q] = st.nphase[q];
   for (int q = 0; q < 8; ++q) out->stretch_phase_cycles[q] = st.phase[q];
   return TOKENSIM_OK;
 }

@@ -452,6 +452,13 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   u64 cyc_ff = 0, cyc_ff_fail = 0, cyc_normal = 0;
   long long clk_a = 0, clk_p = 0;
   u64 ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  u64 nph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define NPH(i)                           \
+  do {                                   \
+    const long long _c = clock64();      \
+    nph[i] += (u64)(_c - clk_p);         \
+    clk_p = _c;                          \
+  } while (0)
 #define PH(i)                            \
   do {                                   \
     const long long _c = clock64();      \
@@ -864,6 +871,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       cyc_ff_fail += (u64)(c1 - clk_a);
       clk_a = c1;
     }
+    clk_p = clock64();
 
     // ---------------------------------------------------------------- 3. decode reservation
     // one pass: needing survivors -> requester list (ascending id), sum of c = ctx+1
@@ -921,6 +929,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     u32 nres = 0, nadm = 0, nrej = 0;
     u64 swap_in = 0, tokens = nR;
     if (m == 0) {
+      NPH(0);
       // 4. resume, head first, stop at the first misfit
       if (nQ > 0) {
         u64 cum_need = 0, cum_tok = 0;
@@ -975,8 +984,20 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         nQ -= nres;
         __syncwarp();
       }
+      NPH(1);
       // 5. fresh FCFS admission
-      if (nQ == 0 && (!STATICP || nR == 0)) {
+      bool head_blocked = false;
+      if (nQ == 0 && (!STATICP || nR == 0) && adm < arr) {
+        // quick exit: a head that is not rejected but cannot be admitted stops step 5 at once
+        const u32 off = adm - win;
+        const u32 pw = __shfl_sync(FULLMASK, wp, off & 31u);
+        const u32 ph = (adm >= win && off < 32) ? pw : PR[adm];
+        const u32 nh = B.cdiv(ph);
+        head_blocked = (u64)nh <= HP.cap_fresh &&
+                       ((u64)nR + 1 > mns || tokens + ph > (u64)mbt || (i64)nfree - (i64)nh < wm ||
+                        (RATIO && (total - nfree) + nh > HP.ratio_limit));
+      }
+      if (nQ == 0 && (!STATICP || nR == 0) && !head_blocked) {
         while (adm < arr) {
           const u32 i = adm + lane;
           const bool valid = i < arr;
@@ -1048,6 +1069,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       }
     }
     nrej_tot += nrej;
+    NPH(2);
     // 6. empty batch (every candidate rejected): back to 0 without advancing t
     if (nR == 0) continue;
     // block extraction for all requesters of this iteration, in phase order
@@ -1055,6 +1077,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       flags |= TOKENSIM_PT_INTERNAL_ERROR;
       break;
     }
+    NPH(3);
     // 7. cost: decodes are positions [0, D), prefills [D, nR)
     const u32 D = nR3 + (SWAPM ? nres : 0u);
     const u32 Sp = nR - D;
@@ -1065,6 +1088,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       Ap = warp_sum64(app);
     }
     const i64 T = iter_time_ns(K, Np, Ap, Sp, D, Cd, swap_out + swap_in);
+    NPH(4);
     // 8. commit
     const i64 ts = t, te = t + T;
     const u64 blocks = total - nfree;
@@ -1111,9 +1135,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
       }
     }
+    NPH(5);
     rmin = __reduce_min_sync(FULLMASK, rmin_l);
     __syncwarp();
     req_iters += nR;
+    NPH(6);
     if (nfin) {
       // stable compaction of R u Q, dropping finished entries (rem == 0 within R)
       const u32 len = nR + nQ;
@@ -1155,6 +1181,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       last_fin = te;
     }
     if (nR == 0) rmin = 0;
+    NPH(7);
     // schedule digest fields (logged; folded lane-parallel when the log fills)
     it_reserve(L, 1);
     if (lane == 0) it_put(L, 0, k, ts, T, Np, Cd, blocks, Sp, D, m, nres, nadm, nfin, nrej);
@@ -1242,6 +1269,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     st.cyc_ff_fail = cyc_ff_fail;
     st.cyc_normal = cyc_normal;
     for (int q = 0; q < 8; ++q) st.phase[q] = ph[q];
+    for (int q = 0; q < 8; ++q) st.nphase[q] = nph[q];
     P.stats[j] = st;
   }
   __syncwarp();

@@ -749,6 +749,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     st.cyc_ff = st.cyc_ff_fail = 0;
     st.cyc_normal = st.cycles;
     for (int q = 0; q < 8; ++q) st.phase[q] = 0;
+    for (int q = 0; q < 8; ++q) st.nphase[q] = 0;
     P.stats[j] = st;
   }
   __syncwarp();

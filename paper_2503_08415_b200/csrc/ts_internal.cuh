@@ -59,6 +59,7 @@ struct SimStats {
   u64 cycles;             // SM clock cycles the warp spent on this point
   u64 cyc_ff, cyc_ff_fail, cyc_normal;  // cycles in stretches / failed attempts / normal iterations
   u64 phase[8];                         // stretch phases: pass/cost/list+alloc/update/fold/trace/compact/tail
+  u64 nphase[8];                        // normal-iteration phases (see tokensim_point_profile)
 };
 
 struct SweepParams {

@@ -54,3 +54,4 @@ if os.environ.get("PROFILE_POINTS"):
                                                                        x["cycles_normal"] / nn, x["cycles_ff_failed"]))
         ns = max(1, x["ff_stretches"])
         print("     stretch phases (cycles/stretch):", " ".join("%.0f" % (c / ns) for c in x["stretch_phase_cycles"]))
+        print("     normal phases (cycles/iter):", " ".join("%.0f" % (c / nn) for c in x["normal_phase_cycles"]))
