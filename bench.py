@@ -53,6 +53,9 @@ def env_rank():
 def config_for(name: str, world: int) -> si.SweepConfig:
     if name == "c2":
         return si.c2(n_seeds=8 * world)
+    if name == "c5":  # 65,536 points = 8 seeds x 8,192; one seed (8,192 points) per GPU
+        cfg = si.c5()
+        return replace(cfg, workload=replace(cfg.workload, seeds=list(range(world))))
     cfg = si.PRESETS[name]()
     if world > 1:  # weak scaling: replicate the seed axis
         w = cfg.workload
@@ -65,7 +68,7 @@ WORKLOAD_DESC = {
     "c2": "C2: LLaMA-2-13B, 1,000 ShareGPT-shaped requests, lambda 1..16 req/s x 8 seeds = 128 points per GPU",
     "c3": "C3: LLaMA-2-7B hardware sweep 16 F x 16 B x 6 C x {STATIC, CONT, CONT_RATIO 0.9}, 10k requests, 4,608 points",
     "c4": "C4: LLaMA-2-70B TP 2/4/8 x {CONT, CONT_RATIO 0.9} x {SWAP, RECOMPUTE} x 16 rates x 12 seeds, 10k req, 2,304 points",
-    "c5": "C5: 1P:1D pairs 16x16 x {SWAP, RECOMPUTE} x 16 rates x 8 seeds, 10k requests, 65,536 points",
+    "c5": "C5: 1P:1D pairs 16x16 x {SWAP, RECOMPUTE} x 16 rates, 10k requests; 8,192 points (one seed) per GPU, 65,536 at 8 GPUs",
 }
 
 

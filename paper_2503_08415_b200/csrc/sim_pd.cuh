@@ -88,6 +88,44 @@ __device__ __forceinline__ void trace_iter(TraceAcc &A, bool binned, bool full, 
   }
 }
 
+// memory trace of a stretch: lanes j < J hold iterations [tsj, tej) with blkj blocks
+__device__ __forceinline__ void trace_stretch(TraceAcc &A, bool binned, bool full, tokensim_mem_sample *trc, u64 cap,
+                                              i64 W, u32 J, i64 tsj, i64 tej, u64 blkj, u32 &flags) {
+  const u32 lane = lane_id();
+  const bool lj = lane < J;
+  const i64 tend = __shfl_sync(FULLMASK, tej, J - 1), tsl = __shfl_sync(FULLMASK, tsj, J - 1);
+  if (binned) {
+    while (true) {
+      const i64 bstart = A.bin_end - W;
+      i64 ov = 0;
+      bool cnt_here = false;
+      if (lj) {
+        const i64 lo = tsj > bstart ? tsj : bstart;
+        const i64 hi = tej < A.bin_end ? tej : A.bin_end;
+        ov = hi - lo;
+        cnt_here = tsj >= bstart && tsj < A.bin_end;
+      }
+      A.acc_bns += warp_sum64(ov > 0 ? blkj * (u64)ov : 0ull);
+      A.acc_max = max(A.acc_max, __reduce_max_sync(FULLMASK, ov > 0 ? (u32)blkj : 0u));
+      A.acc_nit += __popc(__ballot_sync(FULLMASK, cnt_here));
+      if (tend > A.bin_end || tsl >= A.bin_end) trace_flush_bin(A, trc, cap, W, flags);
+      else break;
+    }
+  } else if (full) {
+    if (lj && A.tn + lane < cap) {
+      tokensim_mem_sample sm;
+      sm.t_ns = tsj;
+      sm.dur_ns = tej - tsj;
+      sm.block_ns = blkj * (u64)(tej - tsj);
+      sm.blocks_max = (u32)blkj;
+      sm.n_iter = 1;
+      trc[A.tn + lane] = sm;
+    }
+    if (A.tn + J > cap) flags |= TOKENSIM_PT_TRACE_OVERFLOW;
+    A.tn += J;
+  }
+}
+
 template <int CAP>
 __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsigned char *pd_smem, u32 *bt) {
   const u32 lane = lane_id();
@@ -175,6 +213,10 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       xbytes = 0;
   u32 flags = 0;
   i64 last_fin = 0;
+  const bool ff_on = P.ff_enable != 0;
+  u32 rminD = 0;              // min rem over D's running slots after the last commit
+  u64 ffw = 0, ffk = 0;       // memory-cut retry guard (as in the unified worker)
+  u64 ff_iters = 0, ff_runs = 0;
   u64 nit = 0;  // iteration records are kept in processing order across both workers
   const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
   const bool FULLT = P.trace_mode == TOKENSIM_TRACE_FULL;
@@ -227,6 +269,305 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
         xhead_end = nX ? fifo[fdadm - nX].xend : INF;
       }
       __syncwarp();
+      // ---------------------------------------------------------- D fast-forward (H3)
+      // Quiescent decode stretch on D: nothing completes a transfer, nothing is pulled or
+      // resumed, nothing is preempted, and P (which may push pending requests) has no boundary
+      // before the stretch's iterations; the last iteration may finish requests.
+      if (ff_on && nRun > 0 && rminD >= 2 && (nfreeD > ffw || kD >= ffk)) {
+        bool quiet = true, mem_check = false;
+        u32 need_h = 0;
+        i64 join_cut = INF;
+        const u32 nA0 = nD - nX;
+        if (nQ > 0) {
+          // first preempted slot = the resume head
+          u32 qpos = 0;
+          for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+            const u32 jj = b0 + lane;
+            const u32 qb = __ballot_sync(FULLMASK, jj < nA0 && stt[jj] == ST_QUEUED);
+            if (qb) {
+              qpos = b0 + (u32)(__ffs(qb) - 1);
+              break;
+            }
+          }
+          u32 tokq;
+          if (SWAPM) {
+            const u32 c = S.ctx[qpos];
+            need_h = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
+            tokq = 1;
+          } else {
+            const u32 id = S.id[qpos];
+            tokq = PR[id] + (OU[id] - S.rem[qpos]);
+            need_h = B.cdiv(tokq);
+          }
+          if (!((u64)nRun + nX + 1 > mns || (u64)nRun + tokq > mbt)) {
+            mem_check = true;
+            if ((i64)nfreeD - (i64)nRun - (i64)need_h >= wm) quiet = false;  // resume is certain
+          }
+        } else if (!STATICP) {
+          if (fdadm < ftail) {
+            const i64 jh = fifo[fdadm].join;
+            if (jh <= t) {  // a visible pending head: blocked now => blocked for the stretch
+              need_h = B.cdiv(PR[fifo[fdadm].id]);
+              if (!((u64)nRun + nX + 1 > mns)) {
+                mem_check = true;
+                if ((i64)nfreeD - (i64)nRun - (i64)need_h >= wm) quiet = false;
+              }
+            } else {
+              join_cut = jh;  // the head becomes visible later
+            }
+          }
+        }
+        if (quiet) {
+          S.scratch[lane] = 0;
+          S.scratch[32 + lane] = 0;
+          __syncwarp();
+          u64 cdp0 = 0;
+          u32 rmn = 0xffffffffu;
+          i64 lmin = INF;
+          for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+            const u32 jj = b0 + lane;
+            u32 key = 64u + lane;
+            if (jj < nA0 && stt[jj] == ST_RUN) {
+              const u32 c = S.ctx[jj];
+              cdp0 += c + 1;
+              rmn = min(rmn, S.rem[jj]);
+              const i64 lt = S.last[jj];
+              lmin = lt < lmin ? lt : lmin;
+              const u32 r = B.mod(c);
+              const u32 j0 = r ? B.bs - r : 0u;
+              if (j0 < 32) key = j0;
+            }
+            const u32 peers = __match_any_sync(FULLMASK, key);
+            if (key < 32 && (peers & ltm) == 0u) {
+              S.scratch[key] += __popc(peers);
+              S.scratch[32 + key] = peers;
+            }
+            __syncwarp();
+          }
+          const u64 Cd0 = warp_sum64(cdp0);
+          const u32 rm = __reduce_min_sync(FULLMASK, rmn);
+          i64 lm = lmin;
+#pragma unroll
+          for (u32 o = 16; o; o >>= 1) {
+            const i64 y = __shfl_xor_sync(FULLMASK, lm, o);
+            lm = y < lm ? y : lm;
+          }
+          const u32 nj = S.scratch[B.bs >= 32 ? lane : B.mod(lane)];
+          const u32 Aj = scan_incl(nj);
+          const u64 Cdj = Cd0 + (u64)lane * nRun;
+          const i64 Tj = iter_time_ns(KD, 0, 0, 0, nRun, Cdj, 0);
+          const i64 tej = t + scan_incl_i64(Tj);
+          const i64 tsj = tej - Tj;
+          bool ok = ((u64)Aj <= nfreeD) && (Aj <= (u32)CAP) && (lane < rm);
+          if (lane > 0) {
+            if (P.horizon >= 0 && tsj >= P.horizon) ok = false;
+            if (tsj >= xhead_end || tsj >= join_cut || tsj > tP) ok = false;
+          }
+          if (mem_check) {
+            const u64 fr = nfreeD - (u64)__shfl_sync(FULLMASK, Aj, 0);
+            if (!((i64)fr - (i64)need_h < wm)) ok = false;
+          }
+          const u32 okm = __ballot_sync(FULLMASK, ok);
+          const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+          const u32 memcut = __ballot_sync(FULLMASK, !((u64)Aj <= nfreeD));
+          if (J < 2 && memcut && (u32)(__ffs(memcut) - 1) < 2) {
+            ffw = nfreeD;
+            ffk = kD + 4;
+          }
+          if (J >= 2) {
+            const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
+            __syncwarp();
+            S.scratch[lane] = Aj - nj;  // bucket cursors
+            __syncwarp();
+            bool done_alloc = Ktot == 0;
+            if (!done_alloc && nA0 <= 32 && Ktot <= 32 && hintD < nwD) {
+              const u32 wi = hintD + lane;
+              u32 word = wi < nwD ? S.bitmap[wi] : 0u;
+              const u32 cw = __popc(word);
+              const u32 cum = scan_incl(cw);
+              if (__shfl_sync(FULLMASK, cum, 31) >= Ktot) {
+                ev_reserve(L, 32);
+                const bool act = lane < Ktot;
+                const u32 o = act ? lane : 0u;
+                u32 jb = 0;
+#pragma unroll
+                for (u32 st = 16; st; st >>= 1) {
+                  const u32 v = __shfl_sync(FULLMASK, Aj, jb + st - 1);
+                  if (v <= o) jb += st;
+                }
+                const u32 excl = __shfl_sync(FULLMASK, Aj - nj, jb);
+                u32 lo = 0;
+#pragma unroll
+                for (u32 st = 16; st; st >>= 1) {
+                  const u32 v = __shfl_sync(FULLMASK, cum, lo + st - 1);
+                  if (v <= o) lo += st;
+                }
+                const u32 wv = __shfl_sync(FULLMASK, word, lo);
+                const u32 bv = __shfl_sync(FULLMASK, cum - cw, lo);
+                if (act) {
+                  const u32 mask = S.scratch[32 + (B.bs >= 32 ? jb : B.mod(jb))];
+                  const u32 pos = select_bit(mask, o - excl);
+                  const u32 blk = (hintD + lo) * 32 + select_bit(wv, o - bv);
+                  btD[(size_t)(S.info[pos] & 0xffffu) * btl + B.div(S.ctx[pos] + jb)] = blk;
+                  ev_put(L, o, kD + jb, 3, S.id[pos], blk);
+                }
+                L.nev += Ktot;
+                const u32 before = cum - cw;
+                const u32 tk = Ktot > before ? min(cw, Ktot - before) : 0u;
+                if (tk && wi < nwD) {
+                  word = clear_lowest(word, tk, cw);
+                  S.bitmap[wi] = word;
+                }
+                const u32 nz = __ballot_sync(FULLMASK, word != 0u);
+                hintD = nz ? hintD + (u32)(__ffs(nz) - 1) : hintD + 32;
+                __syncwarp();
+                done_alloc = true;
+              }
+            }
+            if (!done_alloc) {
+              const u32 nrep = (32 + B.bs - 1) / B.bs;
+              for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+                const u32 jj = b0 + lane;
+                const bool run = jj < nA0 && stt[jj] == ST_RUN;
+                const u32 c = run ? S.ctx[jj] : 0u;
+                const u32 r = B.mod(c);
+                u32 jx = r ? B.bs - r : 0u;
+                for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
+                  const bool v = run && jx < J;
+                  const u32 key = v ? jx : 64u + lane;
+                  const u32 peers = __match_any_sync(FULLMASK, key);
+                  u32 base = 0;
+                  if (v) base = S.scratch[jx];
+                  __syncwarp();
+                  if (v) {
+                    const u32 e = base + __popc(peers & ltm);
+                    S.req_cum[e] = e + 1;
+                    S.req_pt[e] = jj | (jx << 10) | (B.div(c + jx) << 15);
+                    if ((peers & ltm) == 0u) S.scratch[jx] = base + __popc(peers);
+                  }
+                  __syncwarp();
+                }
+              }
+              if (!alloc_ordered(S, Ktot, Ktot, btD, btl, kD, 2, L, hintD, nwD)) {
+                flags |= TOKENSIM_PT_INTERNAL_ERROR;
+                break;
+              }
+            }
+            const u64 blk0 = totD - nfreeD;
+            nfreeD -= Ktot;
+            const u64 klast = kD + J - 1;
+            const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
+            const i64 te0 = __shfl_sync(FULLMASK, tej, 0);
+            const bool lj = lane < J;
+            i64 tm1 = (lj && lane > 0) ? Tj : 0;  // gaps of iterations 1.. are their T
+#pragma unroll
+            for (u32 o = 16; o; o >>= 1) {
+              const i64 y = __shfl_xor_sync(FULLMASK, tm1, o);
+              tm1 = y > tm1 ? y : tm1;
+            }
+            u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
+            for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+              const u32 jj = b0 + lane;
+              bool fin = false;
+              if (jj < nA0 && stt[jj] == ST_RUN) {
+                const u32 r = S.rem[jj] - J;
+                S.rem[jj] = r;
+                S.ctx[jj] += J;
+                const i64 g0 = te0 - S.last[jj];  // first gap: from the slot's last token
+                i64 mg = S.maxgap[jj];
+                mg = g0 > mg ? g0 : mg;
+                mg = tm1 > mg ? tm1 : mg;
+                S.maxgap[jj] = mg;
+                S.last[jj] = tend;
+                fin = r == 0;
+                if (fin)
+                  write_record(rec + S.id[jj], S.ttft[jj], tend - S.arr[jj], mg, S.info[jj] >> 16,
+                               TOKENSIM_REQ_FINISHED, (u32)klast);
+                else
+                  rmin_l = min(rmin_l, r);
+              }
+              u32 fm = __ballot_sync(FULLMASK, fin);
+              __syncwarp();
+              if (fm && first_fin == 0xffffffffu) first_fin = b0 + (u32)(__ffs(fm) - 1);
+              nfin += __popc(fm);
+              while (fm) {
+                const u32 l = (u32)(__ffs(fm) - 1);
+                fm &= fm - 1;
+                const u32 pos = b0 + l;
+                const u32 held = B.cdiv(S.ctx[pos]);
+                const u32 slot = S.info[pos] & 0xffffu;
+                free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], klast, 2, L, hintD);
+                nfreeD += held;
+                if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
+              }
+            }
+            __syncwarp();
+            const u64 blkj = blk0 + Aj;
+            it_reserve(L, 32);
+            if (lj)
+              it_put(L, lane, (kD + lane) | (1ull << 40), tsj, Tj, 0, Cdj, blkj, 0, nRun, 0, 0, 0,
+                     lane == J - 1 ? nfin : 0u, 0);
+            L.nit += J;
+            nit += J;
+            bnsD += warp_sum64(lj ? blkj * (u64)Tj : 0ull);
+            trace_stretch(TA[1], BINNED, FULLT, trcD, P.trace_cap, W, J, tsj, tej, blkj, flags);
+            const u64 blk_last = blk0 + Ktot;
+            peakD = blk_last > peakD ? blk_last : peakD;
+            req_iters += (u64)nRun * J;
+            if (nfin) {
+              u32 out = first_fin;
+              for (u32 b0 = first_fin; b0 < nD; b0 += 32) {
+                const u32 jj = b0 + lane;
+                const bool valid = jj < nD;
+                u32 vid = 0, vctx = 0, vrem = 0, vinfo = 0, vst = 0;
+                i64 vl = 0, vm = 0, va = 0, vt = 0;
+                if (valid) {
+                  vid = S.id[jj];
+                  vctx = S.ctx[jj];
+                  vrem = S.rem[jj];
+                  vinfo = S.info[jj];
+                  vl = S.last[jj];
+                  vm = S.maxgap[jj];
+                  va = S.arr[jj];
+                  vt = S.ttft[jj];
+                  vst = stt[jj];
+                }
+                const bool keep = valid && vrem != 0;
+                const u32 km = __ballot_sync(FULLMASK, keep);
+                __syncwarp();
+                if (keep) {
+                  const u32 d = out + __popc(km & ltm);
+                  S.id[d] = vid;
+                  S.ctx[d] = vctx;
+                  S.rem[d] = vrem;
+                  S.info[d] = vinfo;
+                  S.last[d] = vl;
+                  S.maxgap[d] = vm;
+                  S.arr[d] = va;
+                  S.ttft[d] = vt;
+                  stt[d] = vst;
+                }
+                __syncwarp();
+                out += __popc(km);
+              }
+              nRun -= nfin;
+              nD -= nfin;
+              n_done += nfin;
+              nfin_tot += nfin;
+              last_fin = tend > last_fin ? tend : last_fin;
+            }
+            rminD = nRun ? __reduce_min_sync(FULLMASK, rmin_l) : 0u;
+            ff_iters += J;
+            ++ff_runs;
+            tD = tend;
+            lastD = tend;
+            kD += J;
+            D_idle = false;
+            continue;
+          }
+        }
+        rminD = 0;
+      }
       const u32 nA = nD - nX;  // running + preempted prefix
       // 3. decode reservation: RUN slots needing a block -> requester list (ascending id)
       u32 E = 0;
@@ -444,7 +785,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       const i64 te = t + T;
       const u64 blocks = totD - nfreeD;
       // 8. commit
-      u32 nfin = 0, first_fin = 0xffffffffu;
+      u32 nfin = 0, first_fin = 0xffffffffu, rmin_d = 0xffffffffu;
       for (u32 b0 = 0; b0 < nA; b0 += 32) {
         const u32 jj = b0 + lane;
         bool fin = false;
@@ -462,6 +803,8 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
             if (fin)
               write_record(rec + S.id[jj], S.ttft[jj], te - S.arr[jj], S.maxgap[jj], S.info[jj] >> 16,
                            TOKENSIM_REQ_FINISHED, (u32)kD);
+            else
+              rmin_d = min(rmin_d, r);
           }
         }
         u32 fm = __ballot_sync(FULLMASK, fin);
@@ -523,6 +866,8 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
         nfin_tot += nfin;
         last_fin = te > last_fin ? te : last_fin;
       }
+      rminD = __reduce_min_sync(FULLMASK, rmin_d);
+      if (nRun == 0) rminD = 0;
       fold_iter(kD, 1, t, T, nrecomp, Dn, Np, Cd, m, nres, nadm, 0, nfin, blocks);
       trace_iter(TA[1], BINNED, FULLT, trcD, P.trace_cap, W, t, te, blocks, flags);
       peakD = blocks > peakD ? blocks : peakD;
@@ -743,8 +1088,8 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     st.iter_n = min(nit, P.it_cap);
     st.n_transfers = n_xfer;
     st.transfer_bytes = xbytes;
-    st.ff_iters = 0;
-    st.ff_runs = 0;
+    st.ff_iters = ff_iters;
+    st.ff_runs = ff_runs;
     st.cycles = (u64)(clock64() - clk0);
     st.cyc_ff = st.cyc_ff_fail = 0;
     st.cyc_normal = st.cycles;

@@ -189,16 +189,20 @@ def test_sharegpt_builtin_equals_table(api):
 def test_fast_forward_is_bit_identical(api):
     """Time-parallel evaluation of quiescent stretches must not change a single
     bit of any result: compare full summaries, records and traces with it switched off."""
+    c5r = si.subset(si.c5(), rates=[0, 15], seeds=[0], hws=[0, 5, 10, 15])
+    c5r = replace(c5r, workload=replace(c5r.workload, num_requests=400),
+                  options=replace(c5r.options, iteration_trace_cap=1 << 16))
     for cfg in (si.c2(), replace(si.c1(), options=si.Options(trace_mode=si.FULL, iteration_trace_cap=1 << 16)),
-                replace(si.c1(), options=si.Options(trace_bin_ns=7_000_000))):
+                replace(si.c1(), options=si.Options(trace_bin_ns=7_000_000)), c5r):
         on = run_gpu(api, cfg)
         off = run_gpu(api, replace(cfg, options=replace(cfg.options, fast_forward=False)))
         assert on.summaries().tobytes() == off.summaries().tobytes()
         for p in range(0, cfg.num_points, 13):
             assert on.records(p).tobytes() == off.records(p).tobytes()
-            assert on.mem_trace(p).tobytes() == off.mem_trace(p).tobytes()
-        if cfg.options.iteration_trace_cap:
-            assert on.iteration_trace(0).tobytes() == off.iteration_trace(0).tobytes()
+            for w in ((0, 1) if cfg.options.topology == si.PD_PAIR else (0,)):
+                assert on.mem_trace(p, w).tobytes() == off.mem_trace(p, w).tobytes()
+            if cfg.options.iteration_trace_cap:
+                assert on.iteration_trace(p).tobytes() == off.iteration_trace(p).tobytes()
 
 
 # ------------------------------------------------------------------ a.9 P/D pair
@@ -247,7 +251,7 @@ def _micro_pd(rng):
                     trace_output=o.tolist(), prompt_table=None, output_table=None)
     opts = si.Options(topology=si.PD_PAIR, pd_link_bw=float(rng.choice([1e9, 200e9])),
                       trace_mode=str(rng.choice([si.FULL, si.BINNED])), trace_bin_ns=50_000_000,
-                      iteration_trace_cap=1 << 16)
+                      iteration_trace_cap=1 << 16, fast_forward=bool(rng.random() < 0.8))
     return si.SweepConfig("micro-pd", model, hws, [pol], w, opts)
 
 
