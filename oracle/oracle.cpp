@@ -522,14 +522,44 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
       t = req[arr].a;
       continue;
     }
-    std::map<u32, Kind> kind;
+    std::map<u32, Kind> kind;  // this iteration's batch: id -> entry kind
+    u64 n_res = 0, n_adm = 0, n_rej = 0, swap_in = 0, m = 0, swap_out = 0;
+    // NEXT-3 prefill-first (vLLM v0.6.2 default, reading R-N3): when fresh requests can be
+    // admitted the iteration runs only their prefills; the running requests pause
+    auto fresh_admission = [&](u64 tokens) {
+      while (adm < arr) {
+        Req &x = req[adm];
+        const u64 need = ceil_div(x.p, bs);
+        const u64 cap = RATIO ? d.ratio_limit : total - c.watermark_blocks;
+        if (need > cap) {
+          x.status = 2;
+          ++n_rej;
+          ++adm;
+          continue;
+        }
+        const u64 fr = freeset.size();
+        if (R.size() + 1 > c.max_num_seqs) break;
+        if (tokens + x.p > c.max_batched_tokens) break;
+        if ((i64)fr - (i64)need < (i64)c.watermark_blocks) break;
+        if (RATIO && (total - fr) + need > d.ratio_limit) break;
+        alloc_lowest(adm, need);
+        R.insert(adm);
+        kind[adm] = K_PRE_FRESH;
+        tokens += x.p;
+        ++n_adm;
+        ++adm;
+      }
+    };
+    const bool PF = c.iter_mode == OR_PREFILL_FIRST;
+    if (PF && Q.empty() && (c.kind != OR_STATIC || R.empty())) fresh_admission(0);
+    const bool pf_only = PF && n_adm > 0;
     // 3. decode reservation + preemption (reading A7)
     const u64 F = freeset.size();
-    std::vector<u32> Rv(R.begin(), R.end());
+    std::vector<u32> Rv;
+    if (!pf_only) Rv.assign(R.begin(), R.end());
     auto need_of = [&](u32 id) -> u64 { return (req[id].ctx % bs == 0) ? 1 : 0; };
     u64 sum_need = 0;
     for (u32 id : Rv) sum_need += need_of(id);
-    u64 m = 0, swap_out = 0;
     if (sum_need > F) {
       const u64 nr = Rv.size();
       for (m = 1; m <= nr; ++m) {
@@ -559,14 +589,15 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
       }
       n_preempt_total += m;
     }
-    for (u32 id : R) {  // surviving requests, ascending id
-      kind[id] = K_DEC;
-      if (need_of(id)) alloc_lowest(id, 1);
+    if (!pf_only) {
+      for (u32 id : R) {  // surviving requests, ascending id
+        kind[id] = K_DEC;
+        if (need_of(id)) alloc_lowest(id, 1);
+      }
     }
-    const u64 D3 = R.size();
-    u64 n_res = 0, n_adm = 0, n_rej = 0, swap_in = 0;
+    const u64 D3 = pf_only ? 0 : R.size();
     u64 tokens = D3;
-    if (m == 0) {
+    if (m == 0 && !pf_only) {
       // 4. resume, head first, stop at the first misfit (reading A6)
       std::vector<u32> Qv(Q.begin(), Q.end());
       for (u32 id : Qv) {
@@ -594,45 +625,24 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
           kind[id] = K_PRE_RECOMP;
         }
       }
-      // 5. fresh FCFS admission (STATIC P:167/A16; ratio P:460/A15)
-      if (Q.empty() && (c.kind != OR_STATIC || R.empty())) {
-        while (adm < arr) {
-          Req &x = req[adm];
-          const u64 need = ceil_div(x.p, bs);
-          const u64 cap = RATIO ? d.ratio_limit : total - c.watermark_blocks;
-          if (need > cap) {
-            x.status = 2;
-            ++n_rej;
-            ++adm;
-            continue;
-          }
-          const u64 fr = freeset.size();
-          if (R.size() + 1 > c.max_num_seqs) break;
-          if (tokens + x.p > c.max_batched_tokens) break;
-          if ((i64)fr - (i64)need < (i64)c.watermark_blocks) break;
-          if (RATIO && (total - fr) + need > d.ratio_limit) break;
-          alloc_lowest(adm, need);
-          R.insert(adm);
-          kind[adm] = K_PRE_FRESH;
-          tokens += x.p;
-          ++n_adm;
-          ++adm;
-        }
-      }
+      // 5. fresh FCFS admission (STATIC P:167/A16; ratio P:460/A15); in
+      // prefill-first mode it was already attempted at the top of the pass
+      if (!PF && Q.empty() && (c.kind != OR_STATIC || R.empty())) fresh_admission(tokens);
     }
     n_rej_total += n_rej;
     // 6. empty batch
-    if (R.empty()) continue;
+    if (kind.empty()) continue;
     // 7. cost (c.5)
     std::vector<Prefill> pf;
     std::vector<u64> dec;
     u64 Np = 0, Cd = 0;
-    for (u32 id : R) {
+    for (const auto &kv : kind) {
+      const u32 id = kv.first;
       const Req &x = req[id];
-      if (kind[id] == K_DEC) {
+      if (kv.second == K_DEC) {
         dec.push_back(x.ctx + 1);
         Cd += x.ctx + 1;
-      } else if (kind[id] == K_PRE_FRESH) {
+      } else if (kv.second == K_PRE_FRESH) {
         pf.push_back({x.p, 0});
         Np += x.p;
       } else {
@@ -644,12 +654,12 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
     // 8. commit
     const i64 ts = t, te = t + T;
     const u64 blocks = total - freeset.size();
-    const u64 entries = R.size();
+    const u64 entries = kind.size();
     u64 n_fin = 0;
-    std::vector<u32> Rc(R.begin(), R.end());
-    for (u32 id : Rc) {
+    for (const auto &kv : kind) {
+      const u32 id = kv.first;
       Req &x = req[id];
-      const Kind kd = kind[id];
+      const Kind kd = kv.second;
       if (kd == K_PRE_FRESH) {
         x.ctx = x.p;
         x.gen = 1;
@@ -749,8 +759,8 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
 // advanced in time order of their next boundary, D first on ties (reading A2).  An idle worker
 // wakes at the earliest event that can change its decision.
 oracle_run *simulate_pd(const oracle_cfg &c) {
-  if (c.kind == OR_CONT_RATIO) {
-    g_err = "PD_PAIR supports STATIC and CONT policies only";
+  if (c.kind == OR_CONT_RATIO || c.iter_mode != OR_MIXED) {
+    g_err = "PD_PAIR supports STATIC and CONT policies in MIXED mode only";
     return nullptr;
   }
   oracle_derived dP, dD;

@@ -21,6 +21,7 @@ enum { OR_SWAP = 0, OR_RECOMPUTE = 1 };
 enum { OR_LEN_FIXED = 1, OR_LEN_UNIFORM = 2, OR_LEN_TABLE = 3, OR_LEN_TRACE = 4 };
 enum { OR_TRACE_NONE = 0, OR_TRACE_BINNED = 1, OR_TRACE_FULL = 2 };
 enum { OR_UNIFIED = 0, OR_PD_PAIR = 1 };
+enum { OR_MIXED = 0, OR_PREFILL_FIRST = 1 };
 
 typedef struct {
   /* model */
@@ -63,6 +64,7 @@ typedef struct {
   int64_t horizon_ns;
   uint32_t check_invariants;   /* 1: assert c.8 invariants every iteration */
   uint32_t keep_events;        /* 1: keep the block event log              */
+  uint32_t iter_mode;          /* OR_MIXED (A3) | OR_PREFILL_FIRST (NEXT-3) */
 } oracle_cfg;
 
 typedef struct {

@@ -63,7 +63,7 @@ class OracleCfg(C.Structure):
         ("topology", u32), ("pd_link_bw", f64), ("trace_mode", u32),
         ("trace_bin_ns", u64), ("trace_cap_samples", u64),
         ("slo_ttft_s", f64), ("slo_mtpot_s", f64), ("horizon_ns", i64),
-        ("check_invariants", u32), ("keep_events", u32),
+        ("check_invariants", u32), ("keep_events", u32), ("iter_mode", u32),
     ]
 
 
@@ -177,6 +177,7 @@ def make_cfg(cfg: si.SweepConfig, point: int, check_invariants: bool = False,
     c.kind, c.preempt, c.max_mem_ratio = _KIND[p.kind], _PRE[p.preempt], p.max_mem_ratio
     c.max_num_seqs, c.max_batched_tokens = p.max_num_seqs, p.max_batched_tokens
     c.block_size, c.watermark_blocks = p.block_size, p.watermark_blocks
+    c.iter_mode = {si.MIXED: 0, si.PREFILL_FIRST: 1}[p.iteration_mode]
     c.num_requests, c.rate, c.seed = w.num_requests, w.rates[rate_i], w.seeds[seed_i]
     c.len_dist = _LEN[w.len_dist]
     c.prompt_a, c.prompt_b, c.output_a, c.output_b = w.prompt_a, w.prompt_b, w.output_a, w.output_b

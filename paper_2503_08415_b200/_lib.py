@@ -22,6 +22,7 @@ STATUS_NAMES = {0: "OK", -1: "E_INVALID", -2: "E_NOMEM", -3: "E_CUDA", -4: "E_ST
                 -6: "E_TRUNCATED", -7: "E_OVERFLOW"}
 STATIC, CONT, CONT_RATIO = 0, 1, 2
 SWAP, RECOMPUTE = 0, 1
+MIXED, PREFILL_FIRST = 0, 1
 LEN_SHAREGPT_SYNTH_V1, LEN_FIXED, LEN_UNIFORM, LEN_TABLE, LEN_TRACE = 0, 1, 2, 3, 4
 TRACE_NONE, TRACE_BINNED, TRACE_FULL = 0, 1, 2
 UNIFIED, PD_PAIR = 0, 1
@@ -46,7 +47,7 @@ class Hw(C.Structure):
 class Policy(C.Structure):
     _fields_ = [("struct_size", u32), ("kind", u32), ("preempt", u32), ("max_mem_ratio", f64),
                 ("max_num_seqs", u32), ("max_batched_tokens", u32), ("block_size", u32),
-                ("watermark_blocks", u32)]
+                ("watermark_blocks", u32), ("iteration_mode", u32)]
 
 
 class LenTable(C.Structure):

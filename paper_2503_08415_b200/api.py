@@ -30,6 +30,7 @@ class TokensimError(RuntimeError):
 
 _KIND = {si.STATIC: T.STATIC, si.CONT: T.CONT, si.CONT_RATIO: T.CONT_RATIO}
 _PRE = {si.SWAP: T.SWAP, si.RECOMPUTE: T.RECOMPUTE}
+_MODE = {si.MIXED: T.MIXED, si.PREFILL_FIRST: T.PREFILL_FIRST}
 _LEN = {si.FIXED: T.LEN_FIXED, si.UNIFORM: T.LEN_UNIFORM, si.TABLE: T.LEN_TABLE, si.TRACE: T.LEN_TRACE,
         "sharegpt_synth_v1": T.LEN_SHAREGPT_SYNTH_V1}
 _TRC = {si.NONE_TRACE: T.TRACE_NONE, si.BINNED: T.TRACE_BINNED, si.FULL: T.TRACE_FULL}
@@ -56,7 +57,8 @@ def marshal(cfg: si.SweepConfig):
     pols = (T.Policy * len(cfg.policies))()
     for i, p in enumerate(cfg.policies):
         pols[i] = T.Policy(C.sizeof(T.Policy), _KIND[p.kind], _PRE[p.preempt], p.max_mem_ratio,
-                           p.max_num_seqs, p.max_batched_tokens, p.block_size, p.watermark_blocks)
+                           p.max_num_seqs, p.max_batched_tokens, p.block_size, p.watermark_blocks,
+                           _MODE[p.iteration_mode])
     w = cfg.workload
     rates, prates = _arr(w.rates, np.float64, C.c_double)
     seeds, pseeds = _arr(w.seeds, np.uint64, C.c_uint64)

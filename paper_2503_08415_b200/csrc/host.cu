@@ -272,6 +272,9 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
     const std::string pp = "policies[" + std::to_string(i) + "].";
     if (p.kind > TOKENSIM_CONT_RATIO) return bad(pp + "kind: unknown");
     if (p.preempt > TOKENSIM_RECOMPUTE) return bad(pp + "preempt: unknown");
+    if (p.iteration_mode > TOKENSIM_PREFILL_FIRST) return bad(pp + "iteration_mode: unknown");
+    if (opt->topology == TOKENSIM_PD_PAIR && p.iteration_mode != TOKENSIM_MIXED)
+      return bad(pp + "iteration_mode: PD_PAIR workers are prefill-only / decode-only already");
     if (opt->topology == TOKENSIM_PD_PAIR && p.kind == TOKENSIM_CONT_RATIO)
       return bad(pp + "kind: PD_PAIR supports STATIC and CONT (reading R-PD1)");
     if (p.kind == TOKENSIM_CONT_RATIO && !(p.max_mem_ratio > 0 && p.max_mem_ratio <= 1))
@@ -290,7 +293,7 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
     d.bs = p.block_size;
     d.wm = p.watermark_blocks;
     d.bs_sh = (p.block_size & (p.block_size - 1)) ? 0xffffffffu : (u32)__builtin_ctz(p.block_size);
-    d.pad = 0;
+    d.mode = p.iteration_mode;
     h->dpol.push_back(d);
   }
   h->cap = max_mns <= 32 ? 32 : (max_mns <= 256 ? 256 : 1024);

@@ -409,6 +409,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const bool SWAPM = PL.preempt == TOKENSIM_SWAP;
   const bool RATIO = PL.kind == TOKENSIM_CONT_RATIO;
   const bool STATICP = PL.kind == TOKENSIM_STATIC;
+  const bool PFM = PL.mode == TOKENSIM_PREFILL_FIRST;
   const u64 total = HP.total_blocks;
   const u32 nwords = HP.nwords;
   const u32 btl = P.bt_len;
@@ -567,13 +568,15 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           hd_p = (adm >= win && off < 32) ? pw : PR[adm];
         }
         need_h = B.cdiv(hd_p);
+        // prefill-first admits before any decode block: no decode tokens, no decode blocks
+        const u64 dtok = PFM ? 0u : nR;
         if ((u64)need_h > HP.cap_fresh) quiet = false;  // would be rejected at this boundary
-        else if (!((u64)nR + 1 > mns || (u64)nR + hd_p > mbt)) {
+        else if (!((u64)nR + 1 > mns || dtok + hd_p > mbt)) {
           mem_check = true;
           ratio_h = RATIO;
           // admission is certain even if every running request takes a block now: don't try
-          if ((i64)nfree - (i64)nR - (i64)need_h >= wm &&
-              (!RATIO || (total - nfree + nR) + need_h <= HP.ratio_limit))
+          if ((i64)nfree - (i64)dtok - (i64)need_h >= wm &&
+              (!RATIO || (total - nfree + dtok) + need_h <= HP.ratio_limit))
             quiet = false;
         }
       }
@@ -624,7 +627,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           if (nQ == 0 && adm == arr && arr < n && tsj >= a_next) ok = false;
         }
         if (mem_check) {  // head blocked by memory at this boundary? (then for the whole stretch)
-          const u64 fr = nfree - (u64)__shfl_sync(FULLMASK, Aj, 0);
+          const u64 n0 = (u64)__shfl_sync(FULLMASK, Aj, 0);
+          const u64 fr = nfree - ((PFM && nQ == 0) ? 0ull : n0);
           const bool blocked = ((i64)fr - (i64)need_h < wm) || (ratio_h && (total - fr) + need_h > HP.ratio_limit);
           if (!blocked) ok = false;
         }
@@ -874,120 +878,12 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     clk_p = clock64();
 
     // ---------------------------------------------------------------- 3. decode reservation
-    // one pass: needing survivors -> requester list (ascending id), sum of c = ctx+1
-    u32 E = 0;
-    u64 cdp = 0, npp = 0, app = 0;
-    for (u32 b0 = 0; b0 < nR; b0 += 32) {
-      const u32 jj = b0 + lane;
-      const u32 c = jj < nR ? S.ctx[jj] : 1u;
-      const bool need = jj < nR && B.mod(c) == 0;
-      if (jj < nR) cdp += c + 1;
-      const u32 bal = __ballot_sync(FULLMASK, need);
-      if (need) {
-        const u32 e = E + __popc(bal & ltm);
-        S.req_cum[e] = e + 1;
-        S.req_pt[e] = jj | (B.div(c) << 15);
-      }
-      E += __popc(bal);
-    }
-    u32 m = 0;
-    u64 swap_out = 0;
-    if ((u64)E > nfree) {
-      // minimal m with sum_{j<=n-m} need_j <= F + sum_{j>n-m} held_j (SURVEY c.4 step 3)
-      u64 Sn = E, Hh = 0;
-      do {
-        ++m;
-        const u32 c = S.ctx[nR - m];
-        Sn -= (B.mod(c) == 0) ? 1 : 0;
-        Hh += B.cdiv(c);
-      } while (Sn > nfree + Hh);
-      u64 csub = 0;
-      for (u32 v = nR - m; v < nR; ++v) {  // victims: latest arrivals (reading A7)
-        const u32 c = S.ctx[v];
-        const u32 held = B.cdiv(c);
-        const u32 slot = S.info[v] & 0xffffu;
-        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, 0, L, hint);
-        nfree += held;
-        csub += c + 1;
-        if (SWAPM) swap_out += (u64)held * HP.block_bytes;
-        __syncwarp();
-        if (lane == 0) {
-          S.info[v] += 1u << 16;
-          if (!SWAPM) S.ctx[v] = 0;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) cdp -= csub;
-      E = (u32)Sn;  // the requester list is in position order: victims are its tail
-      nR -= m;
-      nQ += m;
-      npre += m;
-    }
-    const u32 nR3 = nR;
-    u32 Kb = E;
-    nfree -= E;
-    u32 nres = 0, nadm = 0, nrej = 0;
-    u64 swap_in = 0, tokens = nR;
-    if (m == 0) {
-      NPH(0);
-      // 4. resume, head first, stop at the first misfit
-      if (nQ > 0) {
-        u64 cum_need = 0, cum_tok = 0;
-        for (u32 b0 = 0; b0 < nQ; b0 += 32) {
-          const u32 jj = nR3 + b0 + lane;
-          const bool valid = b0 + lane < nQ;
-          u32 need = 0, tok = 0, held0 = 0, c = 0;
-          if (valid) {
-            if (SWAPM) {
-              c = S.ctx[jj];
-              need = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
-              tok = 1;
-              held0 = B.cdiv(c);
-            } else {
-              const u32 id = S.id[jj];
-              const u32 Pq = PR[id] + (OU[id] - S.rem[jj]);  // p + gen
-              need = B.cdiv(Pq);
-              tok = Pq;
-            }
-          }
-          const u32 cn = scan_incl(need), ct = scan_incl(tok);
-          const bool ok = valid && ((u64)nR3 + b0 + lane + 1 <= (u64)mns) &&
-                          (tokens + cum_tok + ct <= (u64)mbt) && ((i64)nfree - (i64)(cum_need + cn) >= wm);
-          const u32 okm = __ballot_sync(FULLMASK, ok);
-          const u32 cnt = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
-          if (lane < cnt) {
-            S.req_cum[E + lane] = Kb + cn;
-            S.req_pt[E + lane] = jj;
-            if (SWAPM) {
-              cdp += c + 1;
-            } else {
-              S.ctx[jj] = tok;  // recompute prefill of P = p + gen; ctx after commit
-              npp += tok;
-              app += (u64)tok * (tok + 1) / 2;
-            }
-          }
-          const u64 sw = warp_sum64(lane < cnt ? (u64)held0 : 0ull);
-          if (cnt) {
-            const u32 sn = __shfl_sync(FULLMASK, cn, cnt - 1), stk = __shfl_sync(FULLMASK, ct, cnt - 1);
-            cum_need += sn;
-            cum_tok += stk;
-            Kb += sn;
-            E += cnt;
-            nres += cnt;
-            if (SWAPM) swap_in += sw * HP.block_bytes;
-          }
-          if (cnt < 32) break;
-        }
-        nfree -= cum_need;
-        tokens += cum_tok;
-        nR += nres;
-        nQ -= nres;
-        __syncwarp();
-      }
-      NPH(1);
-      // 5. fresh FCFS admission
+    u32 E = 0, Kb = 0, m = 0, nres = 0, nadm = 0, nrej = 0;
+    u64 cdp = 0, npp = 0, app = 0, swap_out = 0, swap_in = 0, tokens = 0;
+    // 5. fresh FCFS admission (its own pass in prefill-first mode, NEXT-3)
+    auto fresh_admit = [&]() {
       bool head_blocked = false;
-      if (nQ == 0 && (!STATICP || nR == 0) && adm < arr) {
+      if (adm < arr) {
         // quick exit: a head that is not rejected but cannot be admitted stops step 5 at once
         const u32 off = adm - win;
         const u32 pw = __shfl_sync(FULLMASK, wp, off & 31u);
@@ -997,7 +893,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
                        ((u64)nR + 1 > mns || tokens + ph > (u64)mbt || (i64)nfree - (i64)nh < wm ||
                         (RATIO && (total - nfree) + nh > HP.ratio_limit));
       }
-      if (nQ == 0 && (!STATICP || nR == 0) && !head_blocked) {
+      if (!head_blocked) {
         while (adm < arr) {
           const u32 i = adm + lane;
           const bool valid = i < arr;
@@ -1067,6 +963,123 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           if (stop < nvalid) break;
         }
       }
+    };
+    const u32 nR_old = nR;
+    bool pf_only = false;
+    if (PFM && nQ == 0 && (!STATICP || nR == 0)) {  // prefill-first: fresh prefills alone, if any
+      fresh_admit();
+      pf_only = nadm > 0;
+    }
+    u32 nR3 = nR;
+    if (!pf_only) {
+    // one pass: needing survivors -> requester list (ascending id), sum of c = ctx+1
+    for (u32 b0 = 0; b0 < nR; b0 += 32) {
+      const u32 jj = b0 + lane;
+      const u32 c = jj < nR ? S.ctx[jj] : 1u;
+      const bool need = jj < nR && B.mod(c) == 0;
+      if (jj < nR) cdp += c + 1;
+      const u32 bal = __ballot_sync(FULLMASK, need);
+      if (need) {
+        const u32 e = E + __popc(bal & ltm);
+        S.req_cum[e] = e + 1;
+        S.req_pt[e] = jj | (B.div(c) << 15);
+      }
+      E += __popc(bal);
+    }
+    if ((u64)E > nfree) {
+      // minimal m with sum_{j<=n-m} need_j <= F + sum_{j>n-m} held_j (SURVEY c.4 step 3)
+      u64 Sn = E, Hh = 0;
+      do {
+        ++m;
+        const u32 c = S.ctx[nR - m];
+        Sn -= (B.mod(c) == 0) ? 1 : 0;
+        Hh += B.cdiv(c);
+      } while (Sn > nfree + Hh);
+      u64 csub = 0;
+      for (u32 v = nR - m; v < nR; ++v) {  // victims: latest arrivals (reading A7)
+        const u32 c = S.ctx[v];
+        const u32 held = B.cdiv(c);
+        const u32 slot = S.info[v] & 0xffffu;
+        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, 0, L, hint);
+        nfree += held;
+        csub += c + 1;
+        if (SWAPM) swap_out += (u64)held * HP.block_bytes;
+        __syncwarp();
+        if (lane == 0) {
+          S.info[v] += 1u << 16;
+          if (!SWAPM) S.ctx[v] = 0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) cdp -= csub;
+      E = (u32)Sn;  // the requester list is in position order: victims are its tail
+      nR -= m;
+      nQ += m;
+      npre += m;
+    }
+    nR3 = nR;
+    Kb = E;
+    nfree -= E;
+    tokens = nR;
+    if (m == 0) {
+      NPH(0);
+      // 4. resume, head first, stop at the first misfit
+      if (nQ > 0) {
+        u64 cum_need = 0, cum_tok = 0;
+        for (u32 b0 = 0; b0 < nQ; b0 += 32) {
+          const u32 jj = nR3 + b0 + lane;
+          const bool valid = b0 + lane < nQ;
+          u32 need = 0, tok = 0, held0 = 0, c = 0;
+          if (valid) {
+            if (SWAPM) {
+              c = S.ctx[jj];
+              need = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
+              tok = 1;
+              held0 = B.cdiv(c);
+            } else {
+              const u32 id = S.id[jj];
+              const u32 Pq = PR[id] + (OU[id] - S.rem[jj]);  // p + gen
+              need = B.cdiv(Pq);
+              tok = Pq;
+            }
+          }
+          const u32 cn = scan_incl(need), ct = scan_incl(tok);
+          const bool ok = valid && ((u64)nR3 + b0 + lane + 1 <= (u64)mns) &&
+                          (tokens + cum_tok + ct <= (u64)mbt) && ((i64)nfree - (i64)(cum_need + cn) >= wm);
+          const u32 okm = __ballot_sync(FULLMASK, ok);
+          const u32 cnt = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+          if (lane < cnt) {
+            S.req_cum[E + lane] = Kb + cn;
+            S.req_pt[E + lane] = jj;
+            if (SWAPM) {
+              cdp += c + 1;
+            } else {
+              S.ctx[jj] = tok;  // recompute prefill of P = p + gen; ctx after commit
+              npp += tok;
+              app += (u64)tok * (tok + 1) / 2;
+            }
+          }
+          const u64 sw = warp_sum64(lane < cnt ? (u64)held0 : 0ull);
+          if (cnt) {
+            const u32 sn = __shfl_sync(FULLMASK, cn, cnt - 1), stk = __shfl_sync(FULLMASK, ct, cnt - 1);
+            cum_need += sn;
+            cum_tok += stk;
+            Kb += sn;
+            E += cnt;
+            nres += cnt;
+            if (SWAPM) swap_in += sw * HP.block_bytes;
+          }
+          if (cnt < 32) break;
+        }
+        nfree -= cum_need;
+        tokens += cum_tok;
+        nR += nres;
+        nQ -= nres;
+        __syncwarp();
+      }
+      NPH(1);
+      if (!PFM && nQ == 0 && (!STATICP || nR == 0)) fresh_admit();
+    }
     }
     nrej_tot += nrej;
     NPH(2);
@@ -1078,9 +1091,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       break;
     }
     NPH(3);
-    // 7. cost: decodes are positions [0, D), prefills [D, nR)
-    const u32 D = nR3 + (SWAPM ? nres : 0u);
-    const u32 Sp = nR - D;
+    // 7. cost: decodes are positions [0, D), prefills [D, nR); a prefill-first iteration runs
+    // only the fresh prefills at [nR_old, nR)
+    const u32 D = pf_only ? 0u : nR3 + (SWAPM ? nres : 0u);
+    const u32 Sp = pf_only ? nR - nR_old : nR - D;
+    const u32 c0 = pf_only ? nR_old : 0u;
     const u64 Cd = warp_sum64(cdp);
     u64 Np = 0, Ap = 0;
     if (Sp) {
@@ -1094,7 +1109,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     const u64 blocks = total - nfree;
     u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
     const u32 fresh0 = nR3 + nres;
-    for (u32 b0 = 0; b0 < nR; b0 += 32) {
+    for (u32 b0 = c0; b0 < nR; b0 += 32) {
       const u32 jj = b0 + lane;
       bool fin = false;
       if (jj < nR) {
@@ -1136,9 +1151,12 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       }
     }
     NPH(5);
-    rmin = __reduce_min_sync(FULLMASK, rmin_l);
+    {
+      const u32 rn = __reduce_min_sync(FULLMASK, rmin_l);
+      rmin = pf_only ? min(rmin, rn) : rn;  // paused requests keep their rem
+    }
     __syncwarp();
-    req_iters += nR;
+    req_iters += nR - c0;
     NPH(6);
     if (nfin) {
       // stable compaction of R u Q, dropping finished entries (rem == 0 within R)

@@ -272,3 +272,17 @@ def test_c5_reduced_grid(api):
     s = sw.summaries()
     assert (s["n_finished"] == 300).all() and (s["status_flags"] & 16 == 0).all()
     check_pd_points(sw, cfg, sample_points(cfg.num_points, target=40, corners=[0, 1, 767, 768, 1535]))
+
+
+def test_prefill_first_parity(api):
+    """NEXT-3 prefill-first iterations: C2 in full, and random micro configs."""
+    cfg = replace(si.c2(), policies=[si.Policy(iteration_mode=si.PREFILL_FIRST)])
+    sw = run_gpu(api, cfg)
+    check_points(sw, cfg, list(range(cfg.num_points)), records=True)
+    off = run_gpu(api, replace(cfg, options=replace(cfg.options, fast_forward=False)))
+    assert sw.summaries().tobytes() == off.summaries().tobytes()
+    rng = np.random.default_rng(23)
+    for _ in range(40):
+        c = _micro(rng)
+        c = replace(c, policies=[replace(c.policies[0], iteration_mode=si.PREFILL_FIRST)])
+        check_points(run_gpu(api, c), c, [0], records=True, trace=True, iters=True)

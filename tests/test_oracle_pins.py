@@ -607,3 +607,41 @@ def test_pd_finding5_prefill_footprint(oracle_lib):
     uP = tp["block_ns"][sel].sum() / O.derive(cfg, 1, 0)["total_blocks"]
     uD = td["block_ns"][sel].sum() / O.derive(cfg, 1, 1)["total_blocks"]
     assert uP < 0.5 * uD
+
+
+# ------------------------------------------------------------------ NEXT-3 prefill-first iterations
+def test_prefill_first_two_request_trace(oracle_lib):
+    """vLLM v0.6.2 default (ext, reading R-N3): an admissible fresh request gets a prefill-only
+    iteration and the running request pauses, so its next token gap spans that iteration."""
+    reqs = [(0, 20, 3), (1_000_000, 10, 2)]
+    cfg = trace_cfg(reqs, pol=si.Policy(iteration_mode=si.PREFILL_FIRST))
+    r = _sim(cfg, want=("summary", "records", "iters"))
+    it, rec = r["iters"], r["records"]
+    t_pre20, t_pre10 = _t(cfg, prefills=[20]), _t(cfg, prefills=[10])
+    t_d = _t(cfg, decodes=[21, 11])
+    t_d2 = _t(cfg, decodes=[22])
+    assert list(it["T_ns"]) == [t_pre20, t_pre10, t_d, t_d2]
+    assert list(it["S_p"]) == [1, 1, 0, 0] and list(it["D"]) == [0, 0, 2, 1]
+    assert rec["ttft_ns"][0] == t_pre20
+    assert rec["ttft_ns"][1] == t_pre20 + t_pre10 - 1_000_000
+    assert rec["e2e_ns"][1] == t_pre20 + t_pre10 + t_d - 1_000_000
+    assert rec["e2e_ns"][0] == t_pre20 + t_pre10 + t_d + t_d2
+    assert rec["mtpot_ns"][0] == max(t_pre10 + t_d, t_d2)       # the paused iteration counts
+    mixed = _sim(trace_cfg(reqs), want=("summary", "iters"))
+    assert mixed["summary"]["n_iterations"] == 3
+
+
+def test_prefill_first_iteration_shapes(oracle_lib):
+    """Every prefill-first iteration is either prefill-only (fresh admissions, no decodes) or a
+    decode iteration with no fresh admission; invariants hold on random micro configs."""
+    rng = np.random.default_rng(31)
+    for _ in range(60):
+        cfg, o = _random_micro(rng)
+        cfg = replace(cfg, policies=[replace(cfg.policies[0], iteration_mode=si.PREFILL_FIRST)])
+        r = _sim(cfg, want=("summary", "records", "iters"))
+        it, s = r["iters"], r["summary"]
+        pf = it["n_admitted"] > 0
+        assert (it["D"][pf] == 0).all() and (it["S_p"][pf] == it["n_admitted"][pf]).all()
+        assert (it["n_admitted"][~pf] == 0).all()
+        fin = r["records"]["status"] == 1
+        assert s["n_request_iterations"] == int(o[fin].sum()) and s["n_finished"] + s["n_rejected"] == len(o)
