@@ -970,7 +970,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       fresh_admit();
       pf_only = nadm > 0;
     }
-    u32 nR3 = nR;
+    u32 nR3 = nR_old;  // fresh prefills of a prefill-first iteration start at nR_old
     if (!pf_only) {
     // one pass: needing survivors -> requester list (ascending id), sum of c = ctx+1
     for (u32 b0 = 0; b0 < nR; b0 += 32) {
