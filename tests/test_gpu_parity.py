@@ -286,3 +286,19 @@ def test_prefill_first_parity(api):
         c = _micro(rng)
         c = replace(c, policies=[replace(c.policies[0], iteration_mode=si.PREFILL_FIRST)])
         check_points(run_gpu(api, c), c, [0], records=True, trace=True, iters=True)
+
+
+def test_large_point_summary_scratch_path(api):
+    """n = 20,000 requests per point exceeds the summary kernel's shared-memory key buffer
+    (12,288), so quantiles run over the workspace scratch path; also exercises a trace cap."""
+    w = si.Workload(20_000, [30.0, 60.0], [5], len_dist=si.UNIFORM, prompt_a=16, prompt_b=256,
+                    output_a=2, output_b=64)
+    cfg = si.SweepConfig("big", si.LLAMA2_7B, [si.Hw(mem_capacity=40 * 10 ** 9)],
+                         [si.Policy(), si.Policy(kind=si.CONT_RATIO, max_mem_ratio=0.5, preempt=si.RECOMPUTE)], w,
+                         si.Options(trace_cap_bytes=32 * 100))
+    sw = run_gpu(api, cfg)
+    check_points(sw, cfg, list(range(cfg.num_points)), records=True, trace=True)
+    assert (sw.summaries()["status_flags"] & 1).all()   # 100-sample cap overflowed
+    for p in range(cfg.num_points):
+        q = sw.latency_quantiles(p, "e2e", [1234, 5000, 9999])
+        assert (np.diff(q) >= 0).all()
