@@ -225,7 +225,8 @@ bool workload(const oracle_cfg &c, std::vector<i64> &a, std::vector<u32> &p, std
 
 // ----------------------------------------------------------------- c.5 cost model
 struct Prefill {
-  u64 P, c0;
+  u64 P, c0;          // P new tokens after c0 already-computed ones (c0 > 0: a later chunk)
+  bool emits = true;  // the entry samples a token (false for a non-final chunk, reading R-N3b)
 };
 
 struct CostCtx {
@@ -256,12 +257,13 @@ CostCtx cost_ctx(const oracle_cfg &c, const oracle_derived &d, int decode_worker
 
 i64 iter_time(const CostCtx &K, const std::vector<Prefill> &pf, const std::vector<u64> &dec,
               u64 swap_bytes) {
-  u64 Np = 0, Ap = 0, Kp = 0, Cd = 0;
-  const u64 Sp = pf.size(), D = dec.size();
+  u64 Np = 0, Ap = 0, Kp = 0, Cd = 0, Sp = 0;
+  const u64 D = dec.size();
   for (const Prefill &e : pf) {
     Np += e.P;
     Ap += e.P * e.c0 + e.P * (e.P + 1) / 2;
     Kp += e.c0 + e.P;
+    Sp += e.emits ? 1 : 0;  // LM head rows: entries that sample a token
   }
   for (u64 c : dec) Cd += c;
   const u64 N = Np + D, S = Sp + D;
@@ -309,6 +311,8 @@ struct Req {
   i64 first_tok = 0, last_tok = 0, max_gap = 0;
   u32 n_preempt = 0;
   std::vector<u32> blocks;  // logical order
+  bool pref = false;        // CHUNKED: prefill in progress (blocks held for p + gen)
+  u64 pdone = 0;            // CHUNKED: prefill tokens computed so far
   i64 finish = 0;
   u64 finish_k = 0;
 };
@@ -440,9 +444,18 @@ bool check_invariants(const std::vector<Req> &req, const std::set<u32> &R, const
                       const std::set<u32> &freeset, u64 total, u64 bs) {
   std::set<u32> seen(freeset.begin(), freeset.end());
   u64 alloc = 0;
+  u32 n_pref = 0;
   for (u32 id : R) {
     const Req &r = req[id];
-    if (r.blocks.size() != ceil_div(r.ctx, bs)) return fail("held != ceil(ctx/bs) for request " + std::to_string(id));
+    // a chunked prefill in progress holds the blocks of its whole target p + gen (reading R-N3b)
+    const u64 want = r.pref ? ceil_div((u64)r.p + r.gen, bs) : ceil_div(r.ctx, bs);
+    if (r.blocks.size() != want) return fail("held != ceil(ctx/bs) for request " + std::to_string(id));
+    if (r.pref) {
+      // derived property of R-N3b (the budget runs out at the last prefill entry): at most one
+      // prefill is in progress and it is the latest arrival in R
+      if (++n_pref > 1 || id != *R.rbegin()) return fail("chunked prefill not at the tail of R");
+      if (r.pdone == 0 || r.pdone >= (u64)r.p + r.gen) return fail("chunk progress out of range");
+    }
     for (u32 b : r.blocks) {
       if (b >= total) return fail("block id out of range");
       if (!seen.insert(b).second) return fail("block " + std::to_string(b) + " in two lists");
@@ -461,6 +474,10 @@ bool check_invariants(const std::vector<Req> &req, const std::set<u32> &R, const
 oracle_run *simulate_unified(const oracle_cfg &c) {
   oracle_derived d;
   if (!derive(c, 0, d)) return nullptr;
+  if (c.iter_mode == OR_CHUNKED && c.max_batched_tokens < c.max_num_seqs) {
+    g_err = "CHUNKED needs max_batched_tokens >= max_num_seqs (every decode fits the budget)";
+    return nullptr;
+  }
   const CostCtx K = cost_ctx(c, d, 0);
   std::vector<i64> A;
   std::vector<u32> Pl, Ol;
@@ -526,6 +543,8 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
     u64 n_res = 0, n_adm = 0, n_rej = 0, swap_in = 0, m = 0, swap_out = 0;
     // NEXT-3 prefill-first (vLLM v0.6.2 default, reading R-N3): when fresh requests can be
     // admitted the iteration runs only their prefills; the running requests pause
+    const bool CH = c.iter_mode == OR_CHUNKED;
+    std::map<u32, u64> chunk;  // CHUNKED: this iteration's chunk length per prefill entry
     auto fresh_admission = [&](u64 tokens) {
       while (adm < arr) {
         Req &x = req[adm];
@@ -539,13 +558,22 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
         }
         const u64 fr = freeset.size();
         if (R.size() + 1 > c.max_num_seqs) break;
-        if (tokens + x.p > c.max_batched_tokens) break;
+        // CHUNKED (R-N3b): one token of budget suffices; the chunk is what is left of it
+        if (CH ? tokens + 1 > c.max_batched_tokens : tokens + x.p > c.max_batched_tokens) break;
         if ((i64)fr - (i64)need < (i64)c.watermark_blocks) break;
         if (RATIO && (total - fr) + need > d.ratio_limit) break;
         alloc_lowest(adm, need);
         R.insert(adm);
         kind[adm] = K_PRE_FRESH;
-        tokens += x.p;
+        if (CH) {
+          const u64 ch = std::min<u64>(x.p, c.max_batched_tokens - tokens);
+          x.pref = true;
+          x.pdone = 0;
+          chunk[adm] = ch;
+          tokens += ch;
+        } else {
+          tokens += x.p;
+        }
         ++n_adm;
         ++adm;
       }
@@ -557,7 +585,8 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
     const u64 F = freeset.size();
     std::vector<u32> Rv;
     if (!pf_only) Rv.assign(R.begin(), R.end());
-    auto need_of = [&](u32 id) -> u64 { return (req[id].ctx % bs == 0) ? 1 : 0; };
+    // a prefill in progress decodes nothing and already holds its blocks (R-N3b)
+    auto need_of = [&](u32 id) -> u64 { return (!req[id].pref && req[id].ctx % bs == 0) ? 1 : 0; };
     u64 sum_need = 0;
     for (u32 id : Rv) sum_need += need_of(id);
     if (sum_need > F) {
@@ -579,7 +608,11 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
         const u64 held = x.blocks.size();
         free_all(id);
         x.n_preempt += 1;
-        if (SWAPM) {
+        if (x.pref) {  // partial prefill: its KV is discarded whatever the mode (R-N3b)
+          x.pref = false;
+          x.pdone = 0;
+          x.ctx = 0;
+        } else if (SWAPM) {
           swap_out += held * d.block_bytes;
         } else {
           x.ctx = 0;
@@ -589,40 +622,66 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
       }
       n_preempt_total += m;
     }
+    u64 D3 = 0;
     if (!pf_only) {
       for (u32 id : R) {  // surviving requests, ascending id
+        if (req[id].pref) continue;
         kind[id] = K_DEC;
+        ++D3;
         if (need_of(id)) alloc_lowest(id, 1);
       }
     }
-    const u64 D3 = pf_only ? 0 : R.size();
     u64 tokens = D3;
+    if (CH) {
+      // continuing chunked prefills take the budget left by the decodes, in id order (R-N3b)
+      for (u32 id : R) {
+        Req &x = req[id];
+        if (!x.pref) continue;
+        const u64 ch = std::min<u64>((u64)x.p + x.gen - x.pdone, c.max_batched_tokens - tokens);
+        if (ch == 0) continue;  // no budget left: it sits this iteration out
+        kind[id] = x.gen == 0 ? K_PRE_FRESH : K_PRE_RECOMP;
+        chunk[id] = ch;
+        tokens += ch;
+      }
+    }
     if (m == 0 && !pf_only) {
       // 4. resume, head first, stop at the first misfit (reading A6)
       std::vector<u32> Qv(Q.begin(), Q.end());
       for (u32 id : Qv) {
         Req &x = req[id];
         u64 need, tok;
-        if (SWAPM) {
+        // re-prefill p + gen under RECOMPUTE, and (CHUNKED) after losing a partial prefill
+        const bool recomp = !SWAPM || x.ctx == 0;
+        if (!recomp) {
           need = ceil_div(x.ctx, bs) + ((x.ctx % bs == 0) ? 1 : 0);
           tok = 1;
         } else {
           need = ceil_div(x.p + x.gen, bs);
           tok = x.p + x.gen;
         }
-        const bool ok = (R.size() + 1 <= c.max_num_seqs) && (tokens + tok <= c.max_batched_tokens) &&
+        const bool ok = (R.size() + 1 <= c.max_num_seqs) &&
+                        (CH ? tokens + 1 <= c.max_batched_tokens : tokens + tok <= c.max_batched_tokens) &&
                         ((i64)freeset.size() - (i64)need >= (i64)c.watermark_blocks);
         if (!ok) break;
         alloc_lowest(id, need);
         Q.erase(id);
         R.insert(id);
         ++n_res;
-        tokens += tok;
-        if (SWAPM) {
+        if (CH && recomp) {
+          const u64 ch = std::min<u64>(tok, c.max_batched_tokens - tokens);
+          x.pref = true;
+          x.pdone = 0;
+          chunk[id] = ch;
+          tokens += ch;
+        } else {
+          tokens += tok;
+        }
+        if (!recomp) {
           swap_in += ceil_div(x.ctx, bs) * d.block_bytes;
           kind[id] = K_DEC;
         } else {
-          kind[id] = K_PRE_RECOMP;
+          // gen = 0: a chunked prefill lost before its first token starts over as a fresh one
+          kind[id] = x.gen == 0 ? K_PRE_FRESH : K_PRE_RECOMP;
         }
       }
       // 5. fresh FCFS admission (STATIC P:167/A16; ratio P:460/A15); in
@@ -642,6 +701,10 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
       if (kv.second == K_DEC) {
         dec.push_back(x.ctx + 1);
         Cd += x.ctx + 1;
+      } else if (CH) {  // a chunk of L tokens after pdone computed ones (R-N3b)
+        const u64 L = chunk.at(id);
+        pf.push_back({L, x.pdone, x.pdone + L == (u64)x.p + x.gen});
+        Np += L;
       } else if (kv.second == K_PRE_FRESH) {
         pf.push_back({x.p, 0});
         Np += x.p;
@@ -660,6 +723,12 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
       const u32 id = kv.first;
       Req &x = req[id];
       const Kind kd = kv.second;
+      if (CH && kd != K_DEC) {
+        x.pdone += chunk.at(id);
+        if (x.pdone < (u64)x.p + x.gen) continue;  // non-final chunk: no token yet
+        x.pref = false;
+        x.pdone = 0;
+      }
       if (kd == K_PRE_FRESH) {
         x.ctx = x.p;
         x.gen = 1;
@@ -1210,14 +1279,14 @@ int oracle_workload(const oracle_cfg *cfg, int64_t *arrival, uint32_t *prompt, u
 }
 
 int64_t oracle_iter_time_ns(const oracle_cfg *cfg, int decode_worker, uint32_t n_prefill,
-                            const uint32_t *P, const uint32_t *c0, uint32_t n_decode,
-                            const uint32_t *c, uint64_t swap_bytes) {
+                            const uint32_t *P, const uint32_t *c0, const uint32_t *emits,
+                            uint32_t n_decode, const uint32_t *c, uint64_t swap_bytes) {
   oracle_derived d;
   if (!derive(*cfg, decode_worker, d)) return -1;
   const CostCtx K = cost_ctx(*cfg, d, decode_worker);
   std::vector<Prefill> pf;
   std::vector<u64> dec;
-  for (u32 i = 0; i < n_prefill; ++i) pf.push_back({P[i], c0[i]});
+  for (u32 i = 0; i < n_prefill; ++i) pf.push_back({P[i], c0[i], emits ? emits[i] != 0 : true});
   for (u32 i = 0; i < n_decode; ++i) dec.push_back(c[i]);
   return iter_time(K, pf, dec, swap_bytes);
 }

@@ -21,7 +21,7 @@ enum { OR_SWAP = 0, OR_RECOMPUTE = 1 };
 enum { OR_LEN_FIXED = 1, OR_LEN_UNIFORM = 2, OR_LEN_TABLE = 3, OR_LEN_TRACE = 4 };
 enum { OR_TRACE_NONE = 0, OR_TRACE_BINNED = 1, OR_TRACE_FULL = 2 };
 enum { OR_UNIFIED = 0, OR_PD_PAIR = 1 };
-enum { OR_MIXED = 0, OR_PREFILL_FIRST = 1 };
+enum { OR_MIXED = 0, OR_PREFILL_FIRST = 1, OR_CHUNKED = 2 };
 
 typedef struct {
   /* model */
@@ -64,7 +64,7 @@ typedef struct {
   int64_t horizon_ns;
   uint32_t check_invariants;   /* 1: assert c.8 invariants every iteration */
   uint32_t keep_events;        /* 1: keep the block event log              */
-  uint32_t iter_mode;          /* OR_MIXED (A3) | OR_PREFILL_FIRST (NEXT-3) */
+  uint32_t iter_mode;          /* OR_MIXED (A3) | OR_PREFILL_FIRST | OR_CHUNKED (NEXT-3) */
 } oracle_cfg;
 
 typedef struct {
@@ -119,10 +119,11 @@ double oracle_det_log(double u);
 /* returns 0, or -1 with a message from oracle_error() */
 int oracle_derive(const oracle_cfg *cfg, int decode_worker, oracle_derived *out);
 int oracle_workload(const oracle_cfg *cfg, int64_t *arrival, uint32_t *prompt, uint32_t *output);
-/* iteration time of one explicit batch (c.5): prefill entries (P[i], c0[i]), decode contexts c[j] */
+/* iteration time of one explicit batch (c.5): prefill entries (P[i], c0[i]) -- emits[i] = 0 marks
+   a non-final chunk without an LM-head row (NULL: all emit) -- and decode contexts c[j] */
 int64_t oracle_iter_time_ns(const oracle_cfg *cfg, int decode_worker, uint32_t n_prefill,
-                            const uint32_t *P, const uint32_t *c0, uint32_t n_decode,
-                            const uint32_t *c, uint64_t swap_bytes);
+                            const uint32_t *P, const uint32_t *c0, const uint32_t *emits,
+                            uint32_t n_decode, const uint32_t *c, uint64_t swap_bytes);
 uint64_t oracle_fold(const uint64_t *fields, uint32_t n);
 
 /* ---- one point, start to finish ---- */

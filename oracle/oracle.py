@@ -111,7 +111,7 @@ def lib():
         L.oracle_derive.restype = C.c_int
         L.oracle_workload.argtypes = [C.POINTER(OracleCfg), PI64, PU32, PU32]
         L.oracle_workload.restype = C.c_int
-        L.oracle_iter_time_ns.argtypes = [C.POINTER(OracleCfg), C.c_int, u32, PU32, PU32, u32, PU32, u64]
+        L.oracle_iter_time_ns.argtypes = [C.POINTER(OracleCfg), C.c_int, u32, PU32, PU32, PU32, u32, PU32, u64]
         L.oracle_iter_time_ns.restype = i64
         L.oracle_fold.argtypes = [C.POINTER(u64), u32]
         L.oracle_fold.restype = u64
@@ -177,7 +177,7 @@ def make_cfg(cfg: si.SweepConfig, point: int, check_invariants: bool = False,
     c.kind, c.preempt, c.max_mem_ratio = _KIND[p.kind], _PRE[p.preempt], p.max_mem_ratio
     c.max_num_seqs, c.max_batched_tokens = p.max_num_seqs, p.max_batched_tokens
     c.block_size, c.watermark_blocks = p.block_size, p.watermark_blocks
-    c.iter_mode = {si.MIXED: 0, si.PREFILL_FIRST: 1}[p.iteration_mode]
+    c.iter_mode = {si.MIXED: 0, si.PREFILL_FIRST: 1, si.CHUNKED: 2}[p.iteration_mode]
     c.num_requests, c.rate, c.seed = w.num_requests, w.rates[rate_i], w.seeds[seed_i]
     c.len_dist = _LEN[w.len_dist]
     c.prompt_a, c.prompt_b, c.output_a, c.output_b = w.prompt_a, w.prompt_b, w.output_a, w.output_b
@@ -296,13 +296,14 @@ def workload(cfg: si.SweepConfig, point: int = 0):
 
 def iter_time_ns(cfg: si.SweepConfig, prefills=(), decodes=(), swap_bytes: int = 0,
                  point: int = 0, decode_worker: int = 0) -> int:
-    """T_ns of one explicit batch: prefills = [(P, c0), ...], decodes = [c, ...]."""
+    """T_ns of one explicit batch: prefills = [(P, c0) or (P, c0, emits), ...], decodes = [c, ...]."""
     L = lib()
     c, keep = make_cfg(cfg, point)
     P, pP = _u32arr([x[0] for x in prefills] or [0])
     c0, pc0 = _u32arr([x[1] for x in prefills] or [0])
+    em, pem = _u32arr([int(x[2]) if len(x) > 2 else 1 for x in prefills] or [1])
     dc, pdc = _u32arr(list(decodes) or [0])
-    return L.oracle_iter_time_ns(C.byref(c), decode_worker, len(prefills), pP, pc0, len(decodes), pdc,
+    return L.oracle_iter_time_ns(C.byref(c), decode_worker, len(prefills), pP, pc0, pem, len(decodes), pdc,
                                  swap_bytes)
 
 

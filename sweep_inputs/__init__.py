@@ -65,7 +65,7 @@ A100_IDEAL = Hw(eff_flops=1.0, eff_bw=1.0, iter_overhead_s=0.0)
 # ---------------------------------------------------------------- policies
 STATIC, CONT, CONT_RATIO = "static", "cont", "cont_ratio"
 SWAP, RECOMPUTE = "swap", "recompute"
-MIXED, PREFILL_FIRST = "mixed", "prefill_first"
+MIXED, PREFILL_FIRST, CHUNKED = "mixed", "prefill_first", "chunked"
 
 
 @dataclass(frozen=True)
@@ -78,7 +78,7 @@ class Policy:
     max_batched_tokens: int = UINT32_MAX
     block_size: int = 16
     watermark_blocks: int = 0
-    iteration_mode: str = MIXED     # MIXED (A3) | PREFILL_FIRST (vLLM v0.6.2 default, NEXT-3)
+    iteration_mode: str = MIXED     # MIXED (A3) | PREFILL_FIRST (vLLM v0.6.2 default) | CHUNKED (NEXT-3)
 
 
 # ---------------------------------------------------------------- workload

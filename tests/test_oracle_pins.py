@@ -645,3 +645,121 @@ def test_prefill_first_iteration_shapes(oracle_lib):
         assert (it["n_admitted"][~pf] == 0).all()
         fin = r["records"]["status"] == 1
         assert s["n_request_iterations"] == int(o[fin].sum()) and s["n_finished"] + s["n_rejected"] == len(o)
+
+
+# ------------------------------------------------------------------ NEXT-3b chunked prefill
+def _tc(cfg, prefills=(), decodes=()):
+    """Cost of a batch with explicit chunks (P, c0, emits)."""
+    from oracle import oracle as O
+    return O.iter_time_ns(cfg, list(prefills), decodes, 0)
+
+
+@pytest.mark.parametrize("model", [si.LLAMA2_7B, si.LLAMA2_70B])
+def test_chunk_cost_limits(oracle_lib, model):
+    """A chunk of L tokens after c0 computed ones (c.5 with c0 > 0): compute-bound it costs
+    2 FLOPs per linear weight per token plus causal attention 4*q*Lyr*(L*c0 + L(L+1)/2), plus the
+    LM-head row only if it emits; memory-bound each prefix token adds exactly kvb bytes."""
+    pub = gold("llama2_published.json")["models"][model.name]
+    F, B = 312e12, 2.039e12
+    cfg_f = _one(model, si.Hw(peak_flops=F, mem_bw=1e30, eff_flops=1, eff_bw=1, iter_overhead_s=0,
+                              mem_capacity=10 ** 12))
+    cfg_b = _one(model, si.Hw(peak_flops=1e30, mem_bw=B, eff_flops=1, eff_bw=1, iter_overhead_s=0,
+                              mem_capacity=10 ** 12))
+    L, h, V = model.num_layers, model.hidden, model.vocab
+    q = model.num_heads * model.head_dim
+    linear = pub["params"] - 2 * V * h - (2 * L + 1) * h
+    for P, c0 in ((1, 0), (16, 16), (512, 1536), (100, 7)):
+        for emits in (True, False):
+            flops = 2 * P * linear + 4 * q * L * (P * c0 + P * (P + 1) // 2) + (2 * h * V if emits else 0)
+            assert abs(_tc(cfg_f, [(P, c0, emits)]) - flops / F * 1e9) <= 2
+    # the causal-attention FLOPs of the chunks of one prompt add up to the whole prompt's
+    chunks = [(16, 0, False), (16, 16, False), (8, 32, True)]
+    att = sum(4 * q * L * (P * c0 + P * (P + 1) // 2) for P, c0, _ in chunks)
+    assert att == 4 * q * L * 40 * 41 // 2
+    d = _tc(cfg_b, [(1, 1001, False)]) - _tc(cfg_b, [(1, 1, False)])
+    assert abs(d - 1000 * pub["kvb"] / B * 1e9) <= 2
+
+
+def test_chunked_single_request_trace(oracle_lib):
+    """Budget 16 (R-N3b): a 40-token prompt runs as chunks 16 + 16 + 8; only the last emits the
+    first token; then two decodes."""
+    pol = si.Policy(iteration_mode=si.CHUNKED, max_batched_tokens=16, max_num_seqs=8)
+    cfg = trace_cfg([(0, 40, 3)], pol=pol)
+    r = _sim(cfg, want=("summary", "records", "iters"))
+    it, rec, s = r["iters"], r["records"][0], r["summary"]
+    T = [_tc(cfg, [(16, 0, False)]), _tc(cfg, [(16, 16, False)]), _tc(cfg, [(8, 32, True)]),
+         _tc(cfg, decodes=[41]), _tc(cfg, decodes=[42])]
+    assert list(it["T_ns"]) == T
+    assert list(it["S_p"]) == [1, 1, 1, 0, 0] and list(it["D"]) == [0, 0, 0, 1, 1]
+    assert list(it["N_p"]) == [16, 16, 8, 0, 0]
+    assert rec["ttft_ns"] == sum(T[:3]) and rec["e2e_ns"] == sum(T) and rec["mtpot_ns"] == max(T[3:])
+    assert s["n_request_iterations"] == 5
+
+
+def test_chunked_two_request_budget_split(oracle_lib):
+    """Decodes take the budget first, then the prefill in progress, then new arrivals (vLLM v0.6.2
+    chunked-prefill order): r0 decodes while r1's 30-token prompt is chunked 15 + 15 under a
+    budget of 16."""
+    pol = si.Policy(iteration_mode=si.CHUNKED, max_batched_tokens=16, max_num_seqs=4)
+    cfg = trace_cfg([(0, 8, 4), (0, 30, 2)], pol=pol)
+    r = _sim(cfg, want=("summary", "records", "iters"))
+    it, rec = r["iters"], r["records"]
+    # k0: r0 prefill 8 (emits) + r1 chunk 8 (budget 16); k1: r0 decode + r1 chunk 15;
+    # k2: r0 decode + r1 chunk 7 (emits); k3: r0 decode (finishes) + r1 decode (finishes)
+    T = [_tc(cfg, [(8, 0, True), (8, 0, False)]),
+         _tc(cfg, [(15, 8, False)], [9]),
+         _tc(cfg, [(7, 23, True)], [10]),
+         _tc(cfg, decodes=[11, 31])]
+    assert list(it["T_ns"]) == T
+    assert list(it["N_p"]) == [16, 15, 7, 0] and list(it["D"]) == [0, 1, 1, 2]
+    assert list(it["n_admitted"]) == [2, 0, 0, 0]
+    assert rec["ttft_ns"][0] == T[0] and rec["ttft_ns"][1] == sum(T[:3])
+    assert rec["e2e_ns"][0] == sum(T) and rec["e2e_ns"][1] == sum(T)
+    assert rec["mtpot_ns"][0] == max(T[1:]) and rec["mtpot_ns"][1] == T[3]
+
+
+def test_chunked_unbounded_budget_equals_mixed(oracle_lib):
+    """With an unbounded token budget every chunk is the whole prefill, so CHUNKED reduces to
+    MIXED (A3) exactly: same iterations, records and summary."""
+    rng = np.random.default_rng(77)
+    for _ in range(60):
+        cfg, _o = _random_micro(rng)
+        pol = replace(cfg.policies[0], max_batched_tokens=si.UINT32_MAX)
+        a = _sim(replace(cfg, policies=[pol]), want=("summary", "records", "iters"))
+        b = _sim(replace(cfg, policies=[replace(pol, iteration_mode=si.CHUNKED)]),
+                 want=("summary", "records", "iters"))
+        assert repr(a["summary"]) == repr(b["summary"])
+        assert a["records"].tobytes() == b["records"].tobytes()
+        assert a["iters"].tobytes() == b["iters"].tobytes()
+
+
+def test_chunked_budget_and_invariants(oracle_lib):
+    """Random micro configs under small budgets: every iteration fits the budget (N_p + D <= B),
+    held = blocks of the whole target, at most one prefill in progress (checked inside the
+    oracle), FCFS first tokens, every request finished or rejected, and prompts longer than the
+    budget are served."""
+    rng = np.random.default_rng(4242)
+    long_served = npre = 0
+    for _ in range(120):
+        cfg, o = _random_micro(rng)
+        pol = cfg.policies[0]
+        budget = int(rng.choice([pol.max_num_seqs, 16, 40, 100])) if pol.max_num_seqs <= 16 else \
+            int(rng.choice([256, 300]))
+        budget = max(budget, min(pol.max_num_seqs, 256))
+        pol = replace(pol, iteration_mode=si.CHUNKED, max_batched_tokens=budget)
+        cfg = replace(cfg, policies=[pol])
+        r = _sim(cfg, want=("summary", "records", "iters"))
+        s, rec, it = r["summary"], r["records"], r["iters"]
+        assert (it["N_p"].astype(np.int64) + it["D"] <= budget).all()
+        fin = rec["status"] == 1
+        assert s["n_finished"] + s["n_rejected"] == len(rec)
+        assert s["n_request_iterations"] >= int(o[fin].sum())
+        assert s["n_request_iterations"] == int((it["S_p"] + it["D"]).sum())
+        first = rec["ttft_ns"][fin] + np.asarray(cfg.workload.trace_arrival_ns)[fin]
+        assert (np.diff(first) >= 0).all()
+        p = np.asarray(cfg.workload.trace_prompt)
+        long_served += int((fin & (p > budget)).sum())
+        npre += s["n_preemptions"]
+        if pol.kind != si.CONT_RATIO:
+            assert s["n_rejected"] == 0
+    assert long_served > 0 and npre > 0
