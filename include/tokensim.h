@@ -61,7 +61,7 @@ typedef enum {
 /* ---- enums --------------------------------------------------------------- */
 enum { TOKENSIM_STATIC = 0, TOKENSIM_CONT = 1, TOKENSIM_CONT_RATIO = 2 };   /* policy.kind   */
 enum { TOKENSIM_SWAP = 0, TOKENSIM_RECOMPUTE = 1 };                         /* policy.preempt*/
-enum { TOKENSIM_MIXED = 0, TOKENSIM_PREFILL_FIRST = 1 };                    /* policy.iteration_mode */
+enum { TOKENSIM_MIXED = 0, TOKENSIM_PREFILL_FIRST = 1, TOKENSIM_CHUNKED = 2 };                    /* policy.iteration_mode */
 enum { TOKENSIM_LEN_SHAREGPT_SYNTH_V1 = 0, TOKENSIM_LEN_FIXED = 1, TOKENSIM_LEN_UNIFORM = 2,
        TOKENSIM_LEN_TABLE = 3, TOKENSIM_LEN_TRACE = 4 };                      /* len_dist      */
 enum { TOKENSIM_TRACE_NONE = 0, TOKENSIM_TRACE_BINNED = 1, TOKENSIM_TRACE_FULL = 2 };
@@ -113,7 +113,12 @@ typedef struct {
   uint32_t iteration_mode;    /* MIXED: prefills and decodes share an iteration (A3);
                                  PREFILL_FIRST: vLLM v0.6.2 default -- when fresh requests
                                  can be admitted the iteration runs only their prefills
-                                 (NEXT-3, reading R-N3); UNIFIED topology only  */
+                                 (NEXT-3, reading R-N3); CHUNKED: vLLM chunked prefill --
+                                 decodes, then the prefill in progress, resumes and fresh
+                                 requests share max_batched_tokens in that order, prompts
+                                 split into chunks (P, c0) (NEXT-3, reading R-N3b; needs
+                                 max_batched_tokens >= max_num_seqs instead of >=
+                                 max_model_len); UNIFIED topology only  */
 } tokensim_policy;
 
 /* Bucketed length table: bucket b covers [lo[b], hi[b]); cdf32 holds n_buckets-1 u32

@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "OK", -1: "E_INVALID", -2: "E_NOMEM", -3: "E_CUDA", -4: "E_ST
                 -6: "E_TRUNCATED", -7: "E_OVERFLOW"}
 STATIC, CONT, CONT_RATIO = 0, 1, 2
 SWAP, RECOMPUTE = 0, 1
-MIXED, PREFILL_FIRST = 0, 1
+MIXED, PREFILL_FIRST, CHUNKED = 0, 1, 2
 LEN_SHAREGPT_SYNTH_V1, LEN_FIXED, LEN_UNIFORM, LEN_TABLE, LEN_TRACE = 0, 1, 2, 3, 4
 TRACE_NONE, TRACE_BINNED, TRACE_FULL = 0, 1, 2
 UNIFIED, PD_PAIR = 0, 1

@@ -30,7 +30,7 @@ class TokensimError(RuntimeError):
 
 _KIND = {si.STATIC: T.STATIC, si.CONT: T.CONT, si.CONT_RATIO: T.CONT_RATIO}
 _PRE = {si.SWAP: T.SWAP, si.RECOMPUTE: T.RECOMPUTE}
-_MODE = {si.MIXED: T.MIXED, si.PREFILL_FIRST: T.PREFILL_FIRST}
+_MODE = {si.MIXED: T.MIXED, si.PREFILL_FIRST: T.PREFILL_FIRST, si.CHUNKED: T.CHUNKED}
 _LEN = {si.FIXED: T.LEN_FIXED, si.UNIFORM: T.LEN_UNIFORM, si.TABLE: T.LEN_TABLE, si.TRACE: T.LEN_TRACE,
         "sharegpt_synth_v1": T.LEN_SHAREGPT_SYNTH_V1}
 _TRC = {si.NONE_TRACE: T.TRACE_NONE, si.BINNED: T.TRACE_BINNED, si.FULL: T.TRACE_FULL}

@@ -272,7 +272,7 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
     const std::string pp = "policies[" + std::to_string(i) + "].";
     if (p.kind > TOKENSIM_CONT_RATIO) return bad(pp + "kind: unknown");
     if (p.preempt > TOKENSIM_RECOMPUTE) return bad(pp + "preempt: unknown");
-    if (p.iteration_mode > TOKENSIM_PREFILL_FIRST) return bad(pp + "iteration_mode: unknown");
+    if (p.iteration_mode > TOKENSIM_CHUNKED) return bad(pp + "iteration_mode: unknown");
     if (opt->topology == TOKENSIM_PD_PAIR && p.iteration_mode != TOKENSIM_MIXED)
       return bad(pp + "iteration_mode: PD_PAIR workers are prefill-only / decode-only already");
     if (opt->topology == TOKENSIM_PD_PAIR && p.kind == TOKENSIM_CONT_RATIO)
@@ -280,7 +280,13 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
     if (p.kind == TOKENSIM_CONT_RATIO && !(p.max_mem_ratio > 0 && p.max_mem_ratio <= 1))
       return bad(pp + "max_mem_ratio: must be in (0, 1]");
     if (p.max_num_seqs < 1 || p.max_num_seqs > 1024) return bad(pp + "max_num_seqs: must be in [1, 1024]");
-    if (p.max_batched_tokens < mml) return bad(pp + "max_batched_tokens: must be >= max_model_len");
+    if (p.iteration_mode == TOKENSIM_CHUNKED) {
+      // every running decode must fit the budget (reading R-N3b); prompts are chunked
+      if (p.max_batched_tokens < p.max_num_seqs)
+        return bad(pp + "max_batched_tokens: CHUNKED needs max_batched_tokens >= max_num_seqs");
+    } else if (p.max_batched_tokens < mml) {
+      return bad(pp + "max_batched_tokens: must be >= max_model_len");
+    }
     if (p.block_size < 1) return bad(pp + "block_size: must be >= 1");
     max_mns = std::max(max_mns, p.max_num_seqs);
     min_bs = std::min(min_bs, p.block_size);
@@ -309,9 +315,13 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
       const u128 Np = std::min<u128>(pol[i].max_batched_tokens, mns * mml);
       const u128 N = Np + mns, S = mns;
       const u128 Ap = mns * (u128)mml * (mml + 1) / 2, Cd = mns * (u128)(mml + 1);
+      // chunks (CHUNKED): A_p <= N_p * mml and K_p <= N_p + mns * mml
+      const bool chk = pol[i].iteration_mode == TOKENSIM_CHUNKED;
+      const u128 Apc = chk ? Np * (u128)mml : 0, Kpc = chk ? Np + mns * (u128)mml : Np;
+      const u128 Ab = Ap > Apc ? Ap : Apc, Kb = Kpc > Cd ? Kpc : Cd;
       const u128 cand[] = {2 * N * M.hq2g, M.s * (M.hq2g + N * M.h + N * M.q2g), 2 * N * M.hfu,
-                           M.s * (M.hfu + N * M.h + N * M.fu), 4 * (u128)M.q * Ap, 4 * (u128)M.q * Cd,
-                           M.s * (N * M.att_tok + M.g2 * (Np > Cd ? Np : Cd)), 2 * S * M.Vh,
+                           M.s * (M.hfu + N * M.h + N * M.fu), 4 * (u128)M.q * Ab, 4 * (u128)M.q * Cd,
+                           M.s * (N * M.att_tok + M.g2 * Kb), 2 * S * M.Vh,
                            M.s * (M.Vh + S * M.h + S * M.V)};
       for (u128 c : cand) worst = std::max(worst, c);
     }

@@ -64,10 +64,12 @@ __device__ __forceinline__ double roof(double F, double B, const CostK &K) {
   return fmax(__dmul_rn(F, K.invF), __dmul_rn(B, K.invB));
 }
 
-// T_ns of a batch from its exact aggregates (c0 = 0, so K_p = N_p); SURVEY c.5 order.
-__device__ __forceinline__ i64 iter_time_ns(const CostK &K, u64 Np, u64 Ap, u64 Sp, u64 D, u64 Cd,
-                                            u64 swap_bytes) {
-  const double N = __ull2double_rn(Np + D), S = __ull2double_rn(Sp + D);
+// T_ns of a batch from its exact aggregates; SURVEY c.5 order.  Np = sum of prefill lengths,
+// Ap = sum of P*c0 + P(P+1)/2, Kp = sum of c0 + P (keys a prefill reads), Slm = LM-head rows of
+// the prefill entries (a non-final chunk samples nothing, reading R-N3b).
+__device__ __forceinline__ i64 iter_time_chunk_ns(const CostK &K, u64 Np, u64 Ap, u64 Kp, u64 Slm, u64 D,
+                                                  u64 Cd, u64 swap_bytes) {
+  const double N = __ull2double_rn(Np + D), S = __ull2double_rn(Slm + D);
   double tQKV = 0.0, tATTP = 0.0, tATTD = 0.0, tO = 0.0, tUP = 0.0, tDOWN = 0.0, tLM = 0.0;
   const double N2 = __dmul_rn(2.0, N);
   if (Np + D > 0) {
@@ -80,13 +82,13 @@ __device__ __forceinline__ i64 iter_time_ns(const CostK &K, u64 Np, u64 Ap, u64 
   if (Np > 0) {
     const double Npd = __ull2double_rn(Np);
     tATTP = roof(__dmul_rn(K.q4, __ull2double_rn(Ap)),
-                 __dmul_rn(K.s, __dadd_rn(__dmul_rn(Npd, K.att_tok), __dmul_rn(K.g2, Npd))), K);
+                 __dmul_rn(K.s, __dadd_rn(__dmul_rn(Npd, K.att_tok), __dmul_rn(K.g2, __ull2double_rn(Kp)))), K);
   }
   if (D > 0) {
     const double Dd = __ull2double_rn(D), Cdd = __ull2double_rn(Cd);
     tATTD = roof(__dmul_rn(K.q4, Cdd), __dmul_rn(K.s, __dadd_rn(__dmul_rn(Dd, K.att_tok), __dmul_rn(K.g2, Cdd))), K);
   }
-  if (Sp + D > 0)
+  if (Slm + D > 0)
     tLM = roof(__dmul_rn(__dmul_rn(2.0, S), K.Vh),
                __dmul_rn(K.s, __dadd_rn(__dadd_rn(K.Vh, __dmul_rn(S, K.h)), __dmul_rn(S, K.V))), K);
   const double tl =
@@ -97,6 +99,11 @@ __device__ __forceinline__ i64 iter_time_ns(const CostK &K, u64 Np, u64 Ap, u64 
   if (swap_bytes > 0) T = __dadd_rn(T, __dmul_rn(__ull2double_rn(swap_bytes), K.invH));
   T = __dadd_rn(T, K.overhead);
   return (i64)floor(__dadd_rn(__dmul_rn(T, 1e9), 0.5));
+}
+// whole prefills (c0 = 0, so K_p = N_p, every entry emits)
+__device__ __forceinline__ i64 iter_time_ns(const CostK &K, u64 Np, u64 Ap, u64 Sp, u64 D, u64 Cd,
+                                            u64 swap_bytes) {
+  return iter_time_chunk_ns(K, Np, Ap, Np, Sp, D, Cd, swap_bytes);
 }
 
 // ------------------------------------------------------------------ per-warp shared memory
@@ -142,6 +149,10 @@ __device__ __forceinline__ WarpSmem carve(unsigned char *base, u32 cap) {
 }
 
 #define PT_POS(pt) ((pt)&1023u)
+// info word of a slot: block-table slot (bits 0-9) | CHUNKED flags (bits 14-15) | n_preempt << 16
+#define SLOT(info) ((info)&1023u)
+constexpr u32 INFO_NT = 1u << 14;   // CHUNKED: no token emitted yet (the next prefill completion is the first token)
+constexpr u32 INFO_PFB = 1u << 15;  // CHUNKED: a resumed re-prefill in this iteration's batch
 #define PT_J(pt) (((pt) >> 10) & 31u)
 #define PT_TPOS(pt) ((pt) >> 15)
 
@@ -250,7 +261,7 @@ __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl,
         const u32 pt = S.req_pt[a];
         const u32 pos = PT_POS(pt);
         const u32 tpos = PT_TPOS(pt) + (o - start);
-        const u32 slot = S.info[pos] & 0xffffu;
+        const u32 slot = SLOT(S.info[pos]);
         bt[(size_t)slot * btl + tpos] = blk;
         ev_put(L, idx - r0, k + PT_J(pt), 1 + kind_off, S.id[pos], blk);
       }
@@ -410,6 +421,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const bool RATIO = PL.kind == TOKENSIM_CONT_RATIO;
   const bool STATICP = PL.kind == TOKENSIM_STATIC;
   const bool PFM = PL.mode == TOKENSIM_PREFILL_FIRST;
+  const bool CHK = PL.mode == TOKENSIM_CHUNKED;
   const u64 total = HP.total_blocks;
   const u32 nwords = HP.nwords;
   const u32 btl = P.bt_len;
@@ -436,6 +448,10 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   u64 nfree = total;
   u32 hint = 0;
   u32 rmin = 0;  // min rem over R after the last commit (0 when unknown / R empty)
+  // CHUNKED (NEXT-3b): the budget runs out at the last prefill entry of an iteration, so at most
+  // one prefill is in progress and it is the last entry of R (reading R-N3b): xdone of xtgt done
+  bool hx = false;
+  u32 xdone = 0, xtgt = 0;
   u64 ff_mem_wait = 0, ff_mem_k = 0;  // after a memory-cut failure: skip attempts while nfree <= wait, k < k
   const u32 gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   Logs L;
@@ -534,7 +550,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     // ---------------------------------------------------------------- fast-forward (H3)
     clk_a = clock64();
     clk_p = clk_a;
-    if (ff_on && nR > 0 && rmin >= 2 && (nfree > ff_mem_wait || k >= ff_mem_k)) {
+    if (ff_on && nR > 0 && rmin >= 2 && !hx && (nfree > ff_mem_wait || k >= ff_mem_k)) {
       // The stretch must admit nothing and resume nothing.  With Q != {} fresh admission is
       // off (c.4 step 5) and a Q head that cannot resume now cannot resume later (R frozen,
       // free count only falls).  With Q = {}: STATIC never admits while R != {}; an empty fresh
@@ -546,15 +562,16 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       if (nQ > 0) {
         const u32 x = nR;  // Q head position
         u32 tokq;
-        if (SWAPM) {
-          const u32 c = S.ctx[x];
-          need_h = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
+        const u32 cq = S.ctx[x];
+        if (SWAPM && !(CHK && cq == 0)) {
+          need_h = B.cdiv(cq) + (B.mod(cq) == 0 ? 1u : 0u);
           tokq = 1;
         } else {
           const u32 id = S.id[x];
           tokq = PR[id] + (OU[id] - S.rem[x]);
           need_h = B.cdiv(tokq);
         }
+        if (CHK) tokq = 1;  // one token of budget admits a chunk
         if (!((u64)nR + 1 > mns || (u64)nR + tokq > mbt)) {
           mem_check = true;
           // resume is certain even if every running request takes a block now: don't try
@@ -571,7 +588,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         // prefill-first admits before any decode block: no decode tokens, no decode blocks
         const u64 dtok = PFM ? 0u : nR;
         if ((u64)need_h > HP.cap_fresh) quiet = false;  // would be rejected at this boundary
-        else if (!((u64)nR + 1 > mns || dtok + hd_p > mbt)) {
+        else if (!((u64)nR + 1 > mns || dtok + (CHK ? 1u : hd_p) > mbt)) {
           mem_check = true;
           ratio_h = RATIO;
           // admission is certain even if every running request takes a block now: don't try
@@ -679,7 +696,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
                 const u32 pos = select_bit(mask, o - excl);
                 const u32 blk = (hint + lo) * 32 + select_bit(wv, o - bv);
                 const u32 tpos = B.div(S.ctx[pos] + jb);
-                bt[(size_t)(S.info[pos] & 0xffffu) * btl + tpos] = blk;
+                bt[(size_t)(SLOT(S.info[pos])) * btl + tpos] = blk;
                 ev_put(L, o, k + jb, 1, S.id[pos], blk);
               }
               L.nev += Ktot;
@@ -767,7 +784,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               fm &= fm - 1;
               const u32 pos = b0 + l;
               const u32 held = B.cdiv(S.ctx[pos]);
-              const u32 slot = S.info[pos] & 0xffffu;
+              const u32 slot = SLOT(S.info[pos]);
               free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, 0, L, hint);
               nfree += held;
               if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
@@ -880,6 +897,21 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     // ---------------------------------------------------------------- 3. decode reservation
     u32 E = 0, Kb = 0, m = 0, nres = 0, nadm = 0, nrej = 0;
     u64 cdp = 0, npp = 0, app = 0, swap_out = 0, swap_in = 0, tokens = 0;
+    // CHUNKED: keys read by prefills, LM-head rows, the entry left partial this iteration
+    u64 kpp = 0;
+    u32 semit = 0, nres_sw = 0;
+    bool hnew = false;
+    u32 xnew_pos = 0, xnew_done = 0, xnew_tgt = 0;
+    auto note_partial = [&](bool part, u32 pos, u32 ch, u32 tgt) {
+      const u32 pm = __ballot_sync(FULLMASK, part);
+      if (pm) {
+        const int src = __ffs(pm) - 1;
+        hnew = true;
+        xnew_pos = __shfl_sync(FULLMASK, pos, src);
+        xnew_done = __shfl_sync(FULLMASK, ch, src);
+        xnew_tgt = __shfl_sync(FULLMASK, tgt, src);
+      }
+    };
     // 5. fresh FCFS admission (its own pass in prefill-first mode, NEXT-3)
     auto fresh_admit = [&]() {
       bool head_blocked = false;
@@ -890,7 +922,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 ph = (adm >= win && off < 32) ? pw : PR[adm];
         const u32 nh = B.cdiv(ph);
         head_blocked = (u64)nh <= HP.cap_fresh &&
-                       ((u64)nR + 1 > mns || tokens + ph > (u64)mbt || (i64)nfree - (i64)nh < wm ||
+                       ((u64)nR + 1 > mns || tokens + (CHK ? 1u : ph) > (u64)mbt || (i64)nfree - (i64)nh < wm ||
                         (RATIO && (total - nfree) + nh > HP.ratio_limit));
       }
       if (!head_blocked) {
@@ -917,7 +949,9 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const u32 ce = scan_incl(el ? 1u : 0u);
           const u32 cneed = scan_incl(el ? need : 0u);
           const u32 cp = scan_incl(el ? p : 0u);
-          const bool ok = el && ((u64)nR + ce <= (u64)mns) && (tokens + cp <= (u64)mbt) &&
+          // CHUNKED: a request is admitted while one token of budget is left (reading R-N3b)
+          const bool tok_ok = CHK ? tokens + cp - p < (u64)mbt : tokens + cp <= (u64)mbt;
+          const bool ok = el && ((u64)nR + ce <= (u64)mns) && tok_ok &&
                           ((i64)nfree - (i64)cneed >= wm) && (!RATIO || (total - nfree) + cneed <= HP.ratio_limit);
           const u32 failm = __ballot_sync(FULLMASK, el && !ok);
           const u32 nvalid = min(32u, arr - adm);
@@ -929,21 +963,26 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           if (cnt) {
             const u32 rank = __popc(takem & ltm);
             const u32 slot = alloc_btslots(S.btfree, CAP / 32, take, rank, cnt);
+            u32 ch = p;
+            if (CHK && take) ch = (u32)min((u64)p, (u64)mbt - (tokens + cp - p));
             if (take) {
               const u32 pos = nR + rank;
               S.id[pos] = i;
               S.ctx[pos] = p;  // fresh prefill of P = p; ctx after commit
               S.rem[pos] = o;
-              S.info[pos] = slot;
+              S.info[pos] = CHK ? (slot | INFO_NT) : slot;
               S.last[pos] = 0;
               S.maxgap[pos] = 0;
               S.arr[pos] = a;
               S.ttft[pos] = 0;
               S.req_cum[E + rank] = Kb + cneed;
               S.req_pt[E + rank] = pos;
-              npp += p;
-              app += (u64)p * (p + 1) / 2;
+              npp += ch;
+              app += (u64)ch * (ch + 1) / 2;
+              kpp += ch;
+              semit += ch == p ? 1u : 0u;
             }
+            if (CHK) note_partial(take && ch < p, nR + rank, ch, p);
           }
           if (rj) reinterpret_cast<uint8_t *>(rec + i)[26] = (uint8_t)TOKENSIM_REQ_REJECTED;
           const u32 nrj = __popc(__ballot_sync(FULLMASK, rj));
@@ -952,7 +991,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             const u32 sp = __shfl_sync(FULLMASK, cp, stop - 1);
             nfree -= sneed;
             Kb += sneed;
-            tokens += sp;
+            tokens = CHK ? min(tokens + sp, (u64)mbt) : tokens + sp;
           }
           E += cnt;
           nR += cnt;
@@ -971,13 +1010,16 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       pf_only = nadm > 0;
     }
     u32 nR3 = nR_old;  // fresh prefills of a prefill-first iteration start at nR_old
+    u32 chx = 0;        // CHUNKED: chunk of the prefill in progress (0: it sits this one out)
+    bool xpart = false;  // ... and it stays partial
     if (!pf_only) {
     // one pass: needing survivors -> requester list (ascending id), sum of c = ctx+1
     for (u32 b0 = 0; b0 < nR; b0 += 32) {
       const u32 jj = b0 + lane;
-      const u32 c = jj < nR ? S.ctx[jj] : 1u;
-      const bool need = jj < nR && B.mod(c) == 0;
-      if (jj < nR) cdp += c + 1;
+      const bool dec = jj < nR && !(hx && jj == nR - 1);  // the prefill in progress decodes nothing
+      const u32 c = dec ? S.ctx[jj] : 1u;
+      const bool need = dec && B.mod(c) == 0;
+      if (dec) cdp += c + 1;
       const u32 bal = __ballot_sync(FULLMASK, need);
       if (need) {
         const u32 e = E + __popc(bal & ltm);
@@ -991,25 +1033,28 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       u64 Sn = E, Hh = 0;
       do {
         ++m;
-        const u32 c = S.ctx[nR - m];
-        Sn -= (B.mod(c) == 0) ? 1 : 0;
+        const u32 c = S.ctx[nR - m];  // ctx = target of a prefill in progress: its held blocks
+        Sn -= (B.mod(c) == 0 && !(hx && m == 1)) ? 1 : 0;
         Hh += B.cdiv(c);
       } while (Sn > nfree + Hh);
       u64 csub = 0;
       for (u32 v = nR - m; v < nR; ++v) {  // victims: latest arrivals (reading A7)
         const u32 c = S.ctx[v];
         const u32 held = B.cdiv(c);
-        const u32 slot = S.info[v] & 0xffffu;
+        const u32 slot = SLOT(S.info[v]);
+        // a partial prefill loses its KV whatever the mode: re-prefill from scratch (R-N3b)
+        const bool vx = hx && v == nR - 1;
         free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, 0, L, hint);
         nfree += held;
-        csub += c + 1;
-        if (SWAPM) swap_out += (u64)held * HP.block_bytes;
+        if (!vx) csub += c + 1;
+        if (SWAPM && !vx) swap_out += (u64)held * HP.block_bytes;
         __syncwarp();
         if (lane == 0) {
           S.info[v] += 1u << 16;
-          if (!SWAPM) S.ctx[v] = 0;
+          if (!SWAPM || vx) S.ctx[v] = 0;
         }
       }
+      hx = false;  // a prefill in progress is the tail of R: always the first victim
       __syncwarp();
       if (lane == 0) cdp -= csub;
       E = (u32)Sn;  // the requester list is in position order: victims are its tail
@@ -1020,7 +1065,19 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     nR3 = nR;
     Kb = E;
     nfree -= E;
-    tokens = nR;
+    tokens = nR - (hx ? 1u : 0u);
+    if (CHK && hx) {  // the prefill in progress takes the budget the decodes leave (R-N3b)
+      const u32 rest = xtgt - xdone;
+      chx = (u32)min((u64)rest, (u64)mbt - tokens);
+      xpart = chx < rest;
+      if (lane == 0 && chx) {
+        npp += chx;
+        app += (u64)chx * xdone + (u64)chx * (chx + 1) / 2;
+        kpp += (u64)xdone + chx;
+        semit += xpart ? 0u : 1u;
+      }
+      tokens += chx;
+    }
     if (m == 0) {
       NPH(0);
       // 4. resume, head first, stop at the first misfit
@@ -1030,9 +1087,10 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const u32 jj = nR3 + b0 + lane;
           const bool valid = b0 + lane < nQ;
           u32 need = 0, tok = 0, held0 = 0, c = 0;
+          bool isrc = false;  // re-prefill p + gen (RECOMPUTE; CHUNKED: a lost partial prefill)
           if (valid) {
-            if (SWAPM) {
-              c = S.ctx[jj];
+            c = S.ctx[jj];
+            if (SWAPM && !(CHK && c == 0)) {
               need = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
               tok = 1;
               held0 = B.cdiv(c);
@@ -1041,23 +1099,38 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               const u32 Pq = PR[id] + (OU[id] - S.rem[jj]);  // p + gen
               need = B.cdiv(Pq);
               tok = Pq;
+              isrc = true;
             }
           }
           const u32 cn = scan_incl(need), ct = scan_incl(tok);
-          const bool ok = valid && ((u64)nR3 + b0 + lane + 1 <= (u64)mns) &&
-                          (tokens + cum_tok + ct <= (u64)mbt) && ((i64)nfree - (i64)(cum_need + cn) >= wm);
+          const bool tok_ok = CHK ? tokens + cum_tok + ct - tok < (u64)mbt : tokens + cum_tok + ct <= (u64)mbt;
+          const bool ok = valid && ((u64)nR3 + b0 + lane + 1 <= (u64)mns) && tok_ok &&
+                          ((i64)nfree - (i64)(cum_need + cn) >= wm);
           const u32 okm = __ballot_sync(FULLMASK, ok);
           const u32 cnt = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+          u32 ch = tok;
           if (lane < cnt) {
             S.req_cum[E + lane] = Kb + cn;
             S.req_pt[E + lane] = jj;
-            if (SWAPM) {
+            if (!isrc) {
               cdp += c + 1;
             } else {
+              if (CHK) {
+                ch = (u32)min((u64)tok, (u64)mbt - (tokens + cum_tok + ct - tok));
+                S.info[jj] |= INFO_PFB;
+              }
               S.ctx[jj] = tok;  // recompute prefill of P = p + gen; ctx after commit
-              npp += tok;
-              app += (u64)tok * (tok + 1) / 2;
+              npp += ch;
+              app += (u64)ch * (ch + 1) / 2;
+              kpp += ch;
+              semit += ch == tok ? 1u : 0u;
             }
+          }
+          if (CHK) {
+            note_partial(lane < cnt && isrc && ch < tok, jj, ch, tok);
+            nres_sw += __popc(__ballot_sync(FULLMASK, lane < cnt && !isrc));
+          } else if (SWAPM) {
+            nres_sw += cnt;
           }
           const u64 sw = warp_sum64(lane < cnt ? (u64)held0 : 0ull);
           if (cnt) {
@@ -1072,7 +1145,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           if (cnt < 32) break;
         }
         nfree -= cum_need;
-        tokens += cum_tok;
+        tokens = CHK ? min(tokens + cum_tok, (u64)mbt) : tokens + cum_tok;
         nR += nres;
         nQ -= nres;
         __syncwarp();
@@ -1093,26 +1166,66 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     NPH(3);
     // 7. cost: decodes are positions [0, D), prefills [D, nR); a prefill-first iteration runs
     // only the fresh prefills at [nR_old, nR)
-    const u32 D = pf_only ? 0u : nR3 + (SWAPM ? nres : 0u);
-    const u32 Sp = pf_only ? nR - nR_old : nR - D;
+    // CHUNKED: the prefill in progress (position nR3 - 1 when hx) is not a decode; with chx = 0
+    // it is not in the batch at all
+    const bool xout = hx && chx == 0;
+    const u32 D = pf_only ? 0u : nR3 - (hx ? 1u : 0u) + nres_sw;
+    const u32 Sp = pf_only ? nR - nR_old : nR - D - (xout ? 1u : 0u);
     const u32 c0 = pf_only ? nR_old : 0u;
     const u64 Cd = warp_sum64(cdp);
-    u64 Np = 0, Ap = 0;
+    u64 Np = 0, Ap = 0, Kp = 0, Slm = Sp;
     if (Sp) {
       Np = warp_sum64(npp);
       Ap = warp_sum64(app);
+      Kp = Np;
+      if (CHK) {
+        Kp = warp_sum64(kpp);
+        Slm = __reduce_add_sync(FULLMASK, semit);
+      }
     }
-    const i64 T = iter_time_ns(K, Np, Ap, Sp, D, Cd, swap_out + swap_in);
+    const i64 T = iter_time_chunk_ns(K, Np, Ap, Kp, Slm, D, Cd, swap_out + swap_in);
     NPH(4);
     // 8. commit
     const i64 ts = t, te = t + T;
     const u64 blocks = total - nfree;
     u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
     const u32 fresh0 = nR3 + nres;
+    // CHUNKED: position of the entry whose prefill stays partial (no token this iteration)
+    const u32 ppos = (hx && xpart) ? nR3 - 1 : (hnew ? xnew_pos : 0xffffffffu);
     for (u32 b0 = c0; b0 < nR; b0 += 32) {
       const u32 jj = b0 + lane;
       bool fin = false;
-      if (jj < nR) {
+      if (CHK) {
+        if (jj < nR) {
+          const u32 inf = S.info[jj];
+          const bool isx = hx && jj == nR3 - 1;
+          const bool emit = jj != ppos && !(isx && chx == 0);
+          const bool dec = (jj < nR3 && !isx) || (jj >= nR3 && jj < fresh0 && !(inf & INFO_PFB));
+          u32 r = S.rem[jj];
+          if (emit) {
+            r -= 1;
+            S.rem[jj] = r;
+            if (dec) S.ctx[jj] += 1;
+            if (inf & INFO_NT) {  // the first token
+              S.ttft[jj] = te - S.arr[jj];
+            } else {
+              const i64 gap = te - S.last[jj];
+              if (gap > S.maxgap[jj]) S.maxgap[jj] = gap;
+            }
+            S.last[jj] = te;
+            if (inf & (INFO_NT | INFO_PFB)) S.info[jj] = inf & ~(INFO_NT | INFO_PFB);
+          } else if (inf & INFO_PFB) {
+            S.info[jj] = inf & ~INFO_PFB;
+          }
+          fin = emit && r == 0;
+          if (fin) {
+            write_record(rec + S.id[jj], S.ttft[jj], te - S.arr[jj], S.maxgap[jj], S.info[jj] >> 16,
+                         TOKENSIM_REQ_FINISHED, (u32)k);
+          } else {
+            rmin_l = min(rmin_l, r);
+          }
+        }
+      } else if (jj < nR) {
         const u32 r = S.rem[jj] - 1;
         S.rem[jj] = r;
         if (jj >= fresh0) {
@@ -1144,7 +1257,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 pos = b0 + l;
         const u32 c = S.ctx[pos];
         const u32 held = B.cdiv(c);
-        const u32 slot = S.info[pos] & 0xffffu;
+        const u32 slot = SLOT(S.info[pos]);
         free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, 0, L, hint);
         nfree += held;
         if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
@@ -1156,7 +1269,18 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       rmin = pf_only ? min(rmin, rn) : rn;  // paused requests keep their rem
     }
     __syncwarp();
-    req_iters += nR - c0;
+    req_iters += nR - c0 - (xout ? 1u : 0u);
+    if (CHK) {  // the prefill in progress after this iteration (R-N3b)
+      if (hx && !xout) {
+        if (xpart) xdone += chx;
+        else hx = false;
+      }
+      if (hnew) {
+        hx = true;
+        xdone = xnew_done;
+        xtgt = xnew_tgt;
+      }
+    }
     NPH(6);
     if (nfin) {
       // stable compaction of R u Q, dropping finished entries (rem == 0 within R)

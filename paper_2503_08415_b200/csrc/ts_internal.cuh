@@ -42,7 +42,7 @@ struct DevHP {
 struct DevPol {
   u32 kind, preempt, mns, mbt, bs, wm;
   u32 bs_sh;  // log2(bs) if bs is a power of two, else 0xffffffff
-  u32 mode;   // TOKENSIM_MIXED | TOKENSIM_PREFILL_FIRST
+  u32 mode;   // TOKENSIM_MIXED | TOKENSIM_PREFILL_FIRST | TOKENSIM_CHUNKED
 };
 
 // Per point, written once by the simulation kernel.

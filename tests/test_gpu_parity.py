@@ -302,3 +302,28 @@ def test_large_point_summary_scratch_path(api):
     for p in range(cfg.num_points):
         q = sw.latency_quantiles(p, "e2e", [1234, 5000, 9999])
         assert (np.diff(q) >= 0).all()
+
+
+def test_chunked_prefill_parity(api):
+    """NEXT-3b chunked prefill (reading R-N3b): random micro configs under small token budgets
+    (prompts longer than the budget, preemption of partial prefills), FF on/off identical, and
+    the C2 grid + a memory-pressure grid under vLLM's chunked default budget of 512."""
+    rng = np.random.default_rng(29)
+    for _ in range(60):
+        c = _micro(rng)
+        pol = c.policies[0]
+        budget = int(rng.choice([max(pol.max_num_seqs, 16), max(pol.max_num_seqs, 40), 300]))
+        c = replace(c, policies=[replace(pol, iteration_mode=si.CHUNKED, max_batched_tokens=budget)])
+        sw = run_gpu(api, c)
+        check_points(sw, c, [0], records=True, trace=True, iters=True)
+    pols = [si.Policy(kind=k, preempt=pm, iteration_mode=si.CHUNKED, max_batched_tokens=512)
+            for k in (si.CONT, si.STATIC) for pm in (si.SWAP, si.RECOMPUTE)]
+    for cfg in (replace(si.c2(), policies=[si.Policy(iteration_mode=si.CHUNKED, max_batched_tokens=512)]),
+                si.SweepConfig("pressure", si.LLAMA2_13B, [si.Hw(mem_capacity=30 * 10 ** 9), si.A100], pols,
+                               si.Workload(300, [4.0, 16.0], [0, 1]))):
+        sw = run_gpu(api, cfg)
+        check_points(sw, cfg, list(range(cfg.num_points)), records=True, trace=True)
+        off = run_gpu(api, replace(cfg, options=replace(cfg.options, fast_forward=False)))
+        assert sw.summaries().tobytes() == off.summaries().tobytes()
+        if cfg.name == "pressure":
+            assert sw.summaries()["n_preemptions"].sum() > 0
