@@ -323,7 +323,7 @@ struct oracle_run {
   oracle_summary summary;
   std::vector<oracle_record> records;
   std::vector<oracle_iter> iters;
-  std::vector<oracle_sample> trace[2];
+  std::vector<oracle_sample> trace[OR_MAX_WORKERS];
   std::vector<oracle_event> events;
 };
 
@@ -1251,6 +1251,539 @@ oracle_run *simulate_pd(const oracle_cfg &c) {
   return run;
 }
 
+// ----------------------------------------------------------------- NEXT-1 xP:yD node
+// SURVEY §8(f) NEXT-1 and readings R-X1..R-X6 in DESIGN.md.  x prefill workers P_0..P_{x-1} (the
+// prefill profile) and y decode workers D_0..D_{y-1} (the decode profile) run the a.9 worker
+// loops; a global scheduler dispatches every arrival to a prefill
+// worker and, at the end-of-prefill breakpoint, every request to a decode worker.  Dispatch
+// events at time t are handled before worker boundaries at t (reading A2), in request-id order;
+// boundaries at equal times go decode workers first, then prefill workers, lower index first.
+// Each decode worker has its own FIFO ingress link.  With x = y = 1 this is exactly simulate_pd.
+oracle_run *simulate_pdn(const oracle_cfg &c) {
+  const u32 X = c.n_prefill ? c.n_prefill : 1, Y = c.n_decode ? c.n_decode : 1;
+  if (c.kind == OR_CONT_RATIO || c.iter_mode != OR_MIXED) {
+    g_err = "PD_PAIR supports STATIC and CONT policies in MIXED mode only";
+    return nullptr;
+  }
+  if (X + Y > OR_MAX_WORKERS || c.dispatch > OR_DISPATCH_LEAST_MEMORY) {
+    g_err = "PD node: need x + y <= 8 workers and a known dispatch policy";
+    return nullptr;
+  }
+  oracle_derived dP, dD;
+  if (!derive(c, 0, dP) || !derive(c, 1, dD)) return nullptr;
+  const CostK_ KP = {cost_ctx(c, dP, 0)}, KD = {cost_ctx(c, dD, 1)};
+  std::vector<i64> A;
+  std::vector<u32> Pl, Ol;
+  if (!workload(c, A, Pl, Ol)) return nullptr;
+  const u32 n = c.num_requests;
+  const u64 bs = c.block_size, totP = dP.total_blocks, totD = dD.total_blocks;
+  const bool SWAPM = c.preempt == OR_SWAP;
+  const i64 INF = INT64_MAX;
+  const double inv_link = 1.0 / c.pd_link_bw;
+
+  struct NReq {
+    i64 a = 0;
+    u32 p = 0, o = 0, status = 0;
+    u64 ctx = 0, gen = 0;
+    i64 first_tok = 0, last_tok = 0, max_gap = 0, finish = 0, join = 0, xend = 0;
+    u32 n_preempt = 0, pw = 0, dw = 0;
+    bool xstarted = false;
+    std::vector<u32> pblocks, dblocks;
+    u64 finish_k = 0;
+  };
+  struct PW {  // a prefill worker
+    std::set<u32> free;
+    std::deque<u32> queue;      // dispatched, not yet admitted (dispatch order)
+    std::vector<u32> batch;     // the running prefill batch, dispatched onward at tdisp
+    std::set<u32> holders;      // finished prefill, P blocks held until the transfer ends
+    i64 t = 0, tdisp = INT64_MAX, last = 0;
+    u64 k = 0;
+    bool idle = false;
+  };
+  struct DW {  // a decode worker
+    std::set<u32> free;
+    std::deque<u32> pending;    // dispatched, not yet pulled (dispatch order)
+    std::set<u32> xfer, R, Q;
+    i64 t = 0, link_busy = 0, last = 0;
+    u64 k = 0, peak = 0, bns = 0;
+    bool idle = false;
+  };
+  std::vector<NReq> req(n);
+  for (u32 i = 0; i < n; ++i) {
+    req[i].a = A[i];
+    req[i].p = Pl[i];
+    req[i].o = Ol[i];
+  }
+  std::vector<PW> Pw(X);
+  std::vector<DW> Dw(Y);
+  for (PW &w : Pw)
+    for (u64 b = 0; b < totP; ++b) w.free.insert((u32)b);
+  for (DW &w : Dw)
+    for (u64 b = 0; b < totD; ++b) w.free.insert((u32)b);
+  oracle_run *run = new oracle_run();
+  std::memset(&run->summary, 0, sizeof(run->summary));
+  oracle_summary &S = run->summary;
+  u32 arr = 0, n_done = 0;
+  u64 rrP = 0, rrD = 0;
+  u64 sched_d = 0, block_d = 0, req_d = 0, req_iters = 0, npre = 0, swo = 0, swi = 0, nrej_tot = 0;
+  u64 n_xfer = 0, xfer_bytes = 0;
+
+  auto ev = [&](u64 k, u32 kind, u32 worker, u32 id, u32 b) {
+    block_d += fold({k, kind + 2 * worker, id, b});
+    if (c.keep_events) run->events.push_back({k, kind, id, b, worker});
+  };
+  auto finish_req = [&](u32 id, i64 te, u64 k) {
+    NReq &x = req[id];
+    x.status = 1;
+    x.finish = te;
+    x.finish_k = k;
+    req_d += fold({id, (u64)(x.first_tok - x.a), (u64)(x.finish - x.a), (u64)x.max_gap, x.n_preempt, k});
+    ++n_done;
+  };
+  // the global scheduler (reading R-X2): round robin in dispatch order, or the argmin of the
+  // outstanding requests / allocated blocks as of each worker's last processed boundary; ties go
+  // to the lowest worker index
+  auto pick = [&](bool toD) -> u32 {
+    const u32 cnt = toD ? Y : X;
+    if (c.dispatch == OR_DISPATCH_RR) return (u32)((toD ? rrD++ : rrP++) % cnt);
+    u32 best = 0;
+    u64 bestv = UINT64_MAX;
+    for (u32 w = 0; w < cnt; ++w) {
+      u64 v;
+      if (c.dispatch == OR_DISPATCH_LEAST_OUTSTANDING) {
+        v = toD ? Dw[w].pending.size() + Dw[w].xfer.size() + Dw[w].R.size() + Dw[w].Q.size()
+                : Pw[w].queue.size() + Pw[w].batch.size();
+      } else {
+        v = toD ? totD - Dw[w].free.size() : totP - Pw[w].free.size();
+      }
+      if (v < bestv) {
+        bestv = v;
+        best = w;
+      }
+    }
+    return best;
+  };
+
+  while (true) {
+    if (n_done == n) break;
+    i64 td = arr < n ? req[arr].a : INF;  // next dispatch event
+    for (const PW &w : Pw)
+      if (!w.batch.empty()) td = std::min(td, w.tdisp);
+    i64 tb = INF;  // next worker boundary
+    for (const PW &w : Pw) tb = std::min(tb, w.t);
+    for (const DW &w : Dw) tb = std::min(tb, w.t);
+    const i64 tnext = std::min(td, tb);
+    if (tnext == INF) {
+      g_err = "P/D deadlock: every worker waits";
+      delete run;
+      return nullptr;
+    }
+    if (c.horizon_ns >= 0 && tnext >= c.horizon_ns) {
+      S.status_flags |= 4;
+      break;
+    }
+    if (td <= tb) {
+      // ============================================================ dispatch events at td
+      std::vector<u32> ids;
+      std::vector<char> done_prefill;
+      for (PW &w : Pw) {
+        if (w.batch.empty() || w.tdisp != td) continue;
+        ids.insert(ids.end(), w.batch.begin(), w.batch.end());
+        w.batch.clear();
+        w.tdisp = INF;
+      }
+      std::sort(ids.begin(), ids.end());
+      const size_t n_comp = ids.size();
+      while (arr < n && req[arr].a == td) ids.push_back(arr++);  // arrivals: larger ids
+      for (size_t q = 0; q < ids.size(); ++q) {
+        const u32 id = ids[q];
+        NReq &x = req[id];
+        if (q < n_comp) {  // end-of-prefill breakpoint: to a decode worker (o = 1 finished on P)
+          if (x.status == 1) continue;
+          const u32 j = pick(true);
+          x.dw = j;
+          x.join = td;
+          Dw[j].pending.push_back(id);
+          if (Dw[j].idle && td < Dw[j].t) Dw[j].t = td;
+        } else {  // arrival: to a prefill worker
+          const u32 i = pick(false);
+          x.pw = i;
+          Pw[i].queue.push_back(id);
+          if (Pw[i].idle && td < Pw[i].t) Pw[i].t = td;
+        }
+      }
+      continue;
+    }
+    // the worker to advance: earliest boundary, decode workers first, lower index first
+    int wsel = -1;
+    for (u32 j = 0; j < Y && wsel < 0; ++j)
+      if (Dw[j].t == tb) wsel = (int)(X + j);
+    for (u32 i = 0; i < X && wsel < 0; ++i)
+      if (Pw[i].t == tb) wsel = (int)i;
+    if (wsel >= (int)X) {
+      // ================================================================ D_j boundary
+      const u32 j = (u32)wsel - X;
+      DW &w = Dw[j];
+      const u32 wid = (u32)wsel;
+      const i64 t = w.t;
+      std::vector<u32> xv(w.xfer.begin(), w.xfer.end());
+      for (u32 id : xv) {
+        if (req[id].xend <= t) {
+          w.xfer.erase(id);
+          w.R.insert(id);
+        }
+      }
+      std::map<u32, Kind> kind;
+      const u64 F = w.free.size();
+      std::vector<u32> Rv(w.R.begin(), w.R.end());
+      auto need_of = [&](u32 id) -> u64 { return (req[id].ctx % bs == 0) ? 1 : 0; };
+      u64 sum_need = 0;
+      for (u32 id : Rv) sum_need += need_of(id);
+      u64 m = 0, swap_out = 0;
+      if (sum_need > F) {
+        const u64 nr = Rv.size();
+        for (m = 1; m <= nr; ++m) {
+          u64 lhs = 0, rhs = F;
+          for (u64 q = 0; q < nr - m; ++q) lhs += need_of(Rv[q]);
+          for (u64 q = nr - m; q < nr; ++q) rhs += req[Rv[q]].dblocks.size();
+          if (lhs <= rhs) break;
+        }
+        if (m > nr) {
+          g_err = "P/D: no victim count satisfies c.4 step 3";
+          delete run;
+          return nullptr;
+        }
+        for (u64 q = 0; q < m; ++q) {
+          const u32 id = Rv[nr - 1 - q];
+          NReq &x = req[id];
+          const u64 held = x.dblocks.size();
+          for (u32 b : x.dblocks) {
+            w.free.insert(b);
+            ev(w.k, 2, wid, id, b);
+          }
+          x.dblocks.clear();
+          x.n_preempt += 1;
+          if (SWAPM) swap_out += held * dD.block_bytes;
+          else x.ctx = 0;
+          w.R.erase(id);
+          w.Q.insert(id);
+        }
+        npre += m;
+      }
+      for (u32 id : w.R) {
+        kind[id] = K_DEC;
+        if (need_of(id)) {
+          const u32 b = *w.free.begin();
+          w.free.erase(w.free.begin());
+          req[id].dblocks.push_back(b);
+          ev(w.k, 1, wid, id, b);
+        }
+      }
+      u64 n_res = 0, n_adm = 0, swap_in = 0, tokens = w.R.size();
+      if (m == 0) {
+        std::vector<u32> Qv(w.Q.begin(), w.Q.end());
+        for (u32 id : Qv) {
+          NReq &x = req[id];
+          u64 need, tok;
+          if (SWAPM) {
+            need = ceil_div(x.ctx, bs) + ((x.ctx % bs == 0) ? 1 : 0);
+            tok = 1;
+          } else {
+            need = ceil_div(x.p + x.gen, bs);
+            tok = x.p + x.gen;
+          }
+          const bool ok = (w.R.size() + w.xfer.size() + 1 <= c.max_num_seqs) &&
+                          (tokens + tok <= c.max_batched_tokens) &&
+                          ((i64)w.free.size() - (i64)need >= (i64)c.watermark_blocks);
+          if (!ok) break;
+          for (u64 q = 0; q < need; ++q) {
+            const u32 b = *w.free.begin();
+            w.free.erase(w.free.begin());
+            x.dblocks.push_back(b);
+            ev(w.k, 1, wid, id, b);
+          }
+          w.Q.erase(id);
+          w.R.insert(id);
+          ++n_res;
+          tokens += tok;
+          if (SWAPM) {
+            swap_in += ceil_div(x.ctx, bs) * dD.block_bytes;
+            kind[id] = K_DEC;
+          } else {
+            kind[id] = K_PRE_RECOMP;
+          }
+        }
+        // pull pending requests FCFS onto this worker's ingress link (reading R-X3)
+        if (w.Q.empty() && (c.kind != OR_STATIC || (w.R.empty() && w.xfer.empty()))) {
+          while (!w.pending.empty() && req[w.pending.front()].join <= t) {
+            const u32 id = w.pending.front();
+            NReq &x = req[id];
+            const u64 need = ceil_div(x.p, bs);
+            if (w.R.size() + w.xfer.size() + 1 > c.max_num_seqs) break;
+            if ((i64)w.free.size() - (i64)need < (i64)c.watermark_blocks) break;
+            for (u64 q = 0; q < need; ++q) {
+              const u32 b = *w.free.begin();
+              w.free.erase(w.free.begin());
+              x.dblocks.push_back(b);
+              ev(w.k, 1, wid, id, b);
+            }
+            const u64 bytes = (u64)x.p * dD.kvb;
+            const double sec = (double)bytes * inv_link;
+            const i64 dur = (i64)std::floor(sec * 1e9 + 0.5);
+            const i64 start = std::max(t, w.link_busy);
+            x.xend = start + dur;
+            x.xstarted = true;
+            w.link_busy = x.xend;
+            w.xfer.insert(id);
+            w.pending.pop_front();
+            ++n_adm;
+            ++n_xfer;
+            xfer_bytes += bytes;
+            PW &pw = Pw[x.pw];
+            if (pw.idle && x.xend < pw.t) pw.t = x.xend;  // its prefill worker waits for these blocks
+          }
+        }
+      }
+      if (w.R.empty()) {  // nothing runnable: wait for a transfer end (dispatches wake it too)
+        i64 wake = INF;
+        for (u32 id : w.xfer) wake = std::min(wake, req[id].xend);
+        for (u32 id : w.pending)
+          if (req[id].join > t) wake = std::min(wake, req[id].join);
+        w.t = wake;
+        w.idle = true;
+        continue;
+      }
+      std::vector<Prefill> pf;
+      std::vector<u64> dec;
+      u64 Np = 0, Cd = 0;
+      for (u32 id : w.R) {
+        const NReq &x = req[id];
+        if (kind[id] == K_DEC) {
+          dec.push_back(x.ctx + 1);
+          Cd += x.ctx + 1;
+        } else {
+          pf.push_back({x.p + x.gen, 0});
+          Np += x.p + x.gen;
+        }
+      }
+      const i64 T = iter_time(KD.k, pf, dec, swap_out + swap_in);
+      const i64 te = t + T;
+      const u64 blocks = totD - w.free.size();
+      const u64 entries = w.R.size();
+      u64 n_fin = 0;
+      std::vector<u32> Rc(w.R.begin(), w.R.end());
+      for (u32 id : Rc) {
+        NReq &x = req[id];
+        if (kind[id] == K_PRE_RECOMP) {
+          x.ctx = x.p + x.gen;
+          x.gen += 1;
+        } else {
+          x.ctx += 1;
+          x.gen += 1;
+        }
+        const i64 gap = te - x.last_tok;
+        x.max_gap = std::max(x.max_gap, gap);
+        x.last_tok = te;
+        if (x.gen == x.o) {
+          finish_req(id, te, w.k);
+          for (u32 b : x.dblocks) {
+            w.free.insert(b);
+            ev(w.k, 2, wid, id, b);
+          }
+          x.dblocks.clear();
+          w.R.erase(id);
+          ++n_fin;
+        }
+      }
+      sched_d += fold({w.k | ((u64)wid << 40), (u64)t, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0,
+                       n_fin, blocks});
+      run->iters.push_back({w.k, t, T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0, n_fin, blocks, wid, 0});
+      req_iters += entries;
+      w.peak = std::max(w.peak, blocks);
+      w.bns += blocks * (u64)T;
+      swo += swap_out;
+      swi += swap_in;
+      w.t = te;
+      w.last = te;
+      ++w.k;
+      w.idle = false;
+    } else {
+      // ================================================================ P_i boundary
+      const u32 i = (u32)wsel;
+      PW &w = Pw[i];
+      const i64 t = w.t;
+      std::vector<u32> hv(w.holders.begin(), w.holders.end());
+      for (u32 id : hv) {  // blocks of finished transfers come back (ascending id)
+        NReq &x = req[id];
+        if (!(x.xstarted && x.xend <= t)) continue;
+        for (u32 b : x.pblocks) {
+          w.free.insert(b);
+          ev(w.k, 2, i, id, b);
+        }
+        x.pblocks.clear();
+        w.holders.erase(id);
+      }
+      u64 tokens = 0, n_rej = 0;
+      while (!w.queue.empty()) {
+        const u32 id = w.queue.front();
+        NReq &x = req[id];
+        const u64 need = ceil_div(x.p, bs);
+        if (need > totP - c.watermark_blocks) {
+          x.status = 2;
+          ++n_rej;
+          ++n_done;
+          w.queue.pop_front();
+          continue;
+        }
+        if (w.batch.size() + 1 > c.max_num_seqs) break;
+        if (tokens + x.p > c.max_batched_tokens) break;
+        if ((i64)w.free.size() - (i64)need < (i64)c.watermark_blocks) break;
+        for (u64 q = 0; q < need; ++q) {
+          const u32 b = *w.free.begin();
+          w.free.erase(w.free.begin());
+          x.pblocks.push_back(b);
+          ev(w.k, 1, i, id, b);
+        }
+        w.batch.push_back(id);
+        tokens += x.p;
+        w.queue.pop_front();
+      }
+      nrej_tot += n_rej;
+      if (w.batch.empty()) {  // idle: wait for a dispatch or for P blocks to come back
+        i64 wake = INF;
+        for (u32 id : w.holders)
+          if (req[id].xstarted) wake = std::min(wake, req[id].xend);
+        w.t = wake;
+        w.idle = true;
+        continue;
+      }
+      std::vector<Prefill> pf;
+      u64 Np = 0;
+      for (u32 id : w.batch) {
+        pf.push_back({req[id].p, 0});
+        Np += req[id].p;
+      }
+      const i64 T = iter_time(KP.k, pf, {}, 0);
+      const i64 te = t + T;
+      const u64 blocks = totP - w.free.size();
+      u64 n_fin = 0;
+      for (u32 id : w.batch) {  // the first token at the end-of-prefill breakpoint
+        NReq &x = req[id];
+        x.ctx = x.p;
+        x.gen = 1;
+        x.first_tok = te;
+        x.last_tok = te;
+        if (x.gen == x.o) {
+          finish_req(id, te, w.k);
+          for (u32 b : x.pblocks) {
+            w.free.insert(b);
+            ev(w.k, 2, i, id, b);
+          }
+          x.pblocks.clear();
+          ++n_fin;
+        } else {
+          w.holders.insert(id);
+        }
+      }
+      sched_d += fold({w.k | ((u64)i << 40), (u64)t, (u64)T, w.batch.size(), 0, Np, 0, 0, 0, w.batch.size(), n_rej,
+                       n_fin, blocks});
+      run->iters.push_back({w.k, t, T, w.batch.size(), 0, Np, 0, 0, 0, w.batch.size(), n_rej, n_fin, blocks, i, 0});
+      req_iters += w.batch.size();
+      w.tdisp = te;  // the batch goes to the global scheduler at te
+      w.t = te;
+      w.last = te;
+      ++w.k;
+      w.idle = false;
+    }
+    if (c.check_invariants) {
+      bool ok = true;
+      for (u32 q = 0; q < X; ++q) {
+        u64 h = 0;
+        for (u32 id = 0; id < n; ++id)
+          if (req[id].pw == q) h += req[id].pblocks.size();
+        ok &= h + Pw[q].free.size() == totP;
+      }
+      for (u32 q = 0; q < Y; ++q) {
+        const DW &w = Dw[q];
+        u64 h = 0;
+        for (u32 id = 0; id < n; ++id)
+          if (req[id].dw == q) h += req[id].dblocks.size();
+        ok &= h + w.free.size() == totD;
+        for (u32 id : w.R) ok &= req[id].dblocks.size() == ceil_div(req[id].ctx, bs) && req[id].dw == q;
+        for (u32 id : w.xfer) ok &= req[id].dblocks.size() == ceil_div(req[id].p, bs) && req[id].dw == q;
+        for (u32 id : w.Q) ok &= req[id].dblocks.empty();
+      }
+      if (!ok) {
+        g_err = "P/D node invariant violated";
+        delete run;
+        return nullptr;
+      }
+    }
+  }
+
+  run->records.resize(n);
+  u64 n_fin = 0;
+  for (u32 i = 0; i < n; ++i) {
+    const NReq &x = req[i];
+    oracle_record &rec = run->records[i];
+    rec.ttft_ns = (x.gen >= 1 || x.status == 1) ? x.first_tok - x.a : 0;
+    rec.e2e_ns = x.status == 1 ? x.finish - x.a : 0;
+    rec.mtpot_ns = x.status == 1 ? x.max_gap : 0;
+    rec.n_preempt = x.n_preempt;
+    rec.status = x.status;
+    rec.finish_k = x.status == 1 ? x.finish_k : 0;
+    if (x.status == 1) ++n_fin;
+  }
+  i64 t_final = 0;
+  u64 kall = 0, peak = 0, bns = 0;
+  for (const PW &w : Pw) {
+    t_final = std::max(t_final, w.last);
+    kall += w.k;
+  }
+  for (const DW &w : Dw) {
+    t_final = std::max(t_final, w.last);
+    kall += w.k;
+    peak = std::max(peak, w.peak);
+    bns += w.bns;
+  }
+  S.n_requests = n;
+  S.n_finished = n_fin;
+  S.n_rejected = nrej_tot;
+  S.n_unfinished = n - n_fin - nrej_tot;
+  if (nrej_tot == n) S.status_flags |= 2;
+  S.n_iterations = kall;
+  S.n_request_iterations = req_iters;
+  S.n_preemptions = npre;
+  S.swap_out_bytes = swo;
+  S.swap_in_bytes = swi;
+  S.t_final = t_final;
+  S.sched_digest = sched_d;
+  S.block_digest = block_d;
+  S.request_digest = req_d;
+  // the decode pool (reading R-X5): y workers' blocks; peak = the largest single-worker peak
+  S.total_blocks = (u64)Y * totD;
+  S.peak_blocks = peak;
+  S.block_ns_sum = bns;
+  S.mean_util = (t_final > 0 && totD > 0) ? (double)bns / ((double)S.total_blocks * (double)t_final) : 0.0;
+  S.n_transfers = n_xfer;
+  S.transfer_bytes = xfer_bytes;
+  std::vector<Req> rr(n);
+  for (u32 i = 0; i < n; ++i) {
+    rr[i].a = req[i].a;
+    rr[i].p = req[i].p;
+    rr[i].o = req[i].o;
+    rr[i].status = req[i].status;
+    rr[i].first_tok = req[i].first_tok;
+    rr[i].finish = req[i].finish;
+    rr[i].max_gap = req[i].max_gap;
+  }
+  metrics(c, dD, rr, S);
+  bool ovf = false;
+  for (u32 w = 0; w < X + Y; ++w) build_trace(c, run->iters, w, t_final, run->trace[w], ovf);
+  if (ovf) S.status_flags |= 1;
+  return run;
+}
+
 }  // namespace
 
 // ======================================================================== C ABI
@@ -1299,7 +1832,10 @@ uint64_t oracle_fold(const uint64_t *fields, uint32_t n) {
 
 oracle_run *oracle_simulate(const oracle_cfg *cfg) {
   g_err.clear();
-  if (cfg->topology == OR_PD_PAIR) return simulate_pd(*cfg);
+  if (cfg->topology == OR_PD_PAIR) {
+    const bool one = (cfg->n_prefill <= 1 && cfg->n_decode <= 1);
+    return (one && !cfg->force_general) ? simulate_pd(*cfg) : simulate_pdn(*cfg);
+  }
   return simulate_unified(*cfg);
 }
 
@@ -1316,7 +1852,8 @@ uint64_t oracle_iters(const oracle_run *r, oracle_iter *out) {
   return r->iters.size();
 }
 uint64_t oracle_trace(const oracle_run *r, int worker, oracle_sample *out) {
-  const std::vector<oracle_sample> &v = r->trace[worker ? 1 : 0];
+  static const std::vector<oracle_sample> empty;
+  const std::vector<oracle_sample> &v = (worker >= 0 && worker < OR_MAX_WORKERS) ? r->trace[worker] : empty;
   if (out) std::copy(v.begin(), v.end(), out);
   return v.size();
 }

@@ -22,6 +22,8 @@ enum { OR_LEN_FIXED = 1, OR_LEN_UNIFORM = 2, OR_LEN_TABLE = 3, OR_LEN_TRACE = 4 
 enum { OR_TRACE_NONE = 0, OR_TRACE_BINNED = 1, OR_TRACE_FULL = 2 };
 enum { OR_UNIFIED = 0, OR_PD_PAIR = 1 };
 enum { OR_MIXED = 0, OR_PREFILL_FIRST = 1, OR_CHUNKED = 2 };
+enum { OR_DISPATCH_RR = 0, OR_DISPATCH_LEAST_OUTSTANDING = 1, OR_DISPATCH_LEAST_MEMORY = 2 };
+enum { OR_MAX_WORKERS = 8 };
 
 typedef struct {
   /* model */
@@ -65,6 +67,10 @@ typedef struct {
   uint32_t check_invariants;   /* 1: assert c.8 invariants every iteration */
   uint32_t keep_events;        /* 1: keep the block event log              */
   uint32_t iter_mode;          /* OR_MIXED (A3) | OR_PREFILL_FIRST | OR_CHUNKED (NEXT-3) */
+  /* NEXT-1 xP:yD node (PD_PAIR topology): x prefill + y decode workers, x + y <= 8 */
+  uint32_t n_prefill, n_decode;  /* 0 reads as 1 */
+  uint32_t dispatch;             /* OR_DISPATCH_* (global scheduler) */
+  uint32_t force_general;        /* 1: run the x:y loop even for 1:1 (pins it to the 1:1 loop) */
 } oracle_cfg;
 
 typedef struct {
@@ -83,7 +89,7 @@ typedef struct {
   uint64_t k;
   int64_t t_start, T_ns;
   uint64_t S_p, D, N_p, C_d, m, n_resumed, n_admitted, n_rejected, n_finished, blocks;
-  uint32_t worker; /* 0 unified / prefill, 1 decode */
+  uint32_t worker; /* 0 unified; PD: prefill workers 0..x-1, decode workers x..x+y-1 */
   uint32_t pad;
 } oracle_iter;
 
@@ -132,7 +138,7 @@ const char *oracle_error(void);
 void oracle_summary_get(const oracle_run *r, oracle_summary *out);
 uint64_t oracle_records(const oracle_run *r, oracle_record *out);   /* out may be NULL */
 uint64_t oracle_iters(const oracle_run *r, oracle_iter *out);
-uint64_t oracle_trace(const oracle_run *r, int worker, oracle_sample *out);
+uint64_t oracle_trace(const oracle_run *r, int worker, oracle_sample *out);  /* worker < x + y */
 uint64_t oracle_events(const oracle_run *r, oracle_event *out);
 void oracle_free(oracle_run *r);
 

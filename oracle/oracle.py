@@ -64,6 +64,7 @@ class OracleCfg(C.Structure):
         ("trace_bin_ns", u64), ("trace_cap_samples", u64),
         ("slo_ttft_s", f64), ("slo_mtpot_s", f64), ("horizon_ns", i64),
         ("check_invariants", u32), ("keep_events", u32), ("iter_mode", u32),
+        ("n_prefill", u32), ("n_decode", u32), ("dispatch", u32), ("force_general", u32),
     ]
 
 
@@ -205,6 +206,8 @@ def make_cfg(cfg: si.SweepConfig, point: int, check_invariants: bool = False,
     c.slo_ttft_s, c.slo_mtpot_s, c.horizon_ns = o.slo_ttft_s, o.slo_mtpot_s, o.horizon_ns
     c.check_invariants = 1 if check_invariants else 0
     c.keep_events = 1 if keep_events else 0
+    c.n_prefill, c.n_decode = o.pd_prefill, o.pd_decode
+    c.dispatch = {si.ROUND_ROBIN: 0, si.LEAST_OUTSTANDING: 1, si.LEAST_MEMORY: 2}[o.dispatch]
     return c, keep
 
 
@@ -219,10 +222,11 @@ def summary_to_dict(s: OracleSummary) -> Dict:
 
 
 def simulate(cfg: si.SweepConfig, point: int, check_invariants: bool = False,
-             keep_events: bool = False, want=("summary", "records")) -> Dict:
+             keep_events: bool = False, want=("summary", "records"), force_general: bool = False) -> Dict:
     """Run one grid point in the oracle; returns a dict of numpy arrays / summary."""
     L = lib()
     c, keep = make_cfg(cfg, point, check_invariants, keep_events)
+    c.force_general = 1 if force_general else 0
     h = L.oracle_simulate(C.byref(c))
     if not h:
         raise OracleError(L.oracle_error().decode())
@@ -243,7 +247,8 @@ def simulate(cfg: si.SweepConfig, point: int, check_invariants: bool = False,
             out["iters"] = a
         if "trace" in want:
             tr = []
-            for wk in (0, 1):
+            nw = cfg.options.pd_prefill + cfg.options.pd_decode if cfg.options.topology == si.PD_PAIR else 2
+            for wk in range(nw):
                 n = L.oracle_trace(h, wk, None)
                 a = np.zeros(n, SAMPLE_DTYPE)
                 L.oracle_trace(h, wk, a.ctypes.data)

@@ -66,6 +66,7 @@ A100_IDEAL = Hw(eff_flops=1.0, eff_bw=1.0, iter_overhead_s=0.0)
 STATIC, CONT, CONT_RATIO = "static", "cont", "cont_ratio"
 SWAP, RECOMPUTE = "swap", "recompute"
 MIXED, PREFILL_FIRST, CHUNKED = "mixed", "prefill_first", "chunked"
+ROUND_ROBIN, LEAST_OUTSTANDING, LEAST_MEMORY = "round_robin", "least_outstanding", "least_memory"
 
 
 @dataclass(frozen=True)
@@ -142,6 +143,9 @@ class Options:
     slo_mtpot_s: float = 0.3
     horizon_ns: int = -1
     fast_forward: bool = True          # CUDA path only: time-parallel quiescent stretches
+    pd_prefill: int = 1                # PD: prefill workers x (NEXT-1 xP:yD node; x + y <= 8)
+    pd_decode: int = 1                 # PD: decode workers y
+    dispatch: str = "round_robin"      # global scheduler: ROUND_ROBIN | LEAST_OUTSTANDING | LEAST_MEMORY
 
 
 @dataclass(frozen=True)

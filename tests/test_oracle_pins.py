@@ -763,3 +763,123 @@ def test_chunked_budget_and_invariants(oracle_lib):
         if pol.kind != si.CONT_RATIO:
             assert s["n_rejected"] == 0
     assert long_served > 0 and npre > 0
+
+
+# ------------------------------------------------------------------ NEXT-1 xP:yD node
+def _node(cfg, x, y, dispatch=si.ROUND_ROBIN):
+    return replace(cfg, options=replace(cfg.options, pd_prefill=x, pd_decode=y, dispatch=dispatch))
+
+
+def test_node_1p1d_equals_pair(oracle_lib):
+    """With x = y = 1 the general x:y loop (dispatch events, per-worker links) reduces to the
+    a.9 pair loop exactly, under every dispatch policy."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(515)
+    for it in range(60):
+        cfg, _p, _o = _random_pd(rng)
+        if it % 3 == 0:
+            cfg = replace(cfg, options=replace(cfg.options, horizon_ns=int(rng.integers(1, 2_000_000_000))))
+        a = O.simulate(cfg, 1, check_invariants=True, want=("summary", "records", "iters", "trace"))
+        for d in (si.ROUND_ROBIN, si.LEAST_OUTSTANDING, si.LEAST_MEMORY):
+            b = O.simulate(_node(cfg, 1, 1, d), 1, check_invariants=True, force_general=True,
+                           want=("summary", "records", "iters", "trace"))
+            assert repr(a["summary"]) == repr(b["summary"])
+            assert a["records"].tobytes() == b["records"].tobytes()
+            assert a["iters"].tobytes() == b["iters"].tobytes()
+            for w in (0, 1):
+                assert a["trace"][w].tobytes() == b["trace"][w].tobytes()
+
+
+def test_node_round_robin_splits_evenly(oracle_lib):
+    """round robin over 3 prefill workers, 6 simultaneous requests -> each gets 2; their
+    prefill iterations run concurrently, so every TTFT equals one 2-request prefill."""
+    from oracle import oracle as O
+    cfg = _node(_pd_cfg([(0, 32, 2)] * 6), 3, 2)
+    r = O.simulate(cfg, 1, check_invariants=True, want=("summary", "records", "iters"))
+    it = r["iters"]
+    first = [it[it["worker"] == w][0] for w in range(3)]
+    assert [int(x["S_p"]) for x in first] == [2, 2, 2] and all(int(x["t_start"]) == 0 for x in first)
+    tp = O.iter_time_ns(cfg, [(32, 0), (32, 0)], [], point=1, decode_worker=0)
+    assert (r["records"]["ttft_ns"] == tp).all()
+    # the six completions (same instant, id order) alternate D_0, D_1: three one-decode requests each
+    dec = it[it["worker"] >= 3]
+    assert sorted(set(dec["worker"].tolist())) == [3, 4]
+    assert int(dec[dec["worker"] == 3]["D"].sum()) == 3 and int(dec[dec["worker"] == 4]["D"].sum()) == 3
+
+
+def test_node_least_outstanding_vs_round_robin(oracle_lib):
+    """least-outstanding picks the argmin (ties -> lowest id).  P_0 gets a long prompt,
+    P_1 and P_2 short ones; a fourth request arriving after P_1/P_2 finished goes to P_1 under
+    least-outstanding (P_0 still busy) but to P_0 under round robin, where it waits."""
+    from oracle import oracle as O
+    reqs = [(0, 2000, 2), (0, 8, 2), (0, 8, 2), (60_000_000, 8, 2)]
+    base = _pd_cfg(reqs, model=replace(si.LLAMA2_7B, max_model_len=4096))
+    t_long = O.iter_time_ns(base, [(2000, 0)], [], point=1, decode_worker=0)
+    t_short = O.iter_time_ns(base, [(8, 0)], [], point=1, decode_worker=0)
+    assert t_short < 60_000_000 < t_long
+    lo = O.simulate(_node(base, 3, 1, si.LEAST_OUTSTANDING), 1, check_invariants=True, want=("records", "iters"))
+    rr = O.simulate(_node(base, 3, 1, si.ROUND_ROBIN), 1, check_invariants=True, want=("records", "iters"))
+    assert lo["records"]["ttft_ns"][3] == t_short
+    assert rr["records"]["ttft_ns"][3] == t_long - 60_000_000 + t_short
+    assert 1 in lo["iters"][lo["iters"]["t_start"] == 60_000_000]["worker"].tolist()
+
+
+def test_node_least_memory_prefers_empty_worker(oracle_lib):
+    """S:387 least-memory: a decode worker holding a long context is avoided; the argmin of
+    allocated blocks (ties -> lowest id) receives the next request."""
+    from oracle import oracle as O
+    reqs = [(0, 1000, 400), (500_000_000, 16, 4)]
+    base = _pd_cfg(reqs, model=replace(si.LLAMA2_7B, max_model_len=2048))
+    lm = O.simulate(_node(base, 1, 2, si.LEAST_MEMORY), 1, check_invariants=True, want=("iters",))
+    rr = O.simulate(_node(base, 1, 2, si.ROUND_ROBIN), 1, check_invariants=True, want=("iters",))
+    # both send r1 to D_1 (RR: second completion; LM: D_0 holds r0's blocks) ...
+    for r in (lm, rr):
+        it = r["iters"]
+        assert int(it[it["worker"] == 2]["D"].max()) == 1
+    # ... while with 3 requests RR returns to D_0 and LM keeps avoiding it
+    reqs3 = reqs + [(900_000_000, 16, 4)]
+    b3 = _pd_cfg(reqs3, model=replace(si.LLAMA2_7B, max_model_len=2048))
+    lm3 = O.simulate(_node(b3, 1, 2, si.LEAST_MEMORY), 1, check_invariants=True, want=("iters",))
+    rr3 = O.simulate(_node(b3, 1, 2, si.ROUND_ROBIN), 1, check_invariants=True, want=("iters",))
+    assert int(rr3["iters"][rr3["iters"]["worker"] == 1]["D"].max()) == 2
+    assert int(lm3["iters"][lm3["iters"]["worker"] == 1]["D"].max()) == 1
+
+
+def test_node_isolated_requests_match_pair(oracle_lib):
+    """Requests far apart never interact, so every x:y node gives the 1:1 pair's latencies
+    (finish_k differs: iteration indices are per worker)."""
+    from oracle import oracle as O
+    reqs = [(k * 10 ** 12, 20 + 7 * k, 1 + k % 5) for k in range(8)]
+    pair = O.simulate(_pd_cfg(reqs), 1, want=("records",))["records"]
+    fields = ["ttft_ns", "e2e_ns", "mtpot_ns", "n_preempt", "status"]
+    for x, y in ((2, 2), (3, 5), (7, 1), (1, 7)):
+        for d in (si.ROUND_ROBIN, si.LEAST_OUTSTANDING, si.LEAST_MEMORY):
+            got = O.simulate(_node(_pd_cfg(reqs), x, y, d), 1, check_invariants=True, want=("records",))["records"]
+            for f in fields:
+                assert (got[f] == pair[f]).all(), f
+
+
+def test_node_invariants_random(oracle_lib):
+    """Random x:y nodes: conservation per worker and every decode on one worker (checked
+    inside the oracle), one transfer per finished request with o >= 2, request-iterations = sum o,
+    prefill workers run prefill-only iterations, and per-worker iteration indices are dense."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(616)
+    for _ in range(60):
+        cfg, p, o = _random_pd(rng)
+        x = int(rng.integers(1, 5))
+        y = int(rng.integers(1, 9 - x))
+        d = str(rng.choice([si.ROUND_ROBIN, si.LEAST_OUTSTANDING, si.LEAST_MEMORY]))
+        cfg = _node(cfg, x, y, d)
+        r = O.simulate(cfg, 1, check_invariants=True, want=("summary", "records", "iters", "trace"))
+        s, rec, it = r["summary"], r["records"], r["iters"]
+        assert s["n_finished"] == len(rec) and s["n_request_iterations"] == int(o.sum())
+        multi = o >= 2
+        assert s["n_transfers"] == int(multi.sum())
+        pw = it["worker"] < x
+        assert (it["S_p"][pw] == it["n_admitted"][pw]).all() and (it["D"][pw] == 0).all()
+        for w in range(x + y):
+            k = it["k"][it["worker"] == w]
+            assert (k == np.arange(len(k))).all()
+        assert len(r["trace"]) == x + y
+        assert s["total_blocks"] == y * O.derive(cfg, 1, 1)["total_blocks"]
