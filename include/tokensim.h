@@ -66,6 +66,8 @@ enum { TOKENSIM_LEN_SHAREGPT_SYNTH_V1 = 0, TOKENSIM_LEN_FIXED = 1, TOKENSIM_LEN_
        TOKENSIM_LEN_TABLE = 3, TOKENSIM_LEN_TRACE = 4 };                      /* len_dist      */
 enum { TOKENSIM_TRACE_NONE = 0, TOKENSIM_TRACE_BINNED = 1, TOKENSIM_TRACE_FULL = 2 };
 enum { TOKENSIM_UNIFIED = 0, TOKENSIM_PD_PAIR = 1 };                        /* topology      */
+enum { TOKENSIM_DISPATCH_ROUND_ROBIN = 0, TOKENSIM_DISPATCH_LEAST_OUTSTANDING = 1,
+       TOKENSIM_DISPATCH_LEAST_MEMORY = 2 };                                 /* options.dispatch */
 enum { TOKENSIM_TTFT = 0, TOKENSIM_TPOT = 1, TOKENSIM_E2E = 2, TOKENSIM_NORM = 3,
        TOKENSIM_MTPOT = 4 };                                                /* metric        */
 enum { TOKENSIM_REQ_UNFINISHED = 0, TOKENSIM_REQ_FINISHED = 1, TOKENSIM_REQ_REJECTED = 2 };
@@ -155,10 +157,20 @@ typedef struct {
   double slo_mtpot_s;         /* 0.3                                         */
   int64_t horizon_ns;         /* -1 = run to completion                              */
   uint32_t flags;             /* TOKENSIM_OPT_*; 0 = defaults                        */
+  /* NEXT-1: PD_PAIR generalizes to an xP:yD node -- x prefill workers on the
+   * prefill profile, y decode workers on the decode profile (x, y >= 1, x + y <= 8; 0 reads
+   * as 1) -- with a global scheduler dispatching arrivals to
+   * prefill workers and end-of-prefill requests to decode workers (readings R-X1..R-X6). */
+  uint32_t pd_prefill_workers;
+  uint32_t pd_decode_workers;
+  uint32_t dispatch;          /* TOKENSIM_DISPATCH_*; ties go to the lowest worker index    */
 } tokensim_options;
 /* options.flags: evaluate quiescent decode stretches one iteration at a time instead of
  * 32 at once (results are identical either way; this exists to prove it). */
-enum { TOKENSIM_OPT_NO_FAST_FORWARD = 1 };
+enum { TOKENSIM_OPT_NO_FAST_FORWARD = 1,
+       /* run a 1P:1D pair through the general xP:yD node loop (results are identical; this
+        * exists to prove it) */
+       TOKENSIM_OPT_NODE_LOOP = 2 };
 
 /* ---- results ------------------------------------------------------------- */
 typedef struct {               /* 32 B; index = request id                         */
@@ -240,8 +252,9 @@ uint64_t tokensim_sweep_num_run(const tokensim_sweep *h);
  * imported with tokensim_import_summaries; anything else is E_STATE. */
 tokensim_status tokensim_get_latency_quantiles(const tokensim_sweep *h, uint64_t point, uint32_t metric,
                                                const uint32_t *q_bp, uint32_t n_q, double *out_seconds);
-/* KV memory over time of one worker (0 = unified / prefill, 1 = decode in
- * PD_PAIR).  Returns E_OVERFLOW (with the samples that fit) if the trace hit its cap. */
+/* KV memory over time of one worker: 0 = unified; PD_PAIR: prefill workers
+ * 0..x-1, decode workers x..x+y-1 (1P:1D: 0 = prefill, 1 = decode).  E_RANGE for any other
+ * worker.  Returns E_OVERFLOW (with the samples that fit) if the trace hit its cap. */
 tokensim_status tokensim_get_mem_trace(const tokensim_sweep *h, uint64_t point, uint32_t worker,
                                        tokensim_mem_sample *out, uint64_t capacity, uint64_t *n_out);
 tokensim_status tokensim_get_summary(const tokensim_sweep *h, uint64_t point, tokensim_summary *out);

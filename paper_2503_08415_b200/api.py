@@ -30,6 +30,8 @@ class TokensimError(RuntimeError):
 
 _KIND = {si.STATIC: T.STATIC, si.CONT: T.CONT, si.CONT_RATIO: T.CONT_RATIO}
 _PRE = {si.SWAP: T.SWAP, si.RECOMPUTE: T.RECOMPUTE}
+_DISPATCH = {si.ROUND_ROBIN: T.DISPATCH_ROUND_ROBIN, si.LEAST_OUTSTANDING: T.DISPATCH_LEAST_OUTSTANDING,
+             si.LEAST_MEMORY: T.DISPATCH_LEAST_MEMORY}
 _MODE = {si.MIXED: T.MIXED, si.PREFILL_FIRST: T.PREFILL_FIRST, si.CHUNKED: T.CHUNKED}
 _LEN = {si.FIXED: T.LEN_FIXED, si.UNIFORM: T.LEN_UNIFORM, si.TABLE: T.LEN_TABLE, si.TRACE: T.LEN_TRACE,
         "sharegpt_synth_v1": T.LEN_SHAREGPT_SYNTH_V1}
@@ -88,9 +90,10 @@ def marshal(cfg: si.SweepConfig):
         keep += [ta, tp, to]
         cw.trace_arrival_ns, cw.trace_prompt, cw.trace_output = pta, ptp, pto
     o = cfg.options
+    flags = (0 if o.fast_forward else T.OPT_NO_FAST_FORWARD) | (T.OPT_NODE_LOOP if o.node_loop else 0)
     co = T.Options(C.sizeof(T.Options), _TOP[o.topology], o.pd_link_bw, _TRC[o.trace_mode], o.trace_bin_ns,
                    o.trace_cap_bytes, o.iteration_trace_cap, o.slo_ttft_s, o.slo_mtpot_s, o.horizon_ns,
-                   0 if o.fast_forward else T.OPT_NO_FAST_FORWARD)
+                   flags, o.pd_prefill, o.pd_decode, _DISPATCH[o.dispatch])
     return cm, hws, pols, cw, co, keep
 
 

@@ -33,7 +33,7 @@ const uint32_t kOutputThr[7] = {429496730u, 773094113u, 1159641170u, 1717986918u
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, ring, fifo, evlog, itlog,
+  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, ring, fifo, pdn, pdn_per_warp, evlog, itlog,
       total;
   u64 n_run;
   u32 warps_total, wpb, blocks;
@@ -60,6 +60,14 @@ struct tokensim_sweep {
   std::vector<DevPol> dpol;
   std::vector<double> est_T1;  // per (hw,pol): rough per-iteration time for LPT ordering
   u32 cap = 256, nwords_max = 1, bt_len = 1, n_hw_axis = 0;
+  u32 pd_x = 0, pd_y = 0;  // NEXT-1 node: prefill / decode workers (0 = unified)
+  bool pd_general = false;  // run the general xP:yD loop
+  u32 trace_nw() const { return pd_general ? std::max<u32>(2, pd_x + pd_y) : 2; }
+  u32 bt_tables() const { return pd_general ? pd_y + 1 : 2; }
+  size_t smem_per_warp() const {
+    return sim_smem_per_warp((int)cap, nwords_max, opt.topology == TOKENSIM_PD_PAIR, pd_general ? pd_x : 0,
+                             pd_general ? pd_y : 0);
+  }
   u64 n_points = 0, max_total_blocks = 0;
   // device tables
   int dev = -1;
@@ -144,6 +152,13 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
   if (opt->topology > TOKENSIM_PD_PAIR) return fail(nullptr, TOKENSIM_E_INVALID, "options.topology: unknown");
   if (opt->topology == TOKENSIM_PD_PAIR && !(opt->pd_link_bw > 0))
     return fail(nullptr, TOKENSIM_E_INVALID, "options.pd_link_bw: must be > 0 with PD_PAIR");
+  if (opt->topology == TOKENSIM_PD_PAIR) {
+    const u32 x = opt->pd_prefill_workers ? opt->pd_prefill_workers : 1u;
+    const u32 y = opt->pd_decode_workers ? opt->pd_decode_workers : 1u;
+    if (x + y > 8) return fail(nullptr, TOKENSIM_E_INVALID, "options.pd_prefill_workers + pd_decode_workers: at most 8");
+    if (opt->dispatch > TOKENSIM_DISPATCH_LEAST_MEMORY)
+      return fail(nullptr, TOKENSIM_E_INVALID, "options.dispatch: unknown");
+  }
   if (opt->trace_mode > TOKENSIM_TRACE_FULL) return fail(nullptr, TOKENSIM_E_INVALID, "options.trace_mode: unknown");
   if (opt->trace_mode == TOKENSIM_TRACE_BINNED && opt->trace_bin_ns == 0)
     return fail(nullptr, TOKENSIM_E_INVALID, "options.trace_bin_ns: must be > 0");
@@ -390,7 +405,12 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
   u64 max_total = 0;
   for (const DevHP &x : h->dhp) max_total = std::max(max_total, x.total_blocks);
   h->max_total_blocks = max_total;
-  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max, opt->topology == TOKENSIM_PD_PAIR);
+  if (opt->topology == TOKENSIM_PD_PAIR) {
+    h->pd_x = opt->pd_prefill_workers ? opt->pd_prefill_workers : 1u;
+    h->pd_y = opt->pd_decode_workers ? opt->pd_decode_workers : 1u;
+    h->pd_general = h->pd_x > 1 || h->pd_y > 1 || (opt->flags & TOKENSIM_OPT_NODE_LOOP);
+  }
+  const size_t per_warp = h->smem_per_warp();
   if (per_warp > 227 * 1024) {
     delete h;
     return fail(nullptr, TOKENSIM_E_INVALID, "max_num_seqs x total_blocks needs more than 227 KB of shared memory per point");
@@ -414,7 +434,8 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   const u64 groups = trace_mode ? 1 : (u64)h->rates.size() * h->seeds.size();
   L.n_run = n_run;
   const bool pd = h->opt.topology == TOKENSIM_PD_PAIR;
-  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max, pd);
+  const bool pair = pd && !h->pd_general;
+  const size_t per_warp = h->smem_per_warp();
   u32 wpb = (u32)std::max<size_t>(1, std::min<size_t>(4, (227 * 1024) / per_warp));
   u32 bps = (u32)std::max<size_t>(1, (227 * 1024) / (per_warp * wpb));
   bps = std::min<u32>(bps, 16);
@@ -437,15 +458,17 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   L.output = take(trace_mode ? 0 : groups * n * 4);
   L.rec = take(n_run * n * sizeof(tokensim_request_record));
   L.stats = take(n_run * sizeof(SimStats));
-  L.trace = take(n_run * 2 * trace_cap * sizeof(tokensim_mem_sample));
+  L.trace = take(n_run * h->trace_nw() * trace_cap * sizeof(tokensim_mem_sample));
   L.itrec = take(n_run * (u64)h->opt.iteration_trace_cap * sizeof(tokensim_iter_record));
   L.summ = take(n_run * sizeof(tokensim_summary));
-  L.bt = take((size_t)L.warps_total * 2 * h->cap * h->bt_len * 4);
+  L.bt = take((size_t)L.warps_total * h->bt_tables() * h->cap * h->bt_len * 4);
   L.order = take(n_run * 4 + 4);
   L.queue = take(256);
   L.scratch = take(n > kSummarySmemKeys ? n_run * n * 8 : 0);
-  L.ring = take(pd ? (size_t)L.warps_total * h->max_total_blocks * 4 : 0);
-  L.fifo = take(pd ? (size_t)L.warps_total * n * 32 : 0);
+  L.ring = take(pair ? (size_t)L.warps_total * h->max_total_blocks * 4 : 0);
+  L.fifo = take(pair ? (size_t)L.warps_total * n * 32 : 0);
+  L.pdn_per_warp = h->pd_general ? align256(pdn_global_per_warp(n, h->cap, h->bt_len, h->pd_x, h->pd_y)) : 0;
+  L.pdn = take((size_t)L.warps_total * L.pdn_per_warp);
   L.evlog = take((size_t)L.warps_total * 1024 * 16);
   L.itlog = take((size_t)L.warps_total * 256 * 64);
   L.total = o;
@@ -530,7 +553,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   if (s != TOKENSIM_OK) return s;
   const u64 n_run = count_run(begin, end, stride);
   int sms = device_sms(device);
-  const size_t per_warp = sim_smem_per_warp((int)h->cap, h->nwords_max, h->opt.topology == TOKENSIM_PD_PAIR);
+  const size_t per_warp = h->smem_per_warp();
   Layout L0 = make_layout(h, n_run, sms, 0);
   int occ = 0;
   e = sim_occupancy((int)h->cap, (int)L0.wpb, per_warp * L0.wpb, &occ);
@@ -595,6 +618,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.rec = reinterpret_cast<tokensim_request_record *>(ws + L.rec);
   P.stats = reinterpret_cast<SimStats *>(ws + L.stats);
   P.trace = reinterpret_cast<tokensim_mem_sample *>(ws + L.trace);
+  P.trace_nw = h->trace_nw();
+  P.bt_tables = h->bt_tables();
   P.trace_cap = h->opt.trace_mode == TOKENSIM_TRACE_NONE ? 0 : h->opt.trace_cap_bytes / sizeof(tokensim_mem_sample);
   P.itrec = reinterpret_cast<tokensim_iter_record *>(ws + L.itrec);
   P.it_cap = h->opt.iteration_trace_cap;
@@ -615,6 +640,12 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.pd_ring = reinterpret_cast<u32 *>(ws + L.ring);
   P.pd_ring_len = h->max_total_blocks ? h->max_total_blocks : 1;
   P.pd_fifo = reinterpret_cast<unsigned char *>(ws + L.fifo);
+  P.pdn_scratch = reinterpret_cast<unsigned char *>(ws + L.pdn);
+  P.pdn_bytes_per_warp = L.pdn_per_warp;
+  P.pd_x = h->pd_x;
+  P.pd_y = h->pd_y;
+  P.dispatch = h->opt.dispatch;
+  P.pd_general = h->pd_general ? 1u : 0u;
   P.evlog = reinterpret_cast<uint4 *>(ws + L.evlog);
   P.itlog = reinterpret_cast<ulonglong2 *>(ws + L.itlog);
 
@@ -778,7 +809,8 @@ tokensim_status tokensim_get_mem_trace(const tokensim_sweep *hc, uint64_t point,
                                        tokensim_mem_sample *out, uint64_t capacity, uint64_t *n_out) {
   tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
   if (!h || !n_out) return TOKENSIM_E_INVALID;
-  if (worker > (h->opt.topology == TOKENSIM_PD_PAIR ? 1u : 0u)) return TOKENSIM_E_RANGE;
+  const u32 n_workers = h->opt.topology == TOKENSIM_PD_PAIR ? h->pd_x + h->pd_y : 1u;
+  if (worker >= n_workers) return TOKENSIM_E_RANGE;
   u64 j;
   tokensim_status s = local_index(h, point, &j);
   if (s != TOKENSIM_OK) return fail(h, s, "get_mem_trace: point not run by this handle");
@@ -790,7 +822,7 @@ tokensim_status tokensim_get_mem_trace(const tokensim_sweep *hc, uint64_t point,
   *n_out = cnt;
   if (!out || capacity == 0) return TOKENSIM_OK;
   if (capacity < cnt) return TOKENSIM_E_TRUNCATED;
-  s = copy_d2h(h, out, h->P.trace + (j * 2 + worker) * h->P.trace_cap, cnt * sizeof(tokensim_mem_sample));
+  s = copy_d2h(h, out, h->P.trace + (j * h->P.trace_nw + worker) * h->P.trace_cap, cnt * sizeof(tokensim_mem_sample));
   if (s != TOKENSIM_OK) return s;
   return (st.flags & TOKENSIM_PT_TRACE_OVERFLOW) ? TOKENSIM_E_OVERFLOW : TOKENSIM_OK;
 }
@@ -890,7 +922,7 @@ tokensim_status tokensim_get_run_info(const tokensim_sweep *hc, tokensim_run_inf
   out->n_launches = h->n_launches;
   out->sim_blocks = h->lay.blocks;
   out->sim_warps_per_block = h->lay.wpb;
-  out->smem_per_warp = (u32)sim_smem_per_warp((int)h->cap, h->nwords_max, h->opt.topology == TOKENSIM_PD_PAIR);
+  out->smem_per_warp = (u32)h->smem_per_warp();
   out->n_run = h->n_run;
   out->h2d_bytes = h->h2d_bytes;
   out->workspace_bytes = h->lay.total;

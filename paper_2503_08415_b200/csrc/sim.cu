@@ -124,9 +124,7 @@ __host__ __device__ inline size_t smem_per_warp_bytes(u32 cap, u32 nwords_max) {
 __host__ __device__ inline size_t smem_pd_extra(u32 cap, u32 nwords_max) {
   return ((size_t)cap * 4 * 5 + (size_t)nwords_max * 4 + 15) & ~(size_t)15;
 }
-size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd) {
-  return smem_per_warp_bytes((u32)cap, nwords_max) + (pd ? smem_pd_extra((u32)cap, nwords_max) : 0);
-}
+size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_y);
 
 __device__ __forceinline__ WarpSmem carve(unsigned char *base, u32 cap) {
   WarpSmem S;
@@ -394,6 +392,12 @@ __device__ __forceinline__ i64 scan_incl_i64(i64 x) {
 }
 
 #include "sim_pd.cuh"
+#include "sim_pdn.cuh"
+
+size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_y) {
+  if (node_x) return pdn_smem_per_warp((u32)cap, nwords_max, node_x, node_y);
+  return smem_per_warp_bytes((u32)cap, nwords_max) + (pd ? smem_pd_extra((u32)cap, nwords_max) : 0);
+}
 
 // ------------------------------------------------------------------ a.2-a.7 one point
 // Everything is executed by all 32 lanes; scalar state is lane-uniform in registers.
@@ -414,7 +418,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const u32 *PR = P.prompt + (size_t)g * n;
   const u32 *OU = P.output + (size_t)g * n;
   tokensim_request_record *rec = P.rec + (size_t)j * n;
-  tokensim_mem_sample *trc = P.trace + (size_t)j * 2 * P.trace_cap;
+  tokensim_mem_sample *trc = P.trace + (size_t)j * P.trace_nw * P.trace_cap;
   tokensim_iter_record *itr = P.itrec + (size_t)j * P.it_cap;
   const BSz B = {PL.bs, PL.bs_sh, PL.bs - 1u, PL.bs_sh != 0xffffffffu};
   const bool SWAPM = PL.preempt == TOKENSIM_SWAP;
@@ -1400,7 +1404,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     st.peak_blocks = peak;
     st.block_ns_sum = bns;
     st.trace_n[0] = min(tn, P.trace_cap);
-    st.trace_n[1] = 0;
+    for (int q = 1; q < 8; ++q) st.trace_n[q] = 0;
     st.iter_n = min(k, P.it_cap);
     st.n_transfers = 0;
     st.transfer_bytes = 0;
@@ -1422,18 +1426,21 @@ __global__ void __launch_bounds__(128) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
   const bool pd = P.topology == TOKENSIM_PD_PAIR;
+  const bool node = pd && P.pd_general;
   const size_t base = smem_per_warp_bytes(CAP, P.nwords_max);
-  const size_t per_warp = base + (pd ? smem_pd_extra(CAP, P.nwords_max) : 0);
+  const size_t per_warp =
+      node ? pdn_smem_per_warp(CAP, P.nwords_max, P.pd_x, P.pd_y) : base + (pd ? smem_pd_extra(CAP, P.nwords_max) : 0);
   const WarpSmem S = carve(smem_raw + wib * per_warp, CAP);
   const u32 gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
-  u32 *bt = P.bt + (size_t)gwarp * 2 * CAP * P.bt_len;
+  u32 *bt = P.bt + (size_t)gwarp * P.bt_tables * CAP * P.bt_len;
   while (true) {
     u32 qi = 0;
     if (lane == 0) qi = atomicAdd(P.queue, 1u);
     qi = __shfl_sync(FULLMASK, qi, 0);
     if ((u64)qi >= P.n_run) break;
     const u64 j = P.order[qi];
-    if (pd) simulate_pd<CAP>(P, j, S, smem_raw + wib * per_warp + base, bt);
+    if (node) simulate_pdn<CAP>(P, j, smem_raw + wib * per_warp, bt);
+    else if (pd) simulate_pd<CAP>(P, j, S, smem_raw + wib * per_warp + base, bt);
     else simulate_unified<CAP>(P, j, S, bt);
   }
 }

@@ -144,7 +144,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
   const u32 *PR = P.prompt + (size_t)g * n;
   const u32 *OU = P.output + (size_t)g * n;
   tokensim_request_record *rec = P.rec + (size_t)j * n;
-  tokensim_mem_sample *trcP = P.trace + (size_t)j * 2 * P.trace_cap;
+  tokensim_mem_sample *trcP = P.trace + (size_t)j * P.trace_nw * P.trace_cap;
   tokensim_mem_sample *trcD = trcP + P.trace_cap;
   tokensim_iter_record *itr = P.itrec + (size_t)j * P.it_cap;
   const BSz B = {PL.bs, PL.bs_sh, PL.bs - 1u, PL.bs_sh != 0xffffffffu};
@@ -1085,6 +1085,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     st.block_ns_sum = bnsD;
     st.trace_n[0] = min(TA[0].tn, P.trace_cap);
     st.trace_n[1] = min(TA[1].tn, P.trace_cap);
+    for (int q = 2; q < 8; ++q) st.trace_n[q] = 0;
     st.iter_n = min(nit, P.it_cap);
     st.n_transfers = n_xfer;
     st.transfer_bytes = xbytes;

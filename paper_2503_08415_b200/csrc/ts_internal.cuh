@@ -52,7 +52,7 @@ struct SimStats {
   i64 last_finish, t_final;
   u64 sched_d, block_d, req_d;
   u64 total_blocks, peak_blocks, block_ns_sum;
-  u64 trace_n[2];
+  u64 trace_n[8];  // per worker (x + y <= 8 for a P/D node)
   u64 iter_n;
   u64 n_transfers, transfer_bytes;
   u64 ff_iters, ff_runs;  // iterations committed by fast-forward stretches, stretch count
@@ -89,7 +89,8 @@ struct SweepParams {
   // outputs, indexed by local j
   tokensim_request_record *rec;  // [j][n]
   SimStats *stats;               // [j]
-  tokensim_mem_sample *trace;    // [j][2][trace_cap]
+  tokensim_mem_sample *trace;    // [j][trace_nw][trace_cap]
+  u32 trace_nw, bt_tables;       // workers per trace row (2, or x + y); block tables per warp
   u64 trace_cap;
   tokensim_iter_record *itrec;   // [j][it_cap]
   u64 it_cap;
@@ -106,6 +107,9 @@ struct SweepParams {
   u32 *pd_ring;        // P/D: per-warp ring of P block ids [warp][pd_ring_len]
   u64 pd_ring_len;
   unsigned char *pd_fifo;  // P/D: per-warp pending/transfer FIFO [warp][n_req] x 32 B
+  unsigned char *pdn_scratch;  // NEXT-1 node: per-warp FIFOs, queues, holders, P block lists
+  u64 pdn_bytes_per_warp;
+  u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
   uint4 *evlog;            // per-warp block-event log [warp][1024]
   ulonglong2 *itlog;       // per-warp iteration log [warp][256][4]
 };
@@ -133,7 +137,13 @@ cudaError_t launch_summary(const SweepParams &p, cudaStream_t st);
 cudaError_t launch_quantiles(const SweepParams &p, u64 j, u32 metric, const u32 *d_ranks, u32 n_q,
                              double *d_out, u64 *d_keys, cudaStream_t st);
 constexpr u32 kSummarySmemKeys = 12288;  // keys held in shared memory by summary_kernel
-size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd);
+size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_y);
+// NEXT-1 node, per-warp global scratch: decode FIFOs [y][n] x 32 B, prefill queues and holder
+// lists [x][n] x 4 B each, in-flight batches [x][cap] x 4 B, transfer ends [n] x 8 B, prefill
+// block lists [n][bt_len] x 4 B (sim_pdn.cuh)
+inline size_t pdn_global_per_warp(u64 n, u32 cap, u32 btl, u32 x, u32 y) {
+  return (size_t)y * n * 32 + (size_t)x * n * 4 * 2 + (size_t)x * cap * 4 + n * 8 + n * (size_t)btl * 4 + 256;
+}
 cudaError_t sim_occupancy(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
 
 }  // namespace ts

@@ -146,6 +146,7 @@ class Options:
     pd_prefill: int = 1                # PD: prefill workers x (NEXT-1 xP:yD node; x + y <= 8)
     pd_decode: int = 1                 # PD: decode workers y
     dispatch: str = "round_robin"      # global scheduler: ROUND_ROBIN | LEAST_OUTSTANDING | LEAST_MEMORY
+    node_loop: bool = False            # CUDA path only: run a 1P:1D pair through the xP:yD loop
 
 
 @dataclass(frozen=True)

@@ -209,12 +209,14 @@ def test_fast_forward_is_bit_identical(api):
 def check_pd_points(sw, cfg, points, iters=False):
     want = ("summary", "records", "trace") + (("iters",) if iters else ())
     ora = oracle_points(cfg, points, want=want)
+    nw = cfg.options.pd_prefill + cfg.options.pd_decode
+    node = nw > 2 or cfg.options.node_loop
     bad = []
     for p in points:
         o = ora[p]
         bad += compare_summary(sw.summary(p), o["summary"], p)
         bad += compare_records(sw.records(p), o["records"], p)
-        for w in (0, 1):
+        for w in range(nw):
             bad += compare_trace(sw.mem_trace(p, w), o["trace"][w], p)
         prof = sw.point_profile(p)
         if (prof["n_transfers"], prof["transfer_bytes"]) != (o["summary"]["n_transfers"], o["summary"]["transfer_bytes"]):
@@ -222,6 +224,9 @@ def check_pd_points(sw, cfg, points, iters=False):
                        f"oracle={o['summary']['n_transfers']},{o['summary']['transfer_bytes']}")
         if iters:
             g, oi = sw.iteration_trace(p), o["iters"]
+            if node:  # a decode worker's stretch commits ahead of other workers: compare by (worker, k)
+                g = g[np.lexsort((g["k"], g["worker"]))]
+                oi = oi[np.lexsort((oi["k"], oi["worker"]))]
             pairs = [("k", "k"), ("t_start_ns", "t_start"), ("T_ns", "T_ns"), ("n_prefill", "S_p"),
                      ("n_decode", "D"), ("n_admitted", "n_admitted"), ("n_finished", "n_finished"),
                      ("blocks_in_use", "blocks"), ("worker", "worker")]
@@ -327,3 +332,46 @@ def test_chunked_prefill_parity(api):
         assert sw.summaries().tobytes() == off.summaries().tobytes()
         if cfg.name == "pressure":
             assert sw.summaries()["n_preemptions"].sum() > 0
+
+
+# ------------------------------------------------------------------ NEXT-1 xP:yD node
+def test_node_micro_configs(api):
+    """Random x:y nodes (x + y <= 8) under all three dispatch policies vs the oracle's node loop:
+    summaries, records, every worker's memory trace and the iteration records."""
+    rng = np.random.default_rng(41)
+    for _ in range(40):
+        cfg = _micro_pd(rng)
+        x = int(rng.integers(1, 5))
+        y = int(rng.integers(1, 9 - x))
+        d = str(rng.choice([si.ROUND_ROBIN, si.LEAST_OUTSTANDING, si.LEAST_MEMORY]))
+        cfg = replace(cfg, options=replace(cfg.options, pd_prefill=x, pd_decode=y, dispatch=d))
+        sw = run_gpu(api, cfg)
+        check_pd_points(sw, cfg, list(range(cfg.num_points)), iters=True)
+
+
+def test_node_loop_equals_pair(api):
+    """The general node loop run on 1P:1D pairs gives the pair kernel's bytes."""
+    rng = np.random.default_rng(43)
+    for _ in range(12):
+        cfg = _micro_pd(rng)
+        a = run_gpu(api, cfg)
+        b = run_gpu(api, replace(cfg, options=replace(cfg.options, node_loop=True)))
+        assert a.summaries().tobytes() == b.summaries().tobytes()
+        for p in range(cfg.num_points):
+            assert a.records(p).tobytes() == b.records(p).tobytes()
+
+
+def test_node_sharegpt_grid(api):
+    """fig:pd-shaped node sweeps (8 workers: P1-D7, P2-D6, P4-D4) on LLaMA-2-7B with ShareGPT-like
+    lengths, 3 rates x {SWAP, RECOMPUTE}, every dispatch policy; FF on/off identical."""
+    base = si.SweepConfig("node", si.LLAMA2_7B, [si.A100], [si.Policy(preempt=si.SWAP), si.Policy(preempt=si.RECOMPUTE)],
+                          si.Workload(400, [4.0, 16.0, 48.0], [0]), si.Options(topology=si.PD_PAIR))
+    for x, y in ((1, 7), (2, 6), (4, 4)):
+        for d in (si.ROUND_ROBIN, si.LEAST_OUTSTANDING, si.LEAST_MEMORY):
+            cfg = replace(base, options=replace(base.options, pd_prefill=x, pd_decode=y, dispatch=d))
+            sw = run_gpu(api, cfg)
+            assert (sw.summaries()["n_finished"] == 400).all()
+            check_pd_points(sw, cfg, list(range(cfg.num_points)))
+            if d == si.LEAST_MEMORY:
+                off = run_gpu(api, replace(cfg, options=replace(cfg.options, fast_forward=False)))
+                assert sw.summaries().tobytes() == off.summaries().tobytes()
