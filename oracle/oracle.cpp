@@ -233,7 +233,25 @@ struct CostCtx {
   u64 L, h, q, g, f, fu, V, s;
   double invF, invB, invH, invT, overhead;
   u32 tp;
+  u32 link_mode;    // OR_LINK_SEQUENTIAL (A10) | OR_LINK_PRELOAD (NEXT-4)
+  u64 preload_buf;  // PRELOAD buffer bytes
 };
+
+// NEXT-4 preload-buffer pipeline (reading R-N4): n chunks; the producer
+// (the link) loads chunk i in `a` seconds once it has loaded chunk i-1 and a buffer slot is free
+// (the consumer has taken chunk i-K); the consumer takes chunk i at S_i = max(C_{i-1}, P_i) and
+// finishes it `b` later.  Returns C_n, the time the consumer finishes the last chunk.
+double pipeline(u64 n, double a, double b, u64 K) {
+  std::vector<double> P(n + 1, 0.0), S(n + 1, 0.0), C(n + 1, 0.0);
+  for (u64 i = 1; i <= n; ++i) {
+    double ready = P[i - 1];
+    if (i > K) ready = std::fmax(ready, S[i - K]);
+    P[i] = ready + a;
+    S[i] = std::fmax(C[i - 1], P[i]);
+    C[i] = S[i] + b;
+  }
+  return C[n];
+}
 
 CostCtx cost_ctx(const oracle_cfg &c, const oracle_derived &d, int decode_worker) {
   const Profile pr = profile_of(c, decode_worker);
@@ -252,11 +270,13 @@ CostCtx cost_ctx(const oracle_cfg &c, const oracle_derived &d, int decode_worker
   k.invT = d.invT;
   k.overhead = pr.iter_overhead_s;
   k.tp = pr.tp_degree;
+  k.link_mode = c.link_mode;
+  k.preload_buf = c.preload_buffer_bytes;
   return k;
 }
 
 i64 iter_time(const CostCtx &K, const std::vector<Prefill> &pf, const std::vector<u64> &dec,
-              u64 swap_bytes) {
+              u64 swap_out, u64 swap_in = 0) {
   u64 Np = 0, Ap = 0, Kp = 0, Cd = 0, Sp = 0;
   const u64 D = dec.size();
   for (const Prefill &e : pf) {
@@ -280,13 +300,25 @@ i64 iter_time(const CostCtx &K, const std::vector<Prefill> &pf, const std::vecto
   if (D > 0) tATTD = roof(4 * q * Cd, s * (D * (2 * q + 2 * g) + 2 * g * Cd));
   if (S > 0) tLM = roof(2 * S * h * V, s * (V * h + S * h + S * V));
   const double t_layer = ((((tQKV + tATTP) + tATTD) + tO) + tUP) + tDOWN;
-  double T = t_layer * (double)K.L;
+  // PRELOAD (reading R-N4): the swap-in streams layer by layer (chunk = swap_in / L bytes, exact
+  // since kvb has a factor L) through the buffer while the layers compute; the swap-out before
+  // it stays serial.  SEQUENTIAL (A10): every swap byte, then the compute.
+  const bool pipe = K.link_mode == OR_LINK_PRELOAD && swap_in > 0;
+  double T;
+  if (pipe) {
+    const u64 chunk = swap_in / K.L;
+    const u64 slots = std::max<u64>(1, K.preload_buf / chunk);
+    T = pipeline(K.L, (double)chunk * K.invH, t_layer, slots);
+  } else {
+    T = t_layer * (double)K.L;
+  }
   T = T + tLM;
   if (K.tp > 1) {
     const u64 b_ar = 2 * (u64)(K.tp - 1) * N * h * s;
     const double ar = (double)b_ar * K.invT;
     T = T + ar * (double)(2 * K.L);
   }
+  const u64 swap_bytes = pipe ? swap_out : swap_out + swap_in;
   if (swap_bytes > 0) {
     const double sw = (double)swap_bytes * K.invH;
     T = T + sw;
@@ -713,7 +745,7 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
         Np += x.p + x.gen;
       }
     }
-    const i64 T = iter_time(K, pf, dec, swap_out + swap_in);
+    const i64 T = iter_time(K, pf, dec, swap_out, swap_in);
     // 8. commit
     const i64 ts = t, te = t + T;
     const u64 blocks = total - freeset.size();
@@ -1050,7 +1082,7 @@ oracle_run *simulate_pd(const oracle_cfg &c) {
           Np += x.p + x.gen;
         }
       }
-      const i64 T = iter_time(KD.k, pf, dec, swap_out + swap_in);
+      const i64 T = iter_time(KD.k, pf, dec, swap_out, swap_in);
       const i64 te = t + T;
       const u64 blocks = totD - freeD.size();
       const u64 entries = R.size();
@@ -1566,7 +1598,7 @@ oracle_run *simulate_pdn(const oracle_cfg &c) {
           Np += x.p + x.gen;
         }
       }
-      const i64 T = iter_time(KD.k, pf, dec, swap_out + swap_in);
+      const i64 T = iter_time(KD.k, pf, dec, swap_out, swap_in);
       const i64 te = t + T;
       const u64 blocks = totD - w.free.size();
       const u64 entries = w.R.size();
@@ -1813,7 +1845,7 @@ int oracle_workload(const oracle_cfg *cfg, int64_t *arrival, uint32_t *prompt, u
 
 int64_t oracle_iter_time_ns(const oracle_cfg *cfg, int decode_worker, uint32_t n_prefill,
                             const uint32_t *P, const uint32_t *c0, const uint32_t *emits,
-                            uint32_t n_decode, const uint32_t *c, uint64_t swap_bytes) {
+                            uint32_t n_decode, const uint32_t *c, uint64_t swap_out, uint64_t swap_in) {
   oracle_derived d;
   if (!derive(*cfg, decode_worker, d)) return -1;
   const CostCtx K = cost_ctx(*cfg, d, decode_worker);
@@ -1821,7 +1853,11 @@ int64_t oracle_iter_time_ns(const oracle_cfg *cfg, int decode_worker, uint32_t n
   std::vector<u64> dec;
   for (u32 i = 0; i < n_prefill; ++i) pf.push_back({P[i], c0[i], emits ? emits[i] != 0 : true});
   for (u32 i = 0; i < n_decode; ++i) dec.push_back(c[i]);
-  return iter_time(K, pf, dec, swap_bytes);
+  return iter_time(K, pf, dec, swap_out, swap_in);
+}
+
+double oracle_pipeline(uint64_t n_chunks, double a, double b, uint64_t slots) {
+  return pipeline(n_chunks, a, b, slots);
 }
 
 uint64_t oracle_fold(const uint64_t *fields, uint32_t n) {

@@ -24,6 +24,7 @@ enum { OR_UNIFIED = 0, OR_PD_PAIR = 1 };
 enum { OR_MIXED = 0, OR_PREFILL_FIRST = 1, OR_CHUNKED = 2 };
 enum { OR_DISPATCH_RR = 0, OR_DISPATCH_LEAST_OUTSTANDING = 1, OR_DISPATCH_LEAST_MEMORY = 2 };
 enum { OR_MAX_WORKERS = 8 };
+enum { OR_LINK_SEQUENTIAL = 0, OR_LINK_PRELOAD = 1 };
 
 typedef struct {
   /* model */
@@ -71,6 +72,9 @@ typedef struct {
   uint32_t n_prefill, n_decode;  /* 0 reads as 1 */
   uint32_t dispatch;             /* OR_DISPATCH_* (global scheduler) */
   uint32_t force_general;        /* 1: run the x:y loop even for 1:1 (pins it to the 1:1 loop) */
+  /* NEXT-4 communication model: swap-in link mode and buffer */
+  uint32_t link_mode;            /* OR_LINK_SEQUENTIAL | OR_LINK_PRELOAD */
+  uint64_t preload_buffer_bytes;
 } oracle_cfg;
 
 typedef struct {
@@ -129,7 +133,10 @@ int oracle_workload(const oracle_cfg *cfg, int64_t *arrival, uint32_t *prompt, u
    a non-final chunk without an LM-head row (NULL: all emit) -- and decode contexts c[j] */
 int64_t oracle_iter_time_ns(const oracle_cfg *cfg, int decode_worker, uint32_t n_prefill,
                             const uint32_t *P, const uint32_t *c0, const uint32_t *emits,
-                            uint32_t n_decode, const uint32_t *c, uint64_t swap_bytes);
+                            uint32_t n_decode, const uint32_t *c, uint64_t swap_out, uint64_t swap_in);
+/* NEXT-4: completion time of an n-chunk preload pipeline (load a, consume b, `slots` buffer
+   chunks) -- the consumer's finish of the last chunk */
+double oracle_pipeline(uint64_t n_chunks, double a, double b, uint64_t slots);
 uint64_t oracle_fold(const uint64_t *fields, uint32_t n);
 
 /* ---- one point, start to finish ---- */

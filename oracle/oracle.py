@@ -65,6 +65,7 @@ class OracleCfg(C.Structure):
         ("slo_ttft_s", f64), ("slo_mtpot_s", f64), ("horizon_ns", i64),
         ("check_invariants", u32), ("keep_events", u32), ("iter_mode", u32),
         ("n_prefill", u32), ("n_decode", u32), ("dispatch", u32), ("force_general", u32),
+        ("link_mode", u32), ("preload_buffer_bytes", u64),
     ]
 
 
@@ -112,7 +113,9 @@ def lib():
         L.oracle_derive.restype = C.c_int
         L.oracle_workload.argtypes = [C.POINTER(OracleCfg), PI64, PU32, PU32]
         L.oracle_workload.restype = C.c_int
-        L.oracle_iter_time_ns.argtypes = [C.POINTER(OracleCfg), C.c_int, u32, PU32, PU32, PU32, u32, PU32, u64]
+        L.oracle_iter_time_ns.argtypes = [C.POINTER(OracleCfg), C.c_int, u32, PU32, PU32, PU32, u32, PU32, u64, u64]
+        L.oracle_pipeline.argtypes = [u64, C.c_double, C.c_double, u64]
+        L.oracle_pipeline.restype = C.c_double
         L.oracle_iter_time_ns.restype = i64
         L.oracle_fold.argtypes = [C.POINTER(u64), u32]
         L.oracle_fold.restype = u64
@@ -207,6 +210,8 @@ def make_cfg(cfg: si.SweepConfig, point: int, check_invariants: bool = False,
     c.check_invariants = 1 if check_invariants else 0
     c.keep_events = 1 if keep_events else 0
     c.n_prefill, c.n_decode = o.pd_prefill, o.pd_decode
+    c.link_mode = {si.SEQUENTIAL: 0, si.PRELOAD: 1}[o.link_mode]
+    c.preload_buffer_bytes = o.preload_buffer_bytes
     c.dispatch = {si.ROUND_ROBIN: 0, si.LEAST_OUTSTANDING: 1, si.LEAST_MEMORY: 2}[o.dispatch]
     return c, keep
 
@@ -300,7 +305,7 @@ def workload(cfg: si.SweepConfig, point: int = 0):
 
 
 def iter_time_ns(cfg: si.SweepConfig, prefills=(), decodes=(), swap_bytes: int = 0,
-                 point: int = 0, decode_worker: int = 0) -> int:
+                 point: int = 0, decode_worker: int = 0, swap_in: int = 0) -> int:
     """T_ns of one explicit batch: prefills = [(P, c0) or (P, c0, emits), ...], decodes = [c, ...]."""
     L = lib()
     c, keep = make_cfg(cfg, point)
@@ -309,7 +314,12 @@ def iter_time_ns(cfg: si.SweepConfig, prefills=(), decodes=(), swap_bytes: int =
     em, pem = _u32arr([int(x[2]) if len(x) > 2 else 1 for x in prefills] or [1])
     dc, pdc = _u32arr(list(decodes) or [0])
     return L.oracle_iter_time_ns(C.byref(c), decode_worker, len(prefills), pP, pc0, pem, len(decodes), pdc,
-                                 swap_bytes)
+                                 swap_bytes, swap_in)
+
+
+def pipeline(n_chunks: int, a: float, b: float, slots: int) -> float:
+    """NEXT-4 preload pipeline completion time (see oracle.h)."""
+    return lib().oracle_pipeline(n_chunks, a, b, slots)
 
 
 def fold(fields) -> int:

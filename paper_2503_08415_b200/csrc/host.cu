@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -437,6 +438,10 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   const bool pair = pd && !h->pd_general;
   const size_t per_warp = h->smem_per_warp();
   u32 wpb = (u32)std::max<size_t>(1, std::min<size_t>(4, (227 * 1024) / per_warp));
+  // fewer points than SMs x wpb: spread them one warp per SM first (each point is a serial
+  // latency-bound chain; co-resident warps would only share the SM's LSU/MIO pipes)
+  if (const char *e = getenv("TOKENSIM_WPB")) wpb = (u32)std::max(1, std::min(4, atoi(e)));
+  else if ((u64)n_run <= (u64)sm_count) wpb = 1;
   u32 bps = (u32)std::max<size_t>(1, (227 * 1024) / (per_warp * wpb));
   bps = std::min<u32>(bps, 16);
   if (blocks_per_sm_limit > 0) bps = std::min<u32>(bps, (u32)blocks_per_sm_limit);

@@ -67,6 +67,7 @@ STATIC, CONT, CONT_RATIO = "static", "cont", "cont_ratio"
 SWAP, RECOMPUTE = "swap", "recompute"
 MIXED, PREFILL_FIRST, CHUNKED = "mixed", "prefill_first", "chunked"
 ROUND_ROBIN, LEAST_OUTSTANDING, LEAST_MEMORY = "round_robin", "least_outstanding", "least_memory"
+SEQUENTIAL, PRELOAD = "sequential", "preload"
 
 
 @dataclass(frozen=True)
@@ -147,6 +148,8 @@ class Options:
     pd_decode: int = 1                 # PD: decode workers y
     dispatch: str = "round_robin"      # global scheduler: ROUND_ROBIN | LEAST_OUTSTANDING | LEAST_MEMORY
     node_loop: bool = False            # CUDA path only: run a 1P:1D pair through the xP:yD loop
+    link_mode: str = "sequential"      # swap-in link: SEQUENTIAL (A10) | PRELOAD (NEXT-4)
+    preload_buffer_bytes: int = 1 << 30  # PRELOAD buffer
 
 
 @dataclass(frozen=True)
