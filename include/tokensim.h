@@ -66,6 +66,7 @@ enum { TOKENSIM_LEN_SHAREGPT_SYNTH_V1 = 0, TOKENSIM_LEN_FIXED = 1, TOKENSIM_LEN_
        TOKENSIM_LEN_TABLE = 3, TOKENSIM_LEN_TRACE = 4 };                      /* len_dist      */
 enum { TOKENSIM_TRACE_NONE = 0, TOKENSIM_TRACE_BINNED = 1, TOKENSIM_TRACE_FULL = 2 };
 enum { TOKENSIM_UNIFIED = 0, TOKENSIM_PD_PAIR = 1 };                        /* topology      */
+enum { TOKENSIM_LINK_SEQUENTIAL = 0, TOKENSIM_LINK_PRELOAD = 1 };              /* options.link_mode */
 enum { TOKENSIM_DISPATCH_ROUND_ROBIN = 0, TOKENSIM_DISPATCH_LEAST_OUTSTANDING = 1,
        TOKENSIM_DISPATCH_LEAST_MEMORY = 2 };                                 /* options.dispatch */
 enum { TOKENSIM_TTFT = 0, TOKENSIM_TPOT = 1, TOKENSIM_E2E = 2, TOKENSIM_NORM = 3,
@@ -164,6 +165,12 @@ typedef struct {
   uint32_t pd_prefill_workers;
   uint32_t pd_decode_workers;
   uint32_t dispatch;          /* TOKENSIM_DISPATCH_*; ties go to the lowest worker index    */
+  /* NEXT-4: the swap-in link.  SEQUENTIAL (A10): an iteration's swap
+   * bytes move before its compute.  PRELOAD: the swap-in streams one layer's chunk at a time
+   * through a buffer of preload_buffer_bytes while the layers compute (reading R-N4); never
+   * slower than SEQUENTIAL.  The P->D transfer already overlaps both workers (a.9). */
+  uint32_t link_mode;         /* TOKENSIM_LINK_SEQUENTIAL | TOKENSIM_LINK_PRELOAD           */
+  uint64_t preload_buffer_bytes;  /* PRELOAD: > 0; one chunk fits even if smaller           */
 } tokensim_options;
 /* options.flags: evaluate quiescent decode stretches one iteration at a time instead of
  * 32 at once (results are identical either way; this exists to prove it). */

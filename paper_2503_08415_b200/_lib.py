@@ -30,6 +30,7 @@ TTFT, TPOT, E2E, NORM, MTPOT = 0, 1, 2, 3, 4
 REQ_UNFINISHED, REQ_FINISHED, REQ_REJECTED = 0, 1, 2
 OPT_NO_FAST_FORWARD, OPT_NODE_LOOP = 1, 2
 DISPATCH_ROUND_ROBIN, DISPATCH_LEAST_OUTSTANDING, DISPATCH_LEAST_MEMORY = 0, 1, 2
+LINK_SEQUENTIAL, LINK_PRELOAD = 0, 1
 PT_TRACE_OVERFLOW, PT_ALL_REJECTED, PT_HORIZON_HIT, PT_INTERNAL_ERROR = 1, 2, 4, 16
 
 
@@ -67,7 +68,8 @@ class Options(C.Structure):
     _fields_ = [("struct_size", u32), ("topology", u32), ("pd_link_bw", f64), ("trace_mode", u32),
                 ("trace_bin_ns", u64), ("trace_cap_bytes", u64), ("iteration_trace_cap", u32),
                 ("slo_ttft_s", f64), ("slo_mtpot_s", f64), ("horizon_ns", i64), ("flags", u32),
-                ("pd_prefill_workers", u32), ("pd_decode_workers", u32), ("dispatch", u32)]
+                ("pd_prefill_workers", u32), ("pd_decode_workers", u32), ("dispatch", u32),
+                ("link_mode", u32), ("preload_buffer_bytes", u64)]
 
 
 class PointProfile(C.Structure):

@@ -93,7 +93,8 @@ def marshal(cfg: si.SweepConfig):
     flags = (0 if o.fast_forward else T.OPT_NO_FAST_FORWARD) | (T.OPT_NODE_LOOP if o.node_loop else 0)
     co = T.Options(C.sizeof(T.Options), _TOP[o.topology], o.pd_link_bw, _TRC[o.trace_mode], o.trace_bin_ns,
                    o.trace_cap_bytes, o.iteration_trace_cap, o.slo_ttft_s, o.slo_mtpot_s, o.horizon_ns,
-                   flags, o.pd_prefill, o.pd_decode, _DISPATCH[o.dispatch])
+                   flags, o.pd_prefill, o.pd_decode, _DISPATCH[o.dispatch],
+                   {si.SEQUENTIAL: T.LINK_SEQUENTIAL, si.PRELOAD: T.LINK_PRELOAD}[o.link_mode], o.preload_buffer_bytes)
     return cm, hws, pols, cw, co, keep
 
 

@@ -153,6 +153,11 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
   if (opt->topology > TOKENSIM_PD_PAIR) return fail(nullptr, TOKENSIM_E_INVALID, "options.topology: unknown");
   if (opt->topology == TOKENSIM_PD_PAIR && !(opt->pd_link_bw > 0))
     return fail(nullptr, TOKENSIM_E_INVALID, "options.pd_link_bw: must be > 0 with PD_PAIR");
+  if (opt->link_mode > TOKENSIM_LINK_PRELOAD) return fail(nullptr, TOKENSIM_E_INVALID, "options.link_mode: unknown");
+  if (opt->link_mode == TOKENSIM_LINK_PRELOAD && opt->preload_buffer_bytes == 0)
+    return fail(nullptr, TOKENSIM_E_INVALID, "options.preload_buffer_bytes: must be > 0 with PRELOAD");
+  if (opt->link_mode == TOKENSIM_LINK_PRELOAD && m.num_layers > 2000)
+    return fail(nullptr, TOKENSIM_E_INVALID, "model.num_layers: at most 2000 with a PRELOAD link");
   if (opt->topology == TOKENSIM_PD_PAIR) {
     const u32 x = opt->pd_prefill_workers ? opt->pd_prefill_workers : 1u;
     const u32 y = opt->pd_decode_workers ? opt->pd_decode_workers : 1u;
@@ -650,6 +655,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.pd_x = h->pd_x;
   P.pd_y = h->pd_y;
   P.dispatch = h->opt.dispatch;
+  P.link_mode = h->opt.link_mode;
+  P.preload_buf = h->opt.preload_buffer_bytes;
   P.pd_general = h->pd_general ? 1u : 0u;
   P.evlog = reinterpret_cast<uint4 *>(ws + L.evlog);
   P.itlog = reinterpret_cast<ulonglong2 *>(ws + L.itlog);

@@ -29,10 +29,17 @@ struct CostK {
   double h, q2g, hq2g, qh, q, q4, hfu, fu, fh, f, Vh, V, s, att_tok, g2, L, twoL, bar_coef;
   double invF, invB, invH, invT, overhead;
   u32 tp;
+  u32 preload;      // NEXT-4: swap-in through a preload buffer (reading R-N4)
+  u64 preload_buf;  // buffer bytes
+  u64 Lu;           // layers (chunks of a swap-in)
 };
 
-__device__ __forceinline__ CostK make_costk(const DevModel &M, const DevHw &H) {
+__device__ __forceinline__ CostK make_costk(const DevModel &M, const DevHw &H, u32 link_mode = 0,
+                                            u64 preload_buf = 0) {
   CostK K;
+  K.preload = link_mode == TOKENSIM_LINK_PRELOAD ? 1u : 0u;
+  K.preload_buf = preload_buf;
+  K.Lu = M.L;
   K.h = __ull2double_rn(M.h);
   K.q2g = __ull2double_rn(M.q2g);
   K.hq2g = __ull2double_rn(M.hq2g);
@@ -64,11 +71,29 @@ __device__ __forceinline__ double roof(double F, double B, const CostK &K) {
   return fmax(__dmul_rn(F, K.invF), __dmul_rn(B, K.invB));
 }
 
+// NEXT-4 preload pipeline (reading R-N4), lane 0 only: n chunks, load `a`
+// once the previous load is done and a buffer slot is free (chunk i-K taken), the consumer takes
+// chunk i at S_i = max(C_{i-1}, P_i) and finishes it `b` later; ring holds S_1..S_n.
+__device__ __noinline__ double preload_pipeline(u64 n, double a, double b, u64 K, double *ring) {
+  double Pv = 0.0, Cv = 0.0;
+  for (u64 i = 1; i <= n; ++i) {
+    double ready = Pv;
+    if (i > K) ready = fmax(ready, ring[i - K]);
+    Pv = __dadd_rn(ready, a);
+    const double Sv = fmax(Cv, Pv);
+    ring[i] = Sv;
+    Cv = __dadd_rn(Sv, b);
+  }
+  return Cv;
+}
+
 // T_ns of a batch from its exact aggregates; SURVEY c.5 order.  Np = sum of prefill lengths,
 // Ap = sum of P*c0 + P(P+1)/2, Kp = sum of c0 + P (keys a prefill reads), Slm = LM-head rows of
-// the prefill entries (a non-final chunk samples nothing, reading R-N3b).
+// the prefill entries (a non-final chunk samples nothing, reading R-N3b).  With a preload link
+// and swap_in > 0 (warp-collective then; `ring` = >= L+1 doubles of scratch) the swap-in
+// streams layer by layer through the buffer while the layers compute (reading R-N4).
 __device__ __forceinline__ i64 iter_time_chunk_ns(const CostK &K, u64 Np, u64 Ap, u64 Kp, u64 Slm, u64 D,
-                                                  u64 Cd, u64 swap_bytes) {
+                                                  u64 Cd, u64 swap_out, u64 swap_in = 0, double *ring = nullptr) {
   const double N = __ull2double_rn(Np + D), S = __ull2double_rn(Slm + D);
   double tQKV = 0.0, tATTP = 0.0, tATTD = 0.0, tO = 0.0, tUP = 0.0, tDOWN = 0.0, tLM = 0.0;
   const double N2 = __dmul_rn(2.0, N);
@@ -93,9 +118,21 @@ __device__ __forceinline__ i64 iter_time_chunk_ns(const CostK &K, u64 Np, u64 Ap
                __dmul_rn(K.s, __dadd_rn(__dadd_rn(K.Vh, __dmul_rn(S, K.h)), __dmul_rn(S, K.V))), K);
   const double tl =
       __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(tQKV, tATTP), tATTD), tO), tUP), tDOWN);
-  double T = __dmul_rn(tl, K.L);
+  const bool pipe = K.preload && swap_in > 0;
+  double T;
+  if (pipe) {
+    const u64 chunk = swap_in / K.Lu;  // exact: kvb has a factor L
+    const u64 q = K.preload_buf / chunk;
+    double c = 0.0;
+    if (lane_id() == 0)
+      c = preload_pipeline(K.Lu, __dmul_rn(__ull2double_rn(chunk), K.invH), tl, q ? q : 1ull, ring);
+    T = __shfl_sync(FULLMASK, c, 0);
+  } else {
+    T = __dmul_rn(tl, K.L);
+  }
   T = __dadd_rn(T, tLM);
   if (K.tp > 1) T = __dadd_rn(T, __dmul_rn(__dmul_rn(__dmul_rn(K.bar_coef, N), K.invT), K.twoL));
+  const u64 swap_bytes = pipe ? swap_out : swap_out + swap_in;
   if (swap_bytes > 0) T = __dadd_rn(T, __dmul_rn(__ull2double_rn(swap_bytes), K.invH));
   T = __dadd_rn(T, K.overhead);
   return (i64)floor(__dadd_rn(__dmul_rn(T, 1e9), 0.5));
@@ -411,7 +448,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const DevHw H = P.hw[cd.hw];
   const DevHP HP = P.hp[(size_t)cd.hw * P.n_pol + cd.pol];
   const DevPol PL = P.pol[cd.pol];
-  const CostK K = make_costk(P.M, H);
+  const CostK K = make_costk(P.M, H, P.link_mode, P.preload_buf);
   const u32 g = P.group_of_point_mode ? 0u : cd.rate * P.n_seeds + cd.seed;
   const u32 n = P.n_req;
   const i64 *A = P.arrival + (size_t)g * n;
@@ -1187,7 +1224,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         Slm = __reduce_add_sync(FULLMASK, semit);
       }
     }
-    const i64 T = iter_time_chunk_ns(K, Np, Ap, Kp, Slm, D, Cd, swap_out + swap_in);
+    if (K.preload && swap_in > 0) ev_flush(L);  // the event log doubles as the pipeline's scratch
+    const i64 T = iter_time_chunk_ns(K, Np, Ap, Kp, Slm, D, Cd, swap_out, swap_in, reinterpret_cast<double *>(L.ev));
     NPH(4);
     // 8. commit
     const i64 ts = t, te = t + T;

@@ -137,7 +137,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
   const DevHP HPD = P.hp[(size_t)hwD * P.n_pol + cd.pol];
   const DevPol PL = P.pol[cd.pol];
   const CostK KP = make_costk(P.M, P.hw[hwP]);
-  const CostK KD = make_costk(P.M, P.hw[hwD]);
+  const CostK KD = make_costk(P.M, P.hw[hwD], P.link_mode, P.preload_buf);
   const u32 g = P.group_of_point_mode ? 0u : cd.rate * P.n_seeds + cd.seed;
   const u32 n = P.n_req;
   const i64 *A = P.arrival + (size_t)g * n;
@@ -781,7 +781,8 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
         Np = warp_sum64(npp);
         Ap = warp_sum64(app);
       }
-      const i64 T = iter_time_ns(KD, Np, Ap, nrecomp, Dn, Cd, swap_out + swap_in);
+      if (KD.preload && swap_in > 0) ev_flush(L);  // the event log doubles as the pipeline's scratch
+      const i64 T = iter_time_chunk_ns(KD, Np, Ap, Np, nrecomp, Dn, Cd, swap_out, swap_in, reinterpret_cast<double *>(L.ev));
       const i64 te = t + T;
       const u64 blocks = totD - nfreeD;
       // 8. commit

@@ -110,6 +110,8 @@ struct SweepParams {
   unsigned char *pdn_scratch;  // NEXT-1 node: per-warp FIFOs, queues, holders, P block lists
   u64 pdn_bytes_per_warp;
   u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
+  u32 link_mode, pad2;                    // NEXT-4: TOKENSIM_LINK_SEQUENTIAL | PRELOAD
+  u64 preload_buf;                        // preload buffer bytes
   uint4 *evlog;            // per-warp block-event log [warp][1024]
   ulonglong2 *itlog;       // per-warp iteration log [warp][256][4]
 };

@@ -375,3 +375,29 @@ def test_node_sharegpt_grid(api):
             if d == si.LEAST_MEMORY:
                 off = run_gpu(api, replace(cfg, options=replace(cfg.options, fast_forward=False)))
                 assert sw.summaries().tobytes() == off.summaries().tobytes()
+
+
+# ------------------------------------------------------------------ NEXT-4 preload-buffer link
+def test_preload_link_parity(api):
+    """PRELOAD swap-in pipeline (reading R-N4) on the unified worker, the P/D pair and a node:
+    SWAP-heavy micro configs and a memory-pressure grid vs the oracle."""
+    rng = np.random.default_rng(61)
+    for it in range(30):
+        c = _micro(rng)
+        c = replace(c, policies=[replace(c.policies[0], preempt=si.SWAP)],
+                    options=replace(c.options, link_mode=si.PRELOAD,
+                                    preload_buffer_bytes=int(rng.choice([1, 1 << 14, 1 << 20, 1 << 34]))))
+        check_points(run_gpu(api, c), c, [0], records=True, trace=True, iters=True)
+    pols = [si.Policy(kind=si.CONT, preempt=si.SWAP), si.Policy(kind=si.STATIC, preempt=si.SWAP)]
+    cfg = si.SweepConfig("pressure", si.LLAMA2_13B, [si.Hw(mem_capacity=30 * 10 ** 9), si.A100], pols,
+                         si.Workload(300, [4.0, 16.0], [0, 1]),
+                         si.Options(link_mode=si.PRELOAD, preload_buffer_bytes=64 << 20))
+    sw = run_gpu(api, cfg)
+    check_points(sw, cfg, list(range(cfg.num_points)), records=True, trace=True)
+    assert sw.summaries()["swap_in_bytes"].sum() > 0
+    for x, y in ((1, 1), (2, 3)):
+        c = _micro_pd(rng)
+        c = replace(c, policies=[replace(c.policies[0], preempt=si.SWAP)],
+                    options=replace(c.options, pd_prefill=x, pd_decode=y, link_mode=si.PRELOAD,
+                                    preload_buffer_bytes=1 << 16))
+        check_pd_points(run_gpu(api, c), c, list(range(c.num_points)), iters=True)

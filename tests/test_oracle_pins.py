@@ -883,3 +883,104 @@ def test_node_invariants_random(oracle_lib):
             assert (k == np.arange(len(k))).all()
         assert len(r["trace"]) == x + y
         assert s["total_blocks"] == y * O.derive(cfg, 1, 1)["total_blocks"]
+
+
+# ------------------------------------------------------------------ NEXT-4 preload-buffer link
+def _brute_pipeline(n, a, b, K):
+    """Tick-by-tick simulation of a producer/consumer pair with a K-chunk buffer (integer
+    durations): a chunk occupies a slot from its load start until the consumer takes it; at each
+    tick finished work completes first, then the consumer takes the next loaded chunk, then the
+    producer starts the next load if a slot is free."""
+    t = 0
+    loaded = 0            # chunks fully loaded
+    taken = 0             # chunks the consumer has started
+    load_end = None       # end tick of the load in progress
+    cons_end = None       # end tick of the chunk being consumed
+    done = 0
+    while done < n:
+        if load_end is not None and load_end == t:
+            loaded += 1
+            load_end = None
+        if cons_end is not None and cons_end == t:
+            done += 1
+            cons_end = None
+        if cons_end is None and taken < loaded:
+            taken += 1
+            cons_end = t + b
+        in_buf = loaded - taken + (1 if load_end is not None else 0)
+        started = loaded + (1 if load_end is not None else 0)
+        if load_end is None and started < n and in_buf < K:
+            load_end = t + a
+        if done == n:
+            return t
+        t += 1
+    return t
+
+
+def test_preload_pipeline_brute_force(oracle_lib):
+    """S:444 property test: the oracle's pipeline recurrence equals a step-by-step simulation."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(8)
+    for _ in range(400):
+        n, a, b, K = (int(rng.integers(1, 12)), int(rng.integers(1, 9)), int(rng.integers(1, 9)),
+                      int(rng.integers(1, 14)))
+        assert O.pipeline(n, float(a), float(b), K) == _brute_pipeline(n, a, b, K), (n, a, b, K)
+
+
+def test_preload_pipeline_closed_forms(oracle_lib):
+    """Buffer >= all chunks: the producer never stalls and the two-machine flow shop gives
+    max_i(i*a + (n-i+1)*b); one slot with a slower consumer: a + n*b (consumer-governed, S:439);
+    with a slower link: n*a + b."""
+    from oracle import oracle as O
+    for n, a, b in ((32, 3.0, 5.0), (32, 5.0, 3.0), (80, 1.0, 1.0), (7, 2.0, 9.0)):
+        assert O.pipeline(n, a, b, n) == max(i * a + (n - i + 1) * b for i in range(1, n + 1))
+        one = O.pipeline(n, a, b, 1)
+        assert one == (a + n * b if a <= b else n * a + b)
+        assert one <= n * (a + b)
+
+
+def test_preload_iteration_never_slower(oracle_lib):
+    """with swap-in the PRELOAD iteration is never slower than SEQUENTIAL and is
+    non-increasing in the buffer size (strictly faster with a large buffer); without swap-in the
+    two modes agree (the swap-out stays serial)."""
+    from oracle import oracle as O
+    m = si.LLAMA2_13B
+    hw = si.Hw(mem_capacity=40 * 10 ** 9, host_link_bw=16e9)
+    seq = _one(m, hw)
+    L = m.num_layers
+    kvb = 2 * L * m.num_kv_heads * m.head_dim * 2
+    for blocks in (1, 7, 64):
+        swap_in = blocks * 16 * kvb
+        t_seq = O.iter_time_ns(seq, [], [300] * 20, 0, swap_in=swap_in)
+        prev = t_seq
+        for buf in (1, swap_in // L, 4 * swap_in // L, swap_in, 1 << 40):
+            c = replace(seq, options=replace(seq.options, link_mode=si.PRELOAD, preload_buffer_bytes=buf))
+            t = O.iter_time_ns(c, [], [300] * 20, 0, swap_in=swap_in)
+            assert t <= prev + 1
+            prev = t
+        big = replace(seq, options=replace(seq.options, link_mode=si.PRELOAD, preload_buffer_bytes=1 << 40))
+        t_big = O.iter_time_ns(big, [], [300] * 20, 0, swap_in=swap_in)
+        assert t_big < t_seq
+        c0 = replace(seq, options=replace(seq.options, link_mode=si.PRELOAD, preload_buffer_bytes=1))
+        assert O.iter_time_ns(c0, [(64, 0)], [300] * 20, 4096) == O.iter_time_ns(seq, [(64, 0)], [300] * 20, 4096)
+
+
+def test_preload_simulation_invariants(oracle_lib):
+    """Random SWAP-heavy micro configs under a PRELOAD link: the c.8 invariants hold, and a
+    config that never swaps in runs exactly as under SEQUENTIAL."""
+    rng = np.random.default_rng(909)
+    differs = 0
+    for _ in range(60):
+        cfg, o = _random_micro(rng)
+        cfg = replace(cfg, policies=[replace(cfg.policies[0], preempt=si.SWAP)])
+        pre = replace(cfg, options=replace(cfg.options, link_mode=si.PRELOAD,
+                                           preload_buffer_bytes=int(rng.choice([1, 1 << 16, 1 << 30]))))
+        a = _sim(cfg, want=("summary", "records"))
+        b = _sim(pre, want=("summary", "records"))
+        s = b["summary"]
+        assert s["n_finished"] + s["n_rejected"] == len(o)
+        if a["summary"]["swap_in_bytes"] == 0:
+            assert a["records"].tobytes() == b["records"].tobytes()
+        else:
+            differs += a["records"].tobytes() != b["records"].tobytes()
+    assert differs > 0
