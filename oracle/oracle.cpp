@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <list>
 #include <map>
 #include <set>
 #include <string>
@@ -276,7 +277,7 @@ CostCtx cost_ctx(const oracle_cfg &c, const oracle_derived &d, int decode_worker
 }
 
 i64 iter_time(const CostCtx &K, const std::vector<Prefill> &pf, const std::vector<u64> &dec,
-              u64 swap_out, u64 swap_in = 0) {
+              u64 swap_out, u64 swap_in = 0, u64 fetch_blocks = 0, double fetch_s = 0.0) {
   u64 Np = 0, Ap = 0, Kp = 0, Cd = 0, Sp = 0;
   const u64 D = dec.size();
   for (const Prefill &e : pf) {
@@ -323,6 +324,7 @@ i64 iter_time(const CostCtx &K, const std::vector<Prefill> &pf, const std::vecto
     const double sw = (double)swap_bytes * K.invH;
     T = T + sw;
   }
+  if (fetch_blocks > 0) T = T + (double)fetch_blocks * fetch_s;  // NEXT-2 cache hits
   T = T + K.overhead;
   const double Tn = T * 1e9;
   return (i64)std::floor(Tn + 0.5);
@@ -1816,6 +1818,475 @@ oracle_run *simulate_pdn(const oracle_cfg &c) {
   return run;
 }
 
+// ----------------------------------------------------------------- NEXT-2 multi-round workload
+// SURVEY §8(f) NEXT-2 and reading R-N2 in DESIGN.md.  num_requests conversations
+// arrive as the a.1 Poisson stream (round 0 uses the a.1 draws).  Y2 gives the round count: top
+// bit 0 -> 1 round (probability 1/2), else 2 + floor(low31 * 6 / 2^31) in {2..7}.  Round r >= 1
+// draws Z = philox((c, 2, r, 0)): think gap -det_log(u(Z0, Z1)) * think_mean, new-turn prompt
+// length from (Z2, Z3); W = philox((c, 3, r, 0)): output length from (W0, W1).  Its prompt is the
+// prior context plus the new turn, P_r = P_{r-1} + o_{r-1} + q_r; a round with P_r + 1 > mml ends
+// the conversation; o_r = min(o_r, mml - P_r).  Request rid = base_c + r, in conversation order.
+struct Rounds {
+  std::vector<i64> at;  // round 0: arrival; round r >= 1: think gap after round r-1 finishes
+  std::vector<u32> P, O, conv;
+  std::vector<u32> base, nr;
+};
+
+u32 draw_len(const oracle_cfg &c, bool prompt, u32 w0, u32 w1) {
+  if (c.len_dist == OR_LEN_FIXED) return prompt ? c.prompt_a : c.output_a;
+  if (c.len_dist == OR_LEN_UNIFORM) {
+    const u32 a = prompt ? c.prompt_a : c.output_a, b = prompt ? c.prompt_b : c.output_b;
+    return a + (u32)(((u64)w0 * (u64)(b - a + 1)) >> 32);
+  }
+  return prompt ? table_draw(c.pt_n, c.pt_lo, c.pt_hi, c.pt_thr, w0, w1)
+                : table_draw(c.ot_n, c.ot_lo, c.ot_hi, c.ot_thr, w0, w1);
+}
+
+bool workload_rounds(const oracle_cfg &c, Rounds &W) {
+  if (c.len_dist == OR_LEN_TRACE) return fail("multi-round workloads need generated lengths (not TRACE)");
+  std::vector<i64> A;
+  std::vector<u32> Pl, Ol;
+  if (!workload(c, A, Pl, Ol)) return false;  // round 0 = the a.1 stream
+  const u32 n = c.num_requests;
+  const u32 key[2] = {(u32)(c.seed & 0xffffffffu), (u32)(c.seed >> 32)};
+  const double think_ns = c.think_mean_s * 1e9;
+  W = Rounds();
+  W.base.assign(n, 0);
+  W.nr.assign(n, 0);
+  for (u32 i = 0; i < n; ++i) {
+    const u32 cy[4] = {i, 1, 0, 0};
+    u32 Y[4];
+    philox(cy, key, Y);
+    const u32 R = (Y[2] >> 31) == 0 ? 1u : 2u + (u32)(((u64)(Y[2] & 0x7fffffffu) * 6u) >> 31);
+    W.base[i] = (u32)W.P.size();
+    W.at.push_back(A[i]);
+    W.P.push_back(Pl[i]);
+    W.O.push_back(Ol[i]);
+    W.conv.push_back(i);
+    u64 prevP = Pl[i], prevO = Ol[i];
+    u32 made = 1;
+    for (u32 r = 1; r < R; ++r) {
+      const u32 cz[4] = {i, 2, r, 0}, cw[4] = {i, 3, r, 0};
+      u32 Z[4], Wd[4];
+      philox(cz, key, Z);
+      philox(cw, key, Wd);
+      const u64 v = ((u64)Z[0] << 21) | (u64)(Z[1] >> 11);
+      const double u = (double)(v + 1) * 0x1p-53;
+      const double E = -det_log(u);
+      const i64 gap = (i64)std::floor(E * think_ns + 0.5);
+      const u64 q = draw_len(c, true, Z[2], Z[3]);
+      u64 o = draw_len(c, false, Wd[0], Wd[1]);
+      const u64 Pr = prevP + prevO + q;
+      if (Pr + 1 > c.max_model_len) break;  // the context no longer fits: the conversation ends
+      if (o > c.max_model_len - Pr) o = c.max_model_len - Pr;
+      W.at.push_back(gap);
+      W.P.push_back((u32)Pr);
+      W.O.push_back((u32)o);
+      W.conv.push_back(i);
+      prevP = Pr;
+      prevO = o;
+      ++made;
+    }
+    W.nr[i] = made;
+  }
+  return true;
+}
+
+// ----------------------------------------------------------------- NEXT-2 simulation
+// The c.4 unified loop (MIXED) over a dynamic request stream: round 0 of conversation c arrives
+// at its a.1 time, round r >= 1 at (finish of round r-1) + its think gap.  Arrived requests queue
+// FCFS by (arrival time, conversation); "id order" (victims, resumes, requesters) is arrival
+// order.  With the memory cache: a finishing round stores its context (P + o - 1
+// tokens with KV) for its conversation as the most recently used entry of a host LRU cache of
+// capacity blocks (evicting least recently used entries); admitting round r >= 1 whose
+// conversation is cached is a hit: its prefill is the (P - c0, c0) row with c0 = the cached
+// tokens, the entry becomes most recently used, and the iteration pays 800 ns per cached block
+// before the prefill.  Reading R-N2.
+oracle_run *simulate_mr(const oracle_cfg &c) {
+  if (c.iter_mode != OR_MIXED) {
+    g_err = "multi-round workloads run MIXED iterations";
+    return nullptr;
+  }
+  oracle_derived d;
+  if (!derive(c, 0, d)) return nullptr;
+  CostCtx K = cost_ctx(c, d, 0);
+  Rounds Wr;
+  if (!workload_rounds(c, Wr)) return nullptr;
+  const u32 nconv = c.num_requests;
+  const u32 n = (u32)Wr.P.size();
+  const u64 bs = c.block_size, total = d.total_blocks;
+  const bool SWAPM = c.preempt == OR_SWAP;
+  const bool RATIO = c.kind == OR_CONT_RATIO;
+  const bool CACHE = c.memory_cache != 0;
+  const u64 cache_cap = c.cache_capacity_blocks ? c.cache_capacity_blocks : 4 * total;
+  const double fetch_s = c.cache_fetch_ns_per_block * 1e-9;
+
+  std::vector<Req> req(n);
+  for (u32 i = 0; i < n; ++i) {
+    req[i].p = Wr.P[i];
+    req[i].o = Wr.O[i];
+  }
+  oracle_run *run = new oracle_run();
+  std::memset(&run->summary, 0, sizeof(run->summary));
+  oracle_summary &S = run->summary;
+  std::set<u32> freeset;
+  for (u64 b = 0; b < total; ++b) freeset.insert((u32)b);
+  std::vector<u32> seq2rid;        // arrival sequence -> request
+  std::set<u32> R, Q;              // arrival sequence numbers
+  std::deque<u32> waitq;           // arrived, not admitted (arrival sequence order)
+  std::set<std::pair<i64, u32>> pend;  // follow-up rounds: (arrival time, conversation)
+  std::vector<u32> next_round(nconv, 0);
+  std::vector<u32> seq_of(n, 0);
+  // host LRU cache: conversation -> cached tokens; front = least recently used
+  std::list<u32> lru;
+  std::map<u32, std::pair<u64, std::list<u32>::iterator>> cache;
+  u64 cache_used = 0;
+  u32 next0 = 0;  // next conversation whose round 0 has not arrived
+  i64 t = 0;
+  u64 k = 0;
+  u32 n_done = 0;
+  u64 sched_d = 0, block_d = 0, req_d = 0;
+  u64 req_iters = 0, n_preempt_total = 0, swap_out_total = 0, swap_in_total = 0;
+  u64 peak = 0, block_ns_sum = 0, n_rej_total = 0;
+
+  auto alloc_lowest = [&](u32 rid, u64 cnt) {
+    for (u64 j = 0; j < cnt; ++j) {
+      const u32 b = *freeset.begin();
+      freeset.erase(freeset.begin());
+      req[rid].blocks.push_back(b);
+      block_d += fold({k, 1, rid, b});
+      if (c.keep_events) run->events.push_back({k, 1, rid, b, 0});
+    }
+  };
+  auto free_all = [&](u32 rid) {
+    for (u32 b : req[rid].blocks) {
+      freeset.insert(b);
+      block_d += fold({k, 2, rid, b});
+      if (c.keep_events) run->events.push_back({k, 2, rid, b, 0});
+    }
+    req[rid].blocks.clear();
+  };
+  auto cache_touch = [&](u32 cv) {  // make most recently used
+    auto it = cache.find(cv);
+    lru.erase(it->second.second);
+    lru.push_back(cv);
+    it->second.second = std::prev(lru.end());
+  };
+  auto cache_store = [&](u32 cv, u64 tokens) {
+    const u64 blk = ceil_div(tokens, bs);
+    auto it = cache.find(cv);
+    if (it != cache.end()) {
+      cache_used -= ceil_div(it->second.first, bs);
+      lru.erase(it->second.second);
+      cache.erase(it);
+    }
+    if (blk > cache_cap) return;  // larger than the whole cache: not stored
+    lru.push_back(cv);
+    cache[cv] = {tokens, std::prev(lru.end())};
+    cache_used += blk;
+    while (cache_used > cache_cap) {  // evict least recently used
+      const u32 ev = lru.front();
+      lru.pop_front();
+      cache_used -= ceil_div(cache[ev].first, bs);
+      cache.erase(ev);
+    }
+  };
+  // the next arrival: (time, conversation, round)
+  auto next_arrival = [&](i64 &ta, u32 &cv) -> bool {
+    ta = INT64_MAX;
+    bool any = false;
+    if (next0 < nconv) {
+      ta = Wr.at[Wr.base[next0]];
+      cv = next0;
+      any = true;
+    }
+    if (!pend.empty()) {
+      const auto &e = *pend.begin();
+      if (!any || e.first < ta || (e.first == ta && e.second < cv)) {
+        ta = e.first;
+        cv = e.second;
+        any = true;
+      }
+    }
+    return any;
+  };
+
+  while (true) {
+    if (n_done == n) break;
+    if (c.horizon_ns >= 0 && t >= c.horizon_ns) {
+      S.status_flags |= 4;
+      break;
+    }
+    // 1. ingest: arrivals at or before t join the FCFS queue in (time, conversation) order
+    {
+      i64 ta;
+      u32 cv;
+      while (next_arrival(ta, cv) && ta <= t) {
+        const u32 r = next_round[cv];
+        const u32 rid = Wr.base[cv] + r;
+        if (r == 0) ++next0;
+        else pend.erase(pend.begin());
+        req[rid].a = ta;
+        seq_of[rid] = (u32)seq2rid.size();
+        seq2rid.push_back(rid);
+        waitq.push_back(seq_of[rid]);
+      }
+    }
+    // 2. idle skip
+    if (R.empty() && Q.empty() && waitq.empty()) {
+      i64 ta;
+      u32 cv;
+      if (!next_arrival(ta, cv)) {
+        g_err = "multi-round: nothing left to arrive but requests unresolved";
+        delete run;
+        return nullptr;
+      }
+      t = ta;
+      continue;
+    }
+    std::map<u32, Kind> kind;  // by arrival sequence
+    std::map<u32, u64> c0_of;  // cache-hit prefix of fresh entries
+    u64 n_res = 0, n_adm = 0, n_rej = 0, swap_in = 0, m = 0, swap_out = 0, fetch_blocks = 0;
+    // 3. decode reservation + preemption (victims: latest arrivals)
+    const u64 F = freeset.size();
+    std::vector<u32> Rv(R.begin(), R.end());
+    auto rid_of = [&](u32 s) { return seq2rid[s]; };
+    auto need_of = [&](u32 s) -> u64 { return (req[rid_of(s)].ctx % bs == 0) ? 1 : 0; };
+    u64 sum_need = 0;
+    for (u32 s : Rv) sum_need += need_of(s);
+    if (sum_need > F) {
+      const u64 nr = Rv.size();
+      for (m = 1; m <= nr; ++m) {
+        u64 lhs = 0, rhs = F;
+        for (u64 j = 0; j < nr - m; ++j) lhs += need_of(Rv[j]);
+        for (u64 j = nr - m; j < nr; ++j) rhs += req[rid_of(Rv[j])].blocks.size();
+        if (lhs <= rhs) break;
+      }
+      if (m >= nr) {
+        g_err = "preemption would evict r_1 (validation should make this impossible)";
+        delete run;
+        return nullptr;
+      }
+      for (u64 i = 0; i < m; ++i) {
+        const u32 s = Rv[nr - 1 - i];
+        Req &x = req[rid_of(s)];
+        const u64 held = x.blocks.size();
+        free_all(rid_of(s));
+        x.n_preempt += 1;
+        if (SWAPM) swap_out += held * d.block_bytes;
+        else x.ctx = 0;
+        R.erase(s);
+        Q.insert(s);
+      }
+      n_preempt_total += m;
+    }
+    for (u32 s : R) {
+      kind[s] = K_DEC;
+      if (need_of(s)) alloc_lowest(rid_of(s), 1);
+    }
+    u64 tokens = R.size();
+    if (m == 0) {
+      // 4. resume, head first
+      std::vector<u32> Qv(Q.begin(), Q.end());
+      for (u32 s : Qv) {
+        Req &x = req[rid_of(s)];
+        u64 need, tok;
+        if (SWAPM) {
+          need = ceil_div(x.ctx, bs) + ((x.ctx % bs == 0) ? 1 : 0);
+          tok = 1;
+        } else {
+          need = ceil_div(x.p + x.gen, bs);
+          tok = x.p + x.gen;
+        }
+        const bool ok = (R.size() + 1 <= c.max_num_seqs) && (tokens + tok <= c.max_batched_tokens) &&
+                        ((i64)freeset.size() - (i64)need >= (i64)c.watermark_blocks);
+        if (!ok) break;
+        alloc_lowest(rid_of(s), need);
+        Q.erase(s);
+        R.insert(s);
+        ++n_res;
+        tokens += tok;
+        if (SWAPM) {
+          swap_in += ceil_div(x.ctx, bs) * d.block_bytes;
+          kind[s] = K_DEC;
+        } else {
+          kind[s] = K_PRE_RECOMP;
+        }
+      }
+      // 5. fresh FCFS admission over the arrival queue, with cache lookups
+      if (Q.empty() && (c.kind != OR_STATIC || R.empty())) {
+        while (!waitq.empty()) {
+          const u32 s = waitq.front();
+          const u32 rid = rid_of(s);
+          Req &x = req[rid];
+          const u64 need = ceil_div(x.p, bs);
+          const u64 cap = RATIO ? d.ratio_limit : total - c.watermark_blocks;
+          if (need > cap) {  // rejected; its conversation's later rounds never arrive
+            const u32 cv = Wr.conv[rid];
+            const u32 last = Wr.base[cv] + Wr.nr[cv];
+            for (u32 q = rid; q < last; ++q) {
+              req[q].status = 2;
+              ++n_rej;
+              ++n_done;
+            }
+            waitq.pop_front();
+            continue;
+          }
+          const u64 fr = freeset.size();
+          if (R.size() + 1 > c.max_num_seqs) break;
+          if (tokens + x.p > c.max_batched_tokens) break;
+          if ((i64)fr - (i64)need < (i64)c.watermark_blocks) break;
+          if (RATIO && (total - fr) + need > d.ratio_limit) break;
+          alloc_lowest(rid, need);
+          R.insert(s);
+          kind[s] = K_PRE_FRESH;
+          tokens += x.p;
+          ++n_adm;
+          waitq.pop_front();
+          u64 c0 = 0;
+          const u32 cv = Wr.conv[rid];
+          if (CACHE && rid > Wr.base[cv]) {
+            auto it = cache.find(cv);
+            if (it != cache.end()) {  // hit
+              c0 = it->second.first;
+              fetch_blocks += ceil_div(c0, bs);
+              cache_touch(cv);
+            }
+          }
+          c0_of[s] = c0;
+        }
+      }
+    }
+    n_rej_total += n_rej;
+    if (kind.empty()) continue;
+    // 7. cost
+    std::vector<Prefill> pf;
+    std::vector<u64> dec;
+    u64 Np = 0, Cd = 0;
+    for (const auto &kv : kind) {
+      const Req &x = req[rid_of(kv.first)];
+      if (kv.second == K_DEC) {
+        dec.push_back(x.ctx + 1);
+        Cd += x.ctx + 1;
+      } else if (kv.second == K_PRE_FRESH) {
+        const u64 c0 = c0_of[kv.first];
+        pf.push_back({x.p - c0, c0});
+        Np += x.p - c0;
+      } else {
+        pf.push_back({x.p + x.gen, 0});
+        Np += x.p + x.gen;
+      }
+    }
+    const i64 T = iter_time(K, pf, dec, swap_out, swap_in, fetch_blocks, fetch_s);
+    // 8. commit
+    const i64 ts = t, te = t + T;
+    const u64 blocks = total - freeset.size();
+    const u64 entries = kind.size();
+    u64 n_fin = 0;
+    for (const auto &kv : kind) {
+      const u32 s = kv.first;
+      const u32 rid = rid_of(s);
+      Req &x = req[rid];
+      if (kv.second == K_PRE_FRESH) {
+        x.ctx = x.p;
+        x.gen = 1;
+        x.first_tok = te;
+        x.last_tok = te;
+      } else {
+        if (kv.second == K_PRE_RECOMP) {
+          x.ctx = x.p + x.gen;
+          x.gen += 1;
+        } else {
+          x.ctx += 1;
+          x.gen += 1;
+        }
+        const i64 gap = te - x.last_tok;
+        x.max_gap = std::max(x.max_gap, gap);
+        x.last_tok = te;
+      }
+      if (x.gen == x.o) {
+        x.status = 1;
+        x.finish = te;
+        x.finish_k = k;
+        req_d += fold({rid, (u64)(x.first_tok - x.a), (u64)(x.finish - x.a), (u64)x.max_gap, x.n_preempt, k});
+        free_all(rid);
+        R.erase(s);
+        ++n_fin;
+        ++n_done;
+        const u32 cv = Wr.conv[rid];
+        if (CACHE) cache_store(cv, (u64)x.p + x.o - 1);
+        const u32 r = rid - Wr.base[cv];
+        if (r + 1 < Wr.nr[cv]) {
+          next_round[cv] = r + 1;
+          pend.insert({te + Wr.at[rid + 1], cv});
+        }
+      }
+    }
+    sched_d += fold({k, (u64)ts, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej, n_fin, blocks});
+    run->iters.push_back({k, ts, T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej, n_fin, blocks, 0, 0});
+    req_iters += entries;
+    peak = std::max(peak, blocks);
+    block_ns_sum += blocks * (u64)T;
+    swap_out_total += swap_out;
+    swap_in_total += swap_in;
+    t = te;
+    ++k;
+    if (c.check_invariants) {
+      std::set<u32> Rr, Qr;
+      for (u32 s : R) Rr.insert(rid_of(s));
+      for (u32 s : Q) Qr.insert(rid_of(s));
+      if (!check_invariants(req, Rr, Qr, freeset, total, bs)) {
+        delete run;
+        return nullptr;
+      }
+      u64 used = 0;
+      for (const auto &e : cache) used += ceil_div(e.second.first, bs);
+      if (used != cache_used || cache_used > cache_cap) {
+        g_err = "memory cache accounting";
+        delete run;
+        return nullptr;
+      }
+    }
+  }
+
+  run->records.resize(n);
+  u64 n_fin = 0;
+  for (u32 i = 0; i < n; ++i) {
+    const Req &x = req[i];
+    oracle_record &rec = run->records[i];
+    rec.ttft_ns = (x.gen >= 1 || x.status == 1) ? x.first_tok - x.a : 0;
+    rec.e2e_ns = x.status == 1 ? x.finish - x.a : 0;
+    rec.mtpot_ns = x.status == 1 ? x.max_gap : 0;
+    rec.n_preempt = x.n_preempt;
+    rec.status = x.status;
+    rec.finish_k = x.status == 1 ? x.finish_k : 0;
+    if (x.status == 1) ++n_fin;
+  }
+  S.n_requests = n;
+  S.n_finished = n_fin;
+  S.n_rejected = n_rej_total;
+  S.n_unfinished = n - n_fin - n_rej_total;
+  if (n_rej_total == n) S.status_flags |= 2;
+  S.n_iterations = k;
+  S.n_request_iterations = req_iters;
+  S.n_preemptions = n_preempt_total;
+  S.swap_out_bytes = swap_out_total;
+  S.swap_in_bytes = swap_in_total;
+  S.t_final = t;
+  S.sched_digest = sched_d;
+  S.block_digest = block_d;
+  S.request_digest = req_d;
+  S.total_blocks = total;
+  S.peak_blocks = peak;
+  S.block_ns_sum = block_ns_sum;
+  S.mean_util = (t > 0 && total > 0) ? (double)block_ns_sum / ((double)total * (double)t) : 0.0;
+  metrics(c, d, req, S);
+  bool ovf = false;
+  build_trace(c, run->iters, 0, t, run->trace[0], ovf);
+  if (ovf) S.status_flags |= 1;
+  return run;
+}
+
 }  // namespace
 
 // ======================================================================== C ABI
@@ -1856,6 +2327,20 @@ int64_t oracle_iter_time_ns(const oracle_cfg *cfg, int decode_worker, uint32_t n
   return iter_time(K, pf, dec, swap_out, swap_in);
 }
 
+int64_t oracle_workload_rounds(const oracle_cfg *cfg, int64_t *arrival_or_think, uint32_t *prompt,
+                               uint32_t *output, uint32_t *conv) {
+  g_err.clear();
+  Rounds W;
+  if (!workload_rounds(*cfg, W)) return -1;
+  for (size_t i = 0; i < W.P.size(); ++i) {
+    if (arrival_or_think) arrival_or_think[i] = W.at[i];
+    if (prompt) prompt[i] = W.P[i];
+    if (output) output[i] = W.O[i];
+    if (conv) conv[i] = W.conv[i];
+  }
+  return (int64_t)W.P.size();
+}
+
 double oracle_pipeline(uint64_t n_chunks, double a, double b, uint64_t slots) {
   return pipeline(n_chunks, a, b, slots);
 }
@@ -1868,6 +2353,13 @@ uint64_t oracle_fold(const uint64_t *fields, uint32_t n) {
 
 oracle_run *oracle_simulate(const oracle_cfg *cfg) {
   g_err.clear();
+  if (cfg->multi_round) {
+    if (cfg->topology != OR_UNIFIED) {
+      g_err = "multi-round workloads run on the unified topology";
+      return nullptr;
+    }
+    return simulate_mr(*cfg);
+  }
   if (cfg->topology == OR_PD_PAIR) {
     const bool one = (cfg->n_prefill <= 1 && cfg->n_decode <= 1);
     return (one && !cfg->force_general) ? simulate_pd(*cfg) : simulate_pdn(*cfg);

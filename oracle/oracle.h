@@ -75,6 +75,12 @@ typedef struct {
   /* NEXT-4 communication model: swap-in link mode and buffer */
   uint32_t link_mode;            /* OR_LINK_SEQUENTIAL | OR_LINK_PRELOAD */
   uint64_t preload_buffer_bytes;
+  /* NEXT-2 multi-round conversations and host memory cache */
+  uint32_t multi_round;          /* num_requests = conversations of 1..7 rounds */
+  double think_mean_s;
+  uint32_t memory_cache;         /* 1: hits skip the cached prefix at 800 ns/block */
+  uint64_t cache_capacity_blocks;  /* 0 = 4x device KV blocks */
+  double cache_fetch_ns_per_block;
 } oracle_cfg;
 
 typedef struct {
@@ -138,6 +144,12 @@ int64_t oracle_iter_time_ns(const oracle_cfg *cfg, int decode_worker, uint32_t n
    chunks) -- the consumer's finish of the last chunk */
 double oracle_pipeline(uint64_t n_chunks, double a, double b, uint64_t slots);
 uint64_t oracle_fold(const uint64_t *fields, uint32_t n);
+
+/* NEXT-2: the multi-round workload of one point -- per request (conversation c, round r) in id
+   order rid = base_c + r: round-0 arrival (r = 0) or think gap (r >= 1), prompt, output, conv.
+   Returns the number of requests (<= 7 * num_requests), or -1. */
+int64_t oracle_workload_rounds(const oracle_cfg *cfg, int64_t *arrival_or_think, uint32_t *prompt,
+                               uint32_t *output, uint32_t *conv);
 
 /* ---- one point, start to finish ---- */
 oracle_run *oracle_simulate(const oracle_cfg *cfg);      /* NULL on error */

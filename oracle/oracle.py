@@ -66,6 +66,8 @@ class OracleCfg(C.Structure):
         ("check_invariants", u32), ("keep_events", u32), ("iter_mode", u32),
         ("n_prefill", u32), ("n_decode", u32), ("dispatch", u32), ("force_general", u32),
         ("link_mode", u32), ("preload_buffer_bytes", u64),
+        ("multi_round", u32), ("think_mean_s", f64), ("memory_cache", u32), ("cache_capacity_blocks", u64),
+        ("cache_fetch_ns_per_block", f64),
     ]
 
 
@@ -115,6 +117,8 @@ def lib():
         L.oracle_workload.restype = C.c_int
         L.oracle_iter_time_ns.argtypes = [C.POINTER(OracleCfg), C.c_int, u32, PU32, PU32, PU32, u32, PU32, u64, u64]
         L.oracle_pipeline.argtypes = [u64, C.c_double, C.c_double, u64]
+        L.oracle_workload_rounds.argtypes = [C.POINTER(OracleCfg), PI64, PU32, PU32, PU32]
+        L.oracle_workload_rounds.restype = i64
         L.oracle_pipeline.restype = C.c_double
         L.oracle_iter_time_ns.restype = i64
         L.oracle_fold.argtypes = [C.POINTER(u64), u32]
@@ -211,6 +215,9 @@ def make_cfg(cfg: si.SweepConfig, point: int, check_invariants: bool = False,
     c.keep_events = 1 if keep_events else 0
     c.n_prefill, c.n_decode = o.pd_prefill, o.pd_decode
     c.link_mode = {si.SEQUENTIAL: 0, si.PRELOAD: 1}[o.link_mode]
+    c.multi_round, c.think_mean_s = int(w.multi_round), w.think_mean_s
+    c.memory_cache, c.cache_capacity_blocks = int(o.memory_cache), o.cache_capacity_blocks
+    c.cache_fetch_ns_per_block = o.cache_fetch_ns_per_block
     c.preload_buffer_bytes = o.preload_buffer_bytes
     c.dispatch = {si.ROUND_ROBIN: 0, si.LEAST_OUTSTANDING: 1, si.LEAST_MEMORY: 2}[o.dispatch]
     return c, keep
@@ -302,6 +309,22 @@ def workload(cfg: si.SweepConfig, point: int = 0):
                          o.ctypes.data_as(PU32)) != 0:
         raise OracleError(L.oracle_error().decode())
     return a, p, o
+
+
+def workload_rounds(cfg: si.SweepConfig, point: int = 0):
+    """NEXT-2 multi-round stream of one point: (arrival_or_think, prompt, output, conv) per request."""
+    L = lib()
+    c, keep = make_cfg(cfg, point)
+    cap = 7 * c.num_requests
+    a = np.zeros(cap, np.int64)
+    p = np.zeros(cap, np.uint32)
+    o = np.zeros(cap, np.uint32)
+    cv = np.zeros(cap, np.uint32)
+    n = L.oracle_workload_rounds(C.byref(c), a.ctypes.data_as(PI64), p.ctypes.data_as(PU32),
+                                 o.ctypes.data_as(PU32), cv.ctypes.data_as(PU32))
+    if n < 0:
+        raise OracleError(L.oracle_error().decode())
+    return a[:n], p[:n], o[:n], cv[:n]
 
 
 def iter_time_ns(cfg: si.SweepConfig, prefills=(), decodes=(), swap_bytes: int = 0,

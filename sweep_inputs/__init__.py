@@ -126,6 +126,8 @@ class Workload:
     trace_arrival_ns: Optional[Sequence[int]] = None
     trace_prompt: Optional[Sequence[int]] = None
     trace_output: Optional[Sequence[int]] = None
+    multi_round: bool = False          # NEXT-2: num_requests conversations of 1..7 rounds
+    think_mean_s: float = 5.0          # NEXT-2: mean think time between rounds
 
 
 NONE_TRACE, BINNED, FULL = "none", "binned", "full"
@@ -149,6 +151,9 @@ class Options:
     dispatch: str = "round_robin"      # global scheduler: ROUND_ROBIN | LEAST_OUTSTANDING | LEAST_MEMORY
     node_loop: bool = False            # CUDA path only: run a 1P:1D pair through the xP:yD loop
     link_mode: str = "sequential"      # swap-in link: SEQUENTIAL (A10) | PRELOAD (NEXT-4)
+    memory_cache: bool = False         # NEXT-2: host KV cache of conversation contexts
+    cache_capacity_blocks: int = 0     # 0 = 4x the device KV blocks
+    cache_fetch_ns_per_block: float = 800.0
     preload_buffer_bytes: int = 1 << 30  # PRELOAD buffer
 
 

@@ -984,3 +984,138 @@ def test_preload_simulation_invariants(oracle_lib):
         else:
             differs += a["records"].tobytes() != b["records"].tobytes()
     assert differs > 0
+
+
+# ------------------------------------------------------------------ NEXT-2 multi-round + memory cache
+def _mr_cfg(n=1, seed=0, rate=1.0, len_dist=si.FIXED, pa=64, oa=16, cache=True, mml=4096, cap=0,
+            think=5.0, pol=si.Policy(), hw=si.A100, **wkw):
+    w = si.Workload(n, [rate], [seed], len_dist=len_dist, prompt_a=pa, prompt_b=wkw.pop("pb", 0),
+                    output_a=oa, output_b=wkw.pop("ob", 0), multi_round=True, think_mean_s=think, **wkw)
+    return si.SweepConfig("mr", replace(si.LLAMA2_7B, max_model_len=mml), [hw], [pol], w,
+                          si.Options(memory_cache=cache, cache_capacity_blocks=cap))
+
+
+def test_rounds_workload_statistics(oracle_lib):
+    """S:129-133: half the conversations are single-round, the rest uniform over 2..7 rounds;
+    think gaps are Exp(mean 5 s); round r's prompt is the prior context plus a new turn drawn
+    from the prompt distribution; round 0 is exactly the a.1 stream."""
+    from oracle import oracle as O
+    from scipy import stats
+    cfg = _mr_cfg(n=20000, seed=3, len_dist=si.UNIFORM, pa=10, pb=50, oa=5, ob=20, mml=1 << 16)
+    at, P, Oo, cv = O.workload_rounds(cfg)
+    rounds = np.bincount(cv, minlength=20000)
+    single = (rounds == 1).mean()
+    assert abs(single - 0.5) < 5 * math.sqrt(0.25 / 20000)
+    multi = rounds[rounds > 1]
+    cnt = np.bincount(multi, minlength=8)[2:8]
+    assert stats.chisquare(cnt).pvalue > 1e-4
+    first = np.r_[True, cv[1:] != cv[:-1]]
+    a0, p0, o0 = O.workload(cfg)
+    assert (at[first] == a0).all() and (P[first] == p0).all() and (Oo[first] == o0).all()
+    gaps = at[~first] / 1e9
+    assert abs(gaps.mean() - 5.0) / 5.0 < 0.03
+    assert stats.kstest(gaps, "expon", args=(0, 5.0)).pvalue > 1e-4
+    idx = np.nonzero(~first)[0]
+    q = P[idx].astype(np.int64) - P[idx - 1] - Oo[idx - 1]
+    assert q.min() >= 10 and q.max() <= 50 and abs(q.mean() - 30) < 0.5
+    assert ((Oo >= 5) & (Oo <= 20)).all()
+
+
+def test_rounds_context_cap(oracle_lib):
+    """A round whose prompt (prior context + new turn) leaves no room for one output token ends
+    its conversation; every kept round satisfies P + o <= max_model_len."""
+    from oracle import oracle as O
+    cfg = _mr_cfg(n=3000, seed=1, len_dist=si.UNIFORM, pa=100, pb=400, oa=50, ob=300, mml=1024)
+    at, P, Oo, cv = O.workload_rounds(cfg)
+    assert (P.astype(np.int64) + Oo <= 1024).all() and (Oo >= 1).all()
+    rounds = np.bincount(cv)
+    assert rounds.max() < 7    # contexts outgrow 1024 tokens before 7 rounds
+
+
+def _two_round_seed():
+    from oracle import oracle as O
+    for seed in range(200):
+        at, P, Oo, cv = O.workload_rounds(_mr_cfg(seed=seed))
+        if len(P) >= 2:
+            return seed, at, P, Oo
+    raise AssertionError("no multi-round seed")
+
+
+def test_memory_cache_hand_trace(oracle_lib):
+    """One conversation, isolated rounds: round r >= 1 arrives its think gap after round r-1
+    finishes; with the cache its prefill is the (P - c0, c0) row, c0 = P_{r-1} + o_{r-1} - 1, plus
+    800 ns per cached block; without the cache it re-prefills all P tokens."""
+    from oracle import oracle as O
+    seed, at, P, Oo = _two_round_seed()
+    on = _mr_cfg(seed=seed)
+    off = _mr_cfg(seed=seed, cache=False)
+    ron = O.simulate(on, 0, check_invariants=True, want=("summary", "records", "iters"))
+    roff = O.simulate(off, 0, check_invariants=True, want=("summary", "records", "iters"))
+    # round 0 is identical
+    assert ron["records"][0].tobytes() == roff["records"][0].tobytes()
+    c0 = int(P[0] + Oo[0] - 1)
+    t_hit = O.iter_time_ns(on, [(int(P[1]) - c0, c0)], [])
+    t_miss = O.iter_time_ns(off, [(int(P[1]), 0)], [])
+    blocks = -(-c0 // 16)
+    assert abs(ron["records"]["ttft_ns"][1] - (t_hit + 800 * blocks)) <= 1
+    assert roff["records"]["ttft_ns"][1] == t_miss
+    fin0 = ron["records"]["e2e_ns"][0] + at[0]
+    it1 = ron["iters"][ron["iters"]["t_start"] >= fin0]
+    assert int(it1["t_start"][0]) == fin0 + at[1]   # causality: arrival = finish + think
+    assert int(it1["N_p"][0]) == int(P[1]) - c0
+
+
+def test_memory_cache_prefill_work(oracle_lib):
+    """the cache can only reduce prefill work.  With SWAP preemption every admitted round
+    r >= 1 hits a large cache, so total prefill tokens = sum of round-0 prompts + sum over later
+    rounds of (new turn + 1); a cache too small for any context changes nothing at all."""
+    from oracle import oracle as O
+    for seed in range(3):
+        base = _mr_cfg(n=60, seed=seed, rate=4.0, len_dist=si.UNIFORM, pa=16, pb=128, oa=4, ob=64,
+                       think=0.5, pol=si.Policy(preempt=si.SWAP))
+        at, P, Oo, cv = O.workload_rounds(base)
+        first = np.r_[True, cv[1:] != cv[:-1]]
+        idx = np.nonzero(~first)[0]
+        expect = int(P[first].sum()) + int((P[idx].astype(np.int64) - P[idx - 1] - Oo[idx - 1] + 1).sum())
+        big = replace(base, options=replace(base.options, cache_capacity_blocks=1 << 40))
+        rb = O.simulate(big, 0, check_invariants=True, want=("summary", "iters"))
+        assert rb["summary"]["n_finished"] == len(P)
+        assert int(rb["iters"]["N_p"].sum()) == expect
+        off = O.simulate(replace(base, options=replace(base.options, memory_cache=False)), 0,
+                         want=("summary", "records", "iters"))
+        assert int(off["iters"]["N_p"].sum()) == int(P.sum()) >= expect
+        tiny = O.simulate(replace(base, options=replace(base.options, cache_capacity_blocks=1)), 0,
+                          want=("summary", "records"))
+        assert tiny["records"].tobytes() == off["records"].tobytes()
+
+
+def test_memory_cache_invariants_random(oracle_lib):
+    """Random multi-round configs (all policies, both preemption modes, LRU capacities):
+    conservation and cache accounting every iteration, every request finished or rejected."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(321)
+    for _ in range(40):
+        bs = int(rng.choice([4, 16]))
+        total = int(rng.integers(-(-512 // bs), -(-512 // bs) + 60))
+        pol = si.Policy(kind=str(rng.choice([si.STATIC, si.CONT, si.CONT_RATIO])),
+                        preempt=str(rng.choice([si.SWAP, si.RECOMPUTE])), max_mem_ratio=0.8,
+                        max_num_seqs=int(rng.choice([2, 8, 256])), block_size=bs)
+        cfg = _mr_cfg(n=int(rng.integers(1, 40)), seed=int(rng.integers(0, 1000)), rate=float(rng.choice([1.0, 8.0])),
+                      len_dist=si.UNIFORM, pa=8, pb=120, oa=2, ob=60, mml=512, think=float(rng.choice([0.05, 1.0])),
+                      cap=int(rng.choice([0, 8, 64])), pol=pol, hw=replace(si.A100, kv_blocks_override=total))
+        r = O.simulate(cfg, 0, check_invariants=True, want=("summary", "records"))
+        s = r["summary"]
+        assert s["n_finished"] + s["n_rejected"] == s["n_requests"] == len(r["records"])
+
+
+def test_finding6_cache_helps_short_outputs(oracle_lib):
+    """Finding 6: at a high request rate the memory cache lowers P99 latency of
+    multi-round conversations with ~64-token outputs."""
+    from oracle import oracle as O
+    res = {}
+    for cache in (False, True):
+        cfg = _mr_cfg(n=400, seed=7, rate=12.0, len_dist=si.UNIFORM, pa=200, pb=600, oa=32, ob=96,
+                      think=1.0, cache=cache, mml=4096)
+        s = O.simulate(cfg, 0, want=("summary",))["summary"]
+        res[cache] = s["stat"][2][2]   # E2E P99
+    assert res[True] < res[False]
