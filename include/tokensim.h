@@ -144,6 +144,13 @@ typedef struct {
   const tokensim_len_table *prompt_table, *output_table;  /* TABLE                */
   const int64_t *trace_arrival_ns;      /* TRACE: non-decreasing, >= 0            */
   const uint32_t *trace_prompt, *trace_output;
+  /* NEXT-2 (reading R-N2): num_requests CONVERSATIONS arrive as above
+   * (round 0); half have one round, the rest 2..7 (uniform); round r >= 1 arrives an Exp(think
+   * mean) gap after round r-1 finishes and its prompt is the prior context plus a new turn drawn
+   * like a prompt.  Requests are numbered rid = (rounds of earlier conversations) + r, at most
+   * 7 * num_requests per point.  Generated lengths only (not TRACE); UNIFIED topology, MIXED. */
+  uint32_t multi_round;
+  double think_mean_s;                  /* 5                              */
 } tokensim_workload;
 
 typedef struct {
@@ -171,6 +178,13 @@ typedef struct {
    * slower than SEQUENTIAL.  The P->D transfer already overlaps both workers (a.9). */
   uint32_t link_mode;         /* TOKENSIM_LINK_SEQUENTIAL | TOKENSIM_LINK_PRELOAD           */
   uint64_t preload_buffer_bytes;  /* PRELOAD: > 0; one chunk fits even if smaller           */
+  /* NEXT-2 memory cache: a host LRU cache of conversation contexts.
+   * A finishing round stores its context (prompt + output - 1 tokens of KV); admitting a later
+   * round of a cached conversation skips that prefix (c.5 prefill row with c0 > 0) and pays
+   * cache_fetch_ns_per_block per cached block before its prefill. */
+  uint32_t memory_cache;      /* 1 = on (multi-round workloads)                             */
+  uint64_t cache_capacity_blocks;  /* 0 = 4 x the point's device KV blocks          */
+  double cache_fetch_ns_per_block;  /* 800                                          */
 } tokensim_options;
 /* options.flags: evaluate quiescent decode stretches one iteration at a time instead of
  * 32 at once (results are identical either way; this exists to prove it). */

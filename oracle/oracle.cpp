@@ -1926,6 +1926,7 @@ oracle_run *simulate_mr(const oracle_cfg &c) {
     req[i].p = Wr.P[i];
     req[i].o = Wr.O[i];
   }
+  for (u32 cv = 0; cv < nconv; ++cv) req[Wr.base[cv]].a = Wr.at[Wr.base[cv]];  // round 0 arrivals are known
   oracle_run *run = new oracle_run();
   std::memset(&run->summary, 0, sizeof(run->summary));
   oracle_summary &S = run->summary;

@@ -61,7 +61,8 @@ class Workload(C.Structure):
                 ("num_seeds", u32), ("seeds", PU64), ("len_dist", u32), ("prompt_a", u32),
                 ("prompt_b", u32), ("output_a", u32), ("output_b", u32),
                 ("prompt_table", C.POINTER(LenTable)), ("output_table", C.POINTER(LenTable)),
-                ("trace_arrival_ns", PI64), ("trace_prompt", PU32), ("trace_output", PU32)]
+                ("trace_arrival_ns", PI64), ("trace_prompt", PU32), ("trace_output", PU32),
+                ("multi_round", u32), ("think_mean_s", f64)]
 
 
 class Options(C.Structure):
@@ -69,7 +70,8 @@ class Options(C.Structure):
                 ("trace_bin_ns", u64), ("trace_cap_bytes", u64), ("iteration_trace_cap", u32),
                 ("slo_ttft_s", f64), ("slo_mtpot_s", f64), ("horizon_ns", i64), ("flags", u32),
                 ("pd_prefill_workers", u32), ("pd_decode_workers", u32), ("dispatch", u32),
-                ("link_mode", u32), ("preload_buffer_bytes", u64)]
+                ("link_mode", u32), ("preload_buffer_bytes", u64),
+                ("memory_cache", u32), ("cache_capacity_blocks", u64), ("cache_fetch_ns_per_block", f64)]
 
 
 class PointProfile(C.Structure):

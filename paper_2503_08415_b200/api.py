@@ -72,6 +72,7 @@ def marshal(cfg: si.SweepConfig):
     cw.num_seeds, cw.seeds = len(w.seeds), pseeds
     cw.len_dist = _LEN[w.len_dist]
     cw.prompt_a, cw.prompt_b, cw.output_a, cw.output_b = w.prompt_a, w.prompt_b, w.output_a, w.output_b
+    cw.multi_round, cw.think_mean_s = int(w.multi_round), w.think_mean_s
     if w.len_dist == si.TABLE:
         tabs = []
         for t in (w.prompt_table, w.output_table):
@@ -94,7 +95,8 @@ def marshal(cfg: si.SweepConfig):
     co = T.Options(C.sizeof(T.Options), _TOP[o.topology], o.pd_link_bw, _TRC[o.trace_mode], o.trace_bin_ns,
                    o.trace_cap_bytes, o.iteration_trace_cap, o.slo_ttft_s, o.slo_mtpot_s, o.horizon_ns,
                    flags, o.pd_prefill, o.pd_decode, _DISPATCH[o.dispatch],
-                   {si.SEQUENTIAL: T.LINK_SEQUENTIAL, si.PRELOAD: T.LINK_PRELOAD}[o.link_mode], o.preload_buffer_bytes)
+                   {si.SEQUENTIAL: T.LINK_SEQUENTIAL, si.PRELOAD: T.LINK_PRELOAD}[o.link_mode], o.preload_buffer_bytes,
+                   int(o.memory_cache), o.cache_capacity_blocks, o.cache_fetch_ns_per_block)
     return cm, hws, pols, cw, co, keep
 
 
@@ -196,8 +198,10 @@ class Sweep:
         self._check(self._L.tokensim_import_summaries(self._h, arr.ctypes.data, arr.nbytes), "import_summaries")
 
     def records(self, point: int) -> np.ndarray:
-        out = np.zeros(self._n_req, T.RECORD_DTYPE)
+        """Per-request records of one point (multi-round: one per round, rid order)."""
         n = C.c_uint64()
+        self._check(self._L.tokensim_get_request_records(self._h, point, None, 0, C.byref(n)), "get_request_records")
+        out = np.zeros(n.value, T.RECORD_DTYPE)
         self._check(self._L.tokensim_get_request_records(self._h, point, out.ctypes.data, len(out), C.byref(n)),
                     "get_request_records")
         return out
@@ -244,7 +248,9 @@ class Sweep:
         return d
 
     def workload(self, point: int):
-        n = self._n_req
+        """The point's generated requests (multi-round: 7 x conversations slots in rid order,
+        arrival = round 0's time or round r's think gap; unused slots are zero)."""
+        n = self._n_req * (7 if self.cfg.workload.multi_round else 1)
         a = np.zeros(n, np.int64)
         p = np.zeros(n, np.uint32)
         o = np.zeros(n, np.uint32)

@@ -34,7 +34,8 @@ const uint32_t kOutputThr[7] = {429496730u, 773094113u, 1159641170u, 1717986918u
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, ring, fifo, pdn, pdn_per_warp, evlog, itlog,
+  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, ring, fifo, pdn, pdn_per_warp,
+      mr_conv, mr_base, mr_nr, mr_ntot, mr_a0, mr_p0, mr_o0, mr, mr_per_warp, evlog, itlog,
       total;
   u64 n_run;
   u32 warps_total, wpb, blocks;
@@ -65,6 +66,8 @@ struct tokensim_sweep {
   bool pd_general = false;  // run the general xP:yD loop
   u32 trace_nw() const { return pd_general ? std::max<u32>(2, pd_x + pd_y) : 2; }
   u32 bt_tables() const { return pd_general ? pd_y + 1 : 2; }
+  // requests per point (record stride): 7 x conversations with multi-round workloads
+  u64 n_slots() const { return wl.multi_round ? 7ull * wl.num_requests : (u64)wl.num_requests; }
   size_t smem_per_warp() const {
     return sim_smem_per_warp((int)cap, nwords_max, opt.topology == TOKENSIM_PD_PAIR, pd_general ? pd_x : 0,
                              pd_general ? pd_y : 0);
@@ -262,6 +265,18 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
     default:
       return bad("workload.len_dist: unknown");
   }
+  // NEXT-2 multi-round conversations and the memory cache (reading R-N2)
+  if (w.multi_round) {
+    if (w.len_dist == TOKENSIM_LEN_TRACE) return bad("workload.multi_round: needs generated lengths, not TRACE");
+    if (opt->topology != TOKENSIM_UNIFIED) return bad("workload.multi_round: UNIFIED topology only");
+    if (!(w.think_mean_s >= 0) || !std::isfinite(w.think_mean_s)) return bad("workload.think_mean_s: must be >= 0");
+    if ((u64)w.num_requests * 7 > (1u << 30)) return bad("workload.num_requests: too many conversations");
+    for (u32 i = 0; i < n_pol; ++i)
+      if (pol[i].iteration_mode != TOKENSIM_MIXED) return bad("workload.multi_round: MIXED iterations only");
+  }
+  if (opt->memory_cache && !w.multi_round) return bad("options.memory_cache: needs a multi_round workload");
+  if (!(opt->cache_fetch_ns_per_block >= 0) || !std::isfinite(opt->cache_fetch_ns_per_block))
+    return bad("options.cache_fetch_ns_per_block: must be >= 0");
 
   // ---- model constants
   DevModel &M = h->M;
@@ -435,7 +450,9 @@ static u64 count_run(u64 begin, u64 end, u64 stride) { return end > begin ? (end
 
 static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int blocks_per_sm_limit) {
   Layout L{};
-  const u64 n = h->wl.num_requests;
+  const u64 n = h->n_slots();
+  const u64 nconv = h->wl.num_requests;
+  const bool mr = h->wl.multi_round != 0;
   const bool trace_mode = h->wl.len_dist == TOKENSIM_LEN_TRACE;
   const u64 groups = trace_mode ? 1 : (u64)h->rates.size() * h->seeds.size();
   L.n_run = n_run;
@@ -479,6 +496,17 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   L.fifo = take(pair ? (size_t)L.warps_total * n * 32 : 0);
   L.pdn_per_warp = h->pd_general ? align256(pdn_global_per_warp(n, h->cap, h->bt_len, h->pd_x, h->pd_y)) : 0;
   L.pdn = take((size_t)L.warps_total * L.pdn_per_warp);
+  L.mr_conv = take(mr ? groups * n * 4 : 0);
+  L.mr_base = take(mr ? groups * nconv * 4 : 0);
+  L.mr_nr = take(mr ? groups * nconv * 4 : 0);
+  L.mr_ntot = take(mr ? groups * 4 : 0);
+  L.mr_a0 = take(mr ? groups * nconv * 8 : 0);
+  L.mr_p0 = take(mr ? groups * nconv * 4 : 0);
+  L.mr_o0 = take(mr ? groups * nconv * 4 : 0);
+  // per warp: arrival FIFO (rid u32 + time i64) x n, follow-up heap (time i64 + conv u32) x
+  // nconv, next round / cached tokens / LRU prev / LRU next (u32) x nconv
+  L.mr_per_warp = mr ? align256(n * 12 + nconv * 12 + nconv * 16 + 64) : 0;
+  L.mr = take((size_t)L.warps_total * L.mr_per_warp);
   L.evlog = take((size_t)L.warps_total * 1024 * 16);
   L.itlog = take((size_t)L.warps_total * 256 * 64);
   L.total = o;
@@ -599,7 +627,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.n_rates = (u32)h->rates.size();
   P.n_seeds = (u32)h->seeds.size();
   P.topology = h->opt.topology;
-  P.n_req = h->wl.num_requests;
+  P.n_req = (u32)h->n_slots();
   const bool trace_mode = h->wl.len_dist == TOKENSIM_LEN_TRACE;
   P.len_dist = h->wl.len_dist == TOKENSIM_LEN_SHAREGPT_SYNTH_V1 ? (u32)TOKENSIM_LEN_TABLE : h->wl.len_dist;
   P.n_groups = trace_mode ? 0 : P.n_rates * P.n_seeds;
@@ -657,6 +685,21 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.dispatch = h->opt.dispatch;
   P.link_mode = h->opt.link_mode;
   P.preload_buf = h->opt.preload_buffer_bytes;
+  P.multi_round = h->wl.multi_round ? 1u : 0u;
+  P.memory_cache = h->opt.memory_cache ? 1u : 0u;
+  P.n_conv = h->wl.num_requests;
+  P.think_ns = h->wl.think_mean_s * 1e9;
+  P.fetch_s = h->opt.cache_fetch_ns_per_block * 1e-9;
+  P.cache_cap = h->opt.cache_capacity_blocks;
+  P.mr_conv = reinterpret_cast<u32 *>(ws + L.mr_conv);
+  P.mr_base = reinterpret_cast<u32 *>(ws + L.mr_base);
+  P.mr_nr = reinterpret_cast<u32 *>(ws + L.mr_nr);
+  P.mr_ntot = reinterpret_cast<u32 *>(ws + L.mr_ntot);
+  P.mr_a0 = reinterpret_cast<i64 *>(ws + L.mr_a0);
+  P.mr_p0 = reinterpret_cast<u32 *>(ws + L.mr_p0);
+  P.mr_o0 = reinterpret_cast<u32 *>(ws + L.mr_o0);
+  P.mr_scratch = reinterpret_cast<unsigned char *>(ws + L.mr);
+  P.mr_bytes_per_warp = L.mr_per_warp;
   P.pd_general = h->pd_general ? 1u : 0u;
   P.evlog = reinterpret_cast<uint4 *>(ws + L.evlog);
   P.itlog = reinterpret_cast<ulonglong2 *>(ws + L.itlog);
@@ -792,12 +835,19 @@ tokensim_status tokensim_get_request_records(const tokensim_sweep *hc, uint64_t 
   u64 j;
   tokensim_status s = local_index(h, point, &j);
   if (s != TOKENSIM_OK) return fail(h, s, "get_request_records: point not run by this handle");
-  const u64 n = h->wl.num_requests;
+  const u64 stride = h->n_slots();
+  u64 n = stride;
+  if (h->wl.multi_round) {  // this point's requests (rounds of its conversations)
+    if ((s = sync_run(h)) != TOKENSIM_OK) return s;
+    SimStats st;
+    if ((s = copy_d2h(h, &st, h->P.stats + j, sizeof st)) != TOKENSIM_OK) return s;
+    n = st.n_req;
+  }
   *n_out = n;
   if (!out || capacity == 0) return TOKENSIM_OK;
   if (capacity < n) return TOKENSIM_E_TRUNCATED;
   if ((s = sync_run(h)) != TOKENSIM_OK) return s;
-  return copy_d2h(h, out, h->P.rec + j * n, n * sizeof(tokensim_request_record));
+  return copy_d2h(h, out, h->P.rec + j * stride, n * sizeof(tokensim_request_record));
 }
 
 tokensim_status tokensim_get_iteration_trace(const tokensim_sweep *hc, uint64_t point, tokensim_iter_record *out,
@@ -859,7 +909,7 @@ tokensim_status tokensim_get_latency_quantiles(const tokensim_sweep *hc, uint64_
   }
   if (s != TOKENSIM_OK) return fail(h, s, "get_latency_quantiles: point not run by this handle");
   if ((s = sync_run(h)) != TOKENSIM_OK) return s;
-  const u64 n = h->wl.num_requests;
+  const u64 n = h->n_slots();
   char *buf = nullptr;
   const size_t bytes = align256(n_q * 4) + align256(n_q * 8) + n * 8;
   cudaError_t e = cudaMalloc(&buf, bytes);
@@ -883,7 +933,7 @@ tokensim_status tokensim_get_workload(const tokensim_sweep *hc, uint64_t point, 
   u64 j;
   tokensim_status s = local_index(h, point, &j);
   if (s != TOKENSIM_OK) return fail(h, s, "get_workload: point not run by this handle");
-  const u64 n = h->wl.num_requests;
+  const u64 n = h->n_slots();  // multi-round: per request, arrival = round 0 time or think gap
   if (capacity < n) return TOKENSIM_E_TRUNCATED;
   if ((s = sync_run(h)) != TOKENSIM_OK) return s;
   const Coords c = decode_point(point, h->P.n_pol, h->P.n_rates, h->P.n_seeds);

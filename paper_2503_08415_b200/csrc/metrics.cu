@@ -234,10 +234,11 @@ __global__ void __launch_bounds__(256) summary_kernel(SweepParams P, u64 *scratc
     S.version = 1;
     S.status_flags = st.flags;
     S.point = point;
-    S.n_requests = n;
+    const u64 nreq = P.multi_round ? st.n_req : (u64)n;  // multi-round: this point's rounds
+    S.n_requests = nreq;
     S.n_finished = nfin;
     S.n_rejected = st.n_rejected;
-    S.n_unfinished = n - nfin - st.n_rejected;
+    S.n_unfinished = nreq - nfin - st.n_rejected;
     S.n_iterations = st.n_iterations;
     S.n_request_iterations = st.n_req_iters;
     S.n_preemptions = st.n_preempt;

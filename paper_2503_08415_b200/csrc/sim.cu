@@ -29,14 +29,16 @@ struct CostK {
   double h, q2g, hq2g, qh, q, q4, hfu, fu, fh, f, Vh, V, s, att_tok, g2, L, twoL, bar_coef;
   double invF, invB, invH, invT, overhead;
   u32 tp;
+  double fetch_s;   // NEXT-2: memory-cache fetch seconds per block
   u32 preload;      // NEXT-4: swap-in through a preload buffer (reading R-N4)
   u64 preload_buf;  // buffer bytes
   u64 Lu;           // layers (chunks of a swap-in)
 };
 
 __device__ __forceinline__ CostK make_costk(const DevModel &M, const DevHw &H, u32 link_mode = 0,
-                                            u64 preload_buf = 0) {
+                                            u64 preload_buf = 0, double fetch_s = 0.0) {
   CostK K;
+  K.fetch_s = fetch_s;
   K.preload = link_mode == TOKENSIM_LINK_PRELOAD ? 1u : 0u;
   K.preload_buf = preload_buf;
   K.Lu = M.L;
@@ -93,7 +95,8 @@ __device__ __noinline__ double preload_pipeline(u64 n, double a, double b, u64 K
 // and swap_in > 0 (warp-collective then; `ring` = >= L+1 doubles of scratch) the swap-in
 // streams layer by layer through the buffer while the layers compute (reading R-N4).
 __device__ __forceinline__ i64 iter_time_chunk_ns(const CostK &K, u64 Np, u64 Ap, u64 Kp, u64 Slm, u64 D,
-                                                  u64 Cd, u64 swap_out, u64 swap_in = 0, double *ring = nullptr) {
+                                                  u64 Cd, u64 swap_out, u64 swap_in = 0, double *ring = nullptr,
+                                                  u64 fetch_blocks = 0) {
   const double N = __ull2double_rn(Np + D), S = __ull2double_rn(Slm + D);
   double tQKV = 0.0, tATTP = 0.0, tATTD = 0.0, tO = 0.0, tUP = 0.0, tDOWN = 0.0, tLM = 0.0;
   const double N2 = __dmul_rn(2.0, N);
@@ -134,6 +137,7 @@ __device__ __forceinline__ i64 iter_time_chunk_ns(const CostK &K, u64 Np, u64 Ap
   if (K.tp > 1) T = __dadd_rn(T, __dmul_rn(__dmul_rn(__dmul_rn(K.bar_coef, N), K.invT), K.twoL));
   const u64 swap_bytes = pipe ? swap_out : swap_out + swap_in;
   if (swap_bytes > 0) T = __dadd_rn(T, __dmul_rn(__ull2double_rn(swap_bytes), K.invH));
+  if (fetch_blocks > 0) T = __dadd_rn(T, __dmul_rn(__ull2double_rn(fetch_blocks), K.fetch_s));  // NEXT-2
   T = __dadd_rn(T, K.overhead);
   return (i64)floor(__dadd_rn(__dmul_rn(T, 1e9), 0.5));
 }
@@ -436,6 +440,111 @@ size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_
   return smem_per_warp_bytes((u32)cap, nwords_max) + (pd ? smem_pd_extra((u32)cap, nwords_max) : 0);
 }
 
+// ------------------------------------------------------------------ NEXT-2 per-point state
+// Multi-round conversations and the host memory cache (reading R-N2).  All of this is scalar
+// code run identically by every lane (equal values written to equal addresses), so the state
+// stays lane-uniform without broadcasts.
+constexpr u32 MR_NIL = 0xffffffffu;
+struct MrState {
+  const u32 *CONV, *BASE, *NR;
+  u32 *wq_id;          // arrival FIFO: request ids in arrival order, and their arrival times
+  i64 *wq_t;
+  i64 *hp_t;           // follow-up rounds: min-heap on (time, conversation)
+  u32 *hp_c;
+  u32 *nxr;            // round index of a conversation's pending follow-up
+  u32 *ctok;           // cached context tokens per conversation (0 = not cached)
+  u32 *lprev, *lnext;  // LRU list (head = least recently used)
+  u32 nconv, ntot, next0, hsize, lhead, ltail;
+  u64 used, cap;
+};
+__device__ __forceinline__ bool mr_less(i64 t1, u32 c1, i64 t2, u32 c2) { return t1 < t2 || (t1 == t2 && c1 < c2); }
+__device__ __forceinline__ void mr_heap_push(MrState &M, i64 t, u32 c) {
+  u32 i = M.hsize++;
+  while (i > 0) {
+    const u32 p = (i - 1) >> 1;
+    if (!mr_less(t, c, M.hp_t[p], M.hp_c[p])) break;
+    M.hp_t[i] = M.hp_t[p];
+    M.hp_c[i] = M.hp_c[p];
+    i = p;
+  }
+  M.hp_t[i] = t;
+  M.hp_c[i] = c;
+}
+__device__ __forceinline__ void mr_heap_pop(MrState &M) {
+  const u32 n = --M.hsize;
+  if (n == 0) return;
+  const i64 t = M.hp_t[n];
+  const u32 c = M.hp_c[n];
+  u32 i = 0;
+  while (true) {
+    u32 l = 2 * i + 1;
+    if (l >= n) break;
+    if (l + 1 < n && mr_less(M.hp_t[l + 1], M.hp_c[l + 1], M.hp_t[l], M.hp_c[l])) ++l;
+    if (!mr_less(M.hp_t[l], M.hp_c[l], t, c)) break;
+    M.hp_t[i] = M.hp_t[l];
+    M.hp_c[i] = M.hp_c[l];
+    i = l;
+  }
+  M.hp_t[i] = t;
+  M.hp_c[i] = c;
+}
+// the next arrival (round 0 stream vs pending follow-ups), ties to the lower conversation
+__device__ __forceinline__ bool mr_next(const MrState &M, const i64 *A, i64 &ta, u32 &cv, bool &from0) {
+  ta = INT64_MAX;
+  from0 = false;
+  bool any = false;
+  if (M.next0 < M.nconv) {
+    ta = A[M.BASE[M.next0]];
+    cv = M.next0;
+    from0 = true;
+    any = true;
+  }
+  if (M.hsize) {
+    const i64 ht = M.hp_t[0];
+    const u32 hc = M.hp_c[0];
+    if (!any || mr_less(ht, hc, ta, cv)) {
+      ta = ht;
+      cv = hc;
+      from0 = false;
+      any = true;
+    }
+  }
+  return any;
+}
+__device__ __forceinline__ void mr_unlink(MrState &M, u32 c) {
+  const u32 p = M.lprev[c], nx = M.lnext[c];
+  if (p != MR_NIL) M.lnext[p] = nx;
+  else M.lhead = nx;
+  if (nx != MR_NIL) M.lprev[nx] = p;
+  else M.ltail = p;
+}
+__device__ __forceinline__ void mr_append(MrState &M, u32 c) {
+  M.lprev[c] = M.ltail;
+  M.lnext[c] = MR_NIL;
+  if (M.ltail != MR_NIL) M.lnext[M.ltail] = c;
+  else M.lhead = c;
+  M.ltail = c;
+}
+// a finishing round stores its context as the most recently used entry; evict LRU entries
+__device__ __forceinline__ void mr_cache_store(MrState &M, u32 c, u32 tokens, const BSz &B) {
+  if (M.ctok[c]) {
+    M.used -= B.cdiv(M.ctok[c]);
+    mr_unlink(M, c);
+    M.ctok[c] = 0;
+  }
+  const u64 blk = B.cdiv(tokens);
+  if (blk > M.cap) return;  // larger than the whole cache
+  mr_append(M, c);
+  M.ctok[c] = tokens;
+  M.used += blk;
+  while (M.used > M.cap) {
+    const u32 e = M.lhead;
+    mr_unlink(M, e);
+    M.used -= B.cdiv(M.ctok[e]);
+    M.ctok[e] = 0;
+  }
+}
+
 // ------------------------------------------------------------------ a.2-a.7 one point
 // Everything is executed by all 32 lanes; scalar state is lane-uniform in registers.
 template <int CAP>
@@ -448,7 +557,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const DevHw H = P.hw[cd.hw];
   const DevHP HP = P.hp[(size_t)cd.hw * P.n_pol + cd.pol];
   const DevPol PL = P.pol[cd.pol];
-  const CostK K = make_costk(P.M, H, P.link_mode, P.preload_buf);
+  const CostK K = make_costk(P.M, H, P.link_mode, P.preload_buf, P.fetch_s);
   const u32 g = P.group_of_point_mode ? 0u : cd.rate * P.n_seeds + cd.seed;
   const u32 n = P.n_req;
   const i64 *A = P.arrival + (size_t)g * n;
@@ -463,12 +572,14 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const bool STATICP = PL.kind == TOKENSIM_STATIC;
   const bool PFM = PL.mode == TOKENSIM_PREFILL_FIRST;
   const bool CHK = PL.mode == TOKENSIM_CHUNKED;
+  const bool MRM = P.multi_round != 0;  // NEXT-2: request ids are (conversation, round) rids
+  const bool CACHE = MRM && P.memory_cache != 0;
   const u64 total = HP.total_blocks;
   const u32 nwords = HP.nwords;
   const u32 btl = P.bt_len;
   const u32 mns = PL.mns, mbt = PL.mbt;
   const i64 wm = (i64)PL.wm;
-  const bool ff_on = P.ff_enable != 0;
+  const bool ff_on = P.ff_enable != 0 && !MRM;  // multi-round points step one iteration at a time
   const long long clk0 = clock64();
 
   // ---- init: records, bitmap, slot pool
@@ -505,6 +616,31 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   L.dig_b = 0;
   L.nev = 0;
   L.nit = 0;
+  MrState mr;
+  if (MRM) {
+    unsigned char *mb = P.mr_scratch + (size_t)gwarp * P.mr_bytes_per_warp;
+    const u32 nc = P.n_conv;
+    mr.CONV = P.mr_conv + (size_t)g * n;
+    mr.BASE = P.mr_base + (size_t)g * nc;
+    mr.NR = P.mr_nr + (size_t)g * nc;
+    mr.wq_t = reinterpret_cast<i64 *>(mb);
+    mr.hp_t = mr.wq_t + n;
+    mr.wq_id = reinterpret_cast<u32 *>(mr.hp_t + nc);
+    mr.hp_c = mr.wq_id + n;
+    mr.nxr = mr.hp_c + nc;
+    mr.ctok = mr.nxr + nc;
+    mr.lprev = mr.ctok + nc;
+    mr.lnext = mr.lprev + nc;
+    mr.nconv = nc;
+    mr.ntot = P.mr_ntot[g];
+    mr.next0 = 0;
+    mr.hsize = 0;
+    mr.lhead = mr.ltail = MR_NIL;
+    mr.used = 0;
+    mr.cap = P.cache_cap ? P.cache_cap : 4 * total;
+    for (u32 x = lane; x < nc; x += 32) mr.ctok[x] = 0;
+    __syncwarp();
+  }
   u64 req_iters = 0, npre = 0, swo_tot = 0, swi_tot = 0, nrej_tot = 0, nfin_tot = 0, peak = 0, bns = 0;
   u64 ff_iters = 0, ff_runs = 0;
   u64 cyc_ff = 0, cyc_ff_fail = 0, cyc_normal = 0;
@@ -570,21 +706,50 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
 
   while (true) {
     // 0. termination
-    if (adm == n && nR == 0 && nQ == 0) break;
+    if (MRM ? (mr.next0 == mr.nconv && mr.hsize == 0 && adm == arr && nR == 0 && nQ == 0)
+            : (adm == n && nR == 0 && nQ == 0))
+      break;
     if (P.horizon >= 0 && t >= P.horizon) {
       flags |= TOKENSIM_PT_HORIZON_HIT;
       break;
     }
     // 1. ingest: a_i <= t become visible at this boundary
-    while (arr < n) {
-      if (arr >= win + 32) load_win(arr);
-      const u32 m = __ballot_sync(FULLMASK, (win + lane >= arr) && (wa <= t));
-      arr += __popc(m);
-      if (arr < win + 32) break;
+    if (MRM) {
+      // multi-round: the round-0 stream and pending follow-ups join the arrival FIFO in
+      // (time, conversation) order; [adm, arr) of the FIFO is the fresh queue
+      i64 ta;
+      u32 cv;
+      bool from0;
+      while (mr_next(mr, A, ta, cv, from0) && ta <= t) {
+        const u32 r = from0 ? 0u : mr.nxr[cv];
+        if (from0) ++mr.next0;
+        else mr_heap_pop(mr);
+        mr.wq_id[arr] = mr.BASE[cv] + r;
+        mr.wq_t[arr] = ta;
+        ++arr;
+      }
+    } else {
+      while (arr < n) {
+        if (arr >= win + 32) load_win(arr);
+        const u32 m = __ballot_sync(FULLMASK, (win + lane >= arr) && (wa <= t));
+        arr += __popc(m);
+        if (arr < win + 32) break;
+      }
     }
     // 2. idle skip
     if (nR == 0 && nQ == 0 && adm == arr) {
-      t = __shfl_sync(FULLMASK, wa, arr - win);
+      if (MRM) {
+        i64 ta;
+        u32 cv;
+        bool from0;
+        if (!mr_next(mr, A, ta, cv, from0)) {
+          flags |= TOKENSIM_PT_INTERNAL_ERROR;
+          break;
+        }
+        t = ta;
+      } else {
+        t = __shfl_sync(FULLMASK, wa, arr - win);
+      }
       continue;
     }
 
@@ -941,6 +1106,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     // CHUNKED: keys read by prefills, LM-head rows, the entry left partial this iteration
     u64 kpp = 0;
     u32 semit = 0, nres_sw = 0;
+    u64 fetch_blocks = 0;  // NEXT-2: cached blocks fetched by this iteration's hits
     bool hnew = false;
     u32 xnew_pos = 0, xnew_done = 0, xnew_tgt = 0;
     auto note_partial = [&](bool part, u32 pos, u32 ch, u32 tgt) {
@@ -960,7 +1126,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         // quick exit: a head that is not rejected but cannot be admitted stops step 5 at once
         const u32 off = adm - win;
         const u32 pw = __shfl_sync(FULLMASK, wp, off & 31u);
-        const u32 ph = (adm >= win && off < 32) ? pw : PR[adm];
+        const u32 ph = MRM ? PR[mr.wq_id[adm]] : ((adm >= win && off < 32) ? pw : PR[adm]);
         const u32 nh = B.cdiv(ph);
         head_blocked = (u64)nh <= HP.cap_fresh &&
                        ((u64)nR + 1 > mns || tokens + (CHK ? 1u : ph) > (u64)mbt || (i64)nfree - (i64)nh < wm ||
@@ -975,10 +1141,16 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           u32 p = __shfl_sync(FULLMASK, wp, off & 31u);
           u32 o = __shfl_sync(FULLMASK, wo, off & 31u);
           i64 a = __shfl_sync(FULLMASK, wa, off & 31u);
+          u32 rid = i;  // request id (multi-round: from the arrival FIFO)
           if (!valid) {
             p = 0;
             o = 0;
             a = 0;
+          } else if (MRM) {
+            rid = mr.wq_id[i];
+            p = PR[rid];
+            o = OU[rid];
+            a = mr.wq_t[i];
           } else if (!inw) {
             p = PR[i];
             o = OU[i];
@@ -1001,14 +1173,35 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const bool rj = rej && lane < stop;
           const u32 takem = __ballot_sync(FULLMASK, take);
           const u32 cnt = __popc(takem);
+          // NEXT-2 cache lookups, in admission order: a later round of a cached conversation
+          // skips its cached prefix c0 and pays the fetch of its blocks (reading R-N2)
+          u32 c0 = 0;
+          if (CACHE && cnt) {
+            u32 tm = takem;
+            while (tm) {
+              const u32 l = (u32)(__ffs(tm) - 1);
+              tm &= tm - 1;
+              const u32 lrid = __shfl_sync(FULLMASK, rid, l);
+              const u32 cv = mr.CONV[lrid];
+              u32 hit = 0;
+              if (lrid > mr.BASE[cv] && mr.ctok[cv]) {
+                hit = mr.ctok[cv];
+                fetch_blocks += B.cdiv(hit);
+                mr_unlink(mr, cv);
+                mr_append(mr, cv);
+              }
+              if (lane == l) c0 = hit;
+            }
+            __syncwarp();
+          }
           if (cnt) {
             const u32 rank = __popc(takem & ltm);
             const u32 slot = alloc_btslots(S.btfree, CAP / 32, take, rank, cnt);
-            u32 ch = p;
+            u32 ch = p - c0;
             if (CHK && take) ch = (u32)min((u64)p, (u64)mbt - (tokens + cp - p));
             if (take) {
               const u32 pos = nR + rank;
-              S.id[pos] = i;
+              S.id[pos] = rid;
               S.ctx[pos] = p;  // fresh prefill of P = p; ctx after commit
               S.rem[pos] = o;
               S.info[pos] = CHK ? (slot | INFO_NT) : slot;
@@ -1019,14 +1212,27 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               S.req_cum[E + rank] = Kb + cneed;
               S.req_pt[E + rank] = pos;
               npp += ch;
-              app += (u64)ch * (ch + 1) / 2;
-              kpp += ch;
+              app += (u64)ch * c0 + (u64)ch * (ch + 1) / 2;
+              kpp += (u64)c0 + ch;
               semit += ch == p ? 1u : 0u;
             }
             if (CHK) note_partial(take && ch < p, nR + rank, ch, p);
           }
-          if (rj) reinterpret_cast<uint8_t *>(rec + i)[26] = (uint8_t)TOKENSIM_REQ_REJECTED;
-          const u32 nrj = __popc(__ballot_sync(FULLMASK, rj));
+          if (rj) reinterpret_cast<uint8_t *>(rec + rid)[26] = (uint8_t)TOKENSIM_REQ_REJECTED;
+          u32 nrj = __popc(__ballot_sync(FULLMASK, rj));
+          if (MRM) {  // a rejected round ends its conversation: its later rounds never arrive
+            u32 rm = __ballot_sync(FULLMASK, rj);
+            while (rm) {
+              const u32 l = (u32)(__ffs(rm) - 1);
+              rm &= rm - 1;
+              const u32 lrid = __shfl_sync(FULLMASK, rid, l);
+              const u32 cv = mr.CONV[lrid];
+              const u32 last = mr.BASE[cv] + mr.NR[cv];
+              for (u32 q = lrid + 1 + lane; q < last; q += 32)
+                reinterpret_cast<uint8_t *>(rec + q)[26] = (uint8_t)TOKENSIM_REQ_REJECTED;
+              nrj += last - lrid - 1;
+            }
+          }
           if (stop) {
             const u32 sneed = __shfl_sync(FULLMASK, cneed, stop - 1);
             const u32 sp = __shfl_sync(FULLMASK, cp, stop - 1);
@@ -1219,13 +1425,12 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       Np = warp_sum64(npp);
       Ap = warp_sum64(app);
       Kp = Np;
-      if (CHK) {
-        Kp = warp_sum64(kpp);
-        Slm = __reduce_add_sync(FULLMASK, semit);
-      }
+      if (CHK || CACHE) Kp = warp_sum64(kpp);
+      if (CHK) Slm = __reduce_add_sync(FULLMASK, semit);
     }
     if (K.preload && swap_in > 0) ev_flush(L);  // the event log doubles as the pipeline's scratch
-    const i64 T = iter_time_chunk_ns(K, Np, Ap, Kp, Slm, D, Cd, swap_out, swap_in, reinterpret_cast<double *>(L.ev));
+    const i64 T = iter_time_chunk_ns(K, Np, Ap, Kp, Slm, D, Cd, swap_out, swap_in, reinterpret_cast<double *>(L.ev),
+                                     fetch_blocks);
     NPH(4);
     // 8. commit
     const i64 ts = t, te = t + T;
@@ -1303,6 +1508,17 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, 0, L, hint);
         nfree += held;
         if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
+        if (MRM) {  // NEXT-2: store the context; schedule the conversation's next round
+          const u32 rid = S.id[pos];
+          const u32 cv = mr.CONV[rid];
+          const u32 r = rid - mr.BASE[cv];
+          if (CACHE) mr_cache_store(mr, cv, PR[rid] + OU[rid] - 1u, B);
+          if (r + 1 < mr.NR[cv]) {
+            mr.nxr[cv] = r + 1;
+            mr_heap_push(mr, te + A[rid + 1], cv);
+          }
+          __syncwarp();
+        }
       }
     }
     NPH(5);
@@ -1454,6 +1670,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     st.cyc_normal = cyc_normal;
     for (int q = 0; q < 8; ++q) st.phase[q] = ph[q];
     for (int q = 0; q < 8; ++q) st.nphase[q] = nph[q];
+    st.n_req = MRM ? mr.ntot : n;
     P.stats[j] = st;
   }
   __syncwarp();

@@ -1097,6 +1097,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     st.cyc_normal = st.cycles;
     for (int q = 0; q < 8; ++q) st.phase[q] = 0;
     for (int q = 0; q < 8; ++q) st.nphase[q] = 0;
+    st.n_req = P.n_req;
     P.stats[j] = st;
   }
   __syncwarp();

@@ -1314,6 +1314,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     st.cyc_normal = 0;
     for (int q = 0; q < 8; ++q) st.phase[q] = 0;
     for (int q = 0; q < 8; ++q) st.nphase[q] = 0;
+    st.n_req = P.n_req;
     P.stats[j] = st;
   }
   __syncwarp();

@@ -60,6 +60,7 @@ struct SimStats {
   u64 cyc_ff, cyc_ff_fail, cyc_normal;  // cycles in stretches / failed attempts / normal iterations
   u64 phase[8];                         // stretch phases: pass/cost/list+alloc/update/fold/trace/compact/tail
   u64 nphase[8];                        // normal-iteration phases (see tokensim_point_profile)
+  u64 n_req;                            // requests of this point (NEXT-2: rounds; else n_req)
 };
 
 struct SweepParams {
@@ -112,6 +113,19 @@ struct SweepParams {
   u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
   u32 link_mode, pad2;                    // NEXT-4: TOKENSIM_LINK_SEQUENTIAL | PRELOAD
   u64 preload_buf;                        // preload buffer bytes
+  // NEXT-2 multi-round conversations + memory cache.  With multi_round, n_req = 7 * n_conv is
+  // the per-group / per-point request stride and arrival/prompt/output are indexed by request
+  // (rid = base[conv] + round; arrival holds round 0's arrival or round r's think gap).
+  u32 multi_round, memory_cache, n_conv, pad3;
+  double think_ns, fetch_s;
+  u64 cache_cap;                          // blocks; 0 = 4 x the point's device KV blocks
+  u32 *mr_conv;                           // [group][n_req] conversation of each request
+  u32 *mr_base, *mr_nr;                   // [group][n_conv] first rid, number of rounds
+  u32 *mr_ntot;                           // [group] requests
+  i64 *mr_a0;                             // [group][n_conv] round-0 stream (a.1 output)
+  u32 *mr_p0, *mr_o0;
+  unsigned char *mr_scratch;              // per warp: arrival FIFO, follow-up heap, LRU cache
+  u64 mr_bytes_per_warp;
   uint4 *evlog;            // per-warp block-event log [warp][1024]
   ulonglong2 *itlog;       // per-warp iteration log [warp][256][4]
 };

@@ -401,3 +401,42 @@ def test_preload_link_parity(api):
                     options=replace(c.options, pd_prefill=x, pd_decode=y, link_mode=si.PRELOAD,
                                     preload_buffer_bytes=1 << 16))
         check_pd_points(run_gpu(api, c), c, list(range(c.num_points)), iters=True)
+
+
+# ------------------------------------------------------------------ NEXT-2 multi-round + memory cache
+def _micro_mr(rng):
+    bs = int(rng.choice([4, 16]))
+    mml = 512
+    total = int(rng.integers(-(-mml // bs), -(-mml // bs) + 60))
+    pol = si.Policy(kind=str(rng.choice([si.STATIC, si.CONT, si.CONT_RATIO])),
+                    preempt=str(rng.choice([si.SWAP, si.RECOMPUTE])), max_mem_ratio=float(rng.choice([0.5, 0.8, 1.0])),
+                    max_num_seqs=int(rng.choice([2, 8, 256])), block_size=bs)
+    w = si.Workload(int(rng.integers(1, 40)), [float(rng.choice([1.0, 8.0]))], [int(rng.integers(0, 1000))],
+                    len_dist=si.UNIFORM, prompt_a=8, prompt_b=120, output_a=2, output_b=60, multi_round=True,
+                    think_mean_s=float(rng.choice([0.05, 1.0])))
+    opts = si.Options(memory_cache=bool(rng.random() < 0.8), cache_capacity_blocks=int(rng.choice([0, 8, 64])),
+                      trace_mode=si.FULL if rng.random() < 0.5 else si.BINNED, trace_bin_ns=100_000_000,
+                      iteration_trace_cap=1 << 16, horizon_ns=int(rng.choice([-1, -1, 2_000_000_000])))
+    return si.SweepConfig("micro-mr", replace(si.LLAMA2_7B, max_model_len=mml),
+                          [replace(si.A100, kv_blocks_override=total)], [pol], w, opts)
+
+
+def test_multi_round_cache_parity(api):
+    """NEXT-2 (reading R-N2): multi-round conversations with and without the host LRU memory
+    cache -- random micro configs (every policy, both preemption modes, small caches that evict,
+    horizons) and a LLaMA-2-7B rate x seed grid -- bit-exact against the oracle."""
+    rng = np.random.default_rng(73)
+    for _ in range(40):
+        c = _micro_mr(rng)
+        check_points(run_gpu(api, c), c, [0], records=True, trace=True, iters=True)
+    for cache in (False, True):
+        cfg = si.SweepConfig("mr-grid", si.LLAMA2_7B, [si.A100],
+                             [si.Policy(preempt=si.SWAP), si.Policy(preempt=si.RECOMPUTE)],
+                             si.Workload(300, [2.0, 8.0, 24.0], [0, 1], len_dist=si.UNIFORM, prompt_a=64,
+                                         prompt_b=512, output_a=16, output_b=128, multi_round=True,
+                                         think_mean_s=2.0),
+                             si.Options(memory_cache=cache))
+        sw = run_gpu(api, cfg)
+        check_points(sw, cfg, list(range(cfg.num_points)), records=True, trace=True)
+        s = sw.summaries()
+        assert (s["n_requests"] > 300).all() and (s["n_finished"] == s["n_requests"]).all()
