@@ -15,9 +15,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("workload.cu", "sim.cu", "metrics.cu", "host.cu")]
-HEADERS = [os.path.join(CSRC, f) for f in ("ts_internal.cuh", "dev_common.cuh")] + \
-    [os.path.join(ROOT, "include", "tokensim.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("sim_full.cu", "sim_base.cu", "workload.cu", "metrics.cu", "host.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in ("ts_internal.cuh", "dev_common.cuh", "sim_core.cuh", "sim_pd.cuh",
+                                           "sim_pdn.cuh")] + [os.path.join(ROOT, "include", "tokensim.h")]
 LIB = os.path.join(PKG, "libtokensim.so")
 
 NVCC_FLAGS = [
@@ -25,7 +25,6 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
     "-Xptxas", "-warn-spills",
-    "-shared",
 ]
 
 
@@ -44,14 +43,24 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit to an object in parallel, then link the shared library."""
     if not force and not stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+    import concurrent.futures as cf
+    import tempfile
+    with tempfile.TemporaryDirectory(prefix="tokensim_build_") as td:
+        objs = [os.path.join(td, os.path.basename(s) + ".o") for s in SOURCES]
+        cmds = [[nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", "-o", o, s]
+                for s, o in zip(SOURCES, objs)]
+        if verbose:
+            for c in cmds:
+                print(" ".join(c), file=sys.stderr)
+        with cf.ThreadPoolExecutor(len(cmds)) as ex:
+            for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+                f.result()
+        tmp = LIB + f".tmp{os.getpid()}"
+        subprocess.check_call([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs])
+        os.replace(tmp, LIB)
     return LIB
 
 

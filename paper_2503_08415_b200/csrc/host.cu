@@ -64,6 +64,7 @@ struct tokensim_sweep {
   u32 cap = 256, nwords_max = 1, bt_len = 1, n_hw_axis = 0;
   u32 pd_x = 0, pd_y = 0;  // NEXT-1 node: prefill / decode workers (0 = unified)
   bool pd_general = false;  // run the general xP:yD loop
+  bool full = false;        // needs the full kernel variant (sim_full.cu)
   u32 trace_nw() const { return pd_general ? std::max<u32>(2, pd_x + pd_y) : 2; }
   u32 bt_tables() const { return pd_general ? pd_y + 1 : 2; }
   // requests per point (record stride): 7 x conversations with multi-round workloads
@@ -431,6 +432,9 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
     h->pd_y = opt->pd_decode_workers ? opt->pd_decode_workers : 1u;
     h->pd_general = h->pd_x > 1 || h->pd_y > 1 || (opt->flags & TOKENSIM_OPT_NODE_LOOP);
   }
+  h->full = opt->topology == TOKENSIM_PD_PAIR || w.multi_round || opt->memory_cache ||
+            opt->link_mode == TOKENSIM_LINK_PRELOAD;
+  for (u32 i = 0; i < n_pol; ++i) h->full |= pol[i].iteration_mode == TOKENSIM_CHUNKED;
   const size_t per_warp = h->smem_per_warp();
   if (per_warp > 227 * 1024) {
     delete h;
@@ -594,7 +598,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   const size_t per_warp = h->smem_per_warp();
   Layout L0 = make_layout(h, n_run, sms, 0);
   int occ = 0;
-  e = sim_occupancy((int)h->cap, (int)L0.wpb, per_warp * L0.wpb, &occ);
+  e = sim_occupancy(h->full, (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
   const Layout L = make_layout(h, n_run, sms, occ);
@@ -701,6 +705,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.mr_scratch = reinterpret_cast<unsigned char *>(ws + L.mr);
   P.mr_bytes_per_warp = L.mr_per_warp;
   P.pd_general = h->pd_general ? 1u : 0u;
+  P.full = h->full ? 1u : 0u;
   P.evlog = reinterpret_cast<uint4 *>(ws + L.evlog);
   P.itlog = reinterpret_cast<ulonglong2 *>(ws + L.itlog);
 

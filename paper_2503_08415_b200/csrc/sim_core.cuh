@@ -1,4 +1,7 @@
-// sim.cu -- a.2-a.7: the persistent per-point simulation kernel.
+// sim_core.cuh -- a.2-a.7: the persistent per-point simulation kernel.
+// Included by sim_base.cu (MIXED / prefill-first unified sweeps: every later feature compiled
+// out, so the common path keeps its registers and instruction count) and sim_full.cu (chunked
+// prefill, multi-round + memory cache, preload link, the P/D pair and the xP:yD node).
 //
 // ONE WARP PER POINT, pulled from an atomic longest-first queue.  The running set R and
 // the resume queue Q are one array of request slots in ascending id (R is a prefix, Q
@@ -18,6 +21,7 @@
 // PAPER.md anchors: worker loop / default end-of-iteration breakpoint P:243; continuous
 // vs static batching P:166-169; PagedAttention P:172-173; preemption
 // P:456-457; max-memory-ratio admission P:460; compute simulator P:216.
+#pragma once
 #include "dev_common.cuh"
 
 namespace ts {
@@ -76,7 +80,7 @@ __device__ __forceinline__ double roof(double F, double B, const CostK &K) {
 // NEXT-4 preload pipeline (reading R-N4), lane 0 only: n chunks, load `a`
 // once the previous load is done and a buffer slot is free (chunk i-K taken), the consumer takes
 // chunk i at S_i = max(C_{i-1}, P_i) and finishes it `b` later; ring holds S_1..S_n.
-__device__ __noinline__ double preload_pipeline(u64 n, double a, double b, u64 K, double *ring) {
+static __device__ __noinline__ double preload_pipeline(u64 n, double a, double b, u64 K, double *ring) {
   double Pv = 0.0, Cv = 0.0;
   for (u64 i = 1; i <= n; ++i) {
     double ready = Pv;
@@ -210,7 +214,7 @@ struct Logs {
   u32 nev, nit;
 };
 
-__device__ __noinline__ void ev_flush(Logs &L) {
+static __device__ __noinline__ void ev_flush(Logs &L) {
   __syncwarp();
   for (u32 x = lane_id(); x < L.nev; x += 32) {
     const uint4 e = L.ev[x];
@@ -252,7 +256,7 @@ __device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 hel
 // "serve the requesters one after another with take-the-lowest-free-block" (c.4 steps
 // 3-5, reading A14) done in one bitmap pass.  Entry iteration offsets (fast-forward)
 // shift the digest's iteration index.
-__device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl, u64 k, u32 kind_off, Logs &L,
+static __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl, u64 k, u32 kind_off, Logs &L,
                               u32 &hint, u32 nwords) {
   const bool unit = E == K;  // every requester takes one block: owner of order index o is o
   const u32 lane = lane_id();
@@ -376,7 +380,7 @@ __device__ __forceinline__ u64 sched_fold(u64 k, i64 ts, i64 T, u64 Sp, u64 D, u
 
 // iteration entry: k (worker in bit 40), t_start, T, N_p, C_d, blocks,
 // S_p | D<<16 | m<<32 | n_resumed<<48, n_admitted | n_finished<<16 | n_rejected<<32
-__device__ __noinline__ void it_flush(Logs &L) {
+static __device__ __noinline__ void it_flush(Logs &L) {
   __syncwarp();
   for (u32 x = lane_id(); x < L.nit; x += 32) {
     const ulonglong2 a = L.it[4 * x], b = L.it[4 * x + 1], c = L.it[4 * x + 2], d = L.it[4 * x + 3];
@@ -435,7 +439,7 @@ __device__ __forceinline__ i64 scan_incl_i64(i64 x) {
 #include "sim_pd.cuh"
 #include "sim_pdn.cuh"
 
-size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_y) {
+inline size_t sim_smem_per_warp_impl(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_y) {
   if (node_x) return pdn_smem_per_warp((u32)cap, nwords_max, node_x, node_y);
   return smem_per_warp_bytes((u32)cap, nwords_max) + (pd ? smem_pd_extra((u32)cap, nwords_max) : 0);
 }
@@ -547,7 +551,7 @@ __device__ __forceinline__ void mr_cache_store(MrState &M, u32 c, u32 tokens, co
 
 // ------------------------------------------------------------------ a.2-a.7 one point
 // Everything is executed by all 32 lanes; scalar state is lane-uniform in registers.
-template <int CAP>
+template <int CAP, bool FULL>
 __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S, u32 *bt) {
   static_assert(CAP % 32 == 0 && CAP <= 1024, "CAP");
   const u32 lane = lane_id();
@@ -557,7 +561,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const DevHw H = P.hw[cd.hw];
   const DevHP HP = P.hp[(size_t)cd.hw * P.n_pol + cd.pol];
   const DevPol PL = P.pol[cd.pol];
-  const CostK K = make_costk(P.M, H, P.link_mode, P.preload_buf, P.fetch_s);
+  const CostK K = make_costk(P.M, H, FULL ? P.link_mode : 0u, P.preload_buf, FULL ? P.fetch_s : 0.0);
   const u32 g = P.group_of_point_mode ? 0u : cd.rate * P.n_seeds + cd.seed;
   const u32 n = P.n_req;
   const i64 *A = P.arrival + (size_t)g * n;
@@ -571,8 +575,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const bool RATIO = PL.kind == TOKENSIM_CONT_RATIO;
   const bool STATICP = PL.kind == TOKENSIM_STATIC;
   const bool PFM = PL.mode == TOKENSIM_PREFILL_FIRST;
-  const bool CHK = PL.mode == TOKENSIM_CHUNKED;
-  const bool MRM = P.multi_round != 0;  // NEXT-2: request ids are (conversation, round) rids
+  const bool CHK = FULL && PL.mode == TOKENSIM_CHUNKED;
+  const bool MRM = FULL && P.multi_round != 0;  // NEXT-2: request ids are (conversation, round) rids
   const bool CACHE = MRM && P.memory_cache != 0;
   const u64 total = HP.total_blocks;
   const u32 nwords = HP.nwords;
@@ -1676,11 +1680,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   __syncwarp();
 }
 
-template <int CAP>
+template <int CAP, bool FULL>
 __global__ void __launch_bounds__(128) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
-  const bool pd = P.topology == TOKENSIM_PD_PAIR;
+  const bool pd = FULL && P.topology == TOKENSIM_PD_PAIR;
   const bool node = pd && P.pd_general;
   const size_t base = smem_per_warp_bytes(CAP, P.nwords_max);
   const size_t per_warp =
@@ -1694,40 +1698,45 @@ __global__ void __launch_bounds__(128) sim_kernel(SweepParams P) {
     qi = __shfl_sync(FULLMASK, qi, 0);
     if ((u64)qi >= P.n_run) break;
     const u64 j = P.order[qi];
-    if (node) simulate_pdn<CAP>(P, j, smem_raw + wib * per_warp, bt);
-    else if (pd) simulate_pd<CAP>(P, j, S, smem_raw + wib * per_warp + base, bt);
-    else simulate_unified<CAP>(P, j, S, bt);
+    if constexpr (FULL) {
+      if (node) simulate_pdn<CAP>(P, j, smem_raw + wib * per_warp, bt);
+      else if (pd) simulate_pd<CAP>(P, j, S, smem_raw + wib * per_warp + base, bt);
+      else simulate_unified<CAP, true>(P, j, S, bt);
+    } else {
+      simulate_unified<CAP, false>(P, j, S, bt);
+    }
   }
 }
 
-template <int CAP>
+// launch / occupancy helpers for one variant (instantiated by sim_base.cu / sim_full.cu)
+template <int CAP, bool FULL>
 static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  sim_kernel<CAP><<<blocks, wpb * 32, smem, st>>>(p);
+  sim_kernel<CAP, FULL><<<blocks, wpb * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
-
-cudaError_t launch_sim(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
+template <int CAP, bool FULL>
+static cudaError_t occ_t(int wpb, size_t smem, int *b) {
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP, FULL>, wpb * 32, smem);
+}
+template <bool FULL>
+static cudaError_t launch_sim_v(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
   switch (cap) {
-    case 32: return launch_sim_t<32>(p, wpb, blocks, smem, st);
-    case 256: return launch_sim_t<256>(p, wpb, blocks, smem, st);
-    case 1024: return launch_sim_t<1024>(p, wpb, blocks, smem, st);
+    case 32: return launch_sim_t<32, FULL>(p, wpb, blocks, smem, st);
+    case 256: return launch_sim_t<256, FULL>(p, wpb, blocks, smem, st);
+    case 1024: return launch_sim_t<1024, FULL>(p, wpb, blocks, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
-
-template <int CAP>
-static cudaError_t occ_t(int wpb, size_t smem, int *b) {
-  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP>, wpb * 32, smem);
-}
-cudaError_t sim_occupancy(int cap, int wpb, size_t smem, int *b) {
+template <bool FULL>
+static cudaError_t sim_occupancy_v(int cap, int wpb, size_t smem, int *b) {
   switch (cap) {
-    case 32: return occ_t<32>(wpb, smem, b);
-    case 256: return occ_t<256>(wpb, smem, b);
-    case 1024: return occ_t<1024>(wpb, smem, b);
+    case 32: return occ_t<32, FULL>(wpb, smem, b);
+    case 256: return occ_t<256, FULL>(wpb, smem, b);
+    case 1024: return occ_t<1024, FULL>(wpb, smem, b);
     default: return cudaErrorInvalidValue;
   }
 }

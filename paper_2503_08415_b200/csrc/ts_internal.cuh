@@ -111,6 +111,7 @@ struct SweepParams {
   unsigned char *pdn_scratch;  // NEXT-1 node: per-warp FIFOs, queues, holders, P block lists
   u64 pdn_bytes_per_warp;
   u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
+  u32 full, pad4;                         // 1: the full kernel variant (sim_full.cu)
   u32 link_mode, pad2;                    // NEXT-4: TOKENSIM_LINK_SEQUENTIAL | PRELOAD
   u64 preload_buf;                        // preload buffer bytes
   // NEXT-2 multi-round conversations + memory cache.  With multi_round, n_req = 7 * n_conv is
@@ -147,8 +148,15 @@ __host__ __device__ inline Coords decode_point(u64 point, u32 n_pol, u32 n_rates
 
 // launchers (sweep.cu)
 cudaError_t launch_workload(const SweepParams &p, cudaStream_t st);
-cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
-                       cudaStream_t st);
+cudaError_t launch_sim_base(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
+                            cudaStream_t st);
+cudaError_t launch_sim_full(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
+                            cudaStream_t st);
+inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
+                              cudaStream_t st) {
+  return p.full ? launch_sim_full(p, cap, warps_per_block, blocks, smem, st)
+                : launch_sim_base(p, cap, warps_per_block, blocks, smem, st);
+}
 cudaError_t launch_summary(const SweepParams &p, cudaStream_t st);
 cudaError_t launch_quantiles(const SweepParams &p, u64 j, u32 metric, const u32 *d_ranks, u32 n_q,
                              double *d_out, u64 *d_keys, cudaStream_t st);
@@ -160,6 +168,11 @@ size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_
 inline size_t pdn_global_per_warp(u64 n, u32 cap, u32 btl, u32 x, u32 y) {
   return (size_t)y * n * 32 + (size_t)x * n * 4 * 2 + (size_t)x * cap * 4 + n * 8 + n * (size_t)btl * 4 + 256;
 }
-cudaError_t sim_occupancy(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
+cudaError_t sim_occupancy_base(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
+cudaError_t sim_occupancy_full(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
+inline cudaError_t sim_occupancy(bool full, int cap, int warps_per_block, size_t smem, int *blocks_per_sm) {
+  return full ? sim_occupancy_full(cap, warps_per_block, smem, blocks_per_sm)
+              : sim_occupancy_base(cap, warps_per_block, smem, blocks_per_sm);
+}
 
 }  // namespace ts
