@@ -110,6 +110,15 @@ u64 fold(std::initializer_list<u64> f) {
 
 u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
 
+// c.6 digests (our own verification device, not a paper quantity): a block event folds
+// (k | kind << 48, id | block << 32); an iteration folds (k | worker << 40, t, T, N_p, C_d, blocks,
+// S_p | D << 16 | m << 32 | n_res << 48, n_adm | n_fin << 16 | n_rej << 32).
+u64 fold_block(u64 k, u64 kind, u64 id, u64 b) { return fold({k | (kind << 48), id | (b << 32)}); }
+u64 fold_sched(u64 kw, u64 t, u64 T, u64 Sp, u64 D, u64 Np, u64 Cd, u64 m, u64 nres, u64 nadm, u64 nrej, u64 nfin,
+               u64 blocks) {
+  return fold({kw, t, T, Np, Cd, blocks, Sp | (D << 16) | (m << 32) | (nres << 48), nadm | (nfin << 16) | (nrej << 32)});
+}
+
 // ----------------------------------------------------------------- per-worker profile
 struct Profile {
   double peak_flops, mem_bw, eff_flops, eff_bw;
@@ -546,14 +555,14 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
       const u32 b = *freeset.begin();
       freeset.erase(freeset.begin());
       req[id].blocks.push_back(b);
-      block_d += fold({k, 1, id, b});
+      block_d += fold_block(k, 1, id, b);
       if (c.keep_events) run->events.push_back({k, 1, id, b, 0});
     }
   };
   auto free_all = [&](u32 id) {
     for (u32 b : req[id].blocks) {  // logical order
       freeset.insert(b);
-      block_d += fold({k, 2, id, b});
+      block_d += fold_block(k, 2, id, b);
       if (c.keep_events) run->events.push_back({k, 2, id, b, 0});
     }
     req[id].blocks.clear();
@@ -791,8 +800,8 @@ oracle_run *simulate_unified(const oracle_cfg &c) {
         ++n_fin;
       }
     }
-    sched_d += fold({k, (u64)ts, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej,
-                     n_fin, blocks});
+    sched_d += fold_sched(k, (u64)ts, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej,
+                     n_fin, blocks);
     run->iters.push_back({k, ts, T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej, n_fin,
                           blocks, 0, 0});
     req_iters += entries;
@@ -911,7 +920,7 @@ oracle_run *simulate_pd(const oracle_cfg &c) {
   u64 peakD = 0, bnsD = 0, n_xfer = 0, xfer_bytes = 0;
 
   auto ev = [&](u64 k, u32 kind, u32 worker, u32 id, u32 b) {
-    block_d += fold({k, kind + 2 * worker, id, b});
+    block_d += fold_block(k, kind + 2 * worker, id, b);
     if (c.keep_events) run->events.push_back({k, kind, id, b, worker});
   };
   auto finish_req = [&](u32 id, i64 te, u64 k) {
@@ -1113,8 +1122,8 @@ oracle_run *simulate_pd(const oracle_cfg &c) {
           ++n_fin;
         }
       }
-      sched_d += fold({kD | (1ull << 40), (u64)t, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0, n_fin,
-                       blocks});
+      sched_d += fold_sched(kD | (1ull << 40), (u64)t, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0, n_fin,
+                       blocks);
       run->iters.push_back({kD, t, T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0, n_fin, blocks, 1, 0});
       req_iters += entries;
       peakD = std::max(peakD, blocks);
@@ -1204,7 +1213,7 @@ oracle_run *simulate_pd(const oracle_cfg &c) {
           pholders.push_back(id);
         }
       }
-      sched_d += fold({kP, (u64)t, (u64)T, pf.size(), 0, Np, 0, 0, 0, batch.size(), n_rej, n_fin, blocks});
+      sched_d += fold_sched(kP, (u64)t, (u64)T, pf.size(), 0, Np, 0, 0, 0, batch.size(), n_rej, n_fin, blocks);
       run->iters.push_back({kP, t, T, pf.size(), 0, Np, 0, 0, 0, batch.size(), n_rej, n_fin, blocks, 0, 0});
       req_iters += batch.size();
       tP = te;
@@ -1363,7 +1372,7 @@ oracle_run *simulate_pdn(const oracle_cfg &c) {
   u64 n_xfer = 0, xfer_bytes = 0;
 
   auto ev = [&](u64 k, u32 kind, u32 worker, u32 id, u32 b) {
-    block_d += fold({k, kind + 2 * worker, id, b});
+    block_d += fold_block(k, kind + 2 * worker, id, b);
     if (c.keep_events) run->events.push_back({k, kind, id, b, worker});
   };
   auto finish_req = [&](u32 id, i64 te, u64 k) {
@@ -1629,8 +1638,8 @@ oracle_run *simulate_pdn(const oracle_cfg &c) {
           ++n_fin;
         }
       }
-      sched_d += fold({w.k | ((u64)wid << 40), (u64)t, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0,
-                       n_fin, blocks});
+      sched_d += fold_sched(w.k | ((u64)wid << 40), (u64)t, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0,
+                       n_fin, blocks);
       run->iters.push_back({w.k, t, T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, 0, n_fin, blocks, wid, 0});
       req_iters += entries;
       w.peak = std::max(w.peak, blocks);
@@ -1719,8 +1728,8 @@ oracle_run *simulate_pdn(const oracle_cfg &c) {
           w.holders.insert(id);
         }
       }
-      sched_d += fold({w.k | ((u64)i << 40), (u64)t, (u64)T, w.batch.size(), 0, Np, 0, 0, 0, w.batch.size(), n_rej,
-                       n_fin, blocks});
+      sched_d += fold_sched(w.k | ((u64)i << 40), (u64)t, (u64)T, w.batch.size(), 0, Np, 0, 0, 0, w.batch.size(), n_rej,
+                       n_fin, blocks);
       run->iters.push_back({w.k, t, T, w.batch.size(), 0, Np, 0, 0, 0, w.batch.size(), n_rej, n_fin, blocks, i, 0});
       req_iters += w.batch.size();
       w.tdisp = te;  // the batch goes to the global scheduler at te
@@ -1955,14 +1964,14 @@ oracle_run *simulate_mr(const oracle_cfg &c) {
       const u32 b = *freeset.begin();
       freeset.erase(freeset.begin());
       req[rid].blocks.push_back(b);
-      block_d += fold({k, 1, rid, b});
+      block_d += fold_block(k, 1, rid, b);
       if (c.keep_events) run->events.push_back({k, 1, rid, b, 0});
     }
   };
   auto free_all = [&](u32 rid) {
     for (u32 b : req[rid].blocks) {
       freeset.insert(b);
-      block_d += fold({k, 2, rid, b});
+      block_d += fold_block(k, 2, rid, b);
       if (c.keep_events) run->events.push_back({k, 2, rid, b, 0});
     }
     req[rid].blocks.clear();
@@ -2223,7 +2232,7 @@ oracle_run *simulate_mr(const oracle_cfg &c) {
         }
       }
     }
-    sched_d += fold({k, (u64)ts, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej, n_fin, blocks});
+    sched_d += fold_sched(k, (u64)ts, (u64)T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej, n_fin, blocks);
     run->iters.push_back({k, ts, T, pf.size(), dec.size(), Np, Cd, m, n_res, n_adm, n_rej, n_fin, blocks, 0, 0});
     req_iters += entries;
     peak = std::max(peak, blocks);

@@ -67,12 +67,11 @@ __device__ __forceinline__ u64 mix64(u64 x) {
   return x;
 }
 #define FOLD_INIT 0x9E3779B97F4A7C15ull
-__device__ __forceinline__ u64 fold4(u64 a, u64 b, u64 c, u64 d) {
+// block event (k, kind, id, block) -> fold(k | kind << 48, id | block << 32)
+__device__ __forceinline__ u64 fold_event(u32 k, u32 kind, u32 id, u32 blk) {
   u64 h = FOLD_INIT;
-  h = mix64(h ^ a);
-  h = mix64(h ^ b);
-  h = mix64(h ^ c);
-  h = mix64(h ^ d);
+  h = mix64(h ^ ((u64)k | ((u64)kind << 48)));
+  h = mix64(h ^ ((u64)id | ((u64)blk << 32)));
   return h;
 }
 

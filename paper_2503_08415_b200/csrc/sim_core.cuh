@@ -218,7 +218,7 @@ static __device__ __noinline__ void ev_flush(Logs &L) {
   __syncwarp();
   for (u32 x = lane_id(); x < L.nev; x += 32) {
     const uint4 e = L.ev[x];
-    L.dig_b += fold4(e.x, e.y, e.z, e.w);
+    L.dig_b += fold_event(e.x, e.y, e.z, e.w);
   }
   L.nev = 0;
   __syncwarp();
@@ -359,22 +359,18 @@ __device__ __forceinline__ void write_record(tokensim_request_record *r, i64 ttf
   q[1] = make_ulonglong2((unsigned long long)mt, (unsigned long long)w3);
 }
 
-__device__ __forceinline__ u64 sched_fold(u64 k, i64 ts, i64 T, u64 Sp, u64 D, u64 Np, u64 Cd, u64 m, u64 nres,
-                                          u64 nadm, u64 nrej, u64 nfin, u64 blocks) {
+// iteration digest term: fold(k | worker << 40, t, T, N_p, C_d, blocks,
+//                            S_p | D << 16 | m << 32 | n_res << 48, n_adm | n_fin << 16 | n_rej << 32)
+__device__ __forceinline__ u64 sched_fold(u64 k, i64 ts, i64 T, u64 Np, u64 Cd, u64 blocks, u64 w6, u64 w7) {
   u64 h = FOLD_INIT;
   h = mix64(h ^ k);
   h = mix64(h ^ (u64)ts);
   h = mix64(h ^ (u64)T);
-  h = mix64(h ^ Sp);
-  h = mix64(h ^ D);
   h = mix64(h ^ Np);
   h = mix64(h ^ Cd);
-  h = mix64(h ^ m);
-  h = mix64(h ^ nres);
-  h = mix64(h ^ nadm);
-  h = mix64(h ^ nrej);
-  h = mix64(h ^ nfin);
   h = mix64(h ^ blocks);
+  h = mix64(h ^ w6);
+  h = mix64(h ^ w7);
   return h;
 }
 
@@ -388,7 +384,7 @@ static __device__ __noinline__ void it_flush(Logs &L) {
     const i64 ts = (i64)a.y, T = (i64)b.x;
     const u64 Sp = w6 & 0xffff, D = (w6 >> 16) & 0xffff, m = (w6 >> 32) & 0xffff, nres = w6 >> 48;
     const u64 nadm = w7 & 0xffff, nfin = (w7 >> 16) & 0xffff, nrej = w7 >> 32;
-    L.dig_s += sched_fold(k, ts, T, Sp, D, Np, Cd, m, nres, nadm, nrej, nfin, blocks);
+    L.dig_s += sched_fold(k, ts, T, Np, Cd, blocks, w6, w7);
     const u64 idx = L.it_base + x;
     if (idx < L.it_cap) {
       tokensim_iter_record ir;
@@ -1681,7 +1677,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
 }
 
 template <int CAP, bool FULL>
-__global__ void __launch_bounds__(128) sim_kernel(SweepParams P) {
+__global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
   const bool pd = FULL && P.topology == TOKENSIM_PD_PAIR;
