@@ -81,6 +81,21 @@ def test_create_and_grid(T):
                                                trace_prompt=[1, 1], trace_output=[1, 1])), b"trace_arrival_ns[1]"),
     (lambda c: replace(c, workload=si.Workload(1, [1.0], [0], len_dist=si.FIXED, prompt_a=2000, output_a=100)),
      b"prompt_a/output_a"),
+    # NEXT-3b: chunked prefill needs a budget >= max_num_seqs
+    (lambda c: replace(c, policies=[si.Policy(iteration_mode=si.CHUNKED, max_batched_tokens=8, max_num_seqs=16)]),
+     b"CHUNKED needs max_batched_tokens"),
+    # NEXT-1: at most 8 workers per node; a known dispatch policy
+    (lambda c: replace(c, options=si.Options(topology=si.PD_PAIR, pd_prefill=4, pd_decode=5)), b"at most 8"),
+    # a.9 / NEXT-1: P/D workers are prefill-only / decode-only
+    (lambda c: replace(c, policies=[si.Policy(iteration_mode=si.PREFILL_FIRST)],
+                       options=si.Options(topology=si.PD_PAIR)), b"iteration_mode"),
+    # NEXT-4: a preload link needs a buffer
+    (lambda c: replace(c, options=si.Options(link_mode=si.PRELOAD, preload_buffer_bytes=0)), b"preload_buffer_bytes"),
+    # NEXT-2: the memory cache needs multi-round conversations; those need generated lengths
+    (lambda c: replace(c, options=si.Options(memory_cache=True)), b"memory_cache"),
+    (lambda c: replace(c, workload=si.Workload(2, [1.0], [0], len_dist=si.TRACE, trace_arrival_ns=[0, 1],
+                                               trace_prompt=[1, 1], trace_output=[1, 1], multi_round=True)),
+     b"multi_round"),
 ])
 def test_create_validation_messages(T, mutate, needle):
     from paper_2503_08415_b200 import TokensimError
