@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtokensim.so")
+LIB_PATH = os.environ.get("TOKENSIM_LIB") or os.path.join(_HERE, "libtokensim.so")  # env: A/B builds
 
 u8, u16, u32, u64, i64, f64 = C.c_uint8, C.c_uint16, C.c_uint32, C.c_uint64, C.c_int64, C.c_double
 PU32, PU64, PI64, PF64 = C.POINTER(u32), C.POINTER(u64), C.POINTER(i64), C.POINTER(f64)
