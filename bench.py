@@ -69,6 +69,11 @@ WORKLOAD_DESC = {
     "c3": "C3: LLaMA-2-7B hardware sweep 16 F x 16 B x 6 C x {STATIC, CONT, CONT_RATIO 0.9}, 10k requests, 4,608 points",
     "c4": "C4: LLaMA-2-70B TP 2/4/8 x {CONT, CONT_RATIO 0.9} x {SWAP, RECOMPUTE} x 16 rates x 12 seeds, 10k req, 2,304 points",
     "c5": "C5: 1P:1D pairs 16x16 x {SWAP, RECOMPUTE} x 16 rates, 10k requests; 8,192 points (one seed) per GPU, 65,536 at 8 GPUs",
+    # widened rows; measurement only, not BASELINE configs
+    "c6": "NEXT-1: P2:D6 node, LLaMA-2-7B, least-outstanding dispatch, {SWAP, RECOMPUTE} x 16 rates x 8 seeds, 10k req, 256 points",
+    "c7": "NEXT-2: multi-round conversations + memory cache, LLaMA-2-7B, 2k conversations, {SWAP, RECOMPUTE} x 16 rates x 8 seeds",
+    "c8": "NEXT-3: C2 grid x {MIXED, PREFILL_FIRST, CHUNKED 512}, LLaMA-2-13B, 1k requests, 384 points",
+    "c9": "NEXT-4: LLaMA-2-70B TP2 SWAP under a 64 MiB preload link, {CONT, CONT_RATIO} x 16 rates x 12 seeds, 10k req",
 }
 
 

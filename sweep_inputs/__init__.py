@@ -245,7 +245,45 @@ def c5() -> SweepConfig:
                        Options(topology=PD_PAIR))
 
 
-PRESETS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
+# ---- sweeps for the SURVEY §8(f) rows (measurement of each widened row; not BASELINE configs)
+def c6() -> SweepConfig:
+    """NEXT-1: one 8-GPU node as P2:D6 (fig:pd shape), LLaMA-2-7B on A100-like workers,
+    least-outstanding dispatch, {SWAP, RECOMPUTE} x 16 rates (3 x 2^(k/4) req/s) x 8 seeds,
+    10k requests: 256 points."""
+    pols = [Policy(preempt=SWAP), Policy(preempt=RECOMPUTE)]
+    rates = [3.0 * 2.0 ** (k / 4.0) for k in range(16)]
+    return SweepConfig("c6", LLAMA2_7B, [A100], pols, Workload(10_000, rates, list(range(8))),
+                       Options(topology=PD_PAIR, pd_prefill=2, pd_decode=6, dispatch=LEAST_OUTSTANDING))
+
+
+def c7() -> SweepConfig:
+    """NEXT-2: multi-round conversations with the host memory cache (Finding 6 shape),
+    LLaMA-2-7B, 2,000 conversations (half single-round, else 2..7 rounds, 5 s think time),
+    CONT x {SWAP, RECOMPUTE} x 16 rates (0.5 x 2^(k/4)) x 8 seeds: 256 points."""
+    pols = [Policy(preempt=SWAP), Policy(preempt=RECOMPUTE)]
+    rates = [0.5 * 2.0 ** (k / 4.0) for k in range(16)]
+    return SweepConfig("c7", LLAMA2_7B, [A100], pols,
+                       Workload(2_000, rates, list(range(8)), multi_round=True, think_mean_s=5.0),
+                       Options(memory_cache=True))
+
+
+def c8() -> SweepConfig:
+    """NEXT-3: the C2 grid under {MIXED, PREFILL_FIRST, CHUNKED (512-token budget)} iterations:
+    384 points."""
+    pols = [Policy(), Policy(iteration_mode=PREFILL_FIRST), Policy(iteration_mode=CHUNKED, max_batched_tokens=512)]
+    return SweepConfig("c8", LLAMA2_13B, [A100], pols, Workload(1000, [float(r) for r in range(1, 17)], list(range(8))))
+
+
+def c9() -> SweepConfig:
+    """NEXT-4: C4's preemption-heavy TP2 profile with SWAP under a 64 MiB preload link,
+    {CONT, CONT_RATIO 0.9} x 16 rates x 12 seeds, 10k requests: 384 points."""
+    pols = [Policy(kind=k, preempt=SWAP, max_mem_ratio=r) for (k, r) in ((CONT, 1.0), (CONT_RATIO, 0.9))]
+    rates = [0.5 * 2.0 ** (k / 4.0) for k in range(16)]
+    return SweepConfig("c9", LLAMA2_70B, c4_hws()[:1], pols, Workload(10_000, rates, list(range(12))),
+                       Options(link_mode=PRELOAD, preload_buffer_bytes=64 << 20))
+
+
+PRESETS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5, "c6": c6, "c7": c7, "c8": c8, "c9": c9}
 
 
 def with_requests(cfg: SweepConfig, n: int) -> SweepConfig:
