@@ -579,7 +579,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const u32 btl = P.bt_len;
   const u32 mns = PL.mns, mbt = PL.mbt;
   const i64 wm = (i64)PL.wm;
-  const bool ff_on = P.ff_enable != 0 && !MRM;  // multi-round points step one iteration at a time
+  const bool ff_on = P.ff_enable != 0;
   const long long clk0 = clock64();
 
   // ---- init: records, bitmap, slot pool
@@ -788,7 +788,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           hd_idx = adm;
           const u32 off = adm - win;
           const u32 pw = __shfl_sync(FULLMASK, wp, off & 31u);
-          hd_p = (adm >= win && off < 32) ? pw : PR[adm];
+          hd_p = MRM ? PR[mr.wq_id[adm]] : ((adm >= win && off < 32) ? pw : PR[adm]);
         }
         need_h = B.cdiv(hd_p);
         // prefill-first admits before any decode block: no decode tokens, no decode blocks
@@ -843,11 +843,17 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         // cut: the stretch is the longest prefix of iterations that stay quiescent; the
         // last one may finish requests (rem reaching 0), no earlier one may
         // (warp collectives stay outside lane-dependent branches)
-        const i64 a_next = __shfl_sync(FULLMASK, wa, (arr - win) & 31u);
+        i64 a_next = __shfl_sync(FULLMASK, wa, (arr - win) & 31u);
+        bool more = arr < n;
+        if (MRM) {  // the next round-0 arrival or pending follow-up round
+          u32 cv;
+          bool f0;
+          more = mr_next(mr, A, a_next, cv, f0);
+        }
         bool ok = ((u64)Aj <= nfree) && (Aj <= (u32)CAP) && (lane < rm);
         if (lane > 0) {
           if (P.horizon >= 0 && tsj >= P.horizon) ok = false;
-          if (nQ == 0 && adm == arr && arr < n && tsj >= a_next) ok = false;
+          if (nQ == 0 && adm == arr && more && tsj >= a_next) ok = false;
         }
         if (mem_check) {  // head blocked by memory at this boundary? (then for the whole stretch)
           const u64 n0 = (u64)__shfl_sync(FULLMASK, Aj, 0);
@@ -994,6 +1000,17 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, 0, L, hint);
               nfree += held;
               if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
+              if (MRM) {  // NEXT-2: store the context; schedule the conversation's next round
+                const u32 rid = S.id[pos];
+                const u32 cv = mr.CONV[rid];
+                const u32 r = rid - mr.BASE[cv];
+                if (CACHE) mr_cache_store(mr, cv, PR[rid] + OU[rid] - 1u, B);
+                if (r + 1 < mr.NR[cv]) {
+                  mr.nxr[cv] = r + 1;
+                  mr_heap_push(mr, tend + A[rid + 1], cv);
+                }
+                __syncwarp();
+              }
             }
           }
           __syncwarp();

@@ -440,3 +440,5 @@ def test_multi_round_cache_parity(api):
         check_points(sw, cfg, list(range(cfg.num_points)), records=True, trace=True)
         s = sw.summaries()
         assert (s["n_requests"] > 300).all() and (s["n_finished"] == s["n_requests"]).all()
+        off = run_gpu(api, replace(cfg, options=replace(cfg.options, fast_forward=False)))
+        assert sw.summaries().tobytes() == off.summaries().tobytes()
