@@ -442,3 +442,18 @@ def test_multi_round_cache_parity(api):
         assert (s["n_requests"] > 300).all() and (s["n_finished"] == s["n_requests"]).all()
         off = run_gpu(api, replace(cfg, options=replace(cfg.options, fast_forward=False)))
         assert sw.summaries().tobytes() == off.summaries().tobytes()
+
+
+def test_widened_row_presets_sampled(api):
+    """The bench sweeps of the widened rows (c6 node, c7 multi-round + cache, c8 prefill-first /
+    chunked, c9 preload link) at full size on the GPU, checked against the oracle on samples."""
+    for name, target in (("c6", 4), ("c7", 8), ("c8", 10), ("c9", 6)):
+        cfg = si.PRESETS[name]()
+        sw = run_gpu(api, cfg)
+        s = sw.summaries()
+        assert (s["n_finished"] + s["n_rejected"] == s["n_requests"]).all(), name
+        pts = sample_points(cfg.num_points, target=target, corners=[0, cfg.num_points - 1])
+        if cfg.options.topology == si.PD_PAIR:
+            check_pd_points(sw, cfg, pts)
+        else:
+            check_points(sw, cfg, pts, records=True)
