@@ -457,3 +457,31 @@ def test_widened_row_presets_sampled(api):
             check_pd_points(sw, cfg, pts)
         else:
             check_points(sw, cfg, pts, records=True)
+
+
+def test_edge_shapes(api):
+    """Edge shapes: non-power-of-two block sizes (the div/mod path of BSz), max_num_seqs > 256
+    (the CAP = 1024 kernel instantiation) and max_num_seqs = 1024, on the unified worker, the P/D
+    pair, a node, chunked prefill and multi-round workloads."""
+    rng = np.random.default_rng(97)
+    for bs, mns in ((12, 8), (20, 256), (7, 600), (16, 1024), (5, 1024)):
+        for _ in range(3):
+            c = _micro(rng)
+            mml = c.model.max_model_len
+            pol = replace(c.policies[0], block_size=bs, max_num_seqs=mns, watermark_blocks=0)
+            hw = replace(c.hws[0], kv_blocks_override=int(rng.integers(-(-mml // bs), -(-mml // bs) + 50)))
+            c = replace(c, policies=[pol], hws=[hw])
+            check_points(run_gpu(api, c), c, [0], records=True, trace=True, iters=True)
+            cc = replace(c, policies=[replace(pol, iteration_mode=si.CHUNKED, max_batched_tokens=max(mns, 64))])
+            check_points(run_gpu(api, cc), cc, [0], records=True, iters=True)
+        p = _micro_pd(rng)
+        ppol = replace(p.policies[0], block_size=bs, max_num_seqs=mns)
+        phws = [replace(h, kv_blocks_override=int(rng.integers(-(-128 // bs), -(-128 // bs) + 30))) for h in p.hws]
+        p = replace(p, policies=[ppol], hws=phws)
+        check_pd_points(run_gpu(api, p), p, list(range(p.num_points)), iters=True)
+        pn = replace(p, options=replace(p.options, pd_prefill=2, pd_decode=2))
+        check_pd_points(run_gpu(api, pn), pn, list(range(pn.num_points)), iters=True)
+        m = _micro_mr(rng)
+        m = replace(m, policies=[replace(m.policies[0], block_size=bs, max_num_seqs=mns)],
+                    hws=[replace(m.hws[0], kv_blocks_override=int(rng.integers(-(-512 // bs), -(-512 // bs) + 60)))])
+        check_points(run_gpu(api, m), m, [0], records=True, iters=True)
