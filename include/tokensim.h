@@ -322,6 +322,9 @@ typedef struct {
   uint64_t normal_phase_cycles[8];  /* normal iterations: reservation+preemption / resume /
                                        admission / block allocation / cost / commit pass /
                                        compaction / digests+trace                           */
+  uint64_t ff_failed[5];  /* unified worker: fast-forward attempts that did not run (< 2
+                             iterations), by what stopped them: an admission/resume was possible /
+                             memory / the next arrival / the blocked head unblocks / other */
 } tokensim_point_profile;
 tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t point, tokensim_point_profile *out);
 

@@ -245,6 +245,7 @@ class Sweep:
         d = {n: getattr(pp, n) for n, _ in T.PointProfile._fields_}
         d["stretch_phase_cycles"] = list(d["stretch_phase_cycles"])
         d["normal_phase_cycles"] = list(d["normal_phase_cycles"])
+        d["ff_failed"] = list(d["ff_failed"])
         return d
 
     def workload(self, point: int):

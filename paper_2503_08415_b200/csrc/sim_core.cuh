@@ -647,6 +647,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   long long clk_a = 0, clk_p = 0;
   u64 ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   u64 nph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  u32 ffr[5] = {0, 0, 0, 0, 0};  // failed fast-forward attempts: not quiet / memory / arrival / head / other
 #define NPH(i)                           \
   do {                                   \
     const long long _c = clock64();      \
@@ -803,6 +804,17 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             quiet = false;
         }
       }
+      // cheap predictors of a failed attempt (they only choose the path, never the result): the
+      // running set needs about ceil(nR / bs) blocks per iteration -- with fewer free blocks the
+      // stretch is cut at once by memory, and a head that still fits after that many is likely
+      // admitted by the exact check below
+      if (quiet) {
+        const u64 est = B.cdiv(nR);
+        if (nfree < est) quiet = false;
+        else if (mem_check && (i64)nfree - (i64)est - (i64)need_h >= wm &&
+                 (!ratio_h || (total - nfree + est) + need_h <= HP.ratio_limit))
+          quiet = false;
+      }
       if (quiet) {
         // pass over R: C_d(0), min rem, and the needs histogram by iteration offset (lane j
         // <-> iteration k+j).  A slot needs a block at offsets j = j0 (mod bs), j0 = -ctx mod bs,
@@ -851,18 +863,29 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           more = mr_next(mr, A, a_next, cv, f0);
         }
         bool ok = ((u64)Aj <= nfree) && (Aj <= (u32)CAP) && (lane < rm);
+        u32 why = ((u64)Aj > nfree ? 1u : 0u) | (lane >= rm ? 2u : 0u);  // observability: cut reasons
         if (lane > 0) {
           if (P.horizon >= 0 && tsj >= P.horizon) ok = false;
-          if (nQ == 0 && adm == arr && more && tsj >= a_next) ok = false;
+          if (nQ == 0 && adm == arr && more && tsj >= a_next) {
+            ok = false;
+            why |= 4u;
+          }
         }
         if (mem_check) {  // head blocked by memory at this boundary? (then for the whole stretch)
           const u64 n0 = (u64)__shfl_sync(FULLMASK, Aj, 0);
           const u64 fr = nfree - ((PFM && nQ == 0) ? 0ull : n0);
           const bool blocked = ((i64)fr - (i64)need_h < wm) || (ratio_h && (total - fr) + need_h > HP.ratio_limit);
-          if (!blocked) ok = false;
+          if (!blocked) {
+            ok = false;
+            why |= 8u;
+          }
         }
         const u32 okm = __ballot_sync(FULLMASK, ok);
         const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+        if (J < 2) {
+          const u32 w = __shfl_sync(FULLMASK, why, J);
+          ffr[(w & 1u) ? 1 : (w & 4u) ? 2 : (w & 8u) ? 3 : 4] += 1;
+        }
         // a stretch cut short by memory will not grow until blocks come back: remember the level
         const u32 memcut = __ballot_sync(FULLMASK, !((u64)Aj <= nfree));
         if (J < 2 && memcut && (u32)(__ffs(memcut) - 1) < 2) {
@@ -1110,6 +1133,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           continue;
         }
       }
+      if (!quiet) ffr[0] += 1;
       rmin = 0;  // retry only after the next normal commit recomputes it
       const long long c1 = clock64();
       cyc_ff_fail += (u64)(c1 - clk_a);
@@ -1688,6 +1712,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     for (int q = 0; q < 8; ++q) st.phase[q] = ph[q];
     for (int q = 0; q < 8; ++q) st.nphase[q] = nph[q];
     st.n_req = MRM ? mr.ntot : n;
+    for (int q = 0; q < 5; ++q) st.ff_fail[q] = ffr[q];
     P.stats[j] = st;
   }
   __syncwarp();

@@ -61,6 +61,7 @@ struct SimStats {
   u64 phase[8];                         // stretch phases: pass/cost/list+alloc/update/fold/trace/compact/tail
   u64 nphase[8];                        // normal-iteration phases (see tokensim_point_profile)
   u64 n_req;                            // requests of this point (NEXT-2: rounds; else n_req)
+  u64 ff_fail[5];                       // failed fast-forward attempts by reason (see the profile)
 };
 
 struct SweepParams {

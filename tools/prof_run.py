@@ -55,3 +55,4 @@ if os.environ.get("PROFILE_POINTS"):
         ns = max(1, x["ff_stretches"])
         print("     stretch phases (cycles/stretch):", " ".join("%.0f" % (c / ns) for c in x["stretch_phase_cycles"]))
         print("     normal phases (cycles/iter):", " ".join("%.0f" % (c / nn) for c in x["normal_phase_cycles"]))
+        print("     failed FF attempts (not quiet / memory / arrival / head / other):", x["ff_failed"])
