@@ -325,6 +325,8 @@ typedef struct {
   uint64_t ff_failed[5];  /* unified worker: fast-forward attempts that did not run (< 2
                              iterations), by what stopped them: an admission/resume was possible /
                              memory / the next arrival / the blocked head unblocks / other */
+  uint64_t ff_cut[5];     /* what ended each stretch: memory / a finishing request / the next
+                             arrival / the blocked head / 32 iterations or other */
 } tokensim_point_profile;
 tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t point, tokensim_point_profile *out);
 

@@ -78,7 +78,7 @@ class PointProfile(C.Structure):
     _fields_ = [("n_iterations", u64), ("ff_iterations", u64), ("ff_stretches", u64), ("sm_cycles", u64),
                 ("cycles_ff", u64), ("cycles_ff_failed", u64), ("cycles_normal", u64),
                 ("stretch_phase_cycles", u64 * 8), ("n_transfers", u64), ("transfer_bytes", u64),
-                ("normal_phase_cycles", u64 * 8), ("ff_failed", u64 * 5)]
+                ("normal_phase_cycles", u64 * 8), ("ff_failed", u64 * 5), ("ff_cut", u64 * 5)]
 
 
 class RunInfo(C.Structure):

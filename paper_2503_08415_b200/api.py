@@ -246,6 +246,7 @@ class Sweep:
         d["stretch_phase_cycles"] = list(d["stretch_phase_cycles"])
         d["normal_phase_cycles"] = list(d["normal_phase_cycles"])
         d["ff_failed"] = list(d["ff_failed"])
+        d["ff_cut"] = list(d["ff_cut"])
         return d
 
     def workload(self, point: int):

@@ -970,6 +970,7 @@ tokensim_status tokensim_get_point_profile(const tokensim_sweep *hc, uint64_t po
   for (int q = 0; q < 8; ++q) out->normal_phase_cycles[q] = st.nphase[q];
   for (int q = 0; q < 8; ++q) out->stretch_phase_cycles[q] = st.phase[q];
   for (int q = 0; q < 5; ++q) out->ff_failed[q] = st.ff_fail[q];
+  for (int q = 0; q < 5; ++q) out->ff_cut[q] = st.ff_cut[q];
   return TOKENSIM_OK;
 }
 

@@ -648,6 +648,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   u64 ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   u64 nph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   u32 ffr[5] = {0, 0, 0, 0, 0};  // failed fast-forward attempts: not quiet / memory / arrival / head / other
+  u32 ffc[5] = {0, 0, 0, 0, 0};  // stretches ended by memory / a finish / an arrival / the head / 32 or other
 #define NPH(i)                           \
   do {                                   \
     const long long _c = clock64();      \
@@ -885,6 +886,9 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         if (J < 2) {
           const u32 w = __shfl_sync(FULLMASK, why, J);
           ffr[(w & 1u) ? 1 : (w & 4u) ? 2 : (w & 8u) ? 3 : 4] += 1;
+        } else {  // what ended a stretch: memory / a finish / an arrival / the head / 32 or other
+          const u32 w = J < 32 ? __shfl_sync(FULLMASK, why, J) : 0u;
+          ffc[(w & 1u) ? 0 : (w & 2u) ? 1 : (w & 4u) ? 2 : (w & 8u) ? 3 : 4] += 1;
         }
         // a stretch cut short by memory will not grow until blocks come back: remember the level
         const u32 memcut = __ballot_sync(FULLMASK, !((u64)Aj <= nfree));
@@ -1713,6 +1717,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     for (int q = 0; q < 8; ++q) st.nphase[q] = nph[q];
     st.n_req = MRM ? mr.ntot : n;
     for (int q = 0; q < 5; ++q) st.ff_fail[q] = ffr[q];
+    for (int q = 0; q < 5; ++q) st.ff_cut[q] = ffc[q];
     P.stats[j] = st;
   }
   __syncwarp();

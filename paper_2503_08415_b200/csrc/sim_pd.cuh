@@ -1099,6 +1099,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     for (int q = 0; q < 8; ++q) st.nphase[q] = 0;
     st.n_req = P.n_req;
     for (int q = 0; q < 5; ++q) st.ff_fail[q] = 0;
+    for (int q = 0; q < 5; ++q) st.ff_cut[q] = 0;
     P.stats[j] = st;
   }
   __syncwarp();

@@ -62,6 +62,7 @@ struct SimStats {
   u64 nphase[8];                        // normal-iteration phases (see tokensim_point_profile)
   u64 n_req;                            // requests of this point (NEXT-2: rounds; else n_req)
   u64 ff_fail[5];                       // failed fast-forward attempts by reason (see the profile)
+  u64 ff_cut[5];                        // what ended each stretch (see the profile)
 };
 
 struct SweepParams {

@@ -44,6 +44,8 @@ if os.environ.get("PROFILE_POINTS"):
     X = np.stack([normal, st, ri], 1)
     coef, *_ = np.linalg.lstsq(X, cy, rcond=None)
     print("cycles ~ %.0f/normal-iter + %.0f/stretch + %.2f/req-iter" % tuple(coef))
+    cuts = np.array([x["ff_cut"] for x in prof], dtype=np.float64).sum(0)
+    print("all points: stretches ended by (memory / finish / arrival / head / 32+other):", cuts.astype(int).tolist())
     order = np.argsort(-cy)[:6]
     for p in order:
         x = prof[p]
@@ -56,3 +58,4 @@ if os.environ.get("PROFILE_POINTS"):
         print("     stretch phases (cycles/stretch):", " ".join("%.0f" % (c / ns) for c in x["stretch_phase_cycles"]))
         print("     normal phases (cycles/iter):", " ".join("%.0f" % (c / nn) for c in x["normal_phase_cycles"]))
         print("     failed FF attempts (not quiet / memory / arrival / head / other):", x["ff_failed"])
+        print("     stretches ended by (memory / finish / arrival / head / 32+other):", x["ff_cut"])
