@@ -218,6 +218,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
   u64 ffw = 0, ffk = 0;       // memory-cut retry guard (as in the unified worker)
   u64 ff_iters = 0, ff_runs = 0;
   u64 nit = 0;  // iteration records are kept in processing order across both workers
+  u64 cyc_ffD = 0, cyc_failD = 0, cyc_normD = 0;
   const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
   const bool FULLT = P.trace_mode == TOKENSIM_TRACE_FULL;
   const i64 W = (i64)P.bin_ns;
@@ -260,6 +261,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     if (tD <= tP) {
       // ============================================================ D boundary
       const i64 t = tD;
+      long long cD = clock64();  // observability: cycles by path (point profile)
       // 1. finished transfers become runnable (the in-flight tail completes in FIFO order)
       while (nX > 0 && xhead_end <= t) {
         const u32 pos = nD - nX;
@@ -563,10 +565,14 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
             lastD = tend;
             kD += J;
             D_idle = false;
+            cyc_ffD += (u64)(clock64() - cD);
             continue;
           }
         }
         rminD = 0;
+        const long long c1 = clock64();
+        cyc_failD += (u64)(c1 - cD);
+        cD = c1;
       }
       const u32 nA = nD - nX;  // running + preempted prefix
       // 3. decode reservation: RUN slots needing a block -> requester list (ascending id)
@@ -879,6 +885,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       lastD = te;
       ++kD;
       D_idle = false;
+      cyc_normD += (u64)(clock64() - cD);
     } else {
       // ============================================================ P boundary
       const i64 t = tP;
@@ -1093,8 +1100,9 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     st.ff_iters = ff_iters;
     st.ff_runs = ff_runs;
     st.cycles = (u64)(clock64() - clk0);
-    st.cyc_ff = st.cyc_ff_fail = 0;
-    st.cyc_normal = st.cycles;
+    st.cyc_ff = cyc_ffD;        // D: fast-forward stretches
+    st.cyc_ff_fail = cyc_failD;  // D: attempts that did not run
+    st.cyc_normal = cyc_normD;   // D: normal iterations (the rest: P, dispatch, idle D boundaries)
     for (int q = 0; q < 8; ++q) st.phase[q] = 0;
     for (int q = 0; q < 8; ++q) st.nphase[q] = 0;
     st.n_req = P.n_req;
