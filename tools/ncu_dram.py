@@ -1,0 +1,61 @@
+"""Run on the GPU box (short kernels only: a full-set capture replays the kernel ~40 times): one `ncu --set full` capture of the sim kernel for a preset and a JSON
+summary (DRAM bytes per launch for bench.py's roofline `traffic`, issue and stall shares).
+
+    python tools/ncu_dram.py c2 [out_dir]
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+cfg = sys.argv[1]
+out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/ncu"
+os.makedirs(out, exist_ok=True)
+rep = os.path.join(out, f"sim_{cfg}")
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "-k", "regex:sim_kernel",
+       "-c", "1", "-f", "-o", rep, sys.executable, os.path.join(root, "tools", "prof_run.py"), "--config", cfg]
+subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+raw = subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "raw", "--csv", "--print-units", "base"], check=True,
+                     capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units, vals = rows[0], rows[1], rows[2]
+d = dict(zip(hdr, vals))
+
+
+def f(name):
+    try:
+        return float(d[name].replace(",", ""))
+    except (KeyError, ValueError):
+        return None
+
+
+stalls = {}
+for k in hdr:
+    if k.startswith("smsp__average_warp_latency_issue_stalled_") and k.endswith(".ratio"):
+        stalls[k[len("smsp__average_warp_latency_issue_stalled_"):-len(".ratio")]] = f(k)
+tot = sum(v for v in stalls.values() if v) or 1.0
+summary = {
+    "source": f"ncu --set full --clock-control none --import-source on -k regex:sim_kernel -c 1 "
+              f"(tools/prof_run.py --config {cfg}), B200, round 1",
+    "kernel": d.get("Kernel Name"),
+    "duration_ms": (f("gpu__time_duration.sum") or 0) / 1e6,  # base unit: ns
+    "dram_bytes_read": f("dram__bytes_read.sum"),
+    "dram_bytes_write": f("dram__bytes_write.sum"),
+    "dram_bytes_per_launch": (f("dram__bytes_read.sum") or 0) + (f("dram__bytes_write.sum") or 0),
+    "issue_active_pct": f("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+    "warps_active_pct": f("sm__warps_active.avg.pct_of_peak_sustained_active"),
+    "registers_per_thread": f("launch__registers_per_thread"),
+    "grid": f("launch__grid_size"),
+    "block": f("launch__block_size"),
+    "warp_instructions": f("smsp__inst_executed.sum"),
+    "stall_share_pct": {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda x: -(x[1] or 0))
+                        if v and 100 * v / tot >= 0.5},
+}
+with open(os.path.join(out, f"dram_{cfg}.json"), "w") as fh:
+    json.dump(summary, fh, indent=1)
+os.remove(rep + ".ncu-rep")
+print(json.dumps({k: summary[k] for k in ("kernel", "duration_ms", "dram_bytes_per_launch", "issue_active_pct")}))
