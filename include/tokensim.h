@@ -311,7 +311,10 @@ typedef struct {
 tokensim_status tokensim_get_run_info(const tokensim_sweep *h, tokensim_run_info *out);
 
 /* Per-point execution profile of the last run (observability): iterations simulated, how
- * many of them were committed by time-parallel fast-forward stretches, and SM cycles. */
+ * many of them were committed by time-parallel fast-forward stretches, and SM cycles.
+ * sm_cycles is always measured.  The path/phase cycle splits and ff_failed / ff_cut are
+ * compiled out of the product library (they cost 5-10% of the simulation kernel) and read 0
+ * unless the library was built with -DTS_PROFILE=1 (libtokensim_prof.so, tools/prof_run.py). */
 typedef struct {
   uint64_t n_iterations, ff_iterations, ff_stretches, sm_cycles;
   uint64_t cycles_ff, cycles_ff_failed, cycles_normal;  /* split of sm_cycles by path */

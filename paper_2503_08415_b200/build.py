@@ -42,15 +42,19 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every translation unit to an object in parallel, then link the shared library."""
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: list | None = None) -> str:
+    """Compile every translation unit to an object in parallel, then link the shared library.
+
+    ``out``/``defines`` build an A/B variant elsewhere (e.g. ``-DTS_PROFILE=0``); the default
+    in-tree library is the product."""
+    lib = out or LIB
+    if out is None and not force and not stale():
         return LIB
     import concurrent.futures as cf
     import tempfile
     with tempfile.TemporaryDirectory(prefix="tokensim_build_") as td:
         objs = [os.path.join(td, os.path.basename(s) + ".o") for s in SOURCES]
-        cmds = [[nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", "-o", o, s]
+        cmds = [[nvcc(), *NVCC_FLAGS, *(defines or []), "-I", os.path.join(ROOT, "include"), "-c", "-o", o, s]
                 for s, o in zip(SOURCES, objs)]
         if verbose:
             for c in cmds:
@@ -58,12 +62,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with cf.ThreadPoolExecutor(len(cmds)) as ex:
             for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
                 f.result()
-        tmp = LIB + f".tmp{os.getpid()}"
+        tmp = lib + f".tmp{os.getpid()}"
         subprocess.check_call([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs])
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
+
+
+PROF_LIB = os.path.join(PKG, "libtokensim_prof.so")
+
+
+def build_profiling() -> str:
+    """The observability build (-DTS_PROFILE=1: per-path/phase cycle counters); tools only."""
+    if os.path.exists(PROF_LIB) and not any(os.path.getmtime(p) > os.path.getmtime(PROF_LIB)
+                                            for p in SOURCES + HEADERS):
+        return PROF_LIB
+    return build(out=PROF_LIB, defines=["-DTS_PROFILE=1"])
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    args = sys.argv[1:]
+    o = args[args.index("--out") + 1] if "--out" in args else None
+    print(build(force="--force" in args, verbose=True, out=o, defines=[a for a in args if a.startswith("-D")]))

@@ -10,6 +10,20 @@ namespace ts {
 
 #define FULLMASK 0xffffffffu
 
+// Per-path / per-phase cycle counters of the point profile (tokensim_get_point_profile).
+// Off in the product build (they cost 5-10% of the simulation kernel); build with
+// -DTS_PROFILE=1 (tools/prof_run.py --build) to read them, otherwise they read 0.
+#ifndef TS_PROFILE
+#define TS_PROFILE 0
+#endif
+__device__ __forceinline__ long long prof_clock() {
+#if TS_PROFILE
+  return clock64();
+#else
+  return 0;
+#endif
+}
+
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ u32 lanemask_lt() {
   u32 m;

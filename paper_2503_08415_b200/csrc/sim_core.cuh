@@ -214,6 +214,11 @@ struct Logs {
   u32 nev, nit;
 };
 
+// The folds are out of line.  In the lean variant they take/return values, so the Logs fields
+// stay in registers (a reference to a local struct puts it on the stack for every append); the
+// full variant (sim_full.cu sets TS_LOGS_BYREF) keeps the by-reference form, which measured
+// faster there because the stack copy relieves its register pressure.
+#if TS_LOGS_BYREF
 static __device__ __noinline__ void ev_flush(Logs &L) {
   __syncwarp();
   for (u32 x = lane_id(); x < L.nev; x += 32) {
@@ -223,6 +228,22 @@ static __device__ __noinline__ void ev_flush(Logs &L) {
   L.nev = 0;
   __syncwarp();
 }
+#else
+static __device__ __noinline__ u64 ev_fold(const uint4 *ev, u32 nev) {
+  __syncwarp();
+  u64 d = 0;
+  for (u32 x = lane_id(); x < nev; x += 32) {
+    const uint4 e = ev[x];
+    d += fold_event(e.x, e.y, e.z, e.w);
+  }
+  __syncwarp();
+  return d;
+}
+__device__ __forceinline__ void ev_flush(Logs &L) {
+  L.dig_b += ev_fold(L.ev, L.nev);
+  L.nev = 0;
+}
+#endif
 __device__ __forceinline__ void ev_reserve(Logs &L, u32 cnt) {
   if (L.nev + cnt > EVCAP) ev_flush(L);
 }
@@ -376,17 +397,19 @@ __device__ __forceinline__ u64 sched_fold(u64 k, i64 ts, i64 T, u64 Np, u64 Cd, 
 
 // iteration entry: k (worker in bit 40), t_start, T, N_p, C_d, blocks,
 // S_p | D<<16 | m<<32 | n_resumed<<48, n_admitted | n_finished<<16 | n_rejected<<32
-static __device__ __noinline__ void it_flush(Logs &L) {
+static __device__ __noinline__ u64 it_fold(const ulonglong2 *it, u32 nit, tokensim_iter_record *itr, u64 it_cap,
+                                          u64 it_base) {
   __syncwarp();
-  for (u32 x = lane_id(); x < L.nit; x += 32) {
-    const ulonglong2 a = L.it[4 * x], b = L.it[4 * x + 1], c = L.it[4 * x + 2], d = L.it[4 * x + 3];
+  u64 dg = 0;
+  for (u32 x = lane_id(); x < nit; x += 32) {
+    const ulonglong2 a = it[4 * x], b = it[4 * x + 1], c = it[4 * x + 2], d = it[4 * x + 3];
     const u64 k = a.x, Np = b.y, Cd = c.x, blocks = c.y, w6 = d.x, w7 = d.y;
     const i64 ts = (i64)a.y, T = (i64)b.x;
     const u64 Sp = w6 & 0xffff, D = (w6 >> 16) & 0xffff, m = (w6 >> 32) & 0xffff, nres = w6 >> 48;
     const u64 nadm = w7 & 0xffff, nfin = (w7 >> 16) & 0xffff, nrej = w7 >> 32;
-    L.dig_s += sched_fold(k, ts, T, Np, Cd, blocks, w6, w7);
-    const u64 idx = L.it_base + x;
-    if (idx < L.it_cap) {
+    dg += sched_fold(k, ts, T, Np, Cd, blocks, w6, w7);
+    const u64 idx = it_base + x;
+    if (idx < it_cap) {
       tokensim_iter_record ir;
       ir.k = k & ((1ull << 40) - 1);
       ir.t_start_ns = ts;
@@ -403,13 +426,25 @@ static __device__ __noinline__ void it_flush(Logs &L) {
       ir.blocks_in_use = (u32)blocks;
       ir.worker = (u32)(k >> 40);
       ir.pad = 0;
-      L.itr[idx] = ir;
+      itr[idx] = ir;
     }
   }
+  __syncwarp();
+  return dg;
+}
+#if TS_LOGS_BYREF
+static __device__ __noinline__ void it_flush(Logs &L) {
+  L.dig_s += it_fold(L.it, L.nit, L.itr, L.it_cap, L.it_base);
   L.it_base += L.nit;
   L.nit = 0;
-  __syncwarp();
 }
+#else
+__device__ __forceinline__ void it_flush(Logs &L) {
+  L.dig_s += it_fold(L.it, L.nit, L.itr, L.it_cap, L.it_base);
+  L.it_base += L.nit;
+  L.nit = 0;
+}
+#endif
 __device__ __forceinline__ void it_reserve(Logs &L, u32 cnt) {
   if (L.nit + cnt > ITCAP) it_flush(L);
 }
@@ -649,6 +684,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   u64 nph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   u32 ffr[5] = {0, 0, 0, 0, 0};  // failed fast-forward attempts: not quiet / memory / arrival / head / other
   u32 ffc[5] = {0, 0, 0, 0, 0};  // stretches ended by memory / a finish / an arrival / the head / 32 or other
+#if TS_PROFILE
 #define NPH(i)                           \
   do {                                   \
     const long long _c = clock64();      \
@@ -661,6 +697,10 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     ph[i] += (u64)(_c - clk_p);          \
     clk_p = _c;                          \
   } while (0)
+#else
+#define NPH(i) do {} while (0)
+#define PH(i) do {} while (0)
+#endif
   i64 last_fin = 0;
   u32 flags = 0;
   u32 hd_idx = 0xffffffffu, hd_p = 0;  // cached prompt length of the fresh-queue head
@@ -756,7 +796,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     }
 
     // ---------------------------------------------------------------- fast-forward (H3)
-    clk_a = clock64();
+    clk_a = prof_clock();
     clk_p = clk_a;
     if (ff_on && nR > 0 && rmin >= 2 && !hx && (nfree > ff_mem_wait || k >= ff_mem_k)) {
       // The stretch must admit nothing and resume nothing.  With Q != {} fresh admission is
@@ -883,7 +923,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         }
         const u32 okm = __ballot_sync(FULLMASK, ok);
         const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
-        if (J < 2) {
+        if (!TS_PROFILE) {
+        } else if (J < 2) {
           const u32 w = __shfl_sync(FULLMASK, why, J);
           ffr[(w & 1u) ? 1 : (w & 4u) ? 2 : (w & 8u) ? 3 : 4] += 1;
         } else {  // what ended a stretch: memory / a finish / an arrival / the head / 32 or other
@@ -1133,17 +1174,17 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           ++ff_runs;
           t = tend;
           k += J;
-          cyc_ff += (u64)(clock64() - clk_a);
+          cyc_ff += (u64)(prof_clock() - clk_a);
           continue;
         }
       }
-      if (!quiet) ffr[0] += 1;
+      if (TS_PROFILE && !quiet) ffr[0] += 1;
       rmin = 0;  // retry only after the next normal commit recomputes it
-      const long long c1 = clock64();
+      const long long c1 = prof_clock();
       cyc_ff_fail += (u64)(c1 - clk_a);
       clk_a = c1;
     }
-    clk_p = clock64();
+    clk_p = prof_clock();
 
     // ---------------------------------------------------------------- 3. decode reservation
     u32 E = 0, Kb = 0, m = 0, nres = 0, nadm = 0, nrej = 0;
@@ -1669,7 +1710,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     }
     t = te;
     ++k;
-    cyc_normal += (u64)(clock64() - clk_a);
+    cyc_normal += (u64)(prof_clock() - clk_a);
   }
   ev_flush(L);
   it_flush(L);

@@ -1,6 +1,7 @@
 // sim_full.cu -- the full simulation kernel variant: chunked prefill (NEXT-3b), multi-round
 // conversations + memory cache (NEXT-2), the preload link (NEXT-4), the 1P:1D pair (a.9) and the
 // xP:yD node (NEXT-1) (see sim_core.cuh).
+#define TS_LOGS_BYREF 1
 #include "sim_core.cuh"
 
 namespace ts {

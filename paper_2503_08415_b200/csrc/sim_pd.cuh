@@ -261,7 +261,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     if (tD <= tP) {
       // ============================================================ D boundary
       const i64 t = tD;
-      long long cD = clock64();  // observability: cycles by path (point profile)
+      long long cD = prof_clock();  // observability: cycles by path (point profile)
       // 1. finished transfers become runnable (the in-flight tail completes in FIFO order)
       while (nX > 0 && xhead_end <= t) {
         const u32 pos = nD - nX;
@@ -565,12 +565,12 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
             lastD = tend;
             kD += J;
             D_idle = false;
-            cyc_ffD += (u64)(clock64() - cD);
+            cyc_ffD += (u64)(prof_clock() - cD);
             continue;
           }
         }
         rminD = 0;
-        const long long c1 = clock64();
+        const long long c1 = prof_clock();
         cyc_failD += (u64)(c1 - cD);
         cD = c1;
       }
@@ -885,7 +885,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       lastD = te;
       ++kD;
       D_idle = false;
-      cyc_normD += (u64)(clock64() - cD);
+      cyc_normD += (u64)(prof_clock() - cD);
     } else {
       // ============================================================ P boundary
       const i64 t = tP;

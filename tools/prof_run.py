@@ -8,6 +8,14 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+if not os.environ.get("TOKENSIM_LIB"):  # the cycle splits need the profiling build
+    import importlib.util  # load build.py alone: importing the package would load the product library
+    _spec = importlib.util.spec_from_file_location(
+        "ts_build", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2503_08415_b200",
+                                 "build.py"))
+    _b = importlib.util.module_from_spec(_spec)
+    _spec.loader.exec_module(_b)
+    os.environ["TOKENSIM_LIB"] = _b.build_profiling()
 import torch  # noqa: E402
 
 import sweep_inputs as si  # noqa: E402
