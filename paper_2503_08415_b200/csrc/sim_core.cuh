@@ -272,14 +272,64 @@ __device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 hel
   hint = min(hint, mn);
 }
 
+// Take the K lowest free blocks (in ascending order) into out[0..K) and clear them (32-word
+// windows from the hint).  false if fewer than K are free at or above the hint.
+static __device__ bool take_lowest(u32 *bitmap, u32 K, u32 *out, u32 &hint, u32 nwords) {
+  const u32 lane = lane_id();
+  u32 o_base = 0, w = hint;
+  while (o_base < K) {
+    if (w >= nwords) return false;
+    const u32 wi = w + lane;
+    u32 word = wi < nwords ? bitmap[wi] : 0u;
+    const u32 c = __popc(word);
+    const u32 cum = scan_incl(c);
+    const u32 tot = __shfl_sync(FULLMASK, cum, 31);
+    if (tot == 0) {
+      w += 32;
+      continue;
+    }
+    const u32 take = min(tot, K - o_base);
+    const u32 before = cum - c;
+    for (u32 r0 = 0; r0 < take; r0 += 32) {
+      const u32 idx = r0 + lane;
+      const u32 tgt = idx < take ? idx : 0u;
+      u32 lo = 0;
+#pragma unroll
+      for (u32 s = 16; s; s >>= 1) {
+        const u32 v = __shfl_sync(FULLMASK, cum, lo + s - 1);
+        if (v <= tgt) lo += s;
+      }
+      const u32 wv = __shfl_sync(FULLMASK, word, lo);
+      const u32 bv = __shfl_sync(FULLMASK, before, lo);
+      if (idx < take) out[o_base + idx] = (w + lo) * 32 + select_bit(wv, tgt - bv);
+    }
+    const u32 tk = take > before ? min(c, take - before) : 0u;
+    if (tk && wi < nwords) {
+      word = clear_lowest(word, tk, c);
+      bitmap[wi] = word;
+    }
+    o_base += take;
+    if (o_base < K) {
+      w += 32;
+    } else {
+      const u32 nz = __ballot_sync(FULLMASK, word != 0u);
+      w = nz ? w + (u32)(__ffs(nz) - 1) : w + 32;
+    }
+  }
+  hint = w;
+  __syncwarp();
+  return true;
+}
+
 // Hand out the K lowest free blocks, in order, to the E requesters in S.req_* (entry e
 // owns order indices [req_cum[e-1], req_cum[e]) and writes its table from tpos).  This is
 // "serve the requesters one after another with take-the-lowest-free-block" (c.4 steps
 // 3-5, reading A14) done in one bitmap pass.  Entry iteration offsets (fast-forward)
-// shift the digest's iteration index.
+// shift the digest's iteration index.  The first E1 entries take one block each (decode
+// requesters come first in phase order), so their owner needs no search.
 static __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u32 btl, u64 k, u32 kind_off, Logs &L,
-                              u32 &hint, u32 nwords) {
-  const bool unit = E == K;  // every requester takes one block: owner of order index o is o
+                              u32 &hint, u32 nwords, u32 E1 = 0) {
+  if (E == K) E1 = E;  // every requester takes one block: owner of order index o is o
   const u32 lane = lane_id();
   u32 o_base = 0, w = hint;
   while (o_base < K) {
@@ -312,8 +362,8 @@ static __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u
         const u32 blk = (w + lo) * 32 + select_bit(wv, tgt - bv);
         const u32 o = o_base + idx;
         u32 a = o, start = o;
-        if (!unit) {
-          a = 0;
+        if (o >= E1) {
+          a = E1;
           u32 bnd = E;
           while (a < bnd) {
             const u32 mid = (a + bnd) >> 1;
@@ -353,6 +403,14 @@ static __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u
 __device__ __forceinline__ u32 alloc_btslots(u32 *btfree, u32 nw, bool take, u32 rank, u32 cnt) {
   const u32 lane = lane_id();
   u32 word = lane < nw ? btfree[lane] : 0u;
+  if (cnt == 1) {  // one admission (the common case): the lowest set bit of the first nonzero word
+    const u32 nz = __ballot_sync(FULLMASK, word != 0u);
+    const u32 l = (u32)(__ffs(nz) - 1);
+    const u32 wv = __shfl_sync(FULLMASK, word, l);
+    if (lane == l) btfree[l] = wv & (wv - 1u);
+    __syncwarp();
+    return l * 32 + (u32)(__ffs(wv) - 1);
+  }
   const u32 c = __popc(word);
   const u32 cum = scan_incl(c);
   const u32 before = cum - c;
@@ -877,10 +935,16 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             if (j0 < 32) key = j0;
           }
           const u32 peers = __match_any_sync(FULLMASK, key);
+          u32 old = 0;
           if (key < 32 && (peers & ltm) == 0u) {
-            S.scratch[key] += __popc(peers);
+            old = S.scratch[key];
+            S.scratch[key] = old + __popc(peers);
             S.scratch[32 + key] = peers;  // slot positions of this residue (meaningful if nR <= 32)
           }
+          // rank of the slot among the slots of its residue class, in position order (= its
+          // place among the requesters of every iteration in which that class needs blocks)
+          const u32 rbase = __shfl_sync(FULLMASK, old, (u32)(__ffs(peers) - 1));
+          if (key < 32) S.req_pt[jj] = rbase + __popc(peers & ltm);
           __syncwarp();
         }
         const u64 Cd0 = warp_sum64(cdp);
@@ -940,10 +1004,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         if (J >= 2) {
           const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
           PH(1);
-          // requester list ordered by (iteration, slot): bucket cursors = exclusive scan
-          __syncwarp();  // every lane has read its histogram bucket
-          S.scratch[lane] = Aj - nj;
-          __syncwarp();
           bool done_alloc = Ktot == 0;
           if (!done_alloc && nR <= 32 && Ktot <= 32 && hint < nwords) {
             // fused small case: lane o takes the o-th lowest free block of the 32-word window at
@@ -993,32 +1053,36 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             }
           }
           if (!done_alloc) {
-            const u32 nrep = (32 + B.bs - 1) / B.bs;
-            for (u32 b0 = 0; b0 < nR; b0 += 32) {
-              const u32 jj = b0 + lane;
-              const u32 c = jj < nR ? S.ctx[jj] : 0u;
-              const u32 r = B.mod(c);
-              u32 jx = r ? B.bs - r : 0u;
-              for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
-                const bool v = jj < nR && jx < J;
-                const u32 key = v ? jx : 64u + lane;
-                const u32 peers = __match_any_sync(FULLMASK, key);
-                u32 base = 0;
-                if (v) base = S.scratch[jx];
-                __syncwarp();
-                if (v) {
-                  const u32 e = base + __popc(peers & ltm);
-                  S.req_cum[e] = e + 1;
-                  S.req_pt[e] = jj | (jx << 10) | (B.div(c + jx) << 15);
-                  if ((peers & ltm) == 0u) S.scratch[jx] = base + __popc(peers);
-                }
-                __syncwarp();
-              }
-            }
-            if (!alloc_ordered(S, Ktot, Ktot, bt, btl, k, 0, L, hint, nwords)) {
+            // the Ktot lowest free blocks in order, then every request places itself: the
+            // request of a slot at iteration offset jx has order index (blocks of iterations
+            // before jx) + (its rank in its residue class)
+            u32 *fl = S.req_cum;  // free in a stretch; Ktot <= CAP (cut condition)
+            if (!take_lowest(S.bitmap, Ktot, fl, hint, nwords)) {
               flags |= TOKENSIM_PT_INTERNAL_ERROR;
               break;
             }
+            ev_reserve(L, Ktot);
+            const u32 excl = Aj - nj;
+            const u32 nrep = (32 + B.bs - 1) / B.bs;
+            for (u32 b0 = 0; b0 < nR; b0 += 32) {
+              const u32 jj = b0 + lane;
+              const bool in = jj < nR;
+              const u32 c = in ? S.ctx[jj] : 0u;
+              const u32 rank = in ? S.req_pt[jj] : 0u;
+              const u32 r = B.mod(c);
+              u32 jx = r ? B.bs - r : 0u;
+              for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
+                const u32 ex = __shfl_sync(FULLMASK, excl, jx & 31u);
+                if (in && jx < J) {
+                  const u32 o = ex + rank;
+                  const u32 blk = fl[o];
+                  bt[(size_t)SLOT(S.info[jj]) * btl + B.div(c + jx)] = blk;
+                  ev_put(L, o, k + jx, 1, S.id[jj], blk);
+                }
+              }
+            }
+            L.nev += Ktot;
+            __syncwarp();
           }
           const u64 blk0 = total - nfree;
           nfree -= Ktot;
@@ -1187,7 +1251,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     clk_p = prof_clock();
 
     // ---------------------------------------------------------------- 3. decode reservation
-    u32 E = 0, Kb = 0, m = 0, nres = 0, nadm = 0, nrej = 0;
+    u32 E = 0, Kb = 0, m = 0, nres = 0, nadm = 0, nrej = 0, Edec = 0;
     u64 cdp = 0, npp = 0, app = 0, swap_out = 0, swap_in = 0, tokens = 0;
     // CHUNKED: keys read by prefills, LM-head rows, the entry left partial this iteration
     u64 kpp = 0;
@@ -1397,6 +1461,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     }
     nR3 = nR;
     Kb = E;
+    Edec = E;  // decode requesters: one block each, first in phase order
     nfree -= E;
     tokens = nR - (hx ? 1u : 0u);
     if (CHK && hx) {  // the prefill in progress takes the budget the decodes leave (R-N3b)
@@ -1492,7 +1557,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     // 6. empty batch (every candidate rejected): back to 0 without advancing t
     if (nR == 0) continue;
     // block extraction for all requesters of this iteration, in phase order
-    if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, 0, L, hint, nwords)) {
+    if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, 0, L, hint, nwords, Edec)) {
       flags |= TOKENSIM_PT_INTERNAL_ERROR;
       break;
     }

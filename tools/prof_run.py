@@ -54,7 +54,11 @@ if os.environ.get("PROFILE_POINTS"):
     print("cycles ~ %.0f/normal-iter + %.0f/stretch + %.2f/req-iter" % tuple(coef))
     cuts = np.array([x["ff_cut"] for x in prof], dtype=np.float64).sum(0)
     print("all points: stretches ended by (memory / finish / arrival / head / 32+other):", cuts.astype(int).tolist())
-    order = np.argsort(-cy)[:6]
+    if os.environ.get("PROFILE_GROUPS"):  # worst point of each group of G consecutive points
+        G = int(os.environ["PROFILE_GROUPS"])
+        order = [g * G + int(np.argmax(cy[g * G:(g + 1) * G])) for g in range((end + G - 1) // G)]
+    else:
+        order = np.argsort(-cy)[:6]
     for p in order:
         x = prof[p]
         nn = max(1, x["n_iterations"] - x["ff_iterations"])
