@@ -471,6 +471,7 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   u32 bps = (u32)std::max<size_t>(1, (227 * 1024) / (per_warp * wpb));
   bps = std::min<u32>(bps, 16);
   if (blocks_per_sm_limit > 0) bps = std::min<u32>(bps, (u32)blocks_per_sm_limit);
+  if (const char *e = getenv("TOKENSIM_BPS")) bps = std::min<u32>(bps, (u32)std::max(1, atoi(e)));  // A/B experiments
   const u64 need_warps = std::max<u64>(1, n_run);
   u64 blocks = std::min<u64>((u64)sm_count * bps, ceil_div(need_warps, wpb));
   L.wpb = wpb;
@@ -621,6 +622,27 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
 
   SweepParams P{};
   P.M = h->M;
+  {
+    const DevModel &M = h->M;  // exact: every coefficient is an integer below 2^53 (validated at create)
+    DevModelF &F = P.MF;
+    F.h = (double)M.h;
+    F.q2g = (double)M.q2g;
+    F.hq2g = (double)M.hq2g;
+    F.qh = (double)M.qh;
+    F.q = (double)M.q;
+    F.q4 = (double)(4 * M.q);
+    F.hfu = (double)M.hfu;
+    F.fu = (double)M.fu;
+    F.fh = (double)M.fh;
+    F.f = (double)M.f;
+    F.Vh = (double)M.Vh;
+    F.V = (double)M.V;
+    F.s = (double)M.s;
+    F.att_tok = (double)M.att_tok;
+    F.g2 = (double)M.g2;
+    F.L = (double)M.L;
+    F.twoL = (double)(2 * M.L);
+  }
   P.hw = reinterpret_cast<const DevHw *>(h->d_tab + h->off_hw);
   P.hp = reinterpret_cast<const DevHP *>(h->d_tab + h->off_hp);
   P.pol = reinterpret_cast<const DevPol *>(h->d_tab + h->off_pol);
@@ -706,6 +728,11 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.mr_bytes_per_warp = L.mr_per_warp;
   P.pd_general = h->pd_general ? 1u : 0u;
   P.full = h->full ? 1u : 0u;
+  {
+    bool p2 = true;  // the kernels specialise their block arithmetic to shifts and masks
+    for (const auto &pl : h->pol) p2 = p2 && (pl.block_size & (pl.block_size - 1)) == 0;
+    P.all_p2 = p2 ? 1u : 0u;
+  }
   P.evlog = reinterpret_cast<uint4 *>(ws + L.evlog);
   P.itlog = reinterpret_cast<ulonglong2 *>(ws + L.itlog);
 

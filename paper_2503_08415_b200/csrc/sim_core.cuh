@@ -39,30 +39,30 @@ struct CostK {
   u64 Lu;           // layers (chunks of a swap-in)
 };
 
-__device__ __forceinline__ CostK make_costk(const DevModel &M, const DevHw &H, u32 link_mode = 0,
+__device__ __forceinline__ CostK make_costk(const DevModel &M, const DevModelF &F, const DevHw &H, u32 link_mode = 0,
                                             u64 preload_buf = 0, double fetch_s = 0.0) {
   CostK K;
   K.fetch_s = fetch_s;
   K.preload = link_mode == TOKENSIM_LINK_PRELOAD ? 1u : 0u;
   K.preload_buf = preload_buf;
   K.Lu = M.L;
-  K.h = __ull2double_rn(M.h);
-  K.q2g = __ull2double_rn(M.q2g);
-  K.hq2g = __ull2double_rn(M.hq2g);
-  K.qh = __ull2double_rn(M.qh);
-  K.q = __ull2double_rn(M.q);
-  K.q4 = __ull2double_rn(4 * M.q);
-  K.hfu = __ull2double_rn(M.hfu);
-  K.fu = __ull2double_rn(M.fu);
-  K.fh = __ull2double_rn(M.fh);
-  K.f = __ull2double_rn(M.f);
-  K.Vh = __ull2double_rn(M.Vh);
-  K.V = __ull2double_rn(M.V);
-  K.s = __ull2double_rn(M.s);
-  K.att_tok = __ull2double_rn(M.att_tok);
-  K.g2 = __ull2double_rn(M.g2);
-  K.L = __ull2double_rn(M.L);
-  K.twoL = __ull2double_rn(2 * M.L);
+  K.h = F.h;
+  K.q2g = F.q2g;
+  K.hq2g = F.hq2g;
+  K.qh = F.qh;
+  K.q = F.q;
+  K.q4 = F.q4;
+  K.hfu = F.hfu;
+  K.fu = F.fu;
+  K.fh = F.fh;
+  K.f = F.f;
+  K.Vh = F.Vh;
+  K.V = F.V;
+  K.s = F.s;
+  K.att_tok = F.att_tok;
+  K.g2 = F.g2;
+  K.L = F.L;
+  K.twoL = F.twoL;
   K.bar_coef = H.tp > 1 ? __ull2double_rn(2 * (u64)(H.tp - 1) * M.h * M.s) : 0.0;
   K.invF = H.invF;
   K.invB = H.invB;
@@ -640,7 +640,7 @@ __device__ __forceinline__ void mr_cache_store(MrState &M, u32 c, u32 tokens, co
 
 // ------------------------------------------------------------------ a.2-a.7 one point
 // Everything is executed by all 32 lanes; scalar state is lane-uniform in registers.
-template <int CAP, bool FULL>
+template <int CAP, bool FULL, bool P2>
 __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S, u32 *bt) {
   static_assert(CAP % 32 == 0 && CAP <= 1024, "CAP");
   const u32 lane = lane_id();
@@ -650,7 +650,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const DevHw H = P.hw[cd.hw];
   const DevHP HP = P.hp[(size_t)cd.hw * P.n_pol + cd.pol];
   const DevPol PL = P.pol[cd.pol];
-  const CostK K = make_costk(P.M, H, FULL ? P.link_mode : 0u, P.preload_buf, FULL ? P.fetch_s : 0.0);
+  const CostK K = make_costk(P.M, P.MF, H, FULL ? P.link_mode : 0u, P.preload_buf, FULL ? P.fetch_s : 0.0);
   const u32 g = P.group_of_point_mode ? 0u : cd.rate * P.n_seeds + cd.seed;
   const u32 n = P.n_req;
   const i64 *A = P.arrival + (size_t)g * n;
@@ -659,7 +659,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   tokensim_request_record *rec = P.rec + (size_t)j * n;
   tokensim_mem_sample *trc = P.trace + (size_t)j * P.trace_nw * P.trace_cap;
   tokensim_iter_record *itr = P.itrec + (size_t)j * P.it_cap;
-  const BSz B = {PL.bs, PL.bs_sh, PL.bs - 1u, PL.bs_sh != 0xffffffffu};
+  const BSz B = {PL.bs, PL.bs_sh, PL.bs - 1u, P2 || PL.bs_sh != 0xffffffffu};  // P2: folded to shifts
   const bool SWAPM = PL.preempt == TOKENSIM_SWAP;
   const bool RATIO = PL.kind == TOKENSIM_CONT_RATIO;
   const bool STATICP = PL.kind == TOKENSIM_STATIC;
@@ -1829,7 +1829,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   __syncwarp();
 }
 
-template <int CAP, bool FULL>
+template <int CAP, bool FULL, bool P2>
 __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
@@ -1848,46 +1848,60 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
     if ((u64)qi >= P.n_run) break;
     const u64 j = P.order[qi];
     if constexpr (FULL) {
-      if (node) simulate_pdn<CAP>(P, j, smem_raw + wib * per_warp, bt);
-      else if (pd) simulate_pd<CAP>(P, j, S, smem_raw + wib * per_warp + base, bt);
-      else simulate_unified<CAP, true>(P, j, S, bt);
+      if (node) simulate_pdn<CAP, P2>(P, j, smem_raw + wib * per_warp, bt);
+      else if (pd) simulate_pd<CAP, P2>(P, j, S, smem_raw + wib * per_warp + base, bt);
+      else simulate_unified<CAP, true, P2>(P, j, S, bt);
     } else {
-      simulate_unified<CAP, false>(P, j, S, bt);
+      simulate_unified<CAP, false, P2>(P, j, S, bt);
     }
   }
 }
 
 // launch / occupancy helpers for one variant (instantiated by sim_base.cu / sim_full.cu)
-template <int CAP, bool FULL>
+template <int CAP, bool FULL, bool P2>
 static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, FULL, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  sim_kernel<CAP, FULL><<<blocks, wpb * 32, smem, st>>>(p);
+  sim_kernel<CAP, FULL, P2><<<blocks, wpb * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
-template <int CAP, bool FULL>
+template <int CAP, bool FULL, bool P2>
 static cudaError_t occ_t(int wpb, size_t smem, int *b) {
-  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, FULL, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP, FULL>, wpb * 32, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP, FULL, P2>, wpb * 32, smem);
+}
+template <bool FULL, bool P2>
+static cudaError_t launch_sim_c(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
+  switch (cap) {
+    case 32: return launch_sim_t<32, FULL, P2>(p, wpb, blocks, smem, st);
+    case 256: return launch_sim_t<256, FULL, P2>(p, wpb, blocks, smem, st);
+    case 1024: return launch_sim_t<1024, FULL, P2>(p, wpb, blocks, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 template <bool FULL>
 static cudaError_t launch_sim_v(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
+  return p.all_p2 ? launch_sim_c<FULL, true>(p, cap, wpb, blocks, smem, st)
+                  : launch_sim_c<FULL, false>(p, cap, wpb, blocks, smem, st);
+}
+template <bool FULL, bool P2>
+static cudaError_t sim_occupancy_c(int cap, int wpb, size_t smem, int *b) {
   switch (cap) {
-    case 32: return launch_sim_t<32, FULL>(p, wpb, blocks, smem, st);
-    case 256: return launch_sim_t<256, FULL>(p, wpb, blocks, smem, st);
-    case 1024: return launch_sim_t<1024, FULL>(p, wpb, blocks, smem, st);
+    case 32: return occ_t<32, FULL, P2>(wpb, smem, b);
+    case 256: return occ_t<256, FULL, P2>(wpb, smem, b);
+    case 1024: return occ_t<1024, FULL, P2>(wpb, smem, b);
     default: return cudaErrorInvalidValue;
   }
 }
 template <bool FULL>
 static cudaError_t sim_occupancy_v(int cap, int wpb, size_t smem, int *b) {
-  switch (cap) {
-    case 32: return occ_t<32, FULL>(wpb, smem, b);
-    case 256: return occ_t<256, FULL>(wpb, smem, b);
-    case 1024: return occ_t<1024, FULL>(wpb, smem, b);
-    default: return cudaErrorInvalidValue;
-  }
+  int b1 = 0, b2 = 0;  // the same resources either way; take the smaller to be safe
+  cudaError_t e = sim_occupancy_c<FULL, true>(cap, wpb, smem, &b1);
+  if (e != cudaSuccess) return e;
+  e = sim_occupancy_c<FULL, false>(cap, wpb, smem, &b2);
+  *b = b1 < b2 ? b1 : b2;
+  return e;
 }
 
 }  // namespace ts

@@ -126,7 +126,7 @@ __device__ __forceinline__ void trace_stretch(TraceAcc &A, bool binned, bool ful
   }
 }
 
-template <int CAP>
+template <int CAP, bool P2>
 __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsigned char *pd_smem, u32 *bt) {
   const u32 lane = lane_id();
   const u32 ltm = lanemask_lt();
@@ -136,8 +136,8 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
   const DevHP HPP = P.hp[(size_t)hwP * P.n_pol + cd.pol];
   const DevHP HPD = P.hp[(size_t)hwD * P.n_pol + cd.pol];
   const DevPol PL = P.pol[cd.pol];
-  const CostK KP = make_costk(P.M, P.hw[hwP]);
-  const CostK KD = make_costk(P.M, P.hw[hwD], P.link_mode, P.preload_buf);
+  const CostK KP = make_costk(P.M, P.MF, P.hw[hwP]);
+  const CostK KD = make_costk(P.M, P.MF, P.hw[hwD], P.link_mode, P.preload_buf);
   const u32 g = P.group_of_point_mode ? 0u : cd.rate * P.n_seeds + cd.seed;
   const u32 n = P.n_req;
   const i64 *A = P.arrival + (size_t)g * n;
@@ -147,7 +147,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
   tokensim_mem_sample *trcP = P.trace + (size_t)j * P.trace_nw * P.trace_cap;
   tokensim_mem_sample *trcD = trcP + P.trace_cap;
   tokensim_iter_record *itr = P.itrec + (size_t)j * P.it_cap;
-  const BSz B = {PL.bs, PL.bs_sh, PL.bs - 1u, PL.bs_sh != 0xffffffffu};
+  const BSz B = {PL.bs, PL.bs_sh, PL.bs - 1u, P2 || PL.bs_sh != 0xffffffffu};  // P2: folded to shifts
   const bool SWAPM = PL.preempt == TOKENSIM_SWAP;
   const bool STATICP = PL.kind == TOKENSIM_STATIC;
   const u64 totP = HPP.total_blocks, totD = HPD.total_blocks;

@@ -122,7 +122,7 @@ __device__ __forceinline__ u32 warp_argmin64(i64 key, u32 ord, bool valid) {
   return who;
 }
 
-template <int CAP>
+template <int CAP, bool P2>
 __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u32 *bt) {
   const u32 lane = lane_id();
   const u32 ltm = lanemask_lt();
@@ -133,8 +133,8 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   const DevHP HPP = P.hp[(size_t)hwP * P.n_pol + cd.pol];
   const DevHP HPD = P.hp[(size_t)hwD * P.n_pol + cd.pol];
   const DevPol PL = P.pol[cd.pol];
-  const CostK KP = make_costk(P.M, P.hw[hwP]);
-  const CostK KD = make_costk(P.M, P.hw[hwD], P.link_mode, P.preload_buf);
+  const CostK KP = make_costk(P.M, P.MF, P.hw[hwP]);
+  const CostK KD = make_costk(P.M, P.MF, P.hw[hwD], P.link_mode, P.preload_buf);
   const u32 g = P.group_of_point_mode ? 0u : cd.rate * P.n_seeds + cd.seed;
   const u32 n = P.n_req;
   const i64 *A = P.arrival + (size_t)g * n;
@@ -143,7 +143,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   tokensim_request_record *rec = P.rec + (size_t)j * n;
   tokensim_mem_sample *trc0 = P.trace + (size_t)j * P.trace_nw * P.trace_cap;
   tokensim_iter_record *itr = P.itrec + (size_t)j * P.it_cap;
-  const BSz B = {PL.bs, PL.bs_sh, PL.bs - 1u, PL.bs_sh != 0xffffffffu};
+  const BSz B = {PL.bs, PL.bs_sh, PL.bs - 1u, P2 || PL.bs_sh != 0xffffffffu};  // P2: folded to shifts
   const bool SWAPM = PL.preempt == TOKENSIM_SWAP;
   const bool STATICP = PL.kind == TOKENSIM_STATIC;
   const u64 totP = HPP.total_blocks, totD = HPD.total_blocks;

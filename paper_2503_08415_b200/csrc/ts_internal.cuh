@@ -65,8 +65,14 @@ struct SimStats {
   u64 ff_cut[5];                        // what ended each stretch (see the profile)
 };
 
+// The model's cost-table coefficients as exact doubles (integers < 2^53), precomputed on the
+// host so the kernels read them as constant-bank operands instead of holding them in registers.
+struct DevModelF {
+  double h, q2g, hq2g, qh, q, q4, hfu, fu, fh, f, Vh, V, s, att_tok, g2, L, twoL;
+};
 struct SweepParams {
   DevModel M;
+  DevModelF MF;
   const DevHw *hw;      // [n_hw]
   const DevHP *hp;      // [n_hw * n_pol]
   const DevPol *pol;    // [n_pol]
@@ -113,7 +119,7 @@ struct SweepParams {
   unsigned char *pdn_scratch;  // NEXT-1 node: per-warp FIFOs, queues, holders, P block lists
   u64 pdn_bytes_per_warp;
   u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
-  u32 full, pad4;                         // 1: the full kernel variant (sim_full.cu)
+  u32 full, all_p2;                       // 1: the full kernel variant (sim_full.cu); every block size a power of two
   u32 link_mode, pad2;                    // NEXT-4: TOKENSIM_LINK_SEQUENTIAL | PRELOAD
   u64 preload_buf;                        // preload buffer bytes
   // NEXT-2 multi-round conversations + memory cache.  With multi_round, n_req = 7 * n_conv is
