@@ -221,6 +221,7 @@ struct Logs {
 #if TS_LOGS_BYREF
 static __device__ __noinline__ void ev_flush(Logs &L) {
   __syncwarp();
+  #pragma unroll 1
   for (u32 x = lane_id(); x < L.nev; x += 32) {
     const uint4 e = L.ev[x];
     L.dig_b += fold_event(e.x, e.y, e.z, e.w);
@@ -232,6 +233,7 @@ static __device__ __noinline__ void ev_flush(Logs &L) {
 static __device__ __noinline__ u64 ev_fold(const uint4 *ev, u32 nev) {
   __syncwarp();
   u64 d = 0;
+  #pragma unroll 1
   for (u32 x = lane_id(); x < nev; x += 32) {
     const uint4 e = ev[x];
     d += fold_event(e.x, e.y, e.z, e.w);
@@ -257,6 +259,7 @@ __device__ __forceinline__ void ev_put(Logs &L, u32 idx, u64 k, u32 kind, u32 id
 __device__ __forceinline__ void free_blocks(u32 *bitmap, const u32 *tbl, u32 held, u32 id, u64 k, u32 kind_off,
                                             Logs &L, u32 &hint) {
   u32 mn = 0xffffffffu;
+  #pragma unroll 1
   for (u32 x0 = 0; x0 < held; x0 += 32) {
     ev_reserve(L, 32);
     const u32 x = x0 + lane_id();
@@ -290,6 +293,7 @@ static __device__ bool take_lowest(u32 *bitmap, u32 K, u32 *out, u32 &hint, u32 
     }
     const u32 take = min(tot, K - o_base);
     const u32 before = cum - c;
+    #pragma unroll 1
     for (u32 r0 = 0; r0 < take; r0 += 32) {
       const u32 idx = r0 + lane;
       const u32 tgt = idx < take ? idx : 0u;
@@ -345,6 +349,7 @@ static __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u
     }
     const u32 take = min(tot, K - o_base);
     const u32 before = cum - c;
+    #pragma unroll 1
     for (u32 r0 = 0; r0 < take; r0 += 32) {
       ev_reserve(L, 32);
       const u32 idx = r0 + lane;
@@ -459,6 +464,7 @@ static __device__ __noinline__ u64 it_fold(const ulonglong2 *it, u32 nit, tokens
                                           u64 it_base) {
   __syncwarp();
   u64 dg = 0;
+  #pragma unroll 1
   for (u32 x = lane_id(); x < nit; x += 32) {
     const ulonglong2 a = it[4 * x], b = it[4 * x + 1], c = it[4 * x + 2], d = it[4 * x + 3];
     const u64 k = a.x, Np = b.y, Cd = c.x, blocks = c.y, w6 = d.x, w7 = d.y;
@@ -679,10 +685,13 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   {
     ulonglong2 *r2 = reinterpret_cast<ulonglong2 *>(rec);
     const ulonglong2 z = make_ulonglong2(0ull, 0ull);
+    #pragma unroll 1
     for (u32 x = lane; x < 2 * n; x += 32) r2[x] = z;
     const u32 full_words = (u32)(total >> 5), tail = (u32)(total & 31u);
+    #pragma unroll 1
     for (u32 w = lane; w < nwords; w += 32)
       S.bitmap[w] = w < full_words ? 0xffffffffu : (w == full_words && tail ? ((1u << tail) - 1u) : 0u);
+    #pragma unroll 1
     for (u32 w = lane; w < CAP / 32; w += 32) S.btfree[w] = 0xffffffffu;
     __syncwarp();
   }
@@ -731,6 +740,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     mr.lhead = mr.ltail = MR_NIL;
     mr.used = 0;
     mr.cap = P.cache_cap ? P.cache_cap : 4 * total;
+    #pragma unroll 1
     for (u32 x = lane; x < nc; x += 32) mr.ctok[x] = 0;
     __syncwarp();
   }
@@ -923,6 +933,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         __syncwarp();
         u64 cdp = 0;
         u32 rmn = 0xffffffffu;
+        #pragma unroll 1
         for (u32 b0 = 0; b0 < nR; b0 += 32) {
           const u32 jj = b0 + lane;
           u32 key = 64u + lane;
@@ -1064,6 +1075,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             ev_reserve(L, Ktot);
             const u32 excl = Aj - nj;
             const u32 nrep = (32 + B.bs - 1) / B.bs;
+            #pragma unroll 1
             for (u32 b0 = 0; b0 < nR; b0 += 32) {
               const u32 jj = b0 + lane;
               const bool in = jj < nR;
@@ -1071,6 +1083,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               const u32 rank = in ? S.req_pt[jj] : 0u;
               const u32 r = B.mod(c);
               u32 jx = r ? B.bs - r : 0u;
+              #pragma unroll 1
               for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
                 const u32 ex = __shfl_sync(FULLMASK, excl, jx & 31u);
                 if (in && jx < J) {
@@ -1099,6 +1112,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             tmax = y > tmax ? y : tmax;
           }
           u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
+          #pragma unroll 1
           for (u32 b0 = 0; b0 < nR; b0 += 32) {
             const u32 jj = b0 + lane;
             bool fin = false;
@@ -1195,6 +1209,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           if (nfin) {
             const u32 len = nR + nQ;
             u32 out = first_fin;
+            #pragma unroll 1
             for (u32 b0 = first_fin; b0 < len; b0 += 32) {
               const u32 jj = b0 + lane;
               const bool valid = jj < len;
@@ -1378,6 +1393,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               const u32 lrid = __shfl_sync(FULLMASK, rid, l);
               const u32 cv = mr.CONV[lrid];
               const u32 last = mr.BASE[cv] + mr.NR[cv];
+              #pragma unroll 1
               for (u32 q = lrid + 1 + lane; q < last; q += 32)
                 reinterpret_cast<uint8_t *>(rec + q)[26] = (uint8_t)TOKENSIM_REQ_REJECTED;
               nrj += last - lrid - 1;
@@ -1411,6 +1427,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     bool xpart = false;  // ... and it stays partial
     if (!pf_only) {
     // one pass: needing survivors -> requester list (ascending id), sum of c = ctx+1
+    #pragma unroll 1
     for (u32 b0 = 0; b0 < nR; b0 += 32) {
       const u32 jj = b0 + lane;
       const bool dec = jj < nR && !(hx && jj == nR - 1);  // the prefill in progress decodes nothing
@@ -1481,6 +1498,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       // 4. resume, head first, stop at the first misfit
       if (nQ > 0) {
         u64 cum_need = 0, cum_tok = 0;
+        #pragma unroll 1
         for (u32 b0 = 0; b0 < nQ; b0 += 32) {
           const u32 jj = nR3 + b0 + lane;
           const bool valid = b0 + lane < nQ;
@@ -1590,6 +1608,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     const u32 fresh0 = nR3 + nres;
     // CHUNKED: position of the entry whose prefill stays partial (no token this iteration)
     const u32 ppos = (hx && xpart) ? nR3 - 1 : (hnew ? xnew_pos : 0xffffffffu);
+    #pragma unroll 1
     for (u32 b0 = c0; b0 < nR; b0 += 32) {
       const u32 jj = b0 + lane;
       bool fin = false;
@@ -1695,6 +1714,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       // stable compaction of R u Q, dropping finished entries (rem == 0 within R)
       const u32 len = nR + nQ;
       u32 out = first_fin;
+      #pragma unroll 1
       for (u32 b0 = first_fin; b0 < len; b0 += 32) {
         const u32 jj = b0 + lane;
         const bool valid = jj < len;
@@ -1783,6 +1803,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     while ((i64)bin * W < t) flush_bin();
   }
   // unfinished requests still in R u Q: first-token latency and preemption count
+  #pragma unroll 1
   for (u32 x = lane; x < nR + nQ; x += 32) {
     const u32 id = S.id[x];
     write_record(rec + id, S.ttft[x], 0, 0, S.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);

@@ -179,16 +179,21 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
   {
     ulonglong2 *r2 = reinterpret_cast<ulonglong2 *>(rec);
     const ulonglong2 z = make_ulonglong2(0ull, 0ull);
+    #pragma unroll 1
     for (u32 x = lane; x < 2 * n; x += 32) r2[x] = z;
+    #pragma unroll 1
     for (u32 w = lane; w < nwD; w += 32) {
       const u32 fw = (u32)(totD >> 5), tl = (u32)(totD & 31u);
       S.bitmap[w] = w < fw ? 0xffffffffu : (w == fw && tl ? ((1u << tl) - 1u) : 0u);
     }
+    #pragma unroll 1
     for (u32 w = lane; w < nwP; w += 32) {
       const u32 fw = (u32)(totP >> 5), tl = (u32)(totP & 31u);
       bmP[w] = w < fw ? 0xffffffffu : (w == fw && tl ? ((1u << tl) - 1u) : 0u);
     }
+    #pragma unroll 1
     for (u32 w = lane; w < CAP / 32; w += 32) S.btfree[w] = 0xffffffffu;
+    #pragma unroll 1
     for (u32 x = lane; x < CAP; x += 32) pinfo[x] = x;
     __syncwarp();
   }
@@ -283,6 +288,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
         if (nQ > 0) {
           // first preempted slot = the resume head
           u32 qpos = 0;
+          #pragma unroll 1
           for (u32 b0 = 0; b0 < nA0; b0 += 32) {
             const u32 jj = b0 + lane;
             const u32 qb = __ballot_sync(FULLMASK, jj < nA0 && stt[jj] == ST_QUEUED);
@@ -326,6 +332,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
           u64 cdp0 = 0;
           u32 rmn = 0xffffffffu;
           i64 lmin = INF;
+          #pragma unroll 1
           for (u32 b0 = 0; b0 < nA0; b0 += 32) {
             const u32 jj = b0 + lane;
             u32 key = 64u + lane;
@@ -428,12 +435,14 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
             }
             if (!done_alloc) {
               const u32 nrep = (32 + B.bs - 1) / B.bs;
+              #pragma unroll 1
               for (u32 b0 = 0; b0 < nA0; b0 += 32) {
                 const u32 jj = b0 + lane;
                 const bool run = jj < nA0 && stt[jj] == ST_RUN;
                 const u32 c = run ? S.ctx[jj] : 0u;
                 const u32 r = B.mod(c);
                 u32 jx = r ? B.bs - r : 0u;
+                #pragma unroll 1
                 for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
                   const bool v = run && jx < J;
                   const u32 key = v ? jx : 64u + lane;
@@ -468,6 +477,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
               tm1 = y > tm1 ? y : tm1;
             }
             u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
+            #pragma unroll 1
             for (u32 b0 = 0; b0 < nA0; b0 += 32) {
               const u32 jj = b0 + lane;
               bool fin = false;
@@ -518,6 +528,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
             req_iters += (u64)nRun * J;
             if (nfin) {
               u32 out = first_fin;
+              #pragma unroll 1
               for (u32 b0 = first_fin; b0 < nD; b0 += 32) {
                 const u32 jj = b0 + lane;
                 const bool valid = jj < nD;
@@ -578,6 +589,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       // 3. decode reservation: RUN slots needing a block -> requester list (ascending id)
       u32 E = 0;
       u64 cdp = 0, npp = 0, app = 0;
+      #pragma unroll 1
       for (u32 b0 = 0; b0 < nA; b0 += 32) {
         const u32 jj = b0 + lane;
         const bool run = jj < nA && stt[jj] == ST_RUN;
@@ -644,6 +656,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
         if (nQ > 0) {
           u64 cum_need = 0, cum_tok = 0;
           u32 taken = 0;
+          #pragma unroll 1
           for (u32 b0 = 0; b0 < nA; b0 += 32) {
             const u32 jj = b0 + lane;
             const bool q = jj < nA && stt[jj] == ST_QUEUED;
@@ -793,6 +806,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       const u64 blocks = totD - nfreeD;
       // 8. commit
       u32 nfin = 0, first_fin = 0xffffffffu, rmin_d = 0xffffffffu;
+      #pragma unroll 1
       for (u32 b0 = 0; b0 < nA; b0 += 32) {
         const u32 jj = b0 + lane;
         bool fin = false;
@@ -833,6 +847,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       req_iters += nRun;
       if (nfin) {
         u32 out = first_fin;
+        #pragma unroll 1
         for (u32 b0 = first_fin; b0 < nD; b0 += 32) {
           const u32 jj = b0 + lane;
           const bool valid = jj < nD;
@@ -893,6 +908,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       while (fpfree < fdadm && pf_end <= t) {
         const FifoEnt e = fifo[fpfree];
         u32 mn = 0xffffffffu;
+        #pragma unroll 1
         for (u32 x0 = 0; x0 < e.len; x0 += 32) {
           ev_reserve(L, 32);
           const u32 x = x0 + lane;
@@ -995,6 +1011,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       // commit: the first token; o == 1 finishes here, the rest join D's pending FIFO with
       // their P block lists moved into the ring
       u32 nfin = 0;
+      #pragma unroll 1
       for (u32 b0 = 0; b0 < nb; b0 += 32) {
         const u32 pos = b0 + lane;
         const bool v = pos < nb;
@@ -1034,6 +1051,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
             free_blocks(bmP, tbl, lneed, lid, kP, 0, L, hintP);
             nfreeP += lneed;
           } else {
+            #pragma unroll 1
             for (u32 x = lane; x < lneed; x += 32) ring[(ring_tail + lseg + x) % ring_len] = tbl[x];
           }
         }
@@ -1062,8 +1080,10 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       while ((i64)TA[w].bin * W < t_final) trace_flush_bin(TA[w], w ? trcD : trcP, P.trace_cap, W, flags);
   }
   // unfinished: D slots and requests still pending at D carry their first-token latency
+  #pragma unroll 1
   for (u32 x = lane; x < nD; x += 32)
     write_record(rec + S.id[x], S.ttft[x], 0, 0, S.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);
+  #pragma unroll 1
   for (u32 x = fdadm + lane; x < ftail; x += 32) {
     const u32 id = fifo[x].id;
     write_record(rec + id, fifo[x].join - A[id], 0, 0, 0, TOKENSIM_REQ_UNFINISHED, 0);

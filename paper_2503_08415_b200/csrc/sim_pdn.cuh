@@ -176,20 +176,26 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   {
     ulonglong2 *r2 = reinterpret_cast<ulonglong2 *>(rec);
     const ulonglong2 z = make_ulonglong2(0ull, 0ull);
+    #pragma unroll 1
     for (u32 x = lane; x < 2 * n; x += 32) r2[x] = z;
     for (u32 w = 0; w < Y; ++w) {
       u32 *stt;
       const WarpSmem S = dview(M, w, CAP, &stt);
       const u32 fw = (u32)(totD >> 5), tl = (u32)(totD & 31u);
+      #pragma unroll 1
       for (u32 q = lane; q < nwD; q += 32) S.bitmap[q] = q < fw ? 0xffffffffu : (q == fw && tl ? ((1u << tl) - 1u) : 0u);
+      #pragma unroll 1
       for (u32 q = lane; q < CAP / 32; q += 32) S.btfree[q] = 0xffffffffu;
     }
     for (u32 w = 0; w < X; ++w) {
       u32 *bm = M.bmP + (size_t)w * P.nwords_max;
       const u32 fw = (u32)(totP >> 5), tl = (u32)(totP & 31u);
+      #pragma unroll 1
       for (u32 q = lane; q < nwP; q += 32) bm[q] = q < fw ? 0xffffffffu : (q == fw && tl ? ((1u << tl) - 1u) : 0u);
     }
+    #pragma unroll 1
     for (u32 x = lane; x < CAP; x += 32) M.pinfo[x] = x;
+    #pragma unroll 1
     for (u32 x = lane; x < n; x += 32) reqx[x] = INF;
     if (lane == 0) {
       const TraceAcc ta0 = {0, 0, 0, (i64)P.bin_ns, 0, 0};
@@ -386,6 +392,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       // (transfers on this worker's link end in pull order; slots are id-sorted, so find by id)
       while (d.nX > 0 && d.xhead_end <= t) {
         const u32 xid = fifo[d.fhead - d.nX].id;
+        #pragma unroll 1
         for (u32 b0 = 0; b0 < d.nD; b0 += 32) {
           const u32 jj = b0 + lane;
           const u32 hit = __ballot_sync(FULLMASK, jj < d.nD && S.id[jj] == xid);
@@ -433,6 +440,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         const u32 nA0 = d.nD;  // all slots (states are checked)
         if (d.nQ > 0) {
           u32 qpos = 0;
+          #pragma unroll 1
           for (u32 b0 = 0; b0 < nA0; b0 += 32) {
             const u32 jj = b0 + lane;
             const u32 qb = __ballot_sync(FULLMASK, jj < nA0 && stt[jj] == ST_QUEUED);
@@ -469,6 +477,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           __syncwarp();
           u64 cdp0 = 0;
           u32 rmn = 0xffffffffu;
+          #pragma unroll 1
           for (u32 b0 = 0; b0 < nA0; b0 += 32) {
             const u32 jj = b0 + lane;
             u32 key = 64u + lane;
@@ -518,12 +527,14 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
             __syncwarp();
             if (Ktot > 0) {
               const u32 nrep = (32 + B.bs - 1) / B.bs;
+              #pragma unroll 1
               for (u32 b0 = 0; b0 < nA0; b0 += 32) {
                 const u32 jj = b0 + lane;
                 const bool run = jj < nA0 && stt[jj] == ST_RUN;
                 const u32 c = run ? S.ctx[jj] : 0u;
                 const u32 r = B.mod(c);
                 u32 jx = r ? B.bs - r : 0u;
+                #pragma unroll 1
                 for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
                   const bool v = run && jx < J;
                   const u32 key = v ? jx : 64u + lane;
@@ -558,6 +569,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
               tm1 = y > tm1 ? y : tm1;
             }
             u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
+            #pragma unroll 1
             for (u32 b0 = 0; b0 < nA0; b0 += 32) {
               const u32 jj = b0 + lane;
               bool fin = false;
@@ -607,6 +619,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
             req_iters += (u64)d.nRun * J;
             if (nfin) {
               u32 out = first_fin;
+              #pragma unroll 1
               for (u32 b0 = first_fin; b0 < d.nD; b0 += 32) {
                 const u32 jj = b0 + lane;
                 const bool valid = jj < d.nD;
@@ -665,6 +678,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         // 3. decode reservation: RUN slots needing a block -> requester list (ascending id)
         u32 E = 0;
         u64 cdp = 0, npp = 0, app = 0;
+        #pragma unroll 1
         for (u32 b0 = 0; b0 < nA; b0 += 32) {
           const u32 jj = b0 + lane;
           const bool run = jj < nA && stt[jj] == ST_RUN;
@@ -730,6 +744,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           if (d.nQ > 0) {
             u64 cum_need = 0, cum_tok = 0;
             u32 taken = 0;
+            #pragma unroll 1
             for (u32 b0 = 0; b0 < nA; b0 += 32) {
               const u32 jj = b0 + lane;
               const bool q = jj < nA && stt[jj] == ST_QUEUED;
@@ -877,6 +892,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         for (u32 q = d.nD - nadm; q < d.nD; ++q) {
           const u32 qid = S.id[q];
           u32 p = 0;
+          #pragma unroll 1
           for (u32 b0 = 0; b0 < q; b0 += 32) {
             const u32 jj = b0 + lane;
             p += __popc(__ballot_sync(FULLMASK, jj < q && S.id[jj] < qid));
@@ -950,6 +966,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           // 8. commit
           u32 nfin = 0, first_fin = 0xffffffffu, rmin_d = 0xffffffffu;
           const u32 nC = d.nD;  // pulls (now sorted in) may have moved running slots past nA
+          #pragma unroll 1
           for (u32 b0 = 0; b0 < nC; b0 += 32) {
             const u32 jj = b0 + lane;
             bool fin = false;
@@ -990,6 +1007,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           req_iters += d.nRun;
           if (nfin) {
             u32 out = first_fin;
+            #pragma unroll 1
             for (u32 b0 = first_fin; b0 < d.nD; b0 += 32) {
               const u32 jj = b0 + lane;
               const bool valid = jj < d.nD;
@@ -1066,6 +1084,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       if (p.hmin <= t) {
         u32 out = 0;
         i64 hm = INF;
+        #pragma unroll 1
         for (u32 b0 = 0; b0 < p.nhold; b0 += 32) {
           const u32 x = b0 + lane;
           const bool v = x < p.nhold;
@@ -1165,6 +1184,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         // commit: the first token; o == 1 finishes here, the rest become holders whose block
         // lists move to the per-request table; the whole batch is dispatched onward at te
         u32 nfin = 0;
+        #pragma unroll 1
         for (u32 b0 = 0; b0 < nb; b0 += 32) {
           const u32 pos = b0 + lane;
           const bool v = pos < nb;
@@ -1195,6 +1215,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
               free_blocks(bmP, tbl, lneed, lid, p.k, koff, L, p.hint);
               p.nfree += lneed;
             } else {
+              #pragma unroll 1
               for (u32 x = lane; x < lneed; x += 32) pblk[(size_t)lid * btl + x] = tbl[x];
             }
           }
@@ -1258,9 +1279,11 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     u32 *stt;
     const WarpSmem S = dview(M, w, CAP, &stt);
     const DScal &d = M.ds[w];
+    #pragma unroll 1
     for (u32 x = lane; x < d.nD; x += 32)
       write_record(rec + S.id[x], S.ttft[x], 0, 0, S.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);
     const FifoEnt *fifo = fifo0 + (size_t)w * n;
+    #pragma unroll 1
     for (u32 x = d.fhead + lane; x < d.ftail; x += 32) {
       const u32 id = fifo[x].id;
       write_record(rec + id, fifo[x].join - A[id], 0, 0, 0, TOKENSIM_REQ_UNFINISHED, 0);
@@ -1269,6 +1292,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   for (u32 w = 0; w < X; ++w) {
     const PScal &p = M.ps[w];
     if (p.nb == 0) continue;
+    #pragma unroll 1
     for (u32 x = lane; x < p.nb; x += 32) {
       const u32 id = batch0[(size_t)w * CAP + x];
       if (OU[id] > 1) write_record(rec + id, p.tdisp - A[id], 0, 0, 0, TOKENSIM_REQ_UNFINISHED, 0);
