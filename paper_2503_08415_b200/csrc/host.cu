@@ -434,7 +434,8 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
   }
   h->full = opt->topology == TOKENSIM_PD_PAIR || w.multi_round || opt->memory_cache ||
             opt->link_mode == TOKENSIM_LINK_PRELOAD;
-  for (u32 i = 0; i < n_pol; ++i) h->full |= pol[i].iteration_mode == TOKENSIM_CHUNKED;
+  // prefill-first and chunked iterations run in the full variant (the lean one keeps MIXED only)
+  for (u32 i = 0; i < n_pol; ++i) h->full |= pol[i].iteration_mode != TOKENSIM_MIXED;
   const size_t per_warp = h->smem_per_warp();
   if (per_warp > 227 * 1024) {
     delete h;

@@ -1,4 +1,4 @@
-// sim_base.cu -- the lean simulation kernel variant: unified topology, MIXED / prefill-first
+// sim_base.cu -- the lean simulation kernel variant: unified topology, MIXED
 // iterations, generated or traced single-round workloads (see sim_core.cuh).
 #include "sim_core.cuh"
 

@@ -1,7 +1,8 @@
 // sim_core.cuh -- a.2-a.7: the persistent per-point simulation kernel.
-// Included by sim_base.cu (MIXED / prefill-first unified sweeps: every later feature compiled
-// out, so the common path keeps its registers and instruction count) and sim_full.cu (chunked
-// prefill, multi-round + memory cache, preload link, the P/D pair and the xP:yD node).
+// Included by sim_base.cu (MIXED unified sweeps: every later feature compiled out, so the
+// common path keeps its registers and instruction footprint -- the kernel is instruction-fetch
+// bound at 8 warps/SM) and sim_full.cu (prefill-first and chunked iterations, multi-round +
+// memory cache, preload link, the P/D pair and the xP:yD node).
 //
 // ONE WARP PER POINT, pulled from an atomic longest-first queue.  The running set R and
 // the resume queue Q are one array of request slots in ascending id (R is a prefix, Q
@@ -669,7 +670,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   const bool SWAPM = PL.preempt == TOKENSIM_SWAP;
   const bool RATIO = PL.kind == TOKENSIM_CONT_RATIO;
   const bool STATICP = PL.kind == TOKENSIM_STATIC;
-  const bool PFM = PL.mode == TOKENSIM_PREFILL_FIRST;
+  const bool PFM = FULL && PL.mode == TOKENSIM_PREFILL_FIRST;  // the lean variant runs MIXED only
   const bool CHK = FULL && PL.mode == TOKENSIM_CHUNKED;
   const bool MRM = FULL && P.multi_round != 0;  // NEXT-2: request ids are (conversation, round) rids
   const bool CACHE = MRM && P.memory_cache != 0;
