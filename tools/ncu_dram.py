@@ -17,7 +17,10 @@ rep = os.path.join(out, f"sim_{cfg}")
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "-k", "regex:sim_kernel",
        "-c", "1", "-f", "-o", rep, sys.executable, os.path.join(root, "tools", "prof_run.py"), "--config", cfg]
-subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+# the product library (prof_run.py would otherwise pick the profiling build)
+env = dict(os.environ, TOKENSIM_LIB=os.environ.get("TOKENSIM_LIB") or
+           os.path.join(root, "paper_2503_08415_b200", "libtokensim.so"))
+subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, env=env)
 raw = subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "raw", "--csv", "--print-units", "base"], check=True,
                      capture_output=True,
                      text=True).stdout
@@ -33,10 +36,10 @@ def f(name):
         return None
 
 
-stalls = {}
+stalls = {}  # PC-sampling stall reasons (share of all samples)
 for k in hdr:
-    if k.startswith("smsp__average_warp_latency_issue_stalled_") and k.endswith(".ratio"):
-        stalls[k[len("smsp__average_warp_latency_issue_stalled_"):-len(".ratio")]] = f(k)
+    if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued"):
+        stalls[k[len("smsp__pcsamp_warps_issue_stalled_"):]] = f(k)
 tot = sum(v for v in stalls.values() if v) or 1.0
 summary = {
     "source": f"ncu --set full --clock-control none --import-source on -k regex:sim_kernel -c 1 "
@@ -52,6 +55,9 @@ summary = {
     "grid": f("launch__grid_size"),
     "block": f("launch__block_size"),
     "warp_instructions": f("smsp__inst_executed.sum"),
+    "no_instruction_stall_pct_of_samples": (100.0 * f("smsp__pcsamp_warps_issue_stalled_no_instructions") /
+                                            f("smsp__pcsamp_sample_count")
+                                            if f("smsp__pcsamp_sample_count") else None),
     "stall_share_pct": {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda x: -(x[1] or 0))
                         if v and 100 * v / tot >= 0.5},
 }
