@@ -600,7 +600,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   const size_t per_warp = h->smem_per_warp();
   Layout L0 = make_layout(h, n_run, sms, 0);
   int occ = 0;
-  e = sim_occupancy(h->full, (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, &occ);
+  e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general), (int)h->cap, (int)L0.wpb,
+                    per_warp * L0.wpb, &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
   const Layout L = make_layout(h, n_run, sms, occ);

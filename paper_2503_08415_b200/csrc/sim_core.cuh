@@ -1851,12 +1851,14 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   __syncwarp();
 }
 
-template <int CAP, bool FULL, bool P2>
+// V: 0 = lean unified (MIXED), 1 = full unified, 2 = 1P:1D pair, 3 = xP:yD node.  One kernel per
+// variant: its registers and instruction footprint are those of the code it can run.
+template <int CAP, int V, bool P2>
 __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
-  const bool pd = FULL && P.topology == TOKENSIM_PD_PAIR;
-  const bool node = pd && P.pd_general;
+  constexpr bool pd = V >= 2;
+  constexpr bool node = V == 3;
   const size_t base = smem_per_warp_bytes(CAP, P.nwords_max);
   const size_t per_warp =
       node ? pdn_smem_per_warp(CAP, P.nwords_max, P.pd_x, P.pd_y) : base + (pd ? smem_pd_extra(CAP, P.nwords_max) : 0);
@@ -1869,59 +1871,56 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
     qi = __shfl_sync(FULLMASK, qi, 0);
     if ((u64)qi >= P.n_run) break;
     const u64 j = P.order[qi];
-    if constexpr (FULL) {
-      if (node) simulate_pdn<CAP, P2>(P, j, smem_raw + wib * per_warp, bt);
-      else if (pd) simulate_pd<CAP, P2>(P, j, S, smem_raw + wib * per_warp + base, bt);
-      else simulate_unified<CAP, true, P2>(P, j, S, bt);
-    } else {
-      simulate_unified<CAP, false, P2>(P, j, S, bt);
-    }
+    if constexpr (V == 3) simulate_pdn<CAP, P2>(P, j, smem_raw + wib * per_warp, bt);
+    else if constexpr (V == 2) simulate_pd<CAP, P2>(P, j, S, smem_raw + wib * per_warp + base, bt);
+    else simulate_unified<CAP, V == 1, P2>(P, j, S, bt);
   }
 }
 
-// launch / occupancy helpers for one variant (instantiated by sim_base.cu / sim_full.cu)
-template <int CAP, bool FULL, bool P2>
+// launch / occupancy helpers for one variant (instantiated by sim_base.cu, sim_full.cu,
+// sim_pair.cu, sim_node.cu)
+template <int CAP, int V, bool P2>
 static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, FULL, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, V, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  sim_kernel<CAP, FULL, P2><<<blocks, wpb * 32, smem, st>>>(p);
+  sim_kernel<CAP, V, P2><<<blocks, wpb * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
-template <int CAP, bool FULL, bool P2>
+template <int CAP, int V, bool P2>
 static cudaError_t occ_t(int wpb, size_t smem, int *b) {
-  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, FULL, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, V, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP, FULL, P2>, wpb * 32, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP, V, P2>, wpb * 32, smem);
 }
-template <bool FULL, bool P2>
+template <int V, bool P2>
 static cudaError_t launch_sim_c(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
   switch (cap) {
-    case 32: return launch_sim_t<32, FULL, P2>(p, wpb, blocks, smem, st);
-    case 256: return launch_sim_t<256, FULL, P2>(p, wpb, blocks, smem, st);
-    case 1024: return launch_sim_t<1024, FULL, P2>(p, wpb, blocks, smem, st);
+    case 32: return launch_sim_t<32, V, P2>(p, wpb, blocks, smem, st);
+    case 256: return launch_sim_t<256, V, P2>(p, wpb, blocks, smem, st);
+    case 1024: return launch_sim_t<1024, V, P2>(p, wpb, blocks, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
-template <bool FULL>
+template <int V>
 static cudaError_t launch_sim_v(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
-  return p.all_p2 ? launch_sim_c<FULL, true>(p, cap, wpb, blocks, smem, st)
-                  : launch_sim_c<FULL, false>(p, cap, wpb, blocks, smem, st);
+  return p.all_p2 ? launch_sim_c<V, true>(p, cap, wpb, blocks, smem, st)
+                  : launch_sim_c<V, false>(p, cap, wpb, blocks, smem, st);
 }
-template <bool FULL, bool P2>
+template <int V, bool P2>
 static cudaError_t sim_occupancy_c(int cap, int wpb, size_t smem, int *b) {
   switch (cap) {
-    case 32: return occ_t<32, FULL, P2>(wpb, smem, b);
-    case 256: return occ_t<256, FULL, P2>(wpb, smem, b);
-    case 1024: return occ_t<1024, FULL, P2>(wpb, smem, b);
+    case 32: return occ_t<32, V, P2>(wpb, smem, b);
+    case 256: return occ_t<256, V, P2>(wpb, smem, b);
+    case 1024: return occ_t<1024, V, P2>(wpb, smem, b);
     default: return cudaErrorInvalidValue;
   }
 }
-template <bool FULL>
+template <int V>
 static cudaError_t sim_occupancy_v(int cap, int wpb, size_t smem, int *b) {
   int b1 = 0, b2 = 0;  // the same resources either way; take the smaller to be safe
-  cudaError_t e = sim_occupancy_c<FULL, true>(cap, wpb, smem, &b1);
+  cudaError_t e = sim_occupancy_c<V, true>(cap, wpb, smem, &b1);
   if (e != cudaSuccess) return e;
-  e = sim_occupancy_c<FULL, false>(cap, wpb, smem, &b2);
+  e = sim_occupancy_c<V, false>(cap, wpb, smem, &b2);
   *b = b1 < b2 ? b1 : b2;
   return e;
 }

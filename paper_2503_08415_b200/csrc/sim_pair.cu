@@ -1,0 +1,11 @@
+// sim_pair.cu -- the 1P:1D disaggregated pair kernel variant (a.9, sim_pd.cuh).
+#define TS_LOGS_BYREF 1
+
+#include "sim_core.cuh"
+
+namespace ts {
+cudaError_t launch_sim_pair(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
+  return launch_sim_v<2>(p, cap, wpb, blocks, smem, st);
+}
+cudaError_t sim_occupancy_pair(int cap, int wpb, size_t smem, int *b) { return sim_occupancy_v<2>(cap, wpb, smem, b); }
+}  // namespace ts

@@ -156,14 +156,24 @@ __host__ __device__ inline Coords decode_point(u64 point, u32 n_pol, u32 n_rates
 
 // launchers (sweep.cu)
 cudaError_t launch_workload(const SweepParams &p, cudaStream_t st);
+// kernel variants: 0 lean unified, 1 full unified, 2 1P:1D pair, 3 xP:yD node
 cudaError_t launch_sim_base(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                             cudaStream_t st);
 cudaError_t launch_sim_full(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                             cudaStream_t st);
+cudaError_t launch_sim_pair(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
+                            cudaStream_t st);
+cudaError_t launch_sim_node(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
+                            cudaStream_t st);
+inline int sim_variant(bool full, bool pd, bool pd_general) { return !full ? 0 : !pd ? 1 : pd_general ? 3 : 2; }
 inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                               cudaStream_t st) {
-  return p.full ? launch_sim_full(p, cap, warps_per_block, blocks, smem, st)
-                : launch_sim_base(p, cap, warps_per_block, blocks, smem, st);
+  switch (sim_variant(p.full != 0, p.topology == TOKENSIM_PD_PAIR, p.pd_general != 0)) {
+    case 0: return launch_sim_base(p, cap, warps_per_block, blocks, smem, st);
+    case 1: return launch_sim_full(p, cap, warps_per_block, blocks, smem, st);
+    case 2: return launch_sim_pair(p, cap, warps_per_block, blocks, smem, st);
+    default: return launch_sim_node(p, cap, warps_per_block, blocks, smem, st);
+  }
 }
 cudaError_t launch_summary(const SweepParams &p, cudaStream_t st);
 cudaError_t launch_quantiles(const SweepParams &p, u64 j, u32 metric, const u32 *d_ranks, u32 n_q,
@@ -178,9 +188,15 @@ inline size_t pdn_global_per_warp(u64 n, u32 cap, u32 btl, u32 x, u32 y) {
 }
 cudaError_t sim_occupancy_base(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
 cudaError_t sim_occupancy_full(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
-inline cudaError_t sim_occupancy(bool full, int cap, int warps_per_block, size_t smem, int *blocks_per_sm) {
-  return full ? sim_occupancy_full(cap, warps_per_block, smem, blocks_per_sm)
-              : sim_occupancy_base(cap, warps_per_block, smem, blocks_per_sm);
+cudaError_t sim_occupancy_pair(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
+cudaError_t sim_occupancy_node(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
+inline cudaError_t sim_occupancy(int variant, int cap, int warps_per_block, size_t smem, int *blocks_per_sm) {
+  switch (variant) {
+    case 0: return sim_occupancy_base(cap, warps_per_block, smem, blocks_per_sm);
+    case 1: return sim_occupancy_full(cap, warps_per_block, smem, blocks_per_sm);
+    case 2: return sim_occupancy_pair(cap, warps_per_block, smem, blocks_per_sm);
+    default: return sim_occupancy_node(cap, warps_per_block, smem, blocks_per_sm);
+  }
 }
 
 }  // namespace ts
