@@ -16,6 +16,17 @@ namespace ts {
 #ifndef TS_PROFILE
 #define TS_PROFILE 0
 #endif
+// TS_COMPACT (set by sim_base_c.cu, the lean kernel for sweeps with several warps per SM): small hot helpers are
+// compiled out of line, trading a call's latency for a smaller instruction footprint -- at
+// 8 warps per SM the kernels are instruction-fetch bound.
+#ifndef TS_COMPACT
+#define TS_COMPACT 0
+#endif
+#if TS_COMPACT
+#define TS_HELPER static __device__ __noinline__
+#else
+#define TS_HELPER __device__ __forceinline__
+#endif
 __device__ __forceinline__ long long prof_clock() {
 #if TS_PROFILE
   return clock64();
@@ -51,7 +62,7 @@ __device__ __forceinline__ u64 shfl64(u64 x, u32 src) { return __shfl_sync(FULLM
 __device__ __forceinline__ i64 shfl64i(i64 x, u32 src) { return __shfl_sync(FULLMASK, x, src); }
 
 // r-th (0-based) set bit of w (r < popc(w))
-__device__ __forceinline__ u32 select_bit(u32 w, u32 r) {
+TS_HELPER u32 select_bit(u32 w, u32 r) {
   u32 pos = 0;
 #pragma unroll
   for (u32 s = 16; s; s >>= 1) {

@@ -600,8 +600,9 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   const size_t per_warp = h->smem_per_warp();
   Layout L0 = make_layout(h, n_run, sms, 0);
   int occ = 0;
-  e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general), (int)h->cap, (int)L0.wpb,
-                    per_warp * L0.wpb, &occ);
+  e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general,
+                                (u64)L0.blocks * L0.wpb > (u64)sms),
+                    (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
   const Layout L = make_layout(h, n_run, sms, occ);
@@ -730,6 +731,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.mr_bytes_per_warp = L.mr_per_warp;
   P.pd_general = h->pd_general ? 1u : 0u;
   P.full = h->full ? 1u : 0u;
+  P.n_sms = (u32)sms;
   {
     bool p2 = true;  // the kernels specialise their block arithmetic to shifts and masks
     for (const auto &pl : h->pol) p2 = p2 && (pl.block_size & (pl.block_size - 1)) == 0;

@@ -929,11 +929,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         // pass over R: C_d(0), min rem, and the needs histogram by iteration offset (lane j
         // <-> iteration k+j).  A slot needs a block at offsets j = j0 (mod bs), j0 = -ctx mod bs,
         // so n_j = cnt[j mod bs]: count slots per j0 with match_any (no atomics).
+        u64 cdp = 0;
+        u32 rmn = 0xffffffffu;
         S.scratch[lane] = 0;
         S.scratch[32 + lane] = 0;
         __syncwarp();
-        u64 cdp = 0;
-        u32 rmn = 0xffffffffu;
         #pragma unroll 1
         for (u32 b0 = 0; b0 < nR; b0 += 32) {
           const u32 jj = b0 + lane;
@@ -1851,13 +1851,14 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   __syncwarp();
 }
 
-// V: 0 = lean unified (MIXED), 1 = full unified, 2 = 1P:1D pair, 3 = xP:yD node.  One kernel per
-// variant: its registers and instruction footprint are those of the code it can run.
+// V: 0 = lean unified (MIXED), 1 = full unified, 2 = 1P:1D pair, 3 = xP:yD node, 4 = the lean
+// one with compact helpers (sim_base_c.cu; sweeps that run several warps per SM).  One kernel
+// per variant: its registers and instruction footprint are those of the code it can run.
 template <int CAP, int V, bool P2>
 __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
-  constexpr bool pd = V >= 2;
+  constexpr bool pd = V == 2 || V == 3;
   constexpr bool node = V == 3;
   const size_t base = smem_per_warp_bytes(CAP, P.nwords_max);
   const size_t per_warp =
@@ -1873,7 +1874,7 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
     const u64 j = P.order[qi];
     if constexpr (V == 3) simulate_pdn<CAP, P2>(P, j, smem_raw + wib * per_warp, bt);
     else if constexpr (V == 2) simulate_pd<CAP, P2>(P, j, S, smem_raw + wib * per_warp + base, bt);
-    else simulate_unified<CAP, V == 1, P2>(P, j, S, bt);
+    else simulate_unified<CAP, V == 1, P2>(P, j, S, bt);  // V 4: the lean one built with TS_COMPACT
   }
 }
 

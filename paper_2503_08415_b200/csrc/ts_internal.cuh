@@ -120,6 +120,7 @@ struct SweepParams {
   u64 pdn_bytes_per_warp;
   u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
   u32 full, all_p2;                       // 1: the full kernel variant (sim_full.cu); every block size a power of two
+  u32 n_sms, pad5;                        // SMs of the device (launch choice of the compact lean kernel)
   u32 link_mode, pad2;                    // NEXT-4: TOKENSIM_LINK_SEQUENTIAL | PRELOAD
   u64 preload_buf;                        // preload buffer bytes
   // NEXT-2 multi-round conversations + memory cache.  With multi_round, n_req = 7 * n_conv is
@@ -165,11 +166,18 @@ cudaError_t launch_sim_pair(const SweepParams &p, int cap, int warps_per_block, 
                             cudaStream_t st);
 cudaError_t launch_sim_node(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                             cudaStream_t st);
-inline int sim_variant(bool full, bool pd, bool pd_general) { return !full ? 0 : !pd ? 1 : pd_general ? 3 : 2; }
+cudaError_t launch_sim_base_c(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
+                              cudaStream_t st);
+// several warps per SM: the lean kernel with compact helpers (variant 4)
+inline int sim_variant(bool full, bool pd, bool pd_general, bool multi_warp = false) {
+  return !full ? (multi_warp ? 4 : 0) : !pd ? 1 : pd_general ? 3 : 2;
+}
 inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                               cudaStream_t st) {
-  switch (sim_variant(p.full != 0, p.topology == TOKENSIM_PD_PAIR, p.pd_general != 0)) {
+  switch (sim_variant(p.full != 0, p.topology == TOKENSIM_PD_PAIR, p.pd_general != 0,
+                      (u64)blocks * (u64)warps_per_block > (u64)p.n_sms)) {
     case 0: return launch_sim_base(p, cap, warps_per_block, blocks, smem, st);
+    case 4: return launch_sim_base_c(p, cap, warps_per_block, blocks, smem, st);
     case 1: return launch_sim_full(p, cap, warps_per_block, blocks, smem, st);
     case 2: return launch_sim_pair(p, cap, warps_per_block, blocks, smem, st);
     default: return launch_sim_node(p, cap, warps_per_block, blocks, smem, st);
@@ -190,11 +198,13 @@ cudaError_t sim_occupancy_base(int cap, int warps_per_block, size_t smem, int *b
 cudaError_t sim_occupancy_full(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
 cudaError_t sim_occupancy_pair(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
 cudaError_t sim_occupancy_node(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
+cudaError_t sim_occupancy_base_c(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
 inline cudaError_t sim_occupancy(int variant, int cap, int warps_per_block, size_t smem, int *blocks_per_sm) {
   switch (variant) {
     case 0: return sim_occupancy_base(cap, warps_per_block, smem, blocks_per_sm);
     case 1: return sim_occupancy_full(cap, warps_per_block, smem, blocks_per_sm);
     case 2: return sim_occupancy_pair(cap, warps_per_block, smem, blocks_per_sm);
+    case 4: return sim_occupancy_base_c(cap, warps_per_block, smem, blocks_per_sm);
     default: return sim_occupancy_node(cap, warps_per_block, smem, blocks_per_sm);
   }
 }
