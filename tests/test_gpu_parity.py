@@ -82,6 +82,23 @@ def test_c2_sharding_invariance(api):
         assert part.tobytes() == np.ascontiguousarray(ref).tobytes(), (b, s)
 
 
+def test_lean_kernel_variants_agree(api):
+    """More points than SMs run the compact lean kernel (several warps per SM, variant 4); a
+    strided run of at most one point per SM runs the inline one (variant 0).  Same bytes, and a
+    non-power-of-two block size (the general block arithmetic instantiation) agrees too."""
+    for bs in (16, 12):
+        cfg = replace(si.c2(n_seeds=24), policies=[si.Policy(block_size=bs)])
+        assert cfg.num_points > 148
+        full = run_gpu(api, cfg)
+        s = full.summaries()
+        for b in range(3):
+            part = run_gpu(api, cfg, b, None, 3)
+            assert part.summaries().tobytes() == np.ascontiguousarray(s[b::3]).tobytes(), (bs, b)
+            for p in (b, b + 3 * 40):
+                assert part.records(p).tobytes() == full.records(p).tobytes(), (bs, p)
+        check_points(full, cfg, [0, 200, cfg.num_points - 1], records=True)
+
+
 def _micro(rng):
     n = int(rng.integers(1, 80))
     a = np.sort(rng.integers(0, 3_000_000_000, n))
