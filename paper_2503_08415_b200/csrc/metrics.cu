@@ -29,6 +29,8 @@ struct SelShared {
   u32 cnt;
   u32 digit, rem;
   u64 red[32];
+  u32 hist3[3][256];  // block_select3: one histogram per distinct target prefix
+  u32 digit3[3], rem3[3];
 };
 
 // Exact rank-th smallest (1-based) of keys[0..cnt) by MSD radix select, 8 bits per pass,
@@ -84,6 +86,80 @@ __device__ u64 block_select(const u64 *keys, u32 cnt, u32 rank, u64 kmin, u64 km
     __syncthreads();
   }
   return prefix;
+}
+
+// The rank[0..3)-th smallest keys in one set of MSD passes (ranks ascending, so the targets'
+// prefixes are ordered; targets with the same prefix share a histogram).  Same digits as three
+// block_select calls, a third of the passes over the keys.
+__device__ void block_select3(const u64 *keys, u32 cnt, const u32 rank[3], u64 kmin, u64 kmax, SelShared &sh,
+                              u64 out[3]) {
+  const u32 tid = threadIdx.x, nt = blockDim.x;
+  const u64 diff = kmin ^ kmax;
+  if (diff == 0) {
+    out[0] = out[1] = out[2] = kmin;
+    return;
+  }
+  int top = 63 - __clzll((long long)diff);
+  int shift = (top / 8) * 8;
+  u64 mask = shift + 8 >= 64 ? 0ull : ~((1ull << (shift + 8)) - 1ull);
+  u64 pre[3];
+  u32 rem[3];
+  for (int t = 0; t < 3; ++t) {
+    pre[t] = kmin & mask;
+    rem[t] = rank[t];
+  }
+  for (; shift >= 0; shift -= 8) {
+    // histogram index of each target: the first target with the same prefix
+    const u32 h1 = pre[1] == pre[0] ? 0u : 1u;
+    const u32 h2 = pre[2] == pre[1] ? h1 : 2u;
+    for (u32 x = tid; x < 3 * 256; x += nt) (&sh.hist3[0][0])[x] = 0;
+    __syncthreads();
+    for (u32 x = tid; x < cnt; x += nt) {
+      const u64 kk = keys[x];
+      const u64 km = kk & mask;
+      const u32 bin = (u32)(kk >> shift) & 255u;
+      if (km == pre[0]) atomicAdd(&sh.hist3[0][bin], 1u);
+      else if (km == pre[1]) atomicAdd(&sh.hist3[h1][bin], 1u);
+      else if (km == pre[2]) atomicAdd(&sh.hist3[h2][bin], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      for (int t = 0; t < 3; ++t) {
+        const u32 h = t == 0 ? 0u : t == 1 ? h1 : h2;
+        u32 loc[8], sm = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          loc[q] = sh.hist3[h][tid * 8 + q];
+          sm += loc[q];
+        }
+        const u32 incl = scan_incl(sm);
+        const u32 excl = incl - sm;
+        const u32 hit = __ballot_sync(FULLMASK, incl >= rem[t]);
+        const u32 L = (u32)(__ffs(hit) - 1);
+        if (tid == L) {
+          u32 c = excl, d = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (c + loc[q] >= rem[t]) {
+              d = tid * 8 + q;
+              break;
+            }
+            c += loc[q];
+          }
+          sh.digit3[t] = d;
+          sh.rem3[t] = rem[t] - c;
+        }
+      }
+    }
+    __syncthreads();
+    for (int t = 0; t < 3; ++t) {
+      pre[t] |= (u64)sh.digit3[t] << shift;
+      rem[t] = sh.rem3[t];
+    }
+    mask |= 255ull << shift;
+    __syncthreads();
+  }
+  for (int t = 0; t < 3; ++t) out[t] = pre[t];
 }
 
 __device__ u64 block_reduce_u64(u64 v, bool is_max, SelShared &sh) {
@@ -189,35 +265,48 @@ __global__ void __launch_bounds__(256) summary_kernel(SweepParams P, u64 *scratc
   s_e2e = block_reduce_u64(s_e2e, false, sh);
   s_mt = block_reduce_u64(s_mt, false, sh);
   dig_r = block_reduce_u64(dig_r, false, sh);
-  // sequential fp64 sums for TPOT / NORM in ascending id (SURVEY c.6)
+  // sequential fp64 sums for TPOT / NORM in ascending id (SURVEY c.6): the terms (two fp64
+  // divisions each) are formed by all threads into the key buffer, then one thread adds them in
+  // id order; excluded requests contribute +0.0, which leaves a running sum >= +0 unchanged
   __shared__ double seq_tp, seq_norm;
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (u32 i = 0; i < n; ++i) {
+  double *term = reinterpret_cast<double *>(keys);
+  for (u32 pass = 0; pass < 2; ++pass) {
+    for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
       const tokensim_request_record r = rec[i];
-      if (r.status != TOKENSIM_REQ_FINISHED) continue;
       const u32 o = OU[i];
-      if (o >= 2) a = __dadd_rn(a, __ddiv_rn(__ll2double_rn(r.e2e_ns - r.ttft_ns), __uint2double_rn(o - 1)));
-      b = __dadd_rn(b, __ddiv_rn(__ll2double_rn(r.e2e_ns), __uint2double_rn(o)));
+      double v = 0.0;
+      if (r.status == TOKENSIM_REQ_FINISHED) {
+        if (pass == 0) {
+          if (o >= 2) v = __ddiv_rn(__ll2double_rn(r.e2e_ns - r.ttft_ns), __uint2double_rn(o - 1));
+        } else {
+          v = __ddiv_rn(__ll2double_rn(r.e2e_ns), __uint2double_rn(o));
+        }
+      }
+      term[i] = v;
     }
-    seq_tp = a;
-    seq_norm = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0;
+#pragma unroll 8
+      for (u32 i = 0; i < n; ++i) a = __dadd_rn(a, term[i]);
+      if (pass == 0) seq_tp = a;
+      else seq_norm = a;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   tokensim_summary S;
   const u64 nfin = st.n_finished;
   const u32 qbp[4] = {5000, 9000, 9900, 10000};
   for (u32 m = 0; m < 5; ++m) {
     u64 kmin, kmax;
     const u32 cnt = build_keys(m, rec, OU, n, keys, sh, kmin, kmax);
-    for (u32 qi = 0; qi < 4; ++qi) {
-      double v = 0.0;
-      if (cnt) {
-        const u64 key = qi == 3 ? kmax : block_select(keys, cnt, nearest_rank(qbp[qi], cnt), kmin, kmax, sh);
-        v = __longlong_as_double((long long)key);
-      }
-      S.stat[m][qi] = v;
+    u64 sel[3] = {0, 0, 0};
+    if (cnt) {
+      const u32 rk[3] = {nearest_rank(qbp[0], cnt), nearest_rank(qbp[1], cnt), nearest_rank(qbp[2], cnt)};
+      block_select3(keys, cnt, rk, kmin, kmax, sh, sel);
     }
+    for (u32 qi = 0; qi < 4; ++qi)
+      S.stat[m][qi] = cnt ? __longlong_as_double((long long)(qi == 3 ? kmax : sel[qi])) : 0.0;
     double mean = 0.0;
     if (cnt) {
       const double dn = __ull2double_rn(cnt);
