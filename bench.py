@@ -311,10 +311,21 @@ def run_ours(args):
     hbm_peak = peaks.get("hbm_gbs")
     hbm_ach = HBM_BYTES_PER_UNIT * ri_local / sim_avg_s / 1e9
     traffic = None
+    issue_line = None
     tr_path = os.path.join(ROOT, "profiles", f"dram_{args.config}.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+            nc = json.load(open(tr_path))
+            traffic = nc.get("dram_bytes_per_launch")
+            # SM issue line (supplementary, from the same ncu capture): warp instructions the launch
+            # issued / this run's kernel time, against 148 SMs x 4 schedulers x 1 warp-instr/clk
+            wi = nc.get("warp_instructions")
+            if wi:
+                ach = wi / sim_avg_s / 1e9
+                pk = 148 * 4 * 1.965
+                issue_line = {"warp_instructions_per_launch": wi, "achieved_gwips": ach, "peak_gwips": pk,
+                              "frac": ach / pk, "no_instruction_stall_pct": nc.get("no_instruction_stall_pct_of_samples"),
+                              "source": "ncu warp instructions of one launch (profiles/dram_<config>.json)"}
         except Exception:
             traffic = None
 
@@ -340,7 +351,8 @@ def run_ours(args):
                          "peak_source": "148 SMs x 128 lanes x 1965 MHz (B200_PROFILING.md nominal table; DESIGN.md)",
                          "hbm_line": {"bytes_per_unit": HBM_BYTES_PER_UNIT, "achieved_gbs": hbm_ach,
                                       "peak_gbs": hbm_peak, "frac": (hbm_ach / hbm_peak) if hbm_peak else None,
-                                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}},
+                                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
+                         "issue_line": issue_line},
             "kernel_ms": {"workload": statistics.mean(wl_ms), "sim": statistics.mean(sim_ms),
                           "summary": statistics.mean(sum_ms)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -63,5 +63,9 @@ summary = {
 }
 with open(os.path.join(out, f"dram_{cfg}.json"), "w") as fh:
     json.dump(summary, fh, indent=1)
+if os.environ.get("NCU_SOURCE_CSV"):  # keep the source page (per-SASS stalls) for tools/ncu_noinst.py
+    with open(os.path.join(out, f"src_{cfg}.csv"), "w") as fh:
+        subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "source", "--csv", "--print-source=cuda,sass"],
+                       check=True, stdout=fh, stderr=subprocess.DEVNULL)
 os.remove(rep + ".ncu-rep")
 print(json.dumps({k: summary[k] for k in ("kernel", "duration_ms", "dram_bytes_per_launch", "issue_active_pct")}))
