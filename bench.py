@@ -245,6 +245,8 @@ def run_ours(args):
     s = sw.summaries()
     ri_local = int(s["n_request_iterations"].sum())
     assert (s["status_flags"] & 16 == 0).all(), "internal error flag set"
+    it_max = int(s["n_iterations"].max()) if len(s) else 0  # the longest serial chain
+    it_mean = float(s["n_iterations"].mean()) if len(s) else 0.0
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -352,7 +354,11 @@ def run_ours(args):
                          "hbm_line": {"bytes_per_unit": HBM_BYTES_PER_UNIT, "achieved_gbs": hbm_ach,
                                       "peak_gbs": hbm_peak, "frac": (hbm_ach / hbm_peak) if hbm_peak else None,
                                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
-                         "issue_line": issue_line},
+                         "issue_line": issue_line,
+                         # the serial critical path: iterations of the longest point and the kernel
+                         # time per iteration of that chain (one point never splits across warps)
+                         "chain": {"max_iterations_per_point": it_max, "mean_iterations_per_point": it_mean,
+                                   "ns_per_chain_iteration": statistics.mean(sim_ms) * 1e6 / max(1, it_max)}},
             "kernel_ms": {"workload": statistics.mean(wl_ms), "sim": statistics.mean(sim_ms),
                           "summary": statistics.mean(sum_ms)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
