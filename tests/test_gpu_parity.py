@@ -296,6 +296,19 @@ def test_c5_reduced_grid(api):
     check_pd_points(sw, cfg, sample_points(cfg.num_points, target=40, corners=[0, 1, 767, 768, 1535]))
 
 
+def test_c5_bench_config_sampled(api):
+    """C5 exactly as bench.py times it on one GPU (16x16 pairs x {SWAP, RECOMPUTE} x 16 rates, one
+    seed: 8,192 points of 10k requests), checked against the oracle on sampled points incl. the
+    grid corners."""
+    base = si.c5()
+    cfg = replace(base, workload=replace(base.workload, seeds=[0]))
+    assert cfg.num_points == 8192
+    sw = run_gpu(api, cfg)
+    s = sw.summaries()
+    assert (s["n_finished"] + s["n_rejected"] == s["n_requests"]).all() and (s["status_flags"] & 16 == 0).all()
+    check_pd_points(sw, cfg, sample_points(cfg.num_points, target=8, corners=[0, 15, 4096, 8191]))
+
+
 def test_prefill_first_parity(api):
     """NEXT-3 prefill-first iterations: C2 in full, and random micro configs."""
     cfg = replace(si.c2(), policies=[si.Policy(iteration_mode=si.PREFILL_FIRST)])
