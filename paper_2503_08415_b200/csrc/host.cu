@@ -601,7 +601,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   Layout L0 = make_layout(h, n_run, sms, 0);
   int occ = 0;
   e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general,
-                                (u64)L0.blocks * L0.wpb > (u64)sms),
+                                L0.wpb > 1 || (u64)L0.blocks > (u64)sms),
                     (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");

@@ -1,5 +1,7 @@
-// sim_base.cu -- the lean simulation kernel variant: unified topology, MIXED
-// iterations, generated or traced single-round workloads (see sim_core.cuh).
+// sim_base.cu -- the lean simulation kernel variant for sweeps with at most one point per SM:
+// unified topology, MIXED iterations, generated or traced single-round workloads, and a helper
+// warp per CTA (see sim_core.cuh).
+#define TS_HELPER_WARP 1  // one simulating warp per SM, plus a helper warp for digests and traces
 #include "sim_core.cuh"
 
 namespace ts {

@@ -515,7 +515,7 @@ __device__ __forceinline__ void it_reserve(Logs &L, u32 cnt) {
 }
 __device__ __forceinline__ void it_put(Logs &L, u32 idx, u64 k, i64 ts, i64 T, u64 Np, u64 Cd, u64 blocks, u64 Sp,
                                        u64 D, u64 m, u64 nres, u64 nadm, u64 nfin, u64 nrej) {
-  ulonglong2 *e = L.it + 4 * (size_t)(L.nit + idx);
+  ulonglong2 *e = L.it + 4 * (size_t)((L.nit + idx) & (ITCAP - 1));  // a ring in helper mode
   e[0] = make_ulonglong2(k, (unsigned long long)ts);
   e[1] = make_ulonglong2((unsigned long long)T, Np);
   e[2] = make_ulonglong2(Cd, blocks);
@@ -647,8 +647,30 @@ __device__ __forceinline__ void mr_cache_store(MrState &M, u32 c, u32 tokens, co
 
 // ------------------------------------------------------------------ a.2-a.7 one point
 // Everything is executed by all 32 lanes; scalar state is lane-uniform in registers.
+// ------------------------------------------------------------------ helper warp (TS_HELPER_WARP)
+// In the one-warp-per-SM lean kernel (sim_base.cu) a second warp of the CTA consumes the
+// iteration log: schedule digest, iteration records, memory trace, block-ns sum and peak are
+// all functions of the logged (k, t, T, N_p, C_d, blocks, ...) entries, so they leave the
+// simulating warp's serial chain.  The log is a 256-entry ring in global memory; the two warps
+// hand over through counters in shared memory.  Every wait is bounded (~10 s of clock) and
+// raises TOKENSIM_PT_INTERNAL_ERROR instead of hanging.
+#ifndef TS_HELPER_WARP
+#define TS_HELPER_WARP 0
+#endif
+struct HelperChan {
+  u32 state;  // 0 idle, 1 point running, 2 simulation done, 3 helper done, 4 exit
+  u32 prod, cons, tflags;
+  u64 j;
+  i64 t_final;
+  u64 dig, bns, peak, tn;
+};
+constexpr long long HELPER_TIMEOUT = 20000000000ll;  // cycles
+__device__ __forceinline__ u32 chan_load(const volatile u32 *p) { return __shfl_sync(FULLMASK, *p, 0); }
+
 template <int CAP, bool FULL, bool P2>
-__device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S, u32 *bt) {
+__device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S, u32 *bt,
+                                 volatile HelperChan *ch = nullptr) {
+  constexpr bool HELP = TS_HELPER_WARP && !FULL;
   static_assert(CAP % 32 == 0 && CAP <= 1024, "CAP");
   const u32 lane = lane_id();
   const u32 ltm = lanemask_lt();
@@ -708,7 +730,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   bool hx = false;
   u32 xdone = 0, xtgt = 0;
   u64 ff_mem_wait = 0, ff_mem_k = 0;  // after a memory-cut failure: skip attempts while nfree <= wait, k < k
-  const u32 gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const u32 gwarp = HELP ? blockIdx.x : blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   Logs L;
   L.ev = P.evlog + (size_t)gwarp * EVCAP;
   L.it = P.itlog + (size_t)gwarp * ITCAP * 4;
@@ -719,6 +741,28 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   L.dig_b = 0;
   L.nev = 0;
   L.nit = 0;
+  u32 flags = 0;
+  // iteration-log hand-over: reserve cnt entries / publish the entries written
+  auto it_begin = [&](u32 cnt) {
+    if constexpr (HELP) {
+      const long long c0 = clock64();
+      while (L.nit + cnt - chan_load(&ch->cons) > ITCAP) {
+        if (clock64() - c0 > HELPER_TIMEOUT) {
+          flags |= TOKENSIM_PT_INTERNAL_ERROR;
+          break;
+        }
+      }
+    } else {
+      it_reserve(L, cnt);
+    }
+  };
+  auto it_commit = [&]() {
+    if constexpr (HELP) {
+      __threadfence_block();
+      __syncwarp();
+      if (lane_id() == 0) ch->prod = L.nit;
+    }
+  };
   MrState mr;
   if (MRM) {
     unsigned char *mb = P.mr_scratch + (size_t)gwarp * P.mr_bytes_per_warp;
@@ -771,7 +815,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
 #define PH(i) do {} while (0)
 #endif
   i64 last_fin = 0;
-  u32 flags = 0;
   u32 hd_idx = 0xffffffffu, hd_p = 0;  // cached prompt length of the fresh-queue head
   // memory trace state (lane-uniform)
   const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
@@ -1164,13 +1207,15 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           PH(3);
           // iteration records, digests, counters (lanes j < J)
           const u64 blkj = blk0 + Aj;
-          it_reserve(L, 32);
+          it_begin(32);
           if (lj) it_put(L, lane, k + lane, tsj, Tj, 0, Cdj, blkj, 0, nR, 0, 0, 0, lane == J - 1 ? nfin : 0u, 0);
           L.nit += J;
-          const u64 bns_add = warp_sum64(lj ? blkj * (u64)Tj : 0ull);
+          it_commit();
+          const u64 bns_add = HELP ? 0ull : warp_sum64(lj ? blkj * (u64)Tj : 0ull);
           PH(4);
           // memory trace
-          if (BINNED) {
+          if (HELP) {
+          } else if (BINNED) {
             while (true) {
               const i64 bstart = bin_end - W;
               i64 ov = 0;
@@ -1202,9 +1247,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             if (tn + J > P.trace_cap) flags |= TOKENSIM_PT_TRACE_OVERFLOW;
             tn += J;
           }
-          const u64 blk_last = blk0 + Ktot;
-          peak = blk_last > peak ? blk_last : peak;
-          bns += bns_add;
+          if (!HELP) {
+            const u64 blk_last = blk0 + Ktot;
+            peak = blk_last > peak ? blk_last : peak;
+            bns += bns_add;
+          }
           req_iters += (u64)nR * J;
           PH(5);
           if (nfin) {
@@ -1755,14 +1802,18 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     if (nR == 0) rmin = 0;
     NPH(7);
     // schedule digest fields (logged; folded lane-parallel when the log fills)
-    it_reserve(L, 1);
+    it_begin(1);
     if (lane == 0) it_put(L, 0, k, ts, T, Np, Cd, blocks, Sp, D, m, nres, nadm, nfin, nrej);
     L.nit += 1;
-    peak = blocks > peak ? blocks : peak;
-    bns += blocks * (u64)T;
+    it_commit();
+    if (!HELP) {
+      peak = blocks > peak ? blocks : peak;
+      bns += blocks * (u64)T;
+    }
     swo_tot += swap_out;
     swi_tot += swap_in;
-    if (BINNED) {
+    if (HELP) {
+    } else if (BINNED) {
       while (bin_end <= ts) flush_bin();
       ++acc_nit;
       i64 s = ts;
@@ -1799,9 +1850,33 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     cyc_normal += (u64)(prof_clock() - clk_a);
   }
   ev_flush(L);
-  it_flush(L);
-  if (BINNED) {
-    while ((i64)bin * W < t) flush_bin();
+  u64 dig_s = 0;
+  if constexpr (HELP) {  // hand the end time over, wait for the helper's results
+    if (lane_id() == 0) ch->t_final = t;
+    __threadfence_block();
+    __syncwarp();
+    if (lane_id() == 0) ch->state = 2u;
+    const long long c0 = clock64();
+    while (chan_load(&ch->state) != 3u) {
+      if (clock64() - c0 > HELPER_TIMEOUT) {
+        flags |= TOKENSIM_PT_INTERNAL_ERROR;
+        break;
+      }
+    }
+    __threadfence_block();
+    dig_s = ch->dig;
+    bns = ch->bns;
+    peak = ch->peak;
+    tn = ch->tn;
+    flags |= ch->tflags;
+    __syncwarp();
+    if (lane_id() == 0) ch->state = 0u;
+  } else {
+    it_flush(L);
+    if (BINNED) {
+      while ((i64)bin * W < t) flush_bin();
+    }
+    dig_s = warp_sum64(L.dig_s);
   }
   // unfinished requests still in R u Q: first-token latency and preemption count
   #pragma unroll 1
@@ -1809,7 +1884,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     const u32 id = S.id[x];
     write_record(rec + id, S.ttft[x], 0, 0, S.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);
   }
-  const u64 dig_s = warp_sum64(L.dig_s);
   const u64 dig_b = warp_sum64(L.dig_b);
   if (lane == 0) {
     SimStats st;
@@ -1851,6 +1925,169 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   __syncwarp();
 }
 
+// The helper warp of the one-warp-per-SM lean kernel: for each point the simulating warp runs,
+// consume its iteration-log ring 32 entries at a time (lane = entry) and produce what the
+// simulating warp would otherwise compute on its chain (see HelperChan).
+static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch, u32 gwarp) {
+  const u32 lane = lane_id();
+  const ulonglong2 *ring = P.itlog + (size_t)gwarp * ITCAP * 4;
+  const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
+  const bool FULLT = P.trace_mode == TOKENSIM_TRACE_FULL;
+  const i64 W = (i64)P.bin_ns;
+  while (true) {
+    u32 st;
+    long long c0 = clock64();
+    // 1: a point is running; 2: a short point already finished before we looked; 4: exit
+    while ((st = chan_load(&ch->state)) != 1u && st != 2u && st != 4u) {
+      if (clock64() - c0 > HELPER_TIMEOUT) return;
+    }
+    if (st == 4u) return;
+    __threadfence_block();
+    const u64 j = ch->j;
+    tokensim_mem_sample *trc = P.trace + (size_t)j * P.trace_nw * P.trace_cap;
+    tokensim_iter_record *itr = P.itrec + (size_t)j * P.it_cap;
+    u64 dg = 0, bns = 0, peak = 0, tn = 0, bin = 0, acc_bns = 0;
+    u32 tflags = 0, acc_max = 0, acc_nit = 0, cons = 0;
+    i64 bin_end = W;
+    auto flush_bin = [&]() {
+      if (tn < P.trace_cap) {
+        if (lane == 0) {
+          tokensim_mem_sample sm;
+          sm.t_ns = (i64)bin * W;
+          sm.dur_ns = W;
+          sm.block_ns = acc_bns;
+          sm.blocks_max = acc_max;
+          sm.n_iter = acc_nit;
+          trc[tn] = sm;
+        }
+      } else {
+        tflags |= TOKENSIM_PT_TRACE_OVERFLOW;
+      }
+      ++tn;
+      ++bin;
+      bin_end += W;
+      acc_bns = 0;
+      acc_max = 0;
+      acc_nit = 0;
+    };
+    c0 = clock64();
+    while (true) {
+      const u32 s2 = chan_load(&ch->state);  // the state before the producer count
+      __threadfence_block();
+      const u32 prod = chan_load(&ch->prod);
+      __threadfence_block();
+      if (prod != cons) {
+        #pragma unroll 1
+        for (u32 e0 = cons; e0 != prod;) {
+          const u32 m = min(32u, prod - e0);
+          const bool v = lane < m;
+          const u32 e = e0 + lane;
+          u64 k = 0, Np = 0, Cd = 0, blocks = 0, w6 = 0, w7 = 0;
+          i64 ts = 0, T = 0;
+          if (v) {
+            const ulonglong2 *q = ring + 4 * (size_t)(e & (ITCAP - 1));
+            const ulonglong2 a = q[0], b = q[1], c = q[2], d = q[3];
+            k = a.x;
+            ts = (i64)a.y;
+            T = (i64)b.x;
+            Np = b.y;
+            Cd = c.x;
+            blocks = c.y;
+            w6 = d.x;
+            w7 = d.y;
+            dg += sched_fold(k, ts, T, Np, Cd, blocks, w6, w7);
+            if (e < P.it_cap) {
+              tokensim_iter_record ir;
+              ir.k = k & ((1ull << 40) - 1);
+              ir.t_start_ns = ts;
+              ir.T_ns = T;
+              ir.n_prefill = (u32)(w6 & 0xffff);
+              ir.n_decode = (u32)((w6 >> 16) & 0xffff);
+              ir.N_p = Np;
+              ir.C_d = Cd;
+              ir.n_preempted = (u32)((w6 >> 32) & 0xffff);
+              ir.n_resumed = (u32)(w6 >> 48);
+              ir.n_admitted = (u32)(w7 & 0xffff);
+              ir.n_rejected = (u32)(w7 >> 32);
+              ir.n_finished = (u32)((w7 >> 16) & 0xffff);
+              ir.blocks_in_use = (u32)blocks;
+              ir.worker = (u32)(k >> 40);
+              ir.pad = 0;
+              itr[e] = ir;
+            }
+            bns += blocks * (u64)T;
+            peak = blocks > peak ? blocks : peak;
+          }
+          const i64 te = ts + T;
+          if (BINNED) {  // the stretch's lane-parallel bin walk (reading R5)
+            const i64 tend = __shfl_sync(FULLMASK, te, m - 1), tsl = __shfl_sync(FULLMASK, ts, m - 1);
+            while (true) {
+              const i64 bstart = bin_end - W;
+              i64 ov = 0;
+              bool cnt_here = false;
+              if (v) {
+                const i64 lo = ts > bstart ? ts : bstart;
+                const i64 hi = te < bin_end ? te : bin_end;
+                ov = hi - lo;
+                cnt_here = ts >= bstart && ts < bin_end;
+              }
+              acc_bns += warp_sum64(ov > 0 ? blocks * (u64)ov : 0ull);
+              acc_max = max(acc_max, __reduce_max_sync(FULLMASK, ov > 0 ? (u32)blocks : 0u));
+              acc_nit += __popc(__ballot_sync(FULLMASK, cnt_here));
+              if (tend > bin_end || tsl >= bin_end) flush_bin();
+              else break;
+            }
+          } else if (FULLT) {
+            if (v && tn + lane < P.trace_cap) {
+              tokensim_mem_sample sm;
+              sm.t_ns = ts;
+              sm.dur_ns = T;
+              sm.block_ns = blocks * (u64)T;
+              sm.blocks_max = (u32)blocks;
+              sm.n_iter = 1;
+              trc[tn + lane] = sm;
+            }
+            if (tn + m > P.trace_cap) tflags |= TOKENSIM_PT_TRACE_OVERFLOW;
+            tn += m;
+          }
+          e0 += m;
+        }
+        cons = prod;
+        __syncwarp();
+        if (lane == 0) ch->cons = cons;
+        c0 = clock64();
+      } else if (s2 == 2u) {
+        break;
+      } else if (clock64() - c0 > HELPER_TIMEOUT) {
+        tflags |= TOKENSIM_PT_INTERNAL_ERROR;
+        break;
+      }
+    }
+    __threadfence_block();
+    if (BINNED) {
+      const i64 tf = ch->t_final;
+      while ((i64)bin * W < tf) flush_bin();
+    }
+    const u64 dig = warp_sum64(dg), bsum = warp_sum64(bns);
+    u64 pk = peak;
+#pragma unroll
+    for (u32 o = 16; o; o >>= 1) {
+      const u64 y = __shfl_xor_sync(FULLMASK, pk, o);
+      pk = y > pk ? y : pk;
+    }
+    if (lane == 0) {
+      ch->dig = dig;
+      ch->bns = bsum;
+      ch->peak = pk;
+      ch->tn = tn;
+      ch->tflags = tflags;
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) ch->state = 3u;
+  }
+}
+
 // V: 0 = lean unified (MIXED), 1 = full unified, 2 = 1P:1D pair, 3 = xP:yD node, 4 = the lean
 // one with compact helpers (sim_base_c.cu; sweeps that run several warps per SM).  One kernel
 // per variant: its registers and instruction footprint are those of the code it can run.
@@ -1858,13 +2095,24 @@ template <int CAP, int V, bool P2>
 __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
+  constexpr bool HELPK = V == 0 && TS_HELPER_WARP;  // one simulating warp + its helper per CTA
   constexpr bool pd = V == 2 || V == 3;
   constexpr bool node = V == 3;
   const size_t base = smem_per_warp_bytes(CAP, P.nwords_max);
   const size_t per_warp =
       node ? pdn_smem_per_warp(CAP, P.nwords_max, P.pd_x, P.pd_y) : base + (pd ? smem_pd_extra(CAP, P.nwords_max) : 0);
-  const WarpSmem S = carve(smem_raw + wib * per_warp, CAP);
-  const u32 gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
+  volatile HelperChan *ch = nullptr;
+  if constexpr (HELPK) {
+    ch = reinterpret_cast<volatile HelperChan *>(smem_raw + ((per_warp + 15) & ~(size_t)15));
+    if (threadIdx.x == 0) ch->state = 0u;  // shared memory starts as garbage: set before either warp looks
+    __syncthreads();
+    if (wib == 1) {
+      helper_loop(P, ch, blockIdx.x);
+      return;
+    }
+  }
+  const WarpSmem S = carve(smem_raw + (HELPK ? 0 : wib) * per_warp, CAP);
+  const u32 gwarp = HELPK ? blockIdx.x : blockIdx.x * (blockDim.x >> 5) + wib;
   u32 *bt = P.bt + (size_t)gwarp * P.bt_tables * CAP * P.bt_len;
   while (true) {
     u32 qi = 0;
@@ -1872,26 +2120,52 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
     qi = __shfl_sync(FULLMASK, qi, 0);
     if ((u64)qi >= P.n_run) break;
     const u64 j = P.order[qi];
+    if constexpr (HELPK) {  // hand the point to the helper
+      if (lane == 0) {
+        ch->prod = 0u;
+        ch->cons = 0u;
+        ch->j = j;
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) ch->state = 1u;
+    }
     if constexpr (V == 3) simulate_pdn<CAP, P2>(P, j, smem_raw + wib * per_warp, bt);
     else if constexpr (V == 2) simulate_pd<CAP, P2>(P, j, S, smem_raw + wib * per_warp + base, bt);
-    else simulate_unified<CAP, V == 1, P2>(P, j, S, bt);  // V 4: the lean one built with TS_COMPACT
+    else simulate_unified<CAP, V == 1, P2>(P, j, S, bt, ch);  // V 4: the lean one built with TS_COMPACT
+  }
+  if constexpr (HELPK) {
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) ch->state = 4u;
   }
 }
 
 // launch / occupancy helpers for one variant (instantiated by sim_base.cu, sim_full.cu,
 // sim_pair.cu, sim_node.cu)
+// V 0 with the helper warp: one simulating warp (wpb = 1) + the helper, and the hand-over
+// counters after the warp's shared memory
+template <int V>
+static __host__ __forceinline__ int sim_threads(int wpb) { return (V == 0 && TS_HELPER_WARP) ? 64 : wpb * 32; }
+template <int V>
+static __host__ __forceinline__ size_t sim_smem(size_t smem) {
+  return (V == 0 && TS_HELPER_WARP) ? ((smem + 15) & ~(size_t)15) + sizeof(HelperChan) : smem;
+}
 template <int CAP, int V, bool P2>
 static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_t smem, cudaStream_t st) {
+  if (V == 0 && TS_HELPER_WARP && wpb != 1) return cudaErrorInvalidValue;
+  smem = sim_smem<V>(smem);
   cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, V, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  sim_kernel<CAP, V, P2><<<blocks, wpb * 32, smem, st>>>(p);
+  sim_kernel<CAP, V, P2><<<blocks, sim_threads<V>(wpb), smem, st>>>(p);
   return cudaGetLastError();
 }
 template <int CAP, int V, bool P2>
 static cudaError_t occ_t(int wpb, size_t smem, int *b) {
+  smem = sim_smem<V>(smem);
   cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, V, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP, V, P2>, wpb * 32, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP, V, P2>, sim_threads<V>(wpb), smem);
 }
 template <int V, bool P2>
 static cudaError_t launch_sim_c(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {

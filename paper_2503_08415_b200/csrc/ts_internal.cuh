@@ -168,14 +168,15 @@ cudaError_t launch_sim_node(const SweepParams &p, int cap, int warps_per_block, 
                             cudaStream_t st);
 cudaError_t launch_sim_base_c(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                               cudaStream_t st);
-// several warps per SM: the lean kernel with compact helpers (variant 4)
+// several warps per SM: the lean kernel with compact helpers (variant 4); one warp per SM:
+// variant 0, whose CTA adds a helper warp (sim_base.cu)
 inline int sim_variant(bool full, bool pd, bool pd_general, bool multi_warp = false) {
   return !full ? (multi_warp ? 4 : 0) : !pd ? 1 : pd_general ? 3 : 2;
 }
 inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                               cudaStream_t st) {
   switch (sim_variant(p.full != 0, p.topology == TOKENSIM_PD_PAIR, p.pd_general != 0,
-                      (u64)blocks * (u64)warps_per_block > (u64)p.n_sms)) {
+                      warps_per_block > 1 || (u64)blocks > (u64)p.n_sms)) {
     case 0: return launch_sim_base(p, cap, warps_per_block, blocks, smem, st);
     case 4: return launch_sim_base_c(p, cap, warps_per_block, blocks, smem, st);
     case 1: return launch_sim_full(p, cap, warps_per_block, blocks, smem, st);
