@@ -659,11 +659,16 @@ __device__ __forceinline__ void mr_cache_store(MrState &M, u32 c, u32 tokens, co
 #endif
 struct HelperChan {
   u32 state;  // 0 idle, 1 point running, 2 simulation done, 3 helper done, 4 exit
-  u32 prod, cons, tflags;
+  u32 prod, cons, tflags;   // iteration-log ring
+  u32 eprod, econs, pad0, pad1;  // block-event ring (allocations / frees to replay)
   u64 j;
   i64 t_final;
-  u64 dig, bns, peak, tn;
+  u64 dig, bns, peak, tn, digb;
 };
+// Block-event records of the helper mode (uint4): k, kind | count << 2, request id,
+// table slot | table position << 10.  kind 1: take `count` lowest free blocks into the slot's
+// table from the position; kind 2: return the slot's first `count` blocks.
+constexpr u32 HEV_ALLOC = 1, HEV_FREE = 2;
 constexpr long long HELPER_TIMEOUT = 20000000000ll;  // cycles
 __device__ __forceinline__ u32 chan_load(const volatile u32 *p) { return __shfl_sync(FULLMASK, *p, 0); }
 
@@ -762,6 +767,32 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       __syncwarp();
       if (lane_id() == 0) ch->prod = L.nit;
     }
+  };
+  // helper mode: block ids are output-only (every decision uses counts), so allocations and
+  // frees are logged as events and replayed on the bitmap by the helper warp
+  auto ev_begin = [&](u32 cnt) {
+    const long long c0 = clock64();
+    while (L.nev + cnt - chan_load(&ch->econs) > EVCAP) {
+      if (clock64() - c0 > HELPER_TIMEOUT) {
+        flags |= TOKENSIM_PT_INTERNAL_ERROR;
+        break;
+      }
+    }
+  };
+  auto ev_commit = [&]() {
+    __threadfence_block();
+    __syncwarp();
+    if (lane_id() == 0) ch->eprod = L.nev;
+  };
+  auto ev_log = [&](u32 idx, u64 kk, u32 kind, u32 count, u32 id, u32 slot, u32 tpos) {
+    L.ev[(L.nev + idx) & (EVCAP - 1)] = make_uint4((u32)kk, kind | (count << 2), id, slot | (tpos << 10));
+  };
+  // free (kind 2) of a request's `held` blocks: one event from lane 0
+  auto ev_free = [&](u32 held, u32 id, u32 slot, u64 kk) {
+    ev_begin(1);
+    if (lane_id() == 0) ev_log(0, kk, HEV_FREE, held, id, slot, 0);
+    L.nev += 1;
+    ev_commit();
   };
   MrState mr;
   if (MRM) {
@@ -1060,7 +1091,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
           PH(1);
           bool done_alloc = Ktot == 0;
-          if (!done_alloc && nR <= 32 && Ktot <= 32 && hint < nwords) {
+          if (!HELP && !done_alloc && nR <= 32 && Ktot <= 32 && hint < nwords) {
             // fused small case: lane o takes the o-th lowest free block of the 32-word window at
             // the hint and serves order index o = (iteration jb, r-th slot of jb's residue class)
             const u32 wi = hint + lane;
@@ -1112,11 +1143,15 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             // request of a slot at iteration offset jx has order index (blocks of iterations
             // before jx) + (its rank in its residue class)
             u32 *fl = S.req_cum;  // free in a stretch; Ktot <= CAP (cut condition)
-            if (!take_lowest(S.bitmap, Ktot, fl, hint, nwords)) {
-              flags |= TOKENSIM_PT_INTERNAL_ERROR;
-              break;
+            if (HELP) {
+              ev_begin(Ktot);
+            } else {
+              if (!take_lowest(S.bitmap, Ktot, fl, hint, nwords)) {
+                flags |= TOKENSIM_PT_INTERNAL_ERROR;
+                break;
+              }
+              ev_reserve(L, Ktot);
             }
-            ev_reserve(L, Ktot);
             const u32 excl = Aj - nj;
             const u32 nrep = (32 + B.bs - 1) / B.bs;
             #pragma unroll 1
@@ -1132,13 +1167,18 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
                 const u32 ex = __shfl_sync(FULLMASK, excl, jx & 31u);
                 if (in && jx < J) {
                   const u32 o = ex + rank;
-                  const u32 blk = fl[o];
-                  bt[(size_t)SLOT(S.info[jj]) * btl + B.div(c + jx)] = blk;
-                  ev_put(L, o, k + jx, 1, S.id[jj], blk);
+                  if (HELP) {
+                    ev_log(o, k + jx, HEV_ALLOC, 1, S.id[jj], SLOT(S.info[jj]), B.div(c + jx));
+                  } else {
+                    const u32 blk = fl[o];
+                    bt[(size_t)SLOT(S.info[jj]) * btl + B.div(c + jx)] = blk;
+                    ev_put(L, o, k + jx, 1, S.id[jj], blk);
+                  }
                 }
               }
             }
             L.nev += Ktot;
+            if (HELP) ev_commit();
             __syncwarp();
           }
           const u64 blk0 = total - nfree;
@@ -1187,7 +1227,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               const u32 pos = b0 + l;
               const u32 held = B.cdiv(S.ctx[pos]);
               const u32 slot = SLOT(S.info[pos]);
-              free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, 0, L, hint);
+              if (HELP) ev_free(held, S.id[pos], slot, klast);
+              else free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, 0, L, hint);
               nfree += held;
               if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
               if (MRM) {  // NEXT-2: store the context; schedule the conversation's next round
@@ -1506,7 +1547,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 slot = SLOT(S.info[v]);
         // a partial prefill loses its KV whatever the mode: re-prefill from scratch (R-N3b)
         const bool vx = hx && v == nR - 1;
-        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, 0, L, hint);
+        if (HELP) ev_free(held, S.id[v], slot, k);
+        else free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, 0, L, hint);
         nfree += held;
         if (!vx) csub += c + 1;
         if (SWAPM && !vx) swap_out += (u64)held * HP.block_bytes;
@@ -1623,7 +1665,24 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     // 6. empty batch (every candidate rejected): back to 0 without advancing t
     if (nR == 0) continue;
     // block extraction for all requesters of this iteration, in phase order
-    if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, 0, L, hint, nwords, Edec)) {
+    if (HELP) {
+      if (Kb > 0) {  // one event per requester entry, in phase order
+        #pragma unroll 1
+        for (u32 e0 = 0; e0 < E; e0 += 32) {
+          const u32 cnt = min(32u, E - e0);
+          ev_begin(cnt);
+          const u32 e = e0 + lane;
+          if (e < E) {
+            const u32 pt = S.req_pt[e];
+            const u32 pos = PT_POS(pt);
+            const u32 c1 = S.req_cum[e] - (e ? S.req_cum[e - 1] : 0u);
+            ev_log(lane, k + PT_J(pt), HEV_ALLOC, c1, S.id[pos], SLOT(S.info[pos]), PT_TPOS(pt));
+          }
+          L.nev += cnt;
+          ev_commit();
+        }
+      }
+    } else if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, 0, L, hint, nwords, Edec)) {
       flags |= TOKENSIM_PT_INTERNAL_ERROR;
       break;
     }
@@ -1723,7 +1782,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 c = S.ctx[pos];
         const u32 held = B.cdiv(c);
         const u32 slot = SLOT(S.info[pos]);
-        free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, 0, L, hint);
+        if (HELP) ev_free(held, S.id[pos], slot, k);
+        else free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, 0, L, hint);
         nfree += held;
         if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
         if (MRM) {  // NEXT-2: store the context; schedule the conversation's next round
@@ -1849,8 +1909,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     ++k;
     cyc_normal += (u64)(prof_clock() - clk_a);
   }
-  ev_flush(L);
-  u64 dig_s = 0;
+  if (!HELP) ev_flush(L);
+  u64 dig_s = 0, dig_bh = 0;
   if constexpr (HELP) {  // hand the end time over, wait for the helper's results
     if (lane_id() == 0) ch->t_final = t;
     __threadfence_block();
@@ -1865,6 +1925,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     }
     __threadfence_block();
     dig_s = ch->dig;
+    dig_bh = ch->digb;
     bns = ch->bns;
     peak = ch->peak;
     tn = ch->tn;
@@ -1884,7 +1945,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     const u32 id = S.id[x];
     write_record(rec + id, S.ttft[x], 0, 0, S.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);
   }
-  const u64 dig_b = warp_sum64(L.dig_b);
+  const u64 dig_b = HELP ? dig_bh : warp_sum64(L.dig_b);
   if (lane == 0) {
     SimStats st;
     st.flags = flags | ((nrej_tot == n) ? (u32)TOKENSIM_PT_ALL_REJECTED : 0u);
@@ -1928,9 +1989,13 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
 // The helper warp of the one-warp-per-SM lean kernel: for each point the simulating warp runs,
 // consume its iteration-log ring 32 entries at a time (lane = entry) and produce what the
 // simulating warp would otherwise compute on its chain (see HelperChan).
-static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch, u32 gwarp) {
+template <int CAP, bool P2>
+static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch, u32 gwarp, u32 *hbm, u32 *fl) {
   const u32 lane = lane_id();
   const ulonglong2 *ring = P.itlog + (size_t)gwarp * ITCAP * 4;
+  const uint4 *evr = P.evlog + (size_t)gwarp * EVCAP;
+  u32 *bt = P.bt + (size_t)gwarp * P.bt_tables * CAP * P.bt_len;
+  const u32 btl = P.bt_len;
   const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
   const bool FULLT = P.trace_mode == TOKENSIM_TRACE_FULL;
   const i64 W = (i64)P.bin_ns;
@@ -1944,6 +2009,20 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
     if (st == 4u) return;
     __threadfence_block();
     const u64 j = ch->j;
+    // the point's free-block bitmap, replayed from the block events (lowest free first)
+    const u64 point = P.begin + j * P.stride;
+    const Coords cd = decode_point(point, P.n_pol, P.n_rates, P.n_seeds);
+    const DevHP HP = P.hp[(size_t)cd.hw * P.n_pol + cd.pol];
+    const u32 nwords = HP.nwords;
+    {
+      const u32 full_words = (u32)(HP.total_blocks >> 5), tail = (u32)(HP.total_blocks & 31);
+      #pragma unroll 1
+      for (u32 w = lane; w < nwords; w += 32)
+        hbm[w] = w < full_words ? 0xffffffffu : (w == full_words && tail ? ((1u << tail) - 1u) : 0u);
+      __syncwarp();
+    }
+    u32 hint = 0, econs = 0;
+    u64 dgb = 0;
     tokensim_mem_sample *trc = P.trace + (size_t)j * P.trace_nw * P.trace_cap;
     tokensim_iter_record *itr = P.itrec + (size_t)j * P.it_cap;
     u64 dg = 0, bns = 0, peak = 0, tn = 0, bin = 0, acc_bns = 0;
@@ -1972,10 +2051,87 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
     };
     c0 = clock64();
     while (true) {
-      const u32 s2 = chan_load(&ch->state);  // the state before the producer count
+      const u32 s2 = chan_load(&ch->state);  // the state before the producer counts
       __threadfence_block();
       const u32 prod = chan_load(&ch->prod);
+      const u32 eprod = chan_load(&ch->eprod);
       __threadfence_block();
+      bool ev_err = false;
+      #pragma unroll 1
+      while (econs != eprod) {  // block events, in order
+        const u32 m = min(32u, eprod - econs);
+        const bool v = lane < m;
+        uint4 ev = make_uint4(0, 0, 0, 0);
+        if (v) ev = evr[(econs + lane) & (EVCAP - 1)];
+        const u32 kind = ev.y & 3u, cnt = ev.y >> 2;
+        const u32 fm = __ballot_sync(FULLMASK, v && kind == HEV_FREE);
+        if (fm & 1u) {  // a free: return the slot's first cnt blocks
+          const u32 kk = __shfl_sync(FULLMASK, ev.x, 0), held = __shfl_sync(FULLMASK, cnt, 0);
+          const u32 id = __shfl_sync(FULLMASK, ev.z, 0), slot = __shfl_sync(FULLMASK, ev.w, 0) & 1023u;
+          u32 mn = 0xffffffffu;
+          #pragma unroll 1
+          for (u32 x = lane; x < held; x += 32) {
+            const u32 b = bt[(size_t)slot * btl + x];
+            atomicOr(&hbm[b >> 5], 1u << (b & 31u));
+            dgb += fold_event(kk, 2, id, b);
+            mn = min(mn, b >> 5);
+          }
+          mn = __reduce_min_sync(FULLMASK, mn);
+          hint = min(hint, mn);
+          __syncwarp();
+          econs += 1;
+          continue;
+        }
+        const u32 na = fm ? (u32)(__ffs(fm) - 1) : m;  // leading allocations
+        const u32 c = lane < na ? cnt : 0u;
+        const u32 cum = scan_incl(c);
+        const u32 K = __shfl_sync(FULLMASK, cum, na - 1);
+        if (K <= 256) {  // all of them from one extraction, lane per block
+          if (K && !take_lowest(hbm, K, fl, hint, nwords)) ev_err = true;
+          #pragma unroll 1
+          for (u32 o0 = 0; o0 < K; o0 += 32) {
+            const u32 o = o0 + lane;
+            const u32 tgt = o < K ? o : 0u;
+            u32 a = 0;
+#pragma unroll
+            for (u32 st = 16; st; st >>= 1) {
+              const u32 vv = __shfl_sync(FULLMASK, cum, a + st - 1);
+              if (vv <= tgt) a += st;
+            }
+            const u32 ex = __shfl_sync(FULLMASK, cum - c, a);
+            const u32 kk = __shfl_sync(FULLMASK, ev.x, a), id = __shfl_sync(FULLMASK, ev.z, a);
+            const u32 sw = __shfl_sync(FULLMASK, ev.w, a);
+            if (o < K) {
+              const u32 blk = fl[o];
+              bt[(size_t)(sw & 1023u) * btl + (sw >> 10) + (o - ex)] = blk;
+              dgb += fold_event(kk, 1, id, blk);
+            }
+          }
+          __syncwarp();
+        } else {  // a large request: event by event, 256 blocks at a time
+          #pragma unroll 1
+          for (u32 i = 0; i < na; ++i) {
+            const u32 kk = __shfl_sync(FULLMASK, ev.x, i), id = __shfl_sync(FULLMASK, ev.z, i);
+            const u32 sw = __shfl_sync(FULLMASK, ev.w, i), ci = __shfl_sync(FULLMASK, cnt, i);
+            #pragma unroll 1
+            for (u32 s0 = 0; s0 < ci; s0 += 256) {
+              const u32 kc = min(256u, ci - s0);
+              if (!take_lowest(hbm, kc, fl, hint, nwords)) ev_err = true;
+              #pragma unroll 1
+              for (u32 x = lane; x < kc; x += 32) {
+                const u32 blk = fl[x];
+                bt[(size_t)(sw & 1023u) * btl + (sw >> 10) + s0 + x] = blk;
+                dgb += fold_event(kk, 1, id, blk);
+              }
+              __syncwarp();
+            }
+          }
+        }
+        econs += na;
+      }
+      if (ev_err) tflags |= TOKENSIM_PT_INTERNAL_ERROR;
+      __syncwarp();
+      if (lane == 0) ch->econs = econs;
       if (prod != cons) {
         #pragma unroll 1
         for (u32 e0 = cons; e0 != prod;) {
@@ -2056,7 +2212,7 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
         __syncwarp();
         if (lane == 0) ch->cons = cons;
         c0 = clock64();
-      } else if (s2 == 2u) {
+      } else if (s2 == 2u && econs == eprod) {
         break;
       } else if (clock64() - c0 > HELPER_TIMEOUT) {
         tflags |= TOKENSIM_PT_INTERNAL_ERROR;
@@ -2075,8 +2231,10 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
       const u64 y = __shfl_xor_sync(FULLMASK, pk, o);
       pk = y > pk ? y : pk;
     }
+    const u64 digb = warp_sum64(dgb);
     if (lane == 0) {
       ch->dig = dig;
+      ch->digb = digb;
       ch->bns = bsum;
       ch->peak = pk;
       ch->tn = tn;
@@ -2103,11 +2261,17 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
       node ? pdn_smem_per_warp(CAP, P.nwords_max, P.pd_x, P.pd_y) : base + (pd ? smem_pd_extra(CAP, P.nwords_max) : 0);
   volatile HelperChan *ch = nullptr;
   if constexpr (HELPK) {
-    ch = reinterpret_cast<volatile HelperChan *>(smem_raw + ((per_warp + 15) & ~(size_t)15));
-    if (threadIdx.x == 0) ch->state = 0u;  // shared memory starts as garbage: set before either warp looks
+    unsigned char *hb = smem_raw + ((per_warp + 15) & ~(size_t)15);
+    ch = reinterpret_cast<volatile HelperChan *>(hb);
+    if (threadIdx.x == 0) {  // shared memory starts as garbage: set before either warp looks
+      ch->state = 0u;
+      ch->eprod = 0u;
+      ch->econs = 0u;
+    }
     __syncthreads();
     if (wib == 1) {
-      helper_loop(P, ch, blockIdx.x);
+      u32 *hbm = reinterpret_cast<u32 *>(hb + sizeof(HelperChan));
+      helper_loop<CAP, P2>(P, ch, blockIdx.x, hbm, hbm + P.nwords_max);
       return;
     }
   }
@@ -2124,6 +2288,8 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
       if (lane == 0) {
         ch->prod = 0u;
         ch->cons = 0u;
+        ch->eprod = 0u;
+        ch->econs = 0u;
         ch->j = j;
       }
       __threadfence_block();
@@ -2147,14 +2313,16 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
 // counters after the warp's shared memory
 template <int V>
 static __host__ __forceinline__ int sim_threads(int wpb) { return (V == 0 && TS_HELPER_WARP) ? 64 : wpb * 32; }
+// the helper's area: hand-over counters, its replayed bitmap (nwords_max words), 256 extraction slots
 template <int V>
-static __host__ __forceinline__ size_t sim_smem(size_t smem) {
-  return (V == 0 && TS_HELPER_WARP) ? ((smem + 15) & ~(size_t)15) + sizeof(HelperChan) : smem;
+static __host__ __forceinline__ size_t sim_smem(size_t smem, u32 nwords_max) {
+  return (V == 0 && TS_HELPER_WARP) ? ((smem + 15) & ~(size_t)15) + sizeof(HelperChan) + 4 * (size_t)nwords_max + 1024
+                                    : smem;
 }
 template <int CAP, int V, bool P2>
 static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_t smem, cudaStream_t st) {
   if (V == 0 && TS_HELPER_WARP && wpb != 1) return cudaErrorInvalidValue;
-  smem = sim_smem<V>(smem);
+  smem = sim_smem<V>(smem, p.nwords_max);
   cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, V, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   sim_kernel<CAP, V, P2><<<blocks, sim_threads<V>(wpb), smem, st>>>(p);
@@ -2162,7 +2330,7 @@ static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_
 }
 template <int CAP, int V, bool P2>
 static cudaError_t occ_t(int wpb, size_t smem, int *b) {
-  smem = sim_smem<V>(smem);
+  smem = sim_smem<V>(smem, 4096);  // (variant 0 runs one CTA per SM; a generous bitmap bound)
   cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, V, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP, V, P2>, sim_threads<V>(wpb), smem);
