@@ -761,16 +761,27 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       it_reserve(L, cnt);
     }
   };
+  // one fence per iteration publishes both rings (iteration entries and block events)
   auto it_commit = [&]() {
     if constexpr (HELP) {
       __threadfence_block();
       __syncwarp();
-      if (lane_id() == 0) ch->prod = L.nit;
+      if (lane_id() == 0) {
+        ch->eprod = L.nev;
+        ch->prod = L.nit;
+      }
     }
   };
   // helper mode: block ids are output-only (every decision uses counts), so allocations and
   // frees are logged as events and replayed on the bitmap by the helper warp
-  auto ev_begin = [&](u32 cnt) {
+  auto ev_commit = [&]() {
+    __threadfence_block();
+    __syncwarp();
+    if (lane_id() == 0) ch->eprod = L.nev;
+  };
+  auto ev_begin = [&](u32 cnt) {  // room for cnt events; publish first if we must wait
+    if (L.nev + cnt - chan_load(&ch->econs) <= EVCAP) return;
+    ev_commit();
     const long long c0 = clock64();
     while (L.nev + cnt - chan_load(&ch->econs) > EVCAP) {
       if (clock64() - c0 > HELPER_TIMEOUT) {
@@ -778,11 +789,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         break;
       }
     }
-  };
-  auto ev_commit = [&]() {
-    __threadfence_block();
-    __syncwarp();
-    if (lane_id() == 0) ch->eprod = L.nev;
   };
   auto ev_log = [&](u32 idx, u64 kk, u32 kind, u32 count, u32 id, u32 slot, u32 tpos) {
     L.ev[(L.nev + idx) & (EVCAP - 1)] = make_uint4((u32)kk, kind | (count << 2), id, slot | (tpos << 10));
@@ -792,7 +798,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     ev_begin(1);
     if (lane_id() == 0) ev_log(0, kk, HEV_FREE, held, id, slot, 0);
     L.nev += 1;
-    ev_commit();
   };
   MrState mr;
   if (MRM) {
@@ -1178,7 +1183,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               }
             }
             L.nev += Ktot;
-            if (HELP) ev_commit();
             __syncwarp();
           }
           const u64 blk0 = total - nfree;
@@ -1679,7 +1683,6 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             ev_log(lane, k + PT_J(pt), HEV_ALLOC, c1, S.id[pos], SLOT(S.info[pos]), PT_TPOS(pt));
           }
           L.nev += cnt;
-          ev_commit();
         }
       }
     } else if (Kb > 0 && !alloc_ordered(S, E, Kb, bt, btl, k, 0, L, hint, nwords, Edec)) {
@@ -1912,7 +1915,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   if (!HELP) ev_flush(L);
   u64 dig_s = 0, dig_bh = 0;
   if constexpr (HELP) {  // hand the end time over, wait for the helper's results
-    if (lane_id() == 0) ch->t_final = t;
+    if (lane_id() == 0) {
+      ch->t_final = t;
+      ch->eprod = L.nev;
+      ch->prod = L.nit;
+    }
     __threadfence_block();
     __syncwarp();
     if (lane_id() == 0) ch->state = 2u;
