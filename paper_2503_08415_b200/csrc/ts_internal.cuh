@@ -1,6 +1,7 @@
 // ts_internal.cuh -- device-side data layout shared by the kernels and the host runtime.
 // Nothing here is shared with oracle/ (the oracle has its own structs and code).
 #pragma once
+#include <cstdlib>
 #include <cstddef>
 #include <cstdint>
 
@@ -175,8 +176,10 @@ inline int sim_variant(bool full, bool pd, bool pd_general, bool multi_warp = fa
 }
 inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                               cudaStream_t st) {
+  // TOKENSIM_HELPER=1 (A/B experiments): the helper-warp lean kernel even with several CTAs per SM
+  const bool force_helper = warps_per_block == 1 && getenv("TOKENSIM_HELPER") != nullptr;
   switch (sim_variant(p.full != 0, p.topology == TOKENSIM_PD_PAIR, p.pd_general != 0,
-                      warps_per_block > 1 || (u64)blocks > (u64)p.n_sms)) {
+                      !force_helper && (warps_per_block > 1 || (u64)blocks > (u64)p.n_sms))) {
     case 0: return launch_sim_base(p, cap, warps_per_block, blocks, smem, st);
     case 4: return launch_sim_base_c(p, cap, warps_per_block, blocks, smem, st);
     case 1: return launch_sim_full(p, cap, warps_per_block, blocks, smem, st);
