@@ -747,11 +747,15 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   L.nev = 0;
   L.nit = 0;
   u32 flags = 0;
+  // the helper's consumer counters as last seen: they only grow, so a stale copy is a safe
+  // (pessimistic) bound and the shared-memory load + broadcast is paid only when it says full
+  u32 cons_seen = 0, econs_seen = 0;
   // iteration-log hand-over: reserve cnt entries / publish the entries written
   auto it_begin = [&](u32 cnt) {
     if constexpr (HELP) {
+      if (L.nit + cnt - cons_seen <= ITCAP) return;
       const long long c0 = clock64();
-      while (L.nit + cnt - chan_load(&ch->cons) > ITCAP) {
+      while (L.nit + cnt - (cons_seen = chan_load(&ch->cons)) > ITCAP) {
         if (clock64() - c0 > HELPER_TIMEOUT) {
           flags |= TOKENSIM_PT_INTERNAL_ERROR;
           break;
@@ -780,10 +784,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     if (lane_id() == 0) ch->eprod = L.nev;
   };
   auto ev_begin = [&](u32 cnt) {  // room for cnt events; publish first if we must wait
-    if (L.nev + cnt - chan_load(&ch->econs) <= EVCAP) return;
+    if (L.nev + cnt - econs_seen <= EVCAP) return;
+    if (L.nev + cnt - (econs_seen = chan_load(&ch->econs)) <= EVCAP) return;
     ev_commit();
     const long long c0 = clock64();
-    while (L.nev + cnt - chan_load(&ch->econs) > EVCAP) {
+    while (L.nev + cnt - (econs_seen = chan_load(&ch->econs)) > EVCAP) {
       if (clock64() - c0 > HELPER_TIMEOUT) {
         flags |= TOKENSIM_PT_INTERNAL_ERROR;
         break;
