@@ -1198,12 +1198,10 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
           const i64 tsl = __shfl_sync(FULLMASK, tsj, J - 1);
           const bool lj = lane < J;
-          i64 tmax = lj ? Tj : 0;
-#pragma unroll
-          for (u32 o = 16; o; o >>= 1) {
-            const i64 y = __shfl_xor_sync(FULLMASK, tmax, o);
-            tmax = y > tmax ? y : tmax;
-          }
+          // the largest gap of the stretch is its last iteration's: T_j is nondecreasing in j
+          // (only C_d grows, and every rounded product, sum, fmax and floor in the cost model is
+          // monotone in it with nonnegative coefficients), so max_{j<J} T_j = T_{J-1}
+          const i64 tmax = tend - tsl;
           u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
           #pragma unroll 1
           for (u32 b0 = 0; b0 < nR; b0 += 32) {
