@@ -1420,9 +1420,12 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const u32 need = B.cdiv(p);
           const bool rej = valid && (u64)need > HP.cap_fresh;
           const bool el = valid && !rej;
-          const u32 ce = scan_incl(el ? 1u : 0u);
-          const u32 cneed = scan_incl(el ? need : 0u);
-          const u32 cp = scan_incl(el ? p : 0u);
+          // one candidate (the common case at low load): lane 0's prefix sums are its own values,
+          // and every other lane's are masked by !el below, so the three scans are skipped
+          const bool one = arr - adm == 1u;
+          const u32 ce = one ? (el ? 1u : 0u) : scan_incl(el ? 1u : 0u);
+          const u32 cneed = one ? (el ? need : 0u) : scan_incl(el ? need : 0u);
+          const u32 cp = one ? (el ? p : 0u) : scan_incl(el ? p : 0u);
           // CHUNKED: a request is admitted while one token of budget is left (reading R-N3b)
           const bool tok_ok = CHK ? tokens + cp - p < (u64)mbt : tokens + cp <= (u64)mbt;
           const bool ok = el && ((u64)nR + ce <= (u64)mns) && tok_ok &&
