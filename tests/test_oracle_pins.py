@@ -267,6 +267,22 @@ def test_cost_monotone_random_plans(oracle_lib):
                / _t(_one(si.LLAMA2_7B), decodes=[1]) - 1) < 0.01
 
 
+def test_decode_stretch_times_nondecreasing(oracle_lib):
+    """The kernel's fast-forward takes a stretch's largest token gap as its last iteration's T
+    (DESIGN §8 A/B log): in a decode-only stretch only C_d grows (every context +1 per iteration),
+    so T_j must be nondecreasing in j for every model, profile and TP degree, rounding included."""
+    rng = np.random.default_rng(11)
+    hws = [si.A100, si.A100_IDEAL, si.Hw(peak_flops=2.5e15, mem_bw=8e12)] + \
+          [si.Hw(tp_degree=t, tp_link_bw=300e9) for t in (2, 4, 8)]
+    for model in (si.LLAMA2_7B, si.LLAMA2_13B, si.LLAMA2_70B):
+        for hw in hws:
+            cfg = _one(model, hw)
+            for _ in range(4):
+                dec = [int(x) for x in rng.integers(1, 4096, int(rng.integers(1, 64)))]
+                ts = [_t(cfg, decodes=[c + j for c in dec]) for j in range(32)]
+                assert all(a <= b for a, b in zip(ts, ts[1:])), (model.name, hw, ts)
+
+
 # ------------------------------------------------------------------ a.2-a.7 hand-worked traces
 def _sim(cfg, **kw):
     from oracle import oracle as O
