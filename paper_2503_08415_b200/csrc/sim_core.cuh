@@ -1707,7 +1707,9 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     const u64 Cd = warp_sum64(cdp);
     u64 Np = 0, Ap = 0, Kp = 0, Slm = Sp;
     if (Sp) {
-      Np = warp_sum64(npp);
+      // lean kernels (MIXED): every prefill token was admitted under tokens <= mbt (a u32), so
+      // N_p < 2^32 and one 32-bit reduction is exact
+      Np = FULL ? warp_sum64(npp) : (u64)__reduce_add_sync(FULLMASK, (u32)npp);
       Ap = warp_sum64(app);
       Kp = Np;
       if (CHK || CACHE) Kp = warp_sum64(kpp);
