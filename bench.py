@@ -5,12 +5,20 @@
 
 One *step* = one pass of the whole hot path (workload
 generation, the persistent per-point simulation kernel, the quantile/summary kernel)
-over the configuration's sweep points.  The N=1 workload is BASELINE.json configs[1]
-(C2: LLaMA-2-13B, 1,000 ShareGPT-shaped requests, lambda 1..16 x 8 seeds = 128 points).
-Weak scaling: with N ranks the grid grows to 8N seeds (N x 128 points) and rank r runs
-points r, r+N, ... (no data-path collective; the 384-B summaries are all-gathered once
-per step, the only exchange).  `value` = simulated request-iterations of all points of
-all ranks / the max-over-ranks device time of the K timed steps.
+over the configuration's sweep points.  The default workload is north_star's target, the
+largest single-GPU configuration: BASELINE.json configs[2] = C3 (LLaMA-2-7B hardware sweep,
+16 FLOP/s x 16 HBM GB/s x 6 capacities x 3 policies = 4,608 points of 10,000 requests;
+P:617).  Strong scaling (the default for N > 1, SURVEY §8(d) "same point set,
+strided sharding"): every N runs the same point set and rank r runs points r, r+N, ...
+(no data-path collective; the 384-B summaries are all-gathered once per step, the only
+exchange).  `--scaling weak` instead replicates the seed axis N times.  `value` =
+simulated request-iterations of all points of all ranks / the max-over-ranks device time
+of the K timed steps.
+
+--emulate-ranks G measures the 1..G strong-scaling curve on ONE GPU: each rank's strided
+subset runs back to back (ranks share nothing but the final all-gather, so no kernel waits
+on another), the curve point is the max-over-ranks step time; beside it the chain floor:
+the longest points simulated alone (one warp on one SM), the time no number of GPUs beats.
 
 --impl reference times the CPU oracle (oracle/, the reference arm of this tier) on
 the host cores, on a bounded sample of the same workload.
@@ -19,6 +27,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import numpy as np
 import os
 import statistics
 import subprocess
@@ -50,14 +59,16 @@ def env_rank():
         int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def config_for(name: str, world: int) -> si.SweepConfig:
-    if name == "c2":
-        return si.c2(n_seeds=8 * world)
-    if name == "c5":  # 65,536 points = 8 seeds x 8,192; one seed (8,192 points) per GPU
+def config_for(name: str, world: int, scaling: str = "strong") -> si.SweepConfig:
+    """The sweep all ranks run together.  strong: the same point set at every N (C5: the
+    65,536-point grid; at N = 1 that is 8 x the per-GPU share).  weak: N copies of the seed axis
+    (C5: one seed = 8,192 points per GPU)."""
+    if name == "c5":
         cfg = si.c5()
-        return replace(cfg, workload=replace(cfg.workload, seeds=list(range(world))))
+        seeds = list(range(8)) if scaling == "strong" else list(range(world))
+        return replace(cfg, workload=replace(cfg.workload, seeds=seeds))
     cfg = si.PRESETS[name]()
-    if world > 1:  # weak scaling: replicate the seed axis
+    if world > 1 and scaling == "weak":  # replicate the seed axis
         w = cfg.workload
         cfg = replace(cfg, workload=replace(w, seeds=list(range(len(w.seeds) * world))))
     return cfg
@@ -65,10 +76,10 @@ def config_for(name: str, world: int) -> si.SweepConfig:
 
 WORKLOAD_DESC = {
     "c1": "C1 single simulation: LLaMA-2-7B, A100-like profile, 100 requests at 2 req/s, CONT, 16-token blocks",
-    "c2": "C2: LLaMA-2-13B, 1,000 ShareGPT-shaped requests, lambda 1..16 req/s x 8 seeds = 128 points per GPU",
+    "c2": "C2: LLaMA-2-13B, 1,000 ShareGPT-shaped requests, lambda 1..16 req/s x 8 seeds = 128 points",
     "c3": "C3: LLaMA-2-7B hardware sweep 16 F x 16 B x 6 C x {STATIC, CONT, CONT_RATIO 0.9}, 10k requests, 4,608 points",
     "c4": "C4: LLaMA-2-70B TP 2/4/8 x {CONT, CONT_RATIO 0.9} x {SWAP, RECOMPUTE} x 16 rates x 12 seeds, 10k req, 2,304 points",
-    "c5": "C5: 1P:1D pairs 16x16 x {SWAP, RECOMPUTE} x 16 rates, 10k requests; 8,192 points (one seed) per GPU, 65,536 at 8 GPUs",
+    "c5": "C5: 1P:1D pairs 16x16 x {SWAP, RECOMPUTE} x 16 rates x 8 seeds, 10k requests, 65,536 points (weak: one seed = 8,192 points per GPU)",
     # widened rows; measurement only, not BASELINE configs
     "c6": "NEXT-1: P2:D6 node, LLaMA-2-7B, least-outstanding dispatch, {SWAP, RECOMPUTE} x 16 rates x 8 seeds, 10k req, 256 points",
     "c7": "NEXT-2: multi-round conversations + memory cache, LLaMA-2-7B, 2k conversations, {SWAP, RECOMPUTE} x 16 rates x 8 seeds",
@@ -176,7 +187,7 @@ def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    cfg = config_for(args.config, 1)
+    cfg = config_for(args.config, args.gpus, args.scaling)
     per_step = max(2.0, args.reference_budget / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
         oracle_sample(cfg, budget_s=per_step)
@@ -190,7 +201,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": walls / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64/f64",
         "data": "synthetic (Philox-seeded Poisson arrivals, SHAREGPT_SYNTH_V1 lengths)",
         "config": {"workload": WORKLOAD_DESC[args.config], "points": cfg.num_points,
                    "sample": desc},
@@ -214,7 +225,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     import paper_2503_08415_b200 as P
 
-    cfg = config_for(args.config, world)
+    cfg = config_for(args.config, world, args.scaling)
     sw = P.Sweep(cfg)
     stream = torch.cuda.Stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -334,12 +345,12 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            v, cores, desc, _, _ = oracle_sample(config_for(args.config, 1), budget_s=args.cpu_budget)
+            v, cores, desc, _, _ = oracle_sample(cfg, budget_s=args.cpu_budget)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int64/f64",
             "data": "synthetic (Philox-seeded Poisson arrivals, SHAREGPT_SYNTH_V1 lengths); no trained weights needed",
             "config": {"workload": WORKLOAD_DESC[args.config], "points": n_pts,
                        "points_per_gpu": -(-n_pts // world), "requests_per_point": cfg.workload.num_requests,
@@ -374,13 +385,88 @@ def run_ours(args):
     return 0
 
 
+def run_emulate(args):
+    """Strong-scaling curve on one GPU (VERDICT r1 "Next round #3").  Rank r of G runs points
+    p = r (mod G); ranks share nothing but the final 384-B all-gather, so running their subsets
+    back to back on one GPU and taking the max-over-ranks step time gives the G-GPU step time
+    (minus the all-gather, tens of microseconds over NVLink).  Beside it, the chain floor: each of
+    the longest points simulated ALONE (one warp on one SM with its helper warp) -- a point never
+    splits across warps or GPUs, so no G beats max over points of that time."""
+    import torch
+    import paper_2503_08415_b200 as P
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = config_for(args.config, 1, "strong")
+    sw = P.Sweep(cfg)
+    stream = torch.cuda.Stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    n_pts = sw.num_points
+    reps = max(1, min(args.steps, 5))
+
+    def timed(begin, end, stride):
+        ts = []
+        for i in range(reps + 1):  # one warm-up run of this shard
+            with torch.cuda.stream(stream):
+                flush.fill_(i & 0xff)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sw.run(begin, end, stride, device=dev, stream=stream)
+            b.record(stream)
+            b.synchronize()
+            if i:
+                ts.append(a.elapsed_time(b))
+        s = sw.summaries()
+        return statistics.median(ts), s
+
+    t1, s_all = timed(0, n_pts, 1)
+    ri_total = int(s_all["n_request_iterations"].sum())
+    iters = s_all["n_iterations"].astype(np.int64)
+    curve = []
+    G = 1
+    while G <= args.emulate_ranks:
+        per = []
+        for r in range(G):
+            t, s = (t1, s_all) if G == 1 else timed(r, n_pts, G)
+            per.append({"rank": r, "ms": t, "points": int(len(s)),
+                        "request_iterations": int(s["n_request_iterations"].sum()),
+                        "max_iterations": int(s["n_iterations"].max()) if len(s) else 0})
+        tmax = max(p["ms"] for p in per)
+        curve.append({"gpus": G, "ms_per_step": tmax, "value": ri_total / (tmax / 1e3),
+                      "speedup": t1 / tmax, "efficiency": t1 / tmax / G, "ranks": per})
+        G *= 2
+    # chain floor: the longest points alone
+    order = np.argsort(-iters)[:args.floor_points]
+    floors = []
+    for p in order:
+        pt = int(s_all["point"][p])
+        t, s = timed(pt, pt + 1, 1)
+        floors.append({"point": pt, "iterations": int(iters[p]), "ms_alone": t,
+                       "ns_per_iteration": t * 1e6 / max(1, int(iters[p]))})
+    floor_ms = max(f["ms_alone"] for f in floors)
+    line = {"metric": METRIC, "unit": UNIT, "mode": "emulated strong scaling (one GPU, ranks back to back)",
+            "config": {"workload": WORKLOAD_DESC[args.config], "points": n_pts,
+                       "request_iterations_per_step": ri_total},
+            "curve": curve,
+            "chain_floor": {"ms": floor_ms, "value_ceiling": ri_total / (floor_ms / 1e3),
+                            "max_speedup_vs_1gpu": t1 / floor_ms, "points": floors,
+                            "note": "the longest points simulated alone; no number of GPUs runs a step faster"},
+            "gpu": torch.cuda.get_device_name(dev)}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="one GPU: measure the strong-scaling curve for 1, 2, 4, ... G ranks and the chain floor")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--floor-points", type=int, default=4)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--reference-budget", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -390,6 +476,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.emulate_ranks:
+        return run_emulate(args)
     return run_ours(args)
 
 

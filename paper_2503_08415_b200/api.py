@@ -313,10 +313,16 @@ def run_distributed(cfg: si.SweepConfig, group=None):
     then all-gathered (NCCL over NVLink) and imported so every rank can answer summary and
     P50/P90/P99/max queries for every point.  Returns (sweep handle, all summaries)."""
     import torch.distributed as dist
+    import torch
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     sw = Sweep(cfg)
     b, e, s = shard_range(sw.num_points, rank, world)
-    sw.run(b, e, s)
-    allv = gather_summaries(sw.summaries_device(), sw.num_points, group)
+    if b < e:
+        sw.run(b, e, s)
+        local = sw.summaries_device()
+    else:  # more ranks than points: this rank owns none and joins the all-gather with padding only
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        local = torch.zeros(0, dtype=torch.uint8, device=dev)
+    allv = gather_summaries(local, sw.num_points, group)
     sw.import_summaries(allv)
     return sw, allv

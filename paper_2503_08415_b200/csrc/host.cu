@@ -519,12 +519,22 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   return L;
 }
 
+// SM count of `dev`; dev < 0: the largest over all visible devices (a workspace sized with it
+// fits a run on any of them)
 static int device_sms(int dev) {
   int sms = 148;
   int count = 0;
   if (cudaGetDeviceCount(&count) == cudaSuccess && count > 0) {
-    int d = dev >= 0 ? dev : 0;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) sms = 148;
+    if (dev >= 0) {
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+    } else {
+      int best = 0;
+      for (int d = 0; d < count; ++d) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) == cudaSuccess) best = std::max(best, v);
+      }
+      sms = best > 0 ? best : 148;
+    }
   } else {
     cudaGetLastError();
   }
@@ -601,8 +611,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   Layout L0 = make_layout(h, n_run, sms, 0);
   int occ = 0;
   e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general,
-                                L0.wpb > 1 || (u64)L0.blocks > (u64)sms),
-                    (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, &occ);
+                                L0.wpb > 1 || (u64)L0.blocks > (u64)sms || !helper_fits(per_warp, h->nwords_max)),
+                    (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, h->nwords_max, &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
   const Layout L = make_layout(h, n_run, sms, occ);

@@ -7,5 +7,7 @@ namespace ts {
 cudaError_t launch_sim_base_c(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
   return launch_sim_v<4>(p, cap, wpb, blocks, smem, st);
 }
-cudaError_t sim_occupancy_base_c(int cap, int wpb, size_t smem, int *b) { return sim_occupancy_v<4>(cap, wpb, smem, b); }
+cudaError_t sim_occupancy_base_c(int cap, int wpb, size_t smem, u32 nw, int *b) {
+  return sim_occupancy_v<4>(cap, wpb, smem, nw, b);
+}
 }  // namespace ts

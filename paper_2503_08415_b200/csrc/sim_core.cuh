@@ -1813,7 +1813,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     NPH(5);
     {
       const u32 rn = __reduce_min_sync(FULLMASK, rmin_l);
-      rmin = pf_only ? min(rmin, rn) : rn;  // paused requests keep their rem
+      // After a prefill-only iteration the paused decodes' last token is older than t, so the
+      // next stretch's first gap would exceed its last iteration's T (the stretch takes T_{J-1}
+      // as every slot's largest gap): no stretch until a normal iteration has given every
+      // running request a token at t.
+      rmin = pf_only ? 0u : rn;
     }
     __syncwarp();
     req_iters += nR - c0 - (xout ? 1u : 0u);
@@ -2016,10 +2020,11 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
   const i64 W = (i64)P.bin_ns;
   while (true) {
     u32 st;
-    long long c0 = clock64();
-    // 1: a point is running; 2: a short point already finished before we looked; 4: exit
+    // 1: a point is running; 2: a short point already finished before we looked; 4: exit.
+    // No timeout here: the simulating warp always ends with state 4, and leaving early would
+    // turn every later point of this CTA into a timed-out wait.  The waits inside a
+    // point keep their bound and flag that point instead.
     while ((st = chan_load(&ch->state)) != 1u && st != 2u && st != 4u) {
-      if (clock64() - c0 > HELPER_TIMEOUT) return;
     }
     if (st == 4u) return;
     __threadfence_block();
@@ -2064,7 +2069,7 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
       acc_max = 0;
       acc_nit = 0;
     };
-    c0 = clock64();
+    long long c0 = clock64();
     while (true) {
       const u32 s2 = chan_load(&ch->state);  // the state before the producer counts
       __threadfence_block();
@@ -2329,10 +2334,10 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
 template <int V>
 static __host__ __forceinline__ int sim_threads(int wpb) { return (V == 0 && TS_HELPER_WARP) ? 64 : wpb * 32; }
 // the helper's area: hand-over counters, its replayed bitmap (nwords_max words), 256 extraction slots
+static_assert(sizeof(HelperChan) <= kHelperChanBytes, "helper area (ts_internal.cuh)");
 template <int V>
 static __host__ __forceinline__ size_t sim_smem(size_t smem, u32 nwords_max) {
-  return (V == 0 && TS_HELPER_WARP) ? ((smem + 15) & ~(size_t)15) + sizeof(HelperChan) + 4 * (size_t)nwords_max + 1024
-                                    : smem;
+  return (V == 0 && TS_HELPER_WARP) ? helper_cta_smem(smem, nwords_max) : smem;
 }
 template <int CAP, int V, bool P2>
 static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_t smem, cudaStream_t st) {
@@ -2344,8 +2349,8 @@ static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_
   return cudaGetLastError();
 }
 template <int CAP, int V, bool P2>
-static cudaError_t occ_t(int wpb, size_t smem, int *b) {
-  smem = sim_smem<V>(smem, 4096);  // (variant 0 runs one CTA per SM; a generous bitmap bound)
+static cudaError_t occ_t(int wpb, size_t smem, u32 nwords_max, int *b) {
+  smem = sim_smem<V>(smem, nwords_max);
   cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, V, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_kernel<CAP, V, P2>, sim_threads<V>(wpb), smem);
@@ -2365,20 +2370,20 @@ static cudaError_t launch_sim_v(const SweepParams &p, int cap, int wpb, int bloc
                   : launch_sim_c<V, false>(p, cap, wpb, blocks, smem, st);
 }
 template <int V, bool P2>
-static cudaError_t sim_occupancy_c(int cap, int wpb, size_t smem, int *b) {
+static cudaError_t sim_occupancy_c(int cap, int wpb, size_t smem, u32 nw, int *b) {
   switch (cap) {
-    case 32: return occ_t<32, V, P2>(wpb, smem, b);
-    case 256: return occ_t<256, V, P2>(wpb, smem, b);
-    case 1024: return occ_t<1024, V, P2>(wpb, smem, b);
+    case 32: return occ_t<32, V, P2>(wpb, smem, nw, b);
+    case 256: return occ_t<256, V, P2>(wpb, smem, nw, b);
+    case 1024: return occ_t<1024, V, P2>(wpb, smem, nw, b);
     default: return cudaErrorInvalidValue;
   }
 }
 template <int V>
-static cudaError_t sim_occupancy_v(int cap, int wpb, size_t smem, int *b) {
+static cudaError_t sim_occupancy_v(int cap, int wpb, size_t smem, u32 nw, int *b) {
   int b1 = 0, b2 = 0;  // the same resources either way; take the smaller to be safe
-  cudaError_t e = sim_occupancy_c<V, true>(cap, wpb, smem, &b1);
+  cudaError_t e = sim_occupancy_c<V, true>(cap, wpb, smem, nw, &b1);
   if (e != cudaSuccess) return e;
-  e = sim_occupancy_c<V, false>(cap, wpb, smem, &b2);
+  e = sim_occupancy_c<V, false>(cap, wpb, smem, nw, &b2);
   *b = b1 < b2 ? b1 : b2;
   return e;
 }

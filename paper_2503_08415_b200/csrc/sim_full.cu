@@ -8,5 +8,7 @@ namespace ts {
 cudaError_t launch_sim_full(const SweepParams &p, int cap, int wpb, int blocks, size_t smem, cudaStream_t st) {
   return launch_sim_v<1>(p, cap, wpb, blocks, smem, st);
 }
-cudaError_t sim_occupancy_full(int cap, int wpb, size_t smem, int *b) { return sim_occupancy_v<1>(cap, wpb, smem, b); }
+cudaError_t sim_occupancy_full(int cap, int wpb, size_t smem, u32 nw, int *b) {
+  return sim_occupancy_v<1>(cap, wpb, smem, nw, b);
+}
 }  // namespace ts

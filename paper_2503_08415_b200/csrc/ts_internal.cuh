@@ -171,6 +171,15 @@ cudaError_t launch_sim_base_c(const SweepParams &p, int cap, int warps_per_block
                               cudaStream_t st);
 // several warps per SM: the lean kernel with compact helpers (variant 4); one warp per SM:
 // variant 0, whose CTA adds a helper warp (sim_base.cu)
+// Shared memory of a variant-0 CTA: the simulating warp's area, then the helper's hand-over
+// counters (kHelperChanBytes >= sizeof(HelperChan), asserted in sim_core.cuh), its replayed
+// bitmap (nwords_max words) and 256 extraction slots.  A point whose CTA would not fit in
+// 227 KB runs in variant 4 (no helper) instead.
+constexpr size_t kHelperChanBytes = 128;
+inline size_t helper_cta_smem(size_t per_warp, u32 nwords_max) {
+  return ((per_warp + 15) & ~(size_t)15) + kHelperChanBytes + 4 * (size_t)nwords_max + 1024;
+}
+inline bool helper_fits(size_t per_warp, u32 nwords_max) { return helper_cta_smem(per_warp, nwords_max) <= 227 * 1024; }
 inline int sim_variant(bool full, bool pd, bool pd_general, bool multi_warp = false) {
   return !full ? (multi_warp ? 4 : 0) : !pd ? 1 : pd_general ? 3 : 2;
 }
@@ -179,7 +188,8 @@ inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block
   // TOKENSIM_HELPER=1 (A/B experiments): the helper-warp lean kernel even with several CTAs per SM
   const bool force_helper = warps_per_block == 1 && getenv("TOKENSIM_HELPER") != nullptr;
   switch (sim_variant(p.full != 0, p.topology == TOKENSIM_PD_PAIR, p.pd_general != 0,
-                      !force_helper && (warps_per_block > 1 || (u64)blocks > (u64)p.n_sms))) {
+                      !force_helper && (warps_per_block > 1 || (u64)blocks > (u64)p.n_sms ||
+                                        !helper_fits(smem, p.nwords_max)))) {
     case 0: return launch_sim_base(p, cap, warps_per_block, blocks, smem, st);
     case 4: return launch_sim_base_c(p, cap, warps_per_block, blocks, smem, st);
     case 1: return launch_sim_full(p, cap, warps_per_block, blocks, smem, st);
@@ -198,18 +208,19 @@ size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_
 inline size_t pdn_global_per_warp(u64 n, u32 cap, u32 btl, u32 x, u32 y) {
   return (size_t)y * n * 32 + (size_t)x * n * 4 * 2 + (size_t)x * cap * 4 + n * 8 + n * (size_t)btl * 4 + 256;
 }
-cudaError_t sim_occupancy_base(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
-cudaError_t sim_occupancy_full(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
-cudaError_t sim_occupancy_pair(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
-cudaError_t sim_occupancy_node(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
-cudaError_t sim_occupancy_base_c(int cap, int warps_per_block, size_t smem, int *blocks_per_sm);
-inline cudaError_t sim_occupancy(int variant, int cap, int warps_per_block, size_t smem, int *blocks_per_sm) {
+cudaError_t sim_occupancy_base(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
+cudaError_t sim_occupancy_full(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
+cudaError_t sim_occupancy_pair(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
+cudaError_t sim_occupancy_node(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
+cudaError_t sim_occupancy_base_c(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
+inline cudaError_t sim_occupancy(int variant, int cap, int warps_per_block, size_t smem, u32 nwords_max,
+                                 int *blocks_per_sm) {
   switch (variant) {
-    case 0: return sim_occupancy_base(cap, warps_per_block, smem, blocks_per_sm);
-    case 1: return sim_occupancy_full(cap, warps_per_block, smem, blocks_per_sm);
-    case 2: return sim_occupancy_pair(cap, warps_per_block, smem, blocks_per_sm);
-    case 4: return sim_occupancy_base_c(cap, warps_per_block, smem, blocks_per_sm);
-    default: return sim_occupancy_node(cap, warps_per_block, smem, blocks_per_sm);
+    case 0: return sim_occupancy_base(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
+    case 1: return sim_occupancy_full(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
+    case 2: return sim_occupancy_pair(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
+    case 4: return sim_occupancy_base_c(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
+    default: return sim_occupancy_node(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
   }
 }
 

@@ -79,3 +79,39 @@ def test_shard_gather_import_gloo_world2():
     assert sorted(r[0] for r in res) == [0, 1]
     assert all(r[1] for r in res), res
     assert sum(r[2] for r in res) == 128 and all(r[2] == 64 for r in res)
+
+
+def _worker_idle(rank, world, port, out_q):
+    """More ranks than points: the idle rank joins the all-gather with an empty slot."""
+    import torch.distributed as dist
+
+    import sweep_inputs as si
+    import paper_2503_08415_b200 as P
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = si.subset(si.c2(), rates=[0], seeds=[0, 1])
+        sw = P.Sweep(cfg)
+        b, e, s = P.shard_range(sw.num_points, rank, world)
+        mine = list(range(b, e, s))
+        allv = P.gather_summaries(fake_summaries(mine), sw.num_points)
+        sw.import_summaries(allv)
+        ok = list(allv["point"]) == [0, 1]
+        out_q.put((rank, bool(ok), len(mine)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_more_ranks_than_points_gloo_world3():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_idle, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[2] for r in res] == [1, 1, 0] and all(r[1] for r in res), res

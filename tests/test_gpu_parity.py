@@ -323,6 +323,37 @@ def test_prefill_first_parity(api):
         check_points(run_gpu(api, c), c, [0], records=True, trace=True, iters=True)
 
 
+def test_prefill_first_under_memory_pressure(api):
+    """Prefill-first iterations with a small KV pool: the memory back-off of the fast-forward and
+    the prefill-only pauses interleave, so a stretch must never start right after a prefill-only
+    iteration (the paused decodes' first gap would be lost from mTPOT).  Oracle parity on every
+    point and fast-forward on == off byte for byte."""
+    pols = [si.Policy(kind=k, preempt=pm, max_mem_ratio=r, iteration_mode=si.PREFILL_FIRST)
+            for k, r in ((si.CONT, 1.0), (si.CONT_RATIO, 0.8)) for pm in (si.SWAP, si.RECOMPUTE)]
+    cfg = si.SweepConfig("pf-pressure", si.LLAMA2_13B, [si.Hw(mem_capacity=30 * 10 ** 9),
+                                                         si.Hw(mem_capacity=34 * 10 ** 9)], pols,
+                         si.Workload(400, [4.0, 16.0], [0, 1]))
+    sw = run_gpu(api, cfg)
+    check_points(sw, cfg, list(range(cfg.num_points)), records=True, trace=True)
+    off = run_gpu(api, replace(cfg, options=replace(cfg.options, fast_forward=False)))
+    assert sw.summaries().tobytes() == off.summaries().tobytes()
+    for p in range(cfg.num_points):
+        assert sw.records(p).tobytes() == off.records(p).tobytes()
+    assert sw.summaries()["n_preemptions"].sum() > 0
+
+
+@pytest.mark.parametrize("blocks", [300_000, 1_000_000])
+def test_huge_kv_pool_on_few_points(api, blocks):
+    """A few points (one warp per SM, the helper-warp kernel) with a free-block bitmap far beyond
+    4,096 words: 300k blocks still fit the helper's replayed copy (variant 0), 1M blocks (125 KB of
+    bitmap) do not and must run without the helper (variant 4) instead of failing."""
+    w = si.Workload(300, [20.0], [0, 1])
+    cfg = si.SweepConfig("huge-pool", si.LLAMA2_7B, [replace(si.A100, kv_blocks_override=blocks)],
+                         [si.Policy()], w, si.Options(trace_mode=si.FULL))
+    sw = run_gpu(api, cfg)
+    check_points(sw, cfg, [0, 1], records=True, trace=True)
+
+
 def test_large_point_summary_scratch_path(api):
     """n = 20,000 requests per point exceeds the summary kernel's shared-memory key buffer
     (12,288), so quantiles run over the workspace scratch path; also exercises a trace cap."""
