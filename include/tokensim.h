@@ -159,7 +159,9 @@ typedef struct {
   double pd_link_bw;          /* B/s, P->D KV link (200e9)                    */
   uint32_t trace_mode;        /* TOKENSIM_TRACE_NONE | BINNED | FULL                 */
   uint64_t trace_bin_ns;      /* BINNED bin width (1e9)                              */
-  uint64_t trace_cap_bytes;   /* per point per worker; samples are 32 B              */
+  uint64_t trace_cap_bytes;   /* per point per worker: BINNED holds 32-B samples; FULL holds
+                                 the compressed stream (~4 B per iteration, see
+                                 tokensim_get_mem_trace_encoded)                        */
   uint32_t iteration_trace_cap;  /* per point; 0 = off (debug / parity)              */
   double slo_ttft_s;          /* 15                                          */
   double slo_mtpot_s;         /* 0.3                                         */
@@ -275,9 +277,21 @@ tokensim_status tokensim_get_latency_quantiles(const tokensim_sweep *h, uint64_t
                                                const uint32_t *q_bp, uint32_t n_q, double *out_seconds);
 /* KV memory over time of one worker: 0 = unified; PD_PAIR: prefill workers
  * 0..x-1, decode workers x..x+y-1 (1P:1D: 0 = prefill, 1 = decode).  E_RANGE for any other
- * worker.  Returns E_OVERFLOW (with the samples that fit) if the trace hit its cap. */
+ * worker.  Returns E_OVERFLOW (with the samples that fit) if the trace hit its cap.  FULL
+ * traces are stored compressed on the device and decoded here (one sample per iteration:
+ * t_ns = start, dur_ns = T, block_ns = blocks * T, blocks_max = blocks, n_iter = 1). */
 tokensim_status tokensim_get_mem_trace(const tokensim_sweep *h, uint64_t point, uint32_t worker,
                                        tokensim_mem_sample *out, uint64_t capacity, uint64_t *n_out);
+/* The FULL trace as stored: a byte stream (SURVEY §8(a.8) "delta + varint"; reading A28, one
+ * record per iteration k) of three unsigned LEB128 varints per iteration,
+ *     t_start_k - t_end_{k-1}  (>= 0),  zigzag(T_k - T_{k-1}),  zigzag(blocks_k - blocks_{k-1}),
+ * with t_end_{-1} = T_{-1} = blocks_{-1} = 0 and zigzag(v) = (v << 1) ^ (v >> 63).  The
+ * stream holds whole records only: one that would cross trace_cap_bytes ends it (E_OVERFLOW).
+ * *n_bytes = stream length, *n_samples = its iterations; out = NULL or capacity = 0 only
+ * queries them; a smaller buffer is E_TRUNCATED.  E_STATE unless trace_mode = FULL. */
+tokensim_status tokensim_get_mem_trace_encoded(const tokensim_sweep *h, uint64_t point, uint32_t worker,
+                                               uint8_t *out, uint64_t capacity, uint64_t *n_bytes,
+                                               uint64_t *n_samples);
 tokensim_status tokensim_get_summary(const tokensim_sweep *h, uint64_t point, tokensim_summary *out);
 /* All summaries of the last run, in run order (point begin, begin+stride, ...). */
 tokensim_status tokensim_get_summaries(const tokensim_sweep *h, tokensim_summary *out, uint64_t capacity,

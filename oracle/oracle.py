@@ -209,7 +209,11 @@ def make_cfg(cfg: si.SweepConfig, point: int, check_invariants: bool = False,
     c.pd_link_bw = o.pd_link_bw
     c.trace_mode = _TRC[o.trace_mode]
     c.trace_bin_ns = o.trace_bin_ns
-    c.trace_cap_samples = trace_cap_samples if trace_cap_samples is not None else o.trace_cap_bytes // 32
+    # BINNED: the caller's cap in 32-B samples.  FULL: every iteration is kept (the CUDA path stores
+    # FULL compressed, so its cap is a byte budget; parity compares the prefix it holds)
+    if trace_cap_samples is None:
+        trace_cap_samples = (1 << 40) if o.trace_mode == si.FULL else o.trace_cap_bytes // 32
+    c.trace_cap_samples = trace_cap_samples
     c.slo_ttft_s, c.slo_mtpot_s, c.horizon_ns = o.slo_ttft_s, o.slo_mtpot_s, o.horizon_ns
     c.check_invariants = 1 if check_invariants else 0
     c.keep_events = 1 if keep_events else 0

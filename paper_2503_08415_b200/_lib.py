@@ -116,7 +116,7 @@ EXPORTS = [
     "tokensim_get_summaries", "tokensim_get_summaries_device", "tokensim_import_summaries",
     "tokensim_get_request_records", "tokensim_get_iteration_trace", "tokensim_get_workload",
     "tokensim_last_error", "tokensim_sweep_destroy", "tokensim_version", "tokensim_get_run_info",
-    "tokensim_get_point_profile",
+    "tokensim_get_point_profile", "tokensim_get_mem_trace_encoded",
 ]
 
 _lib = None
@@ -146,6 +146,8 @@ def lib():
     L.tokensim_get_latency_quantiles.restype = C.c_int
     L.tokensim_get_mem_trace.argtypes = [vp, u64, u32, vp, u64, PU64]
     L.tokensim_get_mem_trace.restype = C.c_int
+    L.tokensim_get_mem_trace_encoded.argtypes = [vp, u64, u32, vp, u64, PU64, PU64]
+    L.tokensim_get_mem_trace_encoded.restype = C.c_int
     L.tokensim_get_summary.argtypes = [vp, u64, vp]
     L.tokensim_get_summary.restype = C.c_int
     L.tokensim_get_summaries.argtypes = [vp, vp, u64, PU64]

@@ -216,6 +216,20 @@ class Sweep:
                 self._check(st, "get_mem_trace")
         return out
 
+    def mem_trace_encoded(self, point: int, worker: int = 0):
+        """The FULL trace's compressed byte stream as stored on the device (see tokensim.h):
+        (uint8 array, number of iterations it encodes)."""
+        nb, ns = C.c_uint64(), C.c_uint64()
+        self._check(self._L.tokensim_get_mem_trace_encoded(self._h, point, worker, None, 0, C.byref(nb), C.byref(ns)),
+                    "get_mem_trace_encoded")
+        out = np.zeros(nb.value, np.uint8)
+        if nb.value:
+            st = self._L.tokensim_get_mem_trace_encoded(self._h, point, worker, out.ctypes.data, nb.value,
+                                                        C.byref(nb), C.byref(ns))
+            if st not in (T.OK, T.E_OVERFLOW):
+                self._check(st, "get_mem_trace_encoded")
+        return out, ns.value
+
     def iteration_trace(self, point: int) -> np.ndarray:
         n = C.c_uint64()
         self._check(self._L.tokensim_get_iteration_trace(self._h, point, None, 0, C.byref(n)), "get_iteration_trace")

@@ -913,6 +913,41 @@ tokensim_status tokensim_get_iteration_trace(const tokensim_sweep *hc, uint64_t 
   return copy_d2h(h, out, h->P.itrec + j * h->P.it_cap, st.iter_n * sizeof(tokensim_iter_record));
 }
 
+// Decoder of the compressed FULL memory trace (trace_codec.cuh; format in include/tokensim.h):
+// three LEB128 varints per iteration -- idle gap, zigzag dT, zigzag dblocks.  Rebuilds the
+// documented FULL samples (t_start, T, blocks * T, blocks, 1).  false: the stream is malformed.
+static bool read_varint(const unsigned char *&p, const unsigned char *end, u64 &x) {
+  x = 0;
+  for (u32 sh = 0; sh < 64; sh += 7) {
+    if (p == end) return false;
+    const unsigned char b = *p++;
+    x |= (u64)(b & 0x7fu) << sh;
+    if (!(b & 0x80u)) return true;
+  }
+  return false;
+}
+static i64 unzigzag(u64 z) { return (i64)(z >> 1) ^ -(i64)(z & 1u); }
+static bool decode_full_trace(const unsigned char *buf, size_t bytes, u64 n, tokensim_mem_sample *out) {
+  const unsigned char *p = buf, *end = buf + bytes;
+  i64 te = 0, T = 0, blk = 0;
+  for (u64 k = 0; k < n; ++k) {
+    u64 gap, dT, dB;
+    if (!read_varint(p, end, gap) || !read_varint(p, end, dT) || !read_varint(p, end, dB)) return false;
+    const i64 ts = te + (i64)gap;
+    T += unzigzag(dT);
+    blk += unzigzag(dB);
+    if (T < 0 || blk < 0 || blk > 0xffffffffll) return false;
+    te = ts + T;
+    tokensim_mem_sample &sm = out[k];
+    sm.t_ns = ts;
+    sm.dur_ns = T;
+    sm.block_ns = (u64)blk * (u64)T;
+    sm.blocks_max = (u32)blk;
+    sm.n_iter = 1;
+  }
+  return p == end;
+}
+
 tokensim_status tokensim_get_mem_trace(const tokensim_sweep *hc, uint64_t point, uint32_t worker,
                                        tokensim_mem_sample *out, uint64_t capacity, uint64_t *n_out) {
   tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
@@ -930,8 +965,41 @@ tokensim_status tokensim_get_mem_trace(const tokensim_sweep *hc, uint64_t point,
   *n_out = cnt;
   if (!out || capacity == 0) return TOKENSIM_OK;
   if (capacity < cnt) return TOKENSIM_E_TRUNCATED;
-  s = copy_d2h(h, out, h->P.trace + (j * h->P.trace_nw + worker) * h->P.trace_cap, cnt * sizeof(tokensim_mem_sample));
-  if (s != TOKENSIM_OK) return s;
+  const tokensim_mem_sample *src = h->P.trace + (j * h->P.trace_nw + worker) * h->P.trace_cap;
+  if (h->opt.trace_mode == TOKENSIM_TRACE_FULL) {
+    // the compressed stream (trace_codec.cuh): decode it here into one sample per iteration
+    std::vector<unsigned char> buf(st.trace_b[worker]);
+    if (!buf.empty() && (s = copy_d2h(h, buf.data(), src, buf.size())) != TOKENSIM_OK) return s;
+    if (!decode_full_trace(buf.data(), buf.size(), cnt, out))
+      return fail(h, TOKENSIM_E_STATE, "get_mem_trace: corrupt FULL trace stream");
+  } else {
+    s = copy_d2h(h, out, src, cnt * sizeof(tokensim_mem_sample));
+    if (s != TOKENSIM_OK) return s;
+  }
+  return (st.flags & TOKENSIM_PT_TRACE_OVERFLOW) ? TOKENSIM_E_OVERFLOW : TOKENSIM_OK;
+}
+
+tokensim_status tokensim_get_mem_trace_encoded(const tokensim_sweep *hc, uint64_t point, uint32_t worker,
+                                               uint8_t *out, uint64_t capacity, uint64_t *n_bytes,
+                                               uint64_t *n_samples) {
+  tokensim_sweep *h = const_cast<tokensim_sweep *>(hc);
+  if (!h || !n_bytes) return TOKENSIM_E_INVALID;
+  const u32 n_workers = h->opt.topology == TOKENSIM_PD_PAIR ? h->pd_x + h->pd_y : 1u;
+  if (worker >= n_workers) return TOKENSIM_E_RANGE;
+  u64 j;
+  tokensim_status s = local_index(h, point, &j);
+  if (s != TOKENSIM_OK) return fail(h, s, "get_mem_trace_encoded: point not run by this handle");
+  if (h->opt.trace_mode != TOKENSIM_TRACE_FULL) return fail(h, TOKENSIM_E_STATE, "get_mem_trace_encoded: FULL trace mode only");
+  if ((s = sync_run(h)) != TOKENSIM_OK) return s;
+  SimStats st;
+  if ((s = copy_d2h(h, &st, h->P.stats + j, sizeof st)) != TOKENSIM_OK) return s;
+  *n_bytes = st.trace_b[worker];
+  if (n_samples) *n_samples = st.trace_n[worker];
+  if (!out || capacity == 0) return TOKENSIM_OK;
+  if (capacity < st.trace_b[worker]) return TOKENSIM_E_TRUNCATED;
+  if (st.trace_b[worker] &&
+      (s = copy_d2h(h, out, h->P.trace + (j * h->P.trace_nw + worker) * h->P.trace_cap, st.trace_b[worker])) != TOKENSIM_OK)
+    return s;
   return (st.flags & TOKENSIM_PT_TRACE_OVERFLOW) ? TOKENSIM_E_OVERFLOW : TOKENSIM_OK;
 }
 

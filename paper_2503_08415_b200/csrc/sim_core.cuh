@@ -24,6 +24,7 @@
 // P:456-457; max-memory-ratio admission P:460; compute simulator P:216.
 #pragma once
 #include "dev_common.cuh"
+#include "trace_codec.cuh"
 
 namespace ts {
 
@@ -663,7 +664,7 @@ struct HelperChan {
   u32 eprod, econs, pad0, pad1;  // block-event ring (allocations / frees to replay)
   u64 j;
   i64 t_final;
-  u64 dig, bns, peak, tn, digb;
+  u64 dig, bns, peak, tn, digb, tb;  // tb: FULL trace bytes (trace_codec.cuh)
 };
 // Block-event records of the helper mode (uint4): k, kind | count << 2, request id,
 // table slot | table position << 10.  kind 1: take `count` lowest free blocks into the slot's
@@ -864,6 +865,9 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   u64 tn = 0, bin = 0, acc_bns = 0;
   i64 bin_end = W;
   u32 acc_max = 0, acc_nit = 0;
+  FullEnc fe = {0, 0, 0, 0, 0, 0};  // FULL: the compressed stream (trace_codec.cuh)
+  unsigned char *const tbuf = reinterpret_cast<unsigned char *>(trc);
+  const u64 tcap_b = P.trace_cap * sizeof(tokensim_mem_sample);
   auto flush_bin = [&]() {
     if (tn < P.trace_cap) {
       if (lane == 0) {
@@ -1283,17 +1287,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               else break;
             }
           } else if (FULLT) {
-            if (lj && tn + lane < P.trace_cap) {
-              tokensim_mem_sample sm;
-              sm.t_ns = tsj;
-              sm.dur_ns = Tj;
-              sm.block_ns = blkj * (u64)Tj;
-              sm.blocks_max = (u32)blkj;
-              sm.n_iter = 1;
-              trc[tn + lane] = sm;
-            }
-            if (tn + J > P.trace_cap) flags |= TOKENSIM_PT_TRACE_OVERFLOW;
-            tn += J;
+            full_trace_put(fe, tbuf, tcap_b, J, tsj, tsj + Tj, blkj, flags);
           }
           if (!HELP) {
             const u64 blk_last = blk0 + Ktot;
@@ -1905,20 +1899,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         acc_max = max(acc_max, (u32)blocks);
       }
     } else if (FULLT) {
-      if (tn < P.trace_cap) {
-        if (lane == 0) {
-          tokensim_mem_sample s;
-          s.t_ns = ts;
-          s.dur_ns = T;
-          s.block_ns = blocks * (u64)T;
-          s.blocks_max = (u32)blocks;
-          s.n_iter = 1;
-          trc[tn] = s;
-        }
-      } else {
-        flags |= TOKENSIM_PT_TRACE_OVERFLOW;
-      }
-      ++tn;
+      full_trace_put(fe, tbuf, tcap_b, 1u, ts, te, blocks, flags);
     }
     t = te;
     ++k;
@@ -1948,6 +1929,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     bns = ch->bns;
     peak = ch->peak;
     tn = ch->tn;
+    fe.n = ch->tn;
+    fe.bytes = ch->tb;
     flags |= ch->tflags;
     __syncwarp();
     if (lane_id() == 0) ch->state = 0u;
@@ -1984,8 +1967,10 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     st.total_blocks = total;
     st.peak_blocks = peak;
     st.block_ns_sum = bns;
-    st.trace_n[0] = min(tn, P.trace_cap);
+    st.trace_n[0] = FULLT ? fe.n : min(tn, P.trace_cap);
     for (int q = 1; q < 8; ++q) st.trace_n[q] = 0;
+    st.trace_b[0] = FULLT ? fe.bytes : 0;
+    for (int q = 1; q < 8; ++q) st.trace_b[q] = 0;
     st.iter_n = min(k, P.it_cap);
     st.n_transfers = 0;
     st.transfer_bytes = 0;
@@ -2044,6 +2029,7 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
     u32 hint = 0, econs = 0;
     u64 dgb = 0;
     tokensim_mem_sample *trc = P.trace + (size_t)j * P.trace_nw * P.trace_cap;
+    FullEnc fe = {0, 0, 0, 0, 0, 0};
     tokensim_iter_record *itr = P.itrec + (size_t)j * P.it_cap;
     u64 dg = 0, bns = 0, peak = 0, tn = 0, bin = 0, acc_bns = 0;
     u32 tflags = 0, acc_max = 0, acc_nit = 0, cons = 0;
@@ -2214,17 +2200,8 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
               else break;
             }
           } else if (FULLT) {
-            if (v && tn + lane < P.trace_cap) {
-              tokensim_mem_sample sm;
-              sm.t_ns = ts;
-              sm.dur_ns = T;
-              sm.block_ns = blocks * (u64)T;
-              sm.blocks_max = (u32)blocks;
-              sm.n_iter = 1;
-              trc[tn + lane] = sm;
-            }
-            if (tn + m > P.trace_cap) tflags |= TOKENSIM_PT_TRACE_OVERFLOW;
-            tn += m;
+            full_trace_put(fe, reinterpret_cast<unsigned char *>(trc), P.trace_cap * sizeof(tokensim_mem_sample), m,
+                           ts, te, blocks, tflags);
           }
           e0 += m;
         }
@@ -2257,7 +2234,8 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
       ch->digb = digb;
       ch->bns = bsum;
       ch->peak = pk;
-      ch->tn = tn;
+      ch->tn = FULLT ? fe.n : tn;
+      ch->tb = fe.bytes;
       ch->tflags = tflags;
     }
     __threadfence_block();

@@ -28,6 +28,7 @@ struct TraceAcc {  // lane-uniform BINNED/FULL trace state of one worker
   u64 tn, bin, acc_bns;
   i64 bin_end;
   u32 acc_max, acc_nit;
+  FullEnc fe;  // FULL: the compressed stream (trace_codec.cuh)
 };
 
 __device__ __forceinline__ void trace_flush_bin(TraceAcc &A, tokensim_mem_sample *trc, u64 cap, i64 W, u32 &flags) {
@@ -71,20 +72,8 @@ __device__ __forceinline__ void trace_iter(TraceAcc &A, bool binned, bool full, 
       A.acc_max = max(A.acc_max, (u32)blocks);
     }
   } else if (full) {
-    if (A.tn < cap) {
-      if (lane_id() == 0) {
-        tokensim_mem_sample s;
-        s.t_ns = ts;
-        s.dur_ns = te - ts;
-        s.block_ns = blocks * (u64)(te - ts);
-        s.blocks_max = (u32)blocks;
-        s.n_iter = 1;
-        trc[A.tn] = s;
-      }
-    } else {
-      flags |= TOKENSIM_PT_TRACE_OVERFLOW;
-    }
-    ++A.tn;
+    full_trace_put(A.fe, reinterpret_cast<unsigned char *>(trc), cap * sizeof(tokensim_mem_sample), 1u, ts, te, blocks,
+                   flags);
   }
 }
 
@@ -112,17 +101,8 @@ __device__ __forceinline__ void trace_stretch(TraceAcc &A, bool binned, bool ful
       else break;
     }
   } else if (full) {
-    if (lj && A.tn + lane < cap) {
-      tokensim_mem_sample sm;
-      sm.t_ns = tsj;
-      sm.dur_ns = tej - tsj;
-      sm.block_ns = blkj * (u64)(tej - tsj);
-      sm.blocks_max = (u32)blkj;
-      sm.n_iter = 1;
-      trc[A.tn + lane] = sm;
-    }
-    if (A.tn + J > cap) flags |= TOKENSIM_PT_TRACE_OVERFLOW;
-    A.tn += J;
+    full_trace_put(A.fe, reinterpret_cast<unsigned char *>(trc), cap * sizeof(tokensim_mem_sample), J, tsj, tej, blkj,
+                   flags);
   }
 }
 
@@ -1111,9 +1091,12 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     st.total_blocks = totD;
     st.peak_blocks = peakD;
     st.block_ns_sum = bnsD;
-    st.trace_n[0] = min(TA[0].tn, P.trace_cap);
-    st.trace_n[1] = min(TA[1].tn, P.trace_cap);
+    st.trace_n[0] = FULLT ? TA[0].fe.n : min(TA[0].tn, P.trace_cap);
+    st.trace_n[1] = FULLT ? TA[1].fe.n : min(TA[1].tn, P.trace_cap);
     for (int q = 2; q < 8; ++q) st.trace_n[q] = 0;
+    st.trace_b[0] = TA[0].fe.bytes;
+    st.trace_b[1] = TA[1].fe.bytes;
+    for (int q = 2; q < 8; ++q) st.trace_b[q] = 0;
     st.iter_n = min(nit, P.it_cap);
     st.n_transfers = n_xfer;
     st.transfer_bytes = xbytes;

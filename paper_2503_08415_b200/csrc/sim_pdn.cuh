@@ -198,7 +198,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     #pragma unroll 1
     for (u32 x = lane; x < n; x += 32) reqx[x] = INF;
     if (lane == 0) {
-      const TraceAcc ta0 = {0, 0, 0, (i64)P.bin_ns, 0, 0};
+      const TraceAcc ta0 = {0, 0, 0, (i64)P.bin_ns, 0, 0, {0, 0, 0, 0, 0, 0}};
       for (u32 w = 0; w < X; ++w) {
         PScal s;
         s.t = INF;  // a prefill worker starts idle: a dispatch wakes it
@@ -1322,10 +1322,15 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     st.peak_blocks = peak;
     st.block_ns_sum = bns;
     for (u32 w = 0; w < PDN_MAXW; ++w) {
-      u64 tn = 0;
-      if (w < X) tn = M.ps[w].TA.tn;
-      else if (w < NW) tn = M.ds[w - X].TA.tn;
-      st.trace_n[w] = tn < P.trace_cap ? tn : P.trace_cap;
+      u64 tn = 0, fn = 0, fb = 0;
+      if (w < NW) {
+        const TraceAcc &ta = w < X ? M.ps[w].TA : M.ds[w - X].TA;
+        tn = ta.tn;
+        fn = ta.fe.n;
+        fb = ta.fe.bytes;
+      }
+      st.trace_n[w] = FULLT ? fn : (tn < P.trace_cap ? tn : P.trace_cap);
+      st.trace_b[w] = fb;
     }
     st.iter_n = kall < P.it_cap ? kall : P.it_cap;
     st.n_transfers = n_xfer;

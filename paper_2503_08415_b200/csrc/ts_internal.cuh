@@ -53,7 +53,8 @@ struct SimStats {
   i64 last_finish, t_final;
   u64 sched_d, block_d, req_d;
   u64 total_blocks, peak_blocks, block_ns_sum;
-  u64 trace_n[8];  // per worker (x + y <= 8 for a P/D node)
+  u64 trace_n[8];  // per worker (x + y <= 8 for a P/D node); FULL: records in the stream
+  u64 trace_b[8];  // FULL: bytes of each worker's compressed stream (trace_codec.cuh)
   u64 iter_n;
   u64 n_transfers, transfer_bytes;
   u64 ff_iters, ff_runs;  // iterations committed by fast-forward stretches, stretch count

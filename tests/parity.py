@@ -36,10 +36,17 @@ def oracle_points(cfg: si.SweepConfig, points: Iterable[int], want=("summary", "
         return dict(ex.map(_oracle_job, [(cfg, p, want) for p in points]))
 
 
-def compare_summary(g, o: dict, point: int) -> List[str]:
+TRACE_OVERFLOW = 1
+
+
+def compare_summary(g, o: dict, point: int, full_trace: bool = False) -> List[str]:
+    """full_trace: the CUDA path's FULL trace is a compressed stream with a byte budget, the
+    oracle keeps every sample; the overflow bit is then the CUDA side's own (see compare_trace)."""
     bad = []
     for f in EXACT_FIELDS:
         gv, ov = int(g[f]), int(o[f])
+        if f == "status_flags" and full_trace:
+            gv, ov = gv & ~TRACE_OVERFLOW, ov & ~TRACE_OVERFLOW
         if gv != ov:
             bad.append(f"point {point}: {f} gpu={gv} oracle={ov}")
     if int(g["t_final_ns"]) != int(o["t_final"]):
@@ -78,7 +85,11 @@ def compare_records(g: np.ndarray, o: np.ndarray, point: int) -> List[str]:
     return bad
 
 
-def compare_trace(g: np.ndarray, o: np.ndarray, point: int) -> List[str]:
+def compare_trace(g: np.ndarray, o: np.ndarray, point: int, prefix: bool = False) -> List[str]:
+    """prefix: the CUDA FULL stream overflowed its byte budget; it must hold exactly the
+    oracle's first len(g) samples."""
+    if prefix and len(g) <= len(o):
+        o = o[:len(g)]
     if len(g) != len(o):
         return [f"point {point}: trace length gpu={len(g)} oracle={len(o)}"]
     bad = []

@@ -39,13 +39,15 @@ def check_points(sw, cfg, points, records=True, trace=False, iters=False):
            (["iters"] if iters else [])
     ora = oracle_points(cfg, points, want=tuple(want))
     bad = []
+    full = cfg.options.trace_mode == si.FULL
     for p in points:
         o = ora[p]
-        bad += compare_summary(sw.summary(p), o["summary"], p)
+        g = sw.summary(p)
+        bad += compare_summary(g, o["summary"], p, full_trace=full)
         if records:
             bad += compare_records(sw.records(p), o["records"], p)
         if trace:
-            bad += compare_trace(sw.mem_trace(p), o["trace"][0], p)
+            bad += compare_trace(sw.mem_trace(p), o["trace"][0], p, prefix=full and bool(int(g["status_flags"]) & 1))
         if iters:
             bad += compare_iters(sw.iteration_trace(p), o["iters"], p)
     assert not bad, "\n".join(bad[:20])
@@ -229,12 +231,14 @@ def check_pd_points(sw, cfg, points, iters=False):
     nw = cfg.options.pd_prefill + cfg.options.pd_decode
     node = nw > 2 or cfg.options.node_loop
     bad = []
+    full = cfg.options.trace_mode == si.FULL
     for p in points:
         o = ora[p]
-        bad += compare_summary(sw.summary(p), o["summary"], p)
+        g = sw.summary(p)
+        bad += compare_summary(g, o["summary"], p, full_trace=full)
         bad += compare_records(sw.records(p), o["records"], p)
         for w in range(nw):
-            bad += compare_trace(sw.mem_trace(p, w), o["trace"][w], p)
+            bad += compare_trace(sw.mem_trace(p, w), o["trace"][w], p, prefix=full and bool(int(g["status_flags"]) & 1))
         prof = sw.point_profile(p)
         if (prof["n_transfers"], prof["transfer_bytes"]) != (o["summary"]["n_transfers"], o["summary"]["transfer_bytes"]):
             bad.append(f"point {p}: transfers gpu={prof['n_transfers']},{prof['transfer_bytes']} "
@@ -352,6 +356,42 @@ def test_huge_kv_pool_on_few_points(api, blocks):
                          [si.Policy()], w, si.Options(trace_mode=si.FULL))
     sw = run_gpu(api, cfg)
     check_points(sw, cfg, [0, 1], records=True, trace=True)
+
+
+def test_full_trace_codec_c3_points(api):
+    """The compressed FULL memory trace (delta + varint, trace_codec.cuh): whole C3
+    points (10k requests, up to ~1M iterations) fit a 6 MiB stream, decode to exactly the oracle's
+    per-iteration samples, and cost <= 6 B per iteration; the same for C1.  A small budget keeps
+    a prefix of whole iterations and reports E_OVERFLOW."""
+    base = si.c3()
+    # grid corners of C3's fast/slow hardware x capacities x policies, via a subset config
+    cfg = replace(si.subset(base, hws=[0, 5, 1535, 1530, 767, 1000], policies=[0, 1, 2]),
+                  options=si.Options(trace_mode=si.FULL, trace_cap_bytes=6 << 20))
+    sw = run_gpu(api, cfg)
+    pts = list(range(cfg.num_points))
+    check_points(sw, cfg, pts, records=False, trace=True)
+    s = sw.summaries()
+    assert not (s["status_flags"] & 1).any()
+    bpi = []
+    for p in pts:
+        enc, n = sw.mem_trace_encoded(p)
+        assert n == int(s["n_iterations"][p])
+        bpi.append(len(enc) / n)
+    assert max(bpi) <= 6.0, bpi
+    c1 = replace(si.c1(), options=si.Options(trace_mode=si.FULL))
+    sw1 = run_gpu(api, c1)
+    check_points(sw1, c1, [0], records=True, trace=True)
+    enc, n = sw1.mem_trace_encoded(0)
+    assert len(enc) <= 6 * n
+    # a 4 KiB budget: a prefix of whole iterations, E_OVERFLOW, still the oracle's samples
+    c1s = replace(si.c1(), options=si.Options(trace_mode=si.FULL, trace_cap_bytes=4096))
+    sw2 = run_gpu(api, c1s)
+    g = sw2.summary(0)
+    assert int(g["status_flags"]) & 1
+    tr = sw2.mem_trace(0)
+    enc, n = sw2.mem_trace_encoded(0)
+    assert 0 < len(tr) == n < int(g["n_iterations"]) and len(enc) <= 4096
+    check_points(sw2, c1s, [0], records=True, trace=True)
 
 
 def test_large_point_summary_scratch_path(api):

@@ -25,6 +25,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--points", type=int, default=0, help="run only the first N points")
+ap.add_argument("--dump", default="", help="save per-point iterations / cycles / profile to this .npz")
 a = ap.parse_args()
 cfg = si.PRESETS[a.config]()
 sw = P.Sweep(cfg)
@@ -52,6 +53,15 @@ if os.environ.get("PROFILE_POINTS"):
     X = np.stack([normal, st, ri], 1)
     coef, *_ = np.linalg.lstsq(X, cy, rcond=None)
     print("cycles ~ %.0f/normal-iter + %.0f/stretch + %.2f/req-iter" % tuple(coef))
+    if a.dump:
+        np.savez(a.dump, iters=it, ff=ff, stretches=st, cycles=cy, ri=ri,
+                 cycles_ff=np.array([x["cycles_ff"] for x in prof], dtype=np.float64),
+                 cycles_normal=np.array([x["cycles_normal"] for x in prof], dtype=np.float64),
+                 cycles_ff_failed=np.array([x["cycles_ff_failed"] for x in prof], dtype=np.float64),
+                 stretch_phase=np.array([x["stretch_phase_cycles"] for x in prof], dtype=np.float64),
+                 normal_phase=np.array([x["normal_phase_cycles"] for x in prof], dtype=np.float64),
+                 ff_cut=np.array([x["ff_cut"] for x in prof], dtype=np.float64),
+                 preempt=s["n_preemptions"].astype(np.float64), sim_ms=info["ms_sim"])
     cuts = np.array([x["ff_cut"] for x in prof], dtype=np.float64).sum(0)
     print("all points: stretches ended by (memory / finish / arrival / head / 32+other):", cuts.astype(int).tolist())
     if os.environ.get("PROFILE_GROUPS"):  # worst point of each group of G consecutive points
