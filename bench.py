@@ -50,8 +50,19 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # the HBM reference line is the 44 B/request-iteration hot record (read 24 B, write 20 B).
 ALG_OPS_PER_UNIT = 10
 HBM_BYTES_PER_UNIT = 44
-# B200: 148 SMs x 128 INT32/FP32 lanes x 1965 MHz max SM clock (B200_PROFILING.md table)
-ALU_PEAK_GOPS = 148 * 128 * 1.965
+# B200 INT32 ALU peak: MEASURED by tools/alu_peak.cu (profiles/r2/alu_peak.json, 8 independent add
+# chains per thread at full occupancy); fallback, if that file is missing, the nominal
+# 148 SMs x 128 INT32 lanes x 1965 MHz
+ALU_PEAK_PATH = os.path.join(ROOT, "profiles", "r2", "alu_peak.json")
+
+
+def alu_peak():
+    try:
+        d = json.load(open(ALU_PEAK_PATH))
+        return float(d["int32_peak_gops"]), float(d["warp_issue_peak_gwips"]), \
+            "measured: tools/alu_peak.cu INT32 add/xor lane-ops at full occupancy (profiles/r2/alu_peak.json)"
+    except Exception:
+        return 148 * 128 * 1.965, 148 * 4 * 1.965, "nominal: 148 SMs x 128 lanes x 1965 MHz (no measurement found)"
 
 
 def env_rank():
@@ -319,6 +330,7 @@ def run_ours(args):
     e2e_value = ri_all / (float(e2e_t[0]) / 1e3)
 
     peaks = measured_peaks()
+    alu_gops, issue_gwips, alu_src = alu_peak()
     sim_avg_s = statistics.mean(sim_ms) / 1e3
     achieved_gops = ALG_OPS_PER_UNIT * ri_local / sim_avg_s / 1e9
     hbm_peak = peaks.get("hbm_gbs")
@@ -335,7 +347,7 @@ def run_ours(args):
             wi = nc.get("warp_instructions")
             if wi:
                 ach = wi / sim_avg_s / 1e9
-                pk = 148 * 4 * 1.965
+                pk = issue_gwips
                 issue_line = {"warp_instructions_per_launch": wi, "achieved_gwips": ach, "peak_gwips": pk,
                               "frac": ach / pk, "no_instruction_stall_pct": nc.get("no_instruction_stall_pct_of_samples"),
                               "source": "ncu warp instructions of one launch (profiles/dram_<config>.json)"}
@@ -357,11 +369,11 @@ def run_ours(args):
                        "request_iterations_per_step": ri_all, "parallelism": f"points sharded p mod {world}",
                        "l2": "flushed (256 MiB write) between timed steps",
                        "step": "workload_kernel + sim_kernel + summary_kernel" + (" + NCCL all-gather" if world > 1 else "")},
-            "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": ALU_PEAK_GOPS, "unit": "Gop/s",
-                         "frac": achieved_gops / ALU_PEAK_GOPS, "traffic": traffic,
+            "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": alu_gops, "unit": "Gop/s",
+                         "frac": achieved_gops / alu_gops, "traffic": traffic,
                          "kernel": "sim_kernel", "kernel_ms": statistics.mean(sim_ms),
                          "per_unit": f"{ALG_OPS_PER_UNIT} lane-ops per request-iteration (SURVEY §8(d))",
-                         "peak_source": "148 SMs x 128 lanes x 1965 MHz (B200_PROFILING.md nominal table; DESIGN.md)",
+                         "peak_source": alu_src,
                          "hbm_line": {"bytes_per_unit": HBM_BYTES_PER_UNIT, "achieved_gbs": hbm_ach,
                                       "peak_gbs": hbm_peak, "frac": (hbm_ach / hbm_peak) if hbm_peak else None,
                                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
@@ -420,17 +432,25 @@ def run_emulate(args):
         return statistics.median(ts), s
 
     t1, s_all = timed(0, n_pts, 1)
+    info1 = sw.run_info()
     ri_total = int(s_all["n_request_iterations"].sum())
     iters = s_all["n_iterations"].astype(np.int64)
     curve = []
     G = 1
+    gs = [int(x) for x in args.emulate_gs.split(",")] if args.emulate_gs else None
     while G <= args.emulate_ranks:
+        if gs is not None and G not in gs:
+            G *= 2
+            continue
         per = []
         for r in range(G):
             t, s = (t1, s_all) if G == 1 else timed(r, n_pts, G)
+            inf = info1 if G == 1 else sw.run_info()
             per.append({"rank": r, "ms": t, "points": int(len(s)),
                         "request_iterations": int(s["n_request_iterations"].sum()),
-                        "max_iterations": int(s["n_iterations"].max()) if len(s) else 0})
+                        "max_iterations": int(s["n_iterations"].max()) if len(s) else 0,
+                        "helper_mode": inf["helper_mode"], "n_heads": inf["n_heads"],
+                        "grid": [inf["sim_blocks"], inf["sim_warps_per_block"]]})
         tmax = max(p["ms"] for p in per)
         curve.append({"gpus": G, "ms_per_step": tmax, "value": ri_total / (tmax / 1e3),
                       "speedup": t1 / tmax, "efficiency": t1 / tmax / G, "ranks": per})
@@ -467,6 +487,7 @@ def main():
                     help="one GPU: measure the strong-scaling curve for 1, 2, 4, ... G ranks and the chain floor")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--floor-points", type=int, default=4)
+    ap.add_argument("--emulate-gs", default="", help="with --emulate-ranks: only these G (comma list)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--reference-budget", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

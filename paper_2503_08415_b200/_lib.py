@@ -84,7 +84,7 @@ class PointProfile(C.Structure):
 class RunInfo(C.Structure):
     _fields_ = [("ms_workload", f64), ("ms_sim", f64), ("ms_summary", f64), ("n_launches", u32),
                 ("sim_blocks", u32), ("sim_warps_per_block", u32), ("smem_per_warp", u32), ("n_run", u64),
-                ("h2d_bytes", u64), ("workspace_bytes", u64)]
+                ("h2d_bytes", u64), ("workspace_bytes", u64), ("helper_mode", u32), ("n_heads", u32)]
 
 
 RECORD_DTYPE = np.dtype([("ttft_ns", "<i8"), ("e2e_ns", "<i8"), ("mtpot_ns", "<i8"), ("n_preempt", "<u2"),

@@ -34,7 +34,8 @@ const uint32_t kOutputThr[7] = {429496730u, 773094113u, 1159641170u, 1717986918u
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, scratch, ring, fifo, pdn, pdn_per_warp,
+  size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, sched, scratch, ring, fifo, pdn,
+      pdn_per_warp,
       mr_conv, mr_base, mr_nr, mr_ntot, mr_a0, mr_p0, mr_o0, mr, mr_per_warp, evlog, itlog,
       total;
   u64 n_run;
@@ -453,6 +454,17 @@ static bool range_ok(const tokensim_sweep *h, u64 begin, u64 end, u64 stride) {
 }
 static u64 count_run(u64 begin, u64 end, u64 stride) { return end > begin ? (end - begin + stride - 1) / stride : 0; }
 
+// The lean unified kernel runs one point per CTA with a helper warp (variant 0) when a run is
+// latency-bound: at most kHelperPointsPerSm points per SM (a point's serial chain, not the SM's
+// issue rate, then sets the kernel time: DESIGN.md §7).  TOKENSIM_HELPER=0/1 overrides (A/B).
+constexpr u64 kHelperPointsPerSm = 4;
+static bool helper_run(const tokensim_sweep *h, u64 n_run, int sm_count) {
+  if (h->full || h->opt.topology == TOKENSIM_PD_PAIR) return false;
+  if (!helper_fits(h->smem_per_warp(), h->nwords_max)) return false;
+  if (const char *e = getenv("TOKENSIM_HELPER")) return atoi(e) != 0;
+  return n_run <= kHelperPointsPerSm * (u64)sm_count;
+}
+
 static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int blocks_per_sm_limit) {
   Layout L{};
   const u64 n = h->n_slots();
@@ -468,7 +480,7 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   // fewer points than SMs x wpb: spread them one warp per SM first (each point is a serial
   // latency-bound chain; co-resident warps would only share the SM's LSU/MIO pipes)
   if (const char *e = getenv("TOKENSIM_WPB")) wpb = (u32)std::max(1, std::min(4, atoi(e)));
-  else if ((u64)n_run <= (u64)sm_count) wpb = 1;
+  else if ((u64)n_run <= (u64)sm_count || helper_run(h, n_run, sm_count)) wpb = 1;
   u32 bps = (u32)std::max<size_t>(1, (227 * 1024) / (per_warp * wpb));
   bps = std::min<u32>(bps, 16);
   if (blocks_per_sm_limit > 0) bps = std::min<u32>(bps, (u32)blocks_per_sm_limit);
@@ -497,6 +509,7 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   L.bt = take((size_t)L.warps_total * h->bt_tables() * h->cap * h->bt_len * 4);
   L.order = take(n_run * 4 + 4);
   L.queue = take(256);
+  L.sched = take((513 + 1024) * 4);
   L.scratch = take(n > kSummarySmemKeys ? n_run * n * 8 : 0);
   L.ring = take(pair ? (size_t)L.warps_total * h->max_total_blocks * 4 : 0);
   L.fifo = take(pair ? (size_t)L.warps_total * n * 32 : 0);
@@ -610,8 +623,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   const size_t per_warp = h->smem_per_warp();
   Layout L0 = make_layout(h, n_run, sms, 0);
   int occ = 0;
-  e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general,
-                                L0.wpb > 1 || (u64)L0.blocks > (u64)sms || !helper_fits(per_warp, h->nwords_max)),
+  const bool helper = L0.wpb == 1 && helper_run(h, n_run, sms);
+  e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general, !helper),
                     (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, h->nwords_max, &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
@@ -692,6 +705,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.n_run = n_run;
   P.order = reinterpret_cast<const u32 *>(ws + L.order);
   P.queue = reinterpret_cast<u32 *>(ws + L.queue);
+  P.sched = reinterpret_cast<u32 *>(ws + L.sched);
+  P.helper_mode = helper ? 1u : 0u;
   P.rec = reinterpret_cast<tokensim_request_record *>(ws + L.rec);
   P.stats = reinterpret_cast<SimStats *>(ws + L.stats);
   P.trace = reinterpret_cast<tokensim_mem_sample *>(ws + L.trace);
@@ -764,11 +779,21 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
       return a.first > b.first;
     });
     for (u64 j = 0; j < n_run; ++j) order[j] = est[j].second;
+    // Heads (helper mode with more points than SMs): TOKENSIM_HEADS=K gives the K longest-
+    // estimated points an SM each (the other CTAs on a head's SM leave).  Off by default: with
+    // one CTA per point the leaving CTAs' share of the queue is serialised onto the others, and
+    // C3 / C4 at 8 emulated GPUs measured slower for every K > 0.
+    P.n_heads = 0;
+    if (helper && n_run > (u64)sms)
+      if (const char *ev = getenv("TOKENSIM_HEADS"))
+        P.n_heads = (u32)std::min<long>(std::max(0, atoi(ev)), (long)std::min<u64>((u64)sms / 2, 1024));
   }
   e = cudaMemcpyAsync(ws + L.order, order.data(), (n_run + 1) * 4, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(h, e, "cudaMemcpyAsync(order)");
   e = cudaMemsetAsync(ws + L.queue, 0, 256, st);
   if (e != cudaSuccess) return cuda_fail(h, e, "cudaMemsetAsync(queue)");
+  e = cudaMemsetAsync(ws + L.sched, 0, (513 + 1024) * 4, st);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMemsetAsync(sched)");
   h->n_launches = 0;
   cudaEventRecord(h->ev[0], st);
   if (n_run > 0 && !trace_mode) {
@@ -1104,6 +1129,8 @@ tokensim_status tokensim_get_run_info(const tokensim_sweep *hc, tokensim_run_inf
   out->n_run = h->n_run;
   out->h2d_bytes = h->h2d_bytes;
   out->workspace_bytes = h->lay.total;
+  out->helper_mode = h->P.helper_mode;
+  out->n_heads = h->P.n_heads;
   return TOKENSIM_OK;
 }
 

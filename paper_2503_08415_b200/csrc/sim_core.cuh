@@ -2276,10 +2276,68 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   const WarpSmem S = carve(smem_raw + (HELPK ? 0 : wib) * per_warp, CAP);
   const u32 gwarp = HELPK ? blockIdx.x : blockIdx.x * (blockDim.x >> 5) + wib;
   u32 *bt = P.bt + (size_t)gwarp * P.bt_tables * CAP * P.bt_len;
-  while (true) {
+  // Heads (variant 0, strong scaling): the n_heads longest-estimated points each run on an SM
+  // of their own -- the first CTA to arrive on an SM takes a head ticket, and the other CTAs on
+  // a head's SM leave at once, so the longest serial chains run at their alone speed while the
+  // rest of the queue is shared by the other SMs.  Every queue position is claimed exactly once
+  // (head positions by atomicCAS on their claim word), so no point is lost or repeated.
+  u32 head_qi = 0xffffffffu;
+  bool leave = false;
+  if constexpr (HELPK) {
+    const u32 NH = P.n_heads;
+    if (NH) {
+      u32 h = 0xffffffffu, lv = 0;
+      if (lane == 0) {
+        u32 smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        smid &= 255u;
+        u32 *cnt = P.sched, *state = P.sched + 256, *ticket = P.sched + 512, *claim = P.sched + 513;
+        if (atomicAdd(&cnt[smid], 1u) == 0u) {  // first CTA on this SM
+          while (true) {
+            const u32 t = atomicAdd(ticket, 1u);
+            if (t >= NH) break;
+            if (atomicCAS(&claim[t], 0u, 1u) == 0u) {
+              h = t;
+              break;
+            }
+          }
+          atomicExch(&state[smid], h != 0xffffffffu ? 2u : 1u);
+        } else {
+          u32 f;
+          while ((f = atomicAdd(&state[smid], 0u)) == 0u) {
+          }
+          lv = f == 2u;
+        }
+      }
+      head_qi = __shfl_sync(FULLMASK, h, 0);
+      leave = __shfl_sync(FULLMASK, lv, 0) != 0u;
+    }
+  }
+  while (!leave) {
     u32 qi = 0;
-    if (lane == 0) qi = atomicAdd(P.queue, 1u);
-    qi = __shfl_sync(FULLMASK, qi, 0);
+    if (head_qi != 0xffffffffu) {
+      qi = head_qi;
+      head_qi = 0xffffffffu;
+    } else {
+      if (lane == 0) {
+        if constexpr (HELPK) {
+          const u32 NH = P.n_heads;
+          qi = NH + atomicAdd(P.queue, 1u);
+          if (NH && (u64)qi >= P.n_run) {  // leftovers: head positions no first CTA claimed
+            qi = 0xffffffffu;
+            u32 *claim = P.sched + 513;
+            for (u32 t = 0; t < NH; ++t)
+              if (atomicCAS(&claim[t], 0u, 1u) == 0u) {
+                qi = t;
+                break;
+              }
+          }
+        } else {
+          qi = atomicAdd(P.queue, 1u);
+        }
+      }
+      qi = __shfl_sync(FULLMASK, qi, 0);
+    }
     if ((u64)qi >= P.n_run) break;
     const u64 j = P.order[qi];
     if constexpr (HELPK) {  // hand the point to the helper

@@ -122,7 +122,10 @@ struct SweepParams {
   u64 pdn_bytes_per_warp;
   u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
   u32 full, all_p2;                       // 1: the full kernel variant (sim_full.cu); every block size a power of two
-  u32 n_sms, pad5;                        // SMs of the device (launch choice of the compact lean kernel)
+  u32 n_sms, helper_mode;                 // SMs of the device; 1: lean kernel with a helper warp per point (variant 0)
+  u32 n_heads, pad6;                      // variant 0: the first n_heads points (LPT order) each get an SM alone
+  u32 *sched;                             // variant 0 with heads: per-SM arrival counts [256], SM states [256],
+                                          // head ticket [1], head claims [n_heads] (zeroed per run)
   u32 link_mode, pad2;                    // NEXT-4: TOKENSIM_LINK_SEQUENTIAL | PRELOAD
   u64 preload_buf;                        // preload buffer bytes
   // NEXT-2 multi-round conversations + memory cache.  With multi_round, n_req = 7 * n_conv is
@@ -186,11 +189,9 @@ inline int sim_variant(bool full, bool pd, bool pd_general, bool multi_warp = fa
 }
 inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                               cudaStream_t st) {
-  // TOKENSIM_HELPER=1 (A/B experiments): the helper-warp lean kernel even with several CTAs per SM
-  const bool force_helper = warps_per_block == 1 && getenv("TOKENSIM_HELPER") != nullptr;
+  (void)blocks;
   switch (sim_variant(p.full != 0, p.topology == TOKENSIM_PD_PAIR, p.pd_general != 0,
-                      !force_helper && (warps_per_block > 1 || (u64)blocks > (u64)p.n_sms ||
-                                        !helper_fits(smem, p.nwords_max)))) {
+                      !(p.helper_mode && warps_per_block == 1 && helper_fits(smem, p.nwords_max)))) {
     case 0: return launch_sim_base(p, cap, warps_per_block, blocks, smem, st);
     case 4: return launch_sim_base_c(p, cap, warps_per_block, blocks, smem, st);
     case 1: return launch_sim_full(p, cap, warps_per_block, blocks, smem, st);

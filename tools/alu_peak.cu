@@ -30,8 +30,9 @@ __global__ void __launch_bounds__(1024) alu_kernel(unsigned *out, unsigned seed,
                      : "+r"(x0), "+r"(x1), "+r"(x2), "+r"(x3), "+r"(x4), "+r"(x5), "+r"(x6), "+r"(x7)
                      : "r"(y));
       } else if (KIND == 1) {
-        asm volatile("xor.b32 %0, %0, %8;\n\txor.b32 %1, %1, %8;\n\txor.b32 %2, %2, %8;\n\txor.b32 %3, %3, %8;\n\t"
-                     "xor.b32 %4, %4, %8;\n\txor.b32 %5, %5, %8;\n\txor.b32 %6, %6, %8;\n\txor.b32 %7, %7, %8;"
+        // x_i ^= x_{i+1}: a rotating dependency the compiler cannot cancel (x ^ y ^ y = x)
+        asm volatile("xor.b32 %0, %0, %1;\n\txor.b32 %1, %1, %2;\n\txor.b32 %2, %2, %3;\n\txor.b32 %3, %3, %4;\n\t"
+                     "xor.b32 %4, %4, %5;\n\txor.b32 %5, %5, %6;\n\txor.b32 %6, %6, %7;\n\txor.b32 %7, %7, %8;"
                      : "+r"(x0), "+r"(x1), "+r"(x2), "+r"(x3), "+r"(x4), "+r"(x5), "+r"(x6), "+r"(x7)
                      : "r"(y));
       } else {

@@ -26,12 +26,16 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--points", type=int, default=0, help="run only the first N points")
 ap.add_argument("--dump", default="", help="save per-point iterations / cycles / profile to this .npz")
+ap.add_argument("--only", type=int, default=-1, help="run this one point alone (one warp on one SM)")
 a = ap.parse_args()
 cfg = si.PRESETS[a.config]()
 sw = P.Sweep(cfg)
 end = a.points or sw.num_points
+beg = 0
+if a.only >= 0:
+    beg, end = a.only, a.only + 1
 for _ in range(a.reps):
-    sw.run(0, end, 1)
+    sw.run(beg, end, 1)
     torch.cuda.synchronize()
     info = sw.run_info()
     s = sw.summaries()
@@ -40,7 +44,7 @@ for _ in range(a.reps):
           "grid", info["sim_blocks"], "x", info["sim_warps_per_block"], "smem/warp", info["smem_per_warp"])
 if os.environ.get("PROFILE_POINTS"):
     import numpy as np
-    prof = [sw.point_profile(p) for p in range(end)]
+    prof = [sw.point_profile(p) for p in range(beg, end)]
     it = np.array([x["n_iterations"] for x in prof], dtype=np.float64)
     ff = np.array([x["ff_iterations"] for x in prof], dtype=np.float64)
     st = np.array([x["ff_stretches"] for x in prof], dtype=np.float64)
@@ -71,6 +75,8 @@ if os.environ.get("PROFILE_POINTS"):
         order = np.argsort(-cy)[:6]
     for p in order:
         x = prof[p]
+        if a.only >= 0:
+            print("  (point", a.only, "alone)")
         nn = max(1, x["n_iterations"] - x["ff_iterations"])
         print("  point", p, "cycles %.3e" % cy[p], "iters", int(it[p]), "ff", int(ff[p]), "stretches", int(st[p]),
               "req-its", int(ri[p]), "preempt", int(s["n_preemptions"][p]),
