@@ -677,6 +677,10 @@ template <int CAP, bool FULL, bool P2>
 __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S, u32 *bt,
                                  volatile HelperChan *ch = nullptr) {
   constexpr bool HELP = TS_HELPER_WARP && !FULL;
+  // Extended stretches (carried stretch state, up to 64 iterations per stretch) only in the
+  // latency-bound helper-warp kernel: they shorten a lone point's chain, but at 8 warps per SM
+  // the larger hot code costs more in instruction fetch than it saves (DESIGN.md §8 A/B log).
+  constexpr bool XS = HELP;
   static_assert(CAP % 32 == 0 && CAP <= 1024, "CAP");
   const u32 lane = lane_id();
   const u32 ltm = lanemask_lt();
@@ -731,6 +735,14 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   u64 nfree = total;
   u32 hint = 0;
   u32 rmin = 0;  // min rem over R after the last commit (0 when unknown / R empty)
+  // Stretch state carried from one stretch to the next (valid only between back-to-back
+  // stretches; any normal iteration clears it): C_d = sum(ctx + 1) over R and, on lane r < bs,
+  // the number of running slots whose next block boundary is r iterations ahead (j0 = -ctx mod
+  // bs).  A stretch of J iterations rotates that histogram by J and drops its finished slots, so
+  // the next stretch starts without a pass over R (block sizes <= 32 only).
+  bool inc_ok = false;
+  u64 inc_cd = 0;
+  u32 inc_h = 0;  // lane r: running slots of residue class r
   // CHUNKED (NEXT-3b): the budget runs out at the last prefill entry of an iteration, so at most
   // one prefill is in progress and it is the last entry of R (reading R-N3b): xdone of xtgt done
   bool hx = false;
@@ -1014,42 +1026,52 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           quiet = false;
       }
       if (quiet) {
-        // pass over R: C_d(0), min rem, and the needs histogram by iteration offset (lane j
-        // <-> iteration k+j).  A slot needs a block at offsets j = j0 (mod bs), j0 = -ctx mod bs,
-        // so n_j = cnt[j mod bs]: count slots per j0 with match_any (no atomics).
-        u64 cdp = 0;
-        u32 rmn = 0xffffffffu;
-        S.scratch[lane] = 0;
-        S.scratch[32 + lane] = 0;
-        __syncwarp();
-        #pragma unroll 1
-        for (u32 b0 = 0; b0 < nR; b0 += 32) {
-          const u32 jj = b0 + lane;
-          u32 key = 64u + lane;
-          if (jj < nR) {
-            const u32 c = S.ctx[jj];
-            cdp += c + 1;
-            rmn = min(rmn, S.rem[jj]);
-            const u32 r = B.mod(c);
-            const u32 j0 = r ? B.bs - r : 0u;
-            if (j0 < 32) key = j0;
-          }
-          const u32 peers = __match_any_sync(FULLMASK, key);
-          u32 old = 0;
-          if (key < 32 && (peers & ltm) == 0u) {
-            old = S.scratch[key];
-            S.scratch[key] = old + __popc(peers);
-            S.scratch[32 + key] = peers;  // slot positions of this residue (meaningful if nR <= 32)
-          }
-          // rank of the slot among the slots of its residue class, in position order (= its
-          // place among the requesters of every iteration in which that class needs blocks)
-          const u32 rbase = __shfl_sync(FULLMASK, old, (u32)(__ffs(peers) - 1));
-          if (key < 32) S.req_pt[jj] = rbase + __popc(peers & ltm);
+        // C_d(0), min rem, and the needs histogram by iteration offset (lane j <-> iteration
+        // k+j).  A slot needs a block at offsets j = j0 (mod bs), j0 = -ctx mod bs, so
+        // n_j = cnt[j mod bs].  Right after another stretch all three are carried over (inc_*);
+        // otherwise one pass over R counts slots per j0 with match_any (no atomics).
+        u64 Cd0;
+        u32 rm, hcl;
+        if (XS && inc_ok) {
+          Cd0 = inc_cd;
+          rm = rmin;
+          hcl = inc_h;
+        } else {
+          u64 cdp = 0;
+          u32 rmn = 0xffffffffu;
+          S.scratch[lane] = 0;
+          S.scratch[32 + lane] = 0;
           __syncwarp();
+          #pragma unroll 1
+          for (u32 b0 = 0; b0 < nR; b0 += 32) {
+            const u32 jj = b0 + lane;
+            u32 key = 64u + lane;
+            if (jj < nR) {
+              const u32 c = S.ctx[jj];
+              cdp += c + 1;
+              rmn = min(rmn, S.rem[jj]);
+              const u32 r = B.mod(c);
+              const u32 j0 = r ? B.bs - r : 0u;
+              if (j0 < 32) key = j0;
+            }
+            const u32 peers = __match_any_sync(FULLMASK, key);
+            u32 old = 0;
+            if (key < 32 && (peers & ltm) == 0u) {
+              old = S.scratch[key];
+              S.scratch[key] = old + __popc(peers);
+              S.scratch[32 + key] = peers;  // slot positions of this residue (meaningful if nR <= 32)
+            }
+            // rank of the slot among the slots of its residue class, in position order (= its
+            // place among the requesters of every iteration in which that class needs blocks)
+            const u32 rbase = __shfl_sync(FULLMASK, old, (u32)(__ffs(peers) - 1));
+            if (key < 32) S.req_pt[jj] = rbase + __popc(peers & ltm);
+            __syncwarp();
+          }
+          Cd0 = warp_sum64(cdp);
+          rm = __reduce_min_sync(FULLMASK, rmn);
+          hcl = XS ? S.scratch[lane] : S.scratch[B.bs >= 32 ? lane : B.mod(lane)];
         }
-        const u64 Cd0 = warp_sum64(cdp);
-        const u32 rm = __reduce_min_sync(FULLMASK, rmn);
-        const u32 nj = S.scratch[B.bs >= 32 ? lane : B.mod(lane)];
+        const u32 nj = XS ? __shfl_sync(FULLMASK, hcl, B.bs >= 32 ? lane : B.mod(lane)) : hcl;
         const u32 Aj = scan_incl(nj);  // cumulative blocks allocated through iteration k+lane
         PH(0);
         // lane-parallel cost of iteration k+lane: D = nR decodes, C_d grows by nR per iteration
@@ -1086,13 +1108,34 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           }
         }
         const u32 okm = __ballot_sync(FULLMASK, ok);
-        const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+        u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+        // Second half (iterations k+32+lane, block sizes <= 32 only so the needs histogram
+        // covers them): evaluated only when all 32 of the first half pass, so a stretch of up to
+        // 64 iterations costs one pass over R, one set of slot updates and one log publication
+        // instead of two.  Values of iteration j >= 32 are the *1 registers on lane j - 32.
+        u32 nj1 = 0, Aj1 = 0;
+        u64 Cdj1 = 0;
+        i64 Tj1 = 0, tej1 = 0, tsj1 = 0;
+        if (XS && J == 32 && B.bs <= 32u) {
+          nj1 = __shfl_sync(FULLMASK, hcl, B.mod(32u + lane) & 31u);
+          Aj1 = __shfl_sync(FULLMASK, Aj, 31) + scan_incl(nj1);
+          Cdj1 = Cd0 + (u64)(32u + lane) * nR;
+          Tj1 = iter_time_ns(K, 0, 0, 0, nR, Cdj1, 0);
+          tej1 = __shfl_sync(FULLMASK, tej, 31) + scan_incl_i64(Tj1);
+          tsj1 = tej1 - Tj1;
+          bool ok1 = ((u64)Aj1 <= nfree) && (Aj1 <= (u32)CAP) && (32u + lane < rm);
+          if (P.horizon >= 0 && tsj1 >= P.horizon) ok1 = false;
+          if (nQ == 0 && adm == arr && more && tsj1 >= a_next) ok1 = false;
+          const u32 okm1 = __ballot_sync(FULLMASK, ok1);
+          J = 32u + ((~okm1 == 0u) ? 32u : (u32)(__ffs(~okm1) - 1));
+        }
+        const bool two = XS && J > 32u;
         if (!TS_PROFILE) {
         } else if (J < 2) {
           const u32 w = __shfl_sync(FULLMASK, why, J);
           ffr[(w & 1u) ? 1 : (w & 4u) ? 2 : (w & 8u) ? 3 : 4] += 1;
         } else {  // what ended a stretch: memory / a finish / an arrival / the head / 32 or other
-          const u32 w = J < 32 ? __shfl_sync(FULLMASK, why, J) : 0u;
+          const u32 w = J < 32 ? __shfl_sync(FULLMASK, why, J) : 0u;  // (second-half cuts: "other")
           ffc[(w & 1u) ? 0 : (w & 2u) ? 1 : (w & 4u) ? 2 : (w & 8u) ? 3 : 4] += 1;
         }
         // a stretch cut short by memory will not grow until blocks come back: remember the level
@@ -1102,10 +1145,10 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           ff_mem_k = k + 4;  // the needs pattern shifts with the ctx residues: retry soon anyway
         }
         if (J >= 2) {
-          const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
+          const u32 Ktot = __shfl_sync(FULLMASK, two ? Aj1 : Aj, (J - 1) & 31u);
           PH(1);
           bool done_alloc = Ktot == 0;
-          if (!HELP && !done_alloc && nR <= 32 && Ktot <= 32 && hint < nwords) {
+          if (!HELP && !done_alloc && !two && nR <= 32 && Ktot <= 32 && hint < nwords) {
             // fused small case: lane o takes the o-th lowest free block of the 32-word window at
             // the hint and serves order index o = (iteration jb, r-th slot of jb's residue class)
             const u32 wi = hint + lane;
@@ -1166,8 +1209,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               }
               ev_reserve(L, Ktot);
             }
-            const u32 excl = Aj - nj;
-            const u32 nrep = (32 + B.bs - 1) / B.bs;
+            const u32 excl = Aj - nj, excl1 = Aj1 - nj1;
+            const u32 nrep = ((XS ? J : 32u) + B.bs - 1) / B.bs;
             #pragma unroll 1
             for (u32 b0 = 0; b0 < nR; b0 += 32) {
               const u32 jj = b0 + lane;
@@ -1178,7 +1221,9 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               u32 jx = r ? B.bs - r : 0u;
               #pragma unroll 1
               for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
-                const u32 ex = __shfl_sync(FULLMASK, excl, jx & 31u);
+                const u32 ex0 = __shfl_sync(FULLMASK, excl, jx & 31u);
+                const u32 ex1 = two ? __shfl_sync(FULLMASK, excl1, jx & 31u) : 0u;  // (uniform branch)
+                const u32 ex = jx < 32u ? ex0 : ex1;
                 if (in && jx < J) {
                   const u32 o = ex + rank;
                   if (HELP) {
@@ -1199,14 +1244,20 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const u64 klast = k + J - 1;
           PH(2);
           // slot updates for J decode iterations; requests reaching rem == 0 finish in the last
-          const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
-          const i64 tsl = __shfl_sync(FULLMASK, tsj, J - 1);
-          const bool lj = lane < J;
+          const i64 tend = __shfl_sync(FULLMASK, two ? tej1 : tej, (J - 1) & 31u);
+          const i64 tsl = __shfl_sync(FULLMASK, two ? tsj1 : tsj, (J - 1) & 31u);
+          const bool lj = lane < J;               // first-half iterations of the stretch
+          const bool lj1 = two && 32u + lane < J;  // second-half iterations
           // the largest gap of the stretch is its last iteration's: T_j is nondecreasing in j
           // (only C_d grows, and every rounded product, sum, fmax and floor in the cost model is
           // monotone in it with nonnegative coefficients), so max_{j<J} T_j = T_{J-1}
           const i64 tmax = tend - tsl;
           u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
+          // carried state: every slot advanced J tokens (the histogram rotates by J); finished
+          // slots leave R below
+          u64 cd_next = Cd0 + (u64)J * nR;
+          u32 h_next = 0;
+          if constexpr (XS) h_next = __shfl_sync(FULLMASK, hcl, B.mod(lane + J) & 31u);  // bs <= 32 (else unused)
           #pragma unroll 1
           for (u32 b0 = 0; b0 < nR; b0 += 32) {
             const u32 jj = b0 + lane;
@@ -1236,8 +1287,14 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               const u32 l = (u32)(__ffs(fm) - 1);
               fm &= fm - 1;
               const u32 pos = b0 + l;
-              const u32 held = B.cdiv(S.ctx[pos]);
+              const u32 cf = S.ctx[pos];
+              const u32 held = B.cdiv(cf);
               const u32 slot = SLOT(S.info[pos]);
+              if constexpr (XS) {
+                cd_next -= cf + 1;
+                const u32 rf = B.mod(cf);
+                if (lane == (rf ? B.bs - rf : 0u)) h_next -= 1;
+              }
               if (HELP) ev_free(held, S.id[pos], slot, klast);
               else free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, 0, L, hint);
               nfree += held;
@@ -1258,36 +1315,47 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           __syncwarp();
           PH(3);
           // iteration records, digests, counters (lanes j < J)
-          const u64 blkj = blk0 + Aj;
-          it_begin(32);
+          const u64 blkj = blk0 + Aj, blkj1 = blk0 + Aj1;
+          it_begin(XS ? 64u : 32u);
           if (lj) it_put(L, lane, k + lane, tsj, Tj, 0, Cdj, blkj, 0, nR, 0, 0, 0, lane == J - 1 ? nfin : 0u, 0);
+          if (lj1)
+            it_put(L, 32u + lane, k + 32u + lane, tsj1, Tj1, 0, Cdj1, blkj1, 0, nR, 0, 0, 0,
+                   32u + lane == J - 1 ? nfin : 0u, 0);
           L.nit += J;
           it_commit();
-          const u64 bns_add = HELP ? 0ull : warp_sum64(lj ? blkj * (u64)Tj : 0ull);
+          const u64 bns_add =
+              HELP ? 0ull : warp_sum64((lj ? blkj * (u64)Tj : 0ull) + (lj1 ? blkj1 * (u64)Tj1 : 0ull));
           PH(4);
           // memory trace
           if (HELP) {
           } else if (BINNED) {
             while (true) {
               const i64 bstart = bin_end - W;
-              i64 ov = 0;
-              bool cnt_here = false;
+              i64 ov = 0, ov1 = 0;
+              bool cnt_here = false, cnt1 = false;
               if (lj) {
                 const i64 lo = tsj > bstart ? tsj : bstart;
                 const i64 hi = tej < bin_end ? tej : bin_end;
                 ov = hi - lo;
                 cnt_here = tsj >= bstart && tsj < bin_end;
               }
-              const u64 add = warp_sum64(ov > 0 ? blkj * (u64)ov : 0ull);
-              const u32 mx = __reduce_max_sync(FULLMASK, ov > 0 ? (u32)blkj : 0u);
+              if (lj1) {
+                const i64 lo = tsj1 > bstart ? tsj1 : bstart;
+                const i64 hi = tej1 < bin_end ? tej1 : bin_end;
+                ov1 = hi - lo;
+                cnt1 = tsj1 >= bstart && tsj1 < bin_end;
+              }
+              const u64 add = warp_sum64((ov > 0 ? blkj * (u64)ov : 0ull) + (ov1 > 0 ? blkj1 * (u64)ov1 : 0ull));
+              const u32 mx = __reduce_max_sync(FULLMASK, max(ov > 0 ? (u32)blkj : 0u, ov1 > 0 ? (u32)blkj1 : 0u));
               acc_bns += add;
               acc_max = max(acc_max, mx);
-              acc_nit += __popc(__ballot_sync(FULLMASK, cnt_here));
+              acc_nit += __popc(__ballot_sync(FULLMASK, cnt_here)) + __popc(__ballot_sync(FULLMASK, cnt1));
               if (tend > bin_end || tsl >= bin_end) flush_bin();
               else break;
             }
           } else if (FULLT) {
-            full_trace_put(fe, tbuf, tcap_b, J, tsj, tsj + Tj, blkj, flags);
+            full_trace_put(fe, tbuf, tcap_b, two ? 32u : J, tsj, tsj + Tj, blkj, flags);
+            if (two) full_trace_put(fe, tbuf, tcap_b, J - 32u, tsj1, tsj1 + Tj1, blkj1, flags);
           }
           if (!HELP) {
             const u64 blk_last = blk0 + Ktot;
@@ -1338,6 +1406,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           }
           PH(6);
           rmin = nR ? __reduce_min_sync(FULLMASK, rmin_l) : 0u;
+          // ranks within a residue class (S.req_pt) survive the rotation while no slot left R;
+          // a finish compacts the slots, and the next stretch recounts
+          inc_ok = XS && B.bs <= 32u && nfin == 0;
+          inc_cd = cd_next;
+          inc_h = h_next;
           PH(7);
           ff_iters += J;
           ++ff_runs;
@@ -1354,6 +1427,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       clk_a = c1;
     }
     clk_p = prof_clock();
+    inc_ok = false;  // a normal iteration changes R and the contexts: the next stretch recounts
 
     // ---------------------------------------------------------------- 3. decode reservation
     u32 E = 0, Kb = 0, m = 0, nres = 0, nadm = 0, nrej = 0, Edec = 0;
