@@ -673,6 +673,92 @@ constexpr u32 HEV_ALLOC = 1, HEV_FREE = 2;
 constexpr long long HELPER_TIMEOUT = 20000000000ll;  // cycles
 __device__ __forceinline__ u32 chan_load(const volatile u32 *p) { return __shfl_sync(FULLMASK, *p, 0); }
 
+// Replay block events [econs, eprod) of a warp's event ring on a bitmap, in order (a.5,
+// reading A14: lowest free block first, frees in logical order): allocations write the block
+// tables and fold the block digest, frees return a table's first `count` blocks.  Consecutive
+// allocations are served by one extraction.  Used by the helper warp (one point per SM) and by
+// the several-warps-per-SM lean kernel, whose simulating warp drains its own ring when it fills
+// (the simulation itself needs block counts only).  false: the bitmap ran out (an internal error).
+static __device__ __noinline__ bool replay_block_events(const uint4 *evr, u32 &econs, u32 eprod, u32 *hbm, u32 *fl,
+                                                        u32 &hint, u32 nwords, u32 *bt, u32 btl, u64 &dgb) {
+  const u32 lane = lane_id();
+  bool ev_err = false;
+  #pragma unroll 1
+  while (econs != eprod) {  // block events, in order
+    const u32 m = min(32u, eprod - econs);
+    const bool v = lane < m;
+    uint4 ev = make_uint4(0, 0, 0, 0);
+    if (v) ev = evr[(econs + lane) & (EVCAP - 1)];
+    const u32 kind = ev.y & 3u, cnt = ev.y >> 2;
+    const u32 fm = __ballot_sync(FULLMASK, v && kind == HEV_FREE);
+    if (fm & 1u) {  // a free: return the slot's first cnt blocks
+      const u32 kk = __shfl_sync(FULLMASK, ev.x, 0), held = __shfl_sync(FULLMASK, cnt, 0);
+      const u32 id = __shfl_sync(FULLMASK, ev.z, 0), slot = __shfl_sync(FULLMASK, ev.w, 0) & 1023u;
+      u32 mn = 0xffffffffu;
+      #pragma unroll 1
+      for (u32 x = lane; x < held; x += 32) {
+        const u32 b = bt[(size_t)slot * btl + x];
+        atomicOr(&hbm[b >> 5], 1u << (b & 31u));
+        dgb += fold_event(kk, 2, id, b);
+        mn = min(mn, b >> 5);
+      }
+      mn = __reduce_min_sync(FULLMASK, mn);
+      hint = min(hint, mn);
+      __syncwarp();
+      econs += 1;
+      continue;
+    }
+    const u32 na = fm ? (u32)(__ffs(fm) - 1) : m;  // leading allocations
+    const u32 c = lane < na ? cnt : 0u;
+    const u32 cum = scan_incl(c);
+    const u32 K = __shfl_sync(FULLMASK, cum, na - 1);
+    if (K <= 256) {  // all of them from one extraction, lane per block
+      if (K && !take_lowest(hbm, K, fl, hint, nwords)) ev_err = true;
+      #pragma unroll 1
+      for (u32 o0 = 0; o0 < K; o0 += 32) {
+        const u32 o = o0 + lane;
+        const u32 tgt = o < K ? o : 0u;
+        u32 a = 0;
+#pragma unroll
+        for (u32 st = 16; st; st >>= 1) {
+          const u32 vv = __shfl_sync(FULLMASK, cum, a + st - 1);
+          if (vv <= tgt) a += st;
+        }
+        const u32 ex = __shfl_sync(FULLMASK, cum - c, a);
+        const u32 kk = __shfl_sync(FULLMASK, ev.x, a), id = __shfl_sync(FULLMASK, ev.z, a);
+        const u32 sw = __shfl_sync(FULLMASK, ev.w, a);
+        if (o < K) {
+          const u32 blk = fl[o];
+          bt[(size_t)(sw & 1023u) * btl + (sw >> 10) + (o - ex)] = blk;
+          dgb += fold_event(kk, 1, id, blk);
+        }
+      }
+      __syncwarp();
+    } else {  // a large request: event by event, 256 blocks at a time
+      #pragma unroll 1
+      for (u32 i = 0; i < na; ++i) {
+        const u32 kk = __shfl_sync(FULLMASK, ev.x, i), id = __shfl_sync(FULLMASK, ev.z, i);
+        const u32 sw = __shfl_sync(FULLMASK, ev.w, i), ci = __shfl_sync(FULLMASK, cnt, i);
+        #pragma unroll 1
+        for (u32 s0 = 0; s0 < ci; s0 += 256) {
+          const u32 kc = min(256u, ci - s0);
+          if (!take_lowest(hbm, kc, fl, hint, nwords)) ev_err = true;
+          #pragma unroll 1
+          for (u32 x = lane; x < kc; x += 32) {
+            const u32 blk = fl[x];
+            bt[(size_t)(sw & 1023u) * btl + (sw >> 10) + s0 + x] = blk;
+            dgb += fold_event(kk, 1, id, blk);
+          }
+          __syncwarp();
+        }
+      }
+    }
+    econs += na;
+  }
+  return !ev_err;
+}
+
+
 template <int CAP, bool FULL, bool P2>
 __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S, u32 *bt,
                                  volatile HelperChan *ch = nullptr) {
@@ -681,6 +767,13 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   // latency-bound helper-warp kernel: they shorten a lone point's chain, but at 8 warps per SM
   // the larger hot code costs more in instruction fetch than it saves (DESIGN.md §8 A/B log).
   constexpr bool XS = HELP;
+  // Block ids off the simulation chain (HEV): every scheduling decision depends on block counts
+  // only, so allocations and frees are logged as events in a per-warp ring and the helper warp
+  // replays the ring into block ids (tables, bitmap, block digest).  The several-warps-per-SM
+  // kernel replaying its own ring whenever it fills (SD) was measured: bit-identical, but C3
+  // 614 -> 668 ms, so it keeps its inline allocator.
+  constexpr bool SD = false;
+  constexpr bool HEV = HELP || SD;
   static_assert(CAP % 32 == 0 && CAP <= 1024, "CAP");
   const u32 lane = lane_id();
   const u32 ltm = lanemask_lt();
@@ -796,8 +889,18 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     __syncwarp();
     if (lane_id() == 0) ch->eprod = L.nev;
   };
+  u64 sd_dgb = 0;  // SD: block-digest partial of this lane (replay_block_events)
+  auto sd_drain = [&]() {  // SD: replay every logged block event (on this warp's bitmap)
+    __syncwarp();
+    if (!replay_block_events(L.ev, econs_seen, L.nev, S.bitmap, S.req_cum, hint, nwords, bt, btl, sd_dgb))
+      flags |= TOKENSIM_PT_INTERNAL_ERROR;
+  };
   auto ev_begin = [&](u32 cnt) {  // room for cnt events; publish first if we must wait
     if (L.nev + cnt - econs_seen <= EVCAP) return;
+    if constexpr (SD) {
+      sd_drain();
+      return;
+    }
     if (L.nev + cnt - (econs_seen = chan_load(&ch->econs)) <= EVCAP) return;
     ev_commit();
     const long long c0 = clock64();
@@ -1148,7 +1251,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const u32 Ktot = __shfl_sync(FULLMASK, two ? Aj1 : Aj, (J - 1) & 31u);
           PH(1);
           bool done_alloc = Ktot == 0;
-          if (!HELP && !done_alloc && !two && nR <= 32 && Ktot <= 32 && hint < nwords) {
+          if (!HEV && !done_alloc && !two && nR <= 32 && Ktot <= 32 && hint < nwords) {
             // fused small case: lane o takes the o-th lowest free block of the 32-word window at
             // the hint and serves order index o = (iteration jb, r-th slot of jb's residue class)
             const u32 wi = hint + lane;
@@ -1200,7 +1303,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
             // request of a slot at iteration offset jx has order index (blocks of iterations
             // before jx) + (its rank in its residue class)
             u32 *fl = S.req_cum;  // free in a stretch; Ktot <= CAP (cut condition)
-            if (HELP) {
+            if (HEV) {
               ev_begin(Ktot);
             } else {
               if (!take_lowest(S.bitmap, Ktot, fl, hint, nwords)) {
@@ -1226,7 +1329,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
                 const u32 ex = jx < 32u ? ex0 : ex1;
                 if (in && jx < J) {
                   const u32 o = ex + rank;
-                  if (HELP) {
+                  if (HEV) {
                     ev_log(o, k + jx, HEV_ALLOC, 1, S.id[jj], SLOT(S.info[jj]), B.div(c + jx));
                   } else {
                     const u32 blk = fl[o];
@@ -1295,7 +1398,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
                 const u32 rf = B.mod(cf);
                 if (lane == (rf ? B.bs - rf : 0u)) h_next -= 1;
               }
-              if (HELP) ev_free(held, S.id[pos], slot, klast);
+              if (HEV) ev_free(held, S.id[pos], slot, klast);
               else free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], klast, 0, L, hint);
               nfree += held;
               if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
@@ -1625,7 +1728,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 slot = SLOT(S.info[v]);
         // a partial prefill loses its KV whatever the mode: re-prefill from scratch (R-N3b)
         const bool vx = hx && v == nR - 1;
-        if (HELP) ev_free(held, S.id[v], slot, k);
+        if (HEV) ev_free(held, S.id[v], slot, k);
         else free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[v], k, 0, L, hint);
         nfree += held;
         if (!vx) csub += c + 1;
@@ -1743,7 +1846,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     // 6. empty batch (every candidate rejected): back to 0 without advancing t
     if (nR == 0) continue;
     // block extraction for all requesters of this iteration, in phase order
-    if (HELP) {
+    if (HEV) {
       if (Kb > 0) {  // one event per requester entry, in phase order
         #pragma unroll 1
         for (u32 e0 = 0; e0 < E; e0 += 32) {
@@ -1861,7 +1964,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 c = S.ctx[pos];
         const u32 held = B.cdiv(c);
         const u32 slot = SLOT(S.info[pos]);
-        if (HELP) ev_free(held, S.id[pos], slot, k);
+        if (HEV) ev_free(held, S.id[pos], slot, k);
         else free_blocks(S.bitmap, bt + (size_t)slot * btl, held, S.id[pos], k, 0, L, hint);
         nfree += held;
         if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
@@ -1979,7 +2082,8 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     ++k;
     cyc_normal += (u64)(prof_clock() - clk_a);
   }
-  if (!HELP) ev_flush(L);
+  if constexpr (SD) sd_drain();
+  else if (!HELP) ev_flush(L);
   u64 dig_s = 0, dig_bh = 0;
   if constexpr (HELP) {  // hand the end time over, wait for the helper's results
     if (lane_id() == 0) {
@@ -2021,7 +2125,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
     const u32 id = S.id[x];
     write_record(rec + id, S.ttft[x], 0, 0, S.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);
   }
-  const u64 dig_b = HELP ? dig_bh : warp_sum64(L.dig_b);
+  const u64 dig_b = HELP ? dig_bh : warp_sum64(SD ? sd_dgb : L.dig_b);
   if (lane == 0) {
     SimStats st;
     st.flags = flags | ((nrej_tot == n) ? (u32)TOKENSIM_PT_ALL_REJECTED : 0u);
@@ -2136,79 +2240,7 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
       const u32 prod = chan_load(&ch->prod);
       const u32 eprod = chan_load(&ch->eprod);
       __threadfence_block();
-      bool ev_err = false;
-      #pragma unroll 1
-      while (econs != eprod) {  // block events, in order
-        const u32 m = min(32u, eprod - econs);
-        const bool v = lane < m;
-        uint4 ev = make_uint4(0, 0, 0, 0);
-        if (v) ev = evr[(econs + lane) & (EVCAP - 1)];
-        const u32 kind = ev.y & 3u, cnt = ev.y >> 2;
-        const u32 fm = __ballot_sync(FULLMASK, v && kind == HEV_FREE);
-        if (fm & 1u) {  // a free: return the slot's first cnt blocks
-          const u32 kk = __shfl_sync(FULLMASK, ev.x, 0), held = __shfl_sync(FULLMASK, cnt, 0);
-          const u32 id = __shfl_sync(FULLMASK, ev.z, 0), slot = __shfl_sync(FULLMASK, ev.w, 0) & 1023u;
-          u32 mn = 0xffffffffu;
-          #pragma unroll 1
-          for (u32 x = lane; x < held; x += 32) {
-            const u32 b = bt[(size_t)slot * btl + x];
-            atomicOr(&hbm[b >> 5], 1u << (b & 31u));
-            dgb += fold_event(kk, 2, id, b);
-            mn = min(mn, b >> 5);
-          }
-          mn = __reduce_min_sync(FULLMASK, mn);
-          hint = min(hint, mn);
-          __syncwarp();
-          econs += 1;
-          continue;
-        }
-        const u32 na = fm ? (u32)(__ffs(fm) - 1) : m;  // leading allocations
-        const u32 c = lane < na ? cnt : 0u;
-        const u32 cum = scan_incl(c);
-        const u32 K = __shfl_sync(FULLMASK, cum, na - 1);
-        if (K <= 256) {  // all of them from one extraction, lane per block
-          if (K && !take_lowest(hbm, K, fl, hint, nwords)) ev_err = true;
-          #pragma unroll 1
-          for (u32 o0 = 0; o0 < K; o0 += 32) {
-            const u32 o = o0 + lane;
-            const u32 tgt = o < K ? o : 0u;
-            u32 a = 0;
-#pragma unroll
-            for (u32 st = 16; st; st >>= 1) {
-              const u32 vv = __shfl_sync(FULLMASK, cum, a + st - 1);
-              if (vv <= tgt) a += st;
-            }
-            const u32 ex = __shfl_sync(FULLMASK, cum - c, a);
-            const u32 kk = __shfl_sync(FULLMASK, ev.x, a), id = __shfl_sync(FULLMASK, ev.z, a);
-            const u32 sw = __shfl_sync(FULLMASK, ev.w, a);
-            if (o < K) {
-              const u32 blk = fl[o];
-              bt[(size_t)(sw & 1023u) * btl + (sw >> 10) + (o - ex)] = blk;
-              dgb += fold_event(kk, 1, id, blk);
-            }
-          }
-          __syncwarp();
-        } else {  // a large request: event by event, 256 blocks at a time
-          #pragma unroll 1
-          for (u32 i = 0; i < na; ++i) {
-            const u32 kk = __shfl_sync(FULLMASK, ev.x, i), id = __shfl_sync(FULLMASK, ev.z, i);
-            const u32 sw = __shfl_sync(FULLMASK, ev.w, i), ci = __shfl_sync(FULLMASK, cnt, i);
-            #pragma unroll 1
-            for (u32 s0 = 0; s0 < ci; s0 += 256) {
-              const u32 kc = min(256u, ci - s0);
-              if (!take_lowest(hbm, kc, fl, hint, nwords)) ev_err = true;
-              #pragma unroll 1
-              for (u32 x = lane; x < kc; x += 32) {
-                const u32 blk = fl[x];
-                bt[(size_t)(sw & 1023u) * btl + (sw >> 10) + s0 + x] = blk;
-                dgb += fold_event(kk, 1, id, blk);
-              }
-              __syncwarp();
-            }
-          }
-        }
-        econs += na;
-      }
+      const bool ev_err = !replay_block_events(evr, econs, eprod, hbm, fl, hint, nwords, bt, btl, dgb);
       if (ev_err) tflags |= TOKENSIM_PT_INTERNAL_ERROR;
       __syncwarp();
       if (lane == 0) ch->econs = econs;

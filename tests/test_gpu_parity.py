@@ -198,6 +198,26 @@ def test_c4_sampled(api):
     check_points(sw, cfg, pts, records=True)
 
 
+def test_c4_strided_helper_kernel(api):
+    """C4 at 8 emulated GPUs: rank 7's strided shard (288 points <= 4 per SM) runs in the
+    helper-warp kernel with carried stretch state and 64-iteration stretches.  Sampled points
+    (incl. the longest chain, point 1543 = 7 mod 8) against the oracle, and fast-forward on ==
+    off byte for byte over the whole shard."""
+    cfg = si.c4()
+    sw = api.Sweep(cfg)
+    sw.run(7, cfg.num_points, 8)
+    info = sw.run_info()
+    assert info["helper_mode"] == 1 and info["sim_warps_per_block"] == 1
+    s = sw.summaries()
+    assert (s["status_flags"] & 16 == 0).all()
+    check_points(sw, cfg, [7, 1543, 2303, 1159, 391], records=True)
+    off = api.Sweep(replace(cfg, options=replace(cfg.options, fast_forward=False)))
+    off.run(7, cfg.num_points, 8)
+    assert off.summaries().tobytes() == s.tobytes()
+    for p in (1543, 2303):
+        assert off.records(p).tobytes() == sw.records(p).tobytes()
+
+
 def test_sharegpt_builtin_equals_table(api):
     cfg = si.c1()
     a = run_gpu(api, cfg).summaries()

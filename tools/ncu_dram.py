@@ -2,6 +2,7 @@
 summary (DRAM bytes per launch for bench.py's roofline `traffic`, issue and stall shares).
 
     python tools/ncu_dram.py c2 [out_dir]
+    python tools/ncu_dram.py c3 out_dir --rep existing.ncu-rep   (summarise a capture taken earlier)
 """
 import csv
 import io
@@ -10,17 +11,25 @@ import os
 import subprocess
 import sys
 
-cfg = sys.argv[1]
-out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/ncu"
+args = [a for a in sys.argv[1:]]
+existing = None
+if "--rep" in args:
+    i = args.index("--rep")
+    existing = args[i + 1]
+    del args[i:i + 2]
+cfg = args[0]
+out = args[1] if len(args) > 1 else "gpurun_out/ncu"
 os.makedirs(out, exist_ok=True)
-rep = os.path.join(out, f"sim_{cfg}")
+rep = existing[:-len(".ncu-rep")] if existing else os.path.join(out, f"sim_{cfg}")
+ROUND = os.environ.get("NCU_ROUND", "round 2")
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "-k", "regex:sim_kernel",
        "-c", "1", "-f", "-o", rep, sys.executable, os.path.join(root, "tools", "prof_run.py"), "--config", cfg]
 # the product library (prof_run.py would otherwise pick the profiling build)
 env = dict(os.environ, TOKENSIM_LIB=os.environ.get("TOKENSIM_LIB") or
            os.path.join(root, "paper_2503_08415_b200", "libtokensim.so"))
-subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, env=env)
+if not existing:
+    subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, env=env)
 raw = subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "raw", "--csv", "--print-units", "base"], check=True,
                      capture_output=True,
                      text=True).stdout
@@ -43,7 +52,7 @@ for k in hdr:
 tot = sum(v for v in stalls.values() if v) or 1.0
 summary = {
     "source": f"ncu --set full --clock-control none --import-source on -k regex:sim_kernel -c 1 "
-              f"(tools/prof_run.py --config {cfg}), B200, round 1",
+              f"(tools/prof_run.py --config {cfg}), B200, {ROUND}",
     "kernel": d.get("Kernel Name"),
     "duration_ms": (f("gpu__time_duration.sum") or 0) / 1e6,  # base unit: ns
     "dram_bytes_read": f("dram__bytes_read.sum"),
@@ -67,5 +76,6 @@ if os.environ.get("NCU_SOURCE_CSV"):  # keep the source page (per-SASS stalls) f
     with open(os.path.join(out, f"src_{cfg}.csv"), "w") as fh:
         subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "source", "--csv", "--print-source=cuda,sass"],
                        check=True, stdout=fh, stderr=subprocess.DEVNULL)
-os.remove(rep + ".ncu-rep")
+if not existing:
+    os.remove(rep + ".ncu-rep")
 print(json.dumps({k: summary[k] for k in ("kernel", "duration_ms", "dram_bytes_per_launch", "issue_active_pct")}))

@@ -44,8 +44,9 @@ def main():
         if a.variant == "pd":
             from test_gpu_parity import _micro_pd
             cfg = _micro_pd(rng)
-        # a few identical points so the compact variant runs several warps per CTA
-        cfg = replace(cfg, workload=replace(cfg.workload, seeds=[0, 1, 2, 3]))
+        # a few identical points (TRACE mode: repeat the profile) so the compact variant runs
+        # several warps per CTA
+        cfg = replace(cfg, hws=list(cfg.hws) * 4)
         sw = P.Sweep(cfg)
         sw.run()
         torch.cuda.synchronize()
