@@ -62,6 +62,13 @@ struct tokensim_sweep {
   std::vector<DevHP> dhp;
   std::vector<DevPol> dpol;
   std::vector<double> est_T1;  // per (hw,pol): rough per-iteration time for LPT ordering
+  // per (hw,pol) inputs of the LPT cost estimate (lpt_cost): weights / bandwidth, KV read time
+  // per context token, decode FLOP time per token, the overhead, and the memory-bound batch
+  struct EstHP {
+    double w_s, tok_s, flop_s, ovh, bmem, bmax;
+  };
+  std::vector<EstHP> est_hp;
+  double mean_p = 0, mean_o = 0;  // workload means (table / fixed / uniform / trace)
   u32 cap = 256, nwords_max = 1, bt_len = 1, n_hw_axis = 0;
   u32 pd_x = 0, pd_y = 0;  // NEXT-1 node: prefill / decode workers (0 = unified)
   bool pd_general = false;  // run the general xP:yD loop
@@ -277,6 +284,37 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
       if (pol[i].iteration_mode != TOKENSIM_MIXED) return bad("workload.multi_round: MIXED iterations only");
   }
   if (opt->memory_cache && !w.multi_round) return bad("options.memory_cache: needs a multi_round workload");
+  {  // workload length means, for the LPT cost estimate only (lpt_cost)
+    auto tab_mean = [](const std::vector<u32> &t) {
+      const u32 nb = t[0];
+      const u32 *lo = &t[1], *hi = &t[1 + nb], *thr = &t[1 + 2 * nb];
+      double prev = 0, m = 0;
+      for (u32 b = 0; b < nb; ++b) {
+        const double c = b + 1 < nb ? (double)thr[b] : 4294967296.0;
+        m += (c - prev) / 4294967296.0 * ((double)lo[b] + ((double)hi[b] - lo[b] - 1) / 2.0);
+        prev = c;
+      }
+      return m;
+    };
+    if (!h->ptab.empty() && !h->otab.empty()) {
+      h->mean_p = tab_mean(h->ptab);
+      h->mean_o = std::min(tab_mean(h->otab), (double)mml - h->mean_p);
+    } else if (w.len_dist == TOKENSIM_LEN_FIXED) {
+      h->mean_p = w.prompt_a;
+      h->mean_o = w.output_a;
+    } else if (w.len_dist == TOKENSIM_LEN_UNIFORM) {
+      h->mean_p = 0.5 * ((double)w.prompt_a + w.prompt_b);
+      h->mean_o = 0.5 * ((double)w.output_a + w.output_b);
+    } else {
+      double sp = 0, so = 0;
+      for (u32 i = 0; i < w.num_requests; ++i) {
+        sp += h->tr_p[i];
+        so += h->tr_o[i];
+      }
+      h->mean_p = sp / std::max<u32>(1, w.num_requests);
+      h->mean_o = so / std::max<u32>(1, w.num_requests);
+    }
+  }
   if (!(opt->cache_fetch_ns_per_block >= 0) || !std::isfinite(opt->cache_fetch_ns_per_block))
     return bad("options.cache_fetch_ns_per_block: must be >= 0");
 
@@ -419,6 +457,18 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
       h->dhp.push_back(hp);
       // LPT estimate: weights over bandwidth + overhead is the decode step floor
       h->est_T1.push_back((double)W / (x.mem_bw * x.eff_bw) + x.iter_overhead_s);
+      {
+        tokensim_sweep::EstHP e;
+        const double Bw = x.mem_bw * x.eff_bw, Ff = x.peak_flops * x.eff_flops;  // aggregate profile (A22)
+        e.w_s = (double)W / Bw;
+        e.tok_s = (double)M.kvb / Bw;
+        e.flop_s = (double)W / ((double)M.s * 0.5 * Ff);  // ~2 FLOPs per parameter per token
+        e.ovh = x.iter_overhead_s;
+        e.bmem = (double)hp.total_blocks * p.block_size;  // KV tokens (divided by the mean context later)
+        if (p.kind == TOKENSIM_CONT_RATIO) e.bmem *= p.max_mem_ratio;
+        e.bmax = p.max_num_seqs;
+        h->est_hp.push_back(e);
+      }
     }
   }
   h->nwords_max = (u32)((max_words + 31) & ~31ull);
@@ -453,6 +503,32 @@ static bool range_ok(const tokensim_sweep *h, u64 begin, u64 end, u64 stride) {
   return stride >= 1 && begin <= end && end <= h->n_points;
 }
 static u64 count_run(u64 begin, u64 end, u64 stride) { return end > begin ? (end - begin + stride - 1) / stride : 0; }
+
+// LPT cost estimate of one unified-topology point (longest-estimated points start first).  A
+// queueing sketch of the simulated system: decode step time T(b) = overhead + max(weights + b x
+// context KV, b x decode FLOPs) at batch b; the batch the load sustains (Little's law on tokens,
+// b = lambda E[o] T(b), capped by max_num_seqs and by the KV pool over the mean context);
+// iterations = span / T(b) (or E[o] n / b_max when overloaded).  Simulation cost ~ 250 SM cycles
+// per iteration plus ~12k per admission, with four times that when the KV pool binds (preemption
+// churn).  Fitted to round-2 per-point cycle counts of C3 / C4; it only orders
+// the queue, never changes a result.
+static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate) {
+  const auto &e = h->est_hp[hwpol];
+  const double n = h->wl.num_requests, Eo = std::max(1.0, h->mean_o), ctx = h->mean_p + 0.5 * Eo;
+  const double bmem = std::max(1.0, e.bmem / std::max(1.0, ctx));
+  const double bmax = std::max(1.0, std::min(e.bmax, bmem));
+  auto T = [&](double b) { return e.ovh + std::max(e.w_s + b * ctx * e.tok_s, b * e.flop_s); };
+  double b = bmax, iters;
+  if (rate * Eo >= bmax / T(bmax)) {
+    iters = n * Eo / bmax;
+  } else {
+    b = 1.0;
+    for (int it = 0; it < 30; ++it) b = std::min(bmax, std::max(1.0, rate * Eo * T(b)));
+    iters = (n / rate) / T(b);
+  }
+  const bool tight = bmem < e.bmax && b > 0.5 * bmax;
+  return 250.0 * iters + 12000.0 * n * (tight ? 4.0 : 1.0);
+}
 
 // The lean unified kernel runs one point per CTA with a helper warp (variant 0) when a run is
 // latency-bound: at most kHelperPointsPerSm points per SM (a point's serial chain, not the SM's
@@ -773,7 +849,11 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
       const Coords c = decode_point(begin + j * stride, P.n_pol, P.n_rates, P.n_seeds);
       const double span = (double)P.n_req / h->rates[c.rate];
       const u32 hwe = P.topology == TOKENSIM_PD_PAIR ? c.hw % P.n_hw : c.hw;  // decode worker dominates
-      est[j] = {span / h->est_T1[(size_t)hwe * P.n_pol + c.pol], (u32)j};
+      static const bool lpt_old = getenv("TOKENSIM_LPT_OLD") != nullptr;  // A/B: the round-1 estimate
+      const bool unified = !lpt_old && P.topology != TOKENSIM_PD_PAIR && !h->wl.multi_round && !trace_mode;
+      est[j] = {unified ? lpt_cost(h, (u32)((size_t)hwe * P.n_pol + c.pol), h->rates[c.rate])
+                        : span / h->est_T1[(size_t)hwe * P.n_pol + c.pol],
+                (u32)j};
     }
     std::stable_sort(est.begin(), est.end(), [](const std::pair<double, u32> &a, const std::pair<double, u32> &b) {
       return a.first > b.first;

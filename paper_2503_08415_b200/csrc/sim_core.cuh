@@ -655,6 +655,9 @@ __device__ __forceinline__ void mr_cache_store(MrState &M, u32 c, u32 tokens, co
 // simulating warp's serial chain.  The log is a 256-entry ring in global memory; the two warps
 // hand over through counters in shared memory.  Every wait is bounded (~10 s of clock) and
 // raises TOKENSIM_PT_INTERNAL_ERROR instead of hanging.
+#ifndef TS_NO_FUSED  // A/B: 1 = no fused small-allocation path in stretches (general path only)
+#define TS_NO_FUSED 0
+#endif
 #ifndef TS_HELPER_WARP
 #define TS_HELPER_WARP 0
 #endif
@@ -1251,7 +1254,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const u32 Ktot = __shfl_sync(FULLMASK, two ? Aj1 : Aj, (J - 1) & 31u);
           PH(1);
           bool done_alloc = Ktot == 0;
-          if (!HEV && !done_alloc && !two && nR <= 32 && Ktot <= 32 && hint < nwords) {
+          if (!HEV && !TS_NO_FUSED && !done_alloc && !two && nR <= 32 && Ktot <= 32 && hint < nwords) {
             // fused small case: lane o takes the o-th lowest free block of the 32-word window at
             // the hint and serves order index o = (iteration jb, r-th slot of jb's residue class)
             const u32 wi = hint + lane;
@@ -1313,7 +1316,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
               ev_reserve(L, Ktot);
             }
             const u32 excl = Aj - nj, excl1 = Aj1 - nj1;
-            const u32 nrep = ((XS ? J : 32u) + B.bs - 1) / B.bs;
+            const u32 nrep = B.cdiv(XS ? J : 32u);  // (shifts when bs is a power of two)
             #pragma unroll 1
             for (u32 b0 = 0; b0 < nR; b0 += 32) {
               const u32 jj = b0 + lane;

@@ -28,8 +28,7 @@ struct TraceAcc {  // lane-uniform BINNED/FULL trace state of one worker
   u64 tn, bin, acc_bns;
   i64 bin_end;
   u32 acc_max, acc_nit;
-  FullEnc fe;  // FULL: the compressed stream (trace_codec.cuh)
-};
+};  // (FULL traces keep their FullEnc apart: this struct is copied with a worker's scalars)
 
 __device__ __forceinline__ void trace_flush_bin(TraceAcc &A, tokensim_mem_sample *trc, u64 cap, i64 W, u32 &flags) {
   if (A.tn < cap) {
@@ -53,8 +52,8 @@ __device__ __forceinline__ void trace_flush_bin(TraceAcc &A, tokensim_mem_sample
   A.acc_nit = 0;
 }
 
-__device__ __forceinline__ void trace_iter(TraceAcc &A, bool binned, bool full, tokensim_mem_sample *trc, u64 cap,
-                                           i64 W, i64 ts, i64 te, u64 blocks, u32 &flags) {
+__device__ __forceinline__ void trace_iter(TraceAcc &A, FullEnc &fe, bool binned, bool full, tokensim_mem_sample *trc,
+                                           u64 cap, i64 W, i64 ts, i64 te, u64 blocks, u32 &flags) {
   if (binned) {
     while (A.bin_end <= ts) trace_flush_bin(A, trc, cap, W, flags);
     ++A.acc_nit;
@@ -72,13 +71,13 @@ __device__ __forceinline__ void trace_iter(TraceAcc &A, bool binned, bool full, 
       A.acc_max = max(A.acc_max, (u32)blocks);
     }
   } else if (full) {
-    full_trace_put(A.fe, reinterpret_cast<unsigned char *>(trc), cap * sizeof(tokensim_mem_sample), 1u, ts, te, blocks,
+    full_trace_put(fe, reinterpret_cast<unsigned char *>(trc), cap * sizeof(tokensim_mem_sample), 1u, ts, te, blocks,
                    flags);
   }
 }
 
 // memory trace of a stretch: lanes j < J hold iterations [tsj, tej) with blkj blocks
-__device__ __forceinline__ void trace_stretch(TraceAcc &A, bool binned, bool full, tokensim_mem_sample *trc, u64 cap,
+__device__ __forceinline__ void trace_stretch(TraceAcc &A, FullEnc &fe, bool binned, bool full, tokensim_mem_sample *trc, u64 cap,
                                               i64 W, u32 J, i64 tsj, i64 tej, u64 blkj, u32 &flags) {
   const u32 lane = lane_id();
   const bool lj = lane < J;
@@ -101,7 +100,7 @@ __device__ __forceinline__ void trace_stretch(TraceAcc &A, bool binned, bool ful
       else break;
     }
   } else if (full) {
-    full_trace_put(A.fe, reinterpret_cast<unsigned char *>(trc), cap * sizeof(tokensim_mem_sample), J, tsj, tej, blkj,
+    full_trace_put(fe, reinterpret_cast<unsigned char *>(trc), cap * sizeof(tokensim_mem_sample), J, tsj, tej, blkj,
                    flags);
   }
 }
@@ -208,6 +207,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
   const bool FULLT = P.trace_mode == TOKENSIM_TRACE_FULL;
   const i64 W = (i64)P.bin_ns;
   TraceAcc TA[2] = {{0, 0, 0, W, 0, 0}, {0, 0, 0, W, 0, 0}};
+  FullEnc FE[2] = {{0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0}};
   // request window (P side)
   u32 win = 0;
   i64 wa = INT64_MAX;
@@ -414,7 +414,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
               }
             }
             if (!done_alloc) {
-              const u32 nrep = (32 + B.bs - 1) / B.bs;
+              const u32 nrep = B.cdiv(32u);
               #pragma unroll 1
               for (u32 b0 = 0; b0 < nA0; b0 += 32) {
                 const u32 jj = b0 + lane;
@@ -502,7 +502,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
             L.nit += J;
             nit += J;
             bnsD += warp_sum64(lj ? blkj * (u64)Tj : 0ull);
-            trace_stretch(TA[1], BINNED, FULLT, trcD, P.trace_cap, W, J, tsj, tej, blkj, flags);
+            trace_stretch(TA[1], FE[1], BINNED, FULLT, trcD, P.trace_cap, W, J, tsj, tej, blkj, flags);
             const u64 blk_last = blk0 + Ktot;
             peakD = blk_last > peakD ? blk_last : peakD;
             req_iters += (u64)nRun * J;
@@ -871,7 +871,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       rminD = __reduce_min_sync(FULLMASK, rmin_d);
       if (nRun == 0) rminD = 0;
       fold_iter(kD, 1, t, T, nrecomp, Dn, Np, Cd, m, nres, nadm, 0, nfin, blocks);
-      trace_iter(TA[1], BINNED, FULLT, trcD, P.trace_cap, W, t, te, blocks, flags);
+      trace_iter(TA[1], FE[1], BINNED, FULLT, trcD, P.trace_cap, W, t, te, blocks, flags);
       peakD = blocks > peakD ? blocks : peakD;
       bnsD += blocks * (u64)T;
       swo += swap_out;
@@ -1045,7 +1045,7 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
       nfin_tot += nfin;
       if (nfin) last_fin = te > last_fin ? te : last_fin;
       fold_iter(kP, 0, t, T, nb, 0, Np, 0, 0, 0, nb, nrej, nfin, blocksP);
-      trace_iter(TA[0], BINNED, FULLT, trcP, P.trace_cap, W, t, te, blocksP, flags);
+      trace_iter(TA[0], FE[0], BINNED, FULLT, trcP, P.trace_cap, W, t, te, blocksP, flags);
       req_iters += nb;
       tP = te;
       lastP = te;
@@ -1091,11 +1091,11 @@ __device__ void simulate_pd(const SweepParams &P, u64 j, const WarpSmem &S, unsi
     st.total_blocks = totD;
     st.peak_blocks = peakD;
     st.block_ns_sum = bnsD;
-    st.trace_n[0] = FULLT ? TA[0].fe.n : min(TA[0].tn, P.trace_cap);
-    st.trace_n[1] = FULLT ? TA[1].fe.n : min(TA[1].tn, P.trace_cap);
+    st.trace_n[0] = FULLT ? FE[0].n : min(TA[0].tn, P.trace_cap);
+    st.trace_n[1] = FULLT ? FE[1].n : min(TA[1].tn, P.trace_cap);
     for (int q = 2; q < 8; ++q) st.trace_n[q] = 0;
-    st.trace_b[0] = TA[0].fe.bytes;
-    st.trace_b[1] = TA[1].fe.bytes;
+    st.trace_b[0] = FE[0].bytes;
+    st.trace_b[1] = FE[1].bytes;
     for (int q = 2; q < 8; ++q) st.trace_b[q] = 0;
     st.iter_n = min(nit, P.it_cap);
     st.n_transfers = n_xfer;

@@ -198,7 +198,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     #pragma unroll 1
     for (u32 x = lane; x < n; x += 32) reqx[x] = INF;
     if (lane == 0) {
-      const TraceAcc ta0 = {0, 0, 0, (i64)P.bin_ns, 0, 0, {0, 0, 0, 0, 0, 0}};
+      const TraceAcc ta0 = {0, 0, 0, (i64)P.bin_ns, 0, 0};
       for (u32 w = 0; w < X; ++w) {
         PScal s;
         s.t = INF;  // a prefill worker starts idle: a dispatch wakes it
@@ -253,6 +253,8 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
   const bool FULLT = P.trace_mode == TOKENSIM_TRACE_FULL;
   const i64 W = (i64)P.bin_ns;
+  FullEnc FE[PDN_MAXW];  // FULL: each worker's compressed stream (lane-uniform, thread-local)
+  for (u32 w = 0; w < PDN_MAXW; ++w) FE[w] = {0, 0, 0, 0, 0, 0};
   auto fold_iter = [&](u64 kk, u32 worker, i64 ts, i64 T, u64 Sp, u64 D_, u64 Np, u64 Cd, u64 m, u64 nres,
                        u64 nadm, u64 nrej, u64 nfin, u64 blocks) {
     it_reserve(L, 1);
@@ -526,7 +528,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
             S.scratch[lane] = Aj - nj;  // bucket cursors
             __syncwarp();
             if (Ktot > 0) {
-              const u32 nrep = (32 + B.bs - 1) / B.bs;
+              const u32 nrep = B.cdiv(32u);
               #pragma unroll 1
               for (u32 b0 = 0; b0 < nA0; b0 += 32) {
                 const u32 jj = b0 + lane;
@@ -613,7 +615,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
                      lane == J - 1 ? nfin : 0u, 0);
             L.nit += J;
             d.bns += warp_sum64(lj ? blkj * (u64)Tj : 0ull);
-            trace_stretch(d.TA, BINNED, FULLT, trcD, P.trace_cap, W, J, tsj, tej, blkj, flags);
+            trace_stretch(d.TA, FE[wid], BINNED, FULLT, trcD, P.trace_cap, W, J, tsj, tej, blkj, flags);
             const u64 blk_last = blk0 + Ktot;
             d.peak = blk_last > d.peak ? blk_last : d.peak;
             req_iters += (u64)d.nRun * J;
@@ -1051,7 +1053,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           d.rmin = __reduce_min_sync(FULLMASK, rmin_d);
           if (d.nRun == 0) d.rmin = 0;
           fold_iter(d.k, wid, t, T, nrecomp, Dn, Np, Cd, m, nres, nadm, 0, nfin, blocks);
-          trace_iter(d.TA, BINNED, FULLT, trcD, P.trace_cap, W, t, te, blocks, flags);
+          trace_iter(d.TA, FE[wid], BINNED, FULLT, trcD, P.trace_cap, W, t, te, blocks, flags);
           d.peak = blocks > d.peak ? blocks : d.peak;
           d.bns += blocks * (u64)T;
           swo += swap_out;
@@ -1227,7 +1229,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         nfin_tot += nfin;
         if (nfin) last_fin = te > last_fin ? te : last_fin;
         fold_iter(p.k, pi, t, T, nb, 0, Np, 0, 0, 0, nb, nrej, nfin, blocksP);
-        trace_iter(p.TA, BINNED, FULLT, trcP, P.trace_cap, W, t, te, blocksP, flags);
+        trace_iter(p.TA, FE[pi], BINNED, FULLT, trcP, P.trace_cap, W, t, te, blocksP, flags);
         req_iters += nb;
         p.nb = nb;
         p.cur = 0;
@@ -1326,8 +1328,8 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       if (w < NW) {
         const TraceAcc &ta = w < X ? M.ps[w].TA : M.ds[w - X].TA;
         tn = ta.tn;
-        fn = ta.fe.n;
-        fb = ta.fe.bytes;
+        fn = FE[w].n;
+        fb = FE[w].bytes;
       }
       st.trace_n[w] = FULLT ? fn : (tn < P.trace_cap ? tn : P.trace_cap);
       st.trace_b[w] = fb;
