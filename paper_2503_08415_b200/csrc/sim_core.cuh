@@ -26,6 +26,22 @@
 #include "dev_common.cuh"
 #include "trace_codec.cuh"
 
+// Latency fast paths that cost more in instruction fetch than they save at 8 warps per SM
+// (DESIGN.md §8 A/B log): the fused small-allocation path of a stretch is compiled only into
+// the one-warp-per-SM / full kernels.  TS_AB_* switch further ones off for A/B experiments.
+#ifndef TS_NO_FUSED
+#define TS_NO_FUSED TS_COMPACT
+#endif
+#ifndef TS_AB_NO_ONEADM
+#define TS_AB_NO_ONEADM 0
+#endif
+#ifndef TS_AB_NO_BTFAST
+#define TS_AB_NO_BTFAST 0
+#endif
+#ifndef TS_AB_NO_HEADQ
+#define TS_AB_NO_HEADQ 0
+#endif
+
 namespace ts {
 
 // ------------------------------------------------------------------ a.6 cost model
@@ -410,7 +426,7 @@ static __device__ bool alloc_ordered(const WarpSmem &S, u32 E, u32 K, u32 *bt, u
 __device__ __forceinline__ u32 alloc_btslots(u32 *btfree, u32 nw, bool take, u32 rank, u32 cnt) {
   const u32 lane = lane_id();
   u32 word = lane < nw ? btfree[lane] : 0u;
-  if (cnt == 1) {  // one admission (the common case): the lowest set bit of the first nonzero word
+  if (!TS_AB_NO_BTFAST && cnt == 1) {  // one admission (the common case): the lowest set bit of the first nonzero word
     const u32 nz = __ballot_sync(FULLMASK, word != 0u);
     const u32 l = (u32)(__ffs(nz) - 1);
     const u32 wv = __shfl_sync(FULLMASK, word, l);
@@ -655,9 +671,6 @@ __device__ __forceinline__ void mr_cache_store(MrState &M, u32 c, u32 tokens, co
 // simulating warp's serial chain.  The log is a 256-entry ring in global memory; the two warps
 // hand over through counters in shared memory.  Every wait is bounded (~10 s of clock) and
 // raises TOKENSIM_PT_INTERNAL_ERROR instead of hanging.
-#ifndef TS_NO_FUSED  // A/B: 1 = no fused small-allocation path in stretches (general path only)
-#define TS_NO_FUSED 0
-#endif
 #ifndef TS_HELPER_WARP
 #define TS_HELPER_WARP 0
 #endif
@@ -1563,7 +1576,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         const u32 pw = __shfl_sync(FULLMASK, wp, off & 31u);
         const u32 ph = MRM ? PR[mr.wq_id[adm]] : ((adm >= win && off < 32) ? pw : PR[adm]);
         const u32 nh = B.cdiv(ph);
-        head_blocked = (u64)nh <= HP.cap_fresh &&
+        head_blocked = !TS_AB_NO_HEADQ && (u64)nh <= HP.cap_fresh &&
                        ((u64)nR + 1 > mns || tokens + (CHK ? 1u : ph) > (u64)mbt || (i64)nfree - (i64)nh < wm ||
                         (RATIO && (total - nfree) + nh > HP.ratio_limit));
       }
@@ -1596,7 +1609,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           const bool el = valid && !rej;
           // one candidate (the common case at low load): lane 0's prefix sums are its own values,
           // and every other lane's are masked by !el below, so the three scans are skipped
-          const bool one = arr - adm == 1u;
+          const bool one = !TS_AB_NO_ONEADM && arr - adm == 1u;
           const u32 ce = one ? (el ? 1u : 0u) : scan_incl(el ? 1u : 0u);
           const u32 cneed = one ? (el ? need : 0u) : scan_incl(el ? need : 0u);
           const u32 cp = one ? (el ? p : 0u) : scan_incl(el ? p : 0u);
