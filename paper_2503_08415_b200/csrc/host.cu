@@ -66,6 +66,7 @@ struct tokensim_sweep {
   // per context token, decode FLOP time per token, the overhead, and the memory-bound batch
   struct EstHP {
     double w_s, tok_s, flop_s, ovh, bmem, bmax;
+    bool stat;  // static batching
   };
   std::vector<EstHP> est_hp;
   double mean_p = 0, mean_o = 0;  // workload means (table / fixed / uniform / trace)
@@ -467,6 +468,7 @@ tokensim_status tokensim_sweep_create(const tokensim_model *model, const tokensi
         e.bmem = (double)hp.total_blocks * p.block_size;  // KV tokens (divided by the mean context later)
         if (p.kind == TOKENSIM_CONT_RATIO) e.bmem *= p.max_mem_ratio;
         e.bmax = p.max_num_seqs;
+        e.stat = p.kind == TOKENSIM_STATIC;
         h->est_hp.push_back(e);
       }
     }
@@ -508,10 +510,10 @@ static u64 count_run(u64 begin, u64 end, u64 stride) { return end > begin ? (end
 // queueing sketch of the simulated system: decode step time T(b) = overhead + max(weights + b x
 // context KV, b x decode FLOPs) at batch b; the batch the load sustains (Little's law on tokens,
 // b = lambda E[o] T(b), capped by max_num_seqs and by the KV pool over the mean context);
-// iterations = span / T(b) (or E[o] n / b_max when overloaded).  Simulation cost ~ 250 SM cycles
-// per iteration plus ~12k per admission, with four times that when the KV pool binds (preemption
-// churn).  Fitted to round-2 per-point cycle counts of C3 / C4; it only orders
-// the queue, never changes a result.
+// iterations = span / T(b) (or E[o] n / b_max when overloaded).  Simulation cost ~ 256 SM cycles
+// per iteration, ~22k per admission iteration (one per request; static batching: one per batch)
+// and ~14k more per request when the KV pool binds (preemption churn).  Fitted to round-2
+// per-point cycle counts of C3; it only orders the queue, never changes a result.
 static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate) {
   const auto &e = h->est_hp[hwpol];
   const double n = h->wl.num_requests, Eo = std::max(1.0, h->mean_o), ctx = h->mean_p + 0.5 * Eo;
@@ -527,7 +529,9 @@ static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate) {
     iters = (n / rate) / T(b);
   }
   const bool tight = bmem < e.bmax && b > 0.5 * bmax;
-  return 250.0 * iters + 12000.0 * n * (tight ? 4.0 : 1.0);
+  // admission iterations: one per request (continuous), one per batch (static: drain, then admit)
+  const double adm = e.stat ? n / std::max(1.0, b) : n;
+  return 256.0 * iters + 22000.0 * adm + 13600.0 * n * (tight ? 1.0 : 0.0);
 }
 
 // The lean unified kernel runs one point per CTA with a helper warp (variant 0) when a run is
@@ -854,6 +858,14 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
       est[j] = {unified ? lpt_cost(h, (u32)((size_t)hwe * P.n_pol + c.pol), h->rates[c.rate])
                         : span / h->est_T1[(size_t)hwe * P.n_pol + c.pol],
                 (u32)j};
+    }
+    if (const char *cf = getenv("TOKENSIM_LPT_COSTS")) {  // A/B experiments only: measured per-point costs
+      if (FILE *f = fopen(cf, "rb")) {
+        std::vector<double> c(h->n_points);
+        if (fread(c.data(), 8, c.size(), f) == c.size())
+          for (u64 j = 0; j < n_run; ++j) est[j].first = c[begin + j * stride];
+        fclose(f);
+      }
     }
     std::stable_sort(est.begin(), est.end(), [](const std::pair<double, u32> &a, const std::pair<double, u32> &b) {
       return a.first > b.first;
