@@ -528,7 +528,9 @@ static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate) {
     for (int it = 0; it < 30; ++it) b = std::min(bmax, std::max(1.0, rate * Eo * T(b)));
     iters = (n / rate) / T(b);
   }
-  const bool tight = bmem < e.bmax && b > 0.5 * bmax;
+  // churn: Poisson arrivals and the length spread fill a memory-limited pool well before the
+  // mean batch reaches it (C4 TP2 at lambda 4: b ~ 0.46 b_max, ~1.3 preemptions per request)
+  const bool tight = bmem < e.bmax && b > 0.35 * bmax;
   // admission iterations: one per request (continuous), one per batch (static: drain, then admit)
   const double adm = e.stat ? n / std::max(1.0, b) : n;
   return 256.0 * iters + 22000.0 * adm + 13600.0 * n * (tight ? 1.0 : 0.0);
