@@ -104,22 +104,30 @@ __device__ __forceinline__ WarpSmem dview(const PdnSmem &M, u32 j, u32 cap, u32 
 }
 
 // warp argmin over (key, order) for lanes < cnt; returns the winning lane (or 0xffffffff)
-__device__ __forceinline__ u32 warp_argmin64(i64 key, u32 ord, bool valid) {
+// argmin of key over lanes 0..7 (a node has at most 8 workers; lane = worker order), ties to
+// the lower lane; three butterfly steps within each group of 8 lanes, then lane 0's answer
+__device__ __forceinline__ u32 warp_argmin64(i64 key, bool valid) {
   i64 k = valid ? key : INT64_MAX;
-  u32 o = valid ? ord : 0xffffffffu;
   u32 who = valid ? lane_id() : 0xffffffffu;
 #pragma unroll
-  for (u32 s = 16; s; s >>= 1) {
+  for (u32 s = 4; s; s >>= 1) {
     const i64 k2 = __shfl_xor_sync(FULLMASK, k, s);
-    const u32 o2 = __shfl_xor_sync(FULLMASK, o, s);
     const u32 w2 = __shfl_xor_sync(FULLMASK, who, s);
-    if (k2 < k || (k2 == k && o2 < o)) {
+    if (k2 < k || (k2 == k && w2 < who)) {
       k = k2;
-      o = o2;
       who = w2;
     }
   }
-  return who;
+  return __shfl_sync(FULLMASK, who, 0);
+}
+// min over lanes 0..7 (the other lanes hold no worker), broadcast to the warp
+__device__ __forceinline__ i64 min8_i64(i64 x) {
+#pragma unroll
+  for (u32 s = 4; s; s >>= 1) {
+    const i64 y = __shfl_xor_sync(FULLMASK, x, s);
+    x = y < x ? y : x;
+  }
+  return __shfl_sync(FULLMASK, x, 0);
 }
 
 template <int CAP, bool P2>
@@ -284,7 +292,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         v = toD ? totD - M.ds[lane].nfree : totP - M.ps[lane].nfree;
       }
     }
-    const u32 w = warp_argmin64((i64)v, lane, lane < cnt);
+    const u32 w = warp_argmin64((i64)v, lane < cnt);
     return w;
   };
 
@@ -294,19 +302,14 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     i64 td = arr < n ? A[arr] : INF;
     {
       const i64 tdl = (lane < X && M.ps[lane].nb > 0) ? M.ps[lane].tdisp : INF;
-      i64 m_ = tdl;
-#pragma unroll
-      for (u32 s = 16; s; s >>= 1) {
-        const i64 y = __shfl_xor_sync(FULLMASK, m_, s);
-        m_ = y < m_ ? y : m_;
-      }
+      const i64 m_ = min8_i64(tdl);
       td = m_ < td ? m_ : td;
     }
     // worker order: decode workers 0..y-1 first, then prefill workers (ord = lane)
     i64 tw = INF;
     if (lane < Y) tw = M.ds[lane].t;
     else if (lane < NW) tw = M.ps[lane - Y].t;
-    const u32 wsel = warp_argmin64(tw, lane, lane < NW);
+    const u32 wsel = warp_argmin64(tw, lane < NW);
     const i64 tb = __shfl_sync(FULLMASK, tw, wsel & 31u);
     const i64 tnext = td < tb ? td : tb;
     if (tnext == INF) {
@@ -430,11 +433,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
             const i64 tk = M.ds[lane].t;
             if (tk != INF && tk - 1 < c1) c1 = tk - 1;
           }
-#pragma unroll
-          for (u32 s = 16; s; s >>= 1) {
-            const i64 y = __shfl_xor_sync(FULLMASK, c1, s);
-            c1 = y < c1 ? y : c1;
-          }
+          c1 = min8_i64(c1);  // lanes < X (prefill workers) and < Y (decode workers) only
           cut = c1 < cut ? c1 : cut;
         }
         bool quiet = true, mem_check = false;
