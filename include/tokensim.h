@@ -321,7 +321,8 @@ typedef struct {
   uint64_t n_run;                           /* points run                               */
   uint64_t h2d_bytes;                       /* tables (first run on a device) + order   */
   uint64_t workspace_bytes;
-  uint32_t helper_mode;                     /* 1: one point per CTA with a helper warp      */
+  uint32_t helper_mode;                     /* one point per CTA with a helper warp: 1 with
+                                               extended stretches, 2 without; 0: 8 warps/SM */
   uint32_t n_heads;                         /* longest points given an SM of their own      */
 } tokensim_run_info;
 tokensim_status tokensim_get_run_info(const tokensim_sweep *h, tokensim_run_info *out);

@@ -706,7 +706,12 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   Layout L0 = make_layout(h, n_run, sms, 0);
   int occ = 0;
   const bool helper = L0.wpb == 1 && helper_run(h, n_run, sms);
-  e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general, !helper),
+  // extended stretches pay off while the chains have their SM nearly to themselves (<= 2 points
+  // per SM: C4 at 8 GPUs 122 -> 115 ms); beyond that their hot code costs more (C3 at 8 GPUs,
+  // ~4 per SM: 142 -> 162 ms).  TOKENSIM_XS=0/1 overrides (A/B).
+  bool xs = n_run <= 2ull * (u64)sms;
+  if (const char *ev = getenv("TOKENSIM_XS")) xs = atoi(ev) != 0;
+  e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general, !helper, xs),
                     (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, h->nwords_max, &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
@@ -788,7 +793,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.order = reinterpret_cast<const u32 *>(ws + L.order);
   P.queue = reinterpret_cast<u32 *>(ws + L.queue);
   P.sched = reinterpret_cast<u32 *>(ws + L.sched);
-  P.helper_mode = helper ? 1u : 0u;
+  P.helper_mode = helper ? (xs ? 1u : 2u) : 0u;
   P.rec = reinterpret_cast<tokensim_request_record *>(ws + L.rec);
   P.stats = reinterpret_cast<SimStats *>(ws + L.stats);
   P.trace = reinterpret_cast<tokensim_mem_sample *>(ws + L.trace);
@@ -856,7 +861,10 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
       const double span = (double)P.n_req / h->rates[c.rate];
       const u32 hwe = P.topology == TOKENSIM_PD_PAIR ? c.hw % P.n_hw : c.hw;  // decode worker dominates
       static const bool lpt_old = getenv("TOKENSIM_LPT_OLD") != nullptr;  // A/B: the round-1 estimate
-      const bool unified = !lpt_old && P.topology != TOKENSIM_PD_PAIR && !h->wl.multi_round && !trace_mode;
+      // the cost estimate orders throughput-bound runs (8 warps per SM); a latency-bound run (the
+      // helper kernel) is set by its longest chains, which span / T(1) -- iterations -- ranks better
+      // (C3 at 8 emulated GPUs: 142 ms by iterations, 163 ms by the cost estimate)
+      const bool unified = !lpt_old && !helper && P.topology != TOKENSIM_PD_PAIR && !h->wl.multi_round && !trace_mode;
       est[j] = {unified ? lpt_cost(h, (u32)((size_t)hwe * P.n_pol + c.pol), h->rates[c.rate])
                         : span / h->est_T1[(size_t)hwe * P.n_pol + c.pol],
                 (u32)j};

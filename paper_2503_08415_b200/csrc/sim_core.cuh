@@ -671,6 +671,9 @@ __device__ __forceinline__ void mr_cache_store(MrState &M, u32 c, u32 tokens, co
 // simulating warp's serial chain.  The log is a 256-entry ring in global memory; the two warps
 // hand over through counters in shared memory.  Every wait is bounded (~10 s of clock) and
 // raises TOKENSIM_PT_INTERNAL_ERROR instead of hanging.
+#ifndef TS_XS  // the helper kernel's extended stretches (0: sim_base_n.cu, for several points per SM)
+#define TS_XS 1
+#endif
 #ifndef TS_HELPER_WARP
 #define TS_HELPER_WARP 0
 #endif
@@ -782,7 +785,7 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
   // Extended stretches (carried stretch state, up to 64 iterations per stretch) only in the
   // latency-bound helper-warp kernel: they shorten a lone point's chain, but at 8 warps per SM
   // the larger hot code costs more in instruction fetch than it saves (DESIGN.md §8 A/B log).
-  constexpr bool XS = HELP;
+  constexpr bool XS = HELP && TS_XS;
   // Block ids off the simulation chain (HEV): every scheduling decision depends on block counts
   // only, so allocations and frees are logged as events in a per-warp ring and the helper warp
   // replays the ring into block ids (tables, bitmap, block digest).  The several-warps-per-SM
@@ -2373,7 +2376,7 @@ template <int CAP, int V, bool P2>
 __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
-  constexpr bool HELPK = V == 0 && TS_HELPER_WARP;  // one simulating warp + its helper per CTA
+  constexpr bool HELPK = (V == 0 || V == 5) && TS_HELPER_WARP;  // one simulating warp + its helper per CTA
   constexpr bool pd = V == 2 || V == 3;
   constexpr bool node = V == 3;
   const size_t base = smem_per_warp_bytes(CAP, P.nwords_max);
@@ -2490,16 +2493,16 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
 // V 0 with the helper warp: one simulating warp (wpb = 1) + the helper, and the hand-over
 // counters after the warp's shared memory
 template <int V>
-static __host__ __forceinline__ int sim_threads(int wpb) { return (V == 0 && TS_HELPER_WARP) ? 64 : wpb * 32; }
+static __host__ __forceinline__ int sim_threads(int wpb) { return ((V == 0 || V == 5) && TS_HELPER_WARP) ? 64 : wpb * 32; }
 // the helper's area: hand-over counters, its replayed bitmap (nwords_max words), 256 extraction slots
 static_assert(sizeof(HelperChan) <= kHelperChanBytes, "helper area (ts_internal.cuh)");
 template <int V>
 static __host__ __forceinline__ size_t sim_smem(size_t smem, u32 nwords_max) {
-  return (V == 0 && TS_HELPER_WARP) ? helper_cta_smem(smem, nwords_max) : smem;
+  return ((V == 0 || V == 5) && TS_HELPER_WARP) ? helper_cta_smem(smem, nwords_max) : smem;
 }
 template <int CAP, int V, bool P2>
 static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_t smem, cudaStream_t st) {
-  if (V == 0 && TS_HELPER_WARP && wpb != 1) return cudaErrorInvalidValue;
+  if ((V == 0 || V == 5) && TS_HELPER_WARP && wpb != 1) return cudaErrorInvalidValue;
   smem = sim_smem<V>(smem, p.nwords_max);
   cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, V, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -122,7 +122,8 @@ struct SweepParams {
   u64 pdn_bytes_per_warp;
   u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
   u32 full, all_p2;                       // 1: the full kernel variant (sim_full.cu); every block size a power of two
-  u32 n_sms, helper_mode;                 // SMs of the device; 1: lean kernel with a helper warp per point (variant 0)
+  u32 n_sms, helper_mode;                 // SMs of the device; lean kernel with a helper warp per point: 1 = with
+                                          // extended stretches (variant 0), 2 = without (variant 5)
   u32 n_heads, pad6;                      // variant 0: the first n_heads points (LPT order) each get an SM alone
   u32 *sched;                             // variant 0 with heads: per-SM arrival counts [256], SM states [256],
                                           // head ticket [1], head claims [n_heads] (zeroed per run)
@@ -173,6 +174,8 @@ cudaError_t launch_sim_node(const SweepParams &p, int cap, int warps_per_block, 
                             cudaStream_t st);
 cudaError_t launch_sim_base_c(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                               cudaStream_t st);
+cudaError_t launch_sim_base_n(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
+                              cudaStream_t st);
 // several warps per SM: the lean kernel with compact helpers (variant 4); one warp per SM:
 // variant 0, whose CTA adds a helper warp (sim_base.cu)
 // Shared memory of a variant-0 CTA: the simulating warp's area, then the helper's hand-over
@@ -184,15 +187,17 @@ inline size_t helper_cta_smem(size_t per_warp, u32 nwords_max) {
   return ((per_warp + 15) & ~(size_t)15) + kHelperChanBytes + 4 * (size_t)nwords_max + 1024;
 }
 inline bool helper_fits(size_t per_warp, u32 nwords_max) { return helper_cta_smem(per_warp, nwords_max) <= 227 * 1024; }
-inline int sim_variant(bool full, bool pd, bool pd_general, bool multi_warp = false) {
-  return !full ? (multi_warp ? 4 : 0) : !pd ? 1 : pd_general ? 3 : 2;
+// xs: the helper kernel with extended stretches (variant 0) rather than without (variant 5)
+inline int sim_variant(bool full, bool pd, bool pd_general, bool multi_warp = false, bool xs = true) {
+  return !full ? (multi_warp ? 4 : xs ? 0 : 5) : !pd ? 1 : pd_general ? 3 : 2;
 }
 inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                               cudaStream_t st) {
   (void)blocks;
   switch (sim_variant(p.full != 0, p.topology == TOKENSIM_PD_PAIR, p.pd_general != 0,
-                      !(p.helper_mode && warps_per_block == 1 && helper_fits(smem, p.nwords_max)))) {
+                      !(p.helper_mode && warps_per_block == 1 && helper_fits(smem, p.nwords_max)), p.helper_mode == 1)) {
     case 0: return launch_sim_base(p, cap, warps_per_block, blocks, smem, st);
+    case 5: return launch_sim_base_n(p, cap, warps_per_block, blocks, smem, st);
     case 4: return launch_sim_base_c(p, cap, warps_per_block, blocks, smem, st);
     case 1: return launch_sim_full(p, cap, warps_per_block, blocks, smem, st);
     case 2: return launch_sim_pair(p, cap, warps_per_block, blocks, smem, st);
@@ -215,6 +220,7 @@ cudaError_t sim_occupancy_full(int cap, int warps_per_block, size_t smem, u32 nw
 cudaError_t sim_occupancy_pair(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_node(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_base_c(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
+cudaError_t sim_occupancy_base_n(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 inline cudaError_t sim_occupancy(int variant, int cap, int warps_per_block, size_t smem, u32 nwords_max,
                                  int *blocks_per_sm) {
   switch (variant) {
@@ -222,6 +228,7 @@ inline cudaError_t sim_occupancy(int variant, int cap, int warps_per_block, size
     case 1: return sim_occupancy_full(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
     case 2: return sim_occupancy_pair(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
     case 4: return sim_occupancy_base_c(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
+    case 5: return sim_occupancy_base_n(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
     default: return sim_occupancy_node(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
   }
 }

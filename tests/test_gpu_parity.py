@@ -101,6 +101,30 @@ def test_lean_kernel_variants_agree(api):
         check_points(full, cfg, [0, 200, cfg.num_points - 1], records=True)
 
 
+def test_kernel_variants_byte_identical(api, monkeypatch):
+    """The same 384-point sweep through the three lean kernels the host chooses between --
+    8 independent warps per SM (variant 4), the helper-warp kernel without (variant 5) and with
+    (variant 0) extended stretches -- gives identical bytes (summaries, records)."""
+    cfg = si.c2(n_seeds=24)
+    runs = {}
+    for name, env in (("auto", {}), ("v4", {"TOKENSIM_HELPER": "0"}), ("v0", {"TOKENSIM_XS": "1"}),
+                      ("v5", {"TOKENSIM_XS": "0"})):
+        for k in ("TOKENSIM_HELPER", "TOKENSIM_XS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        sw = run_gpu(api, cfg)
+        runs[name] = (sw, sw.run_info()["helper_mode"])
+    for k in ("TOKENSIM_HELPER", "TOKENSIM_XS"):
+        monkeypatch.delenv(k, raising=False)
+    assert runs["v4"][1] == 0 and runs["v0"][1] == 1 and runs["v5"][1] == 2 and runs["auto"][1] == 2
+    ref = runs["auto"][0]
+    for name, (sw, _) in runs.items():
+        assert sw.summaries().tobytes() == ref.summaries().tobytes(), name
+        for p in (0, 191, 383):
+            assert sw.records(p).tobytes() == ref.records(p).tobytes(), (name, p)
+
+
 def _micro(rng):
     n = int(rng.integers(1, 80))
     a = np.sort(rng.integers(0, 3_000_000_000, n))
