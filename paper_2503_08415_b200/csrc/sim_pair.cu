@@ -1,5 +1,8 @@
-// sim_pair.cu -- the 1P:1D disaggregated pair kernel variant (a.9, sim_pd.cuh).
+// sim_pair.cu -- the 1P:1D disaggregated pair kernel variant (a.9, sim_pd.cuh).  Built with
+// the compact (out-of-line) helpers: its sweeps (C5: 8,192 pairs per GPU) put 8 warps on an SM,
+// where instruction fetch binds (C5 every-8th-point 3542 -> 3449 ms).
 #define TS_LOGS_BYREF 1
+#define TS_COMPACT 1
 
 #include "sim_core.cuh"
 
