@@ -671,6 +671,9 @@ __device__ __forceinline__ void mr_cache_store(MrState &M, u32 c, u32 tokens, co
 // simulating warp's serial chain.  The log is a 256-entry ring in global memory; the two warps
 // hand over through counters in shared memory.  Every wait is bounded (~10 s of clock) and
 // raises TOKENSIM_PT_INTERNAL_ERROR instead of hanging.
+#ifndef TS_SPEC  // A/B: the second stretch half's costs evaluated alongside the first
+#define TS_SPEC 0
+#endif
 #ifndef TS_XS  // the helper kernel's extended stretches (0: sim_base_n.cu, for several points per SM)
 #define TS_XS 1
 #endif
@@ -1199,6 +1202,13 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
         // lane-parallel cost of iteration k+lane: D = nR decodes, C_d grows by nR per iteration
         const u64 Cdj = Cd0 + (u64)lane * nR;
         const i64 Tj = iter_time_ns(K, 0, 0, 0, nR, Cdj, 0);
+        // extended-stretch kernel: the second half's times in the same basic block (the two
+        // evaluations and their scans interleave; unused when the first half is cut)
+        i64 Tj1s = 0, sc1s = 0;
+        if constexpr (XS && TS_SPEC) {
+          Tj1s = iter_time_ns(K, 0, 0, 0, nR, Cd0 + (u64)(32u + lane) * nR, 0);
+          sc1s = scan_incl_i64(Tj1s);
+        }
         const i64 tej = t + scan_incl_i64(Tj);
         const i64 tsj = tej - Tj;
         // cut: the stretch is the longest prefix of iterations that stay quiescent; the
@@ -1242,8 +1252,13 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
           nj1 = __shfl_sync(FULLMASK, hcl, B.mod(32u + lane) & 31u);
           Aj1 = __shfl_sync(FULLMASK, Aj, 31) + scan_incl(nj1);
           Cdj1 = Cd0 + (u64)(32u + lane) * nR;
-          Tj1 = iter_time_ns(K, 0, 0, 0, nR, Cdj1, 0);
-          tej1 = __shfl_sync(FULLMASK, tej, 31) + scan_incl_i64(Tj1);
+          if constexpr (TS_SPEC) {
+            Tj1 = Tj1s;
+            tej1 = __shfl_sync(FULLMASK, tej, 31) + sc1s;
+          } else {
+            Tj1 = iter_time_ns(K, 0, 0, 0, nR, Cdj1, 0);
+            tej1 = __shfl_sync(FULLMASK, tej, 31) + scan_incl_i64(Tj1);
+          }
           tsj1 = tej1 - Tj1;
           bool ok1 = ((u64)Aj1 <= nfree) && (Aj1 <= (u32)CAP) && (32u + lane < rm);
           if (P.horizon >= 0 && tsj1 >= P.horizon) ok1 = false;
