@@ -514,7 +514,7 @@ static u64 count_run(u64 begin, u64 end, u64 stride) { return end > begin ? (end
 // per iteration, ~22k per admission iteration (one per request; static batching: one per batch)
 // and ~14k more per request when the KV pool binds (preemption churn).  Fitted to round-2
 // per-point cycle counts of C3; it only orders the queue, never changes a result.
-static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate) {
+static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate, double *quiet = nullptr) {
   const auto &e = h->est_hp[hwpol];
   const double n = h->wl.num_requests, Eo = std::max(1.0, h->mean_o), ctx = h->mean_p + 0.5 * Eo;
   const double bmem = std::max(1.0, e.bmem / std::max(1.0, ctx));
@@ -530,6 +530,8 @@ static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate) {
   }
   // churn: Poisson arrivals and the length spread fill a memory-limited pool well before the
   // mean batch reaches it (C4 TP2 at lambda 4: b ~ 0.46 b_max, ~1.3 preemptions per request)
+  // iterations between two events (an arrival or a finish, each at rate lambda in steady state)
+  if (quiet) *quiet = 1.0 / (2.0 * rate * T(b));
   const bool tight = bmem < e.bmax && b > 0.35 * bmax;
   // admission iterations: one per request (continuous), one per batch (static: drain, then admit)
   const double adm = e.stat ? n / std::max(1.0, b) : n;
@@ -710,6 +712,18 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   // per SM: C4 at 8 GPUs 122 -> 115 ms); beyond that their hot code costs more (C3 at 8 GPUs,
   // ~4 per SM: 142 -> 162 ms).  TOKENSIM_XS=0/1 overrides (A/B).
   bool xs = n_run <= 2ull * (u64)sms;
+  if (xs && helper && !h->wl.multi_round && h->wl.len_dist != TOKENSIM_LEN_TRACE) {
+    // ... and only for chains with long quiet stretches: the median point's expected iterations
+    // between events >= 6 (C1 27: 0.83 -> 0.78 ms with them; C2 1.9: 7.51 -> 7.80 ms without)
+    std::vector<double> q(n_run);
+    for (u64 j = 0; j < n_run; ++j) {
+      const Coords c = decode_point(begin + j * stride, (u32)h->pol.size(), (u32)h->rates.size(),
+                                    (u32)h->seeds.size());
+      lpt_cost(h, (u32)((size_t)c.hw * h->pol.size() + c.pol), h->rates[c.rate], &q[j]);
+    }
+    std::nth_element(q.begin(), q.begin() + n_run / 2, q.end());
+    xs = q[n_run / 2] >= 6.0;
+  }
   if (const char *ev = getenv("TOKENSIM_XS")) xs = atoi(ev) != 0;
   e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general, !helper, xs),
                     (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, h->nwords_max, &occ);
