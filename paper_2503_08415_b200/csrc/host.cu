@@ -514,7 +514,8 @@ static u64 count_run(u64 begin, u64 end, u64 stride) { return end > begin ? (end
 // per iteration, ~22k per admission iteration (one per request; static batching: one per batch)
 // and ~14k more per request when the KV pool binds (preemption churn).  Fitted to round-2
 // per-point cycle counts of C3; it only orders the queue, never changes a result.
-static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate, double *quiet = nullptr) {
+static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate, double *quiet = nullptr,
+                       double *iters_out = nullptr) {
   const auto &e = h->est_hp[hwpol];
   const double n = h->wl.num_requests, Eo = std::max(1.0, h->mean_o), ctx = h->mean_p + 0.5 * Eo;
   const double bmem = std::max(1.0, e.bmem / std::max(1.0, ctx));
@@ -532,6 +533,7 @@ static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate, double *
   // mean batch reaches it (C4 TP2 at lambda 4: b ~ 0.46 b_max, ~1.3 preemptions per request)
   // iterations between two events (an arrival or a finish, each at rate lambda in steady state)
   if (quiet) *quiet = 1.0 / (2.0 * rate * T(b));
+  if (iters_out) *iters_out = iters;
   const bool tight = bmem < e.bmax && b > 0.35 * bmax;
   // admission iterations: one per request (continuous), one per batch (static: drain, then admit)
   const double adm = e.stat ? n / std::max(1.0, b) : n;
@@ -878,10 +880,15 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
       // the cost estimate orders throughput-bound runs (8 warps per SM); a latency-bound run (the
       // helper kernel) is set by its longest chains, which span / T(1) -- iterations -- ranks better
       // (C3 at 8 emulated GPUs: 142 ms by iterations, 163 ms by the cost estimate)
-      const bool unified = !lpt_old && !helper && P.topology != TOKENSIM_PD_PAIR && !h->wl.multi_round && !trace_mode;
-      est[j] = {unified ? lpt_cost(h, (u32)((size_t)hwe * P.n_pol + c.pol), h->rates[c.rate])
-                        : span / h->est_T1[(size_t)hwe * P.n_pol + c.pol],
-                (u32)j};
+      const bool unified = !lpt_old && P.topology != TOKENSIM_PD_PAIR && !h->wl.multi_round && !trace_mode;
+      static const int lpt_helper = getenv("TOKENSIM_LPT_HELPER") ? atoi(getenv("TOKENSIM_LPT_HELPER")) : 0;
+      double est_j = span / h->est_T1[(size_t)hwe * P.n_pol + c.pol];
+      if (unified && (!helper || lpt_helper)) {
+        double it_j = 0;
+        const double cst = lpt_cost(h, (u32)((size_t)hwe * P.n_pol + c.pol), h->rates[c.rate], nullptr, &it_j);
+        est_j = !helper ? cst : lpt_helper == 1 ? it_j : cst;
+      }
+      est[j] = {est_j, (u32)j};
     }
     if (const char *cf = getenv("TOKENSIM_LPT_COSTS")) {  // A/B experiments only: measured per-point costs
       if (FILE *f = fopen(cf, "rb")) {
