@@ -714,7 +714,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   // per SM: C4 at 8 GPUs 122 -> 115 ms); beyond that their hot code costs more (C3 at 8 GPUs,
   // ~4 per SM: 142 -> 162 ms).  TOKENSIM_XS=0/1 overrides (A/B).
   bool xs = n_run <= 2ull * (u64)sms;
-  if (xs && helper && !h->wl.multi_round && h->wl.len_dist != TOKENSIM_LEN_TRACE) {
+  if (xs && helper && n_run > 0 && !h->wl.multi_round && h->wl.len_dist != TOKENSIM_LEN_TRACE) {
     // ... and only for chains with long quiet stretches: the median point's expected iterations
     // between events >= 6 (C1 27: 0.83 -> 0.78 ms with them; C2 1.9: 7.51 -> 7.80 ms without)
     std::vector<double> q(n_run);
