@@ -125,6 +125,21 @@ def test_kernel_variants_byte_identical(api, monkeypatch):
             assert sw.records(p).tobytes() == ref.records(p).tobytes(), (name, p)
 
 
+def test_head_reservation_is_byte_identical(api, monkeypatch):
+    """TOKENSIM_HEADS=K (the K longest points each get an SM; the other CTAs there leave): every
+    queue position is claimed exactly once, so results are byte-identical to the default run."""
+    cfg = si.c2(n_seeds=24)
+    base = run_gpu(api, cfg)
+    for k in (8, 40):
+        monkeypatch.setenv("TOKENSIM_HEADS", str(k))
+        sw = run_gpu(api, cfg)
+        assert sw.run_info()["n_heads"] == k
+        assert sw.summaries().tobytes() == base.summaries().tobytes(), k
+        for p in (0, 100, 383):
+            assert sw.records(p).tobytes() == base.records(p).tobytes(), (k, p)
+    monkeypatch.delenv("TOKENSIM_HEADS", raising=False)
+
+
 def _micro(rng):
     n = int(rng.integers(1, 80))
     a = np.sort(rng.integers(0, 3_000_000_000, n))
