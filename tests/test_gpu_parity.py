@@ -104,18 +104,20 @@ def test_lean_kernel_variants_agree(api):
 def test_kernel_variants_byte_identical(api, monkeypatch):
     """The same 384-point sweep through the three lean kernels the host chooses between --
     8 independent warps per SM (variant 4), the helper-warp kernel without (variant 5) and with
-    (variant 0) extended stretches -- gives identical bytes (summaries, records)."""
+    (variant 0) extended stretches -- and through other queue orders and launch shapes gives
+    identical bytes (summaries, records)."""
     cfg = si.c2(n_seeds=24)
     runs = {}
     for name, env in (("auto", {}), ("v4", {"TOKENSIM_HELPER": "0"}), ("v0", {"TOKENSIM_XS": "1"}),
-                      ("v5", {"TOKENSIM_XS": "0"})):
-        for k in ("TOKENSIM_HELPER", "TOKENSIM_XS"):
+                      ("v5", {"TOKENSIM_XS": "0"}), ("v4-old-order", {"TOKENSIM_HELPER": "0", "TOKENSIM_LPT_OLD": "1"}),
+                      ("v4-wpb2", {"TOKENSIM_HELPER": "0", "TOKENSIM_WPB": "2", "TOKENSIM_BPS": "3"})):
+        for k in ("TOKENSIM_HELPER", "TOKENSIM_XS", "TOKENSIM_LPT_OLD", "TOKENSIM_WPB", "TOKENSIM_BPS"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         sw = run_gpu(api, cfg)
         runs[name] = (sw, sw.run_info()["helper_mode"])
-    for k in ("TOKENSIM_HELPER", "TOKENSIM_XS"):
+    for k in ("TOKENSIM_HELPER", "TOKENSIM_XS", "TOKENSIM_LPT_OLD", "TOKENSIM_WPB", "TOKENSIM_BPS"):
         monkeypatch.delenv(k, raising=False)
     assert runs["v4"][1] == 0 and runs["v0"][1] == 1 and runs["v5"][1] == 2 and runs["auto"][1] == 2
     ref = runs["auto"][0]
