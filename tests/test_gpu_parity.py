@@ -350,6 +350,24 @@ def test_pd_micro_configs(api):
         check_pd_points(sw, cfg, list(range(cfg.num_points)), iters=True)
 
 
+def test_full_trace_overflow_pd_and_node(api):
+    """FULL traces with a 600-byte budget per worker on a 1P:1D pair and a 2P:3D node: every
+    worker's stream keeps a prefix of whole iterations equal to the oracle's samples, and the
+    overflow bit is set."""
+    rng = np.random.default_rng(29)
+    for node in (False, True):
+        cfg = _micro_pd(rng)
+        while cfg.workload.num_requests < 30:
+            cfg = _micro_pd(rng)
+        w = cfg.workload
+        opts = replace(cfg.options, trace_mode=si.FULL, trace_cap_bytes=600, fast_forward=True,
+                       pd_prefill=2 if node else 1, pd_decode=3 if node else 1)
+        c = replace(cfg, workload=w, options=opts)
+        sw = run_gpu(api, c)
+        check_pd_points(sw, c, list(range(c.num_points)))
+        assert (sw.summaries()["status_flags"] & 1).any()
+
+
 def test_c5_reduced_grid(api):
     """C5's 16x16 (P, D) profile pairs x {SWAP, RECOMPUTE}, 3 of its rates, 300 requests per point."""
     base = si.c5()
