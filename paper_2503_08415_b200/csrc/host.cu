@@ -567,6 +567,7 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   // latency-bound chain; co-resident warps would only share the SM's LSU/MIO pipes)
   if (const char *e = getenv("TOKENSIM_WPB")) wpb = (u32)std::max(1, std::min(4, atoi(e)));
   else if ((u64)n_run <= (u64)sm_count || helper_run(h, n_run, sm_count)) wpb = 1;
+  if (h->pd_general) wpb = 1;  // the node kernel: one point per CTA of pd_y warps
   u32 bps = (u32)std::max<size_t>(1, (227 * 1024) / (per_warp * wpb));
   bps = std::min<u32>(bps, 16);
   if (blocks_per_sm_limit > 0) bps = std::min<u32>(bps, (u32)blocks_per_sm_limit);
@@ -612,8 +613,10 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   // nconv, next round / cached tokens / LRU prev / LRU next (u32) x nconv
   L.mr_per_warp = mr ? align256(n * 12 + nconv * 12 + nconv * 16 + 64) : 0;
   L.mr = take((size_t)L.warps_total * L.mr_per_warp);
-  L.evlog = take((size_t)L.warps_total * 1024 * 16);
-  L.itlog = take((size_t)L.warps_total * 256 * 64);
+  // the logs are per simulating warp: a node CTA has pd_y of them
+  const size_t log_warps = (size_t)L.warps_total * (h->pd_general ? h->pd_y : 1u);
+  L.evlog = take(log_warps * 1024 * 16);
+  L.itlog = take(log_warps * 256 * 64);
   L.total = o;
   return L;
 }
@@ -727,8 +730,9 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
     xs = q[n_run / 2] >= 6.0;
   }
   if (const char *ev = getenv("TOKENSIM_XS")) xs = atoi(ev) != 0;
+  // (the node kernel's occupancy is asked for its CTA of pd_y warps)
   e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general, !helper, xs),
-                    (int)h->cap, (int)L0.wpb, per_warp * L0.wpb, h->nwords_max, &occ);
+                    (int)h->cap, h->pd_general ? (int)h->pd_y : (int)L0.wpb, per_warp * L0.wpb, h->nwords_max, &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
   const Layout L = make_layout(h, n_run, sms, occ);

@@ -2392,11 +2392,9 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
   constexpr bool HELPK = (V == 0 || V == 5) && TS_HELPER_WARP;  // one simulating warp + its helper per CTA
-  constexpr bool pd = V == 2 || V == 3;
-  constexpr bool node = V == 3;
+  constexpr bool pd = V == 2;  // (the xP:yD node has a kernel of its own: sim_node_kernel, sim_pdn.cuh)
   const size_t base = smem_per_warp_bytes(CAP, P.nwords_max);
-  const size_t per_warp =
-      node ? pdn_smem_per_warp(CAP, P.nwords_max, P.pd_x, P.pd_y) : base + (pd ? smem_pd_extra(CAP, P.nwords_max) : 0);
+  const size_t per_warp = base + (pd ? smem_pd_extra(CAP, P.nwords_max) : 0);
   volatile HelperChan *ch = nullptr;
   if constexpr (HELPK) {
     unsigned char *hb = smem_raw + ((per_warp + 15) & ~(size_t)15);
@@ -2492,8 +2490,7 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
       __syncwarp();
       if (lane == 0) ch->state = 1u;
     }
-    if constexpr (V == 3) simulate_pdn<CAP, P2>(P, j, smem_raw + wib * per_warp, bt);
-    else if constexpr (V == 2) simulate_pd<CAP, P2>(P, j, S, smem_raw + wib * per_warp + base, bt);
+    if constexpr (V == 2) simulate_pd<CAP, P2>(P, j, S, smem_raw + wib * per_warp + base, bt);
     else simulate_unified<CAP, V == 1, P2>(P, j, S, bt, ch);  // V 4: the lean one built with TS_COMPACT
   }
   if constexpr (HELPK) {

@@ -1,6 +1,7 @@
 // sim_pdn.cuh -- NEXT-1: the xP:yD disaggregated node with a global scheduler (SURVEY §8(f)
-// NEXT-1; readings R-X1..R-X6 in DESIGN.md).  Included by sim.cu after sim_pd.cuh, inside
-// namespace ts; one warp simulates one (prefill profile, decode profile) point.
+// NEXT-1; readings R-X1..R-X6 in DESIGN.md).  Included by sim_core.cuh after sim_pd.cuh, inside
+// namespace ts.  One CTA simulates one (prefill profile, decode profile) point: warp j runs
+// decode worker j, and warp 0 also runs the global scheduler and the prefill workers.
 //
 // x prefill workers and y decode workers run the a.9 worker loops; the
 // global scheduler dispatches every arrival to a prefill worker and,
@@ -10,12 +11,28 @@
 // decode workers first, then prefill workers, lower index first.  Each decode worker pulls its
 // pending FIFO onto its own ingress link.
 //
-// Data: per-worker scalars live in shared memory (loaded into registers for one boundary);
-// decode worker j owns an id-sorted slot array + bitmap in shared memory exactly like the pair's
-// D; prefill workers own a bitmap each and share one batch table.  Per warp in global memory:
-// the decode FIFOs, the prefill queues / in-flight batches / holder lists, and per-request
-// transfer ends and prefill block lists (a prefill worker frees a holder's blocks at its first
-// boundary >= that holder's transfer end, in any order).
+// Parallel decode workers (conservative epochs).  Decode workers interact with the rest of the
+// node only through dispatches to them (which read their state) and through their pulls (which
+// release prefill blocks at the transfer end).  The scheduler warp computes an epoch horizon H no
+// dispatch can precede: the next known end-of-prefill dispatch, and -- since a prefill batch
+// dispatches no earlier than one minimal prefill iteration (Tlb) after it starts -- the next
+// prefill boundary + Tlb, the next arrival + Tlb, and (while a prefill worker is idle with
+// queued requests, which a pull's block release could wake) the next decode boundary + Tlb.
+// Then (1) every decode warp processes its own boundaries before H in parallel (quiet stretches
+// cut at H), and (2) warp 0 processes the arrivals and prefill boundaries before H in time order
+// and the dispatch events at H.  Decode boundaries precede prefill boundaries at equal times and
+// dispatches precede boundaries at equal times, as in the sequential order; a pull that happens
+// after a prefill boundary in time but before it in processing only lowers that worker's
+// holder minimum, which the boundary recomputes from the same transfer ends (R-X6), so the
+// result is the sequential one byte for byte (the node parity tests compare against the oracle's
+// sequential loop).
+//
+// Data: per-worker scalars live in shared memory; decode worker j owns an id-sorted slot array +
+// bitmap + its own requester lists in shared memory exactly like the pair's D; prefill workers own
+// a bitmap each and share one batch table.  Per CTA in global memory: the decode FIFOs, the
+// prefill queues / in-flight batches / holder lists, and per-request transfer ends and prefill
+// block lists (a prefill worker frees a holder's blocks at its first boundary >= that holder's
+// transfer end, in any order).
 
 #pragma once
 // (included inside namespace ts)
@@ -34,26 +51,50 @@ struct PScal {  // one prefill worker
   u32 hint, qhead, qtail, nb, cur, nhold, idle, pad;
   TraceAcc TA;
 };
+struct PdnPart {  // one warp's partial outputs (summed by warp 0 at the end)
+  u64 req_iters, npre, swo, swi, nfin, n_xfer, xbytes, ff_iters, ff_runs, dig_s, dig_b;
+  i64 last_fin;
+  i64 tfin;         // start of the latest iteration in which its decode worker finished requests
+  u32 flags, done;  // done: requests its decode worker finished (read by warp 0 every epoch)
+  FullEnc fe;       // its decode worker's FULL trace stream state
+};
+struct PdnCtl {
+  i64 H;
+  u32 stop, itcur;  // itcur: next free iteration-record position (warps flush in any order)
+};
 
 struct PdnSmem {
   u32 *req_cum, *req_pt, *scratch, *pid, *ppl, *pol, *pinfo;
   PScal *ps;
   DScal *ds;
-  u32 *bmP;        // [x][nwmax]
+  u32 *bmP;              // [x][nwmax]
   unsigned char *dbase;  // decode worker j at dbase + j * dstride
   size_t dstride;
+  u32 *dscr;             // decode warp j's requester lists at dscr + j * (2 cap + 64)
+  PdnPart *part;         // [y]
+  PdnCtl *ctl;
 };
 
 __host__ __device__ inline size_t pdn_dworker_bytes(u32 cap, u32 nw) {
   return ((size_t)cap * (8 * 4 + 4 * 5) + (size_t)(cap / 32) * 4 + (size_t)nw * 4 + 15) & ~(size_t)15;
 }
-__host__ __device__ inline size_t pdn_smem_per_warp(u32 cap, u32 nw, u32 x, u32 y) {
+__host__ __device__ inline size_t pdn_base_bytes(u32 cap, u32 nw, u32 x, u32 y) {
   size_t b = (size_t)cap * 4 * 6 + 64 * 4;
   b = (b + 15) & ~(size_t)15;
   b += (size_t)x * sizeof(PScal) + (size_t)y * sizeof(DScal);
   b = (b + 15) & ~(size_t)15;
   b += ((size_t)x * nw * 4 + 15) & ~(size_t)15;
   b += (size_t)y * pdn_dworker_bytes(cap, nw);
+  return b;
+}
+// shared memory of one node CTA (one point)
+__host__ __device__ inline size_t pdn_smem_per_warp(u32 cap, u32 nw, u32 x, u32 y) {
+  size_t b = pdn_base_bytes(cap, nw, x, y);
+  b += (size_t)y * ((size_t)cap * 8 + 64 * 4);
+  b = (b + 15) & ~(size_t)15;
+  b += (size_t)y * sizeof(PdnPart);
+  b = (b + 15) & ~(size_t)15;
+  b += (sizeof(PdnCtl) + 15) & ~(size_t)15;
   return b;
 }
 
@@ -77,10 +118,18 @@ __device__ __forceinline__ PdnSmem carve_pdn(unsigned char *base, u32 cap, u32 n
   o += ((size_t)x * nw * 4 + 15) & ~(size_t)15;
   M.dbase = base + o;
   M.dstride = pdn_dworker_bytes(cap, nw);
+  o += (size_t)y * M.dstride;
+  M.dscr = reinterpret_cast<u32 *>(base + o);
+  o += (size_t)y * ((size_t)cap * 8 + 64 * 4);
+  o = (o + 15) & ~(size_t)15;
+  M.part = reinterpret_cast<PdnPart *>(base + o);
+  o += (size_t)y * sizeof(PdnPart);
+  o = (o + 15) & ~(size_t)15;
+  M.ctl = reinterpret_cast<PdnCtl *>(base + o);
   return M;
 }
 
-// the WarpSmem view of decode worker j (slots, bitmap) plus the shared requester lists
+// the WarpSmem view of decode worker j (slots, bitmap) plus its own requester lists
 __device__ __forceinline__ WarpSmem dview(const PdnSmem &M, u32 j, u32 cap, u32 **stt) {
   WarpSmem S;
   unsigned char *b = M.dbase + (size_t)j * M.dstride;
@@ -97,13 +146,13 @@ __device__ __forceinline__ WarpSmem dview(const PdnSmem &M, u32 j, u32 cap, u32 
   *stt = p32 + 4 * cap;
   S.btfree = p32 + 5 * cap;
   S.bitmap = p32 + 5 * cap + cap / 32;
-  S.req_cum = M.req_cum;
-  S.req_pt = M.req_pt;
-  S.scratch = M.scratch;
+  u32 *sc = M.dscr + (size_t)j * (2 * cap + 64);
+  S.req_cum = sc;
+  S.req_pt = sc + cap;
+  S.scratch = sc + 2 * cap;
   return S;
 }
 
-// warp argmin over (key, order) for lanes < cnt; returns the winning lane (or 0xffffffff)
 // argmin of key over lanes 0..7 (a node has at most 8 workers; lane = worker order), ties to
 // the lower lane; three butterfly steps within each group of 8 lanes, then lane 0's answer
 __device__ __forceinline__ u32 warp_argmin64(i64 key, bool valid) {
@@ -129,12 +178,26 @@ __device__ __forceinline__ i64 min8_i64(i64 x) {
   }
   return __shfl_sync(FULLMASK, x, 0);
 }
+__device__ __forceinline__ i64 sat_add(i64 a, i64 b) { return a >= INT64_MAX - b ? INT64_MAX : a + b; }
+
+// iteration log of one warp of a node CTA: its records go to positions claimed from the CTA's
+// shared cursor (the warps flush in any order; node records are compared by (worker, k))
+static __device__ __noinline__ void pdn_it_flush(Logs &L, u32 *itcur) {
+  u32 base = 0;
+  if (lane_id() == 0) base = atomicAdd(itcur, L.nit);
+  L.it_base = __shfl_sync(FULLMASK, base, 0);
+  it_flush(L);
+}
+__device__ __forceinline__ void pdn_it_reserve(Logs &L, u32 cnt, u32 *itcur) {
+  if (L.nit + cnt > ITCAP) pdn_it_flush(L, itcur);
+}
 
 template <int CAP, bool P2>
-__device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u32 *bt) {
+__device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u32 *bt, u32 wib) {
   const u32 lane = lane_id();
   const u32 ltm = lanemask_lt();
   const u32 X = P.pd_x, Y = P.pd_y, NW = X + Y;
+  const bool COORD = wib == 0;  // warp 0: the global scheduler and the prefill workers, too
   const u64 point = P.begin + j * P.stride;
   const Coords cd = decode_point(point, P.n_pol, P.n_rates, P.n_seeds);
   const u32 hwP = cd.hw / P.n_hw, hwD = cd.hw % P.n_hw;
@@ -161,10 +224,12 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   const i64 wm = (i64)PL.wm;
   const i64 INF = INT64_MAX;
   const long long clk0 = clock64();
-  const u32 gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const u32 gwarp = blockIdx.x * Y + wib;  // this warp's logs
   const PdnSmem M = carve_pdn(smem, CAP, P.nwords_max, X, Y);
-  // per-warp global scratch
-  unsigned char *gb = P.pdn_scratch + (size_t)gwarp * P.pdn_bytes_per_warp;
+  PdnCtl *ctl = M.ctl;
+  u32 *itcur = &ctl->itcur;
+  // per-CTA global scratch
+  unsigned char *gb = P.pdn_scratch + (size_t)blockIdx.x * P.pdn_bytes_per_warp;
   FifoEnt *fifo0 = reinterpret_cast<FifoEnt *>(gb);                  // [y][n]
   u32 *qP0 = reinterpret_cast<u32 *>(fifo0 + (size_t)Y * n);         // [x][n] dispatch queues
   u32 *hold0 = qP0 + (size_t)X * n;                                  // [x][n] holder lists
@@ -173,76 +238,89 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   u32 *pblk = reinterpret_cast<u32 *>(reqx + n);                     // [n][btl] prefill block lists
   u32 *btD0 = bt;                                                    // [y][CAP][btl]
   u32 *btP = bt + (size_t)Y * CAP * btl;                             // shared prefill batch table
-  WarpSmem SP;  // the prefill batch view for the allocator
+  WarpSmem SP;  // the prefill batch view for the allocator (warp 0)
   SP.id = M.pid;
   SP.info = M.pinfo;
   SP.req_cum = M.req_cum;
   SP.req_pt = M.req_pt;
   SP.scratch = M.scratch;
+  const TraceAcc ta0 = {0, 0, 0, (i64)P.bin_ns, 0, 0};
+  // this warp's decode worker
+  const u32 dj = wib;
+  const u32 wid = X + dj;
+  const u32 koffD = 2 * wid;
+  u32 *stt;
+  const WarpSmem S = dview(M, dj, CAP, &stt);
+  FifoEnt *fifo = fifo0 + (size_t)dj * n;
+  u32 *btD = btD0 + (size_t)dj * CAP * btl;
+  tokensim_mem_sample *trcD = trc0 + (size_t)wid * P.trace_cap;
 
-  // ---- init
+  // ---- init (every warp: its decode worker; warp 0: the prefill workers and the controls)
   {
+    const u32 tid = threadIdx.x, nth = blockDim.x;
     ulonglong2 *r2 = reinterpret_cast<ulonglong2 *>(rec);
     const ulonglong2 z = make_ulonglong2(0ull, 0ull);
     #pragma unroll 1
-    for (u32 x = lane; x < 2 * n; x += 32) r2[x] = z;
-    for (u32 w = 0; w < Y; ++w) {
-      u32 *stt;
-      const WarpSmem S = dview(M, w, CAP, &stt);
+    for (u32 x = tid; x < 2 * n; x += nth) r2[x] = z;
+    #pragma unroll 1
+    for (u32 x = tid; x < n; x += nth) reqx[x] = INF;
+    {
       const u32 fw = (u32)(totD >> 5), tl = (u32)(totD & 31u);
       #pragma unroll 1
       for (u32 q = lane; q < nwD; q += 32) S.bitmap[q] = q < fw ? 0xffffffffu : (q == fw && tl ? ((1u << tl) - 1u) : 0u);
       #pragma unroll 1
       for (u32 q = lane; q < CAP / 32; q += 32) S.btfree[q] = 0xffffffffu;
     }
-    for (u32 w = 0; w < X; ++w) {
-      u32 *bm = M.bmP + (size_t)w * P.nwords_max;
-      const u32 fw = (u32)(totP >> 5), tl = (u32)(totP & 31u);
-      #pragma unroll 1
-      for (u32 q = lane; q < nwP; q += 32) bm[q] = q < fw ? 0xffffffffu : (q == fw && tl ? ((1u << tl) - 1u) : 0u);
-    }
-    #pragma unroll 1
-    for (u32 x = lane; x < CAP; x += 32) M.pinfo[x] = x;
-    #pragma unroll 1
-    for (u32 x = lane; x < n; x += 32) reqx[x] = INF;
     if (lane == 0) {
-      const TraceAcc ta0 = {0, 0, 0, (i64)P.bin_ns, 0, 0};
+      DScal s;
+      s.t = INF;  // a decode worker starts idle: a dispatch wakes it
+      s.link_busy = 0;
+      s.xhead_end = INF;
+      s.last = 0;
+      s.k = 0;
+      s.nfree = totD;
+      s.ffw = s.ffk = s.peak = s.bns = 0;
+      s.hint = 0;
+      s.nD = s.nX = s.nQ = s.nRun = s.rmin = s.fhead = s.ftail = 0;
+      s.idle = 1;
+      s.pad = 0;
+      s.TA = ta0;
+      M.ds[dj] = s;
+      M.part[dj].done = 0;
+      M.part[dj].flags = 0;
+    }
+    if (COORD) {
       for (u32 w = 0; w < X; ++w) {
-        PScal s;
-        s.t = INF;  // a prefill worker starts idle: a dispatch wakes it
-        s.tdisp = INF;
-        s.last = 0;
-        s.hmin = INF;
-        s.k = 0;
-        s.nfree = totP;
-        s.hint = 0;
-        s.qhead = s.qtail = s.nb = s.cur = s.nhold = 0;
-        s.idle = 1;
-        s.pad = 0;
-        s.TA = ta0;
-        M.ps[w] = s;
+        u32 *bm = M.bmP + (size_t)w * P.nwords_max;
+        const u32 fw = (u32)(totP >> 5), tl = (u32)(totP & 31u);
+        #pragma unroll 1
+        for (u32 q = lane; q < nwP; q += 32) bm[q] = q < fw ? 0xffffffffu : (q == fw && tl ? ((1u << tl) - 1u) : 0u);
       }
-      for (u32 w = 0; w < Y; ++w) {
-        DScal s;
-        s.t = INF;  // a decode worker starts idle too
-        s.link_busy = 0;
-        s.xhead_end = INF;
-        s.last = 0;
-        s.k = 0;
-        s.nfree = totD;
-        s.ffw = s.ffk = s.peak = s.bns = 0;
-        s.hint = 0;
-        s.nD = s.nX = s.nQ = s.nRun = s.rmin = s.fhead = s.ftail = 0;
-        s.idle = 1;
-        s.pad = 0;
-        s.TA = ta0;
-        M.ds[w] = s;
+      #pragma unroll 1
+      for (u32 x = lane; x < CAP; x += 32) M.pinfo[x] = x;
+      if (lane == 0) {
+        for (u32 w = 0; w < X; ++w) {
+          PScal s;
+          s.t = INF;  // a prefill worker starts idle: a dispatch wakes it
+          s.tdisp = INF;
+          s.last = 0;
+          s.hmin = INF;
+          s.k = 0;
+          s.nfree = totP;
+          s.hint = 0;
+          s.qhead = s.qtail = s.nb = s.cur = s.nhold = 0;
+          s.idle = 1;
+          s.pad = 0;
+          s.TA = ta0;
+          M.ps[w] = s;
+        }
+        ctl->itcur = 0;
+        ctl->stop = 0;
+        ctl->H = INF;
       }
     }
-    __syncwarp();
+    __syncthreads();
   }
-  u32 arr = 0, n_done = 0;
-  u64 rrP = 0, rrD = 0;
   Logs L;
   L.ev = P.evlog + (size_t)gwarp * EVCAP;
   L.it = P.itlog + (size_t)gwarp * ITCAP * 4;
@@ -253,19 +331,33 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   L.dig_b = 0;
   L.nev = 0;
   L.nit = 0;
-  u64 req_iters = 0, npre = 0, swo = 0, swi = 0, nrej_tot = 0, nfin_tot = 0, n_xfer = 0, xbytes = 0;
+  // this warp's partial outputs
+  u64 req_iters = 0, npre = 0, swo = 0, swi = 0, nfin_tot = 0, n_xfer = 0, xbytes = 0;
   u64 ff_iters = 0, ff_runs = 0;
-  u32 flags = 0;
-  i64 last_fin = 0;
+  u32 flags = 0, done_w = 0;
+  i64 last_fin = 0, tfin_w = 0;
+  // warp 0 only: the scheduler's state
+  u32 arr = 0, n_done_c = 0;
+  u64 rrP = 0, rrD = 0, nrej_tot = 0;
   const bool ff_on = P.ff_enable != 0;
   const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
   const bool FULLT = P.trace_mode == TOKENSIM_TRACE_FULL;
   const i64 W = (i64)P.bin_ns;
-  FullEnc FE[PDN_MAXW];  // FULL: each worker's compressed stream (lane-uniform, thread-local)
-  for (u32 w = 0; w < PDN_MAXW; ++w) FE[w] = {0, 0, 0, 0, 0, 0};
+  FullEnc fe = {0, 0, 0, 0, 0, 0};  // this warp's decode worker's FULL stream (lane-uniform)
+  FullEnc FEp[PDN_MAXW];            // warp 0: the prefill workers' streams
+  for (u32 w = 0; w < PDN_MAXW; ++w) FEp[w] = {0, 0, 0, 0, 0, 0};
+  // a prefill batch takes at least one minimal prefill iteration (1 prompt of 1 token; every
+  // c.5 term grows with the batch), less a margin for rounding: dispatches come >= Tlb after a
+  // batch starts
+  i64 Tlb;
+  {
+    const i64 t1 = iter_time_ns(KP, 1, 1, 1, 0, 0, 0);
+    Tlb = t1 - (t1 >> 6) - 1;
+    if (Tlb < 1) Tlb = 1;
+  }
   auto fold_iter = [&](u64 kk, u32 worker, i64 ts, i64 T, u64 Sp, u64 D_, u64 Np, u64 Cd, u64 m, u64 nres,
                        u64 nadm, u64 nrej, u64 nfin, u64 blocks) {
-    it_reserve(L, 1);
+    pdn_it_reserve(L, 1, itcur);
     if (lane == 0) it_put(L, 0, kk | ((u64)worker << 40), ts, T, Np, Cd, blocks, Sp, D_, m, nres, nadm, nfin, nrej);
     L.nit += 1;
   };
@@ -296,300 +388,650 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     return w;
   };
 
+  i64 td_next = INF;  // warp 0: the next known end-of-prefill dispatch
   while (true) {
-    if (n_done == n) break;
-    // ---- the next event: dispatches (arrivals, end-of-prefill) before worker boundaries
-    i64 td = arr < n ? A[arr] : INF;
-    {
-      const i64 tdl = (lane < X && M.ps[lane].nb > 0) ? M.ps[lane].tdisp : INF;
-      const i64 m_ = min8_i64(tdl);
-      td = m_ < td ? m_ : td;
-    }
-    // worker order: decode workers 0..y-1 first, then prefill workers (ord = lane)
-    i64 tw = INF;
-    if (lane < Y) tw = M.ds[lane].t;
-    else if (lane < NW) tw = M.ps[lane - Y].t;
-    const u32 wsel = warp_argmin64(tw, lane < NW);
-    const i64 tb = __shfl_sync(FULLMASK, tw, wsel & 31u);
-    const i64 tnext = td < tb ? td : tb;
-    if (tnext == INF) {
-      flags |= TOKENSIM_PT_INTERNAL_ERROR;  // every worker waits: cannot happen under validation
-      break;
-    }
-    if (P.horizon >= 0 && tnext >= P.horizon) {
-      flags |= TOKENSIM_PT_HORIZON_HIT;
-      break;
-    }
-    if (td <= tb) {
-      // ================================================ dispatch events at td, request-id order
-      if (lane == 0)
-        for (u32 w = 0; w < X; ++w)
-          if (M.ps[w].nb > 0 && M.ps[w].tdisp == td) M.ps[w].cur = 0;
-      __syncwarp();
-      while (true) {
-        // the smallest id among completing batches' heads, else an arrival at td
-        u32 hid = 0xffffffffu;
+    // ============================================================ epoch horizon (warp 0)
+    if (COORD) {
+      u32 nd = n_done_c;
+      u32 ef = flags;
+      for (u32 w = 0; w < Y; ++w) {
+        nd += M.part[w].done;
+        ef |= M.part[w].flags;
+      }
+      i64 H = INF;
+      u32 stop = 0;
+      if (nd == n || (ef & TOKENSIM_PT_INTERNAL_ERROR)) {
+        stop = 1;
+      } else {
+        const i64 ta = arr < n ? A[arr] : INF;
+        i64 tdk = INF, tp = INF, tdm = INF;
+        bool blk = false;
         if (lane < X) {
           const PScal &p = M.ps[lane];
-          if (p.nb > 0 && p.tdisp == td && p.cur < p.nb) hid = batch0[(size_t)lane * CAP + p.cur];
+          if (p.nb > 0) tdk = p.tdisp;
+          tp = p.t;
+          blk = p.idle && p.qhead < p.qtail;
         }
-        const u32 mid = __reduce_min_sync(FULLMASK, hid);
-        if (mid != 0xffffffffu) {
-          const u32 src = __ffs(__ballot_sync(FULLMASK, hid == mid)) - 1;
-          if (lane == 0) M.ps[src].cur += 1;
-          __syncwarp();
-          if (OU[mid] > 1) {  // o = 1 finished on its prefill worker
-            const u32 dj = pick(true, td);
-            if (lane == 0) {
-              DScal &d = M.ds[dj];
-              FifoEnt e;
-              e.id = mid;
-              e.seg = src;  // the prefill worker holding its blocks
-              e.len = B.cdiv(PR[mid]);
-              e.pad = 0;
-              e.join = td;
-              e.xend = INF;
-              fifo0[(size_t)dj * n + d.ftail] = e;
-              d.ftail += 1;
-              if (d.idle && td < d.t) d.t = td;
-            }
-            __syncwarp();
+        if (lane < Y) tdm = M.ds[lane].t;
+        tdk = min8_i64(tdk);
+        tp = min8_i64(tp);
+        tdm = min8_i64(tdm);
+        const bool blocked = __ballot_sync(FULLMASK, blk) != 0u;
+        i64 tall = ta < tdk ? ta : tdk;
+        tall = tp < tall ? tp : tall;
+        tall = tdm < tall ? tdm : tall;
+        if (tall == INF) {
+          flags |= TOKENSIM_PT_INTERNAL_ERROR;  // every worker waits: cannot happen under validation
+          stop = 1;
+        } else if (P.horizon >= 0 && tall >= P.horizon) {
+          flags |= TOKENSIM_PT_HORIZON_HIT;
+          stop = 1;
+        } else {
+          H = tdk;
+          const i64 h1 = sat_add(ta, Tlb), h2 = sat_add(tp, Tlb);
+          H = h1 < H ? h1 : H;
+          H = h2 < H ? h2 : H;
+          if (blocked) {
+            const i64 h3 = sat_add(tdm, Tlb);
+            H = h3 < H ? h3 : H;
           }
-          continue;
+          if (P.horizon >= 0 && P.horizon < H) H = P.horizon;
         }
-        if (arr < n && A[arr] == td) {
-          const u32 pi = pick(false, td);
-          if (lane == 0) {
-            PScal &p = M.ps[pi];
-            qP0[(size_t)pi * n + p.qtail] = arr;
-            p.qtail += 1;
-            if (p.idle && td < p.t) p.t = td;
-          }
-          __syncwarp();
-          ++arr;
-          continue;
-        }
-        break;
+        td_next = tdk;
       }
-      if (lane == 0)
-        for (u32 w = 0; w < X; ++w)
-          if (M.ps[w].nb > 0 && M.ps[w].tdisp == td) {
-            M.ps[w].nb = 0;
-            M.ps[w].tdisp = INF;
-          }
-      __syncwarp();
-      continue;
+      if (lane == 0) {
+        ctl->H = H;
+        ctl->stop = stop;
+      }
     }
-
-    if (wsel < Y) {
-      // ================================================================ D_j boundary
-      const u32 dj = wsel;
-      const u32 wid = X + dj;
-      const u32 koff = 2 * wid;
-      u32 *stt;
-      const WarpSmem S = dview(M, dj, CAP, &stt);
-      FifoEnt *fifo = fifo0 + (size_t)dj * n;
-      u32 *btD = btD0 + (size_t)dj * CAP * btl;
-      tokensim_mem_sample *trcD = trc0 + (size_t)wid * P.trace_cap;
+    __syncthreads();
+    if (ctl->stop) break;
+    const i64 H = ctl->H;
+    // ============================================== decode phase: every D_j boundary before H
+    {
       DScal d = M.ds[dj];
-      const i64 t = d.t;
-      // 1. finished transfers become runnable (the in-flight tail completes in FIFO order)
-      // (transfers on this worker's link end in pull order; slots are id-sorted, so find by id)
-      while (d.nX > 0 && d.xhead_end <= t) {
-        const u32 xid = fifo[d.fhead - d.nX].id;
-        #pragma unroll 1
-        for (u32 b0 = 0; b0 < d.nD; b0 += 32) {
-          const u32 jj = b0 + lane;
-          const u32 hit = __ballot_sync(FULLMASK, jj < d.nD && S.id[jj] == xid);
-          if (hit) {
-            if (lane == 0) stt[b0 + (u32)(__ffs(hit) - 1)] = ST_RUN;
-            break;
-          }
-        }
-        --d.nX;
-        ++d.nRun;
-        d.xhead_end = d.nX ? fifo[d.fhead - d.nX].xend : INF;
-      }
-      __syncwarp();
-      bool ff_done = false;
-      // ---------------------------------------------------------- D fast-forward (H3)
-      // Quiescent decode stretch: no transfer completes, nothing is pulled or resumed, nothing
-      // is preempted, and no dispatch (which reads this worker's state or feeds its FIFO) can
-      // happen before the stretch's iterations: cut at the next arrival, every prefill
-      // worker's next boundary and every pending end-of-prefill dispatch.
-      if (ff_on && d.nRun > 0 && d.rmin >= 2 && (d.nfree > d.ffw || d.k >= d.ffk)) {
-        i64 cut = arr < n ? A[arr] : INF;  // iterations with start > cut are excluded
-        {
-          i64 c1 = INF;
-          if (lane < X) {
-            const PScal &p = M.ps[lane];
-            c1 = p.t;
-            if (p.nb > 0 && p.tdisp - 1 < c1) c1 = p.tdisp - 1;
-          }
-          // another decode worker's pull can wake an idle prefill worker (its holder's blocks
-          // come back), whose next batch may be dispatched here: cut before such a boundary
-          const bool p_idle = __ballot_sync(FULLMASK, lane < X && M.ps[lane].idle) != 0u;
-          if (p_idle && lane < Y && lane != dj && M.ds[lane].fhead < M.ds[lane].ftail) {
-            const i64 tk = M.ds[lane].t;
-            if (tk != INF && tk - 1 < c1) c1 = tk - 1;
-          }
-          c1 = min8_i64(c1);  // lanes < X (prefill workers) and < Y (decode workers) only
-          cut = c1 < cut ? c1 : cut;
-        }
-        bool quiet = true, mem_check = false;
-        u32 need_h = 0;
-        const u32 nA0 = d.nD;  // all slots (states are checked)
-        if (d.nQ > 0) {
-          u32 qpos = 0;
+      const u32 koff = koffD;
+      while (d.t < H) {
+        const i64 t = d.t;
+        // 1. finished transfers become runnable (the in-flight tail completes in FIFO order)
+        // (transfers on this worker's link end in pull order; slots are id-sorted, so find by id)
+        while (d.nX > 0 && d.xhead_end <= t) {
+          const u32 xid = fifo[d.fhead - d.nX].id;
           #pragma unroll 1
-          for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+          for (u32 b0 = 0; b0 < d.nD; b0 += 32) {
             const u32 jj = b0 + lane;
-            const u32 qb = __ballot_sync(FULLMASK, jj < nA0 && stt[jj] == ST_QUEUED);
-            if (qb) {
-              qpos = b0 + (u32)(__ffs(qb) - 1);
+            const u32 hit = __ballot_sync(FULLMASK, jj < d.nD && S.id[jj] == xid);
+            if (hit) {
+              if (lane == 0) stt[b0 + (u32)(__ffs(hit) - 1)] = ST_RUN;
               break;
             }
           }
-          u32 tokq;
-          if (SWAPM) {
-            const u32 c = S.ctx[qpos];
-            need_h = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
-            tokq = 1;
-          } else {
-            const u32 id = S.id[qpos];
-            tokq = PR[id] + (OU[id] - S.rem[qpos]);
-            need_h = B.cdiv(tokq);
-          }
-          if (!((u64)d.nRun + d.nX + 1 > mns || (u64)d.nRun + tokq > mbt)) {
-            mem_check = true;
-            if ((i64)d.nfree - (i64)d.nRun - (i64)need_h >= wm) quiet = false;
-          }
-        } else if (!STATICP && d.fhead < d.ftail) {
-          // a visible pending head (every FIFO entry is visible): blocked now => blocked later
-          need_h = B.cdiv(PR[fifo[d.fhead].id]);
-          if (!((u64)d.nRun + d.nX + 1 > mns)) {
-            mem_check = true;
-            if ((i64)d.nfree - (i64)d.nRun - (i64)need_h >= wm) quiet = false;
-          }
+          --d.nX;
+          ++d.nRun;
+          d.xhead_end = d.nX ? fifo[d.fhead - d.nX].xend : INF;
         }
-        if (quiet) {
-          S.scratch[lane] = 0;
-          S.scratch[32 + lane] = 0;
-          __syncwarp();
-          u64 cdp0 = 0;
-          u32 rmn = 0xffffffffu;
-          #pragma unroll 1
-          for (u32 b0 = 0; b0 < nA0; b0 += 32) {
-            const u32 jj = b0 + lane;
-            u32 key = 64u + lane;
-            if (jj < nA0 && stt[jj] == ST_RUN) {
-              const u32 c = S.ctx[jj];
-              cdp0 += c + 1;
-              rmn = min(rmn, S.rem[jj]);
-              const u32 r = B.mod(c);
-              const u32 j0 = r ? B.bs - r : 0u;
-              if (j0 < 32) key = j0;
-            }
-            const u32 peers = __match_any_sync(FULLMASK, key);
-            if (key < 32 && (peers & ltm) == 0u) {
-              S.scratch[key] += __popc(peers);
-              S.scratch[32 + key] = peers;
-            }
-            __syncwarp();
-          }
-          const u64 Cd0 = warp_sum64(cdp0);
-          const u32 rm = __reduce_min_sync(FULLMASK, rmn);
-          const u32 nj = S.scratch[B.bs >= 32 ? lane : B.mod(lane)];
-          const u32 Aj = scan_incl(nj);
-          const u64 Cdj = Cd0 + (u64)lane * d.nRun;
-          const i64 Tj = iter_time_ns(KD, 0, 0, 0, d.nRun, Cdj, 0);
-          const i64 tej = t + scan_incl_i64(Tj);
-          const i64 tsj = tej - Tj;
-          bool ok = ((u64)Aj <= d.nfree) && (Aj <= (u32)CAP) && (lane < rm);
-          if (lane > 0) {
-            if (P.horizon >= 0 && tsj >= P.horizon) ok = false;
-            if (tsj >= d.xhead_end || tsj > cut) ok = false;
-          }
-          if (mem_check) {
-            const u64 fr = d.nfree - (u64)__shfl_sync(FULLMASK, Aj, 0);
-            if (!((i64)fr - (i64)need_h < wm)) ok = false;
-          }
-          const u32 okm = __ballot_sync(FULLMASK, ok);
-          const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
-          const u32 memcut = __ballot_sync(FULLMASK, !((u64)Aj <= d.nfree));
-          if (J < 2 && memcut && (u32)(__ffs(memcut) - 1) < 2) {
-            d.ffw = d.nfree;
-            d.ffk = d.k + 4;
-          }
-          if (J >= 2) {
-            const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
-            __syncwarp();
-            S.scratch[lane] = Aj - nj;  // bucket cursors
-            __syncwarp();
-            if (Ktot > 0) {
-              const u32 nrep = B.cdiv(32u);
-              #pragma unroll 1
-              for (u32 b0 = 0; b0 < nA0; b0 += 32) {
-                const u32 jj = b0 + lane;
-                const bool run = jj < nA0 && stt[jj] == ST_RUN;
-                const u32 c = run ? S.ctx[jj] : 0u;
-                const u32 r = B.mod(c);
-                u32 jx = r ? B.bs - r : 0u;
-                #pragma unroll 1
-                for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
-                  const bool v = run && jx < J;
-                  const u32 key = v ? jx : 64u + lane;
-                  const u32 peers = __match_any_sync(FULLMASK, key);
-                  u32 base = 0;
-                  if (v) base = S.scratch[jx];
-                  __syncwarp();
-                  if (v) {
-                    const u32 e = base + __popc(peers & ltm);
-                    S.req_cum[e] = e + 1;
-                    S.req_pt[e] = jj | (jx << 10) | (B.div(c + jx) << 15);
-                    if ((peers & ltm) == 0u) S.scratch[jx] = base + __popc(peers);
-                  }
-                  __syncwarp();
-                }
-              }
-              if (!alloc_ordered(S, Ktot, Ktot, btD, btl, d.k, koff, L, d.hint, nwD)) {
-                flags |= TOKENSIM_PT_INTERNAL_ERROR;
-                break;
-              }
-            }
-            const u64 blk0 = totD - d.nfree;
-            d.nfree -= Ktot;
-            const u64 klast = d.k + J - 1;
-            const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
-            const i64 te0 = __shfl_sync(FULLMASK, tej, 0);
-            const bool lj = lane < J;
-            i64 tm1 = (lj && lane > 0) ? Tj : 0;
-#pragma unroll
-            for (u32 o = 16; o; o >>= 1) {
-              const i64 y = __shfl_xor_sync(FULLMASK, tm1, o);
-              tm1 = y > tm1 ? y : tm1;
-            }
-            u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
+        __syncwarp();
+        bool ff_done = false;
+        // ---------------------------------------------------------- D fast-forward (H3)
+        // Quiescent decode stretch: no transfer completes, nothing is pulled or resumed, nothing
+        // is preempted, and no dispatch (which reads this worker's state or feeds its FIFO) can
+        // happen before the stretch's iterations: every iteration starts before the epoch
+        // horizon H, which no dispatch precedes.
+        if (ff_on && d.nRun > 0 && d.rmin >= 2 && (d.nfree > d.ffw || d.k >= d.ffk)) {
+          const i64 cut = H - 1;  // iterations starting at or after the epoch horizon H are excluded
+          bool quiet = true, mem_check = false;
+          u32 need_h = 0;
+          const u32 nA0 = d.nD;  // all slots (states are checked)
+          if (d.nQ > 0) {
+            u32 qpos = 0;
             #pragma unroll 1
             for (u32 b0 = 0; b0 < nA0; b0 += 32) {
               const u32 jj = b0 + lane;
-              bool fin = false;
+              const u32 qb = __ballot_sync(FULLMASK, jj < nA0 && stt[jj] == ST_QUEUED);
+              if (qb) {
+                qpos = b0 + (u32)(__ffs(qb) - 1);
+                break;
+              }
+            }
+            u32 tokq;
+            if (SWAPM) {
+              const u32 c = S.ctx[qpos];
+              need_h = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
+              tokq = 1;
+            } else {
+              const u32 id = S.id[qpos];
+              tokq = PR[id] + (OU[id] - S.rem[qpos]);
+              need_h = B.cdiv(tokq);
+            }
+            if (!((u64)d.nRun + d.nX + 1 > mns || (u64)d.nRun + tokq > mbt)) {
+              mem_check = true;
+              if ((i64)d.nfree - (i64)d.nRun - (i64)need_h >= wm) quiet = false;
+            }
+          } else if (!STATICP && d.fhead < d.ftail) {
+            // a visible pending head (every FIFO entry is visible): blocked now => blocked later
+            need_h = B.cdiv(PR[fifo[d.fhead].id]);
+            if (!((u64)d.nRun + d.nX + 1 > mns)) {
+              mem_check = true;
+              if ((i64)d.nfree - (i64)d.nRun - (i64)need_h >= wm) quiet = false;
+            }
+          }
+          if (quiet) {
+            S.scratch[lane] = 0;
+            S.scratch[32 + lane] = 0;
+            __syncwarp();
+            u64 cdp0 = 0;
+            u32 rmn = 0xffffffffu;
+            #pragma unroll 1
+            for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+              const u32 jj = b0 + lane;
+              u32 key = 64u + lane;
               if (jj < nA0 && stt[jj] == ST_RUN) {
-                const u32 r = S.rem[jj] - J;
-                S.rem[jj] = r;
-                S.ctx[jj] += J;
-                const i64 g0 = te0 - S.last[jj];
-                i64 mg = S.maxgap[jj];
-                mg = g0 > mg ? g0 : mg;
-                mg = tm1 > mg ? tm1 : mg;
-                S.maxgap[jj] = mg;
-                S.last[jj] = tend;
-                fin = r == 0;
-                if (fin)
-                  write_record(rec + S.id[jj], S.ttft[jj], tend - S.arr[jj], mg, S.info[jj] >> 16,
-                               TOKENSIM_REQ_FINISHED, (u32)klast);
-                else
-                  rmin_l = min(rmin_l, r);
+                const u32 c = S.ctx[jj];
+                cdp0 += c + 1;
+                rmn = min(rmn, S.rem[jj]);
+                const u32 r = B.mod(c);
+                const u32 j0 = r ? B.bs - r : 0u;
+                if (j0 < 32) key = j0;
+              }
+              const u32 peers = __match_any_sync(FULLMASK, key);
+              if (key < 32 && (peers & ltm) == 0u) {
+                S.scratch[key] += __popc(peers);
+                S.scratch[32 + key] = peers;
+              }
+              __syncwarp();
+            }
+            const u64 Cd0 = warp_sum64(cdp0);
+            const u32 rm = __reduce_min_sync(FULLMASK, rmn);
+            const u32 nj = S.scratch[B.bs >= 32 ? lane : B.mod(lane)];
+            const u32 Aj = scan_incl(nj);
+            const u64 Cdj = Cd0 + (u64)lane * d.nRun;
+            const i64 Tj = iter_time_ns(KD, 0, 0, 0, d.nRun, Cdj, 0);
+            const i64 tej = t + scan_incl_i64(Tj);
+            const i64 tsj = tej - Tj;
+            bool ok = ((u64)Aj <= d.nfree) && (Aj <= (u32)CAP) && (lane < rm);
+            if (lane > 0) {
+              if (P.horizon >= 0 && tsj >= P.horizon) ok = false;
+              if (tsj >= d.xhead_end || tsj > cut) ok = false;
+            }
+            if (mem_check) {
+              const u64 fr = d.nfree - (u64)__shfl_sync(FULLMASK, Aj, 0);
+              if (!((i64)fr - (i64)need_h < wm)) ok = false;
+            }
+            const u32 okm = __ballot_sync(FULLMASK, ok);
+            const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+            const u32 memcut = __ballot_sync(FULLMASK, !((u64)Aj <= d.nfree));
+            if (J < 2 && memcut && (u32)(__ffs(memcut) - 1) < 2) {
+              d.ffw = d.nfree;
+              d.ffk = d.k + 4;
+            }
+            if (J >= 2) {
+              const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
+              __syncwarp();
+              S.scratch[lane] = Aj - nj;  // bucket cursors
+              __syncwarp();
+              if (Ktot > 0) {
+                const u32 nrep = B.cdiv(32u);
+                #pragma unroll 1
+                for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+                  const u32 jj = b0 + lane;
+                  const bool run = jj < nA0 && stt[jj] == ST_RUN;
+                  const u32 c = run ? S.ctx[jj] : 0u;
+                  const u32 r = B.mod(c);
+                  u32 jx = r ? B.bs - r : 0u;
+                  #pragma unroll 1
+                  for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
+                    const bool v = run && jx < J;
+                    const u32 key = v ? jx : 64u + lane;
+                    const u32 peers = __match_any_sync(FULLMASK, key);
+                    u32 base = 0;
+                    if (v) base = S.scratch[jx];
+                    __syncwarp();
+                    if (v) {
+                      const u32 e = base + __popc(peers & ltm);
+                      S.req_cum[e] = e + 1;
+                      S.req_pt[e] = jj | (jx << 10) | (B.div(c + jx) << 15);
+                      if ((peers & ltm) == 0u) S.scratch[jx] = base + __popc(peers);
+                    }
+                    __syncwarp();
+                  }
+                }
+                if (!alloc_ordered(S, Ktot, Ktot, btD, btl, d.k, koff, L, d.hint, nwD)) {
+                  flags |= TOKENSIM_PT_INTERNAL_ERROR;
+                  break;
+                }
+              }
+              const u64 blk0 = totD - d.nfree;
+              d.nfree -= Ktot;
+              const u64 klast = d.k + J - 1;
+              const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
+              const i64 te0 = __shfl_sync(FULLMASK, tej, 0);
+              const bool lj = lane < J;
+              i64 tm1 = (lj && lane > 0) ? Tj : 0;
+  #pragma unroll
+              for (u32 o = 16; o; o >>= 1) {
+                const i64 y = __shfl_xor_sync(FULLMASK, tm1, o);
+                tm1 = y > tm1 ? y : tm1;
+              }
+              u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
+              #pragma unroll 1
+              for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+                const u32 jj = b0 + lane;
+                bool fin = false;
+                if (jj < nA0 && stt[jj] == ST_RUN) {
+                  const u32 r = S.rem[jj] - J;
+                  S.rem[jj] = r;
+                  S.ctx[jj] += J;
+                  const i64 g0 = te0 - S.last[jj];
+                  i64 mg = S.maxgap[jj];
+                  mg = g0 > mg ? g0 : mg;
+                  mg = tm1 > mg ? tm1 : mg;
+                  S.maxgap[jj] = mg;
+                  S.last[jj] = tend;
+                  fin = r == 0;
+                  if (fin)
+                    write_record(rec + S.id[jj], S.ttft[jj], tend - S.arr[jj], mg, S.info[jj] >> 16,
+                                 TOKENSIM_REQ_FINISHED, (u32)klast);
+                  else
+                    rmin_l = min(rmin_l, r);
+                }
+                u32 fm = __ballot_sync(FULLMASK, fin);
+                __syncwarp();
+                if (fm && first_fin == 0xffffffffu) first_fin = b0 + (u32)(__ffs(fm) - 1);
+                nfin += __popc(fm);
+                while (fm) {
+                  const u32 l = (u32)(__ffs(fm) - 1);
+                  fm &= fm - 1;
+                  const u32 pos = b0 + l;
+                  const u32 held = B.cdiv(S.ctx[pos]);
+                  const u32 slot = SLOT(S.info[pos]);
+                  free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], klast, koff, L, d.hint);
+                  d.nfree += held;
+                  if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
+                }
+              }
+              __syncwarp();
+              const u64 blkj = blk0 + Aj;
+              pdn_it_reserve(L, 32, itcur);
+              if (lj)
+                it_put(L, lane, (d.k + lane) | ((u64)wid << 40), tsj, Tj, 0, Cdj, blkj, 0, d.nRun, 0, 0, 0,
+                       lane == J - 1 ? nfin : 0u, 0);
+              L.nit += J;
+              d.bns += warp_sum64(lj ? blkj * (u64)Tj : 0ull);
+              trace_stretch(d.TA, fe, BINNED, FULLT, trcD, P.trace_cap, W, J, tsj, tej, blkj, flags);
+              const u64 blk_last = blk0 + Ktot;
+              d.peak = blk_last > d.peak ? blk_last : d.peak;
+              req_iters += (u64)d.nRun * J;
+              if (nfin) {
+                u32 out = first_fin;
+                #pragma unroll 1
+                for (u32 b0 = first_fin; b0 < d.nD; b0 += 32) {
+                  const u32 jj = b0 + lane;
+                  const bool valid = jj < d.nD;
+                  u32 vid = 0, vctx = 0, vrem = 0, vinfo = 0, vst = 0;
+                  i64 vl = 0, vm = 0, va = 0, vt = 0;
+                  if (valid) {
+                    vid = S.id[jj];
+                    vctx = S.ctx[jj];
+                    vrem = S.rem[jj];
+                    vinfo = S.info[jj];
+                    vl = S.last[jj];
+                    vm = S.maxgap[jj];
+                    va = S.arr[jj];
+                    vt = S.ttft[jj];
+                    vst = stt[jj];
+                  }
+                  const bool keep = valid && vrem != 0;
+                  const u32 km = __ballot_sync(FULLMASK, keep);
+                  __syncwarp();
+                  if (keep) {
+                    const u32 dd = out + __popc(km & ltm);
+                    S.id[dd] = vid;
+                    S.ctx[dd] = vctx;
+                    S.rem[dd] = vrem;
+                    S.info[dd] = vinfo;
+                    S.last[dd] = vl;
+                    S.maxgap[dd] = vm;
+                    S.arr[dd] = va;
+                    S.ttft[dd] = vt;
+                    stt[dd] = vst;
+                  }
+                  __syncwarp();
+                  out += __popc(km);
+                }
+                d.nRun -= nfin;
+                d.nD -= nfin;
+                done_w += nfin;
+                nfin_tot += nfin;
+                last_fin = tend > last_fin ? tend : last_fin;
+                tfin_w = __shfl_sync(FULLMASK, tsj, J - 1);
+              }
+              d.rmin = d.nRun ? __reduce_min_sync(FULLMASK, rmin_l) : 0u;
+              ff_iters += J;
+              ++ff_runs;
+              d.t = tend;
+              d.last = tend;
+              d.k += J;
+              d.idle = 0;
+              ff_done = true;
+            }
+          }
+          if (!ff_done) d.rmin = 0;
+        }
+        if (flags & TOKENSIM_PT_INTERNAL_ERROR) break;
+        if (!ff_done) {
+          const u32 nA = d.nD;  // all slots, id-sorted (states are checked)
+          // 3. decode reservation: RUN slots needing a block -> requester list (ascending id)
+          u32 E = 0;
+          u64 cdp = 0, npp = 0, app = 0;
+          #pragma unroll 1
+          for (u32 b0 = 0; b0 < nA; b0 += 32) {
+            const u32 jj = b0 + lane;
+            const bool run = jj < nA && stt[jj] == ST_RUN;
+            const u32 c = run ? S.ctx[jj] : 1u;
+            const bool need = run && B.mod(c) == 0;
+            if (run) cdp += c + 1;
+            const u32 bal = __ballot_sync(FULLMASK, need);
+            if (need) {
+              const u32 e = E + __popc(bal & ltm);
+              S.req_cum[e] = e + 1;
+              S.req_pt[e] = jj | (B.div(c) << 15);
+            }
+            E += __popc(bal);
+          }
+          u32 m = 0;
+          u64 swap_out = 0;
+          if ((u64)E > d.nfree) {
+            // minimal m over the running slots, latest ids first (in-flight blocks are not preemptible)
+            u64 Sn = E, Hh = 0;
+            u32 pos = nA;
+            do {
+              do {
+                --pos;
+              } while (stt[pos] != ST_RUN);
+              ++m;
+              const u32 c = S.ctx[pos];
+              Sn -= (B.mod(c) == 0) ? 1 : 0;
+              Hh += B.cdiv(c);
+            } while (Sn > d.nfree + Hh && m < d.nRun);
+            u64 csub = 0;
+            u32 vpos = nA, done_v = 0;
+            while (done_v < m) {
+              do {
+                --vpos;
+              } while (stt[vpos] != ST_RUN);
+              const u32 c = S.ctx[vpos];
+              const u32 held = B.cdiv(c);
+              free_blocks(S.bitmap, btD + (size_t)SLOT(S.info[vpos]) * btl, held, S.id[vpos], d.k, koff, L, d.hint);
+              d.nfree += held;
+              csub += c + 1;
+              if (SWAPM) swap_out += (u64)held * HPD.block_bytes;
+              __syncwarp();
+              if (lane == 0) {
+                S.info[vpos] += 1u << 16;
+                if (!SWAPM) S.ctx[vpos] = 0;
+                stt[vpos] = ST_QUEUED;
+              }
+              __syncwarp();
+              ++done_v;
+            }
+            if (lane == 0) cdp -= csub;
+            E = (u32)Sn;
+            d.nRun -= m;
+            d.nQ += m;
+            npre += m;
+          }
+          u32 Kb = E;
+          d.nfree -= E;
+          u32 nres = 0, nadm = 0, nrecomp = 0;
+          u64 swap_in = 0, tokens = d.nRun;
+          if (m == 0) {
+            // 4. resume preempted requests in ascending id; |R| counts in-flight transfers too
+            if (d.nQ > 0) {
+              u64 cum_need = 0, cum_tok = 0;
+              u32 taken = 0;
+              #pragma unroll 1
+              for (u32 b0 = 0; b0 < nA; b0 += 32) {
+                const u32 jj = b0 + lane;
+                const bool q = jj < nA && stt[jj] == ST_QUEUED;
+                u32 need = 0, tok = 0, held0 = 0, c = 0;
+                if (q) {
+                  if (SWAPM) {
+                    c = S.ctx[jj];
+                    need = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
+                    tok = 1;
+                    held0 = B.cdiv(c);
+                  } else {
+                    const u32 id = S.id[jj];
+                    tok = PR[id] + (OU[id] - S.rem[jj]);
+                    need = B.cdiv(tok);
+                  }
+                }
+                const u32 qm = __ballot_sync(FULLMASK, q);
+                const u32 rq = __popc(qm & ltm);
+                const u32 cn = scan_incl(need), ct = scan_incl(tok);
+                const bool ok = q && ((u64)d.nRun + d.nX + taken + rq + 1 <= (u64)mns) &&
+                                (tokens + cum_tok + ct <= (u64)mbt) && ((i64)d.nfree - (i64)(cum_need + cn) >= wm);
+                const u32 failm = __ballot_sync(FULLMASK, q && !ok);
+                const u32 stopl = failm ? (u32)(__ffs(failm) - 1) : 32u;
+                const bool take = q && lane < stopl;
+                const u32 tm = __ballot_sync(FULLMASK, take);
+                const u32 cnt = __popc(tm);
+                if (take) {
+                  S.req_cum[E + rq] = Kb + cn;
+                  S.req_pt[E + rq] = jj;
+                  if (SWAPM) {
+                    stt[jj] = ST_RUN;
+                    cdp += c + 1;
+                  } else {
+                    stt[jj] = ST_RUN_RECOMP;
+                    S.ctx[jj] = tok;
+                    npp += tok;
+                    app += (u64)tok * (tok + 1) / 2;
+                  }
+                }
+                const u64 sw = warp_sum64(take ? (u64)held0 : 0ull);
+                if (cnt) {
+                  const u32 last = 31u - __clz(tm);
+                  const u32 sn = __shfl_sync(FULLMASK, cn, last), stk = __shfl_sync(FULLMASK, ct, last);
+                  cum_need += sn;
+                  cum_tok += stk;
+                  Kb += sn;
+                  E += cnt;
+                  nres += cnt;
+                  taken += cnt;
+                  if (SWAPM) swap_in += sw * HPD.block_bytes;
+                  else nrecomp += cnt;
+                }
+                if (failm) break;
+              }
+              d.nfree -= cum_need;
+              tokens += cum_tok;
+              d.nRun += nres;
+              d.nQ -= nres;
+              __syncwarp();
+            }
+            // 5. pull pending requests FCFS and start their transfers on this worker's link
+            if (d.nQ == 0 && (!STATICP || (d.nRun == 0 && d.nX == 0))) {
+              while (d.fhead < d.ftail) {
+                const u32 idx = d.fhead + lane;
+                const bool valid = idx < d.ftail;
+                u32 id = 0, p = 0, o = 0, pw = 0;
+                i64 join = INF, a = 0;
+                if (valid) {
+                  const FifoEnt e = fifo[idx];
+                  id = e.id;
+                  pw = e.seg;
+                  join = e.join;
+                }
+                const bool vis = valid && join <= t;
+                if (vis) {
+                  p = PR[id];
+                  o = OU[id];
+                  a = A[id];
+                }
+                const u32 need = B.cdiv(p);
+                const u32 cneed = scan_incl(vis ? need : 0u);
+                const bool ok = vis && ((u64)d.nRun + d.nX + lane + 1 <= (u64)mns) && ((i64)d.nfree - (i64)cneed >= wm);
+                const u32 okm = __ballot_sync(FULLMASK, ok);
+                const u32 cnt = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+                if (cnt == 0) break;
+                const bool take = lane < cnt;
+                const u32 slot = alloc_btslots(S.btfree, CAP / 32, take, lane, cnt);
+                const i64 dur = take ? xfer_ns(p) : 0;
+                const i64 start0 = t > d.link_busy ? t : d.link_busy;
+                const i64 xend = start0 + scan_incl_i64(dur);
+                if (take) {
+                  const u32 pos = d.nD + lane;
+                  S.id[pos] = id;
+                  S.ctx[pos] = p;
+                  S.rem[pos] = o - 1;
+                  S.info[pos] = slot;
+                  S.last[pos] = join;  // the first token left its prefill worker at `join`
+                  S.maxgap[pos] = 0;
+                  S.arr[pos] = a;
+                  S.ttft[pos] = join - a;
+                  stt[pos] = ST_XFER;
+                  S.req_cum[E + lane] = Kb + cneed;
+                  S.req_pt[E + lane] = pos;
+                  fifo[idx].xend = xend;
+                  reqx[id] = xend;
+                }
+                __syncwarp();
+                // the holders' prefill workers: their blocks come back at xend (wake idle ones)
+                for (u32 l = 0; l < cnt; ++l) {
+                  const u32 lpw = __shfl_sync(FULLMASK, pw, l);
+                  const i64 lx = __shfl_sync(FULLMASK, xend, l);
+                  if (lane == 0) {  // several decode warps may release to one prefill worker at once
+                    PScal &ps = M.ps[lpw];
+                    atomicMin(reinterpret_cast<long long *>(&ps.hmin), (long long)lx);
+                    if (ps.idle) atomicMin(reinterpret_cast<long long *>(&ps.t), (long long)lx);
+                  }
+                }
+                __syncwarp();
+                const u32 sneed = __shfl_sync(FULLMASK, cneed, cnt - 1);
+                const i64 x0 = __shfl_sync(FULLMASK, xend, 0);
+                d.link_busy = __shfl_sync(FULLMASK, xend, cnt - 1);
+                if (d.nX == 0) d.xhead_end = x0;
+                xbytes += warp_sum64(take ? (u64)p * P.M.kvb : 0ull);
+                d.nfree -= sneed;
+                Kb += sneed;
+                E += cnt;
+                d.nD += cnt;
+                d.nX += cnt;
+                d.fhead += cnt;
+                nadm += cnt;
+                n_xfer += cnt;
+                __syncwarp();
+                if (cnt < 32) break;
+              }
+            }
+          }
+          if (Kb > 0 && !alloc_ordered(S, E, Kb, btD, btl, d.k, koff, L, d.hint, nwD)) {
+            flags |= TOKENSIM_PT_INTERNAL_ERROR;
+            break;
+          }
+          // pulled requests were appended in dispatch order, which with several prefill workers
+          // need not be id order: insert them into the id-sorted slots (victims are the latest
+          // arrivals, requesters go in id order -- reading A7).  In-flight slots cannot finish in
+          // this iteration, so doing it before the commit keeps positions stable for it.
+          for (u32 q = d.nD - nadm; q < d.nD; ++q) {
+            const u32 qid = S.id[q];
+            u32 p = 0;
+            #pragma unroll 1
+            for (u32 b0 = 0; b0 < q; b0 += 32) {
+              const u32 jj = b0 + lane;
+              p += __popc(__ballot_sync(FULLMASK, jj < q && S.id[jj] < qid));
+            }
+            if (p == q) continue;
+            const u32 vctx = S.ctx[q], vrem = S.rem[q], vinfo = S.info[q], vst = stt[q];
+            const i64 vl = S.last[q], vm = S.maxgap[q], va = S.arr[q], vt = S.ttft[q];
+            __syncwarp();
+            for (u32 c = q; c > p;) {  // shift [p, q) up by one, highest chunk first
+              const u32 lo = c > p + 32 ? c - 32 : p;
+              const u32 jj = lo + lane;
+              const bool v = jj < c;
+              u32 a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+              i64 b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+              if (v) {
+                a0 = S.id[jj];
+                a1 = S.ctx[jj];
+                a2 = S.rem[jj];
+                a3 = S.info[jj];
+                a4 = stt[jj];
+                b1 = S.last[jj];
+                b2 = S.maxgap[jj];
+                b3 = S.arr[jj];
+                b4 = S.ttft[jj];
+              }
+              __syncwarp();
+              if (v) {
+                S.id[jj + 1] = a0;
+                S.ctx[jj + 1] = a1;
+                S.rem[jj + 1] = a2;
+                S.info[jj + 1] = a3;
+                stt[jj + 1] = a4;
+                S.last[jj + 1] = b1;
+                S.maxgap[jj + 1] = b2;
+                S.arr[jj + 1] = b3;
+                S.ttft[jj + 1] = b4;
+              }
+              __syncwarp();
+              c = lo;
+            }
+            if (lane == 0) {
+              S.id[p] = qid;
+              S.ctx[p] = vctx;
+              S.rem[p] = vrem;
+              S.info[p] = vinfo;
+              stt[p] = vst;
+              S.last[p] = vl;
+              S.maxgap[p] = vm;
+              S.arr[p] = va;
+              S.ttft[p] = vt;
+            }
+            __syncwarp();
+          }
+          if (d.nRun == 0) {  // 6. nothing runnable: wake at the next transfer end (or a dispatch)
+            d.t = d.xhead_end;
+            d.idle = 1;
+          } else {
+            // 7. cost on the decode profile
+            const u32 Dn = d.nRun - nrecomp;
+            const u64 Cd = warp_sum64(cdp);
+            u64 Np = 0, Ap = 0;
+            if (nrecomp) {
+              Np = warp_sum64(npp);
+              Ap = warp_sum64(app);
+            }
+            if (KD.preload && swap_in > 0) ev_flush(L);  // the event log doubles as the pipeline's scratch
+            const i64 T = iter_time_chunk_ns(KD, Np, Ap, Np, nrecomp, Dn, Cd, swap_out, swap_in,
+                                             reinterpret_cast<double *>(L.ev));
+            const i64 te = t + T;
+            const u64 blocks = totD - d.nfree;
+            // 8. commit
+            u32 nfin = 0, first_fin = 0xffffffffu, rmin_d = 0xffffffffu;
+            const u32 nC = d.nD;  // pulls (now sorted in) may have moved running slots past nA
+            #pragma unroll 1
+            for (u32 b0 = 0; b0 < nC; b0 += 32) {
+              const u32 jj = b0 + lane;
+              bool fin = false;
+              if (jj < nC) {
+                const u32 st = stt[jj];
+                if (st == ST_RUN || st == ST_RUN_RECOMP) {
+                  const u32 r = S.rem[jj] - 1;
+                  S.rem[jj] = r;
+                  if (st == ST_RUN) S.ctx[jj] += 1;
+                  else stt[jj] = ST_RUN;
+                  const i64 gap = te - S.last[jj];
+                  if (gap > S.maxgap[jj]) S.maxgap[jj] = gap;
+                  S.last[jj] = te;
+                  fin = r == 0;
+                  if (fin)
+                    write_record(rec + S.id[jj], S.ttft[jj], te - S.arr[jj], S.maxgap[jj], S.info[jj] >> 16,
+                                 TOKENSIM_REQ_FINISHED, (u32)d.k);
+                  else
+                    rmin_d = min(rmin_d, r);
+                }
               }
               u32 fm = __ballot_sync(FULLMASK, fin);
               __syncwarp();
@@ -601,23 +1043,13 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
                 const u32 pos = b0 + l;
                 const u32 held = B.cdiv(S.ctx[pos]);
                 const u32 slot = SLOT(S.info[pos]);
-                free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], klast, koff, L, d.hint);
+                free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], d.k, koff, L, d.hint);
                 d.nfree += held;
                 if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
               }
             }
             __syncwarp();
-            const u64 blkj = blk0 + Aj;
-            it_reserve(L, 32);
-            if (lj)
-              it_put(L, lane, (d.k + lane) | ((u64)wid << 40), tsj, Tj, 0, Cdj, blkj, 0, d.nRun, 0, 0, 0,
-                     lane == J - 1 ? nfin : 0u, 0);
-            L.nit += J;
-            d.bns += warp_sum64(lj ? blkj * (u64)Tj : 0ull);
-            trace_stretch(d.TA, FE[wid], BINNED, FULLT, trcD, P.trace_cap, W, J, tsj, tej, blkj, flags);
-            const u64 blk_last = blk0 + Ktot;
-            d.peak = blk_last > d.peak ? blk_last : d.peak;
-            req_iters += (u64)d.nRun * J;
+            req_iters += d.nRun;
             if (nfin) {
               u32 out = first_fin;
               #pragma unroll 1
@@ -657,421 +1089,69 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
               }
               d.nRun -= nfin;
               d.nD -= nfin;
-              n_done += nfin;
+              done_w += nfin;
               nfin_tot += nfin;
-              last_fin = tend > last_fin ? tend : last_fin;
+              last_fin = te > last_fin ? te : last_fin;
+              tfin_w = t;
             }
-            d.rmin = d.nRun ? __reduce_min_sync(FULLMASK, rmin_l) : 0u;
-            ff_iters += J;
-            ++ff_runs;
-            d.t = tend;
-            d.last = tend;
-            d.k += J;
+            d.rmin = __reduce_min_sync(FULLMASK, rmin_d);
+            if (d.nRun == 0) d.rmin = 0;
+            fold_iter(d.k, wid, t, T, nrecomp, Dn, Np, Cd, m, nres, nadm, 0, nfin, blocks);
+            trace_iter(d.TA, fe, BINNED, FULLT, trcD, P.trace_cap, W, t, te, blocks, flags);
+            d.peak = blocks > d.peak ? blocks : d.peak;
+            d.bns += blocks * (u64)T;
+            swo += swap_out;
+            swi += swap_in;
+            d.t = te;
+            d.last = te;
+            ++d.k;
             d.idle = 0;
-            ff_done = true;
           }
-        }
-        if (!ff_done) d.rmin = 0;
-      }
-      if (flags & TOKENSIM_PT_INTERNAL_ERROR) break;
-      if (!ff_done) {
-        const u32 nA = d.nD;  // all slots, id-sorted (states are checked)
-        // 3. decode reservation: RUN slots needing a block -> requester list (ascending id)
-        u32 E = 0;
-        u64 cdp = 0, npp = 0, app = 0;
-        #pragma unroll 1
-        for (u32 b0 = 0; b0 < nA; b0 += 32) {
-          const u32 jj = b0 + lane;
-          const bool run = jj < nA && stt[jj] == ST_RUN;
-          const u32 c = run ? S.ctx[jj] : 1u;
-          const bool need = run && B.mod(c) == 0;
-          if (run) cdp += c + 1;
-          const u32 bal = __ballot_sync(FULLMASK, need);
-          if (need) {
-            const u32 e = E + __popc(bal & ltm);
-            S.req_cum[e] = e + 1;
-            S.req_pt[e] = jj | (B.div(c) << 15);
-          }
-          E += __popc(bal);
-        }
-        u32 m = 0;
-        u64 swap_out = 0;
-        if ((u64)E > d.nfree) {
-          // minimal m over the running slots, latest ids first (in-flight blocks are not preemptible)
-          u64 Sn = E, Hh = 0;
-          u32 pos = nA;
-          do {
-            do {
-              --pos;
-            } while (stt[pos] != ST_RUN);
-            ++m;
-            const u32 c = S.ctx[pos];
-            Sn -= (B.mod(c) == 0) ? 1 : 0;
-            Hh += B.cdiv(c);
-          } while (Sn > d.nfree + Hh && m < d.nRun);
-          u64 csub = 0;
-          u32 vpos = nA, done_v = 0;
-          while (done_v < m) {
-            do {
-              --vpos;
-            } while (stt[vpos] != ST_RUN);
-            const u32 c = S.ctx[vpos];
-            const u32 held = B.cdiv(c);
-            free_blocks(S.bitmap, btD + (size_t)SLOT(S.info[vpos]) * btl, held, S.id[vpos], d.k, koff, L, d.hint);
-            d.nfree += held;
-            csub += c + 1;
-            if (SWAPM) swap_out += (u64)held * HPD.block_bytes;
-            __syncwarp();
-            if (lane == 0) {
-              S.info[vpos] += 1u << 16;
-              if (!SWAPM) S.ctx[vpos] = 0;
-              stt[vpos] = ST_QUEUED;
-            }
-            __syncwarp();
-            ++done_v;
-          }
-          if (lane == 0) cdp -= csub;
-          E = (u32)Sn;
-          d.nRun -= m;
-          d.nQ += m;
-          npre += m;
-        }
-        u32 Kb = E;
-        d.nfree -= E;
-        u32 nres = 0, nadm = 0, nrecomp = 0;
-        u64 swap_in = 0, tokens = d.nRun;
-        if (m == 0) {
-          // 4. resume preempted requests in ascending id; |R| counts in-flight transfers too
-          if (d.nQ > 0) {
-            u64 cum_need = 0, cum_tok = 0;
-            u32 taken = 0;
-            #pragma unroll 1
-            for (u32 b0 = 0; b0 < nA; b0 += 32) {
-              const u32 jj = b0 + lane;
-              const bool q = jj < nA && stt[jj] == ST_QUEUED;
-              u32 need = 0, tok = 0, held0 = 0, c = 0;
-              if (q) {
-                if (SWAPM) {
-                  c = S.ctx[jj];
-                  need = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
-                  tok = 1;
-                  held0 = B.cdiv(c);
-                } else {
-                  const u32 id = S.id[jj];
-                  tok = PR[id] + (OU[id] - S.rem[jj]);
-                  need = B.cdiv(tok);
-                }
-              }
-              const u32 qm = __ballot_sync(FULLMASK, q);
-              const u32 rq = __popc(qm & ltm);
-              const u32 cn = scan_incl(need), ct = scan_incl(tok);
-              const bool ok = q && ((u64)d.nRun + d.nX + taken + rq + 1 <= (u64)mns) &&
-                              (tokens + cum_tok + ct <= (u64)mbt) && ((i64)d.nfree - (i64)(cum_need + cn) >= wm);
-              const u32 failm = __ballot_sync(FULLMASK, q && !ok);
-              const u32 stopl = failm ? (u32)(__ffs(failm) - 1) : 32u;
-              const bool take = q && lane < stopl;
-              const u32 tm = __ballot_sync(FULLMASK, take);
-              const u32 cnt = __popc(tm);
-              if (take) {
-                S.req_cum[E + rq] = Kb + cn;
-                S.req_pt[E + rq] = jj;
-                if (SWAPM) {
-                  stt[jj] = ST_RUN;
-                  cdp += c + 1;
-                } else {
-                  stt[jj] = ST_RUN_RECOMP;
-                  S.ctx[jj] = tok;
-                  npp += tok;
-                  app += (u64)tok * (tok + 1) / 2;
-                }
-              }
-              const u64 sw = warp_sum64(take ? (u64)held0 : 0ull);
-              if (cnt) {
-                const u32 last = 31u - __clz(tm);
-                const u32 sn = __shfl_sync(FULLMASK, cn, last), stk = __shfl_sync(FULLMASK, ct, last);
-                cum_need += sn;
-                cum_tok += stk;
-                Kb += sn;
-                E += cnt;
-                nres += cnt;
-                taken += cnt;
-                if (SWAPM) swap_in += sw * HPD.block_bytes;
-                else nrecomp += cnt;
-              }
-              if (failm) break;
-            }
-            d.nfree -= cum_need;
-            tokens += cum_tok;
-            d.nRun += nres;
-            d.nQ -= nres;
-            __syncwarp();
-          }
-          // 5. pull pending requests FCFS and start their transfers on this worker's link
-          if (d.nQ == 0 && (!STATICP || (d.nRun == 0 && d.nX == 0))) {
-            while (d.fhead < d.ftail) {
-              const u32 idx = d.fhead + lane;
-              const bool valid = idx < d.ftail;
-              u32 id = 0, p = 0, o = 0, pw = 0;
-              i64 join = INF, a = 0;
-              if (valid) {
-                const FifoEnt e = fifo[idx];
-                id = e.id;
-                pw = e.seg;
-                join = e.join;
-              }
-              const bool vis = valid && join <= t;
-              if (vis) {
-                p = PR[id];
-                o = OU[id];
-                a = A[id];
-              }
-              const u32 need = B.cdiv(p);
-              const u32 cneed = scan_incl(vis ? need : 0u);
-              const bool ok = vis && ((u64)d.nRun + d.nX + lane + 1 <= (u64)mns) && ((i64)d.nfree - (i64)cneed >= wm);
-              const u32 okm = __ballot_sync(FULLMASK, ok);
-              const u32 cnt = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
-              if (cnt == 0) break;
-              const bool take = lane < cnt;
-              const u32 slot = alloc_btslots(S.btfree, CAP / 32, take, lane, cnt);
-              const i64 dur = take ? xfer_ns(p) : 0;
-              const i64 start0 = t > d.link_busy ? t : d.link_busy;
-              const i64 xend = start0 + scan_incl_i64(dur);
-              if (take) {
-                const u32 pos = d.nD + lane;
-                S.id[pos] = id;
-                S.ctx[pos] = p;
-                S.rem[pos] = o - 1;
-                S.info[pos] = slot;
-                S.last[pos] = join;  // the first token left its prefill worker at `join`
-                S.maxgap[pos] = 0;
-                S.arr[pos] = a;
-                S.ttft[pos] = join - a;
-                stt[pos] = ST_XFER;
-                S.req_cum[E + lane] = Kb + cneed;
-                S.req_pt[E + lane] = pos;
-                fifo[idx].xend = xend;
-                reqx[id] = xend;
-              }
-              __syncwarp();
-              // the holders' prefill workers: their blocks come back at xend (wake idle ones)
-              for (u32 l = 0; l < cnt; ++l) {
-                const u32 lpw = __shfl_sync(FULLMASK, pw, l);
-                const i64 lx = __shfl_sync(FULLMASK, xend, l);
-                if (lane == 0) {
-                  PScal &ps = M.ps[lpw];
-                  if (lx < ps.hmin) ps.hmin = lx;
-                  if (ps.idle && lx < ps.t) ps.t = lx;
-                }
-              }
-              __syncwarp();
-              const u32 sneed = __shfl_sync(FULLMASK, cneed, cnt - 1);
-              const i64 x0 = __shfl_sync(FULLMASK, xend, 0);
-              d.link_busy = __shfl_sync(FULLMASK, xend, cnt - 1);
-              if (d.nX == 0) d.xhead_end = x0;
-              xbytes += warp_sum64(take ? (u64)p * P.M.kvb : 0ull);
-              d.nfree -= sneed;
-              Kb += sneed;
-              E += cnt;
-              d.nD += cnt;
-              d.nX += cnt;
-              d.fhead += cnt;
-              nadm += cnt;
-              n_xfer += cnt;
-              __syncwarp();
-              if (cnt < 32) break;
-            }
-          }
-        }
-        if (Kb > 0 && !alloc_ordered(S, E, Kb, btD, btl, d.k, koff, L, d.hint, nwD)) {
-          flags |= TOKENSIM_PT_INTERNAL_ERROR;
-          break;
-        }
-        // pulled requests were appended in dispatch order, which with several prefill workers
-        // need not be id order: insert them into the id-sorted slots (victims are the latest
-        // arrivals, requesters go in id order -- reading A7).  In-flight slots cannot finish in
-        // this iteration, so doing it before the commit keeps positions stable for it.
-        for (u32 q = d.nD - nadm; q < d.nD; ++q) {
-          const u32 qid = S.id[q];
-          u32 p = 0;
-          #pragma unroll 1
-          for (u32 b0 = 0; b0 < q; b0 += 32) {
-            const u32 jj = b0 + lane;
-            p += __popc(__ballot_sync(FULLMASK, jj < q && S.id[jj] < qid));
-          }
-          if (p == q) continue;
-          const u32 vctx = S.ctx[q], vrem = S.rem[q], vinfo = S.info[q], vst = stt[q];
-          const i64 vl = S.last[q], vm = S.maxgap[q], va = S.arr[q], vt = S.ttft[q];
-          __syncwarp();
-          for (u32 c = q; c > p;) {  // shift [p, q) up by one, highest chunk first
-            const u32 lo = c > p + 32 ? c - 32 : p;
-            const u32 jj = lo + lane;
-            const bool v = jj < c;
-            u32 a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
-            i64 b1 = 0, b2 = 0, b3 = 0, b4 = 0;
-            if (v) {
-              a0 = S.id[jj];
-              a1 = S.ctx[jj];
-              a2 = S.rem[jj];
-              a3 = S.info[jj];
-              a4 = stt[jj];
-              b1 = S.last[jj];
-              b2 = S.maxgap[jj];
-              b3 = S.arr[jj];
-              b4 = S.ttft[jj];
-            }
-            __syncwarp();
-            if (v) {
-              S.id[jj + 1] = a0;
-              S.ctx[jj + 1] = a1;
-              S.rem[jj + 1] = a2;
-              S.info[jj + 1] = a3;
-              stt[jj + 1] = a4;
-              S.last[jj + 1] = b1;
-              S.maxgap[jj + 1] = b2;
-              S.arr[jj + 1] = b3;
-              S.ttft[jj + 1] = b4;
-            }
-            __syncwarp();
-            c = lo;
-          }
-          if (lane == 0) {
-            S.id[p] = qid;
-            S.ctx[p] = vctx;
-            S.rem[p] = vrem;
-            S.info[p] = vinfo;
-            stt[p] = vst;
-            S.last[p] = vl;
-            S.maxgap[p] = vm;
-            S.arr[p] = va;
-            S.ttft[p] = vt;
-          }
-          __syncwarp();
-        }
-        if (d.nRun == 0) {  // 6. nothing runnable: wake at the next transfer end (or a dispatch)
-          d.t = d.xhead_end;
-          d.idle = 1;
-        } else {
-          // 7. cost on the decode profile
-          const u32 Dn = d.nRun - nrecomp;
-          const u64 Cd = warp_sum64(cdp);
-          u64 Np = 0, Ap = 0;
-          if (nrecomp) {
-            Np = warp_sum64(npp);
-            Ap = warp_sum64(app);
-          }
-          if (KD.preload && swap_in > 0) ev_flush(L);  // the event log doubles as the pipeline's scratch
-          const i64 T = iter_time_chunk_ns(KD, Np, Ap, Np, nrecomp, Dn, Cd, swap_out, swap_in,
-                                           reinterpret_cast<double *>(L.ev));
-          const i64 te = t + T;
-          const u64 blocks = totD - d.nfree;
-          // 8. commit
-          u32 nfin = 0, first_fin = 0xffffffffu, rmin_d = 0xffffffffu;
-          const u32 nC = d.nD;  // pulls (now sorted in) may have moved running slots past nA
-          #pragma unroll 1
-          for (u32 b0 = 0; b0 < nC; b0 += 32) {
-            const u32 jj = b0 + lane;
-            bool fin = false;
-            if (jj < nC) {
-              const u32 st = stt[jj];
-              if (st == ST_RUN || st == ST_RUN_RECOMP) {
-                const u32 r = S.rem[jj] - 1;
-                S.rem[jj] = r;
-                if (st == ST_RUN) S.ctx[jj] += 1;
-                else stt[jj] = ST_RUN;
-                const i64 gap = te - S.last[jj];
-                if (gap > S.maxgap[jj]) S.maxgap[jj] = gap;
-                S.last[jj] = te;
-                fin = r == 0;
-                if (fin)
-                  write_record(rec + S.id[jj], S.ttft[jj], te - S.arr[jj], S.maxgap[jj], S.info[jj] >> 16,
-                               TOKENSIM_REQ_FINISHED, (u32)d.k);
-                else
-                  rmin_d = min(rmin_d, r);
-              }
-            }
-            u32 fm = __ballot_sync(FULLMASK, fin);
-            __syncwarp();
-            if (fm && first_fin == 0xffffffffu) first_fin = b0 + (u32)(__ffs(fm) - 1);
-            nfin += __popc(fm);
-            while (fm) {
-              const u32 l = (u32)(__ffs(fm) - 1);
-              fm &= fm - 1;
-              const u32 pos = b0 + l;
-              const u32 held = B.cdiv(S.ctx[pos]);
-              const u32 slot = SLOT(S.info[pos]);
-              free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], d.k, koff, L, d.hint);
-              d.nfree += held;
-              if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
-            }
-          }
-          __syncwarp();
-          req_iters += d.nRun;
-          if (nfin) {
-            u32 out = first_fin;
-            #pragma unroll 1
-            for (u32 b0 = first_fin; b0 < d.nD; b0 += 32) {
-              const u32 jj = b0 + lane;
-              const bool valid = jj < d.nD;
-              u32 vid = 0, vctx = 0, vrem = 0, vinfo = 0, vst = 0;
-              i64 vl = 0, vm = 0, va = 0, vt = 0;
-              if (valid) {
-                vid = S.id[jj];
-                vctx = S.ctx[jj];
-                vrem = S.rem[jj];
-                vinfo = S.info[jj];
-                vl = S.last[jj];
-                vm = S.maxgap[jj];
-                va = S.arr[jj];
-                vt = S.ttft[jj];
-                vst = stt[jj];
-              }
-              const bool keep = valid && vrem != 0;
-              const u32 km = __ballot_sync(FULLMASK, keep);
-              __syncwarp();
-              if (keep) {
-                const u32 dd = out + __popc(km & ltm);
-                S.id[dd] = vid;
-                S.ctx[dd] = vctx;
-                S.rem[dd] = vrem;
-                S.info[dd] = vinfo;
-                S.last[dd] = vl;
-                S.maxgap[dd] = vm;
-                S.arr[dd] = va;
-                S.ttft[dd] = vt;
-                stt[dd] = vst;
-              }
-              __syncwarp();
-              out += __popc(km);
-            }
-            d.nRun -= nfin;
-            d.nD -= nfin;
-            n_done += nfin;
-            nfin_tot += nfin;
-            last_fin = te > last_fin ? te : last_fin;
-          }
-          d.rmin = __reduce_min_sync(FULLMASK, rmin_d);
-          if (d.nRun == 0) d.rmin = 0;
-          fold_iter(d.k, wid, t, T, nrecomp, Dn, Np, Cd, m, nres, nadm, 0, nfin, blocks);
-          trace_iter(d.TA, FE[wid], BINNED, FULLT, trcD, P.trace_cap, W, t, te, blocks, flags);
-          d.peak = blocks > d.peak ? blocks : d.peak;
-          d.bns += blocks * (u64)T;
-          swo += swap_out;
-          swi += swap_in;
-          d.t = te;
-          d.last = te;
-          ++d.k;
-          d.idle = 0;
         }
       }
       __syncwarp();
       if (lane == 0) {
-        // keep the fields other workers may have changed while this one ran (none do for D)
         M.ds[dj] = d;
+        M.part[dj].done = done_w;
+        M.part[dj].tfin = tfin_w;
+        M.part[dj].flags = flags;
       }
-      __syncwarp();
-    } else {
+    }
+    __syncthreads();
+    if (!COORD) continue;
+    // The sequential loop stops at the event that finishes the last request (E*): once every
+    // request is done, only events before the decode workers' last finishing boundary (decode
+    // boundaries precede prefill boundaries at equal times) are still processed.
+    u32 dd = 0;
+    i64 tD = 0;
+    for (u32 w = 0; w < Y; ++w) {
+      dd += M.part[w].done;
+      tD = M.part[w].tfin > tD ? M.part[w].tfin : tD;
+    }
+    // ======================= scheduler phase (warp 0): arrivals and P boundaries before H, in
+    // time order (an arrival before a boundary at the same time), then the dispatches at H
+    while (true) {
+      const i64 ta = arr < n ? A[arr] : INF;
+      const i64 tw = lane < X ? M.ps[lane].t : INF;
+      const u32 psel = warp_argmin64(tw, lane < X);
+      const i64 tb = __shfl_sync(FULLMASK, tw, psel & 31u);
+      if (ta >= H && tb >= H) break;
+      if (n_done_c + dd == n && (ta < tb ? ta : tb) >= tD) break;
+      if (ta <= tb) {
+        // an arrival: dispatched to a prefill worker (no batch completes before H)
+        const u32 pi = pick(false, ta);
+        if (lane == 0) {
+          PScal &p = M.ps[pi];
+          qP0[(size_t)pi * n + p.qtail] = arr;
+          p.qtail += 1;
+          if (p.idle && ta < p.t) p.t = ta;
+        }
+        __syncwarp();
+        ++arr;
+        continue;
+      }
       // ================================================================ P_i boundary
-      const u32 pi = wsel - Y;
+      const u32 pi = psel;
       const u32 koff = 2 * pi;
       u32 *bmP = M.bmP + (size_t)pi * P.nwords_max;
       SP.bitmap = bmP;
@@ -1169,7 +1249,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         if (stop < nvalid) break;
       }
       nrej_tot += nrej;
-      n_done += nrej;
+      n_done_c += nrej;
       if (nb == 0) {  // idle: wait for a dispatch or for blocks to come back
         p.t = p.hmin;
         p.idle = 1;
@@ -1224,11 +1304,11 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           nfin += __popc(__ballot_sync(FULLMASK, one));
           __syncwarp();
         }
-        n_done += nfin;
+        n_done_c += nfin;
         nfin_tot += nfin;
         if (nfin) last_fin = te > last_fin ? te : last_fin;
         fold_iter(p.k, pi, t, T, nb, 0, Np, 0, 0, 0, nb, nrej, nfin, blocksP);
-        trace_iter(p.TA, FE[pi], BINNED, FULLT, trcP, P.trace_cap, W, t, te, blocksP, flags);
+        trace_iter(p.TA, FEp[pi], BINNED, FULLT, trcP, P.trace_cap, W, t, te, blocksP, flags);
         req_iters += nb;
         p.nb = nb;
         p.cur = 0;
@@ -1242,112 +1322,239 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       if (lane == 0) M.ps[pi] = p;
       __syncwarp();
     }
-  }
-  // ---- termination: flush traces, records of unfinished requests, stats
-  i64 t_final = 0;
-  u64 kall = 0, peak = 0, bns = 0;
-  for (u32 w = 0; w < NW; ++w) {
-    const bool isD = w >= X;
-    i64 lw;
-    if (isD) {
-      const DScal &d = M.ds[w - X];
-      lw = d.last;
-      kall += d.k;
-      peak = d.peak > peak ? d.peak : peak;
-      bns += d.bns;
-    } else {
-      lw = M.ps[w].last;
-      kall += M.ps[w].k;
-    }
-    t_final = lw > t_final ? lw : t_final;
-  }
-  for (u32 w = 0; w < NW; ++w) {
-    const bool isD = w >= X;
-    TraceAcc ta = isD ? M.ds[w - X].TA : M.ps[w].TA;
-    tokensim_mem_sample *tw = trc0 + (size_t)w * P.trace_cap;
-    if (BINNED)
-      while ((i64)ta.bin * W < t_final) trace_flush_bin(ta, tw, P.trace_cap, W, flags);
-    __syncwarp();
-    if (lane == 0) {
-      if (isD) M.ds[w - X].TA = ta;
-      else M.ps[w].TA = ta;
-    }
-    __syncwarp();
-  }
-  // unfinished: decode slots and pending entries carry their first-token latency, as do the
-  // members of an in-flight prefill batch; queued requests have none
-  for (u32 w = 0; w < Y; ++w) {
-    u32 *stt;
-    const WarpSmem S = dview(M, w, CAP, &stt);
-    const DScal &d = M.ds[w];
-    #pragma unroll 1
-    for (u32 x = lane; x < d.nD; x += 32)
-      write_record(rec + S.id[x], S.ttft[x], 0, 0, S.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);
-    const FifoEnt *fifo = fifo0 + (size_t)w * n;
-    #pragma unroll 1
-    for (u32 x = d.fhead + lane; x < d.ftail; x += 32) {
-      const u32 id = fifo[x].id;
-      write_record(rec + id, fifo[x].join - A[id], 0, 0, 0, TOKENSIM_REQ_UNFINISHED, 0);
-    }
-  }
-  for (u32 w = 0; w < X; ++w) {
-    const PScal &p = M.ps[w];
-    if (p.nb == 0) continue;
-    #pragma unroll 1
-    for (u32 x = lane; x < p.nb; x += 32) {
-      const u32 id = batch0[(size_t)w * CAP + x];
-      if (OU[id] > 1) write_record(rec + id, p.tdisp - A[id], 0, 0, 0, TOKENSIM_REQ_UNFINISHED, 0);
-    }
-  }
-  ev_flush(L);
-  it_flush(L);
-  const u64 dig_s = warp_sum64(L.dig_s);
-  const u64 dig_b = warp_sum64(L.dig_b);
-  if (lane == 0) {
-    SimStats st;
-    st.flags = flags | ((nrej_tot == n) ? (u32)TOKENSIM_PT_ALL_REJECTED : 0u);
-    st.pad = 0;
-    st.n_finished = nfin_tot;
-    st.n_rejected = nrej_tot;
-    st.n_iterations = kall;
-    st.n_req_iters = req_iters;
-    st.n_preempt = npre;
-    st.swap_out = swo;
-    st.swap_in = swi;
-    st.last_finish = last_fin;
-    st.t_final = t_final;
-    st.sched_d = dig_s;
-    st.block_d = dig_b;
-    st.req_d = 0;
-    st.total_blocks = (u64)Y * totD;  // the decode pool (reading R-X5)
-    st.peak_blocks = peak;
-    st.block_ns_sum = bns;
-    for (u32 w = 0; w < PDN_MAXW; ++w) {
-      u64 tn = 0, fn = 0, fb = 0;
-      if (w < NW) {
-        const TraceAcc &ta = w < X ? M.ps[w].TA : M.ds[w - X].TA;
-        tn = ta.tn;
-        fn = FE[w].n;
-        fb = FE[w].bytes;
+    if ((flags & TOKENSIM_PT_INTERNAL_ERROR) || td_next != H || (P.horizon >= 0 && H >= P.horizon) ||
+        n_done_c + dd == n)
+      continue;
+    {
+      const i64 td = H;
+      // ================================================ dispatch events at td, request-id order
+      if (lane == 0)
+        for (u32 w = 0; w < X; ++w)
+          if (M.ps[w].nb > 0 && M.ps[w].tdisp == td) M.ps[w].cur = 0;
+      __syncwarp();
+      while (true) {
+        // the smallest id among completing batches' heads, else an arrival at td
+        u32 hid = 0xffffffffu;
+        if (lane < X) {
+          const PScal &p = M.ps[lane];
+          if (p.nb > 0 && p.tdisp == td && p.cur < p.nb) hid = batch0[(size_t)lane * CAP + p.cur];
+        }
+        const u32 mid = __reduce_min_sync(FULLMASK, hid);
+        if (mid != 0xffffffffu) {
+          const u32 src = __ffs(__ballot_sync(FULLMASK, hid == mid)) - 1;
+          if (lane == 0) M.ps[src].cur += 1;
+          __syncwarp();
+          if (OU[mid] > 1) {  // o = 1 finished on its prefill worker
+            const u32 dq = pick(true, td);
+            if (lane == 0) {
+              DScal &d = M.ds[dq];
+              FifoEnt e;
+              e.id = mid;
+              e.seg = src;  // the prefill worker holding its blocks
+              e.len = B.cdiv(PR[mid]);
+              e.pad = 0;
+              e.join = td;
+              e.xend = INF;
+              fifo0[(size_t)dq * n + d.ftail] = e;
+              d.ftail += 1;
+              if (d.idle && td < d.t) d.t = td;
+            }
+            __syncwarp();
+          }
+          continue;
+        }
+        if (arr < n && A[arr] == td) {
+          const u32 pi = pick(false, td);
+          if (lane == 0) {
+            PScal &p = M.ps[pi];
+            qP0[(size_t)pi * n + p.qtail] = arr;
+            p.qtail += 1;
+            if (p.idle && td < p.t) p.t = td;
+          }
+          __syncwarp();
+          ++arr;
+          continue;
+        }
+        break;
       }
-      st.trace_n[w] = FULLT ? fn : (tn < P.trace_cap ? tn : P.trace_cap);
-      st.trace_b[w] = fb;
+      if (lane == 0)
+        for (u32 w = 0; w < X; ++w)
+          if (M.ps[w].nb > 0 && M.ps[w].tdisp == td) {
+            M.ps[w].nb = 0;
+            M.ps[w].tdisp = INF;
+          }
+      __syncwarp();
+
     }
-    st.iter_n = kall < P.it_cap ? kall : P.it_cap;
-    st.n_transfers = n_xfer;
-    st.transfer_bytes = xbytes;
-    st.ff_iters = ff_iters;
-    st.ff_runs = ff_runs;
-    st.cycles = (u64)(clock64() - clk0);
-    st.cyc_ff = 0;
-    st.cyc_ff_fail = 0;
-    st.cyc_normal = 0;
-    for (int q = 0; q < 8; ++q) st.phase[q] = 0;
-    for (int q = 0; q < 8; ++q) st.nphase[q] = 0;
-    st.n_req = P.n_req;
-    for (int q = 0; q < 5; ++q) st.ff_fail[q] = 0;
-    for (int q = 0; q < 5; ++q) st.ff_cut[q] = 0;
-    P.stats[j] = st;
   }
-  __syncwarp();
+  // ---- termination: every warp hands in its partials; warp 0 flushes traces, writes the
+  // records of unfinished requests and the stats
+  ev_flush(L);
+  pdn_it_flush(L, itcur);
+  {
+    const u64 dig_s = warp_sum64(L.dig_s);
+    const u64 dig_b = warp_sum64(L.dig_b);
+    if (lane == 0) {
+      PdnPart &q = M.part[dj];
+      q.req_iters = req_iters;
+      q.npre = npre;
+      q.swo = swo;
+      q.swi = swi;
+      q.nfin = nfin_tot;
+      q.n_xfer = n_xfer;
+      q.xbytes = xbytes;
+      q.ff_iters = ff_iters;
+      q.ff_runs = ff_runs;
+      q.dig_s = dig_s;
+      q.dig_b = dig_b;
+      q.last_fin = last_fin;
+      q.flags = flags;
+      q.done = done_w;
+      q.fe = fe;
+    }
+  }
+  __syncthreads();
+  if (COORD) {
+    i64 t_final = 0;
+    u64 kall = 0, peak = 0, bns = 0;
+    for (u32 w = 0; w < NW; ++w) {
+      const bool isD = w >= X;
+      i64 lw;
+      if (isD) {
+        const DScal &d = M.ds[w - X];
+        lw = d.last;
+        kall += d.k;
+        peak = d.peak > peak ? d.peak : peak;
+        bns += d.bns;
+      } else {
+        lw = M.ps[w].last;
+        kall += M.ps[w].k;
+      }
+      t_final = lw > t_final ? lw : t_final;
+    }
+    u64 s_req_iters = 0, s_npre = 0, s_swo = 0, s_swi = 0, s_nfin = 0, s_xfer = 0, s_xbytes = 0, s_ffi = 0,
+        s_ffr = 0, s_dig_s = 0, s_dig_b = 0;
+    i64 s_last = 0;
+    u32 s_flags = 0;
+    for (u32 w = 0; w < Y; ++w) {
+      const PdnPart &q = M.part[w];
+      s_req_iters += q.req_iters;
+      s_npre += q.npre;
+      s_swo += q.swo;
+      s_swi += q.swi;
+      s_nfin += q.nfin;
+      s_xfer += q.n_xfer;
+      s_xbytes += q.xbytes;
+      s_ffi += q.ff_iters;
+      s_ffr += q.ff_runs;
+      s_dig_s += q.dig_s;
+      s_dig_b += q.dig_b;
+      s_last = q.last_fin > s_last ? q.last_fin : s_last;
+      s_flags |= q.flags;
+    }
+    for (u32 w = 0; w < NW; ++w) {
+      const bool isD = w >= X;
+      TraceAcc ta = isD ? M.ds[w - X].TA : M.ps[w].TA;
+      tokensim_mem_sample *tw = trc0 + (size_t)w * P.trace_cap;
+      if (BINNED)
+        while ((i64)ta.bin * W < t_final) trace_flush_bin(ta, tw, P.trace_cap, W, s_flags);
+      __syncwarp();
+      if (lane == 0) {
+        if (isD) M.ds[w - X].TA = ta;
+        else M.ps[w].TA = ta;
+      }
+      __syncwarp();
+    }
+    // unfinished: decode slots and pending entries carry their first-token latency, as do the
+    // members of an in-flight prefill batch; queued requests have none
+    for (u32 w = 0; w < Y; ++w) {
+      u32 *sttw;
+      const WarpSmem Sw = dview(M, w, CAP, &sttw);
+      const DScal &d = M.ds[w];
+      #pragma unroll 1
+      for (u32 x = lane; x < d.nD; x += 32)
+        write_record(rec + Sw.id[x], Sw.ttft[x], 0, 0, Sw.info[x] >> 16, TOKENSIM_REQ_UNFINISHED, 0);
+      const FifoEnt *fw = fifo0 + (size_t)w * n;
+      #pragma unroll 1
+      for (u32 x = d.fhead + lane; x < d.ftail; x += 32) {
+        const u32 id = fw[x].id;
+        write_record(rec + id, fw[x].join - A[id], 0, 0, 0, TOKENSIM_REQ_UNFINISHED, 0);
+      }
+    }
+    for (u32 w = 0; w < X; ++w) {
+      const PScal &p = M.ps[w];
+      if (p.nb == 0) continue;
+      #pragma unroll 1
+      for (u32 x = lane; x < p.nb; x += 32) {
+        const u32 id = batch0[(size_t)w * CAP + x];
+        if (OU[id] > 1) write_record(rec + id, p.tdisp - A[id], 0, 0, 0, TOKENSIM_REQ_UNFINISHED, 0);
+      }
+    }
+    if (lane == 0) {
+      SimStats st;
+      st.flags = s_flags | ((nrej_tot == n) ? (u32)TOKENSIM_PT_ALL_REJECTED : 0u);
+      st.pad = 0;
+      st.n_finished = s_nfin;
+      st.n_rejected = nrej_tot;
+      st.n_iterations = kall;
+      st.n_req_iters = s_req_iters;
+      st.n_preempt = s_npre;
+      st.swap_out = s_swo;
+      st.swap_in = s_swi;
+      st.last_finish = s_last;
+      st.t_final = t_final;
+      st.sched_d = s_dig_s;
+      st.block_d = s_dig_b;
+      st.req_d = 0;
+      st.total_blocks = (u64)Y * totD;  // the decode pool (reading R-X5)
+      st.peak_blocks = peak;
+      st.block_ns_sum = bns;
+      for (u32 w = 0; w < PDN_MAXW; ++w) {
+        u64 tn = 0, fn = 0, fb = 0;
+        if (w < NW) {
+          const TraceAcc &ta = w < X ? M.ps[w].TA : M.ds[w - X].TA;
+          const FullEnc &f = w < X ? FEp[w] : M.part[w - X].fe;
+          tn = ta.tn;
+          fn = f.n;
+          fb = f.bytes;
+        }
+        st.trace_n[w] = FULLT ? fn : (tn < P.trace_cap ? tn : P.trace_cap);
+        st.trace_b[w] = fb;
+      }
+      st.iter_n = kall < P.it_cap ? kall : P.it_cap;
+      st.n_transfers = s_xfer;
+      st.transfer_bytes = s_xbytes;
+      st.ff_iters = s_ffi;
+      st.ff_runs = s_ffr;
+      st.cycles = (u64)(clock64() - clk0);
+      st.cyc_ff = 0;
+      st.cyc_ff_fail = 0;
+      st.cyc_normal = 0;
+      for (int q = 0; q < 8; ++q) st.phase[q] = 0;
+      for (int q = 0; q < 8; ++q) st.nphase[q] = 0;
+      st.n_req = P.n_req;
+      for (int q = 0; q < 5; ++q) st.ff_fail[q] = 0;
+      for (int q = 0; q < 5; ++q) st.ff_cut[q] = 0;
+      P.stats[j] = st;
+    }
+  }
+  __syncthreads();  // the CTA's next point reuses the shared memory
+}
+
+// One CTA per node point: y warps (warp j runs decode worker j; warp 0 also the scheduler and
+// the prefill workers), points taken from the LPT queue.
+template <int CAP, bool P2>
+__global__ void __launch_bounds__(256, 1) sim_node_kernel(SweepParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ u32 s_qi;
+  const u32 wib = threadIdx.x >> 5;
+  u32 *bt = P.bt + (size_t)blockIdx.x * P.bt_tables * CAP * P.bt_len;
+  while (true) {
+    if (threadIdx.x == 0) s_qi = atomicAdd(P.queue, 1u);
+    __syncthreads();
+    const u32 qi = s_qi;
+    __syncthreads();
+    if ((u64)qi >= P.n_run) break;
+    simulate_pdn<CAP, P2>(P, P.order[qi], smem_raw, bt, wib);
+  }
 }
