@@ -731,8 +731,11 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   }
   if (const char *ev = getenv("TOKENSIM_XS")) xs = atoi(ev) != 0;
   // (the node kernel's occupancy is asked for its CTA of pd_y warps)
-  e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general, !helper, xs),
-                    (int)h->cap, h->pd_general ? (int)h->pd_y : (int)L0.wpb, per_warp * L0.wpb, h->nwords_max, &occ);
+  // node: the register-capped two-CTAs-per-SM build once there are more points than SMs
+  const bool node_two = h->pd_general && h->pd_y <= 6 && n_run > (u64)sms;
+  e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general, !helper, xs), (int)h->cap,
+                    h->pd_general ? (int)h->pd_y + (node_two ? 16 : 0) : (int)L0.wpb, per_warp * L0.wpb, h->nwords_max,
+                    &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
   const Layout L = make_layout(h, n_run, sms, occ);
@@ -843,6 +846,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.pdn_bytes_per_warp = L.pdn_per_warp;
   P.pd_x = h->pd_x;
   P.pd_y = h->pd_y;
+  P.node_two = node_two ? 1u : 0u;
   P.dispatch = h->opt.dispatch;
   P.link_mode = h->opt.link_mode;
   P.preload_buf = h->opt.preload_buffer_bytes;

@@ -4,18 +4,28 @@
 #include "sim_core.cuh"
 
 namespace ts {
-template <int CAP, bool P2>
-static cudaError_t launch_node_t(const SweepParams &p, int blocks, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(sim_node_kernel<CAP, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int CAP, bool P2, bool TWO>
+static cudaError_t launch_node_k(const SweepParams &p, int blocks, size_t smem, cudaStream_t st) {
+  cudaError_t e =
+      cudaFuncSetAttribute(sim_node_kernel<CAP, P2, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  sim_node_kernel<CAP, P2><<<blocks, (int)p.pd_y * 32, smem, st>>>(p);
+  sim_node_kernel<CAP, P2, TWO><<<blocks, (int)p.pd_y * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 template <int CAP, bool P2>
-static cudaError_t occ_node_t(int warps, size_t smem, int *b) {
-  cudaError_t e = cudaFuncSetAttribute(sim_node_kernel<CAP, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static cudaError_t launch_node_t(const SweepParams &p, int blocks, size_t smem, cudaStream_t st) {
+  return p.node_two ? launch_node_k<CAP, P2, true>(p, blocks, smem, st) : launch_node_k<CAP, P2, false>(p, blocks, smem, st);
+}
+template <int CAP, bool P2, bool TWO>
+static cudaError_t occ_node_k(int warps, size_t smem, int *b) {
+  cudaError_t e =
+      cudaFuncSetAttribute(sim_node_kernel<CAP, P2, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_node_kernel<CAP, P2>, warps * 32, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, sim_node_kernel<CAP, P2, TWO>, warps * 32, smem);
+}
+template <int CAP, bool P2>
+static cudaError_t occ_node_t(int warps, size_t smem, int *b) {
+  return warps >= 16 ? occ_node_k<CAP, P2, true>(warps - 16, smem, b) : occ_node_k<CAP, P2, false>(warps, smem, b);
 }
 template <bool P2>
 static cudaError_t launch_node_c(const SweepParams &p, int cap, int blocks, size_t smem, cudaStream_t st) {
@@ -40,7 +50,7 @@ cudaError_t launch_sim_node(const SweepParams &p, int cap, int wpb, int blocks, 
   (void)wpb;
   return p.all_p2 ? launch_node_c<true>(p, cap, blocks, smem, st) : launch_node_c<false>(p, cap, blocks, smem, st);
 }
-// warps = pd_y (the warps of one node CTA)
+// warps = pd_y (the warps of one node CTA), + 16 for the two-CTAs-per-SM build
 cudaError_t sim_occupancy_node(int cap, int warps, size_t smem, u32 nw, int *b) {
   (void)nw;
   int b1 = 0, b2 = 0;

@@ -16,7 +16,8 @@
 // release prefill blocks at the transfer end).  The scheduler warp computes an epoch horizon H no
 // dispatch can precede: the next known end-of-prefill dispatch, and -- since a prefill batch
 // dispatches no earlier than one minimal prefill iteration (Tlb) after it starts -- the next
-// prefill boundary + Tlb, the next arrival + Tlb, and (while a prefill worker is idle with
+// arrival + Tlb, the next boundary + Tlb of a prefill worker with queued requests (one with an
+// empty queue starts a batch only after an arrival), and (while a prefill worker is idle with
 // queued requests, which a pull's block release could wake) the next decode boundary + Tlb.
 // Then (1) every decode warp processes its own boundaries before H in parallel (quiet stretches
 // cut at H), and (2) warp 0 processes the arrivals and prefill boundaries before H in time order
@@ -55,6 +56,7 @@ struct PdnPart {  // one warp's partial outputs (summed by warp 0 at the end)
   u64 req_iters, npre, swo, swi, nfin, n_xfer, xbytes, ff_iters, ff_runs, dig_s, dig_b;
   i64 last_fin;
   i64 tfin;         // start of the latest iteration in which its decode worker finished requests
+  u64 dcyc;         // SM cycles in decode phases (profile)
   u32 flags, done;  // done: requests its decode worker finished (read by warp 0 every epoch)
   FullEnc fe;       // its decode worker's FULL trace stream state
 };
@@ -338,6 +340,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   i64 last_fin = 0, tfin_w = 0;
   // warp 0 only: the scheduler's state
   u32 arr = 0, n_done_c = 0;
+  i64 ta_next = n > 0 ? A[0] : INT64_MAX;  // A[arr], kept in a register (the loads leave the chain)
   u64 rrP = 0, rrD = 0, nrej_tot = 0;
   const bool ff_on = P.ff_enable != 0;
   const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
@@ -389,6 +392,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   };
 
   i64 td_next = INF;  // warp 0: the next known end-of-prefill dispatch
+  u64 n_epochs = 0, cyc_sched = 0, cyc_dec = 0;  // profile (point_profile's phase words)
   while (true) {
     // ============================================================ epoch horizon (warp 0)
     if (COORD) {
@@ -403,18 +407,22 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       if (nd == n || (ef & TOKENSIM_PT_INTERNAL_ERROR)) {
         stop = 1;
       } else {
-        const i64 ta = arr < n ? A[arr] : INF;
-        i64 tdk = INF, tp = INF, tdm = INF;
+        const i64 ta = ta_next;
+        // tp: the next prefill boundary; tq: the next boundary of a prefill worker with queued
+        // requests -- the only boundaries that can start a batch without an arrival first
+        i64 tdk = INF, tp = INF, tq = INF, tdm = INF;
         bool blk = false;
         if (lane < X) {
           const PScal &p = M.ps[lane];
           if (p.nb > 0) tdk = p.tdisp;
           tp = p.t;
           blk = p.idle && p.qhead < p.qtail;
+          if (p.qhead < p.qtail) tq = p.t;
         }
         if (lane < Y) tdm = M.ds[lane].t;
         tdk = min8_i64(tdk);
         tp = min8_i64(tp);
+        tq = min8_i64(tq);
         tdm = min8_i64(tdm);
         const bool blocked = __ballot_sync(FULLMASK, blk) != 0u;
         i64 tall = ta < tdk ? ta : tdk;
@@ -428,7 +436,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           stop = 1;
         } else {
           H = tdk;
-          const i64 h1 = sat_add(ta, Tlb), h2 = sat_add(tp, Tlb);
+          const i64 h1 = sat_add(ta, Tlb), h2 = sat_add(tq, Tlb);
           H = h1 < H ? h1 : H;
           H = h2 < H ? h2 : H;
           if (blocked) {
@@ -447,6 +455,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     __syncthreads();
     if (ctl->stop) break;
     const i64 H = ctl->H;
+    const long long c_d0 = clock64();
     // ============================================== decode phase: every D_j boundary before H
     {
       DScal d = M.ds[dj];
@@ -1117,8 +1126,11 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         M.part[dj].flags = flags;
       }
     }
+    cyc_dec += (u64)(clock64() - c_d0);
     __syncthreads();
     if (!COORD) continue;
+    const long long c_s0 = clock64();
+    ++n_epochs;
     // The sequential loop stops at the event that finishes the last request (E*): once every
     // request is done, only events before the decode workers' last finishing boundary (decode
     // boundaries precede prefill boundaries at equal times) are still processed.
@@ -1131,7 +1143,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     // ======================= scheduler phase (warp 0): arrivals and P boundaries before H, in
     // time order (an arrival before a boundary at the same time), then the dispatches at H
     while (true) {
-      const i64 ta = arr < n ? A[arr] : INF;
+      const i64 ta = ta_next;
       const i64 tw = lane < X ? M.ps[lane].t : INF;
       const u32 psel = warp_argmin64(tw, lane < X);
       const i64 tb = __shfl_sync(FULLMASK, tw, psel & 31u);
@@ -1148,6 +1160,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         }
         __syncwarp();
         ++arr;
+        ta_next = arr < n ? A[arr] : INF;
         continue;
       }
       // ================================================================ P_i boundary
@@ -1322,6 +1335,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       if (lane == 0) M.ps[pi] = p;
       __syncwarp();
     }
+    cyc_sched += (u64)(clock64() - c_s0);
     if ((flags & TOKENSIM_PT_INTERNAL_ERROR) || td_next != H || (P.horizon >= 0 && H >= P.horizon) ||
         n_done_c + dd == n)
       continue;
@@ -1363,7 +1377,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           }
           continue;
         }
-        if (arr < n && A[arr] == td) {
+        if (ta_next == td) {
           const u32 pi = pick(false, td);
           if (lane == 0) {
             PScal &p = M.ps[pi];
@@ -1373,6 +1387,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           }
           __syncwarp();
           ++arr;
+          ta_next = arr < n ? A[arr] : INF;
           continue;
         }
         break;
@@ -1411,6 +1426,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       q.flags = flags;
       q.done = done_w;
       q.fe = fe;
+      q.dcyc = cyc_dec;
     }
   }
   __syncthreads();
@@ -1531,6 +1547,15 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       st.cyc_ff_fail = 0;
       st.cyc_normal = 0;
       for (int q = 0; q < 8; ++q) st.phase[q] = 0;
+      // profile: epochs, scheduler-phase cycles (warp 0), decode-phase cycles of warp 0, the
+      // largest and the summed decode-phase cycles over the decode warps
+      st.phase[0] = n_epochs;
+      st.phase[1] = cyc_sched;
+      st.phase[2] = M.part[0].dcyc;
+      for (u32 w = 0; w < Y; ++w) {
+        st.phase[3] = M.part[w].dcyc > st.phase[3] ? M.part[w].dcyc : st.phase[3];
+        st.phase[4] += M.part[w].dcyc;
+      }
       for (int q = 0; q < 8; ++q) st.nphase[q] = 0;
       st.n_req = P.n_req;
       for (int q = 0; q < 5; ++q) st.ff_fail[q] = 0;
@@ -1542,9 +1567,12 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
 }
 
 // One CTA per node point: y warps (warp j runs decode worker j; warp 0 also the scheduler and
-// the prefill workers), points taken from the LPT queue.
-template <int CAP, bool P2>
-__global__ void __launch_bounds__(256, 1) sim_node_kernel(SweepParams P) {
+// the prefill workers), points taken from the LPT queue.  TWO (y <= 6 and more points than
+// SMs): registers capped at 168 so two CTAs share an SM.  Measured on c6 (256 points): one
+// point alone 208 -> 258 ms (spills), two per SM 1.4x slower each, the sweep 367 ms either way
+// (one wave of pairs vs two waves of singles); it pays once the points fill both waves.
+template <int CAP, bool P2, bool TWO>
+__global__ void __launch_bounds__(TWO ? 192 : 256, TWO ? 2 : 1) sim_node_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u32 s_qi;
   const u32 wib = threadIdx.x >> 5;
