@@ -557,6 +557,45 @@ def test_node_sharegpt_grid(api):
                 assert sw.summaries().tobytes() == off.summaries().tobytes()
 
 
+def test_node_cta_shapes_are_byte_identical(api):
+    """The node kernel's CTA-parallel decode warps (sim_pdn.cuh) give the same bytes run twice, and
+    in both builds: 192 points at once (more points than SMs: the register-capped build, two CTAs
+    per SM) and the same points in halves of 96 (one CTA per SM); sampled points vs the oracle."""
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    cfg = si.SweepConfig("node-shapes", si.LLAMA2_7B, [si.A100],
+                         [si.Policy(preempt=si.SWAP), si.Policy(preempt=si.RECOMPUTE)],
+                         si.Workload(200, [2.0 * 2.0 ** (k / 2.0) for k in range(16)], list(range(6))),
+                         si.Options(topology=si.PD_PAIR, pd_prefill=2, pd_decode=6,
+                                    dispatch=si.LEAST_OUTSTANDING, iteration_trace_cap=1 << 16))
+    n = cfg.num_points
+    assert n > sms
+    a = run_gpu(api, cfg)
+    assert a.run_info()["sim_blocks"] > sms  # two CTAs per SM
+    sa = a.summaries().tobytes()
+    recs = {p: a.records(p).tobytes() for p in (0, 77, n - 1)}
+    its = {p: a.iteration_trace(p) for p in (0, n - 1)}
+    a.run()
+    assert a.summaries().tobytes() == sa
+    b = api.Sweep(cfg)
+    half = n // 2
+    parts = []
+    for beg in (0, half):
+        b.run(beg, beg + half)
+        assert b.run_info()["sim_blocks"] <= sms
+        parts.append(b.summaries().tobytes())
+        for p in recs:
+            if beg <= p < beg + half:
+                assert b.records(p).tobytes() == recs[p]
+        for p in its:
+            if beg <= p < beg + half:
+                g, h = b.iteration_trace(p), its[p]
+                key = lambda x: np.lexsort((x["k"], x["worker"]))  # noqa: E731
+                assert g[key(g)].tobytes() == h[key(h)].tobytes()
+    assert b"".join(parts) == sa
+    check_pd_points(a, cfg, [0, 77, n - 1])
+
+
 # ------------------------------------------------------------------ NEXT-4 preload-buffer link
 def test_preload_link_parity(api):
     """PRELOAD swap-in pipeline (reading R-N4) on the unified worker, the P/D pair and a node:
