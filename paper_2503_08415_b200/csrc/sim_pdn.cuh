@@ -436,7 +436,36 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           stop = 1;
         } else {
           H = tdk;
-          const i64 h1 = sat_add(ta, Tlb), h2 = sat_add(tq, Tlb);
+          i64 h1 = sat_add(ta, Tlb);
+          // The arrival's own dispatch, exactly: when nothing on the prefill side happens before
+          // it (no batch completes, no queued worker's boundary), the arrival is alone at its
+          // time and its scheduler choice (round robin / least outstanding: unaffected by the
+          // decode phase) is a worker with an empty queue and no batch, whose free blocks admit
+          // it now (pulls only return blocks), its batch is {arrival} and dispatches at
+          // ta + T(prompt): the decode phase runs to that dispatch, which the scheduler phase
+          // then processes -- one epoch per request instead of two.
+          if (ta != INF && tdk > ta && tq > ta && P.dispatch != TOKENSIM_DISPATCH_LEAST_MEMORY &&
+              (arr + 1 >= n || A[arr + 1] != ta)) {
+            u32 pi;
+            if (P.dispatch == TOKENSIM_DISPATCH_ROUND_ROBIN) {
+              pi = (u32)(rrP % X);
+            } else {
+              u64 v = ~0ull;
+              if (lane < X) v = (u64)(M.ps[lane].qtail - M.ps[lane].qhead) + M.ps[lane].nb;
+              pi = warp_argmin64((i64)v, lane < X);
+            }
+            const PScal &p = M.ps[pi];
+            const u32 pp = PR[arr];
+            const u32 need = B.cdiv(pp);
+            if (p.qhead == p.qtail && p.nb == 0 && (u64)need <= HPP.cap_fresh && mns >= 1u && pp <= mbt &&
+                (i64)p.nfree - (i64)need >= wm) {
+              const i64 T1 = iter_time_ns(KP, pp, (u64)pp * (pp + 1) / 2, 1, 0, 0, 0);
+              h1 = ta + T1;
+              const i64 h1n = arr + 1 < n ? sat_add(A[arr + 1], Tlb) : INF;  // the next arrival
+              h1 = h1n < h1 ? h1n : h1;
+            }
+          }
+          const i64 h2 = sat_add(tq, Tlb);
           H = h1 < H ? h1 : H;
           H = h2 < H ? h2 : H;
           if (blocked) {
@@ -445,7 +474,6 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           }
           if (P.horizon >= 0 && P.horizon < H) H = P.horizon;
         }
-        td_next = tdk;
       }
       if (lane == 0) {
         ctl->H = H;
@@ -1336,6 +1364,11 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       __syncwarp();
     }
     cyc_sched += (u64)(clock64() - c_s0);
+    {  // the next known dispatch, now (a batch started in this phase may end exactly at H)
+      const i64 tdl = (lane < X && M.ps[lane].nb > 0) ? M.ps[lane].tdisp : INF;
+      td_next = min8_i64(tdl);
+      if (td_next < H && n_done_c + dd != n) flags |= TOKENSIM_PT_INTERNAL_ERROR;  // the decode phase ran past it
+    }
     if ((flags & TOKENSIM_PT_INTERNAL_ERROR) || td_next != H || (P.horizon >= 0 && H >= P.horizon) ||
         n_done_c + dd == n)
       continue;
