@@ -392,9 +392,10 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   };
 
   i64 td_next = INF;  // warp 0: the next known end-of-prefill dispatch
-  u64 n_epochs = 0, cyc_sched = 0, cyc_dec = 0;  // profile (point_profile's phase words)
+  u64 n_epochs = 0, cyc_sched = 0, cyc_dec = 0, cyc_h = 0, cyc_wait = 0;  // profile (point_profile's phase words)
   while (true) {
     // ============================================================ epoch horizon (warp 0)
+    const long long c_h0 = clock64();
     if (COORD) {
       u32 nd = n_done_c;
       u32 ef = flags;
@@ -480,6 +481,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         ctl->stop = stop;
       }
     }
+    cyc_h += (u64)(clock64() - c_h0);
     __syncthreads();
     if (ctl->stop) break;
     const i64 H = ctl->H;
@@ -1154,10 +1156,12 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         M.part[dj].flags = flags;
       }
     }
-    cyc_dec += (u64)(clock64() - c_d0);
+    const long long c_d1 = clock64();
+    cyc_dec += (u64)(c_d1 - c_d0);
     __syncthreads();
     if (!COORD) continue;
     const long long c_s0 = clock64();
+    cyc_wait += (u64)(c_s0 - c_d1);
     ++n_epochs;
     // The sequential loop stops at the event that finishes the last request (E*): once every
     // request is done, only events before the decode workers' last finishing boundary (decode
@@ -1589,6 +1593,8 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
         st.phase[3] = M.part[w].dcyc > st.phase[3] ? M.part[w].dcyc : st.phase[3];
         st.phase[4] += M.part[w].dcyc;
       }
+      st.phase[5] = cyc_h;     // warp 0: horizon computations
+      st.phase[6] = cyc_wait;  // warp 0: waiting for the slowest decode warp
       for (int q = 0; q < 8; ++q) st.nphase[q] = 0;
       st.n_req = P.n_req;
       for (int q = 0; q < 5; ++q) st.ff_fail[q] = 0;

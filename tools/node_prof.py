@@ -4,7 +4,8 @@
 
 Prints, for the longest points: SM cycles, iterations, epochs, and the cycles warp 0 spent in
 scheduler phases, its own decode phases, and the largest / summed decode-phase cycles over the
-decode warps (point_profile's stretch_phase_cycles[0..4] for node points).
+decode warps, its horizon computations and its waits for the slowest decode warp
+(point_profile's stretch_phase_cycles[0..6] for node points).
 """
 import argparse
 import os
@@ -34,7 +35,8 @@ for p in np.argsort(-cy)[:a.top]:
     ph = x["stretch_phase_cycles"]
     print(f"point {p}: cycles {x['sm_cycles']:.3e} iters {x['n_iterations']} ff {x['ff_iterations']} "
           f"stretches {x['ff_stretches']} epochs {ph[0]} sched {ph[1]:.3e} dec0 {ph[2]:.3e} "
-          f"dec_max {ph[3]:.3e} dec_sum {ph[4]:.3e}  cyc/epoch {x['sm_cycles'] / max(1, ph[0]):.0f}")
+          f"dec_max {ph[3]:.3e} dec_sum {ph[4]:.3e} horizon {ph[5]:.3e} wait {ph[6]:.3e} "
+          f"cyc/epoch {x['sm_cycles'] / max(1, ph[0]):.0f}")
 ms = cy / 1.965e6
 q = np.percentile(ms, [0, 10, 25, 50, 75, 90, 100])
 print("per-point ms at 1.965 GHz: min/p10/p25/p50/p75/p90/max", " ".join("%.0f" % v for v in q),
