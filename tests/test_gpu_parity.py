@@ -529,6 +529,31 @@ def test_node_micro_configs(api):
         check_pd_points(sw, cfg, list(range(cfg.num_points)), iters=True)
 
 
+def test_node_epoch_stress(api):
+    """The node kernel's epoch horizons (sim_pdn.cuh) under adversarial arrivals: bursts of equal
+    timestamps (the exact-dispatch prediction must stand aside), dense and sparse streams, tiny
+    and large KV pools, every dispatch policy, 1..4 prefill x 1..7 decode workers, vs the
+    oracle's sequential node loop (summaries, records, traces, iteration records)."""
+    rng = np.random.default_rng(4242)
+    for it in range(48):
+        cfg = _micro_pd(rng)
+        n = int(rng.integers(20, 160))
+        base = np.sort(rng.integers(0, int(rng.choice([2e8, 2e9, 2e10])), n))
+        if it % 3 == 0:  # bursts: runs of identical arrival times
+            base = np.repeat(base[: max(1, n // 4)], 4)[:n]
+            base = np.sort(base)
+        p = rng.integers(1, 64, len(base))
+        o = rng.integers(1, 64, len(base))
+        w = replace(cfg.workload, num_requests=len(base), trace_arrival_ns=base.tolist(), trace_prompt=p.tolist(),
+                    trace_output=o.tolist())
+        x = int(rng.integers(1, 5))
+        y = int(rng.integers(1, 9 - x))
+        d = str(rng.choice([si.ROUND_ROBIN, si.LEAST_OUTSTANDING, si.LEAST_MEMORY]))
+        cfg = replace(cfg, workload=w, options=replace(cfg.options, pd_prefill=x, pd_decode=y, dispatch=d))
+        sw = run_gpu(api, cfg)
+        check_pd_points(sw, cfg, list(range(cfg.num_points)), iters=True)
+
+
 def test_node_loop_equals_pair(api):
     """The general node loop run on 1P:1D pairs gives the pair kernel's bytes."""
     rng = np.random.default_rng(43)
