@@ -6,4 +6,4 @@ behind the C ABI in include/tokensim.h; this package is the thin Python binding.
 """
 from ._lib import LIB_PATH, RECORD_DTYPE, SAMPLE_DTYPE, ITER_DTYPE, SUMMARY_DTYPE  # noqa: F401
 from .api import (Sweep, TokensimError, METRICS, sweep, run_distributed, gather_summaries,  # noqa: F401
-                  shard_range, version, marshal)
+                  shard_range, version, marshal, sweep_resumable, config_fingerprint)

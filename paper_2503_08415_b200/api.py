@@ -290,6 +290,54 @@ def sweep(cfg: si.SweepConfig, device=None) -> np.ndarray:
         sw.close()
 
 
+def config_fingerprint(cfg: si.SweepConfig) -> str:
+    """A stable hash of a sweep configuration (checkpoints refuse to resume another config)."""
+    import hashlib
+    return hashlib.sha256(repr(cfg).encode()).hexdigest()[:32]
+
+
+def sweep_resumable(cfg: si.SweepConfig, path: str, chunk_points: int = 1024, device=None,
+                    max_chunks: Optional[int] = None) -> np.ndarray:
+    """Point-granular checkpoint / resume: run the sweep in chunks of
+    `chunk_points` consecutive points, writing every finished chunk's summaries to the
+    checkpoint `path` (.npz, replaced atomically); a rerun skips the chunks already there.
+    `max_chunks` stops after that many new chunks (an interrupted job, for tests).  Returns the
+    summaries of every finished point (all points once complete; unfinished rows are zero,
+    with version 0)."""
+    import os
+    fp = config_fingerprint(cfg)
+    npts = cfg.num_points
+    nch = -(-npts // chunk_points)
+    summ = np.zeros(npts, T.SUMMARY_DTYPE)
+    done = np.zeros(nch, np.bool_)
+    if os.path.exists(path):  # validated before any device work
+        z = np.load(path, allow_pickle=False)
+        if str(z["fingerprint"]) != fp or int(z["chunk_points"]) != chunk_points:
+            raise ValueError(f"checkpoint {path} belongs to another sweep (config or chunking differs)")
+        summ = np.ascontiguousarray(z["summaries"]).view(T.SUMMARY_DTYPE).reshape(npts).copy()
+        done = z["done"].astype(np.bool_)
+    sw = Sweep(cfg)
+    try:
+        ran = 0
+        for c in range(nch):
+            if done[c]:
+                continue
+            if max_chunks is not None and ran >= max_chunks:
+                break
+            b, e = c * chunk_points, min(npts, (c + 1) * chunk_points)
+            sw.run(b, e, 1, device=device)
+            summ[b:e] = sw.summaries()
+            done[c] = True
+            ran += 1
+            tmp = path + ".tmp.npz"
+            np.savez(tmp, fingerprint=np.array(fp), chunk_points=np.array(chunk_points),
+                     summaries=summ.view(np.uint8), done=done)
+            os.replace(tmp, path)
+        return summ
+    finally:
+        sw.close()
+
+
 def shard_range(num_points: int, rank: int, world: int):
     """Points owned by `rank`: p = rank (mod world)."""
     return rank, num_points, world

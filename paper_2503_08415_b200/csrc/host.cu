@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges cost nothing unless a profiler injects itself
+
 #include "ts_internal.cuh"
 
 using namespace ts;
@@ -551,6 +553,14 @@ static bool helper_run(const tokensim_sweep *h, u64 n_run, int sm_count) {
   return n_run <= kHelperPointsPerSm * (u64)sm_count;
 }
 
+// NVTX range for the enqueue of one run and of each launch (names appear in nsys / ncu --nvtx)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int blocks_per_sm_limit) {
   Layout L{};
   const u64 n = h->n_slots();
@@ -696,6 +706,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
                                    void *d_workspace, size_t ws_bytes, void *cuda_stream) {
   if (!h) return TOKENSIM_E_INVALID;
   if (!range_ok(h, begin, end, stride)) return fail(h, TOKENSIM_E_RANGE, "run: bad point range");
+  NvtxRange nv_run("tokensim_sweep_run");
   int count = 0;
   cudaError_t e = cudaGetDeviceCount(&count);
   if (e != cudaSuccess || count == 0) {
@@ -928,18 +939,21 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   h->n_launches = 0;
   cudaEventRecord(h->ev[0], st);
   if (n_run > 0 && !trace_mode) {
+    NvtxRange nv("tokensim.workload_kernel");
     e = launch_workload(P, st);
     if (e != cudaSuccess) return cuda_fail(h, e, "workload_kernel");
     ++h->n_launches;
   }
   cudaEventRecord(h->ev[1], st);
   if (n_run > 0) {
+    NvtxRange nv("tokensim.sim_kernel");
     e = launch_sim(P, (int)h->cap, (int)L.wpb, (int)L.blocks, L.smem, st);
     if (e != cudaSuccess) return cuda_fail(h, e, "sim_kernel");
     ++h->n_launches;
   }
   cudaEventRecord(h->ev[2], st);
   if (n_run > 0) {
+    NvtxRange nv("tokensim.summary_kernel");
     e = launch_summary(P, st);
     if (e != cudaSuccess) return cuda_fail(h, e, "summary_kernel");
     ++h->n_launches;

@@ -138,3 +138,22 @@ def test_product_does_not_import_oracle():
             assert not re.search(r"^\s*(from|import)\s+paper_2503_08415_b200", src, re.M), f
             assert not re.search(r'#include\s*[<"].*tokensim', src), f
             assert "libtokensim" not in src, f
+
+
+def test_resume_checkpoint_refuses_another_sweep(T, tmp_path):
+    """sweep_resumable validates its checkpoint before any device work: a checkpoint written
+    for another config (or another chunking) is refused; the fingerprint is stable."""
+    import numpy as np
+    import paper_2503_08415_b200 as P
+    a, b = si.c2(), replace(si.c2(), policies=[replace(si.c2().policies[0], max_num_seqs=128)])
+    assert P.config_fingerprint(a) == P.config_fingerprint(si.c2())
+    assert P.config_fingerprint(a) != P.config_fingerprint(b)
+    path = str(tmp_path / "ck.npz")
+    np.savez(path, fingerprint=np.array(P.config_fingerprint(b)), chunk_points=np.array(16),
+             summaries=np.zeros(a.num_points * P.SUMMARY_DTYPE.itemsize, np.uint8), done=np.zeros(8, np.bool_))
+    with pytest.raises(ValueError, match="another sweep"):
+        P.sweep_resumable(a, path, chunk_points=16)
+    np.savez(path, fingerprint=np.array(P.config_fingerprint(a)), chunk_points=np.array(32),
+             summaries=np.zeros(a.num_points * P.SUMMARY_DTYPE.itemsize, np.uint8), done=np.zeros(4, np.bool_))
+    with pytest.raises(ValueError, match="another sweep"):
+        P.sweep_resumable(a, path, chunk_points=16)

@@ -529,6 +529,20 @@ def test_node_micro_configs(api):
         check_pd_points(sw, cfg, list(range(cfg.num_points)), iters=True)
 
 
+def test_sweep_resumable_equals_one_run(api, tmp_path):
+    """Point-granular checkpoint / resume: a C2 sweep interrupted after 3 chunks of 16 points and
+    resumed gives the bytes of one uninterrupted run."""
+    cfg = si.c2()
+    full = api.sweep(cfg)
+    path = str(tmp_path / "c2.npz")
+    part = api.sweep_resumable(cfg, path, chunk_points=16, max_chunks=3)
+    assert (part["n_requests"][:48] > 0).all() and (part["n_requests"][48:] == 0).all()
+    out = api.sweep_resumable(cfg, path, chunk_points=16)
+    assert out.tobytes() == full.tobytes()
+    again = api.sweep_resumable(cfg, path, chunk_points=16, max_chunks=0)  # nothing left to run
+    assert again.tobytes() == full.tobytes()
+
+
 def test_node_epoch_stress(api):
     """The node kernel's epoch horizons (sim_pdn.cuh) under adversarial arrivals: bursts of equal
     timestamps (the exact-dispatch prediction must stand aside), dense and sparse streams, tiny
