@@ -337,7 +337,12 @@ typedef struct {
   uint64_t cycles_ff, cycles_ff_failed, cycles_normal;  /* split of sm_cycles by path */
   uint64_t stretch_phase_cycles[8];  /* inside successful stretches: scan of R / cost + cut /
                                         block allocation / slot updates + finishes / digests /
-                                        memory trace / compaction / bookkeeping             */
+                                        memory trace / compaction / bookkeeping.  xP:yD node
+                                        points instead: epochs / scheduler-phase cycles (warp 0)
+                                        / warp 0's decode-phase cycles / the largest and the
+                                        summed decode-phase cycles over decode warps / warp 0's
+                                        horizon computations / its waits for the slowest decode
+                                        warp / 0 (the product build measures these too)     */
   uint64_t n_transfers, transfer_bytes;  /* PD_PAIR: P->D KV transfers started and their bytes */
   uint64_t normal_phase_cycles[8];  /* normal iterations: reservation+preemption / resume /
                                        admission / block allocation / cost / commit pass /
@@ -358,6 +363,8 @@ tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t poi
  *   TOKENSIM_WPB=n         simulating warps per CTA (1..4) of the independent-warp kernel
  *   TOKENSIM_BPS=n         at most n CTAs per SM
  *   TOKENSIM_HEADS=K       helper kernel: the K longest-estimated points get an SM each
+ *   TOKENSIM_NODE_TWO=0|1  xP:yD node kernel: one CTA per SM / the 168-register build, two
+ *                          per SM (default: two once there are more points than SMs)
  *   TOKENSIM_LPT_OLD=1     order the queue by span / T(1) (round 1) instead of the cost sketch
  *   TOKENSIM_LPT_HELPER=1|2  helper runs: order by the sketch's iterations / cost
  *   TOKENSIM_LPT_COSTS=path  order by per-point costs read from `path` (n_points doubles) */

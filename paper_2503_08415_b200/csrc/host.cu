@@ -743,7 +743,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   if (const char *ev = getenv("TOKENSIM_XS")) xs = atoi(ev) != 0;
   // (the node kernel's occupancy is asked for its CTA of pd_y warps)
   // node: the register-capped two-CTAs-per-SM build once there are more points than SMs
-  const bool node_two = h->pd_general && h->pd_y <= 6 && n_run > (u64)sms;
+  bool node_two = h->pd_general && h->pd_y <= 6 && n_run > (u64)sms;
+  if (const char *ev = getenv("TOKENSIM_NODE_TWO")) node_two = h->pd_general && h->pd_y <= 6 && atoi(ev) != 0;  // A/B
   e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general, !helper, xs), (int)h->cap,
                     h->pd_general ? (int)h->pd_y + (node_two ? 16 : 0) : (int)L0.wpb, per_warp * L0.wpb, h->nwords_max,
                     &occ);

@@ -75,6 +75,7 @@ struct PdnSmem {
   u32 *dscr;             // decode warp j's requester lists at dscr + j * (2 cap + 64)
   PdnPart *part;         // [y]
   PdnCtl *ctl;
+  CostK *kc;             // [2]: the prefill and decode profiles' cost constants
 };
 
 __host__ __device__ inline size_t pdn_dworker_bytes(u32 cap, u32 nw) {
@@ -97,6 +98,7 @@ __host__ __device__ inline size_t pdn_smem_per_warp(u32 cap, u32 nw, u32 x, u32 
   b += (size_t)y * sizeof(PdnPart);
   b = (b + 15) & ~(size_t)15;
   b += (sizeof(PdnCtl) + 15) & ~(size_t)15;
+  b += (2 * sizeof(CostK) + 15) & ~(size_t)15;
   return b;
 }
 
@@ -128,6 +130,8 @@ __device__ __forceinline__ PdnSmem carve_pdn(unsigned char *base, u32 cap, u32 n
   o += (size_t)y * sizeof(PdnPart);
   o = (o + 15) & ~(size_t)15;
   M.ctl = reinterpret_cast<PdnCtl *>(base + o);
+  o += (sizeof(PdnCtl) + 15) & ~(size_t)15;
+  M.kc = reinterpret_cast<CostK *>(base + o);
   return M;
 }
 
@@ -206,8 +210,16 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   const DevHP HPP = P.hp[(size_t)hwP * P.n_pol + cd.pol];
   const DevHP HPD = P.hp[(size_t)hwD * P.n_pol + cd.pol];
   const DevPol PL = P.pol[cd.pol];
-  const CostK KP = make_costk(P.M, P.MF, P.hw[hwP]);
-  const CostK KD = make_costk(P.M, P.MF, P.hw[hwD], P.link_mode, P.preload_buf);
+  const PdnSmem M = carve_pdn(smem, CAP, P.nwords_max, X, Y);
+  // the cost constants live in shared memory (read at each use: registers stay free for the
+  // chain's state -- the two-CTAs-per-SM build caps them at 168)
+  if (threadIdx.x == 0) {
+    M.kc[0] = make_costk(P.M, P.MF, P.hw[hwP]);
+    M.kc[1] = make_costk(P.M, P.MF, P.hw[hwD], P.link_mode, P.preload_buf);
+  }
+  __syncthreads();
+  const CostK &KP = M.kc[0];
+  const CostK &KD = M.kc[1];
   const u32 g = P.group_of_point_mode ? 0u : cd.rate * P.n_seeds + cd.seed;
   const u32 n = P.n_req;
   const i64 *A = P.arrival + (size_t)g * n;
@@ -227,7 +239,6 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   const i64 INF = INT64_MAX;
   const long long clk0 = clock64();
   const u32 gwarp = blockIdx.x * Y + wib;  // this warp's logs
-  const PdnSmem M = carve_pdn(smem, CAP, P.nwords_max, X, Y);
   PdnCtl *ctl = M.ctl;
   u32 *itcur = &ctl->itcur;
   // per-CTA global scratch
