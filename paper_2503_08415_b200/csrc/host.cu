@@ -749,7 +749,12 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
                     h->pd_general ? (int)h->pd_y + (node_two ? 16 : 0) : (int)L0.wpb, per_warp * L0.wpb, h->nwords_max,
                     &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
-  if (occ < 1) return fail(h, TOKENSIM_E_NOMEM, "run: simulation kernel does not fit on an SM");
+  if (occ < 1)
+    return fail(h, TOKENSIM_E_NOMEM,
+                "run: simulation kernel does not fit on an SM (" + std::to_string(per_warp) +
+                    " B of shared memory per point" +
+                    (h->pd_general ? std::string(", an xP:yD node keeps every decode worker's slots on chip: fewer decode "
+                                                 "workers or max_num_seqs <= 256") : std::string()) + ")");
   const Layout L = make_layout(h, n_run, sms, occ);
   char *ws = static_cast<char *>(d_workspace);
   if (!ws) {

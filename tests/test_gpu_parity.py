@@ -543,6 +543,25 @@ def test_sweep_resumable_equals_one_run(api, tmp_path):
     assert again.tobytes() == full.tobytes()
 
 
+def test_node_large_batch_cap(api):
+    """A node whose policy allows 512 running requests (the 1024-slot kernel build): 1P:2D runs
+    and matches the oracle; 1P:6D needs more shared memory per point than an SM has and is
+    refused loudly at create instead of running anything else."""
+    from paper_2503_08415_b200 import TokensimError
+    rng = np.random.default_rng(77)
+    cfg = _micro_pd(rng)
+    while cfg.workload.num_requests < 30:
+        cfg = _micro_pd(rng)
+    cfg = replace(cfg, policies=[replace(cfg.policies[0], max_num_seqs=512)])
+    ok = replace(cfg, options=replace(cfg.options, pd_prefill=1, pd_decode=2, dispatch=si.LEAST_OUTSTANDING))
+    sw = run_gpu(api, ok)
+    check_pd_points(sw, ok, list(range(ok.num_points)), iters=True)
+    big = replace(cfg, options=replace(cfg.options, pd_prefill=1, pd_decode=6))
+    with pytest.raises(TokensimError) as ei:  # refused at create (validation), before any launch
+        run_gpu(api, big)
+    assert "shared memory per point" in str(ei.value)
+
+
 def test_node_epoch_stress(api):
     """The node kernel's epoch horizons (sim_pdn.cuh) under adversarial arrivals: bursts of equal
     timestamps (the exact-dispatch prediction must stand aside), dense and sparse streams, tiny
