@@ -552,6 +552,7 @@ __device__ __forceinline__ i64 scan_incl_i64(i64 x) {
 #include "sim_pd.cuh"
 #include "sim_pdn.cuh"
 
+// per simulated point: a warp's worth, or a whole node CTA's
 inline size_t sim_smem_per_warp_impl(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_y) {
   if (node_x) return pdn_smem_per_warp((u32)cap, nwords_max, node_x, node_y);
   return smem_per_warp_bytes((u32)cap, nwords_max) + (pd ? smem_pd_extra((u32)cap, nwords_max) : 0);
@@ -2384,9 +2385,10 @@ static __device__ void helper_loop(const SweepParams &P, volatile HelperChan *ch
   }
 }
 
-// V: 0 = lean unified (MIXED), 1 = full unified, 2 = 1P:1D pair, 3 = xP:yD node, 4 = the lean
-// one with compact helpers (sim_base_c.cu; sweeps that run several warps per SM).  One kernel
-// per variant: its registers and instruction footprint are those of the code it can run.
+// V: 0 = lean unified (MIXED), 1 = full unified, 2 = 1P:1D pair, 4 = the lean one with compact
+// helpers (sim_base_c.cu; sweeps that run several warps per SM), 5 = lean with the helper warp
+// and no extended stretches (the xP:yD node, variant 3, is sim_node_kernel: one CTA per point).
+// One kernel per variant: its registers and instruction footprint are those of the code it can run.
 template <int CAP, int V, bool P2>
 __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -2500,8 +2502,8 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   }
 }
 
-// launch / occupancy helpers for one variant (instantiated by sim_base.cu, sim_full.cu,
-// sim_pair.cu, sim_node.cu)
+// launch / occupancy helpers for one variant (instantiated by sim_base.cu, sim_base_n.cu,
+// sim_base_c.cu, sim_full.cu, sim_pair.cu; the node's are in sim_node.cu)
 // V 0 with the helper warp: one simulating warp (wpb = 1) + the helper, and the hand-over
 // counters after the warp's shared memory
 template <int V>

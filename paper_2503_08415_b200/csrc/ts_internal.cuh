@@ -118,7 +118,7 @@ struct SweepParams {
   u32 *pd_ring;        // P/D: per-warp ring of P block ids [warp][pd_ring_len]
   u64 pd_ring_len;
   unsigned char *pd_fifo;  // P/D: per-warp pending/transfer FIFO [warp][n_req] x 32 B
-  unsigned char *pdn_scratch;  // NEXT-1 node: per-warp FIFOs, queues, holders, P block lists
+  unsigned char *pdn_scratch;  // NEXT-1 node: per-CTA FIFOs, queues, holders, P block lists
   u64 pdn_bytes_per_warp;
   u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
   u32 node_two, node_pad;  // node kernel: the register-capped build, two CTAs per SM (sim_node.cu)
@@ -164,7 +164,8 @@ __host__ __device__ inline Coords decode_point(u64 point, u32 n_pol, u32 n_rates
 
 // launchers (sweep.cu)
 cudaError_t launch_workload(const SweepParams &p, cudaStream_t st);
-// kernel variants: 0 lean unified, 1 full unified, 2 1P:1D pair, 3 xP:yD node
+// kernel variants: 0 lean unified (helper warp + extended stretches), 1 full unified, 2 1P:1D pair,
+// 3 xP:yD node (sim_node_kernel), 4 lean with compact helpers, 5 lean with the helper warp only
 cudaError_t launch_sim_base(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                             cudaStream_t st);
 cudaError_t launch_sim_full(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
@@ -210,7 +211,7 @@ cudaError_t launch_quantiles(const SweepParams &p, u64 j, u32 metric, const u32 
                              double *d_out, u64 *d_keys, cudaStream_t st);
 constexpr u32 kSummarySmemKeys = 12288;  // keys held in shared memory by summary_kernel
 size_t sim_smem_per_warp(int cap, u32 nwords_max, bool pd, u32 node_x, u32 node_y);
-// NEXT-1 node, per-warp global scratch: decode FIFOs [y][n] x 32 B, prefill queues and holder
+// NEXT-1 node, global scratch per CTA (one point): decode FIFOs [y][n] x 32 B, prefill queues and holder
 // lists [x][n] x 4 B each, in-flight batches [x][cap] x 4 B, transfer ends [n] x 8 B, prefill
 // block lists [n][bt_len] x 4 B (sim_pdn.cuh)
 inline size_t pdn_global_per_warp(u64 n, u32 cap, u32 btl, u32 x, u32 y) {
@@ -219,7 +220,7 @@ inline size_t pdn_global_per_warp(u64 n, u32 cap, u32 btl, u32 x, u32 y) {
 cudaError_t sim_occupancy_base(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_full(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_pair(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
-// (node: warps_per_block = pd_y, + 16 for the two-CTAs-per-SM build)
+// (node: warps_per_block = pd_y (the CTA's warps), + 16 for the two-CTAs-per-SM build)
 cudaError_t sim_occupancy_node(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_base_c(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_base_n(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
