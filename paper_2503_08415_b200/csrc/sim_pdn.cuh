@@ -351,7 +351,16 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
   i64 last_fin = 0, tfin_w = 0;
   // warp 0 only: the scheduler's state
   u32 arr = 0, n_done_c = 0;
-  i64 ta_next = n > 0 ? A[0] : INT64_MAX;  // A[arr], kept in a register (the loads leave the chain)
+  // A[arr], A[arr + 1] and PR[arr] kept in registers (their loads leave the chain)
+  i64 ta_next = n > 0 ? A[0] : INT64_MAX;
+  i64 ta_next2 = n > 1 ? A[1] : INT64_MAX;
+  u32 pr_next = n > 0 ? PR[0] : 0u;
+  auto advance_arr = [&]() {
+    ++arr;
+    ta_next = ta_next2;
+    ta_next2 = arr + 1 < n ? A[arr + 1] : INT64_MAX;
+    pr_next = arr < n ? PR[arr] : 0u;
+  };
   u64 rrP = 0, rrD = 0, nrej_tot = 0;
   const bool ff_on = P.ff_enable != 0;
   const bool BINNED = P.trace_mode == TOKENSIM_TRACE_BINNED;
@@ -457,7 +466,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           // ta + T(prompt): the decode phase runs to that dispatch, which the scheduler phase
           // then processes -- one epoch per request instead of two.
           if (ta != INF && tdk > ta && tq > ta && P.dispatch != TOKENSIM_DISPATCH_LEAST_MEMORY &&
-              (arr + 1 >= n || A[arr + 1] != ta)) {
+              ta_next2 != ta) {
             u32 pi;
             if (P.dispatch == TOKENSIM_DISPATCH_ROUND_ROBIN) {
               pi = (u32)(rrP % X);
@@ -467,13 +476,13 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
               pi = warp_argmin64((i64)v, lane < X);
             }
             const PScal &p = M.ps[pi];
-            const u32 pp = PR[arr];
+            const u32 pp = pr_next;
             const u32 need = B.cdiv(pp);
             if (p.qhead == p.qtail && p.nb == 0 && (u64)need <= HPP.cap_fresh && mns >= 1u && pp <= mbt &&
                 (i64)p.nfree - (i64)need >= wm) {
               const i64 T1 = iter_time_ns(KP, pp, (u64)pp * (pp + 1) / 2, 1, 0, 0, 0);
               h1 = ta + T1;
-              const i64 h1n = arr + 1 < n ? sat_add(A[arr + 1], Tlb) : INF;  // the next arrival
+              const i64 h1n = sat_add(ta_next2, Tlb);  // the next arrival (INF: none)
               h1 = h1n < h1 ? h1n : h1;
             }
           }
@@ -1202,8 +1211,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           if (p.idle && ta < p.t) p.t = ta;
         }
         __syncwarp();
-        ++arr;
-        ta_next = arr < n ? A[arr] : INF;
+        advance_arr();
         continue;
       }
       // ================================================================ P_i boundary
@@ -1434,8 +1442,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
             if (p.idle && td < p.t) p.t = td;
           }
           __syncwarp();
-          ++arr;
-          ta_next = arr < n ? A[arr] : INF;
+          advance_arr();
           continue;
         }
         break;
