@@ -383,7 +383,8 @@ def run_ours(args):
                        "step": "workload_kernel + sim_kernel + summary_kernel" + (" + NCCL all-gather" if world > 1 else "")},
             "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": alu_gops, "unit": "Gop/s",
                          "frac": achieved_gops / alu_gops, "traffic": traffic,
-                         "kernel": "sim_kernel", "kernel_ms": statistics.mean(sim_ms),
+                         "kernel": ("sim_node_kernel" if cfg.options.topology == si.PD_PAIR and (cfg.options.pd_prefill + cfg.options.pd_decode > 2 or cfg.options.node_loop) else "sim_kernel"),
+                         "kernel_ms": statistics.mean(sim_ms),
                          "per_unit": f"{ALG_OPS_PER_UNIT} lane-ops per request-iteration (SURVEY §8(d))",
                          "peak_source": alu_src,
                          "hbm_line": {"bytes_per_unit": HBM_BYTES_PER_UNIT, "achieved_gbs": hbm_ach,

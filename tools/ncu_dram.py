@@ -23,7 +23,7 @@ os.makedirs(out, exist_ok=True)
 rep = existing[:-len(".ncu-rep")] if existing else os.path.join(out, f"sim_{cfg}")
 ROUND = os.environ.get("NCU_ROUND", "round 2")
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "-k", "regex:sim_kernel",
+cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "-k", "regex:sim_(node_)?kernel",
        "-c", "1", "-f", "-o", rep, sys.executable, os.path.join(root, "tools", "prof_run.py"), "--config", cfg]
 # the product library (prof_run.py would otherwise pick the profiling build)
 env = dict(os.environ, TOKENSIM_LIB=os.environ.get("TOKENSIM_LIB") or
@@ -51,7 +51,7 @@ for k in hdr:
         stalls[k[len("smsp__pcsamp_warps_issue_stalled_"):]] = f(k)
 tot = sum(v for v in stalls.values() if v) or 1.0
 summary = {
-    "source": f"ncu --set full --clock-control none --import-source on -k regex:sim_kernel -c 1 "
+    "source": f"ncu --set full --clock-control none --import-source on -k regex:sim_(node_)?kernel -c 1 "
               f"(tools/prof_run.py --config {cfg}), B200, {ROUND}",
     "kernel": d.get("Kernel Name"),
     "duration_ms": (f("gpu__time_duration.sum") or 0) / 1e6,  # base unit: ns
