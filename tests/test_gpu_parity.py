@@ -4,6 +4,7 @@ Bar (BASELINE.json north_star): schedules, batch compositions, preemptions, bloc
 per-request token counts bit-exact (digests + records + iteration traces); fp64
 latencies/quantiles within 1e-9 relative (expected equal: both sides evaluate the same
 fp64 expressions in the same order without FMA)."""
+import os
 from dataclasses import replace
 
 import numpy as np
@@ -762,3 +763,33 @@ def test_edge_shapes(api):
         m = replace(m, policies=[replace(m.policies[0], block_size=bs, max_num_seqs=mns)],
                     hws=[replace(m.hws[0], kv_blocks_override=int(rng.integers(-(-512 // bs), -(-512 // bs) + 60)))])
         check_points(run_gpu(api, m), m, [0], records=True, iters=True)
+
+
+# ------------------------------------------------------------------ multi-GPU path on one GPU
+def test_run_distributed_nccl_world_one(api, tmp_path):
+    """The NCCL path of run_distributed (device summaries, all_gather_into_tensor over NCCL,
+    import into the handle) under torchrun with one rank on cuda:0 gives the bytes of the
+    plain single-process sweep.  (World sizes > 1 need more GPUs; the host logic of W = 2 and 3
+    is covered with gloo in tests/test_distributed.py.)"""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "dist.npy"
+    script = tmp_path / "dist_run.py"
+    script.write_text(
+        "import sys, numpy as np, torch, torch.distributed as dist\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import sweep_inputs as si, paper_2503_08415_b200 as P\n"
+        "torch.cuda.set_device(0)\n"
+        "dist.init_process_group('nccl', device_id=torch.device('cuda', 0))\n"
+        "sw, allv = P.run_distributed(si.c2())\n"
+        f"np.save({str(out)!r}, np.asarray(allv.cpu()) if hasattr(allv, 'cpu') else allv)\n"
+        "assert dist.get_backend() == 'nccl'\n"
+        "dist.destroy_process_group()\n")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+                        "--master-addr", "127.0.0.1", "--master-port", "29613", str(script)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.load(out)
+    ref = api.sweep(si.c2())
+    assert got.view(np.uint8).tobytes()[:ref.nbytes] == ref.tobytes()
