@@ -15,7 +15,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("sim_full.cu", "sim_node.cu", "sim_pair.cu", "sim_base.cu", "sim_base_c.cu", "sim_base_n.cu", "workload.cu",
+SOURCES = [os.path.join(CSRC, f) for f in ("sim_full.cu", "sim_full_h.cu", "sim_node.cu", "sim_pair.cu", "sim_base.cu", "sim_base_c.cu", "sim_base_n.cu", "workload.cu",
                                            "metrics.cu", "host.cu")]
 HEADERS = [os.path.join(CSRC, f) for f in ("ts_internal.cuh", "dev_common.cuh", "sim_core.cuh", "sim_pd.cuh",
                                            "sim_pdn.cuh")] + [os.path.join(ROOT, "include", "tokensim.h")]

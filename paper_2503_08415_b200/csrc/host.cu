@@ -547,10 +547,13 @@ static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate, double *
 // issue rate, then sets the kernel time: DESIGN.md §7).  TOKENSIM_HELPER=0/1 overrides (A/B).
 constexpr u64 kHelperPointsPerSm = 4;
 static bool helper_run(const tokensim_sweep *h, u64 n_run, int sm_count) {
-  if (h->full || h->opt.topology == TOKENSIM_PD_PAIR) return false;
+  // (the full kernel gets the helper too, except with the preload link: its swap-in pipeline
+  // uses the block-event log as scratch, which the helper warp consumes)
+  if (h->opt.topology == TOKENSIM_PD_PAIR || (h->full && h->opt.link_mode == TOKENSIM_LINK_PRELOAD)) return false;
   if (!helper_fits(h->smem_per_warp(), h->nwords_max)) return false;
   if (const char *e = getenv("TOKENSIM_HELPER")) return atoi(e) != 0;
-  return n_run <= kHelperPointsPerSm * (u64)sm_count;
+  // full kernel: at most 2 points per SM (c7, 256 points: 95 -> 79 ms; c8, 384: 17.1 -> 19.6)
+  return n_run <= (h->full ? 2u : kHelperPointsPerSm) * (u64)sm_count;
 }
 
 // NVTX range for the enqueue of one run and of each launch (names appear in nsys / ncu --nvtx)

@@ -785,7 +785,7 @@ static __device__ __noinline__ bool replay_block_events(const uint4 *evr, u32 &e
 template <int CAP, bool FULL, bool P2>
 __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S, u32 *bt,
                                  volatile HelperChan *ch = nullptr) {
-  constexpr bool HELP = TS_HELPER_WARP && !FULL;
+  constexpr bool HELP = TS_HELPER_WARP;  // V 0 / 5 (lean) and V 6 (full) are built with the helper warp
   // Extended stretches (carried stretch state, up to 64 iterations per stretch) only in the
   // latency-bound helper-warp kernel: they shorten a lone point's chain, but at 8 warps per SM
   // the larger hot code costs more in instruction fetch than it saves (DESIGN.md §8 A/B log).
@@ -2393,7 +2393,7 @@ template <int CAP, int V, bool P2>
 __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const u32 lane = lane_id(), wib = threadIdx.x >> 5;
-  constexpr bool HELPK = (V == 0 || V == 5) && TS_HELPER_WARP;  // one simulating warp + its helper per CTA
+  constexpr bool HELPK = (V == 0 || V == 5 || V == 6) && TS_HELPER_WARP;  // one simulating warp + its helper per CTA
   constexpr bool pd = V == 2;  // (the xP:yD node has a kernel of its own: sim_node_kernel, sim_pdn.cuh)
   const size_t base = smem_per_warp_bytes(CAP, P.nwords_max);
   const size_t per_warp = base + (pd ? smem_pd_extra(CAP, P.nwords_max) : 0);
@@ -2493,7 +2493,7 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
       if (lane == 0) ch->state = 1u;
     }
     if constexpr (V == 2) simulate_pd<CAP, P2>(P, j, S, smem_raw + wib * per_warp + base, bt);
-    else simulate_unified<CAP, V == 1, P2>(P, j, S, bt, ch);  // V 4: the lean one built with TS_COMPACT
+    else simulate_unified<CAP, V == 1 || V == 6, P2>(P, j, S, bt, ch);  // V 4: the lean one built with TS_COMPACT
   }
   if constexpr (HELPK) {
     __threadfence_block();
@@ -2507,16 +2507,16 @@ __global__ void __launch_bounds__(128, 2) sim_kernel(SweepParams P) {
 // V 0 with the helper warp: one simulating warp (wpb = 1) + the helper, and the hand-over
 // counters after the warp's shared memory
 template <int V>
-static __host__ __forceinline__ int sim_threads(int wpb) { return ((V == 0 || V == 5) && TS_HELPER_WARP) ? 64 : wpb * 32; }
+static __host__ __forceinline__ int sim_threads(int wpb) { return ((V == 0 || V == 5 || V == 6) && TS_HELPER_WARP) ? 64 : wpb * 32; }
 // the helper's area: hand-over counters, its replayed bitmap (nwords_max words), 256 extraction slots
 static_assert(sizeof(HelperChan) <= kHelperChanBytes, "helper area (ts_internal.cuh)");
 template <int V>
 static __host__ __forceinline__ size_t sim_smem(size_t smem, u32 nwords_max) {
-  return ((V == 0 || V == 5) && TS_HELPER_WARP) ? helper_cta_smem(smem, nwords_max) : smem;
+  return ((V == 0 || V == 5 || V == 6) && TS_HELPER_WARP) ? helper_cta_smem(smem, nwords_max) : smem;
 }
 template <int CAP, int V, bool P2>
 static cudaError_t launch_sim_t(const SweepParams &p, int wpb, int blocks, size_t smem, cudaStream_t st) {
-  if ((V == 0 || V == 5) && TS_HELPER_WARP && wpb != 1) return cudaErrorInvalidValue;
+  if ((V == 0 || V == 5 || V == 6) && TS_HELPER_WARP && wpb != 1) return cudaErrorInvalidValue;
   smem = sim_smem<V>(smem, p.nwords_max);
   cudaError_t e = cudaFuncSetAttribute(sim_kernel<CAP, V, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

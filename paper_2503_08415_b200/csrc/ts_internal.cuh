@@ -165,11 +165,14 @@ __host__ __device__ inline Coords decode_point(u64 point, u32 n_pol, u32 n_rates
 // launchers (sweep.cu)
 cudaError_t launch_workload(const SweepParams &p, cudaStream_t st);
 // kernel variants: 0 lean unified (helper warp + extended stretches), 1 full unified, 2 1P:1D pair,
-// 3 xP:yD node (sim_node_kernel), 4 lean with compact helpers, 5 lean with the helper warp only
+// 3 xP:yD node (sim_node_kernel), 4 lean with compact helpers, 5 lean with the helper warp only,
+// 6 full with the helper warp
 cudaError_t launch_sim_base(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                             cudaStream_t st);
 cudaError_t launch_sim_full(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                             cudaStream_t st);
+cudaError_t launch_sim_full_h(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
+                              cudaStream_t st);
 cudaError_t launch_sim_pair(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                             cudaStream_t st);
 cudaError_t launch_sim_node(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
@@ -191,7 +194,7 @@ inline size_t helper_cta_smem(size_t per_warp, u32 nwords_max) {
 inline bool helper_fits(size_t per_warp, u32 nwords_max) { return helper_cta_smem(per_warp, nwords_max) <= 227 * 1024; }
 // xs: the helper kernel with extended stretches (variant 0) rather than without (variant 5)
 inline int sim_variant(bool full, bool pd, bool pd_general, bool multi_warp = false, bool xs = true) {
-  return !full ? (multi_warp ? 4 : xs ? 0 : 5) : !pd ? 1 : pd_general ? 3 : 2;
+  return !full ? (multi_warp ? 4 : xs ? 0 : 5) : !pd ? (multi_warp ? 1 : 6) : pd_general ? 3 : 2;
 }
 inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block, int blocks, size_t smem,
                               cudaStream_t st) {
@@ -202,6 +205,7 @@ inline cudaError_t launch_sim(const SweepParams &p, int cap, int warps_per_block
     case 5: return launch_sim_base_n(p, cap, warps_per_block, blocks, smem, st);
     case 4: return launch_sim_base_c(p, cap, warps_per_block, blocks, smem, st);
     case 1: return launch_sim_full(p, cap, warps_per_block, blocks, smem, st);
+    case 6: return launch_sim_full_h(p, cap, warps_per_block, blocks, smem, st);
     case 2: return launch_sim_pair(p, cap, warps_per_block, blocks, smem, st);
     default: return launch_sim_node(p, cap, warps_per_block, blocks, smem, st);
   }
@@ -219,6 +223,7 @@ inline size_t pdn_global_per_warp(u64 n, u32 cap, u32 btl, u32 x, u32 y) {
 }
 cudaError_t sim_occupancy_base(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_full(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
+cudaError_t sim_occupancy_full_h(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_pair(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 // (node: warps_per_block = pd_y (the CTA's warps), + 16 for the two-CTAs-per-SM build)
 cudaError_t sim_occupancy_node(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
@@ -229,6 +234,7 @@ inline cudaError_t sim_occupancy(int variant, int cap, int warps_per_block, size
   switch (variant) {
     case 0: return sim_occupancy_base(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
     case 1: return sim_occupancy_full(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
+    case 6: return sim_occupancy_full_h(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
     case 2: return sim_occupancy_pair(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
     case 4: return sim_occupancy_base_c(cap, warps_per_block, smem, nwords_max, blocks_per_sm);
     case 5: return sim_occupancy_base_n(cap, warps_per_block, smem, nwords_max, blocks_per_sm);

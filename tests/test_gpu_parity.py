@@ -128,6 +128,36 @@ def test_kernel_variants_byte_identical(api, monkeypatch):
             assert sw.records(p).tobytes() == ref.records(p).tobytes(), (name, p)
 
 
+def test_full_kernel_helper_variant_byte_identical(api, monkeypatch):
+    """The full kernel with (variant 6) and without (variant 1) the helper warp gives identical
+    bytes -- summaries, records, iteration records and memory traces -- on multi-round
+    conversations with the memory cache (c7-shaped, small) and on prefill-first / chunked
+    iterations under memory pressure, FULL and BINNED traces, SWAP and RECOMPUTE."""
+    pols = [si.Policy(preempt=si.SWAP, iteration_mode=si.PREFILL_FIRST),
+            si.Policy(preempt=si.RECOMPUTE, iteration_mode=si.CHUNKED, max_batched_tokens=512)]
+    cfgs = [
+        replace(si.c7(), workload=replace(si.c7().workload, num_requests=300, rates=[0.5, 4.0], seeds=[0, 1]),
+                options=replace(si.c7().options, iteration_trace_cap=1 << 16)),
+        si.SweepConfig("pf-chunked", si.LLAMA2_13B, [si.Hw(mem_capacity=30 * 10 ** 9), si.A100], pols,
+                       si.Workload(300, [4.0, 16.0], [0, 1]),
+                       si.Options(trace_mode=si.FULL, iteration_trace_cap=1 << 16)),
+    ]
+    for cfg in cfgs:
+        runs = {}
+        for name, v in (("v6", "1"), ("v1", "0")):
+            monkeypatch.setenv("TOKENSIM_HELPER", v)
+            sw = run_gpu(api, cfg)
+            runs[name] = (sw, sw.run_info()["helper_mode"])
+        monkeypatch.delenv("TOKENSIM_HELPER", raising=False)
+        assert runs["v6"][1] != 0 and runs["v1"][1] == 0
+        a, b = runs["v6"][0], runs["v1"][0]
+        assert a.summaries().tobytes() == b.summaries().tobytes(), cfg.name
+        for p in range(cfg.num_points):
+            assert a.records(p).tobytes() == b.records(p).tobytes(), (cfg.name, p)
+            assert a.iteration_trace(p).tobytes() == b.iteration_trace(p).tobytes(), (cfg.name, p)
+            assert a.mem_trace(p).tobytes() == b.mem_trace(p).tobytes(), (cfg.name, p)
+
+
 def test_head_reservation_is_byte_identical(api, monkeypatch):
     """TOKENSIM_HEADS=K (the K longest points each get an SM; the other CTAs there leave): every
     queue position is claimed exactly once, so results are byte-identical to the default run."""
