@@ -38,7 +38,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t arrival, prompt, output, rec, stats, trace, itrec, summ, bt, order, queue, sched, scratch, ring, fifo, pdn,
       pdn_per_warp,
-      mr_conv, mr_base, mr_nr, mr_ntot, mr_a0, mr_p0, mr_o0, mr, mr_per_warp, evlog, itlog,
+      mr_conv, mr_base, mr_nr, mr_ntot, mr_a0, mr_p0, mr_o0, mr, mr_per_warp, evlog, itlog, pipe, pipe_stride,
       total;
   u64 n_run;
   u32 warps_total, wpb, blocks;
@@ -547,9 +547,7 @@ static double lpt_cost(const tokensim_sweep *h, u32 hwpol, double rate, double *
 // issue rate, then sets the kernel time: DESIGN.md §7).  TOKENSIM_HELPER=0/1 overrides (A/B).
 constexpr u64 kHelperPointsPerSm = 4;
 static bool helper_run(const tokensim_sweep *h, u64 n_run, int sm_count) {
-  // (the full kernel gets the helper too, except with the preload link: its swap-in pipeline
-  // uses the block-event log as scratch, which the helper warp consumes)
-  if (h->opt.topology == TOKENSIM_PD_PAIR || (h->full && h->opt.link_mode == TOKENSIM_LINK_PRELOAD)) return false;
+  if (h->opt.topology == TOKENSIM_PD_PAIR) return false;
   if (!helper_fits(h->smem_per_warp(), h->nwords_max)) return false;
   if (const char *e = getenv("TOKENSIM_HELPER")) return atoi(e) != 0;
   // full kernel: at most 2 points per SM (c7, 256 points: 95 -> 79 ms; c8, 384: 17.1 -> 19.6)
@@ -630,6 +628,9 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   const size_t log_warps = (size_t)L.warps_total * (h->pd_general ? h->pd_y : 1u);
   L.evlog = take(log_warps * 1024 * 16);
   L.itlog = take(log_warps * 256 * 64);
+  // preload pipeline scratch of the helper-warp full kernel (layers + 1 doubles per warp)
+  L.pipe_stride = h->opt.link_mode == TOKENSIM_LINK_PRELOAD ? ((size_t)h->model.num_layers + 1 + 31) & ~(size_t)31 : 0;
+  L.pipe = take(log_warps * L.pipe_stride * 8);
   L.total = o;
   return L;
 }
@@ -895,6 +896,8 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   }
   P.evlog = reinterpret_cast<uint4 *>(ws + L.evlog);
   P.itlog = reinterpret_cast<ulonglong2 *>(ws + L.itlog);
+  P.pipe = reinterpret_cast<double *>(ws + L.pipe);
+  P.pipe_stride = L.pipe_stride;
 
   // longest-estimated-first order (LPT): simulated span / per-iteration floor
   std::vector<u32> order(n_run + 1, 0);

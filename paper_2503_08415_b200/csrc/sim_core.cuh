@@ -1921,8 +1921,11 @@ __device__ void simulate_unified(const SweepParams &P, u64 j, const WarpSmem &S,
       if (CHK || CACHE) Kp = warp_sum64(kpp);
       if (CHK) Slm = __reduce_add_sync(FULLMASK, semit);
     }
-    if (K.preload && swap_in > 0) ev_flush(L);  // the event log doubles as the pipeline's scratch
-    const i64 T = iter_time_chunk_ns(K, Np, Ap, Kp, Slm, D, Cd, swap_out, swap_in, reinterpret_cast<double *>(L.ev),
+    // the preload pipeline's scratch: the block-event log (flushed first), or -- when the helper
+    // warp consumes that log -- a per-warp region of its own
+    double *pring = HELP ? P.pipe + (size_t)gwarp * P.pipe_stride : reinterpret_cast<double *>(L.ev);
+    if (!HELP && K.preload && swap_in > 0) ev_flush(L);
+    const i64 T = iter_time_chunk_ns(K, Np, Ap, Kp, Slm, D, Cd, swap_out, swap_in, pring,
                                      fetch_blocks);
     NPH(4);
     // 8. commit

@@ -2,8 +2,8 @@
 // conversations + memory cache) with a helper warp per CTA (variant 6), for sweeps with at most
 // ~4 points per SM, where each point's serial chain sets the time: block ids, digests and
 // traces move to the helper warp as in the lean helper kernel (sim_base.cu), with its extended
-// stretches (carried state, up to 64 iterations: c7 -8%, prefill-first / chunked neutral).  The
-// preload link keeps the plain full kernel (its pipeline uses the block-event log as scratch).
+// stretches (carried state, up to 64 iterations: c7 -8%, prefill-first / chunked neutral); the
+// preload link's pipeline gets a scratch region of its own (the block-event log is the helper's).
 #define TS_HELPER_WARP 1
 #define TS_XS 1
 #define TS_LOGS_BYREF 1

@@ -145,6 +145,8 @@ struct SweepParams {
   u64 mr_bytes_per_warp;
   uint4 *evlog;            // per-warp block-event log [warp][1024]
   ulonglong2 *itlog;       // per-warp iteration log [warp][256][4]
+  double *pipe;            // helper-warp full kernel: per-warp preload-pipeline scratch
+  u64 pipe_stride;          // doubles per warp (>= layers + 1)
 };
 
 // point -> grid coordinates (row-major)

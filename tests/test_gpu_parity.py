@@ -131,8 +131,9 @@ def test_kernel_variants_byte_identical(api, monkeypatch):
 def test_full_kernel_helper_variant_byte_identical(api, monkeypatch):
     """The full kernel with (variant 6) and without (variant 1) the helper warp gives identical
     bytes -- summaries, records, iteration records and memory traces -- on multi-round
-    conversations with the memory cache (c7-shaped, small) and on prefill-first / chunked
-    iterations under memory pressure, FULL and BINNED traces, SWAP and RECOMPUTE."""
+    conversations with the memory cache (c7-shaped, small), on prefill-first / chunked
+    iterations under memory pressure, FULL and BINNED traces, SWAP and RECOMPUTE, and on
+    SWAP-heavy points under the preload link (c9-shaped, small)."""
     pols = [si.Policy(preempt=si.SWAP, iteration_mode=si.PREFILL_FIRST),
             si.Policy(preempt=si.RECOMPUTE, iteration_mode=si.CHUNKED, max_batched_tokens=512)]
     cfgs = [
@@ -141,6 +142,8 @@ def test_full_kernel_helper_variant_byte_identical(api, monkeypatch):
         si.SweepConfig("pf-chunked", si.LLAMA2_13B, [si.Hw(mem_capacity=30 * 10 ** 9), si.A100], pols,
                        si.Workload(300, [4.0, 16.0], [0, 1]),
                        si.Options(trace_mode=si.FULL, iteration_trace_cap=1 << 16)),
+        replace(si.c9(), workload=replace(si.c9().workload, num_requests=400, rates=[0.5, 2.0], seeds=[0]),
+                options=replace(si.c9().options, iteration_trace_cap=1 << 16)),  # the preload link
     ]
     for cfg in cfgs:
         runs = {}
