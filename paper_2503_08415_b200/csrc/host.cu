@@ -837,7 +837,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.order = reinterpret_cast<const u32 *>(ws + L.order);
   P.queue = reinterpret_cast<u32 *>(ws + L.queue);
   P.sched = reinterpret_cast<u32 *>(ws + L.sched);
-  P.helper_mode = helper ? (xs ? 1u : 2u) : 0u;
+  P.helper_mode = helper ? ((xs || h->full) ? 1u : 2u) : 0u;  // (the full helper kernel always has them)
   P.rec = reinterpret_cast<tokensim_request_record *>(ws + L.rec);
   P.stats = reinterpret_cast<SimStats *>(ws + L.stats);
   P.trace = reinterpret_cast<tokensim_mem_sample *>(ws + L.trace);
