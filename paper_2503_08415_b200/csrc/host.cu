@@ -579,8 +579,15 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   if (const char *e = getenv("TOKENSIM_WPB")) wpb = (u32)std::max(1, std::min(4, atoi(e)));
   else if ((u64)n_run <= (u64)sm_count || helper_run(h, n_run, sm_count)) wpb = 1;
   if (h->pd_general) wpb = 1;  // the node kernel: one point per CTA of pd_y warps
+  // lean kernel without the helper, at most one wave of 8 warps per SM (4-8 points per SM): the
+  // longest chains set the time, and 6 warps per SM (3 x 2 CTAs) run them faster than 8 (the
+  // 2- and 4-GPU shards of C3 / C4: 222 -> 198 ms, 252 -> 237 ms)
+  const bool six = !getenv("TOKENSIM_WPB") && !getenv("TOKENSIM_BPS") && !h->full && !pd &&
+                   !helper_run(h, n_run, sm_count) && n_run > 4ull * (u64)sm_count && n_run <= 8ull * (u64)sm_count &&
+                   wpb >= 3;
+  if (six) wpb = 3;
   u32 bps = (u32)std::max<size_t>(1, (227 * 1024) / (per_warp * wpb));
-  bps = std::min<u32>(bps, 16);
+  bps = std::min<u32>(bps, six ? 2u : 16u);
   if (blocks_per_sm_limit > 0) bps = std::min<u32>(bps, (u32)blocks_per_sm_limit);
   if (const char *e = getenv("TOKENSIM_BPS")) bps = std::min<u32>(bps, (u32)std::max(1, atoi(e)));  // A/B experiments
   const u64 need_warps = std::max<u64>(1, n_run);
