@@ -736,9 +736,9 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   int occ = 0;
   const bool helper = L0.wpb == 1 && helper_run(h, n_run, sms);
   // extended stretches pay off while the chains have their SM nearly to themselves (<= 2 points
-  // per SM: C4 at 8 GPUs 122 -> 115 ms); beyond that their hot code costs more (C3 at 8 GPUs,
-  // ~4 per SM: 142 -> 162 ms).  TOKENSIM_XS=0/1 overrides (A/B).
-  bool xs = n_run <= 2ull * (u64)sms;
+  // per SM: C4 at 8 GPUs 122 -> 115 ms) or have long quiet stretches; otherwise their hot code
+  // costs more (C3 at 8 GPUs, ~4 per SM: 142 -> 162 ms).  TOKENSIM_XS=0/1 overrides (A/B).
+  bool xs = n_run <= 4ull * (u64)sms;
   if (xs && helper && n_run > 0 && !h->wl.multi_round && h->wl.len_dist != TOKENSIM_LEN_TRACE) {
     // ... and only for chains with long quiet stretches: the median point's expected iterations
     // between events >= 6 (C1 27: 0.83 -> 0.78 ms with them; C2 1.9: 7.51 -> 7.80 ms without)
@@ -749,7 +749,10 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
       lpt_cost(h, (u32)((size_t)c.hw * h->pol.size() + c.pol), h->rates[c.rate], &q[j]);
     }
     std::nth_element(q.begin(), q.begin() + n_run / 2, q.end());
-    xs = q[n_run / 2] >= 6.0;
+    // (2-4 points per SM: only for longer quiet stretches -- C4's 4-GPU shard, median 13.7:
+    // 160 -> 143 ms with them; C3's 8-GPU shard, median 9.6: 151 -> 160 ms)
+    xs = q[n_run / 2] >= (n_run <= 2ull * (u64)sms ? 6.0 : 12.0);
+    if (getenv("TOKENSIM_DEBUG_XS")) fprintf(stderr, "tokensim: median quiet %.2f, %.2f points per SM\n", q[n_run / 2], (double)n_run / sms);
   }
   if (const char *ev = getenv("TOKENSIM_XS")) xs = atoi(ev) != 0;
   // (the node kernel's occupancy is asked for its CTA of pd_y warps)
