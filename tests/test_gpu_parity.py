@@ -111,7 +111,8 @@ def test_kernel_variants_byte_identical(api, monkeypatch):
     runs = {}
     for name, env in (("auto", {}), ("v4", {"TOKENSIM_HELPER": "0"}), ("v0", {"TOKENSIM_XS": "1"}),
                       ("v5", {"TOKENSIM_XS": "0"}), ("v4-old-order", {"TOKENSIM_HELPER": "0", "TOKENSIM_LPT_OLD": "1"}),
-                      ("v4-wpb2", {"TOKENSIM_HELPER": "0", "TOKENSIM_WPB": "2", "TOKENSIM_BPS": "3"})):
+                      ("v4-wpb2", {"TOKENSIM_HELPER": "0", "TOKENSIM_WPB": "2", "TOKENSIM_BPS": "3"}),
+                      ("v4-six", {"TOKENSIM_HELPER": "0", "TOKENSIM_WPB": "3", "TOKENSIM_BPS": "2"})):
         for k in ("TOKENSIM_HELPER", "TOKENSIM_XS", "TOKENSIM_LPT_OLD", "TOKENSIM_WPB", "TOKENSIM_BPS"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
