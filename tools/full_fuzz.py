@@ -35,8 +35,7 @@ def main():
             cfg = replace(si.c7(), workload=replace(si.c7().workload, num_requests=int(rng.integers(20, 200)),
                                                     rates=[float(rng.choice([0.5, 2.0, 8.0]))], seeds=[int(it)],
                                                     think_mean_s=float(rng.choice([0.5, 5.0]))),
-                          policies=[si.Policy(preempt=str(rng.choice([si.SWAP, si.RECOMPUTE])),
-                                              )],
+                          policies=[si.Policy(preempt=str(rng.choice([si.SWAP, si.RECOMPUTE])))],
                           options=replace(si.c7().options, memory_cache=bool(rng.random() < 0.7),
                                           iteration_trace_cap=1 << 16, trace_mode=si.BINNED))
         else:
