@@ -1,12 +1,14 @@
 """Randomised parity sweep of the xP:yD node kernel against the oracle's sequential node loop
 (a longer run of tests/test_gpu_parity.py::test_node_epoch_stress's generator).
 
-    python tools/node_fuzz.py [--n 300] [--seed 7]
+    python tools/node_fuzz.py [--n 300] [--seed 7] [--pair]
 
 Every configuration: random x:y (x + y <= 8), dispatch policy, arrivals (sparse, dense, bursts of
 equal times), lengths, KV pool, block size, preemption mode, trace mode, fast-forward; all points
 compared byte for byte (summaries, records, every worker's trace, iteration records by
-(worker, k)).  Prints one line per mismatch and a final count.
+(worker, k)).  --pair: 1P:1D pairs through the pair kernel, which must also give the bytes of the
+same pairs run through the node kernel (options.node_loop).  Prints one line per mismatch and a
+final count.
 """
 import argparse
 import os
@@ -26,6 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=300)
     ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--pair", action="store_true")
     a = ap.parse_args()
     import paper_2503_08415_b200 as P
     from test_gpu_parity import _micro_pd, check_pd_points
@@ -41,19 +44,26 @@ def main():
         o = rng.integers(1, 64, len(base))
         w = replace(cfg.workload, num_requests=len(base), trace_arrival_ns=base.tolist(), trace_prompt=p.tolist(),
                     trace_output=o.tolist())
-        x = int(rng.integers(1, 5))
-        y = int(rng.integers(1, 9 - x))
+        x = 1 if a.pair else int(rng.integers(1, 5))
+        y = 1 if a.pair else int(rng.integers(1, 9 - x))
         d = str(rng.choice([si.ROUND_ROBIN, si.LEAST_OUTSTANDING, si.LEAST_MEMORY]))
         cfg = replace(cfg, workload=w, options=replace(cfg.options, pd_prefill=x, pd_decode=y, dispatch=d))
         sw = P.Sweep(cfg)
         sw.run()
         try:
             check_pd_points(sw, cfg, list(range(cfg.num_points)), iters=True)
+            if a.pair:
+                nl = P.Sweep(replace(cfg, options=replace(cfg.options, node_loop=True)))
+                nl.run()
+                assert nl.summaries().tobytes() == sw.summaries().tobytes(), "node loop summaries differ"
+                for q in range(cfg.num_points):
+                    assert nl.records(q).tobytes() == sw.records(q).tobytes(), f"node loop records differ ({q})"
+                nl.close()
         except AssertionError as e:
             bad += 1
             print(f"config {it}: x={x} y={y} {d} n={len(base)}: {str(e).splitlines()[0]}", flush=True)
         sw.close()
-    print(f"node_fuzz: {a.n} configurations, {bad} mismatching")
+    print(f"node_fuzz{' --pair' if a.pair else ''}: {a.n} configurations, {bad} mismatching")
     return 1 if bad else 0
 
 
