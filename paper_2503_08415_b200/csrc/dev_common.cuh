@@ -41,7 +41,16 @@ __device__ __forceinline__ u32 lanemask_lt() {
   asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
-__device__ __forceinline__ u32 scan_incl(u32 x) {
+// TS_COMPACT_SCAN (A/B): the warp scan and the 64-bit warp sum out of line as well
+#ifndef TS_COMPACT_SCAN
+#define TS_COMPACT_SCAN 0
+#endif
+#if TS_COMPACT_SCAN
+#define TS_SCANFN static __device__ __noinline__
+#else
+#define TS_SCANFN __device__ __forceinline__
+#endif
+TS_SCANFN u32 scan_incl(u32 x) {
   const u32 l = lane_id();
 #pragma unroll
   for (u32 o = 1; o < 32; o <<= 1) {
@@ -52,7 +61,7 @@ __device__ __forceinline__ u32 scan_incl(u32 x) {
 }
 // Exact wrapping 64-bit warp sum with three 32-bit REDUX ops: split into 21/21/22-bit
 // digits (each digit sum over 32 lanes stays below 2^27) and recombine mod 2^64.
-__device__ __forceinline__ u64 warp_sum64(u64 x) {
+TS_SCANFN u64 warp_sum64(u64 x) {
   const u32 a = __reduce_add_sync(FULLMASK, (u32)(x & 0x1FFFFFull));
   const u32 b = __reduce_add_sync(FULLMASK, (u32)((x >> 21) & 0x1FFFFFull));
   const u32 c = __reduce_add_sync(FULLMASK, (u32)(x >> 42));

@@ -539,7 +539,7 @@ __device__ __forceinline__ void it_put(Logs &L, u32 idx, u64 k, i64 ts, i64 T, u
   e[3] = make_ulonglong2(Sp | (D << 16) | (m << 32) | (nres << 48), nadm | (nfin << 16) | (nrej << 32));
 }
 
-__device__ __forceinline__ i64 scan_incl_i64(i64 x) {
+TS_SCANFN i64 scan_incl_i64(i64 x) {
   const u32 l = lane_id();
 #pragma unroll
   for (u32 o = 1; o < 32; o <<= 1) {

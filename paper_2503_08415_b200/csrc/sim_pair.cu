@@ -3,6 +3,7 @@
 // where instruction fetch binds (C5 every-8th-point 3542 -> 3449 ms).
 #define TS_LOGS_BYREF 1
 #define TS_COMPACT 1
+#define TS_COMPACT_SCAN 1  // warp scans / 64-bit sums out of line too: C5 -5% (C3's kernel: +10%)
 
 #include "sim_core.cuh"
 
