@@ -358,16 +358,18 @@ tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t poi
 /* Environment variables read by tokensim_sweep_run -- A/B experiments only; results never
  * depend on them (every kernel variant and queue order gives the same bytes), only the launch
  * choice and the order of the point queue do.  Unset = the measured defaults.
- *   TOKENSIM_HELPER=0|1    helper-warp kernel off / on regardless of points per SM
+ *   TOKENSIM_HELPER=0|1    helper-warp kernel (lean or full) off / on regardless of points per SM
  *   TOKENSIM_XS=0|1        helper kernel without / with extended stretches
- *   TOKENSIM_WPB=n         simulating warps per CTA (1..4) of the independent-warp kernel
+ *   TOKENSIM_WPB=n         simulating warps per CTA (1..4) of the independent-warp kernel (default 4,
+ *                          or 3 x 2 CTAs per SM for a lean run of 4-8 points per SM)
  *   TOKENSIM_BPS=n         at most n CTAs per SM
  *   TOKENSIM_HEADS=K       helper kernel: the K longest-estimated points get an SM each
  *   TOKENSIM_NODE_TWO=0|1  xP:yD node kernel: one CTA per SM / the 168-register build, two
  *                          per SM (default: two once there are more points than SMs)
  *   TOKENSIM_LPT_OLD=1     order the queue by span / T(1) (round 1) instead of the cost sketch
  *   TOKENSIM_LPT_HELPER=1|2  helper runs: order by the sketch's iterations / cost
- *   TOKENSIM_LPT_COSTS=path  order by per-point costs read from `path` (n_points doubles) */
+ *   TOKENSIM_LPT_COSTS=path  order by per-point costs read from `path` (n_points doubles)
+ *   TOKENSIM_DEBUG_XS=1    print the median point's quiet-stretch estimate (extended-stretch choice) */
 
 /* Message of the last failing call on h (NULL: the calling thread's last create error). */
 const char *tokensim_last_error(const tokensim_sweep *h);
