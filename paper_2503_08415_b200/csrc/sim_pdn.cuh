@@ -411,6 +411,856 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     return w;
   };
 
+  // one boundary of this warp's decode worker (the D_j boundary of the sequential loop) before
+  // the epoch horizon H; false on an internal error
+  DScal d;  // this warp's decode worker's scalars, in registers while a phase runs
+  auto d_step = [&](const i64 H) -> bool {
+    const u32 koff = koffD;
+    const i64 t = d.t;
+    // 1. finished transfers become runnable (the in-flight tail completes in FIFO order)
+    // (transfers on this worker's link end in pull order; slots are id-sorted, so find by id)
+    while (d.nX > 0 && d.xhead_end <= t) {
+      const u32 xid = fifo[d.fhead - d.nX].id;
+      #pragma unroll 1
+      for (u32 b0 = 0; b0 < d.nD; b0 += 32) {
+        const u32 jj = b0 + lane;
+        const u32 hit = __ballot_sync(FULLMASK, jj < d.nD && S.id[jj] == xid);
+        if (hit) {
+          if (lane == 0) stt[b0 + (u32)(__ffs(hit) - 1)] = ST_RUN;
+          break;
+        }
+      }
+      --d.nX;
+      ++d.nRun;
+      d.xhead_end = d.nX ? fifo[d.fhead - d.nX].xend : INF;
+    }
+    __syncwarp();
+    bool ff_done = false;
+    // ---------------------------------------------------------- D fast-forward (H3)
+    // Quiescent decode stretch: no transfer completes, nothing is pulled or resumed, nothing
+    // is preempted, and no dispatch (which reads this worker's state or feeds its FIFO) can
+    // happen before the stretch's iterations: every iteration starts before the epoch
+    // horizon H, which no dispatch precedes.
+    if (ff_on && d.nRun > 0 && d.rmin >= 2 && (d.nfree > d.ffw || d.k >= d.ffk)) {
+      const i64 cut = H - 1;  // iterations starting at or after the epoch horizon H are excluded
+      bool quiet = true, mem_check = false;
+      u32 need_h = 0;
+      const u32 nA0 = d.nD;  // all slots (states are checked)
+      if (d.nQ > 0) {
+        u32 qpos = 0;
+        #pragma unroll 1
+        for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+          const u32 jj = b0 + lane;
+          const u32 qb = __ballot_sync(FULLMASK, jj < nA0 && stt[jj] == ST_QUEUED);
+          if (qb) {
+            qpos = b0 + (u32)(__ffs(qb) - 1);
+            break;
+          }
+        }
+        u32 tokq;
+        if (SWAPM) {
+          const u32 c = S.ctx[qpos];
+          need_h = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
+          tokq = 1;
+        } else {
+          const u32 id = S.id[qpos];
+          tokq = PR[id] + (OU[id] - S.rem[qpos]);
+          need_h = B.cdiv(tokq);
+        }
+        if (!((u64)d.nRun + d.nX + 1 > mns || (u64)d.nRun + tokq > mbt)) {
+          mem_check = true;
+          if ((i64)d.nfree - (i64)d.nRun - (i64)need_h >= wm) quiet = false;
+        }
+      } else if (!STATICP && d.fhead < d.ftail) {
+        // a visible pending head (every FIFO entry is visible): blocked now => blocked later
+        need_h = B.cdiv(PR[fifo[d.fhead].id]);
+        if (!((u64)d.nRun + d.nX + 1 > mns)) {
+          mem_check = true;
+          if ((i64)d.nfree - (i64)d.nRun - (i64)need_h >= wm) quiet = false;
+        }
+      }
+      if (quiet) {
+        S.scratch[lane] = 0;
+        S.scratch[32 + lane] = 0;
+        __syncwarp();
+        u64 cdp0 = 0;
+        u32 rmn = 0xffffffffu;
+        #pragma unroll 1
+        for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+          const u32 jj = b0 + lane;
+          u32 key = 64u + lane;
+          if (jj < nA0 && stt[jj] == ST_RUN) {
+            const u32 c = S.ctx[jj];
+            cdp0 += c + 1;
+            rmn = min(rmn, S.rem[jj]);
+            const u32 r = B.mod(c);
+            const u32 j0 = r ? B.bs - r : 0u;
+            if (j0 < 32) key = j0;
+          }
+          const u32 peers = __match_any_sync(FULLMASK, key);
+          if (key < 32 && (peers & ltm) == 0u) {
+            S.scratch[key] += __popc(peers);
+            S.scratch[32 + key] = peers;
+          }
+          __syncwarp();
+        }
+        const u64 Cd0 = warp_sum64(cdp0);
+        const u32 rm = __reduce_min_sync(FULLMASK, rmn);
+        const u32 nj = S.scratch[B.bs >= 32 ? lane : B.mod(lane)];
+        const u32 Aj = scan_incl(nj);
+        const u64 Cdj = Cd0 + (u64)lane * d.nRun;
+        const i64 Tj = iter_time_ns(KD, 0, 0, 0, d.nRun, Cdj, 0);
+        const i64 tej = t + scan_incl_i64(Tj);
+        const i64 tsj = tej - Tj;
+        bool ok = ((u64)Aj <= d.nfree) && (Aj <= (u32)CAP) && (lane < rm);
+        if (lane > 0) {
+          if (P.horizon >= 0 && tsj >= P.horizon) ok = false;
+          if (tsj >= d.xhead_end || tsj > cut) ok = false;
+        }
+        if (mem_check) {
+          const u64 fr = d.nfree - (u64)__shfl_sync(FULLMASK, Aj, 0);
+          if (!((i64)fr - (i64)need_h < wm)) ok = false;
+        }
+        const u32 okm = __ballot_sync(FULLMASK, ok);
+        const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+        const u32 memcut = __ballot_sync(FULLMASK, !((u64)Aj <= d.nfree));
+        if (J < 2 && memcut && (u32)(__ffs(memcut) - 1) < 2) {
+          d.ffw = d.nfree;
+          d.ffk = d.k + 4;
+        }
+        if (J >= 2) {
+          const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
+          __syncwarp();
+          S.scratch[lane] = Aj - nj;  // bucket cursors
+          __syncwarp();
+          if (Ktot > 0) {
+            const u32 nrep = B.cdiv(32u);
+            #pragma unroll 1
+            for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+              const u32 jj = b0 + lane;
+              const bool run = jj < nA0 && stt[jj] == ST_RUN;
+              const u32 c = run ? S.ctx[jj] : 0u;
+              const u32 r = B.mod(c);
+              u32 jx = r ? B.bs - r : 0u;
+              #pragma unroll 1
+              for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
+                const bool v = run && jx < J;
+                const u32 key = v ? jx : 64u + lane;
+                const u32 peers = __match_any_sync(FULLMASK, key);
+                u32 base = 0;
+                if (v) base = S.scratch[jx];
+                __syncwarp();
+                if (v) {
+                  const u32 e = base + __popc(peers & ltm);
+                  S.req_cum[e] = e + 1;
+                  S.req_pt[e] = jj | (jx << 10) | (B.div(c + jx) << 15);
+                  if ((peers & ltm) == 0u) S.scratch[jx] = base + __popc(peers);
+                }
+                __syncwarp();
+              }
+            }
+            if (!alloc_ordered(S, Ktot, Ktot, btD, btl, d.k, koff, L, d.hint, nwD)) {
+              flags |= TOKENSIM_PT_INTERNAL_ERROR;
+              return false;
+            }
+          }
+          const u64 blk0 = totD - d.nfree;
+          d.nfree -= Ktot;
+          const u64 klast = d.k + J - 1;
+          const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
+          const i64 te0 = __shfl_sync(FULLMASK, tej, 0);
+          const bool lj = lane < J;
+          i64 tm1 = (lj && lane > 0) ? Tj : 0;
+  #pragma unroll
+          for (u32 o = 16; o; o >>= 1) {
+            const i64 y = __shfl_xor_sync(FULLMASK, tm1, o);
+            tm1 = y > tm1 ? y : tm1;
+          }
+          u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
+          #pragma unroll 1
+          for (u32 b0 = 0; b0 < nA0; b0 += 32) {
+            const u32 jj = b0 + lane;
+            bool fin = false;
+            if (jj < nA0 && stt[jj] == ST_RUN) {
+              const u32 r = S.rem[jj] - J;
+              S.rem[jj] = r;
+              S.ctx[jj] += J;
+              const i64 g0 = te0 - S.last[jj];
+              i64 mg = S.maxgap[jj];
+              mg = g0 > mg ? g0 : mg;
+              mg = tm1 > mg ? tm1 : mg;
+              S.maxgap[jj] = mg;
+              S.last[jj] = tend;
+              fin = r == 0;
+              if (fin)
+                write_record(rec + S.id[jj], S.ttft[jj], tend - S.arr[jj], mg, S.info[jj] >> 16,
+                             TOKENSIM_REQ_FINISHED, (u32)klast);
+              else
+                rmin_l = min(rmin_l, r);
+            }
+            u32 fm = __ballot_sync(FULLMASK, fin);
+            __syncwarp();
+            if (fm && first_fin == 0xffffffffu) first_fin = b0 + (u32)(__ffs(fm) - 1);
+            nfin += __popc(fm);
+            while (fm) {
+              const u32 l = (u32)(__ffs(fm) - 1);
+              fm &= fm - 1;
+              const u32 pos = b0 + l;
+              const u32 held = B.cdiv(S.ctx[pos]);
+              const u32 slot = SLOT(S.info[pos]);
+              free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], klast, koff, L, d.hint);
+              d.nfree += held;
+              if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
+            }
+          }
+          __syncwarp();
+          const u64 blkj = blk0 + Aj;
+          pdn_it_reserve(L, 32, itcur);
+          if (lj)
+            it_put(L, lane, (d.k + lane) | ((u64)wid << 40), tsj, Tj, 0, Cdj, blkj, 0, d.nRun, 0, 0, 0,
+                   lane == J - 1 ? nfin : 0u, 0);
+          L.nit += J;
+          d.bns += warp_sum64(lj ? blkj * (u64)Tj : 0ull);
+          trace_stretch(d.TA, fe, BINNED, FULLT, trcD, P.trace_cap, W, J, tsj, tej, blkj, flags);
+          const u64 blk_last = blk0 + Ktot;
+          d.peak = blk_last > d.peak ? blk_last : d.peak;
+          req_iters += (u64)d.nRun * J;
+          if (nfin) {
+            u32 out = first_fin;
+            #pragma unroll 1
+            for (u32 b0 = first_fin; b0 < d.nD; b0 += 32) {
+              const u32 jj = b0 + lane;
+              const bool valid = jj < d.nD;
+              u32 vid = 0, vctx = 0, vrem = 0, vinfo = 0, vst = 0;
+              i64 vl = 0, vm = 0, va = 0, vt = 0;
+              if (valid) {
+                vid = S.id[jj];
+                vctx = S.ctx[jj];
+                vrem = S.rem[jj];
+                vinfo = S.info[jj];
+                vl = S.last[jj];
+                vm = S.maxgap[jj];
+                va = S.arr[jj];
+                vt = S.ttft[jj];
+                vst = stt[jj];
+              }
+              const bool keep = valid && vrem != 0;
+              const u32 km = __ballot_sync(FULLMASK, keep);
+              __syncwarp();
+              if (keep) {
+                const u32 dd = out + __popc(km & ltm);
+                S.id[dd] = vid;
+                S.ctx[dd] = vctx;
+                S.rem[dd] = vrem;
+                S.info[dd] = vinfo;
+                S.last[dd] = vl;
+                S.maxgap[dd] = vm;
+                S.arr[dd] = va;
+                S.ttft[dd] = vt;
+                stt[dd] = vst;
+              }
+              __syncwarp();
+              out += __popc(km);
+            }
+            d.nRun -= nfin;
+            d.nD -= nfin;
+            done_w += nfin;
+            nfin_tot += nfin;
+            last_fin = tend > last_fin ? tend : last_fin;
+            tfin_w = __shfl_sync(FULLMASK, tsj, J - 1);
+          }
+          d.rmin = d.nRun ? __reduce_min_sync(FULLMASK, rmin_l) : 0u;
+          ff_iters += J;
+          ++ff_runs;
+          d.t = tend;
+          d.last = tend;
+          d.k += J;
+          d.idle = 0;
+          ff_done = true;
+        }
+      }
+      if (!ff_done) d.rmin = 0;
+    }
+    if (flags & TOKENSIM_PT_INTERNAL_ERROR) return false;
+    if (!ff_done) {
+      const u32 nA = d.nD;  // all slots, id-sorted (states are checked)
+      // 3. decode reservation: RUN slots needing a block -> requester list (ascending id)
+      u32 E = 0;
+      u64 cdp = 0, npp = 0, app = 0;
+      #pragma unroll 1
+      for (u32 b0 = 0; b0 < nA; b0 += 32) {
+        const u32 jj = b0 + lane;
+        const bool run = jj < nA && stt[jj] == ST_RUN;
+        const u32 c = run ? S.ctx[jj] : 1u;
+        const bool need = run && B.mod(c) == 0;
+        if (run) cdp += c + 1;
+        const u32 bal = __ballot_sync(FULLMASK, need);
+        if (need) {
+          const u32 e = E + __popc(bal & ltm);
+          S.req_cum[e] = e + 1;
+          S.req_pt[e] = jj | (B.div(c) << 15);
+        }
+        E += __popc(bal);
+      }
+      u32 m = 0;
+      u64 swap_out = 0;
+      if ((u64)E > d.nfree) {
+        // minimal m over the running slots, latest ids first (in-flight blocks are not preemptible)
+        u64 Sn = E, Hh = 0;
+        u32 pos = nA;
+        do {
+          do {
+            --pos;
+          } while (stt[pos] != ST_RUN);
+          ++m;
+          const u32 c = S.ctx[pos];
+          Sn -= (B.mod(c) == 0) ? 1 : 0;
+          Hh += B.cdiv(c);
+        } while (Sn > d.nfree + Hh && m < d.nRun);
+        u64 csub = 0;
+        u32 vpos = nA, done_v = 0;
+        while (done_v < m) {
+          do {
+            --vpos;
+          } while (stt[vpos] != ST_RUN);
+          const u32 c = S.ctx[vpos];
+          const u32 held = B.cdiv(c);
+          free_blocks(S.bitmap, btD + (size_t)SLOT(S.info[vpos]) * btl, held, S.id[vpos], d.k, koff, L, d.hint);
+          d.nfree += held;
+          csub += c + 1;
+          if (SWAPM) swap_out += (u64)held * HPD.block_bytes;
+          __syncwarp();
+          if (lane == 0) {
+            S.info[vpos] += 1u << 16;
+            if (!SWAPM) S.ctx[vpos] = 0;
+            stt[vpos] = ST_QUEUED;
+          }
+          __syncwarp();
+          ++done_v;
+        }
+        if (lane == 0) cdp -= csub;
+        E = (u32)Sn;
+        d.nRun -= m;
+        d.nQ += m;
+        npre += m;
+      }
+      u32 Kb = E;
+      d.nfree -= E;
+      u32 nres = 0, nadm = 0, nrecomp = 0;
+      u64 swap_in = 0, tokens = d.nRun;
+      if (m == 0) {
+        // 4. resume preempted requests in ascending id; |R| counts in-flight transfers too
+        if (d.nQ > 0) {
+          u64 cum_need = 0, cum_tok = 0;
+          u32 taken = 0;
+          #pragma unroll 1
+          for (u32 b0 = 0; b0 < nA; b0 += 32) {
+            const u32 jj = b0 + lane;
+            const bool q = jj < nA && stt[jj] == ST_QUEUED;
+            u32 need = 0, tok = 0, held0 = 0, c = 0;
+            if (q) {
+              if (SWAPM) {
+                c = S.ctx[jj];
+                need = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
+                tok = 1;
+                held0 = B.cdiv(c);
+              } else {
+                const u32 id = S.id[jj];
+                tok = PR[id] + (OU[id] - S.rem[jj]);
+                need = B.cdiv(tok);
+              }
+            }
+            const u32 qm = __ballot_sync(FULLMASK, q);
+            const u32 rq = __popc(qm & ltm);
+            const u32 cn = scan_incl(need), ct = scan_incl(tok);
+            const bool ok = q && ((u64)d.nRun + d.nX + taken + rq + 1 <= (u64)mns) &&
+                            (tokens + cum_tok + ct <= (u64)mbt) && ((i64)d.nfree - (i64)(cum_need + cn) >= wm);
+            const u32 failm = __ballot_sync(FULLMASK, q && !ok);
+            const u32 stopl = failm ? (u32)(__ffs(failm) - 1) : 32u;
+            const bool take = q && lane < stopl;
+            const u32 tm = __ballot_sync(FULLMASK, take);
+            const u32 cnt = __popc(tm);
+            if (take) {
+              S.req_cum[E + rq] = Kb + cn;
+              S.req_pt[E + rq] = jj;
+              if (SWAPM) {
+                stt[jj] = ST_RUN;
+                cdp += c + 1;
+              } else {
+                stt[jj] = ST_RUN_RECOMP;
+                S.ctx[jj] = tok;
+                npp += tok;
+                app += (u64)tok * (tok + 1) / 2;
+              }
+            }
+            const u64 sw = warp_sum64(take ? (u64)held0 : 0ull);
+            if (cnt) {
+              const u32 last = 31u - __clz(tm);
+              const u32 sn = __shfl_sync(FULLMASK, cn, last), stk = __shfl_sync(FULLMASK, ct, last);
+              cum_need += sn;
+              cum_tok += stk;
+              Kb += sn;
+              E += cnt;
+              nres += cnt;
+              taken += cnt;
+              if (SWAPM) swap_in += sw * HPD.block_bytes;
+              else nrecomp += cnt;
+            }
+            if (failm) break;
+          }
+          d.nfree -= cum_need;
+          tokens += cum_tok;
+          d.nRun += nres;
+          d.nQ -= nres;
+          __syncwarp();
+        }
+        // 5. pull pending requests FCFS and start their transfers on this worker's link
+        if (d.nQ == 0 && (!STATICP || (d.nRun == 0 && d.nX == 0))) {
+          while (d.fhead < d.ftail) {
+            const u32 idx = d.fhead + lane;
+            const bool valid = idx < d.ftail;
+            u32 id = 0, p = 0, o = 0, pw = 0;
+            i64 join = INF, a = 0;
+            if (valid) {
+              const FifoEnt e = fifo[idx];
+              id = e.id;
+              pw = e.seg;
+              join = e.join;
+            }
+            const bool vis = valid && join <= t;
+            if (vis) {
+              p = PR[id];
+              o = OU[id];
+              a = A[id];
+            }
+            const u32 need = B.cdiv(p);
+            const u32 cneed = scan_incl(vis ? need : 0u);
+            const bool ok = vis && ((u64)d.nRun + d.nX + lane + 1 <= (u64)mns) && ((i64)d.nfree - (i64)cneed >= wm);
+            const u32 okm = __ballot_sync(FULLMASK, ok);
+            const u32 cnt = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
+            if (cnt == 0) break;
+            const bool take = lane < cnt;
+            const u32 slot = alloc_btslots(S.btfree, CAP / 32, take, lane, cnt);
+            const i64 dur = take ? xfer_ns(p) : 0;
+            const i64 start0 = t > d.link_busy ? t : d.link_busy;
+            const i64 xend = start0 + scan_incl_i64(dur);
+            if (take) {
+              const u32 pos = d.nD + lane;
+              S.id[pos] = id;
+              S.ctx[pos] = p;
+              S.rem[pos] = o - 1;
+              S.info[pos] = slot;
+              S.last[pos] = join;  // the first token left its prefill worker at `join`
+              S.maxgap[pos] = 0;
+              S.arr[pos] = a;
+              S.ttft[pos] = join - a;
+              stt[pos] = ST_XFER;
+              S.req_cum[E + lane] = Kb + cneed;
+              S.req_pt[E + lane] = pos;
+              fifo[idx].xend = xend;
+              reqx[id] = xend;
+            }
+            __syncwarp();
+            // the holders' prefill workers: their blocks come back at xend (wake idle ones)
+            for (u32 l = 0; l < cnt; ++l) {
+              const u32 lpw = __shfl_sync(FULLMASK, pw, l);
+              const i64 lx = __shfl_sync(FULLMASK, xend, l);
+              if (lane == 0) {  // several decode warps may release to one prefill worker at once
+                PScal &ps = M.ps[lpw];
+                atomicMin(reinterpret_cast<long long *>(&ps.hmin), (long long)lx);
+                if (ps.idle) atomicMin(reinterpret_cast<long long *>(&ps.t), (long long)lx);
+              }
+            }
+            __syncwarp();
+            const u32 sneed = __shfl_sync(FULLMASK, cneed, cnt - 1);
+            const i64 x0 = __shfl_sync(FULLMASK, xend, 0);
+            d.link_busy = __shfl_sync(FULLMASK, xend, cnt - 1);
+            if (d.nX == 0) d.xhead_end = x0;
+            xbytes += warp_sum64(take ? (u64)p * P.M.kvb : 0ull);
+            d.nfree -= sneed;
+            Kb += sneed;
+            E += cnt;
+            d.nD += cnt;
+            d.nX += cnt;
+            d.fhead += cnt;
+            nadm += cnt;
+            n_xfer += cnt;
+            __syncwarp();
+            if (cnt < 32) break;
+          }
+        }
+      }
+      if (Kb > 0 && !alloc_ordered(S, E, Kb, btD, btl, d.k, koff, L, d.hint, nwD)) {
+        flags |= TOKENSIM_PT_INTERNAL_ERROR;
+        return false;
+      }
+      // pulled requests were appended in dispatch order, which with several prefill workers
+      // need not be id order: insert them into the id-sorted slots (victims are the latest
+      // arrivals, requesters go in id order -- reading A7).  In-flight slots cannot finish in
+      // this iteration, so doing it before the commit keeps positions stable for it.
+      for (u32 q = d.nD - nadm; q < d.nD; ++q) {
+        const u32 qid = S.id[q];
+        u32 p = 0;
+        #pragma unroll 1
+        for (u32 b0 = 0; b0 < q; b0 += 32) {
+          const u32 jj = b0 + lane;
+          p += __popc(__ballot_sync(FULLMASK, jj < q && S.id[jj] < qid));
+        }
+        if (p == q) continue;
+        const u32 vctx = S.ctx[q], vrem = S.rem[q], vinfo = S.info[q], vst = stt[q];
+        const i64 vl = S.last[q], vm = S.maxgap[q], va = S.arr[q], vt = S.ttft[q];
+        __syncwarp();
+        for (u32 c = q; c > p;) {  // shift [p, q) up by one, highest chunk first
+          const u32 lo = c > p + 32 ? c - 32 : p;
+          const u32 jj = lo + lane;
+          const bool v = jj < c;
+          u32 a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+          i64 b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+          if (v) {
+            a0 = S.id[jj];
+            a1 = S.ctx[jj];
+            a2 = S.rem[jj];
+            a3 = S.info[jj];
+            a4 = stt[jj];
+            b1 = S.last[jj];
+            b2 = S.maxgap[jj];
+            b3 = S.arr[jj];
+            b4 = S.ttft[jj];
+          }
+          __syncwarp();
+          if (v) {
+            S.id[jj + 1] = a0;
+            S.ctx[jj + 1] = a1;
+            S.rem[jj + 1] = a2;
+            S.info[jj + 1] = a3;
+            stt[jj + 1] = a4;
+            S.last[jj + 1] = b1;
+            S.maxgap[jj + 1] = b2;
+            S.arr[jj + 1] = b3;
+            S.ttft[jj + 1] = b4;
+          }
+          __syncwarp();
+          c = lo;
+        }
+        if (lane == 0) {
+          S.id[p] = qid;
+          S.ctx[p] = vctx;
+          S.rem[p] = vrem;
+          S.info[p] = vinfo;
+          stt[p] = vst;
+          S.last[p] = vl;
+          S.maxgap[p] = vm;
+          S.arr[p] = va;
+          S.ttft[p] = vt;
+        }
+        __syncwarp();
+      }
+      if (d.nRun == 0) {  // 6. nothing runnable: wake at the next transfer end (or a dispatch)
+        d.t = d.xhead_end;
+        d.idle = 1;
+      } else {
+        // 7. cost on the decode profile
+        const u32 Dn = d.nRun - nrecomp;
+        const u64 Cd = warp_sum64(cdp);
+        u64 Np = 0, Ap = 0;
+        if (nrecomp) {
+          Np = warp_sum64(npp);
+          Ap = warp_sum64(app);
+        }
+        if (KD.preload && swap_in > 0) ev_flush(L);  // the event log doubles as the pipeline's scratch
+        const i64 T = iter_time_chunk_ns(KD, Np, Ap, Np, nrecomp, Dn, Cd, swap_out, swap_in,
+                                         reinterpret_cast<double *>(L.ev));
+        const i64 te = t + T;
+        const u64 blocks = totD - d.nfree;
+        // 8. commit
+        u32 nfin = 0, first_fin = 0xffffffffu, rmin_d = 0xffffffffu;
+        const u32 nC = d.nD;  // pulls (now sorted in) may have moved running slots past nA
+        #pragma unroll 1
+        for (u32 b0 = 0; b0 < nC; b0 += 32) {
+          const u32 jj = b0 + lane;
+          bool fin = false;
+          if (jj < nC) {
+            const u32 st = stt[jj];
+            if (st == ST_RUN || st == ST_RUN_RECOMP) {
+              const u32 r = S.rem[jj] - 1;
+              S.rem[jj] = r;
+              if (st == ST_RUN) S.ctx[jj] += 1;
+              else stt[jj] = ST_RUN;
+              const i64 gap = te - S.last[jj];
+              if (gap > S.maxgap[jj]) S.maxgap[jj] = gap;
+              S.last[jj] = te;
+              fin = r == 0;
+              if (fin)
+                write_record(rec + S.id[jj], S.ttft[jj], te - S.arr[jj], S.maxgap[jj], S.info[jj] >> 16,
+                             TOKENSIM_REQ_FINISHED, (u32)d.k);
+              else
+                rmin_d = min(rmin_d, r);
+            }
+          }
+          u32 fm = __ballot_sync(FULLMASK, fin);
+          __syncwarp();
+          if (fm && first_fin == 0xffffffffu) first_fin = b0 + (u32)(__ffs(fm) - 1);
+          nfin += __popc(fm);
+          while (fm) {
+            const u32 l = (u32)(__ffs(fm) - 1);
+            fm &= fm - 1;
+            const u32 pos = b0 + l;
+            const u32 held = B.cdiv(S.ctx[pos]);
+            const u32 slot = SLOT(S.info[pos]);
+            free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], d.k, koff, L, d.hint);
+            d.nfree += held;
+            if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
+          }
+        }
+        __syncwarp();
+        req_iters += d.nRun;
+        if (nfin) {
+          u32 out = first_fin;
+          #pragma unroll 1
+          for (u32 b0 = first_fin; b0 < d.nD; b0 += 32) {
+            const u32 jj = b0 + lane;
+            const bool valid = jj < d.nD;
+            u32 vid = 0, vctx = 0, vrem = 0, vinfo = 0, vst = 0;
+            i64 vl = 0, vm = 0, va = 0, vt = 0;
+            if (valid) {
+              vid = S.id[jj];
+              vctx = S.ctx[jj];
+              vrem = S.rem[jj];
+              vinfo = S.info[jj];
+              vl = S.last[jj];
+              vm = S.maxgap[jj];
+              va = S.arr[jj];
+              vt = S.ttft[jj];
+              vst = stt[jj];
+            }
+            const bool keep = valid && vrem != 0;
+            const u32 km = __ballot_sync(FULLMASK, keep);
+            __syncwarp();
+            if (keep) {
+              const u32 dd = out + __popc(km & ltm);
+              S.id[dd] = vid;
+              S.ctx[dd] = vctx;
+              S.rem[dd] = vrem;
+              S.info[dd] = vinfo;
+              S.last[dd] = vl;
+              S.maxgap[dd] = vm;
+              S.arr[dd] = va;
+              S.ttft[dd] = vt;
+              stt[dd] = vst;
+            }
+            __syncwarp();
+            out += __popc(km);
+          }
+          d.nRun -= nfin;
+          d.nD -= nfin;
+          done_w += nfin;
+          nfin_tot += nfin;
+          last_fin = te > last_fin ? te : last_fin;
+          tfin_w = t;
+        }
+        d.rmin = __reduce_min_sync(FULLMASK, rmin_d);
+        if (d.nRun == 0) d.rmin = 0;
+        fold_iter(d.k, wid, t, T, nrecomp, Dn, Np, Cd, m, nres, nadm, 0, nfin, blocks);
+        trace_iter(d.TA, fe, BINNED, FULLT, trcD, P.trace_cap, W, t, te, blocks, flags);
+        d.peak = blocks > d.peak ? blocks : d.peak;
+        d.bns += blocks * (u64)T;
+        swo += swap_out;
+        swi += swap_in;
+        d.t = te;
+        d.last = te;
+        ++d.k;
+        d.idle = 0;
+      }
+    }
+    return true;
+  };
+  // one prefill boundary (P_i, i = psel) of the scheduler; false on an internal error
+  auto p_step = [&](const u32 psel) -> bool {
+    const u32 pi = psel;
+    const u32 koff = 2 * pi;
+    u32 *bmP = M.bmP + (size_t)pi * P.nwords_max;
+    SP.bitmap = bmP;
+    u32 *qP = qP0 + (size_t)pi * n;
+    u32 *hold = hold0 + (size_t)pi * n;
+    u32 *batch = batch0 + (size_t)pi * CAP;
+    tokensim_mem_sample *trcP = trc0 + (size_t)pi * P.trace_cap;
+    PScal p = M.ps[pi];
+    const i64 t = p.t;
+    // holders whose transfers ended give their blocks back (any order; ascending list order)
+    if (p.hmin <= t) {
+      u32 out = 0;
+      i64 hm = INF;
+      #pragma unroll 1
+      for (u32 b0 = 0; b0 < p.nhold; b0 += 32) {
+        const u32 x = b0 + lane;
+        const bool v = x < p.nhold;
+        const u32 id = v ? hold[x] : 0u;
+        const i64 xe = v ? reqx[id] : INF;
+        const bool fr = v && xe <= t;
+        const bool keep = v && !fr;
+        hm = (keep && xe < hm) ? xe : hm;
+        u32 fm = __ballot_sync(FULLMASK, fr);
+        while (fm) {
+          const u32 l = (u32)(__ffs(fm) - 1);
+          fm &= fm - 1;
+          const u32 lid = __shfl_sync(FULLMASK, id, l);
+          const u32 ln = B.cdiv(PR[lid]);
+          free_blocks(bmP, pblk + (size_t)lid * btl, ln, lid, p.k, koff, L, p.hint);
+          p.nfree += ln;
+        }
+        const u32 km = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) hold[out + __popc(km & ltm)] = id;
+        __syncwarp();
+        out += __popc(km);
+      }
+#pragma unroll
+      for (u32 s = 16; s; s >>= 1) {
+        const i64 y = __shfl_xor_sync(FULLMASK, hm, s);
+        hm = y < hm ? y : hm;
+      }
+      p.nhold = out;
+      p.hmin = hm;
+    }
+    // fresh FCFS admission from this worker's dispatch queue into a prefill batch
+    u32 nb = 0, E = 0, Kb = 0, nrej = 0;
+    u64 tokens = 0, npp = 0, app = 0;
+    while (p.qhead < p.qtail) {
+      const u32 qi = p.qhead + lane;
+      const bool valid = qi < p.qtail;
+      const u32 i = valid ? qP[qi] : 0u;
+      const u32 pp = valid ? PR[i] : 0u;
+      const u32 o = valid ? OU[i] : 0u;
+      const u32 need = B.cdiv(pp);
+      const bool rej = valid && (u64)need > HPP.cap_fresh;
+      const bool el = valid && !rej;
+      const u32 ce = scan_incl(el ? 1u : 0u);
+      const u32 cneed = scan_incl(el ? need : 0u);
+      const u32 cp = scan_incl(el ? pp : 0u);
+      const bool ok = el && ((u64)nb + ce <= (u64)mns) && (tokens + cp <= (u64)mbt) &&
+                      ((i64)p.nfree - (i64)cneed >= wm);
+      const u32 failm = __ballot_sync(FULLMASK, el && !ok);
+      const u32 nvalid = min(32u, p.qtail - p.qhead);
+      const u32 stop = failm ? (u32)(__ffs(failm) - 1) : nvalid;
+      const bool take = el && lane < stop;
+      const bool rj = rej && lane < stop;
+      const u32 takem = __ballot_sync(FULLMASK, take);
+      const u32 cnt = __popc(takem);
+      if (take) {
+        const u32 rank = __popc(takem & ltm);
+        const u32 pos = nb + rank;
+        M.pid[pos] = i;
+        M.ppl[pos] = pp;
+        M.pol[pos] = o;
+        M.req_cum[E + rank] = Kb + cneed;
+        M.req_pt[E + rank] = pos;
+        npp += pp;
+        app += (u64)pp * (pp + 1) / 2;
+      }
+      if (rj) reinterpret_cast<uint8_t *>(rec + i)[26] = (uint8_t)TOKENSIM_REQ_REJECTED;
+      const u32 nrj = __popc(__ballot_sync(FULLMASK, rj));
+      if (stop) {
+        const u32 sneed = __shfl_sync(FULLMASK, cneed, stop - 1);
+        const u32 sp = __shfl_sync(FULLMASK, cp, stop - 1);
+        p.nfree -= sneed;
+        Kb += sneed;
+        tokens += sp;
+      }
+      E += cnt;
+      nb += cnt;
+      nrej += nrj;
+      p.qhead += stop;
+      __syncwarp();
+      if (stop < nvalid) break;
+    }
+    nrej_tot += nrej;
+    n_done_c += nrej;
+    if (nb == 0) {  // idle: wait for a dispatch or for blocks to come back
+      p.t = p.hmin;
+      p.idle = 1;
+    } else {
+      if (!alloc_ordered(SP, E, Kb, btP, btl, p.k, koff, L, p.hint, nwP)) {
+        flags |= TOKENSIM_PT_INTERNAL_ERROR;
+        return false;
+      }
+      const u64 Np = warp_sum64(npp), Ap = warp_sum64(app);
+      const i64 T = iter_time_ns(KP, Np, Ap, nb, 0, 0, 0);
+      const i64 te = t + T;
+      const u64 blocksP = totP - p.nfree;
+      // commit: the first token; o == 1 finishes here, the rest become holders whose block
+      // lists move to the per-request table; the whole batch is dispatched onward at te
+      u32 nfin = 0;
+      #pragma unroll 1
+      for (u32 b0 = 0; b0 < nb; b0 += 32) {
+        const u32 pos = b0 + lane;
+        const bool v = pos < nb;
+        const u32 id = v ? M.pid[pos] : 0u, pp = v ? M.ppl[pos] : 0u, o = v ? M.pol[pos] : 0u;
+        const bool one = v && o == 1;
+        const bool hold_it = v && o > 1;
+        const u32 need = B.cdiv(pp);
+        if (v) batch[pos] = id;
+        if (one) {
+          const i64 a = A[id];
+          write_record(rec + id, te - a, te - a, 0, 0, TOKENSIM_REQ_FINISHED, (u32)p.k);
+        }
+        const u32 hm = __ballot_sync(FULLMASK, hold_it);
+        if (hold_it) {
+          hold[p.nhold + __popc(hm & ltm)] = id;
+          reqx[id] = INF;
+        }
+        u32 vm = __ballot_sync(FULLMASK, v);
+        while (vm) {
+          const u32 l = (u32)(__ffs(vm) - 1);
+          vm &= vm - 1;
+          const u32 lpos = b0 + l;
+          const u32 lneed = __shfl_sync(FULLMASK, need, l);
+          const u32 lid = __shfl_sync(FULLMASK, id, l);
+          const bool lone = __shfl_sync(FULLMASK, (u32)one, l) != 0u;
+          const u32 *tbl = btP + (size_t)lpos * btl;
+          if (lone) {
+            free_blocks(bmP, tbl, lneed, lid, p.k, koff, L, p.hint);
+            p.nfree += lneed;
+          } else {
+            #pragma unroll 1
+            for (u32 x = lane; x < lneed; x += 32) pblk[(size_t)lid * btl + x] = tbl[x];
+          }
+        }
+        p.nhold += __popc(hm);
+        nfin += __popc(__ballot_sync(FULLMASK, one));
+        __syncwarp();
+      }
+      n_done_c += nfin;
+      nfin_tot += nfin;
+      if (nfin) last_fin = te > last_fin ? te : last_fin;
+      fold_iter(p.k, pi, t, T, nb, 0, Np, 0, 0, 0, nb, nrej, nfin, blocksP);
+      trace_iter(p.TA, FEp[pi], BINNED, FULLT, trcP, P.trace_cap, W, t, te, blocksP, flags);
+      req_iters += nb;
+      p.nb = nb;
+      p.cur = 0;
+      p.tdisp = te;
+      p.t = te;
+      p.last = te;
+      ++p.k;
+      p.idle = 0;
+    }
+    __syncwarp();
+    if (lane == 0) M.ps[pi] = p;
+    __syncwarp();
+    return true;
+  };
+  // an arrival at ta: dispatched to a prefill worker (no batch completes before the horizon)
+  auto arrival_step = [&](const i64 ta) {
+    // an arrival: dispatched to a prefill worker (no batch completes before H)
+    const u32 pi = pick(false, ta);
+    if (lane == 0) {
+      PScal &p = M.ps[pi];
+      qP0[(size_t)pi * n + p.qtail] = arr;
+      p.qtail += 1;
+      if (p.idle && ta < p.t) p.t = ta;
+    }
+    __syncwarp();
+    advance_arr();
+  };
   i64 td_next = INF;  // warp 0: the next known end-of-prefill dispatch
   u64 n_epochs = 0, cyc_sched = 0, cyc_dec = 0, cyc_h = 0, cyc_wait = 0;  // profile (point_profile's phase words)
   while (true) {
@@ -508,666 +1358,9 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
     const long long c_d0 = clock64();
     // ============================================== decode phase: every D_j boundary before H
     {
-      DScal d = M.ds[dj];
-      const u32 koff = koffD;
-      while (d.t < H) {
-        const i64 t = d.t;
-        // 1. finished transfers become runnable (the in-flight tail completes in FIFO order)
-        // (transfers on this worker's link end in pull order; slots are id-sorted, so find by id)
-        while (d.nX > 0 && d.xhead_end <= t) {
-          const u32 xid = fifo[d.fhead - d.nX].id;
-          #pragma unroll 1
-          for (u32 b0 = 0; b0 < d.nD; b0 += 32) {
-            const u32 jj = b0 + lane;
-            const u32 hit = __ballot_sync(FULLMASK, jj < d.nD && S.id[jj] == xid);
-            if (hit) {
-              if (lane == 0) stt[b0 + (u32)(__ffs(hit) - 1)] = ST_RUN;
-              break;
-            }
-          }
-          --d.nX;
-          ++d.nRun;
-          d.xhead_end = d.nX ? fifo[d.fhead - d.nX].xend : INF;
-        }
-        __syncwarp();
-        bool ff_done = false;
-        // ---------------------------------------------------------- D fast-forward (H3)
-        // Quiescent decode stretch: no transfer completes, nothing is pulled or resumed, nothing
-        // is preempted, and no dispatch (which reads this worker's state or feeds its FIFO) can
-        // happen before the stretch's iterations: every iteration starts before the epoch
-        // horizon H, which no dispatch precedes.
-        if (ff_on && d.nRun > 0 && d.rmin >= 2 && (d.nfree > d.ffw || d.k >= d.ffk)) {
-          const i64 cut = H - 1;  // iterations starting at or after the epoch horizon H are excluded
-          bool quiet = true, mem_check = false;
-          u32 need_h = 0;
-          const u32 nA0 = d.nD;  // all slots (states are checked)
-          if (d.nQ > 0) {
-            u32 qpos = 0;
-            #pragma unroll 1
-            for (u32 b0 = 0; b0 < nA0; b0 += 32) {
-              const u32 jj = b0 + lane;
-              const u32 qb = __ballot_sync(FULLMASK, jj < nA0 && stt[jj] == ST_QUEUED);
-              if (qb) {
-                qpos = b0 + (u32)(__ffs(qb) - 1);
-                break;
-              }
-            }
-            u32 tokq;
-            if (SWAPM) {
-              const u32 c = S.ctx[qpos];
-              need_h = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
-              tokq = 1;
-            } else {
-              const u32 id = S.id[qpos];
-              tokq = PR[id] + (OU[id] - S.rem[qpos]);
-              need_h = B.cdiv(tokq);
-            }
-            if (!((u64)d.nRun + d.nX + 1 > mns || (u64)d.nRun + tokq > mbt)) {
-              mem_check = true;
-              if ((i64)d.nfree - (i64)d.nRun - (i64)need_h >= wm) quiet = false;
-            }
-          } else if (!STATICP && d.fhead < d.ftail) {
-            // a visible pending head (every FIFO entry is visible): blocked now => blocked later
-            need_h = B.cdiv(PR[fifo[d.fhead].id]);
-            if (!((u64)d.nRun + d.nX + 1 > mns)) {
-              mem_check = true;
-              if ((i64)d.nfree - (i64)d.nRun - (i64)need_h >= wm) quiet = false;
-            }
-          }
-          if (quiet) {
-            S.scratch[lane] = 0;
-            S.scratch[32 + lane] = 0;
-            __syncwarp();
-            u64 cdp0 = 0;
-            u32 rmn = 0xffffffffu;
-            #pragma unroll 1
-            for (u32 b0 = 0; b0 < nA0; b0 += 32) {
-              const u32 jj = b0 + lane;
-              u32 key = 64u + lane;
-              if (jj < nA0 && stt[jj] == ST_RUN) {
-                const u32 c = S.ctx[jj];
-                cdp0 += c + 1;
-                rmn = min(rmn, S.rem[jj]);
-                const u32 r = B.mod(c);
-                const u32 j0 = r ? B.bs - r : 0u;
-                if (j0 < 32) key = j0;
-              }
-              const u32 peers = __match_any_sync(FULLMASK, key);
-              if (key < 32 && (peers & ltm) == 0u) {
-                S.scratch[key] += __popc(peers);
-                S.scratch[32 + key] = peers;
-              }
-              __syncwarp();
-            }
-            const u64 Cd0 = warp_sum64(cdp0);
-            const u32 rm = __reduce_min_sync(FULLMASK, rmn);
-            const u32 nj = S.scratch[B.bs >= 32 ? lane : B.mod(lane)];
-            const u32 Aj = scan_incl(nj);
-            const u64 Cdj = Cd0 + (u64)lane * d.nRun;
-            const i64 Tj = iter_time_ns(KD, 0, 0, 0, d.nRun, Cdj, 0);
-            const i64 tej = t + scan_incl_i64(Tj);
-            const i64 tsj = tej - Tj;
-            bool ok = ((u64)Aj <= d.nfree) && (Aj <= (u32)CAP) && (lane < rm);
-            if (lane > 0) {
-              if (P.horizon >= 0 && tsj >= P.horizon) ok = false;
-              if (tsj >= d.xhead_end || tsj > cut) ok = false;
-            }
-            if (mem_check) {
-              const u64 fr = d.nfree - (u64)__shfl_sync(FULLMASK, Aj, 0);
-              if (!((i64)fr - (i64)need_h < wm)) ok = false;
-            }
-            const u32 okm = __ballot_sync(FULLMASK, ok);
-            const u32 J = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
-            const u32 memcut = __ballot_sync(FULLMASK, !((u64)Aj <= d.nfree));
-            if (J < 2 && memcut && (u32)(__ffs(memcut) - 1) < 2) {
-              d.ffw = d.nfree;
-              d.ffk = d.k + 4;
-            }
-            if (J >= 2) {
-              const u32 Ktot = __shfl_sync(FULLMASK, Aj, J - 1);
-              __syncwarp();
-              S.scratch[lane] = Aj - nj;  // bucket cursors
-              __syncwarp();
-              if (Ktot > 0) {
-                const u32 nrep = B.cdiv(32u);
-                #pragma unroll 1
-                for (u32 b0 = 0; b0 < nA0; b0 += 32) {
-                  const u32 jj = b0 + lane;
-                  const bool run = jj < nA0 && stt[jj] == ST_RUN;
-                  const u32 c = run ? S.ctx[jj] : 0u;
-                  const u32 r = B.mod(c);
-                  u32 jx = r ? B.bs - r : 0u;
-                  #pragma unroll 1
-                  for (u32 rep = 0; rep < nrep; ++rep, jx += B.bs) {
-                    const bool v = run && jx < J;
-                    const u32 key = v ? jx : 64u + lane;
-                    const u32 peers = __match_any_sync(FULLMASK, key);
-                    u32 base = 0;
-                    if (v) base = S.scratch[jx];
-                    __syncwarp();
-                    if (v) {
-                      const u32 e = base + __popc(peers & ltm);
-                      S.req_cum[e] = e + 1;
-                      S.req_pt[e] = jj | (jx << 10) | (B.div(c + jx) << 15);
-                      if ((peers & ltm) == 0u) S.scratch[jx] = base + __popc(peers);
-                    }
-                    __syncwarp();
-                  }
-                }
-                if (!alloc_ordered(S, Ktot, Ktot, btD, btl, d.k, koff, L, d.hint, nwD)) {
-                  flags |= TOKENSIM_PT_INTERNAL_ERROR;
-                  break;
-                }
-              }
-              const u64 blk0 = totD - d.nfree;
-              d.nfree -= Ktot;
-              const u64 klast = d.k + J - 1;
-              const i64 tend = __shfl_sync(FULLMASK, tej, J - 1);
-              const i64 te0 = __shfl_sync(FULLMASK, tej, 0);
-              const bool lj = lane < J;
-              i64 tm1 = (lj && lane > 0) ? Tj : 0;
-  #pragma unroll
-              for (u32 o = 16; o; o >>= 1) {
-                const i64 y = __shfl_xor_sync(FULLMASK, tm1, o);
-                tm1 = y > tm1 ? y : tm1;
-              }
-              u32 nfin = 0, first_fin = 0xffffffffu, rmin_l = 0xffffffffu;
-              #pragma unroll 1
-              for (u32 b0 = 0; b0 < nA0; b0 += 32) {
-                const u32 jj = b0 + lane;
-                bool fin = false;
-                if (jj < nA0 && stt[jj] == ST_RUN) {
-                  const u32 r = S.rem[jj] - J;
-                  S.rem[jj] = r;
-                  S.ctx[jj] += J;
-                  const i64 g0 = te0 - S.last[jj];
-                  i64 mg = S.maxgap[jj];
-                  mg = g0 > mg ? g0 : mg;
-                  mg = tm1 > mg ? tm1 : mg;
-                  S.maxgap[jj] = mg;
-                  S.last[jj] = tend;
-                  fin = r == 0;
-                  if (fin)
-                    write_record(rec + S.id[jj], S.ttft[jj], tend - S.arr[jj], mg, S.info[jj] >> 16,
-                                 TOKENSIM_REQ_FINISHED, (u32)klast);
-                  else
-                    rmin_l = min(rmin_l, r);
-                }
-                u32 fm = __ballot_sync(FULLMASK, fin);
-                __syncwarp();
-                if (fm && first_fin == 0xffffffffu) first_fin = b0 + (u32)(__ffs(fm) - 1);
-                nfin += __popc(fm);
-                while (fm) {
-                  const u32 l = (u32)(__ffs(fm) - 1);
-                  fm &= fm - 1;
-                  const u32 pos = b0 + l;
-                  const u32 held = B.cdiv(S.ctx[pos]);
-                  const u32 slot = SLOT(S.info[pos]);
-                  free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], klast, koff, L, d.hint);
-                  d.nfree += held;
-                  if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
-                }
-              }
-              __syncwarp();
-              const u64 blkj = blk0 + Aj;
-              pdn_it_reserve(L, 32, itcur);
-              if (lj)
-                it_put(L, lane, (d.k + lane) | ((u64)wid << 40), tsj, Tj, 0, Cdj, blkj, 0, d.nRun, 0, 0, 0,
-                       lane == J - 1 ? nfin : 0u, 0);
-              L.nit += J;
-              d.bns += warp_sum64(lj ? blkj * (u64)Tj : 0ull);
-              trace_stretch(d.TA, fe, BINNED, FULLT, trcD, P.trace_cap, W, J, tsj, tej, blkj, flags);
-              const u64 blk_last = blk0 + Ktot;
-              d.peak = blk_last > d.peak ? blk_last : d.peak;
-              req_iters += (u64)d.nRun * J;
-              if (nfin) {
-                u32 out = first_fin;
-                #pragma unroll 1
-                for (u32 b0 = first_fin; b0 < d.nD; b0 += 32) {
-                  const u32 jj = b0 + lane;
-                  const bool valid = jj < d.nD;
-                  u32 vid = 0, vctx = 0, vrem = 0, vinfo = 0, vst = 0;
-                  i64 vl = 0, vm = 0, va = 0, vt = 0;
-                  if (valid) {
-                    vid = S.id[jj];
-                    vctx = S.ctx[jj];
-                    vrem = S.rem[jj];
-                    vinfo = S.info[jj];
-                    vl = S.last[jj];
-                    vm = S.maxgap[jj];
-                    va = S.arr[jj];
-                    vt = S.ttft[jj];
-                    vst = stt[jj];
-                  }
-                  const bool keep = valid && vrem != 0;
-                  const u32 km = __ballot_sync(FULLMASK, keep);
-                  __syncwarp();
-                  if (keep) {
-                    const u32 dd = out + __popc(km & ltm);
-                    S.id[dd] = vid;
-                    S.ctx[dd] = vctx;
-                    S.rem[dd] = vrem;
-                    S.info[dd] = vinfo;
-                    S.last[dd] = vl;
-                    S.maxgap[dd] = vm;
-                    S.arr[dd] = va;
-                    S.ttft[dd] = vt;
-                    stt[dd] = vst;
-                  }
-                  __syncwarp();
-                  out += __popc(km);
-                }
-                d.nRun -= nfin;
-                d.nD -= nfin;
-                done_w += nfin;
-                nfin_tot += nfin;
-                last_fin = tend > last_fin ? tend : last_fin;
-                tfin_w = __shfl_sync(FULLMASK, tsj, J - 1);
-              }
-              d.rmin = d.nRun ? __reduce_min_sync(FULLMASK, rmin_l) : 0u;
-              ff_iters += J;
-              ++ff_runs;
-              d.t = tend;
-              d.last = tend;
-              d.k += J;
-              d.idle = 0;
-              ff_done = true;
-            }
-          }
-          if (!ff_done) d.rmin = 0;
-        }
-        if (flags & TOKENSIM_PT_INTERNAL_ERROR) break;
-        if (!ff_done) {
-          const u32 nA = d.nD;  // all slots, id-sorted (states are checked)
-          // 3. decode reservation: RUN slots needing a block -> requester list (ascending id)
-          u32 E = 0;
-          u64 cdp = 0, npp = 0, app = 0;
-          #pragma unroll 1
-          for (u32 b0 = 0; b0 < nA; b0 += 32) {
-            const u32 jj = b0 + lane;
-            const bool run = jj < nA && stt[jj] == ST_RUN;
-            const u32 c = run ? S.ctx[jj] : 1u;
-            const bool need = run && B.mod(c) == 0;
-            if (run) cdp += c + 1;
-            const u32 bal = __ballot_sync(FULLMASK, need);
-            if (need) {
-              const u32 e = E + __popc(bal & ltm);
-              S.req_cum[e] = e + 1;
-              S.req_pt[e] = jj | (B.div(c) << 15);
-            }
-            E += __popc(bal);
-          }
-          u32 m = 0;
-          u64 swap_out = 0;
-          if ((u64)E > d.nfree) {
-            // minimal m over the running slots, latest ids first (in-flight blocks are not preemptible)
-            u64 Sn = E, Hh = 0;
-            u32 pos = nA;
-            do {
-              do {
-                --pos;
-              } while (stt[pos] != ST_RUN);
-              ++m;
-              const u32 c = S.ctx[pos];
-              Sn -= (B.mod(c) == 0) ? 1 : 0;
-              Hh += B.cdiv(c);
-            } while (Sn > d.nfree + Hh && m < d.nRun);
-            u64 csub = 0;
-            u32 vpos = nA, done_v = 0;
-            while (done_v < m) {
-              do {
-                --vpos;
-              } while (stt[vpos] != ST_RUN);
-              const u32 c = S.ctx[vpos];
-              const u32 held = B.cdiv(c);
-              free_blocks(S.bitmap, btD + (size_t)SLOT(S.info[vpos]) * btl, held, S.id[vpos], d.k, koff, L, d.hint);
-              d.nfree += held;
-              csub += c + 1;
-              if (SWAPM) swap_out += (u64)held * HPD.block_bytes;
-              __syncwarp();
-              if (lane == 0) {
-                S.info[vpos] += 1u << 16;
-                if (!SWAPM) S.ctx[vpos] = 0;
-                stt[vpos] = ST_QUEUED;
-              }
-              __syncwarp();
-              ++done_v;
-            }
-            if (lane == 0) cdp -= csub;
-            E = (u32)Sn;
-            d.nRun -= m;
-            d.nQ += m;
-            npre += m;
-          }
-          u32 Kb = E;
-          d.nfree -= E;
-          u32 nres = 0, nadm = 0, nrecomp = 0;
-          u64 swap_in = 0, tokens = d.nRun;
-          if (m == 0) {
-            // 4. resume preempted requests in ascending id; |R| counts in-flight transfers too
-            if (d.nQ > 0) {
-              u64 cum_need = 0, cum_tok = 0;
-              u32 taken = 0;
-              #pragma unroll 1
-              for (u32 b0 = 0; b0 < nA; b0 += 32) {
-                const u32 jj = b0 + lane;
-                const bool q = jj < nA && stt[jj] == ST_QUEUED;
-                u32 need = 0, tok = 0, held0 = 0, c = 0;
-                if (q) {
-                  if (SWAPM) {
-                    c = S.ctx[jj];
-                    need = B.cdiv(c) + (B.mod(c) == 0 ? 1u : 0u);
-                    tok = 1;
-                    held0 = B.cdiv(c);
-                  } else {
-                    const u32 id = S.id[jj];
-                    tok = PR[id] + (OU[id] - S.rem[jj]);
-                    need = B.cdiv(tok);
-                  }
-                }
-                const u32 qm = __ballot_sync(FULLMASK, q);
-                const u32 rq = __popc(qm & ltm);
-                const u32 cn = scan_incl(need), ct = scan_incl(tok);
-                const bool ok = q && ((u64)d.nRun + d.nX + taken + rq + 1 <= (u64)mns) &&
-                                (tokens + cum_tok + ct <= (u64)mbt) && ((i64)d.nfree - (i64)(cum_need + cn) >= wm);
-                const u32 failm = __ballot_sync(FULLMASK, q && !ok);
-                const u32 stopl = failm ? (u32)(__ffs(failm) - 1) : 32u;
-                const bool take = q && lane < stopl;
-                const u32 tm = __ballot_sync(FULLMASK, take);
-                const u32 cnt = __popc(tm);
-                if (take) {
-                  S.req_cum[E + rq] = Kb + cn;
-                  S.req_pt[E + rq] = jj;
-                  if (SWAPM) {
-                    stt[jj] = ST_RUN;
-                    cdp += c + 1;
-                  } else {
-                    stt[jj] = ST_RUN_RECOMP;
-                    S.ctx[jj] = tok;
-                    npp += tok;
-                    app += (u64)tok * (tok + 1) / 2;
-                  }
-                }
-                const u64 sw = warp_sum64(take ? (u64)held0 : 0ull);
-                if (cnt) {
-                  const u32 last = 31u - __clz(tm);
-                  const u32 sn = __shfl_sync(FULLMASK, cn, last), stk = __shfl_sync(FULLMASK, ct, last);
-                  cum_need += sn;
-                  cum_tok += stk;
-                  Kb += sn;
-                  E += cnt;
-                  nres += cnt;
-                  taken += cnt;
-                  if (SWAPM) swap_in += sw * HPD.block_bytes;
-                  else nrecomp += cnt;
-                }
-                if (failm) break;
-              }
-              d.nfree -= cum_need;
-              tokens += cum_tok;
-              d.nRun += nres;
-              d.nQ -= nres;
-              __syncwarp();
-            }
-            // 5. pull pending requests FCFS and start their transfers on this worker's link
-            if (d.nQ == 0 && (!STATICP || (d.nRun == 0 && d.nX == 0))) {
-              while (d.fhead < d.ftail) {
-                const u32 idx = d.fhead + lane;
-                const bool valid = idx < d.ftail;
-                u32 id = 0, p = 0, o = 0, pw = 0;
-                i64 join = INF, a = 0;
-                if (valid) {
-                  const FifoEnt e = fifo[idx];
-                  id = e.id;
-                  pw = e.seg;
-                  join = e.join;
-                }
-                const bool vis = valid && join <= t;
-                if (vis) {
-                  p = PR[id];
-                  o = OU[id];
-                  a = A[id];
-                }
-                const u32 need = B.cdiv(p);
-                const u32 cneed = scan_incl(vis ? need : 0u);
-                const bool ok = vis && ((u64)d.nRun + d.nX + lane + 1 <= (u64)mns) && ((i64)d.nfree - (i64)cneed >= wm);
-                const u32 okm = __ballot_sync(FULLMASK, ok);
-                const u32 cnt = (~okm == 0u) ? 32u : (u32)(__ffs(~okm) - 1);
-                if (cnt == 0) break;
-                const bool take = lane < cnt;
-                const u32 slot = alloc_btslots(S.btfree, CAP / 32, take, lane, cnt);
-                const i64 dur = take ? xfer_ns(p) : 0;
-                const i64 start0 = t > d.link_busy ? t : d.link_busy;
-                const i64 xend = start0 + scan_incl_i64(dur);
-                if (take) {
-                  const u32 pos = d.nD + lane;
-                  S.id[pos] = id;
-                  S.ctx[pos] = p;
-                  S.rem[pos] = o - 1;
-                  S.info[pos] = slot;
-                  S.last[pos] = join;  // the first token left its prefill worker at `join`
-                  S.maxgap[pos] = 0;
-                  S.arr[pos] = a;
-                  S.ttft[pos] = join - a;
-                  stt[pos] = ST_XFER;
-                  S.req_cum[E + lane] = Kb + cneed;
-                  S.req_pt[E + lane] = pos;
-                  fifo[idx].xend = xend;
-                  reqx[id] = xend;
-                }
-                __syncwarp();
-                // the holders' prefill workers: their blocks come back at xend (wake idle ones)
-                for (u32 l = 0; l < cnt; ++l) {
-                  const u32 lpw = __shfl_sync(FULLMASK, pw, l);
-                  const i64 lx = __shfl_sync(FULLMASK, xend, l);
-                  if (lane == 0) {  // several decode warps may release to one prefill worker at once
-                    PScal &ps = M.ps[lpw];
-                    atomicMin(reinterpret_cast<long long *>(&ps.hmin), (long long)lx);
-                    if (ps.idle) atomicMin(reinterpret_cast<long long *>(&ps.t), (long long)lx);
-                  }
-                }
-                __syncwarp();
-                const u32 sneed = __shfl_sync(FULLMASK, cneed, cnt - 1);
-                const i64 x0 = __shfl_sync(FULLMASK, xend, 0);
-                d.link_busy = __shfl_sync(FULLMASK, xend, cnt - 1);
-                if (d.nX == 0) d.xhead_end = x0;
-                xbytes += warp_sum64(take ? (u64)p * P.M.kvb : 0ull);
-                d.nfree -= sneed;
-                Kb += sneed;
-                E += cnt;
-                d.nD += cnt;
-                d.nX += cnt;
-                d.fhead += cnt;
-                nadm += cnt;
-                n_xfer += cnt;
-                __syncwarp();
-                if (cnt < 32) break;
-              }
-            }
-          }
-          if (Kb > 0 && !alloc_ordered(S, E, Kb, btD, btl, d.k, koff, L, d.hint, nwD)) {
-            flags |= TOKENSIM_PT_INTERNAL_ERROR;
-            break;
-          }
-          // pulled requests were appended in dispatch order, which with several prefill workers
-          // need not be id order: insert them into the id-sorted slots (victims are the latest
-          // arrivals, requesters go in id order -- reading A7).  In-flight slots cannot finish in
-          // this iteration, so doing it before the commit keeps positions stable for it.
-          for (u32 q = d.nD - nadm; q < d.nD; ++q) {
-            const u32 qid = S.id[q];
-            u32 p = 0;
-            #pragma unroll 1
-            for (u32 b0 = 0; b0 < q; b0 += 32) {
-              const u32 jj = b0 + lane;
-              p += __popc(__ballot_sync(FULLMASK, jj < q && S.id[jj] < qid));
-            }
-            if (p == q) continue;
-            const u32 vctx = S.ctx[q], vrem = S.rem[q], vinfo = S.info[q], vst = stt[q];
-            const i64 vl = S.last[q], vm = S.maxgap[q], va = S.arr[q], vt = S.ttft[q];
-            __syncwarp();
-            for (u32 c = q; c > p;) {  // shift [p, q) up by one, highest chunk first
-              const u32 lo = c > p + 32 ? c - 32 : p;
-              const u32 jj = lo + lane;
-              const bool v = jj < c;
-              u32 a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
-              i64 b1 = 0, b2 = 0, b3 = 0, b4 = 0;
-              if (v) {
-                a0 = S.id[jj];
-                a1 = S.ctx[jj];
-                a2 = S.rem[jj];
-                a3 = S.info[jj];
-                a4 = stt[jj];
-                b1 = S.last[jj];
-                b2 = S.maxgap[jj];
-                b3 = S.arr[jj];
-                b4 = S.ttft[jj];
-              }
-              __syncwarp();
-              if (v) {
-                S.id[jj + 1] = a0;
-                S.ctx[jj + 1] = a1;
-                S.rem[jj + 1] = a2;
-                S.info[jj + 1] = a3;
-                stt[jj + 1] = a4;
-                S.last[jj + 1] = b1;
-                S.maxgap[jj + 1] = b2;
-                S.arr[jj + 1] = b3;
-                S.ttft[jj + 1] = b4;
-              }
-              __syncwarp();
-              c = lo;
-            }
-            if (lane == 0) {
-              S.id[p] = qid;
-              S.ctx[p] = vctx;
-              S.rem[p] = vrem;
-              S.info[p] = vinfo;
-              stt[p] = vst;
-              S.last[p] = vl;
-              S.maxgap[p] = vm;
-              S.arr[p] = va;
-              S.ttft[p] = vt;
-            }
-            __syncwarp();
-          }
-          if (d.nRun == 0) {  // 6. nothing runnable: wake at the next transfer end (or a dispatch)
-            d.t = d.xhead_end;
-            d.idle = 1;
-          } else {
-            // 7. cost on the decode profile
-            const u32 Dn = d.nRun - nrecomp;
-            const u64 Cd = warp_sum64(cdp);
-            u64 Np = 0, Ap = 0;
-            if (nrecomp) {
-              Np = warp_sum64(npp);
-              Ap = warp_sum64(app);
-            }
-            if (KD.preload && swap_in > 0) ev_flush(L);  // the event log doubles as the pipeline's scratch
-            const i64 T = iter_time_chunk_ns(KD, Np, Ap, Np, nrecomp, Dn, Cd, swap_out, swap_in,
-                                             reinterpret_cast<double *>(L.ev));
-            const i64 te = t + T;
-            const u64 blocks = totD - d.nfree;
-            // 8. commit
-            u32 nfin = 0, first_fin = 0xffffffffu, rmin_d = 0xffffffffu;
-            const u32 nC = d.nD;  // pulls (now sorted in) may have moved running slots past nA
-            #pragma unroll 1
-            for (u32 b0 = 0; b0 < nC; b0 += 32) {
-              const u32 jj = b0 + lane;
-              bool fin = false;
-              if (jj < nC) {
-                const u32 st = stt[jj];
-                if (st == ST_RUN || st == ST_RUN_RECOMP) {
-                  const u32 r = S.rem[jj] - 1;
-                  S.rem[jj] = r;
-                  if (st == ST_RUN) S.ctx[jj] += 1;
-                  else stt[jj] = ST_RUN;
-                  const i64 gap = te - S.last[jj];
-                  if (gap > S.maxgap[jj]) S.maxgap[jj] = gap;
-                  S.last[jj] = te;
-                  fin = r == 0;
-                  if (fin)
-                    write_record(rec + S.id[jj], S.ttft[jj], te - S.arr[jj], S.maxgap[jj], S.info[jj] >> 16,
-                                 TOKENSIM_REQ_FINISHED, (u32)d.k);
-                  else
-                    rmin_d = min(rmin_d, r);
-                }
-              }
-              u32 fm = __ballot_sync(FULLMASK, fin);
-              __syncwarp();
-              if (fm && first_fin == 0xffffffffu) first_fin = b0 + (u32)(__ffs(fm) - 1);
-              nfin += __popc(fm);
-              while (fm) {
-                const u32 l = (u32)(__ffs(fm) - 1);
-                fm &= fm - 1;
-                const u32 pos = b0 + l;
-                const u32 held = B.cdiv(S.ctx[pos]);
-                const u32 slot = SLOT(S.info[pos]);
-                free_blocks(S.bitmap, btD + (size_t)slot * btl, held, S.id[pos], d.k, koff, L, d.hint);
-                d.nfree += held;
-                if (lane == 0) atomicOr(&S.btfree[slot >> 5], 1u << (slot & 31u));
-              }
-            }
-            __syncwarp();
-            req_iters += d.nRun;
-            if (nfin) {
-              u32 out = first_fin;
-              #pragma unroll 1
-              for (u32 b0 = first_fin; b0 < d.nD; b0 += 32) {
-                const u32 jj = b0 + lane;
-                const bool valid = jj < d.nD;
-                u32 vid = 0, vctx = 0, vrem = 0, vinfo = 0, vst = 0;
-                i64 vl = 0, vm = 0, va = 0, vt = 0;
-                if (valid) {
-                  vid = S.id[jj];
-                  vctx = S.ctx[jj];
-                  vrem = S.rem[jj];
-                  vinfo = S.info[jj];
-                  vl = S.last[jj];
-                  vm = S.maxgap[jj];
-                  va = S.arr[jj];
-                  vt = S.ttft[jj];
-                  vst = stt[jj];
-                }
-                const bool keep = valid && vrem != 0;
-                const u32 km = __ballot_sync(FULLMASK, keep);
-                __syncwarp();
-                if (keep) {
-                  const u32 dd = out + __popc(km & ltm);
-                  S.id[dd] = vid;
-                  S.ctx[dd] = vctx;
-                  S.rem[dd] = vrem;
-                  S.info[dd] = vinfo;
-                  S.last[dd] = vl;
-                  S.maxgap[dd] = vm;
-                  S.arr[dd] = va;
-                  S.ttft[dd] = vt;
-                  stt[dd] = vst;
-                }
-                __syncwarp();
-                out += __popc(km);
-              }
-              d.nRun -= nfin;
-              d.nD -= nfin;
-              done_w += nfin;
-              nfin_tot += nfin;
-              last_fin = te > last_fin ? te : last_fin;
-              tfin_w = t;
-            }
-            d.rmin = __reduce_min_sync(FULLMASK, rmin_d);
-            if (d.nRun == 0) d.rmin = 0;
-            fold_iter(d.k, wid, t, T, nrecomp, Dn, Np, Cd, m, nres, nadm, 0, nfin, blocks);
-            trace_iter(d.TA, fe, BINNED, FULLT, trcD, P.trace_cap, W, t, te, blocks, flags);
-            d.peak = blocks > d.peak ? blocks : d.peak;
-            d.bns += blocks * (u64)T;
-            swo += swap_out;
-            swi += swap_in;
-            d.t = te;
-            d.last = te;
-            ++d.k;
-            d.idle = 0;
-          }
-        }
-      }
+      d = M.ds[dj];
+      while (d.t < H)
+        if (!d_step(H)) break;
       __syncwarp();
       if (lane == 0) {
         M.ds[dj] = d;
@@ -1202,189 +1395,10 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       if (ta >= H && tb >= H) break;
       if (n_done_c + dd == n && (ta < tb ? ta : tb) >= tD) break;
       if (ta <= tb) {
-        // an arrival: dispatched to a prefill worker (no batch completes before H)
-        const u32 pi = pick(false, ta);
-        if (lane == 0) {
-          PScal &p = M.ps[pi];
-          qP0[(size_t)pi * n + p.qtail] = arr;
-          p.qtail += 1;
-          if (p.idle && ta < p.t) p.t = ta;
-        }
-        __syncwarp();
-        advance_arr();
+        arrival_step(ta);
         continue;
       }
-      // ================================================================ P_i boundary
-      const u32 pi = psel;
-      const u32 koff = 2 * pi;
-      u32 *bmP = M.bmP + (size_t)pi * P.nwords_max;
-      SP.bitmap = bmP;
-      u32 *qP = qP0 + (size_t)pi * n;
-      u32 *hold = hold0 + (size_t)pi * n;
-      u32 *batch = batch0 + (size_t)pi * CAP;
-      tokensim_mem_sample *trcP = trc0 + (size_t)pi * P.trace_cap;
-      PScal p = M.ps[pi];
-      const i64 t = p.t;
-      // holders whose transfers ended give their blocks back (any order; ascending list order)
-      if (p.hmin <= t) {
-        u32 out = 0;
-        i64 hm = INF;
-        #pragma unroll 1
-        for (u32 b0 = 0; b0 < p.nhold; b0 += 32) {
-          const u32 x = b0 + lane;
-          const bool v = x < p.nhold;
-          const u32 id = v ? hold[x] : 0u;
-          const i64 xe = v ? reqx[id] : INF;
-          const bool fr = v && xe <= t;
-          const bool keep = v && !fr;
-          hm = (keep && xe < hm) ? xe : hm;
-          u32 fm = __ballot_sync(FULLMASK, fr);
-          while (fm) {
-            const u32 l = (u32)(__ffs(fm) - 1);
-            fm &= fm - 1;
-            const u32 lid = __shfl_sync(FULLMASK, id, l);
-            const u32 ln = B.cdiv(PR[lid]);
-            free_blocks(bmP, pblk + (size_t)lid * btl, ln, lid, p.k, koff, L, p.hint);
-            p.nfree += ln;
-          }
-          const u32 km = __ballot_sync(FULLMASK, keep);
-          __syncwarp();
-          if (keep) hold[out + __popc(km & ltm)] = id;
-          __syncwarp();
-          out += __popc(km);
-        }
-#pragma unroll
-        for (u32 s = 16; s; s >>= 1) {
-          const i64 y = __shfl_xor_sync(FULLMASK, hm, s);
-          hm = y < hm ? y : hm;
-        }
-        p.nhold = out;
-        p.hmin = hm;
-      }
-      // fresh FCFS admission from this worker's dispatch queue into a prefill batch
-      u32 nb = 0, E = 0, Kb = 0, nrej = 0;
-      u64 tokens = 0, npp = 0, app = 0;
-      while (p.qhead < p.qtail) {
-        const u32 qi = p.qhead + lane;
-        const bool valid = qi < p.qtail;
-        const u32 i = valid ? qP[qi] : 0u;
-        const u32 pp = valid ? PR[i] : 0u;
-        const u32 o = valid ? OU[i] : 0u;
-        const u32 need = B.cdiv(pp);
-        const bool rej = valid && (u64)need > HPP.cap_fresh;
-        const bool el = valid && !rej;
-        const u32 ce = scan_incl(el ? 1u : 0u);
-        const u32 cneed = scan_incl(el ? need : 0u);
-        const u32 cp = scan_incl(el ? pp : 0u);
-        const bool ok = el && ((u64)nb + ce <= (u64)mns) && (tokens + cp <= (u64)mbt) &&
-                        ((i64)p.nfree - (i64)cneed >= wm);
-        const u32 failm = __ballot_sync(FULLMASK, el && !ok);
-        const u32 nvalid = min(32u, p.qtail - p.qhead);
-        const u32 stop = failm ? (u32)(__ffs(failm) - 1) : nvalid;
-        const bool take = el && lane < stop;
-        const bool rj = rej && lane < stop;
-        const u32 takem = __ballot_sync(FULLMASK, take);
-        const u32 cnt = __popc(takem);
-        if (take) {
-          const u32 rank = __popc(takem & ltm);
-          const u32 pos = nb + rank;
-          M.pid[pos] = i;
-          M.ppl[pos] = pp;
-          M.pol[pos] = o;
-          M.req_cum[E + rank] = Kb + cneed;
-          M.req_pt[E + rank] = pos;
-          npp += pp;
-          app += (u64)pp * (pp + 1) / 2;
-        }
-        if (rj) reinterpret_cast<uint8_t *>(rec + i)[26] = (uint8_t)TOKENSIM_REQ_REJECTED;
-        const u32 nrj = __popc(__ballot_sync(FULLMASK, rj));
-        if (stop) {
-          const u32 sneed = __shfl_sync(FULLMASK, cneed, stop - 1);
-          const u32 sp = __shfl_sync(FULLMASK, cp, stop - 1);
-          p.nfree -= sneed;
-          Kb += sneed;
-          tokens += sp;
-        }
-        E += cnt;
-        nb += cnt;
-        nrej += nrj;
-        p.qhead += stop;
-        __syncwarp();
-        if (stop < nvalid) break;
-      }
-      nrej_tot += nrej;
-      n_done_c += nrej;
-      if (nb == 0) {  // idle: wait for a dispatch or for blocks to come back
-        p.t = p.hmin;
-        p.idle = 1;
-      } else {
-        if (!alloc_ordered(SP, E, Kb, btP, btl, p.k, koff, L, p.hint, nwP)) {
-          flags |= TOKENSIM_PT_INTERNAL_ERROR;
-          break;
-        }
-        const u64 Np = warp_sum64(npp), Ap = warp_sum64(app);
-        const i64 T = iter_time_ns(KP, Np, Ap, nb, 0, 0, 0);
-        const i64 te = t + T;
-        const u64 blocksP = totP - p.nfree;
-        // commit: the first token; o == 1 finishes here, the rest become holders whose block
-        // lists move to the per-request table; the whole batch is dispatched onward at te
-        u32 nfin = 0;
-        #pragma unroll 1
-        for (u32 b0 = 0; b0 < nb; b0 += 32) {
-          const u32 pos = b0 + lane;
-          const bool v = pos < nb;
-          const u32 id = v ? M.pid[pos] : 0u, pp = v ? M.ppl[pos] : 0u, o = v ? M.pol[pos] : 0u;
-          const bool one = v && o == 1;
-          const bool hold_it = v && o > 1;
-          const u32 need = B.cdiv(pp);
-          if (v) batch[pos] = id;
-          if (one) {
-            const i64 a = A[id];
-            write_record(rec + id, te - a, te - a, 0, 0, TOKENSIM_REQ_FINISHED, (u32)p.k);
-          }
-          const u32 hm = __ballot_sync(FULLMASK, hold_it);
-          if (hold_it) {
-            hold[p.nhold + __popc(hm & ltm)] = id;
-            reqx[id] = INF;
-          }
-          u32 vm = __ballot_sync(FULLMASK, v);
-          while (vm) {
-            const u32 l = (u32)(__ffs(vm) - 1);
-            vm &= vm - 1;
-            const u32 lpos = b0 + l;
-            const u32 lneed = __shfl_sync(FULLMASK, need, l);
-            const u32 lid = __shfl_sync(FULLMASK, id, l);
-            const bool lone = __shfl_sync(FULLMASK, (u32)one, l) != 0u;
-            const u32 *tbl = btP + (size_t)lpos * btl;
-            if (lone) {
-              free_blocks(bmP, tbl, lneed, lid, p.k, koff, L, p.hint);
-              p.nfree += lneed;
-            } else {
-              #pragma unroll 1
-              for (u32 x = lane; x < lneed; x += 32) pblk[(size_t)lid * btl + x] = tbl[x];
-            }
-          }
-          p.nhold += __popc(hm);
-          nfin += __popc(__ballot_sync(FULLMASK, one));
-          __syncwarp();
-        }
-        n_done_c += nfin;
-        nfin_tot += nfin;
-        if (nfin) last_fin = te > last_fin ? te : last_fin;
-        fold_iter(p.k, pi, t, T, nb, 0, Np, 0, 0, 0, nb, nrej, nfin, blocksP);
-        trace_iter(p.TA, FEp[pi], BINNED, FULLT, trcP, P.trace_cap, W, t, te, blocksP, flags);
-        req_iters += nb;
-        p.nb = nb;
-        p.cur = 0;
-        p.tdisp = te;
-        p.t = te;
-        p.last = te;
-        ++p.k;
-        p.idle = 0;
-      }
-      __syncwarp();
-      if (lane == 0) M.ps[pi] = p;
-      __syncwarp();
+      if (!p_step(psel)) break;
     }
     cyc_sched += (u64)(clock64() - c_s0);
     {  // the next known dispatch, now (a batch started in this phase may end exactly at H)
