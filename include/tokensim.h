@@ -366,6 +366,8 @@ tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t poi
  *   TOKENSIM_HEADS=K       helper kernel: the K longest-estimated points get an SM each
  *   TOKENSIM_NODE_TWO=0|1  xP:yD node kernel: one CTA per SM / the 168-register build, two
  *                          per SM (default: two once there are more points than SMs)
+ *   TOKENSIM_NODE_SW=0|1   xP:yD node kernel: the scheduler on a warp of its own (default: when the
+ *                          points fit one CTA per SM and the two-per-SM build is not used)
  *   TOKENSIM_LPT_OLD=1     order the queue by span / T(1) (round 1) instead of the cost sketch
  *   TOKENSIM_LPT_HELPER=1|2  helper runs: order by the sketch's iterations / cost
  *   TOKENSIM_LPT_COSTS=path  order by per-point costs read from `path` (n_points doubles)

@@ -631,8 +631,8 @@ static Layout make_layout(const tokensim_sweep *h, u64 n_run, int sm_count, int 
   // nconv, next round / cached tokens / LRU prev / LRU next (u32) x nconv
   L.mr_per_warp = mr ? align256(n * 12 + nconv * 12 + nconv * 16 + 64) : 0;
   L.mr = take((size_t)L.warps_total * L.mr_per_warp);
-  // the logs are per simulating warp: a node CTA has pd_y of them
-  const size_t log_warps = (size_t)L.warps_total * (h->pd_general ? h->pd_y : 1u);
+  // the logs are per simulating warp: a node CTA has pd_y (+1 with the scheduler warp) of them
+  const size_t log_warps = (size_t)L.warps_total * (h->pd_general ? h->pd_y + 1u : 1u);
   L.evlog = take(log_warps * 1024 * 16);
   L.itlog = take(log_warps * 256 * 64);
   // preload pipeline scratch of the helper-warp full kernel (layers + 1 doubles per warp)
@@ -759,8 +759,12 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   // node: the register-capped two-CTAs-per-SM build once there are more points than SMs
   bool node_two = h->pd_general && h->pd_y <= 6 && n_run > (u64)sms;
   if (const char *ev = getenv("TOKENSIM_NODE_TWO")) node_two = h->pd_general && h->pd_y <= 6 && atoi(ev) != 0;  // A/B
+  // node, one wave: the scheduler on a warp of its own, alongside the decode phases
+  bool node_sw = h->pd_general && !node_two && n_run <= (u64)sms;
+  if (const char *ev = getenv("TOKENSIM_NODE_SW")) node_sw = h->pd_general && !node_two && atoi(ev) != 0;  // A/B
   e = sim_occupancy(sim_variant(h->full, h->opt.topology == TOKENSIM_PD_PAIR, h->pd_general, !helper, xs), (int)h->cap,
-                    h->pd_general ? (int)h->pd_y + (node_two ? 16 : 0) : (int)L0.wpb, per_warp * L0.wpb, h->nwords_max,
+                    h->pd_general ? (int)h->pd_y + (node_sw ? 1 + 32 : 0) + (node_two ? 16 : 0) : (int)L0.wpb,
+                    per_warp * L0.wpb, h->nwords_max,
                     &occ);
   if (e != cudaSuccess) return cuda_fail(h, e, "occupancy");
   if (occ < 1)
@@ -878,6 +882,7 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
   P.pd_x = h->pd_x;
   P.pd_y = h->pd_y;
   P.node_two = node_two ? 1u : 0u;
+  P.node_sw = node_sw ? 1u : 0u;
   P.dispatch = h->opt.dispatch;
   P.link_mode = h->opt.link_mode;
   P.preload_buf = h->opt.preload_buffer_bytes;

@@ -121,7 +121,7 @@ struct SweepParams {
   unsigned char *pdn_scratch;  // NEXT-1 node: per-CTA FIFOs, queues, holders, P block lists
   u64 pdn_bytes_per_warp;
   u32 pd_x, pd_y, dispatch, pd_general;  // prefill / decode workers, global scheduler, node loop
-  u32 node_two, node_pad;  // node kernel: the register-capped build, two CTAs per SM (sim_node.cu)
+  u32 node_two, node_sw;   // node kernel: the register-capped two-CTAs-per-SM build; the scheduler-warp build
   u32 full, all_p2;                       // 1: the full kernel variant (sim_full.cu); every block size a power of two
   u32 n_sms, helper_mode;                 // SMs of the device; lean kernel with a helper warp per point: 1 = with
                                           // extended stretches (variant 0), 2 = without (variant 5)
@@ -227,7 +227,7 @@ cudaError_t sim_occupancy_base(int cap, int warps_per_block, size_t smem, u32 nw
 cudaError_t sim_occupancy_full(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_full_h(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_pair(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
-// (node: warps_per_block = pd_y (the CTA's warps), + 16 for the two-CTAs-per-SM build)
+// (node: warps_per_block = the CTA's warps, + 16 for the two-CTAs-per-SM build, + 32 for the scheduler-warp build)
 cudaError_t sim_occupancy_node(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_base_c(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
 cudaError_t sim_occupancy_base_n(int cap, int warps_per_block, size_t smem, u32 nwords_max, int *blocks_per_sm);
