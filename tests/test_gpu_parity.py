@@ -652,8 +652,9 @@ def test_node_sharegpt_grid(api):
 
 def test_node_cta_shapes_are_byte_identical(api):
     """The node kernel's CTA-parallel decode warps (sim_pdn.cuh) give the same bytes run twice, and
-    in both builds: 192 points at once (more points than SMs: the register-capped build, two CTAs
-    per SM) and the same points in halves of 96 (one CTA per SM); sampled points vs the oracle."""
+    in all three builds: 192 points at once (more points than SMs: the register-capped build, two
+    CTAs per SM) and the same points in halves of 96 (one CTA per SM) with the scheduler on a warp
+    of its own and with the barrier build; sampled points vs the oracle."""
     import torch
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     cfg = si.SweepConfig("node-shapes", si.LLAMA2_7B, [si.A100],
@@ -670,22 +671,28 @@ def test_node_cta_shapes_are_byte_identical(api):
     its = {p: a.iteration_trace(p) for p in (0, n - 1)}
     a.run()
     assert a.summaries().tobytes() == sa
-    b = api.Sweep(cfg)
     half = n // 2
-    parts = []
-    for beg in (0, half):
-        b.run(beg, beg + half)
-        assert b.run_info()["sim_blocks"] <= sms
-        parts.append(b.summaries().tobytes())
-        for p in recs:
-            if beg <= p < beg + half:
-                assert b.records(p).tobytes() == recs[p]
-        for p in its:
-            if beg <= p < beg + half:
-                g, h = b.iteration_trace(p), its[p]
-                key = lambda x: np.lexsort((x["k"], x["worker"]))  # noqa: E731
-                assert g[key(g)].tobytes() == h[key(h)].tobytes()
-    assert b"".join(parts) == sa
+    import os as _os
+    for sw_mode in ("1", "0"):  # halves of one wave: the scheduler-warp build, and the barrier build
+        _os.environ["TOKENSIM_NODE_SW"] = sw_mode
+        try:
+            b = api.Sweep(cfg)
+            parts = []
+            for beg in (0, half):
+                b.run(beg, beg + half)
+                assert b.run_info()["sim_blocks"] <= sms
+                parts.append(b.summaries().tobytes())
+                for p in recs:
+                    if beg <= p < beg + half:
+                        assert b.records(p).tobytes() == recs[p]
+                for p in its:
+                    if beg <= p < beg + half:
+                        g, h = b.iteration_trace(p), its[p]
+                        key = lambda x: np.lexsort((x["k"], x["worker"]))  # noqa: E731
+                        assert g[key(g)].tobytes() == h[key(h)].tobytes()
+            assert b"".join(parts) == sa, sw_mode
+        finally:
+            _os.environ.pop("TOKENSIM_NODE_SW", None)
     check_pd_points(a, cfg, [0, 77, n - 1])
 
 
