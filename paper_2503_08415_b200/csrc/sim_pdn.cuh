@@ -1395,6 +1395,14 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
       volatile PdnPart *vp = M.part;
       bool c_more = COORD;  // the scheduler warp: events may remain before H
       u32 spins = 0;
+      i64 seen_prog = -1;  // lane j < y: decode warp j's last seen progress
+      // a wait only fails after ~2^26 polls in which no decode warp advanced (a lost publication)
+      auto stalled = [&]() -> bool {
+        const i64 pg = lane < Y ? vp[lane].prog : 0;
+        if (__any_sync(FULLMASK, pg != seen_prog)) spins = 0;
+        seen_prog = pg;
+        return ++spins > (1u << 26);
+      };
       if (COORD) d.t = INF;
       else d = M.ds[dj];
       auto publish = [&]() {  // lane 0: this decode worker's progress (its data before prog)
@@ -1440,7 +1448,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
               continue;
             }
             __nanosleep(64);
-            if (++spins > (1u << 26)) {
+            if (stalled()) {
               flags |= TOKENSIM_PT_INTERNAL_ERROR;
               break;
             }
@@ -1460,7 +1468,7 @@ __device__ void simulate_pdn(const SweepParams &P, u64 j, unsigned char *smem, u
           }
           if (!__all_sync(FULLMASK, ok)) {
             __nanosleep(32);
-            if (++spins > (1u << 26)) {
+            if (stalled()) {
               flags |= TOKENSIM_PT_INTERNAL_ERROR;
               break;
             }
