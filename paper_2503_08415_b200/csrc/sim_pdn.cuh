@@ -1,7 +1,8 @@
 // sim_pdn.cuh -- NEXT-1: the xP:yD disaggregated node with a global scheduler (SURVEY §8(f)
 // NEXT-1; readings R-X1..R-X6 in DESIGN.md).  Included by sim_core.cuh after sim_pd.cuh, inside
 // namespace ts.  One CTA simulates one (prefill profile, decode profile) point: warp j runs
-// decode worker j, and warp 0 also runs the global scheduler and the prefill workers.
+// decode worker j, and warp 0 also runs the global scheduler and the prefill workers -- or, in
+// the SW build (one point per SM), warp y runs them on its own.
 //
 // x prefill workers and y decode workers run the a.9 worker loops; the
 // global scheduler dispatches every arrival to a prefill worker and,
@@ -27,6 +28,13 @@
 // holder minimum, which the boundary recomputes from the same transfer ends (R-X6), so the
 // result is the sequential one byte for byte (the node parity tests compare against the oracle's
 // sequential loop).
+//
+// SW build: (2) runs alongside (1) on the scheduler's own warp.  Before a scheduler event at t it
+// waits only for decode warps that could still pull before t (each publishes its next boundary
+// and its unpulled FIFO entries after every boundary); pulls reach the prefill workers through
+// per-worker mailboxes (atomicMin of the transfer end) that the scheduler folds before it looks
+// at a prefill worker; and once every remaining request is with the decode workers it waits for
+// all of them, so that it stops at the sequential loop's last event (E*).
 //
 // Data: per-worker scalars live in shared memory; decode worker j owns an id-sorted slot array +
 // bitmap + its own requester lists in shared memory exactly like the pair's D; prefill workers own
