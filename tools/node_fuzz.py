@@ -1,7 +1,7 @@
 """Randomised parity sweep of the xP:yD node kernel against the oracle's sequential node loop
 (a longer run of tests/test_gpu_parity.py::test_node_epoch_stress's generator).
 
-    python tools/node_fuzz.py [--n 300] [--seed 7] [--pair]
+    python tools/node_fuzz.py [--n 300] [--seed 7] [--pair] [--horizon]
 
 Every configuration: random x:y (x + y <= 8), dispatch policy, arrivals (sparse, dense, bursts of
 equal times), lengths, KV pool, block size, preemption mode, trace mode, fast-forward; all points
@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--n", type=int, default=300)
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--pair", action="store_true")
+    ap.add_argument("--horizon", action="store_true", help="stop every point at a random horizon")
     a = ap.parse_args()
     import paper_2503_08415_b200 as P
     from test_gpu_parity import _micro_pd, check_pd_points
@@ -48,6 +49,9 @@ def main():
         y = 1 if a.pair else int(rng.integers(1, 9 - x))
         d = str(rng.choice([si.ROUND_ROBIN, si.LEAST_OUTSTANDING, si.LEAST_MEMORY]))
         cfg = replace(cfg, workload=w, options=replace(cfg.options, pd_prefill=x, pd_decode=y, dispatch=d))
+        if a.horizon:  # somewhere inside the arrival span, or a little past it
+            hz = int(rng.integers(1, int(base[-1]) + 2)) + int(rng.choice([0, 0, 10 ** 8]))
+            cfg = replace(cfg, options=replace(cfg.options, horizon_ns=hz))
         sw = P.Sweep(cfg)
         sw.run()
         try:
@@ -63,7 +67,7 @@ def main():
             bad += 1
             print(f"config {it}: x={x} y={y} {d} n={len(base)}: {str(e).splitlines()[0]}", flush=True)
         sw.close()
-    print(f"node_fuzz{' --pair' if a.pair else ''}: {a.n} configurations, {bad} mismatching")
+    print(f"node_fuzz{' --pair' if a.pair else ''}{' --horizon' if a.horizon else ''}: {a.n} configurations, {bad} mismatching")
     return 1 if bad else 0
 
 
