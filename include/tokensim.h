@@ -371,7 +371,8 @@ tokensim_status tokensim_get_point_profile(const tokensim_sweep *h, uint64_t poi
  *   TOKENSIM_LPT_OLD=1     order the queue by span / T(1) (round 1) instead of the cost sketch
  *   TOKENSIM_LPT_HELPER=1|2  helper runs: order by the sketch's iterations / cost
  *   TOKENSIM_LPT_COSTS=path  order by per-point costs read from `path` (n_points doubles)
- *   TOKENSIM_DEBUG_XS=1    print the median point's quiet-stretch estimate (extended-stretch choice) */
+ *   TOKENSIM_DEBUG_XS=1    print the median point's quiet-stretch estimate (extended-stretch choice)
+ *   TOKENSIM_LPT_DUMP=path write the queue-order cost estimates (one double per run point) */
 
 /* Message of the last failing call on h (NULL: the calling thread's last create error). */
 const char *tokensim_last_error(const tokensim_sweep *h);

@@ -936,6 +936,12 @@ tokensim_status tokensim_sweep_run(tokensim_sweep *h, int device, uint64_t begin
       }
       est[j] = {est_j, (u32)j};
     }
+    if (const char *df = getenv("TOKENSIM_LPT_DUMP")) {  // observability: the estimates, one double per run point
+      if (FILE *f = fopen(df, "wb")) {
+        for (u64 j = 0; j < n_run; ++j) fwrite(&est[j].first, 8, 1, f);
+        fclose(f);
+      }
+    }
     if (const char *cf = getenv("TOKENSIM_LPT_COSTS")) {  // A/B experiments only: measured per-point costs
       if (FILE *f = fopen(cf, "rb")) {
         std::vector<double> c(h->n_points);
